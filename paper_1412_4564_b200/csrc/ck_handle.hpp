@@ -1,0 +1,76 @@
+// The opaque ck_handle of ck.h and the error plumbing shared by capi.cu,
+// graph.cpp and trainer.cpp.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "ck/ck.h"
+#include "ck_internal.hpp"
+
+namespace ck {
+struct TcState;  // conv_tc.cu: cached tensor maps / layout buffers
+}
+
+struct ck_handle {
+  int device = 0;
+  std::string err;
+  ck::LaunchCounter counter;
+  ck::Workspace ws;       // conv wgrad partials, bnorm statistics
+  ck::Workspace scratch;  // loss per-site values, staging
+  int* flag = nullptr;    // device label-error flag (loss.cpp:14-18, :101-106)
+  int64_t last_classes = 0;
+  ck::TcState* tc = nullptr;
+};
+
+namespace ck {
+
+// A reference exception (error.hpp:9-24) carried to the C boundary.
+struct Err : std::runtime_error {
+  ck_status code;
+  Err(ck_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+// Binds the device and the launch counter for the duration of one API call.
+struct HandleScope {
+  LaunchCounter* prev;
+  explicit HandleScope(ck_handle* h) : prev(g_counter) {
+    cudaSetDevice(h->device);
+    g_counter = &h->counter;
+  }
+  ~HandleScope() { g_counter = prev; }
+};
+
+std::string shape_str(const ck_shape& s);
+bool same(const ck_shape& a, const ck_shape& b);
+int64_t elems(const ck_shape& s);
+void check_tensor(const ck_tensor* t, const char* what);
+void check_out(const ck_tensor* t, const ck_shape& want, const char* what);
+ck_shape conv_output_shape(const ck_shape& x, const ck_shape& f, const ck_conv_geom& g);
+ck_shape convt_output_shape(const ck_shape& x, const ck_shape& f, const ck_convt_geom& g);
+ck_shape pool_output_shape(const ck_shape& x, const ck_pool_geom& g);
+ConvDims conv_dims(const ck_shape& x, const ck_shape& f, const ck_shape& y, const ck_conv_geom& g);
+PoolDims pool_dims(const ck_shape& x, const ck_shape& y, const ck_pool_geom& g);
+void check_cuda(cudaError_t e, const char* what);
+void after_launch();
+
+void conv_forward_dispatch(ck_handle* h, const float* x, const float* f, const float* bias,
+                           float* y, const ConvDims& d, int relu, ck_math math, cudaStream_t s);
+void conv_dgrad_dispatch(ck_handle* h, const float* dy, const float* f, float* dx,
+                         const ConvDims& d, int acc, ck_math math, cudaStream_t s);
+void conv_wgrad_dispatch(ck_handle* h, const float* x, const float* dy, float* df,
+                         const ConvDims& d, int acc, ck_math math, cudaStream_t s);
+
+// conv_tc.cu: the tcgen05 TF32 kernels.  Each returns false (launching
+// nothing) when the problem is outside the kernel's envelope.
+bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
+                     const ConvDims& d, int relu, cudaStream_t s);
+bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, const ConvDims& d,
+                   int acc, cudaStream_t s);
+bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, const ConvDims& d,
+                   int acc, cudaStream_t s);
+void conv_tc_release(ck_handle* h);
+
+}  // namespace ck

@@ -1,0 +1,110 @@
+// Internal declarations shared by the kernels, the C ABI and the graph
+// engine.  Launchers take plain device pointers and pre-validated geometry;
+// all argument checking happens in capi.cu before a launcher is called.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "ck/ck.h"
+
+namespace ck {
+
+// Geometry in the reference's terms (conv.hpp:9-17, pool.hpp:13-23).
+struct ConvDims {
+  int H, W, C, N;      // input x
+  int fh, fw, Cg, K;   // filters (Cg = C / groups)
+  int OH, OW;          // output
+  int sh, sw, pt, pb, pl, pr, groups;
+  // Filter element (fi, fj, c, k) lives at f[fi + fh*(fj + fw*(c*fsc + k*fsk))];
+  // conv: fsc = 1, fsk = Cg.  convt reuses the conv kernels with the
+  // "swapped bank" of conv.cpp:332-342 by exchanging the two strides.
+  int64_t fsc, fsk;
+#ifdef __CUDACC__
+  __host__ __device__
+#endif
+  int Kg() const { return K / groups; }
+};
+
+struct PoolDims {
+  int H, W, C, N, OH, OW;
+  int wh, ww, sh, sw, pt, pl;
+  int mode;  // 0 max, 1 avg
+};
+
+// Per-handle scratch owned by the C ABI / engine.
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void* get(size_t want, cudaStream_t s);
+  void release();
+};
+
+struct LaunchCounter {
+  int64_t n = 0;
+};
+
+// ---- launchers (kernels.cu / conv_simt.cu / conv_tc.cu) -------------------
+extern thread_local LaunchCounter* g_counter;  // counts kernel launches
+inline void count_launch(int k = 1) {
+  if (g_counter) g_counter->n += k;
+}
+
+void relu_forward(const float* x, float* y, int64_t n, cudaStream_t s);
+void relu_backward(const float* x, const float* dy, float* dx, int64_t n, int acc, cudaStream_t s);
+void axpy_inplace(float* y, const float* x, int64_t n, cudaStream_t s);  // y += x
+void sgd_step(float* w, float* v, const float* g, int64_t n, float lr, float mom, float wd,
+              cudaStream_t s);
+
+void pool_forward(const float* x, float* y, const PoolDims& d, cudaStream_t s);
+void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d, int acc,
+                   cudaStream_t s);
+
+void lrn_forward(const float* x, float* y, int H, int W, int C, int N, int size, float kappa,
+                 float alpha, float beta, cudaStream_t s);
+void lrn_backward(const float* x, const float* dy, float* dx, int H, int W, int C, int N, int size,
+                  float kappa, float alpha, float beta, int acc, cudaStream_t s);
+
+// Per-channel sums in double: out[c] = {sum x, sum x^2, sum dy, sum dy*x}
+// (dy may be null).  partial: workspace of splits*C*4 doubles.
+void bnorm_stats(const float* x, const float* dy, double* partial, double* out, int HW, int C,
+                 int N, int splits, cudaStream_t s);
+int bnorm_splits(int HW, int C, int N);
+void bnorm_apply(const float* x, const float* w, const float* b, const double* stats,
+                 const float* fixed_moments, float* y, float* moments_out, double eps, int HW,
+                 int C, int N, cudaStream_t s);
+void bnorm_backward_apply(const float* x, const float* dy, const float* w, const double* stats,
+                          double eps, float* dx, float* dw, float* db, int HW, int C, int N,
+                          int acc, cudaStream_t s);
+
+// softmaxlog: per-site loss into site_loss, then a fixed-order sum into loss.
+void softmaxlog_forward(const float* x, const float* labels, const float* weights,
+                        float* site_loss, float* loss, int* flag, int HW, int C, int N,
+                        cudaStream_t s);
+void softmaxlog_backward(const float* x, const float* labels, const float* weights, float p,
+                         float* dx, int* flag, int HW, int C, int N, int acc, cudaStream_t s);
+void loss_metrics(const float* x, const float* labels, const float* weights, int top_k,
+                  float* site_buf, float* top1, float* topk, int* flag, int HW, int C, int N,
+                  cudaStream_t s);
+
+// ---- convolution -----------------------------------------------------------
+// All conv launchers compute the reference semantics of conv.cpp:193-280 on
+// HWCN tensors; bias may be null; acc != 0 adds into the destination.
+// FP32 (SIMT FFMA) verification path:
+void conv_fwd_fp32(const float* x, const float* f, const float* bias, float* y,
+                   const ConvDims& d, int relu, cudaStream_t s);
+void conv_dgrad_fp32(const float* dy, const float* f, float* dx, const ConvDims& d, int acc,
+                     cudaStream_t s);
+// wgrad uses `ws` (>= conv_wgrad_ws_bytes) for the split-K partials.
+size_t conv_wgrad_ws_bytes(const ConvDims& d);
+void conv_wgrad_fp32(const float* x, const float* dy, float* df, const ConvDims& d, int acc,
+                     void* ws, cudaStream_t s);
+void conv_bgrad(const float* dy, float* db, int OHW, int K, int N, int acc, cudaStream_t s);
+
+// TF32 tensor-core path (tcgen05).  Returns false when the shape is outside
+// the kernel's envelope so the caller can use the FP32 kernel instead.
+bool conv_tc_available();
+
+}  // namespace ck

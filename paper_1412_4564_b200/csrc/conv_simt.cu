@@ -1,0 +1,366 @@
+// Exact-FP32 convolution on CUDA cores: the CK_MATH_FP32 "verification" path.
+//
+// Each pass of conv.cpp:193-280 is an implicit GEMM over HWCN tensors (no
+// im2row buffer is ever materialised):
+//   fprop : M = output pixels (n, oj, oi), N = filters of a group,
+//           K = (c, fj, fi) of the group          -> Y = A F      (conv.cpp:214)
+//   dgrad : M = input pixels (n, j, i),  N = channels of a group,
+//           K = (k, fj, fi), gather form of row2im -> dX = row2im(P F^T) (conv.cpp:270-278)
+//   wgrad : M = (c, fj, fi), N = filters of a group, K = output pixels,
+//           split-K with a deterministic reduction  -> dF = sum_n A^T P   (conv.cpp:260-269)
+// A 64x64 output tile per 256-thread block, 4x4 per thread, BK = 16 staged in
+// shared memory with register double buffering.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ck_internal.hpp"
+
+namespace ck {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
+
+// ---- gather functors --------------------------------------------------------
+
+struct FpropProb {
+  const float* x;
+  const float* f;
+  const float* bias;
+  float* y;
+  ConvDims d;
+  int relu;
+  // per-group bases set by the kernel
+  __device__ int64_t M() const { return (int64_t)d.N * d.OH * d.OW; }
+  __device__ int64_t N() const { return d.Kg(); }
+  __device__ int64_t K() const { return (int64_t)d.fh * d.fw * d.Cg; }
+  // Row m -> its pixel; the A operand gathers x through the conv index map
+  // (conv.cpp:45-53) with zero padding.
+  struct RowCtx {
+    const float* xb;
+    int bi, bj;  // s*oi - pt, s*oj - pl
+    bool valid;
+  };
+  __device__ RowCtx row(int64_t m, int g) const {
+    RowCtx r;
+    r.valid = m < M();
+    if (!r.valid) m = 0;
+    int oi = (int)(m % d.OH);
+    int64_t t = m / d.OH;
+    int oj = (int)(t % d.OW);
+    int n = (int)(t / d.OW);
+    r.xb = x + ((int64_t)n * d.C + (int64_t)g * d.Cg) * d.H * d.W;
+    r.bi = d.sh * oi - d.pt;
+    r.bj = d.sw * oj - d.pl;
+    return r;
+  }
+  __device__ float a(const RowCtx& r, int64_t k) const {
+    if (!r.valid || k >= K()) return 0.f;
+    int fi = (int)(k % d.fh);
+    int64_t t = k / d.fh;
+    int fj = (int)(t % d.fw);
+    int c = (int)(t / d.fw);
+    int ii = r.bi + fi, jj = r.bj + fj;
+    if (ii < 0 || ii >= d.H || jj < 0 || jj >= d.W) return 0.f;
+    return r.xb[(int64_t)c * d.H * d.W + ii + (int64_t)d.H * jj];
+  }
+  __device__ float b(int64_t k, int64_t n, int g) const {
+    if (k >= K() || n >= N()) return 0.f;
+    int fi = (int)(k % d.fh);
+    int64_t t = k / d.fh;
+    int fj = (int)(t % d.fw);
+    int64_t c = t / d.fw;
+    int64_t kk = (int64_t)g * d.Kg() + n;
+    return f[fi + (int64_t)d.fh * (fj + (int64_t)d.fw * (c * d.fsc + kk * d.fsk))];
+  }
+  __device__ void store(int64_t m, int64_t n, int g, float v, int acc) const {
+    if (m >= M() || n >= N()) return;
+    int64_t p = m % ((int64_t)d.OH * d.OW), img = m / ((int64_t)d.OH * d.OW);
+    int64_t k = (int64_t)g * d.Kg() + n;
+    if (bias) v = __fadd_rn(v, bias[k]);
+    if (relu) v = v > 0.f ? v : 0.f;
+    float* dst = y + (img * d.K + k) * d.OH * d.OW + p;
+    *dst = acc ? __fadd_rn(*dst, v) : v;
+  }
+};
+
+struct DgradProb {
+  const float* dy;
+  const float* f;
+  float* dx;
+  ConvDims d;
+  __device__ int64_t M() const { return (int64_t)d.N * d.H * d.W; }
+  __device__ int64_t N() const { return d.Cg; }
+  __device__ int64_t K() const { return (int64_t)d.fh * d.fw * d.Kg(); }
+  struct RowCtx {
+    const float* yb;
+    int i, j;
+    bool valid;
+  };
+  __device__ RowCtx row(int64_t m, int g) const {
+    RowCtx r;
+    r.valid = m < M();
+    if (!r.valid) m = 0;
+    r.i = (int)(m % d.H);
+    int64_t t = m / d.H;
+    r.j = (int)(t % d.W);
+    int n = (int)(t / d.W);
+    r.yb = dy + ((int64_t)n * d.K + (int64_t)g * d.Kg()) * d.OH * d.OW;
+    return r;
+  }
+  // A(m, (k, fj, fi)) = dy[oi, oj, k] where s*oi + fi - pt = i (row2im adjoint).
+  __device__ float a(const RowCtx& r, int64_t kk) const {
+    if (!r.valid || kk >= K()) return 0.f;
+    int fi = (int)(kk % d.fh);
+    int64_t t = kk / d.fh;
+    int fj = (int)(t % d.fw);
+    int k = (int)(t / d.fw);
+    int ni = r.i + d.pt - fi, nj = r.j + d.pl - fj;
+    if (ni < 0 || nj < 0) return 0.f;
+    if (ni % d.sh || nj % d.sw) return 0.f;
+    int oi = ni / d.sh, oj = nj / d.sw;
+    if (oi >= d.OH || oj >= d.OW) return 0.f;
+    return r.yb[(int64_t)k * d.OH * d.OW + oi + (int64_t)d.OH * oj];
+  }
+  __device__ float b(int64_t kk, int64_t n, int g) const {
+    if (kk >= K() || n >= N()) return 0.f;
+    int fi = (int)(kk % d.fh);
+    int64_t t = kk / d.fh;
+    int fj = (int)(t % d.fw);
+    int64_t k = (int64_t)g * d.Kg() + t / d.fw;
+    return f[fi + (int64_t)d.fh * (fj + (int64_t)d.fw * (n * d.fsc + k * d.fsk))];
+  }
+  __device__ void store(int64_t m, int64_t n, int g, float v, int acc) const {
+    if (m >= M() || n >= N()) return;
+    int64_t p = m % ((int64_t)d.H * d.W), img = m / ((int64_t)d.H * d.W);
+    int64_t c = (int64_t)g * d.Cg + n;
+    float* dst = dx + (img * d.C + c) * d.H * d.W + p;
+    *dst = acc ? __fadd_rn(*dst, v) : v;
+  }
+};
+
+// wgrad: rows are (c, fj, fi) of a group, columns filters of the group,
+// reduction over output pixels; each z-slice handles a pixel range and
+// writes a partial tile (reduced later in fixed order).
+struct WgradProb {
+  const float* x;
+  const float* dy;
+  float* part;  // [splits][groups][rows][cols]
+  ConvDims d;
+  __device__ int64_t M() const { return (int64_t)d.fh * d.fw * d.Cg; }
+  __device__ int64_t N() const { return d.Kg(); }
+  __device__ int64_t K() const { return (int64_t)d.N * d.OH * d.OW; }
+  struct RowCtx {
+    const float* xb;
+    int fi, fj;
+    bool valid;
+  };
+  __device__ RowCtx row(int64_t m, int g) const {
+    RowCtx r;
+    r.valid = m < M();
+    if (!r.valid) m = 0;
+    r.fi = (int)(m % d.fh);
+    int64_t t = m / d.fh;
+    r.fj = (int)(t % d.fw);
+    int c = (int)(t / d.fw);
+    r.xb = x + ((int64_t)g * d.Cg + c) * d.H * d.W;
+    return r;
+  }
+  __device__ float a(const RowCtx& r, int64_t kk) const {
+    if (!r.valid || kk >= K()) return 0.f;
+    int oi = (int)(kk % d.OH);
+    int64_t t = kk / d.OH;
+    int oj = (int)(t % d.OW);
+    int64_t n = t / d.OW;
+    int ii = d.sh * oi + r.fi - d.pt, jj = d.sw * oj + r.fj - d.pl;
+    if (ii < 0 || ii >= d.H || jj < 0 || jj >= d.W) return 0.f;
+    return r.xb[n * d.C * d.H * d.W + ii + (int64_t)d.H * jj];
+  }
+  __device__ float b(int64_t kk, int64_t n, int g) const {
+    if (kk >= K() || n >= N()) return 0.f;
+    int64_t p = kk % ((int64_t)d.OH * d.OW), img = kk / ((int64_t)d.OH * d.OW);
+    int64_t k = (int64_t)g * d.Kg() + n;
+    return dy[(img * d.K + k) * d.OH * d.OW + p];
+  }
+  int splits;
+  __device__ void store_part(int64_t m, int64_t n, int g, int split, float v) const {
+    if (m >= M() || n >= N()) return;
+    part[(((int64_t)split * d.groups + g) * N() + n) * M() + m] = v;
+  }
+};
+
+// ---- the tiled kernel ------------------------------------------------------------
+
+template <class P, bool kSplit>
+__global__ void __launch_bounds__(NT) simt_gemm_k(P p, int splits, int acc) {
+  __shared__ float As[2][BK][BM];
+  __shared__ float Bs[2][BK][BN];
+  const int tid = threadIdx.x;
+  const int g = kSplit ? blockIdx.z / splits : blockIdx.z;
+  const int split = kSplit ? blockIdx.z % splits : 0;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  const int64_t Ktot = p.K();
+  int64_t kbeg = 0, kend = Ktot;
+  if (kSplit) {
+    int64_t chunk = (Ktot + splits - 1) / splits;
+    chunk = (chunk + BK - 1) / BK * BK;
+    kbeg = chunk * split;
+    kend = kbeg + chunk < Ktot ? kbeg + chunk : Ktot;
+  }
+  // loader mapping: element e = tid + NT*r (r<4) -> (row = e % 64, k = e / 64)
+  const int lr = tid % 64, lk = tid / 64;  // lk in 0..3, k = lk + 4r
+  auto rc = p.row(m0 + lr, g);
+  float ra[4], rb[4];
+  auto load = [&](int64_t k0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int64_t k = k0 + lk + 4 * r;
+      ra[r] = k < kend ? p.a(rc, k) : 0.f;
+      rb[r] = k < kend ? p.b(k, n0 + lr, g) : 0.f;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      As[buf][lk + 4 * r][lr] = ra[r];
+      Bs[buf][lk + 4 * r][lr] = rb[r];
+    }
+  };
+  float accv[4][4] = {};
+  const int tx = tid % 16, ty = tid / 16;
+  int buf = 0;
+  if (kbeg < kend) {
+    load(kbeg);
+    stash(0);
+  }
+  __syncthreads();
+  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
+    const bool more = k0 + BK < kend;
+    if (more) load(k0 + BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[buf][kk][tx + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][kk][ty + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) accv[i][j] = fmaf(av[i], bv[j], accv[i][j]);
+    }
+    if (more) stash(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int64_t m = m0 + tx + 16 * i, n = n0 + ty + 16 * j;
+      if constexpr (kSplit)
+        p.store_part(m, n, g, split, accv[i][j]);
+      else
+        p.store(m, n, g, accv[i][j], acc);
+    }
+}
+
+// df[fi, fj, c, k] (+)= sum_s part[s][g][k][(c,fj,fi)], in split order.
+__global__ void wgrad_reduce_k(const float* __restrict__ part, float* df, ConvDims d, int splits,
+                               int acc) {
+  const int64_t rows = (int64_t)d.fh * d.fw * d.Cg, cols = d.Kg();
+  const int64_t per = rows * cols * d.groups;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t m = e % rows;
+    int64_t t = e / rows;
+    int64_t n = t % cols;
+    int64_t g = t / cols;
+    float s = 0.f;
+    for (int sp = 0; sp < splits; ++sp) s += part[sp * per + (g * cols + n) * rows + m];
+    // m = fi + fh*(fj + fw*c)
+    int64_t fi = m % d.fh, r = m / d.fh, fj = r % d.fw, c = r / d.fw;
+    int64_t k = g * cols + n;
+    float* dst = df + fi + (int64_t)d.fh * (fj + (int64_t)d.fw * (c * d.fsc + k * d.fsk));
+    *dst = acc ? *dst + s : s;
+  }
+}
+
+// db[k] = sum_n sum_p dy[p, k, n] (conv.cpp:246-252), one block per filter.
+__global__ void bgrad_k(const float* __restrict__ dy, float* db, int OHW, int K, int N, int acc) {
+  const int k = blockIdx.x;
+  double a = 0;
+  for (int n = 0; n < N; ++n) {
+    const float* p = dy + ((int64_t)n * K + k) * OHW;
+    for (int i = threadIdx.x; i < OHW; i += blockDim.x) a += p[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  __shared__ double red[32];
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += red[w];
+    db[k] = acc ? db[k] + (float)t : (float)t;
+  }
+}
+
+int wgrad_splits(const ConvDims& d) {
+  int64_t rows = (int64_t)d.fh * d.fw * d.Cg, cols = d.Kg();
+  int64_t tiles = ((rows + BM - 1) / BM) * ((cols + BN - 1) / BN) * d.groups;
+  int64_t K = (int64_t)d.N * d.OH * d.OW;
+  int64_t want = (148 * 4 + tiles - 1) / tiles;
+  int64_t maxs = (K + 255) / 256;  // at least 256 pixels per split
+  if (want > maxs) want = maxs;
+  if (want > 64) want = 64;
+  if (want < 1) want = 1;
+  return (int)want;
+}
+
+}  // namespace
+
+void conv_fwd_fp32(const float* x, const float* f, const float* bias, float* y,
+                   const ConvDims& d, int relu, cudaStream_t s) {
+  FpropProb p{x, f, bias, y, d, relu};
+  int64_t M = (int64_t)d.N * d.OH * d.OW;
+  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((d.Kg() + BN - 1) / BN), d.groups);
+  count_launch();
+  simt_gemm_k<FpropProb, false><<<grid, NT, 0, s>>>(p, 1, 0);
+}
+
+void conv_dgrad_fp32(const float* dy, const float* f, float* dx, const ConvDims& d, int acc,
+                     cudaStream_t s) {
+  DgradProb p{dy, f, dx, d};
+  int64_t M = (int64_t)d.N * d.H * d.W;
+  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((d.Cg + BN - 1) / BN), d.groups);
+  count_launch();
+  simt_gemm_k<DgradProb, false><<<grid, NT, 0, s>>>(p, 1, acc);
+}
+
+size_t conv_wgrad_ws_bytes(const ConvDims& d) {
+  int64_t rows = (int64_t)d.fh * d.fw * d.Cg, cols = d.Kg();
+  return (size_t)wgrad_splits(d) * rows * cols * d.groups * sizeof(float);
+}
+
+void conv_wgrad_fp32(const float* x, const float* dy, float* df, const ConvDims& d, int acc,
+                     void* ws, cudaStream_t s) {
+  int splits = wgrad_splits(d);
+  WgradProb p{x, dy, (float*)ws, d};
+  p.splits = splits;
+  int64_t rows = (int64_t)d.fh * d.fw * d.Cg;
+  dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((d.Kg() + BN - 1) / BN),
+            d.groups * splits);
+  count_launch(2);
+  simt_gemm_k<WgradProb, true><<<grid, NT, 0, s>>>(p, splits, 0);
+  int64_t per = rows * d.Kg() * d.groups;
+  int blocks = (int)((per + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  wgrad_reduce_k<<<blocks, 256, 0, s>>>((const float*)ws, df, d, splits, acc);
+}
+
+void conv_bgrad(const float* dy, float* db, int OHW, int K, int N, int acc, cudaStream_t s) {
+  count_launch();
+  bgrad_k<<<K, 256, 0, s>>>(dy, db, OHW, K, N, acc);
+}
+
+}  // namespace ck

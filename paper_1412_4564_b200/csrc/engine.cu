@@ -1,0 +1,815 @@
+// engine.cu -- the device-resident DAG engine (graph.hpp / graph.cpp) and
+// the cnn_train data-parallel training step.
+//
+// Semantics follow graph.cpp:
+//   * layers fire in a stable topological order, ties by declaration order
+//     (Graph::finalize);
+//   * forward keeps every value resident on the device ("tape");
+//   * backward seeds d(objective) = 1, walks layers in reverse and
+//     accumulates derivs[in] += d (graph.cpp:548-598).  The zero-init +
+//     accumulate of the reference is fused: the first contribution to a
+//     derivative is written, later ones are added by the producing kernel
+//     (its `acc` epilogue), and derivatives that receive nothing are zeroed
+//     at the end -- bit-identical to 0 + a (+ b ...).
+// The trainer adds SGD with momentum and NCCL allreduce of the parameter
+// derivatives, launched per layer on a communication stream as soon as the
+// layer's backward has produced them, overlapping the rest of backward.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <set>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "ck/ck.h"
+#include "ck_handle.hpp"
+#include "ck_internal.hpp"
+
+using ck::Err;
+
+namespace ck {
+
+enum class Kind { conv, convt, pool, relu, lrn, bnorm, loss, sum };
+
+static Kind kind_from_name(const std::string& s) {
+  if (s == "conv") return Kind::conv;
+  if (s == "convt") return Kind::convt;
+  if (s == "pool") return Kind::pool;
+  if (s == "relu") return Kind::relu;
+  if (s == "lrn") return Kind::lrn;
+  if (s == "bnorm") return Kind::bnorm;
+  if (s == "loss") return Kind::loss;
+  if (s == "sum") return Kind::sum;
+  if (s == "bilinear" || s == "sigmoid" || s == "spnorm" || s == "softmax" || s == "pdist" ||
+      s == "split")
+    throw Err(CK_ERR_ARG, "layer kind '" + s + "' is not on the device hot path");
+  throw Err(CK_ERR_ARG, "unknown layer kind '" + s + "'");
+}
+
+struct Var {
+  std::string name;
+  int role = 2;  // 0 input, 1 param, 2 derived
+  ck_shape shape{0, 0, 0, 0};
+  bool has_shape = false;
+  int producer = -1;
+  std::vector<std::pair<int, int>> consumers;
+  float* value = nullptr;
+  float* deriv = nullptr;
+  bool deriv_live = false;  // received a contribution in this backward
+};
+
+struct Layer {
+  std::string name;
+  Kind kind;
+  std::vector<int> in, out;
+  std::vector<double> p;
+  float* aux = nullptr;  // bnorm moments (K x 2), graph.cpp:306
+};
+
+static std::vector<std::string> split_csv(const char* s) {
+  std::vector<std::string> out;
+  std::stringstream ss(s ? s : "");
+  std::string item;
+  while (std::getline(ss, item, ','))
+    if (!item.empty()) out.push_back(item);
+  return out;
+}
+
+}  // namespace ck
+
+struct ck_graph {
+  ck_handle* h = nullptr;
+  ck_math math = CK_MATH_TF32;
+  std::vector<ck::Var> vars;
+  std::map<std::string, int> by_name;
+  std::vector<ck::Layer> layers;
+  std::vector<int> order;
+  bool finalized = false;
+  std::vector<void*> allocs;
+  float* param_deriv_arena = nullptr;
+  size_t param_deriv_elems = 0;
+  int64_t last_launches = 0;
+  bool profiling = false;
+  // per layer: fwd begin/end, bwd begin/end
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<char> prof_fwd_done, prof_bwd_done;
+
+  int var(const std::string& n) const {
+    auto it = by_name.find(n);
+    if (it == by_name.end()) throw Err(CK_ERR_ARG, "unknown variable '" + n + "'");
+    return it->second;
+  }
+  int intern(const std::string& n, int role) {
+    auto it = by_name.find(n);
+    if (it != by_name.end()) return it->second;
+    ck::Var v;
+    v.name = n;
+    v.role = role;
+    vars.push_back(v);
+    by_name[n] = (int)vars.size() - 1;
+    return (int)vars.size() - 1;
+  }
+  ~ck_graph() {
+    for (void* p : allocs) cudaFree(p);
+    for (auto e : prof_ev) cudaEventDestroy(e);
+  }
+  void prof(int li, int which, cudaStream_t s) {  // which: 0..3
+    if (profiling) cudaEventRecord(prof_ev[4 * li + which], s);
+  }
+};
+
+namespace ck {
+
+static void need(const Layer& l, size_t nin_lo, size_t nin_hi, size_t nout) {
+  if (l.in.size() < nin_lo || l.in.size() > nin_hi || l.out.size() != nout)
+    throw Err(CK_ERR_ARG, "layer '" + l.name + "' has wrong arity");
+}
+
+static void need_params(const Layer& l, size_t n) {
+  if (l.p.size() < n) throw Err(CK_ERR_ARG, "layer '" + l.name + "' needs " + std::to_string(n) + " parameters");
+}
+
+static ck_conv_geom conv_geom_of(const Layer& l) {
+  need_params(l, 7);
+  return ck_conv_geom{(int64_t)l.p[0], (int64_t)l.p[1], (int64_t)l.p[2], (int64_t)l.p[3],
+                      (int64_t)l.p[4], (int64_t)l.p[5], (int64_t)l.p[6]};
+}
+static ck_convt_geom convt_geom_of(const Layer& l) {
+  need_params(l, 6);
+  return ck_convt_geom{(int64_t)l.p[0], (int64_t)l.p[1], (int64_t)l.p[2],
+                       (int64_t)l.p[3], (int64_t)l.p[4], (int64_t)l.p[5]};
+}
+static ck_pool_geom pool_geom_of(const Layer& l) {
+  need_params(l, 9);
+  return ck_pool_geom{(int64_t)l.p[0], (int64_t)l.p[1], (int64_t)l.p[2], (int64_t)l.p[3],
+                      (int64_t)l.p[4], (int64_t)l.p[5], (int64_t)l.p[6], (int64_t)l.p[7],
+                      (int64_t)l.p[8]};
+}
+static ck_lrn_params lrn_of(const Layer& l) {
+  need_params(l, 4);
+  return ck_lrn_params{(int64_t)l.p[0], l.p[1], l.p[2], l.p[3]};
+}
+
+static ck_tensor tv(Var& v, bool deriv) { return ck_tensor{deriv ? v.deriv : v.value, v.shape}; }
+
+// Graph::finalize: arity, single producer, stable topological order, shapes.
+static void finalize(ck_graph* g) {
+  std::vector<int> indeg(g->layers.size(), 0);
+  for (auto& v : g->vars) {
+    v.producer = -1;
+    v.consumers.clear();
+  }
+  for (size_t li = 0; li < g->layers.size(); ++li) {
+    Layer& l = g->layers[li];
+    for (int o : l.out) {
+      if (g->vars[o].producer >= 0)
+        throw Err(CK_ERR_ARG, "variable '" + g->vars[o].name + "' has two producers");
+      if (g->vars[o].role != 2)
+        throw Err(CK_ERR_ARG, "layer '" + l.name + "' writes input/param '" + g->vars[o].name + "'");
+      g->vars[o].producer = (int)li;
+    }
+    for (size_t s = 0; s < l.in.size(); ++s) g->vars[l.in[s]].consumers.push_back({(int)li, (int)s});
+  }
+  for (size_t li = 0; li < g->layers.size(); ++li)
+    for (int i : g->layers[li].in) {
+      if (g->vars[i].role == 2 && g->vars[i].producer < 0)
+        throw Err(CK_ERR_ARG, "variable '" + g->vars[i].name + "' has no producer");
+      if (g->vars[i].producer >= 0) indeg[li]++;
+    }
+  // Kahn's algorithm, always taking the lowest declared index (stable).
+  std::set<int> ready;
+  for (size_t li = 0; li < g->layers.size(); ++li)
+    if (!indeg[li]) ready.insert((int)li);
+  g->order.clear();
+  while (!ready.empty()) {
+    int li = *ready.begin();
+    ready.erase(ready.begin());
+    g->order.push_back(li);
+    for (int o : g->layers[li].out)
+      for (auto [c, s] : g->vars[o].consumers) {
+        (void)s;
+        if (--indeg[c] == 0) ready.insert(c);
+      }
+  }
+  if (g->order.size() != g->layers.size()) throw Err(CK_ERR_ARG, "graph has a cycle");
+
+  for (auto& v : g->vars)
+    if (v.role != 2 && !v.has_shape)
+      throw Err(CK_ERR_ARG, "input/param '" + v.name + "' needs a shape on the device path");
+
+  // Shape inference in firing order (the reference's shape laws).
+  for (int li : g->order) {
+    Layer& l = g->layers[li];
+    auto S = [&](int k) -> ck_shape& { return g->vars[l.in[k]].shape; };
+    ck_shape out{1, 1, 1, 1};
+    switch (l.kind) {
+      case Kind::conv: {
+        need(l, 2, 3, 1);
+        out = conv_output_shape(S(0), S(1), conv_geom_of(l));
+        if (l.in.size() > 2 && elems(S(2)) != S(1).n)
+          throw Err(CK_ERR_SHAPE, "layer '" + l.name + "': bias has " + std::to_string(elems(S(2))) +
+                                      " elements for " + std::to_string(S(1).n) + " filters");
+        break;
+      }
+      case Kind::convt:
+        need(l, 2, 2, 1);
+        out = convt_output_shape(S(0), S(1), convt_geom_of(l));
+        break;
+      case Kind::pool:
+        need(l, 1, 1, 1);
+        out = pool_output_shape(S(0), pool_geom_of(l));
+        break;
+      case Kind::relu:
+        need(l, 1, 1, 1);
+        out = S(0);
+        break;
+      case Kind::lrn: {
+        need(l, 1, 1, 1);
+        ck_lrn_params p = lrn_of(l);
+        if (p.group_size < 1) throw Err(CK_ERR_SHAPE, "lrn group size must be positive");
+        if (p.kappa <= 0) throw Err(CK_ERR_SHAPE, "lrn kappa must be positive");
+        out = S(0);
+        break;
+      }
+      case Kind::bnorm:
+        need(l, 3, 3, 1);
+        need_params(l, 1);
+        if (elems(S(1)) != S(0).c || elems(S(2)) != S(0).c)
+          throw Err(CK_ERR_SHAPE, "layer '" + l.name + "': bnorm expects one multiplier and bias per channel");
+        out = S(0);
+        break;
+      case Kind::loss: {
+        need(l, 2, 3, 1);
+        ck_shape xs = S(0), cs = S(1);
+        if (cs.h != xs.h || cs.w != xs.w || cs.c != 1 || cs.n != xs.n)
+          throw Err(CK_ERR_SHAPE, "layer '" + l.name + "': classification labels must be " +
+                                      shape_str(ck_shape{xs.h, xs.w, 1, xs.n}) + ", got " + shape_str(cs));
+        out = ck_shape{1, 1, 1, 1};
+        break;
+      }
+      case Kind::sum:
+        need(l, 1, 64, 1);
+        for (size_t k = 1; k < l.in.size(); ++k)
+          if (!same(S(k), S(0))) throw Err(CK_ERR_SHAPE, "sum inputs must share one shape");
+        out = S(0);
+        break;
+    }
+    g->vars[l.out[0]].shape = out;
+    g->vars[l.out[0]].has_shape = true;
+  }
+
+  // Allocation: values and derivatives for every variable; parameter
+  // derivatives live in one arena ordered by when backward finishes them,
+  // so each layer's gradient bucket is contiguous for the allreduce.
+  auto alloc = [&](size_t n) -> float* {
+    void* p = nullptr;
+    check_cuda(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(float)), "cudaMalloc");
+    g->allocs.push_back(p);
+    return (float*)p;
+  };
+  std::vector<int> param_order;
+  for (auto it = g->order.rbegin(); it != g->order.rend(); ++it)
+    for (int i : g->layers[*it].in)
+      if (g->vars[i].role == 1 &&
+          std::find(param_order.begin(), param_order.end(), i) == param_order.end())
+        param_order.push_back(i);
+  size_t total = 0;
+  for (int i : param_order) total += (size_t)((elems(g->vars[i].shape) + 31) / 32 * 32);
+  g->param_deriv_arena = alloc(total);
+  g->param_deriv_elems = total;
+  size_t off = 0;
+  for (int i : param_order) {
+    g->vars[i].deriv = g->param_deriv_arena + off;
+    off += (size_t)((elems(g->vars[i].shape) + 31) / 32 * 32);
+  }
+  for (auto& v : g->vars) {
+    v.value = alloc((size_t)elems(v.shape));
+    if (!v.deriv) v.deriv = alloc((size_t)elems(v.shape));
+  }
+  for (auto& l : g->layers)
+    if (l.kind == Kind::bnorm) l.aux = alloc(2 * (size_t)g->vars[l.in[0]].shape.c);
+  g->finalized = true;
+}
+
+static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
+  ck_handle* h = g->h;
+  auto V = [&](int k) { return tv(g->vars[l.in[k]], false); };
+  ck_tensor y = tv(g->vars[l.out[0]], false);
+  ck_status st = CK_OK;
+  switch (l.kind) {
+    case Kind::conv: {
+      ck_tensor x = V(0), f = V(1), b;
+      if (l.in.size() > 2) b = V(2);
+      ck_conv_geom cg = conv_geom_of(l);
+      st = ck_conv_forward(h, &x, &f, l.in.size() > 2 ? &b : nullptr, &cg, &y, g->math, s);
+      break;
+    }
+    case Kind::convt: {
+      ck_tensor x = V(0), f = V(1);
+      ck_convt_geom cg = convt_geom_of(l);
+      st = ck_convt_forward(h, &x, &f, &cg, &y, g->math, s);
+      break;
+    }
+    case Kind::pool: {
+      ck_tensor x = V(0);
+      ck_pool_geom pg = pool_geom_of(l);
+      st = ck_pool_forward(h, &x, &pg, &y, s);
+      break;
+    }
+    case Kind::relu: {
+      ck_tensor x = V(0);
+      st = ck_relu_forward(h, &x, &y, s);
+      break;
+    }
+    case Kind::lrn: {
+      ck_tensor x = V(0);
+      ck_lrn_params p = lrn_of(l);
+      st = ck_lrn_forward(h, &x, &p, &y, s);
+      break;
+    }
+    case Kind::bnorm: {
+      ck_tensor x = V(0), w = V(1), b = V(2);
+      ck_tensor m{l.aux, ck_shape{x.shape.c, 2, 1, 1}};
+      st = ck_bnorm_forward(h, &x, &w, &b, l.p[0], &y, &m, s);
+      break;
+    }
+    case Kind::loss: {
+      ck_tensor x = V(0), c = V(1), w;
+      if (l.in.size() > 2) w = V(2);
+      st = ck_softmaxlog_forward(h, &x, &c, l.in.size() > 2 ? &w : nullptr, y.data, 0, s);
+      break;
+    }
+    case Kind::sum: {
+      ck_tensor x0 = V(0);
+      check_cuda(cudaMemcpyAsync(y.data, x0.data, sizeof(float) * elems(y.shape),
+                                 cudaMemcpyDeviceToDevice, s), "copy");
+      for (size_t k = 1; k < l.in.size(); ++k) axpy_inplace(y.data, V((int)k).data, elems(y.shape), s);
+      break;
+    }
+  }
+  if (st != CK_OK) throw Err(st, "layer '" + l.name + "': " + h->err);
+}
+
+// One layer's backward; contributions for input slot k go to derivs with
+// accumulate = deriv_live (graph.cpp:587-596 fused).
+static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) {
+  ck_handle* h = g->h;
+  auto V = [&](int k) { return tv(g->vars[l.in[k]], false); };
+  auto D = [&](int k) { return tv(g->vars[l.in[k]], true); };
+  auto acc = [&](int k) { return g->vars[l.in[k]].deriv_live ? 1 : 0; };
+  auto mark = [&](int k) { g->vars[l.in[k]].deriv_live = true; };
+  ck_tensor dy = tv(g->vars[l.out[0]], true);
+  ck_status st = CK_OK;
+  switch (l.kind) {
+    case Kind::conv: {
+      ck_tensor x = V(0), f = V(1), dx = D(0), df = D(1), b, db;
+      if (l.in.size() > 2) db = D(2);
+      (void)b;
+      ck_conv_geom cg = conv_geom_of(l);
+      // Independent accumulate flags per output: run the three passes
+      // separately when they differ.
+      int a0 = acc(0), a1 = acc(1), a2 = l.in.size() > 2 ? acc(2) : a1;
+      if (a0 == a1 && a1 == a2) {
+        st = ck_conv_backward(h, &x, &f, &cg, &dy, &dx, &df, l.in.size() > 2 ? &db : nullptr, a0,
+                              g->math, s);
+      } else {
+        st = ck_conv_backward(h, &x, &f, &cg, &dy, &dx, nullptr, nullptr, a0, g->math, s);
+        if (st == CK_OK) st = ck_conv_backward(h, &x, &f, &cg, &dy, nullptr, &df, nullptr, a1, g->math, s);
+        if (st == CK_OK && l.in.size() > 2)
+          st = ck_conv_backward(h, &x, &f, &cg, &dy, nullptr, nullptr, &db, a2, g->math, s);
+      }
+      for (size_t k = 0; k < l.in.size(); ++k) mark((int)k);
+      break;
+    }
+    case Kind::convt: {
+      ck_tensor x = V(0), f = V(1), dx = D(0), df = D(1);
+      ck_convt_geom cg = convt_geom_of(l);
+      int a0 = acc(0), a1 = acc(1);
+      if (a0 == a1) {
+        st = ck_convt_backward(h, &x, &f, &cg, &dy, &dx, &df, a0, g->math, s);
+      } else {
+        st = ck_convt_backward(h, &x, &f, &cg, &dy, &dx, nullptr, a0, g->math, s);
+        if (st == CK_OK) st = ck_convt_backward(h, &x, &f, &cg, &dy, nullptr, &df, a1, g->math, s);
+      }
+      mark(0);
+      mark(1);
+      break;
+    }
+    case Kind::pool: {
+      ck_tensor x = V(0), dx = D(0);
+      ck_pool_geom pg = pool_geom_of(l);
+      st = ck_pool_backward(h, &x, &pg, &dy, &dx, acc(0), s);
+      mark(0);
+      break;
+    }
+    case Kind::relu: {
+      ck_tensor x = V(0), dx = D(0);
+      st = ck_relu_backward(h, &x, &dy, &dx, acc(0), s);
+      mark(0);
+      break;
+    }
+    case Kind::lrn: {
+      ck_tensor x = V(0), dx = D(0);
+      ck_lrn_params p = lrn_of(l);
+      st = ck_lrn_backward(h, &x, &p, &dy, &dx, acc(0), s);
+      mark(0);
+      break;
+    }
+    case Kind::bnorm: {
+      ck_tensor x = V(0), w = V(1), b = V(2), dx = D(0), dw = D(1), db = D(2);
+      int a0 = acc(0), a1 = acc(1), a2 = acc(2);
+      if (a0 == a1 && a1 == a2) {
+        st = ck_bnorm_backward(h, &x, &w, &b, l.p[0], &dy, &dx, &dw, &db, a0, s);
+      } else {
+        st = ck_bnorm_backward(h, &x, &w, &b, l.p[0], &dy, &dx, nullptr, nullptr, a0, s);
+        if (st == CK_OK) st = ck_bnorm_backward(h, &x, &w, &b, l.p[0], &dy, nullptr, &dw, nullptr, a1, s);
+        if (st == CK_OK) st = ck_bnorm_backward(h, &x, &w, &b, l.p[0], &dy, nullptr, nullptr, &db, a2, s);
+      }
+      mark(0);
+      mark(1);
+      mark(2);
+      break;
+    }
+    case Kind::loss: {
+      ck_tensor x = V(0), c = V(1), dx = D(0), w;
+      if (l.in.size() > 2) w = V(2);
+      st = ck_softmaxlog_backward(h, &x, &c, l.in.size() > 2 ? &w : nullptr, seed_p, &dx, acc(0), s);
+      mark(0);  // labels / weights carry no derivative: left for the final zeroing
+      break;
+    }
+    case Kind::sum: {
+      for (size_t k = 0; k < l.in.size(); ++k) {
+        ck_tensor dx = D((int)k);
+        if (acc((int)k))
+          axpy_inplace(dx.data, dy.data, elems(dy.shape), s);
+        else
+          check_cuda(cudaMemcpyAsync(dx.data, dy.data, sizeof(float) * elems(dy.shape),
+                                     cudaMemcpyDeviceToDevice, s), "copy");
+        mark((int)k);
+      }
+      break;
+    }
+  }
+  if (st != CK_OK) throw Err(st, "layer '" + l.name + "': " + h->err);
+}
+
+// graph.cpp:494-545 forward (train mode).
+static void run_forward(ck_graph* g, cudaStream_t s) {
+  for (int li : g->order) {
+    g->prof(li, 0, s);
+    layer_forward(g, g->layers[li], s);
+    g->prof(li, 1, s);
+    if (g->profiling) g->prof_fwd_done[li] = 1;
+  }
+}
+
+struct LayerDone {
+  // Called after each layer's backward with the layer index; used by the
+  // trainer to launch the gradient allreduce of finished parameters.
+  virtual void done(int li, cudaStream_t s) = 0;
+  virtual ~LayerDone() = default;
+};
+
+// graph.cpp:548-598 backward with d(objective) = 1.
+static void run_backward(ck_graph* g, int objective, cudaStream_t s, LayerDone* cb) {
+  for (auto& v : g->vars) v.deriv_live = false;
+  Var& obj = g->vars[objective];
+  if (elems(obj.shape) != 1) throw Err(CK_ERR_ARG, "objective '" + obj.name + "' is not a scalar");
+  const float one = 1.0f;
+  check_cuda(cudaMemcpyAsync(obj.deriv, &one, sizeof(float), cudaMemcpyHostToDevice, s), "seed");
+  obj.deriv_live = true;
+  for (auto it = g->order.rbegin(); it != g->order.rend(); ++it) {
+    Layer& l = g->layers[*it];
+    bool any = false;
+    for (int o : l.out) any |= g->vars[o].deriv_live;
+    if (any) {
+      // A loss layer's projection is the objective seed (graph.cpp:420-425).
+      float p = 1.0f;
+      if (l.kind == Kind::loss && l.out[0] != objective) {
+        check_cuda(cudaMemcpyAsync(&p, g->vars[l.out[0]].deriv, sizeof(float),
+                                   cudaMemcpyDeviceToHost, s), "projection");
+        check_cuda(cudaStreamSynchronize(s), "synchronize");
+      }
+      g->prof(*it, 2, s);
+      layer_backward(g, l, p, s);
+      g->prof(*it, 3, s);
+      if (g->profiling) g->prof_bwd_done[*it] = 1;
+    }
+    if (cb) cb->done(*it, s);
+  }
+  // Derivatives nobody wrote are the reference's zero-initialised tensors.
+  for (auto& v : g->vars)
+    if (!v.deriv_live)
+      check_cuda(cudaMemsetAsync(v.deriv, 0, sizeof(float) * elems(v.shape), s), "zero");
+}
+
+}  // namespace ck
+
+// ---- trainer ---------------------------------------------------------------
+
+struct ck_trainer : ck::LayerDone {
+  ck_graph* g = nullptr;
+  int objective = -1;
+  float lr = 0.01f, momentum = 0.9f, wd = 5e-4f;
+  std::vector<int> params;         // param var indices
+  std::vector<float*> mom;         // momentum buffers
+  // DP
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> ev;     // per layer "gradient ready"
+  cudaEvent_t comm_done = nullptr;
+  std::vector<std::vector<int>> layer_params;  // params finished by layer li
+  float* loss_dev = nullptr;
+
+  void done(int li, cudaStream_t s) override {
+    const auto& ps = layer_params[li];
+    if (ps.empty()) return;
+    if (comm) {
+      // Contiguous bucket [first, last] of this layer's parameter derivs.
+      float* lo = nullptr;
+      float* hi = nullptr;
+      for (int p : ps) {
+        ck::Var& v = g->vars[p];
+        float* a = v.deriv;
+        float* b = v.deriv + ck::elems(v.shape);
+        if (!lo || a < lo) lo = a;
+        if (!hi || b > hi) hi = b;
+      }
+      ck::check_cuda(cudaEventRecord(ev[li], s), "event");
+      ck::check_cuda(cudaStreamWaitEvent(comm_stream, ev[li], 0), "wait");
+      if (ncclAllReduce(lo, lo, (size_t)(hi - lo), ncclFloat, ncclSum, comm, comm_stream) !=
+          ncclSuccess)
+        throw Err(CK_ERR_CUDA, "ncclAllReduce failed");
+      for (int p : ps) sgd(p, comm_stream);
+    } else {
+      for (int p : ps) sgd(p, s);
+    }
+  }
+  void sgd(int p, cudaStream_t s) {
+    ck::Var& v = g->vars[p];
+    size_t k = std::find(params.begin(), params.end(), p) - params.begin();
+    ck_status st = ck_sgd_step(g->h, v.value, mom[k], v.deriv, ck::elems(v.shape), lr, momentum,
+                               wd, s);
+    if (st != CK_OK) throw Err(st, g->h->err);
+  }
+  ~ck_trainer() override {
+    for (float* m : mom) cudaFree(m);
+    for (auto e : ev) cudaEventDestroy(e);
+    if (comm_done) cudaEventDestroy(comm_done);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+    if (comm) ncclCommDestroy(comm);
+    if (loss_dev) cudaFree(loss_dev);
+  }
+};
+
+using namespace ck;
+
+#define CKG_BEGIN(gr)                     \
+  if (!(gr) || !(gr)->h) return CK_ERR_ARG; \
+  ck::HandleScope _scope((gr)->h);        \
+  try {
+#define CKG_END(gr)                       \
+  return CK_OK;                           \
+  }                                       \
+  catch (const ck::Err& e) {              \
+    (gr)->h->err = e.what();              \
+    return e.code;                        \
+  }                                       \
+  catch (const std::exception& e) {       \
+    (gr)->h->err = e.what();              \
+    return CK_ERR_ARG;                    \
+  }
+
+extern "C" {
+
+ck_status ck_graph_create(ck_handle* h, ck_graph** out) {
+  if (!h || !out) return CK_ERR_ARG;
+  *out = new ck_graph();
+  (*out)->h = h;
+  return CK_OK;
+}
+
+void ck_graph_destroy(ck_graph* g) {
+  if (!g) return;
+  cudaSetDevice(g->h->device);
+  cudaDeviceSynchronize();
+  delete g;
+}
+
+static ck_status add_var(ck_graph* g, const char* name, ck_shape shape, int role) {
+  CKG_BEGIN(g)
+  if (g->finalized) throw Err(CK_ERR_ARG, "graph already finalized");
+  if (!name || !*name) throw Err(CK_ERR_ARG, "empty variable name");
+  if (g->by_name.count(name)) throw Err(CK_ERR_ARG, std::string("variable '") + name + "' declared twice");
+  if (shape.h < 1 || shape.w < 1 || shape.c < 1 || shape.n < 1)
+    throw Err(CK_ERR_SHAPE, "invalid tensor shape " + shape_str(shape));
+  int k = g->intern(name, role);
+  g->vars[k].shape = shape;
+  g->vars[k].has_shape = true;
+  CKG_END(g)
+}
+
+ck_status ck_graph_add_input(ck_graph* g, const char* name, ck_shape shape) {
+  return add_var(g, name, shape, 0);
+}
+ck_status ck_graph_add_param(ck_graph* g, const char* name, ck_shape shape) {
+  return add_var(g, name, shape, 1);
+}
+
+ck_status ck_graph_add_layer(ck_graph* g, const char* kind, const char* name,
+                             const char* inputs_csv, const char* outputs_csv,
+                             const double* params, int nparams) {
+  CKG_BEGIN(g)
+  if (g->finalized) throw Err(CK_ERR_ARG, "graph already finalized");
+  Layer l;
+  l.name = name ? name : "";
+  l.kind = kind_from_name(kind ? kind : "");
+  for (auto& n : split_csv(inputs_csv)) l.in.push_back(g->intern(n, 2));
+  for (auto& n : split_csv(outputs_csv)) l.out.push_back(g->intern(n, 2));
+  if (l.out.empty()) throw Err(CK_ERR_ARG, "layer '" + l.name + "' has no outputs");
+  if (params && nparams > 0) l.p.assign(params, params + nparams);
+  g->layers.push_back(std::move(l));
+  CKG_END(g)
+}
+
+ck_status ck_graph_finalize(ck_graph* g, ck_math math) {
+  CKG_BEGIN(g)
+  if (g->finalized) throw Err(CK_ERR_ARG, "graph already finalized");
+  g->math = math;
+  finalize(g);
+  CKG_END(g)
+}
+
+ck_status ck_graph_var(ck_graph* g, const char* name, int deriv, ck_tensor* out) {
+  CKG_BEGIN(g)
+  if (!g->finalized) throw Err(CK_ERR_ARG, "graph not finalized");
+  if (!out) throw Err(CK_ERR_ARG, "null output");
+  Var& v = g->vars[g->var(name ? name : "")];
+  *out = tv(v, deriv != 0);
+  CKG_END(g)
+}
+
+ck_status ck_graph_forward(ck_graph* g, ck_stream stream) {
+  CKG_BEGIN(g)
+  if (!g->finalized) throw Err(CK_ERR_ARG, "forward on a non-finalized graph");
+  int64_t before = g->h->counter.n;
+  run_forward(g, (cudaStream_t)stream);
+  g->last_launches = g->h->counter.n - before;
+  CKG_END(g)
+}
+
+ck_status ck_graph_backward(ck_graph* g, const char* objective, ck_stream stream) {
+  CKG_BEGIN(g)
+  if (!g->finalized) throw Err(CK_ERR_ARG, "backward on a non-finalized graph");
+  int64_t before = g->h->counter.n;
+  run_backward(g, g->var(objective ? objective : ""), (cudaStream_t)stream, nullptr);
+  g->last_launches += g->h->counter.n - before;
+  CKG_END(g)
+}
+
+int64_t ck_graph_last_launches(const ck_graph* g) { return g ? g->last_launches : 0; }
+
+ck_status ck_graph_set_profiling(ck_graph* g, int enable) {
+  CKG_BEGIN(g)
+  if (enable && g->prof_ev.empty()) {
+    g->prof_ev.resize(4 * g->layers.size());
+    for (auto& e : g->prof_ev) check_cuda(cudaEventCreate(&e), "event");
+  }
+  g->prof_fwd_done.assign(g->layers.size(), 0);
+  g->prof_bwd_done.assign(g->layers.size(), 0);
+  g->profiling = enable != 0;
+  CKG_END(g)
+}
+
+int ck_graph_layer_count(const ck_graph* g) { return g ? (int)g->layers.size() : 0; }
+
+const char* ck_graph_layer_name(const ck_graph* g, int layer) {
+  if (!g || layer < 0 || layer >= (int)g->layers.size()) return "";
+  return g->layers[layer].name.c_str();
+}
+
+ck_status ck_graph_layer_ms(ck_graph* g, int layer, float* fwd_ms, float* bwd_ms) {
+  CKG_BEGIN(g)
+  if (layer < 0 || layer >= (int)g->layers.size()) throw Err(CK_ERR_ARG, "bad layer index");
+  if (g->prof_ev.empty()) throw Err(CK_ERR_ARG, "profiling was never enabled");
+  float a = 0.f, b = 0.f;
+  if (g->prof_fwd_done[layer])
+    check_cuda(cudaEventElapsedTime(&a, g->prof_ev[4 * layer], g->prof_ev[4 * layer + 1]), "elapsed");
+  if (g->prof_bwd_done[layer])
+    check_cuda(cudaEventElapsedTime(&b, g->prof_ev[4 * layer + 2], g->prof_ev[4 * layer + 3]), "elapsed");
+  if (fwd_ms) *fwd_ms = a;
+  if (bwd_ms) *bwd_ms = b;
+  CKG_END(g)
+}
+
+ck_status ck_nccl_unique_id(char out[128]) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return CK_ERR_CUDA;
+  std::memcpy(out, &id, 128);
+  return CK_OK;
+}
+
+ck_status ck_trainer_create(ck_graph* g, const char* objective, float lr, float momentum,
+                            float weight_decay, ck_trainer** out) {
+  CKG_BEGIN(g)
+  if (!g->finalized) throw Err(CK_ERR_ARG, "trainer needs a finalized graph");
+  if (!out) throw Err(CK_ERR_ARG, "null output");
+  auto t = std::make_unique<ck_trainer>();
+  t->g = g;
+  t->objective = g->var(objective ? objective : "");
+  t->lr = lr;
+  t->momentum = momentum;
+  t->wd = weight_decay;
+  t->layer_params.assign(g->layers.size(), {});
+  // A parameter is final after its last consumer in backward order, i.e.
+  // its first consumer in firing order.
+  std::vector<int> pos(g->layers.size());
+  for (size_t k = 0; k < g->order.size(); ++k) pos[g->order[k]] = (int)k;
+  for (size_t i = 0; i < g->vars.size(); ++i) {
+    Var& v = g->vars[i];
+    if (v.role != 1 || v.consumers.empty()) continue;
+    int first = v.consumers[0].first;
+    for (auto [c, s] : v.consumers) {
+      (void)s;
+      if (pos[c] < pos[first]) first = c;
+    }
+    t->layer_params[first].push_back((int)i);
+    t->params.push_back((int)i);
+    float* m = nullptr;
+    check_cuda(cudaMalloc(&m, sizeof(float) * std::max<int64_t>(1, elems(v.shape))), "cudaMalloc");
+    check_cuda(cudaMemset(m, 0, sizeof(float) * elems(v.shape)), "memset");
+    t->mom.push_back(m);
+  }
+  t->ev.resize(g->layers.size());
+  for (auto& e : t->ev) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  check_cuda(cudaEventCreateWithFlags(&t->comm_done, cudaEventDisableTiming), "event");
+  check_cuda(cudaMalloc(&t->loss_dev, sizeof(float)), "cudaMalloc");
+  *out = t.release();
+  CKG_END(g)
+}
+
+void ck_trainer_destroy(ck_trainer* t) {
+  if (!t) return;
+  cudaSetDevice(t->g->h->device);
+  cudaDeviceSynchronize();
+  delete t;
+}
+
+ck_status ck_trainer_init_dp(ck_trainer* t, const char id[128], int rank, int world) {
+  if (!t) return CK_ERR_ARG;
+  ck_graph* g = t->g;
+  CKG_BEGIN(g)
+  if (world < 1 || rank < 0 || rank >= world) throw Err(CK_ERR_ARG, "bad rank/world");
+  t->rank = rank;
+  t->world = world;
+  if (world == 1) return CK_OK;
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, 128);
+  if (ncclCommInitRank(&t->comm, world, uid, rank) != ncclSuccess)
+    throw Err(CK_ERR_CUDA, "ncclCommInitRank failed");
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  check_cuda(cudaStreamCreateWithPriority(&t->comm_stream, cudaStreamNonBlocking, hi), "stream");
+  CKG_END(g)
+}
+
+ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
+  if (!t) return CK_ERR_ARG;
+  ck_graph* g = t->g;
+  CKG_BEGIN(g)
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t before = g->h->counter.n;
+  run_forward(g, s);
+  run_backward(g, t->objective, s, t);
+  if (t->comm) {
+    // Loss: summed over ranks for reporting only.
+    Var& obj = g->vars[t->objective];
+    check_cuda(cudaEventRecord(t->ev[0], s), "event");
+    check_cuda(cudaStreamWaitEvent(t->comm_stream, t->ev[0], 0), "wait");
+    if (ncclAllReduce(obj.value, t->loss_dev, 1, ncclFloat, ncclSum, t->comm, t->comm_stream) !=
+        ncclSuccess)
+      throw Err(CK_ERR_CUDA, "ncclAllReduce failed");
+    check_cuda(cudaEventRecord(t->comm_done, t->comm_stream), "event");
+    check_cuda(cudaStreamWaitEvent(s, t->comm_done, 0), "wait");
+  } else {
+    Var& obj = g->vars[t->objective];
+    check_cuda(cudaMemcpyAsync(t->loss_dev, obj.value, sizeof(float), cudaMemcpyDeviceToDevice, s),
+               "copy");
+  }
+  if (loss_host) {
+    check_cuda(cudaMemcpyAsync(loss_host, t->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, s),
+               "copy");
+    check_cuda(cudaStreamSynchronize(s), "synchronize");
+  }
+  g->last_launches = g->h->counter.n - before;
+  CKG_END(g)
+}
+
+}  // extern "C"

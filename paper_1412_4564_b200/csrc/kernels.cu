@@ -1,0 +1,741 @@
+// Memory-bound block kernels for sm_100a: ReLU, pooling, LRN, batch norm,
+// softmaxlog loss, SGD.  All tensors are HWCN fp32 (tensor.hpp:70-72).
+//
+// Parity notes (see tests/test_gpu_blocks.py):
+//  * relu, max/avg pooling, SGD: bit-exact with the reference CPU path.  Every
+//    float operation the reference performs is issued as an explicitly
+//    rounded intrinsic (__fadd_rn / __fmul_rn / __fdiv_rn) so nvcc cannot
+//    contract it into an FMA, and reductions run in the reference's order.
+//  * LRN uses the same explicit rounding; powf may differ from glibc's in the
+//    last ulp, so parity there is within 1e-6 relative.
+//  * bnorm and the loss reduce in double with a fixed, deterministic tree.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ck_internal.hpp"
+
+namespace ck {
+
+thread_local LaunchCounter* g_counter = nullptr;
+
+namespace {
+
+constexpr int kSMs = 148;
+
+inline int blocks_for(int64_t n, int threads, int per_sm = 16) {
+  int64_t b = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)kSMs * per_sm;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+// ---------------------------------------------------------------- ReLU ----
+// activation.cpp:8-12 (y = x > 0 ? x : 0) and :15-22 (dx = x > 0 ? dy : 0).
+
+__global__ void relu_fwd_v4(const float4* __restrict__ x, float4* __restrict__ y, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = x[i];
+    v.x = v.x > 0.f ? v.x : 0.f;
+    v.y = v.y > 0.f ? v.y : 0.f;
+    v.z = v.z > 0.f ? v.z : 0.f;
+    v.w = v.w > 0.f ? v.w : 0.f;
+    y[i] = v;
+  }
+}
+
+__global__ void relu_fwd_s(const float* __restrict__ x, float* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = x[i] > 0.f ? x[i] : 0.f;
+}
+
+template <bool kAcc>
+__global__ void relu_bwd_v4(const float4* __restrict__ x, const float4* __restrict__ dy,
+                            float4* dx, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = x[i], g = dy[i], r;
+    r.x = a.x > 0.f ? g.x : 0.f;
+    r.y = a.y > 0.f ? g.y : 0.f;
+    r.z = a.z > 0.f ? g.z : 0.f;
+    r.w = a.w > 0.f ? g.w : 0.f;
+    if (kAcc) {
+      float4 o = dx[i];
+      r.x = __fadd_rn(o.x, r.x);
+      r.y = __fadd_rn(o.y, r.y);
+      r.z = __fadd_rn(o.z, r.z);
+      r.w = __fadd_rn(o.w, r.w);
+    }
+    dx[i] = r;
+  }
+}
+
+template <bool kAcc>
+__global__ void relu_bwd_s(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
+                           int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float r = x[i] > 0.f ? dy[i] : 0.f;
+    dx[i] = kAcc ? __fadd_rn(dx[i], r) : r;
+  }
+}
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// --------------------------------------------------------- axpy / SGD -----
+
+__global__ void axpy_k(float* y, const float* __restrict__ x, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = __fadd_rn(y[i], x[i]);
+}
+
+// SPEC.md:706 v <- m v - lr (g + wd w); w <- w + v, each product/sum rounded
+// exactly as the scalar C++ expression (no FMA contraction).
+__global__ void sgd_k(float* w, float* v, const float* __restrict__ g, int64_t n, float lr,
+                      float mom, float wd) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float wi = w[i];
+    float t = __fadd_rn(g[i], __fmul_rn(wd, wi));
+    float vi = __fadd_rn(__fmul_rn(mom, v[i]), -__fmul_rn(lr, t));
+    v[i] = vi;
+    w[i] = __fadd_rn(wi, vi);
+  }
+}
+
+// ------------------------------------------------------------- pooling ----
+// pool.cpp:24-32 window_at: the window is clipped to the real signal.
+struct Win {
+  int i0, i1, j0, j1;
+};
+__device__ __forceinline__ Win window_at(const PoolDims& d, int oi, int oj) {
+  Win b;
+  int si = d.sh * oi - d.pt, sj = d.sw * oj - d.pl;
+  b.i0 = max(0, si);
+  b.i1 = min(d.H, si + d.wh);
+  b.j0 = max(0, sj);
+  b.j1 = min(d.W, sj + d.ww);
+  return b;
+}
+
+// One thread per output element, consecutive threads along H (coalesced).
+// max: first strict maximum in j-outer / i-inner order (pool.cpp:58-66).
+// avg: sum in the same order, divided by the clipped area (pool.cpp:67-74).
+__global__ void pool_fwd_k(const float* __restrict__ x, float* __restrict__ y, PoolDims d) {
+  const int64_t total = (int64_t)d.OH * d.OW * d.C * d.N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int oi = (int)(e % d.OH);
+    int64_t r = e / d.OH;
+    int oj = (int)(r % d.OW);
+    int64_t plane = r / d.OW;  // c + C*n
+    const float* xp = x + plane * (int64_t)d.H * d.W;
+    Win b = window_at(d, oi, oj);
+    float out;
+    if (d.mode == 0) {
+      float best = xp[b.i0 + d.H * b.j0];
+      for (int j = b.j0; j < b.j1; ++j)
+        for (int i = b.i0; i < b.i1; ++i) {
+          float v = xp[i + d.H * j];
+          if (v > best) best = v;
+        }
+      out = best;
+    } else {
+      float sum = 0.f;
+      for (int j = b.j0; j < b.j1; ++j)
+        for (int i = b.i0; i < b.i1; ++i) sum = __fadd_rn(sum, xp[i + d.H * j]);
+      float area = (float)((b.i1 - b.i0) * (b.j1 - b.j0));
+      out = __fdiv_rn(sum, area);
+    }
+    y[e] = out;
+  }
+}
+
+// Gather form of pool.cpp:83-126: each input element sums the contributions
+// of the windows that route to it, in the reference's (oj, oi) scatter order,
+// starting from 0 -- so the float sum is bit-identical and needs no atomics.
+template <bool kAcc>
+__global__ void pool_bwd_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
+                           PoolDims d) {
+  const int64_t total = (int64_t)d.H * d.W * d.C * d.N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int i = (int)(e % d.H);
+    int64_t r = e / d.H;
+    int j = (int)(r % d.W);
+    int64_t plane = r / d.W;
+    const float* xp = x + plane * (int64_t)d.H * d.W;
+    const float* dyp = dy + plane * (int64_t)d.OH * d.OW;
+    // Output windows whose (unclipped) span covers i: s*oi - pt <= i < s*oi - pt + wh.
+    int oi_lo = i + d.pt - d.wh + 1;
+    oi_lo = oi_lo <= 0 ? 0 : (oi_lo + d.sh - 1) / d.sh;
+    int oi_hi = min(d.OH - 1, (i + d.pt) / d.sh);
+    int oj_lo = j + d.pl - d.ww + 1;
+    oj_lo = oj_lo <= 0 ? 0 : (oj_lo + d.sw - 1) / d.sw;
+    int oj_hi = min(d.OW - 1, (j + d.pl) / d.sw);
+    float acc = 0.f;
+    for (int oj = oj_lo; oj <= oj_hi; ++oj)
+      for (int oi = oi_lo; oi <= oi_hi; ++oi) {
+        Win b = window_at(d, oi, oj);
+        float p = dyp[oi + d.OH * oj];
+        if (d.mode == 0) {
+          int bi = b.i0, bj = b.j0;
+          float best = xp[b.i0 + d.H * b.j0];
+          for (int jj = b.j0; jj < b.j1; ++jj)
+            for (int ii = b.i0; ii < b.i1; ++ii) {
+              float v = xp[ii + d.H * jj];
+              if (v > best) {
+                best = v;
+                bi = ii;
+                bj = jj;
+              }
+            }
+          if (bi == i && bj == j) acc = __fadd_rn(acc, p);
+        } else {
+          float area = (float)((b.i1 - b.i0) * (b.j1 - b.j0));
+          acc = __fadd_rn(acc, __fdiv_rn(p, area));
+        }
+      }
+    dx[e] = kAcc ? __fadd_rn(dx[e], acc) : acc;
+  }
+}
+
+// ----------------------------------------------------------------- LRN ----
+// normalize.cpp:18-22 lrn_group: [k - (n-1)/2, k + n-1-(n-1)/2] clipped.
+// A block owns kLrnPix consecutive pixels of one image and stages all their
+// channels in shared memory (coalesced loads along H), so the channel-window
+// sums never re-read HBM.
+constexpr int kLrnPix = 32;
+
+__global__ void lrn_fwd_k(const float* __restrict__ x, float* __restrict__ y, int HW, int C,
+                          int size, float kappa, float alpha, float nbeta) {
+  extern __shared__ float sm[];
+  float* sq = sm;  // [C][kLrnPix] squares
+  const int n = blockIdx.y;
+  const int p0 = blockIdx.x * kLrnPix;
+  const int lane = threadIdx.x % kLrnPix;
+  const int row = threadIdx.x / kLrnPix, rows = blockDim.x / kLrnPix;
+  const int p = p0 + lane;
+  const bool ok = p < HW;
+  const float* xb = x + (int64_t)n * C * HW;
+  float* yb = y + (int64_t)n * C * HW;
+  for (int k = row; k < C; k += rows) {
+    float v = ok ? xb[(int64_t)k * HW + p] : 0.f;
+    sq[k * kLrnPix + lane] = __fmul_rn(v, v);
+  }
+  __syncthreads();
+  const int down = (size - 1) / 2, up = size - 1 - down;
+  for (int k = row; k < C; k += rows) {
+    int lo = max(0, k - down), hi = min(C - 1, k + up);
+    float acc = 0.f;
+    for (int t = lo; t <= hi; ++t) acc = __fadd_rn(acc, sq[t * kLrnPix + lane]);
+    float scale = powf(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
+    if (ok) yb[(int64_t)k * HW + p] = __fmul_rn(xb[(int64_t)k * HW + p], scale);
+  }
+}
+
+// normalize.cpp:74-118: dx_d = dy_d L_d^-b - 2 a b x_d sum_{k: d in G(k)} eta_k,
+// eta_k = dy_k L_k^(-b-1) x_k.
+template <bool kAcc>
+__global__ void lrn_bwd_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
+                          int HW, int C, int size, float kappa, float alpha, float beta) {
+  extern __shared__ float sm[];
+  float* xs = sm;                  // [C][P]
+  float* Ls = sm + C * kLrnPix;    // [C][P]
+  float* eta = Ls + C * kLrnPix;   // [C][P]
+  const int n = blockIdx.y;
+  const int p0 = blockIdx.x * kLrnPix;
+  const int lane = threadIdx.x % kLrnPix;
+  const int row = threadIdx.x / kLrnPix, rows = blockDim.x / kLrnPix;
+  const int p = p0 + lane;
+  const bool ok = p < HW;
+  const int64_t base = (int64_t)n * C * HW;
+  for (int k = row; k < C; k += rows) xs[k * kLrnPix + lane] = ok ? x[base + (int64_t)k * HW + p] : 0.f;
+  __syncthreads();
+  const int down = (size - 1) / 2, up = size - 1 - down;
+  const float nb1 = -beta - 1.f;
+  for (int k = row; k < C; k += rows) {
+    int lo = max(0, k - down), hi = min(C - 1, k + up);
+    float acc = 0.f;
+    for (int t = lo; t <= hi; ++t) {
+      float v = xs[t * kLrnPix + lane];
+      acc = __fadd_rn(acc, __fmul_rn(v, v));
+    }
+    float L = __fadd_rn(kappa, __fmul_rn(alpha, acc));
+    Ls[k * kLrnPix + lane] = L;
+    float g = ok ? dy[base + (int64_t)k * HW + p] : 0.f;
+    eta[k * kLrnPix + lane] = __fmul_rn(__fmul_rn(g, powf(L, nb1)), xs[k * kLrnPix + lane]);
+  }
+  __syncthreads();
+  const float c2ab = __fmul_rn(__fmul_rn(2.f, alpha), beta);
+  for (int d = row; d < C; d += rows) {
+    int klo = max(0, d - up), khi = min(C - 1, d + down);
+    float acc = 0.f;
+    for (int k = klo; k <= khi; ++k) acc = __fadd_rn(acc, eta[k * kLrnPix + lane]);
+    if (ok) {
+      int64_t e = base + (int64_t)d * HW + p;
+      float g = dy[e];
+      float r = __fadd_rn(__fmul_rn(g, powf(Ls[d * kLrnPix + lane], -beta)),
+                          -__fmul_rn(__fmul_rn(c2ab, xs[d * kLrnPix + lane]), acc));
+      dx[e] = kAcc ? __fadd_rn(dx[e], r) : r;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- bnorm ---
+// Per-channel moments over H*W*N (normalize.cpp:132-161).  Grid (C, splits):
+// each block reduces a contiguous run of images of one channel in double and
+// writes one partial; bnorm_finish sums the partials in a fixed order.
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <bool kGrad>
+__global__ void bnorm_stats_k(const float* __restrict__ x, const float* __restrict__ dy,
+                              double* partial, int HW, int C, int N, int splits) {
+  const int c = blockIdx.x, s = blockIdx.y;
+  const int n0 = (int)((int64_t)N * s / splits), n1 = (int)((int64_t)N * (s + 1) / splits);
+  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  for (int n = n0; n < n1; ++n) {
+    const int64_t base = ((int64_t)n * C + c) * HW;
+    for (int p = threadIdx.x; p < HW; p += blockDim.x) {
+      double v = x[base + p];
+      a0 += v;
+      a1 += v * v;
+      if (kGrad) {
+        double g = dy[base + p];
+        a2 += g;
+        a3 += g * v;
+      }
+    }
+  }
+  __shared__ double red[4][32];
+  a0 = warp_sum(a0);
+  a1 = warp_sum(a1);
+  if (kGrad) {
+    a2 = warp_sum(a2);
+    a3 = warp_sum(a3);
+  }
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  if (l == 0) {
+    red[0][w] = a0;
+    red[1][w] = a1;
+    red[2][w] = a2;
+    red[3][w] = a3;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double t = 0;
+    for (int k = 0; k < (int)(blockDim.x / 32); ++k) t += red[threadIdx.x][k];
+    partial[((int64_t)s * C + c) * 4 + threadIdx.x] = t;
+  }
+}
+
+__global__ void bnorm_finish_k(const double* partial, double* out, int C, int splits) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double t[4] = {0, 0, 0, 0};
+  for (int s = 0; s < splits; ++s)
+    for (int q = 0; q < 4; ++q) t[q] += partial[((int64_t)s * C + c) * 4 + q];
+  for (int q = 0; q < 4; ++q) out[c * 4 + q] = t[q];
+}
+
+// y = w (x - mu) inv + b (normalize.cpp:172-178); moments_out gets the K x 2
+// (mean, var) tensor of graph.cpp:259-266.  fixed_moments (bnorm_infer) takes
+// precedence over stats.
+__global__ void bnorm_apply_k(const float* __restrict__ x, const float* __restrict__ w,
+                              const float* __restrict__ b, const double* __restrict__ stats,
+                              const float* __restrict__ fixed, float* __restrict__ y,
+                              float* __restrict__ mom_out, double eps, int HW, int C, int N) {
+  const int c = blockIdx.x;
+  const double M = (double)HW * N;
+  float mu, inv;
+  if (fixed) {
+    mu = fixed[c];
+    inv = (float)(1.0 / sqrt((double)fixed[C + c] + eps));
+  } else {
+    double m = stats[c * 4] / M;
+    double var = stats[c * 4 + 1] / M - m * m;
+    if (var < 0) var = 0;
+    mu = (float)m;
+    inv = (float)(1.0 / sqrt(var + eps));
+    if (mom_out && blockIdx.y == 0 && threadIdx.x == 0) {
+      mom_out[c] = (float)m;
+      mom_out[C + c] = (float)var;
+    }
+  }
+  const float wk = w[c], bk = b[c];
+  for (int n = blockIdx.y; n < N; n += gridDim.y) {
+    const int64_t base = ((int64_t)n * C + c) * HW;
+    for (int p = threadIdx.x; p < HW; p += blockDim.x)
+      y[base + p] = __fadd_rn(__fmul_rn(__fmul_rn(wk, __fadd_rn(x[base + p], -mu)), inv), bk);
+  }
+}
+
+// normalize.cpp:212-265 with the moments and both reductions taken from
+// stats = {sum x, sum x^2, sum dy, sum dy x}:
+//   sum dy xhat = inv (sum dy x - mu sum dy)
+//   dx = w inv (dy - mean(dy) - xhat mean(dy xhat))
+template <bool kAcc>
+__global__ void bnorm_bwd_k(const float* __restrict__ x, const float* __restrict__ dy,
+                            const float* __restrict__ w, const double* __restrict__ stats,
+                            double eps, float* dx, float* dw, float* db, int HW, int C, int N,
+                            int acc_params) {
+  const int c = blockIdx.x;
+  const double M = (double)HW * N;
+  const double m = stats[c * 4] / M;
+  double var = stats[c * 4 + 1] / M - m * m;
+  if (var < 0) var = 0;
+  const double invd = 1.0 / sqrt(var + eps);
+  const double sdy = stats[c * 4 + 2];
+  const double sdyx = invd * (stats[c * 4 + 3] - m * sdy);
+  if (blockIdx.y == 0 && threadIdx.x == 0) {
+    if (dw) dw[c] = acc_params ? dw[c] + (float)sdyx : (float)sdyx;
+    if (db) db[c] = acc_params ? db[c] + (float)sdy : (float)sdy;
+  }
+  if (!dx) return;
+  const float mu = (float)m, inv = (float)invd, wk = w[c];
+  const float mdy = (float)(sdy / M), mdyx = (float)(sdyx / M);
+  const float winv = __fmul_rn(wk, inv);
+  for (int n = blockIdx.y; n < N; n += gridDim.y) {
+    const int64_t base = ((int64_t)n * C + c) * HW;
+    for (int p = threadIdx.x; p < HW; p += blockDim.x) {
+      float xhat = __fmul_rn(__fadd_rn(x[base + p], -mu), inv);
+      float r = __fmul_rn(winv, __fadd_rn(__fadd_rn(dy[base + p], -mdy), -__fmul_rn(xhat, mdyx)));
+      dx[base + p] = kAcc ? __fadd_rn(dx[base + p], r) : r;
+    }
+  }
+}
+
+// ----------------------------------------------------------------- loss ---
+// loss.cpp:14-18 as_label, :101-106 range check.  flag bit 1: non-integer
+// label, bit 2: out of range (reported by the C ABI as CK_ERR_DATA).
+__device__ __forceinline__ int read_label(const float* labels, int64_t e, int C, int* flag) {
+  float v = labels[e];
+  float r = nearbyintf(v);
+  if (r != v) {
+    atomicOr(flag, 1);
+    return 0;
+  }
+  int c = (int)r;
+  if (c != 0 && (c < 1 || c > C)) {
+    atomicOr(flag, 2);
+    return 0;
+  }
+  return c;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sumf(float v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One warp per site (i, j, n); channels are HW apart.  Per-site loss
+// w * (-x_c + max + log sum exp(x - max)) (loss.cpp:156-165).
+__global__ void softmaxlog_fwd_k(const float* __restrict__ x, const float* __restrict__ labels,
+                                 const float* __restrict__ weights, float* site_loss, int* flag,
+                                 int HW, int C, int N) {
+  const int64_t sites = (int64_t)HW * N;
+  const int lane = threadIdx.x % 32;
+  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
+       s += (int64_t)gridDim.x * blockDim.x / 32) {
+    int p = (int)(s % HW);
+    int64_t n = s / HW;
+    int c = read_label(labels, s, C, flag);
+    const float* xs = x + n * (int64_t)C * HW + p;
+    float mx = -INFINITY;
+    for (int k = lane; k < C; k += 32) mx = fmaxf(mx, xs[(int64_t)k * HW]);
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int k = lane; k < C; k += 32) sum += expf(xs[(int64_t)k * HW] - mx);
+    sum = warp_sumf(sum);
+    if (lane == 0) {
+      float l = 0.f;
+      if (c > 0) {
+        float wgt = weights ? weights[s] : 1.f;
+        l = wgt * (-xs[(int64_t)(c - 1) * HW] + mx + logf(sum));
+      }
+      site_loss[s] = l;
+    }
+  }
+}
+
+// Deterministic fixed-order sum of the per-site values (one block).
+__global__ void sum_sites_k(const float* __restrict__ v, int64_t n, float* out) {
+  __shared__ double red[32];
+  double a = 0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += v[i];
+  a = warp_sum(a);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int k = 0; k < (int)(blockDim.x / 32); ++k) t += red[k];
+    *out = (float)t;
+  }
+}
+
+template <bool kAcc>
+__global__ void softmaxlog_bwd_k(const float* __restrict__ x, const float* __restrict__ labels,
+                                 const float* __restrict__ weights, float pscale, float* dx,
+                                 int* flag, int HW, int C, int N) {
+  const int64_t sites = (int64_t)HW * N;
+  const int lane = threadIdx.x % 32;
+  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
+       s += (int64_t)gridDim.x * blockDim.x / 32) {
+    int p = (int)(s % HW);
+    int64_t n = s / HW;
+    int c = read_label(labels, s, C, flag);
+    const float* xs = x + n * (int64_t)C * HW + p;
+    float* ds = dx + n * (int64_t)C * HW + p;
+    if (c == 0) {  // ignored site: zero derivative (loss.cpp:252)
+      if (!kAcc)
+        for (int k = lane; k < C; k += 32) ds[(int64_t)k * HW] = 0.f;
+      continue;
+    }
+    float mx = -INFINITY;
+    for (int k = lane; k < C; k += 32) mx = fmaxf(mx, xs[(int64_t)k * HW]);
+    mx = warp_max(mx);
+    float sum = 0.f;
+    for (int k = lane; k < C; k += 32) sum += expf(xs[(int64_t)k * HW] - mx);
+    sum = warp_sumf(sum);
+    const float scale = pscale * (weights ? weights[s] : 1.f);
+    for (int k = lane; k < C; k += 32) {
+      float soft = expf(xs[(int64_t)k * HW] - mx) / sum;
+      float r = scale * (soft - (k == c - 1 ? 1.f : 0.f));
+      ds[(int64_t)k * HW] = kAcc ? ds[(int64_t)k * HW] + r : r;
+    }
+  }
+}
+
+// classerror (loss.cpp:111-141; first strict maximum wins) and topk
+// (loss.cpp:142-149; rank = #{k : x_k >= x_c}), weighted, per site.
+__global__ void metrics_k(const float* __restrict__ x, const float* __restrict__ labels,
+                          const float* __restrict__ weights, int top_k, float* site1,
+                          float* sitek, int* flag, int HW, int C, int N) {
+  const int64_t sites = (int64_t)HW * N;
+  const int lane = threadIdx.x % 32;
+  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
+       s += (int64_t)gridDim.x * blockDim.x / 32) {
+    int p = (int)(s % HW);
+    int64_t n = s / HW;
+    int c = read_label(labels, s, C, flag);
+    const float* xs = x + n * (int64_t)C * HW + p;
+    if (c == 0) {
+      if (lane == 0) site1[s] = sitek[s] = 0.f;
+      continue;
+    }
+    float xc = xs[(int64_t)(c - 1) * HW];
+    float bv = -INFINITY;
+    int best = 0x7fffffff;
+    int rank = 0;
+    for (int k = lane; k < C; k += 32) {
+      float v = xs[(int64_t)k * HW];
+      if (v > bv) {
+        bv = v;
+        best = k;
+      }
+      rank += (v >= xc);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int ob = __shfl_xor_sync(0xffffffffu, best, o);
+      if (ov > bv || (ov == bv && ob < best)) {
+        bv = ov;
+        best = ob;
+      }
+      rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    }
+    if (lane == 0) {
+      float wgt = weights ? weights[s] : 1.f;
+      site1[s] = best == c - 1 ? 0.f : wgt;
+      sitek[s] = rank <= top_k ? 0.f : wgt;
+    }
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ launchers ---
+
+void relu_forward(const float* x, float* y, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  count_launch();
+  if (n % 4 == 0 && aligned16(x) && aligned16(y))
+    relu_fwd_v4<<<blocks_for(n / 4, 256), 256, 0, s>>>((const float4*)x, (float4*)y, n / 4);
+  else
+    relu_fwd_s<<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
+}
+
+void relu_backward(const float* x, const float* dy, float* dx, int64_t n, int acc,
+                   cudaStream_t s) {
+  if (n == 0) return;
+  count_launch();
+  if (n % 4 == 0 && aligned16(x) && aligned16(dy) && aligned16(dx)) {
+    if (acc)
+      relu_bwd_v4<true><<<blocks_for(n / 4, 256), 256, 0, s>>>((const float4*)x,
+                                                               (const float4*)dy, (float4*)dx, n / 4);
+    else
+      relu_bwd_v4<false><<<blocks_for(n / 4, 256), 256, 0, s>>>((const float4*)x,
+                                                                (const float4*)dy, (float4*)dx, n / 4);
+  } else {
+    if (acc)
+      relu_bwd_s<true><<<blocks_for(n, 256), 256, 0, s>>>(x, dy, dx, n);
+    else
+      relu_bwd_s<false><<<blocks_for(n, 256), 256, 0, s>>>(x, dy, dx, n);
+  }
+}
+
+void axpy_inplace(float* y, const float* x, int64_t n, cudaStream_t s) {
+  if (n == 0) return;
+  count_launch();
+  axpy_k<<<blocks_for(n, 256), 256, 0, s>>>(y, x, n);
+}
+
+void sgd_step(float* w, float* v, const float* g, int64_t n, float lr, float mom, float wd,
+              cudaStream_t s) {
+  if (n == 0) return;
+  count_launch();
+  sgd_k<<<blocks_for(n, 256), 256, 0, s>>>(w, v, g, n, lr, mom, wd);
+}
+
+void pool_forward(const float* x, float* y, const PoolDims& d, cudaStream_t s) {
+  int64_t total = (int64_t)d.OH * d.OW * d.C * d.N;
+  if (total == 0) return;
+  count_launch();
+  pool_fwd_k<<<blocks_for(total, 256), 256, 0, s>>>(x, y, d);
+}
+
+void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d, int acc,
+                   cudaStream_t s) {
+  int64_t total = (int64_t)d.H * d.W * d.C * d.N;
+  if (total == 0) return;
+  count_launch();
+  if (acc)
+    pool_bwd_k<true><<<blocks_for(total, 256), 256, 0, s>>>(x, dy, dx, d);
+  else
+    pool_bwd_k<false><<<blocks_for(total, 256), 256, 0, s>>>(x, dy, dx, d);
+}
+
+static void lrn_smem_check(int C, int arrays) {
+  size_t bytes = (size_t)arrays * C * kLrnPix * sizeof(float);
+  static thread_local size_t configured = 0;
+  if (bytes > 48 * 1024 && bytes > configured) {
+    cudaFuncSetAttribute(lrn_fwd_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(lrn_bwd_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(lrn_bwd_k<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    configured = 227 * 1024;
+  }
+}
+
+void lrn_forward(const float* x, float* y, int H, int W, int C, int N, int size, float kappa,
+                 float alpha, float beta, cudaStream_t s) {
+  const int HW = H * W;
+  dim3 grid((HW + kLrnPix - 1) / kLrnPix, N);
+  size_t smem = (size_t)C * kLrnPix * sizeof(float);
+  lrn_smem_check(C, 1);
+  count_launch();
+  lrn_fwd_k<<<grid, 256, smem, s>>>(x, y, HW, C, size, kappa, alpha, -beta);
+}
+
+void lrn_backward(const float* x, const float* dy, float* dx, int H, int W, int C, int N, int size,
+                  float kappa, float alpha, float beta, int acc, cudaStream_t s) {
+  const int HW = H * W;
+  dim3 grid((HW + kLrnPix - 1) / kLrnPix, N);
+  size_t smem = (size_t)3 * C * kLrnPix * sizeof(float);
+  lrn_smem_check(C, 3);
+  count_launch();
+  if (acc)
+    lrn_bwd_k<true><<<grid, 256, smem, s>>>(x, dy, dx, HW, C, size, kappa, alpha, beta);
+  else
+    lrn_bwd_k<false><<<grid, 256, smem, s>>>(x, dy, dx, HW, C, size, kappa, alpha, beta);
+}
+
+int bnorm_splits(int HW, int C, int N) {
+  // Aim for ~4 blocks per SM overall.
+  int want = (kSMs * 4 + C - 1) / C;
+  if (want > N) want = N;
+  if (want < 1) want = 1;
+  (void)HW;
+  return want;
+}
+
+void bnorm_stats(const float* x, const float* dy, double* partial, double* out, int HW, int C,
+                 int N, int splits, cudaStream_t s) {
+  dim3 grid(C, splits);
+  count_launch(2);
+  if (dy)
+    bnorm_stats_k<true><<<grid, 256, 0, s>>>(x, dy, partial, HW, C, N, splits);
+  else
+    bnorm_stats_k<false><<<grid, 256, 0, s>>>(x, nullptr, partial, HW, C, N, splits);
+  bnorm_finish_k<<<(C + 127) / 128, 128, 0, s>>>(partial, out, C, splits);
+}
+
+void bnorm_apply(const float* x, const float* w, const float* b, const double* stats,
+                 const float* fixed_moments, float* y, float* moments_out, double eps, int HW,
+                 int C, int N, cudaStream_t s) {
+  int gy = (kSMs * 8 + C - 1) / C;
+  if (gy > N) gy = N;
+  if (gy < 1) gy = 1;
+  count_launch();
+  bnorm_apply_k<<<dim3(C, gy), 256, 0, s>>>(x, w, b, stats, fixed_moments, y, moments_out, eps,
+                                            HW, C, N);
+}
+
+void bnorm_backward_apply(const float* x, const float* dy, const float* w, const double* stats,
+                          double eps, float* dx, float* dw, float* db, int HW, int C, int N,
+                          int acc, cudaStream_t s) {
+  int gy = (kSMs * 8 + C - 1) / C;
+  if (gy > N) gy = N;
+  if (gy < 1) gy = 1;
+  count_launch();
+  if (acc)
+    bnorm_bwd_k<true><<<dim3(C, gy), 256, 0, s>>>(x, dy, w, stats, eps, dx, dw, db, HW, C, N, 1);
+  else
+    bnorm_bwd_k<false><<<dim3(C, gy), 256, 0, s>>>(x, dy, w, stats, eps, dx, dw, db, HW, C, N, 0);
+}
+
+void softmaxlog_forward(const float* x, const float* labels, const float* weights,
+                        float* site_loss, float* loss, int* flag, int HW, int C, int N,
+                        cudaStream_t s) {
+  int64_t sites = (int64_t)HW * N;
+  count_launch(2);
+  softmaxlog_fwd_k<<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, site_loss,
+                                                                flag, HW, C, N);
+  sum_sites_k<<<1, 1024, 0, s>>>(site_loss, sites, loss);
+}
+
+void softmaxlog_backward(const float* x, const float* labels, const float* weights, float p,
+                         float* dx, int* flag, int HW, int C, int N, int acc, cudaStream_t s) {
+  int64_t sites = (int64_t)HW * N;
+  count_launch();
+  if (acc)
+    softmaxlog_bwd_k<true><<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, p, dx,
+                                                                        flag, HW, C, N);
+  else
+    softmaxlog_bwd_k<false><<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, p,
+                                                                         dx, flag, HW, C, N);
+}
+
+void loss_metrics(const float* x, const float* labels, const float* weights, int top_k,
+                  float* site_buf, float* top1, float* topk, int* flag, int HW, int C, int N,
+                  cudaStream_t s) {
+  int64_t sites = (int64_t)HW * N;
+  count_launch(3);
+  metrics_k<<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, top_k, site_buf,
+                                                         site_buf + sites, flag, HW, C, N);
+  sum_sites_k<<<1, 1024, 0, s>>>(site_buf, sites, top1);
+  sum_sites_k<<<1, 1024, 0, s>>>(site_buf + sites, sites, topk);
+}
+
+}  // namespace ck

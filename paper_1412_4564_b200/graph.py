@@ -1,0 +1,153 @@
+"""Host mirror of the reference DAG API (graph.hpp:93-190) over the device
+engine in libck.so (engine.cu).
+
+``Graph`` keeps the reference's vocabulary -- add_input / add_param /
+add_layer(kind, name, inputs, outputs, hyper) / finalize / forward /
+backward -- and the device engine keeps every value and derivative resident
+in HBM.  Tensors cross the boundary only through ``set`` / ``get`` copies.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ck_shape, ck_tensor, lib, raise_for
+from .blocks import MATH, handle
+
+
+class Graph:
+    def __init__(self, math: str = "tf32", device: int | None = None):
+        self.hd = handle(device)
+        g = C.c_void_p()
+        raise_for(lib().ck_graph_create(self.hd.h, C.byref(g)), self.hd.h)
+        self.g = g
+        self.math = math
+        self.shapes = {}
+        self.params = []
+        self.inputs = []
+
+    def __del__(self):
+        if getattr(self, "g", None) and _lib._lib is not None:
+            _lib._lib.ck_graph_destroy(self.g)
+            self.g = None
+
+    def _check(self, code):
+        raise_for(code, self.hd.h)
+
+    # -- construction (graph.hpp:96-102) --
+    def add_input(self, name, shape):
+        self._check(lib().ck_graph_add_input(self.g, name.encode(), ck_shape(*shape)))
+        self.shapes[name] = tuple(shape)
+        self.inputs.append(name)
+
+    def add_param(self, name, shape):
+        self._check(lib().ck_graph_add_param(self.g, name.encode(), ck_shape(*shape)))
+        self.shapes[name] = tuple(shape)
+        self.params.append(name)
+
+    def add_layer(self, kind, name, inputs, outputs, params=()):
+        p = (C.c_double * max(1, len(params)))(*[float(v) for v in params])
+        self._check(lib().ck_graph_add_layer(self.g, kind.encode(), name.encode(),
+                                             ",".join(inputs).encode(), ",".join(outputs).encode(),
+                                             p, len(params)))
+
+    def finalize(self):
+        self._check(lib().ck_graph_finalize(self.g, MATH[self.math]))
+
+    # -- tensors --
+    def view(self, name, deriv=False) -> ck_tensor:
+        t = ck_tensor()
+        self._check(lib().ck_graph_var(self.g, name.encode(), int(deriv), C.byref(t)))
+        return t
+
+    def shape(self, name):
+        s = self.view(name).shape
+        return (s.h, s.w, s.c, s.n)
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def set(self, name, data):
+        """Copy host (numpy) or device (torch) data into a variable."""
+        t = self.view(name)
+        n = t.shape.h * t.shape.w * t.shape.c * t.shape.n
+        if isinstance(data, torch.Tensor):
+            src = data.contiguous().float()
+            assert src.numel() == n, (name, src.numel(), n)
+            self._check(lib().ck_memcpy(self.hd.h, t.data, src.data_ptr(), 4 * n, self._stream()))
+            torch.cuda.current_stream().synchronize()
+        else:
+            arr = np.ascontiguousarray(data, dtype=np.float32)
+            assert arr.size == n, (name, arr.size, n)
+            self._check(lib().ck_memcpy(self.hd.h, t.data, arr.ctypes.data, 4 * n, self._stream()))
+            torch.cuda.current_stream().synchronize()
+
+    def get(self, name, deriv=False) -> np.ndarray:
+        t = self.view(name, deriv)
+        n = t.shape.h * t.shape.w * t.shape.c * t.shape.n
+        out = np.empty(n, np.float32)
+        self._check(lib().ck_memcpy(self.hd.h, out.ctypes.data, t.data, 4 * n, self._stream()))
+        torch.cuda.current_stream().synchronize()
+        return out
+
+    # -- evaluation (graph.cpp:494, :548) --
+    def forward(self):
+        self._check(lib().ck_graph_forward(self.g, self._stream()))
+
+    def backward(self, objective="objective"):
+        self._check(lib().ck_graph_backward(self.g, objective.encode(), self._stream()))
+
+    @property
+    def last_launches(self) -> int:
+        return lib().ck_graph_last_launches(self.g)
+
+    def set_profiling(self, on: bool):
+        self._check(lib().ck_graph_set_profiling(self.g, int(on)))
+
+    def layer_times(self):
+        """[(layer, fwd_ms, bwd_ms)] of the last profiled evaluation."""
+        torch.cuda.synchronize()
+        out = []
+        for i in range(lib().ck_graph_layer_count(self.g)):
+            f, b = C.c_float(), C.c_float()
+            self._check(lib().ck_graph_layer_ms(self.g, i, C.byref(f), C.byref(b)))
+            out.append((lib().ck_graph_layer_name(self.g, i).decode(), f.value, b.value))
+        return out
+
+
+class Trainer:
+    """cnn_train's SGD step with optional NCCL data parallelism."""
+
+    def __init__(self, graph: Graph, objective="objective", lr=0.01, momentum=0.9,
+                 weight_decay=5e-4):
+        self.graph = graph
+        t = C.c_void_p()
+        graph._check(lib().ck_trainer_create(graph.g, objective.encode(), lr, momentum,
+                                             weight_decay, C.byref(t)))
+        self.t = t
+
+    def __del__(self):
+        if getattr(self, "t", None) and _lib._lib is not None:
+            _lib._lib.ck_trainer_destroy(self.t)
+            self.t = None
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        raise_for(lib().ck_nccl_unique_id(buf), None)
+        return buf.raw
+
+    def init_dp(self, uid: bytes, rank: int, world: int):
+        self.graph._check(lib().ck_trainer_init_dp(self.t, uid, rank, world))
+
+    def step(self, want_loss=True, stream=None):
+        s = C.c_void_p(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
+        if want_loss:
+            v = C.c_float()
+            self.graph._check(lib().ck_trainer_step(self.t, C.byref(v), s))
+            return v.value
+        self.graph._check(lib().ck_trainer_step(self.t, None, s))
+        return None

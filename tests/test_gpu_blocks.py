@@ -1,0 +1,234 @@
+"""Per-block parity of the CUDA kernels (through the C ABI) against the CPU
+oracle on identical seeded inputs.
+
+Tolerances (north star): pooling and ReLU bit-exact; FP32 (CK_MATH_FP32)
+outputs and derivatives within 1e-4 relative; TF32 (CK_MATH_TF32) within a
+stated 1e-2.  Relative error uses the floored denominator of fd_rel_err
+(graph.cpp:685-689): |a-b| / max(|a|+|b|, 1e-2 * rms(ref)).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+B = None
+
+
+@pytest.fixture(scope="module", autouse=True)
+def blocks():
+    global B
+    assert torch.cuda.is_available()
+    from paper_1412_4564_b200 import blocks as _B
+    B = _B
+    yield
+
+
+def dev(a, shape):
+    return B.as_hwcn(torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda(), shape)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy().ravel()
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    floor = 1e-2 * np.sqrt(np.mean(b * b)) + 1e-30
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(a) + np.abs(b), floor)))
+
+
+TOL = {"fp32": 1e-4, "tf32": 1e-2}
+
+CONV_CASES = [
+    ((7, 6, 4, 3), (3, 2, 2, 6), (2, 1, 0, 1, 1, 0, 2)),
+    ((9, 9, 3, 2), (3, 3, 3, 4), (1, 1, 1, 1, 1, 1, 1)),
+    ((11, 10, 2, 2), (5, 4, 2, 3), (3, 2, 2, 0, 1, 3, 1)),
+    ((8, 8, 6, 2), (1, 1, 2, 6), (1, 1, 0, 0, 0, 0, 3)),
+    ((5, 5, 2, 1), (3, 3, 2, 3), (2, 2, 0, 1, 0, 1, 1)),
+    # AlexNet layer shapes at batch 2
+    ((227, 227, 3, 2), (11, 11, 3, 96), (4, 4, 0, 0, 0, 0, 1)),
+    ((27, 27, 96, 2), (5, 5, 48, 256), (1, 1, 2, 2, 2, 2, 2)),
+    ((13, 13, 256, 2), (3, 3, 256, 384), (1, 1, 1, 1, 1, 1, 1)),
+    ((13, 13, 384, 2), (3, 3, 192, 384), (1, 1, 1, 1, 1, 1, 2)),
+    ((13, 13, 384, 2), (3, 3, 192, 256), (1, 1, 1, 1, 1, 1, 2)),
+    ((6, 6, 256, 4), (6, 6, 256, 512), (1, 1, 0, 0, 0, 0, 1)),
+    ((1, 1, 512, 4), (1, 1, 512, 100), (1, 1, 0, 0, 0, 0, 1)),
+]
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("xs,fs,g", CONV_CASES)
+def test_conv(xs, fs, g, math):
+    r = O.Rng(sum(xs) + sum(fs))
+    x = r.uniform(O.size(xs))
+    f = r.uniform(O.size(fs), -0.1, 0.1)
+    b = r.uniform(fs[3])
+    geom = B.ConvGeom(*g)
+    y_ref, ys = O.conv_forward(x, xs, f, fs, b, g)
+    y = B.conv_forward(dev(x, xs), dev(f, fs), torch.from_numpy(b).cuda(), geom, math=math)
+    assert B.hwcn_shape(y) == ys
+    assert rel(host(y), y_ref) < TOL[math]
+    dy = r.uniform(O.size(ys))
+    dx_ref, df_ref, db_ref = O.conv_backward(x, xs, f, fs, g, dy)
+    dx, df, db = B.conv_backward(dev(x, xs), dev(f, fs), geom, dev(dy, ys), math=math)
+    assert rel(host(dx), dx_ref) < TOL[math]
+    assert rel(host(df), df_ref) < TOL[math]
+    assert rel(host(db), db_ref) < TOL["fp32"]
+
+
+def test_conv_accumulate_and_skip():
+    r = O.Rng(31)
+    xs, fs, g = (9, 8, 4, 2), (3, 3, 2, 6), (1, 1, 1, 1, 1, 1, 2)
+    x, f = r.uniform(O.size(xs)), r.uniform(O.size(fs))
+    _, ys = O.conv_forward(x, xs, f, fs, None, g)
+    dy = r.uniform(O.size(ys))
+    dx_ref, df_ref, _ = O.conv_backward(x, xs, f, fs, g, dy)
+    base_dx, base_df = r.uniform(O.size(xs)), r.uniform(O.size(fs))
+    dx, df = dev(base_dx, xs), dev(base_df, fs)
+    B.conv_backward(dev(x, xs), dev(f, fs), B.ConvGeom(*g), dev(dy, ys), math="fp32",
+                    out=(dx, df, None), accumulate=True)
+    assert rel(host(dx), dx_ref + base_dx) < 1e-4
+    assert rel(host(df), df_ref + base_df) < 1e-4
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+def test_convt(math):
+    r = O.Rng(32)
+    xs, fs, cg = (5, 4, 6, 2), (3, 2, 6, 4), (2, 1, 1, 0, 0, 1)
+    x, f = r.uniform(O.size(xs)), r.uniform(O.size(fs))
+    y_ref, ys = O.convt_forward(x, xs, f, fs, cg)
+    geom = B.ConvTransposeGeom(*cg)
+    y = B.convt_forward(dev(x, xs), dev(f, fs), geom, math=math)
+    assert rel(host(y), y_ref) < TOL[math]
+    dy = r.uniform(O.size(ys))
+    dx_ref, df_ref = O.convt_backward(x, xs, f, fs, cg, dy)
+    dx, df = B.convt_backward(dev(x, xs), dev(f, fs), geom, dev(dy, ys), math=math)
+    assert rel(host(dx), dx_ref) < TOL[math]
+    assert rel(host(df), df_ref) < TOL[math]
+
+
+def test_conv_shape_errors():
+    x = B.from_hwcn((5, 5, 4, 1))
+    with pytest.raises(B.ShapeError, match="do not match input channels"):
+        B.conv_forward(x, B.from_hwcn((3, 3, 3, 6)), None, B.ConvGeom())
+    with pytest.raises(B.ShapeError, match="not divisible by groups"):
+        B.conv_forward(x, B.from_hwcn((3, 3, 2, 5)), None, B.ConvGeom(groups=2))
+    with pytest.raises(B.ShapeError, match="larger than padded input"):
+        B.conv_forward(x, B.from_hwcn((7, 3, 4, 2)), None, B.ConvGeom())
+    with pytest.raises(B.ShapeError, match="bias has"):
+        B.conv_forward(x, B.from_hwcn((3, 3, 4, 2)), torch.zeros(3, device="cuda"), B.ConvGeom())
+
+
+POOLS = [(3, 3, 2, 2, 0, 1, 0, 1, 0), (3, 3, 2, 2, 0, 1, 0, 1, 1), (2, 2, 2, 2, 0, 0, 0, 0, 0),
+         (3, 2, 1, 2, 2, 1, 1, 0, 1), (4, 4, 3, 3, 3, 0, 0, 3, 0)]
+
+
+@pytest.mark.parametrize("pg", POOLS)
+@pytest.mark.parametrize("xs", [(13, 11, 3, 2), (55, 55, 8, 2), (1, 1, 2, 1)])
+def test_pool_bitexact(xs, pg):
+    try:
+        _, ys = O.pool_forward(np.zeros(O.size(xs)), xs, pg)
+    except O.OracleError:
+        with pytest.raises(B.ShapeError):
+            B.pool_forward(B.from_hwcn(xs, fill=0.0), B.PoolGeom(*pg[:8], mode="max" if pg[8] == 0 else "avg"))
+        return
+    r = O.Rng(33)
+    x = r.uniform(O.size(xs))
+    x[::5] = x[2::5][: len(x[::5])]  # ties
+    geom = B.PoolGeom(*pg[:8], mode="max" if pg[8] == 0 else "avg")
+    y_ref, ys = O.pool_forward(x, xs, pg)
+    y = B.pool_forward(dev(x, xs), geom)
+    assert np.array_equal(host(y), y_ref)
+    dy = r.uniform(O.size(ys))
+    dx = B.pool_backward(dev(x, xs), geom, dev(dy, ys))
+    assert np.array_equal(host(dx), O.pool_backward(x, xs, pg, dy))
+
+
+def test_relu_bitexact():
+    r = O.Rng(34)
+    for n in (1000, 1001, 4096 * 7 + 3):
+        x = r.uniform(n)
+        x[::9] = 0
+        dy = r.uniform(n)
+        xs = (n, 1, 1, 1)
+        assert np.array_equal(host(B.relu_forward(dev(x, xs))), O.relu_forward(x))
+        assert np.array_equal(host(B.relu_backward(dev(x, xs), dev(dy, xs))), O.relu_backward(x, dy))
+
+
+@pytest.mark.parametrize("p", [(5, 1.0, 2e-5, 0.75), (3, 1.0, 5e-5 / 3, 0.75), (4, 2.0, 0.1, 0.5)])
+@pytest.mark.parametrize("xs", [(7, 5, 9, 2), (27, 27, 96, 1), (13, 13, 256, 1)])
+def test_lrn(xs, p):
+    r = O.Rng(35)
+    x, dy = r.uniform(O.size(xs)) * 3, r.uniform(O.size(xs))
+    lp = B.LrnParams(*p)
+    y = B.lrn_forward(dev(x, xs), lp)
+    assert rel(host(y), O.lrn_forward(x, xs, *p)) < 1e-5
+    dx = B.lrn_backward(dev(x, xs), lp, dev(dy, xs))
+    assert rel(host(dx), O.lrn_backward(x, xs, *p, dy)) < 1e-4
+
+
+@pytest.mark.parametrize("xs", [(6, 5, 4, 3), (28, 28, 64, 8), (1, 1, 7, 5)])
+def test_bnorm(xs):
+    r = O.Rng(36)
+    x, dy = r.uniform(O.size(xs)) * 2 + 0.5, r.uniform(O.size(xs))
+    w, b = r.uniform(xs[2]), r.uniform(xs[2])
+    wt, bt = torch.from_numpy(w).cuda(), torch.from_numpy(b).cuda()
+    y_ref, m_ref, v_ref = O.bnorm_forward(x, xs, w, b, 1e-5)
+    y, mom = B.bnorm_forward(dev(x, xs), wt, bt, 1e-5)
+    assert rel(host(y), y_ref) < 1e-4
+    assert rel(host(mom), np.concatenate([m_ref, v_ref])) < 1e-5
+    yi = B.bnorm_infer(dev(x, xs), wt, bt, 1e-5, mom)
+    assert rel(host(yi), y_ref) < 1e-4
+    dx_ref, dw_ref, db_ref = O.bnorm_backward(x, xs, w, b, 1e-5, dy)
+    dx, dw, db = B.bnorm_backward(dev(x, xs), wt, bt, 1e-5, dev(dy, xs))
+    assert rel(host(dx), dx_ref) < 1e-4
+    assert rel(host(dw), dw_ref) < 1e-4
+    assert rel(host(db), db_ref) < 1e-4
+
+
+def test_softmaxlog():
+    r = O.Rng(37)
+    for xs in [(1, 1, 1000, 64), (2, 3, 17, 4), (1, 1, 10, 100)]:
+        cs = (xs[0], xs[1], 1, xs[3])
+        x = r.uniform(O.size(xs)) * 4
+        c = r.labels(O.size(cs), xs[2])
+        c[1] = 0
+        w = r.uniform(O.size(cs), 0, 2)
+        for wts in (None, w):
+            l_ref = O.loss_forward(x, xs, c, cs, wts)
+            l = B.loss_forward(dev(x, xs), dev(c, cs), None if wts is None else dev(wts, cs))
+            assert abs(host(l)[0] - l_ref) < 1e-5 * max(1.0, abs(l_ref))
+            dx = B.loss_backward(dev(x, xs), dev(c, cs), None if wts is None else dev(wts, cs), 0.5)
+            assert rel(host(dx), O.softmaxlog_backward(x, xs, c, cs, wts, 0.5)) < 1e-5
+        m = host(B.loss_metrics(dev(x, xs), dev(c, cs), None, 5))
+        assert m[0] == O.loss_forward(x, xs, c, cs, None, "classerror")
+        assert m[1] == O.loss_forward(x, xs, c, cs, None, "topk", 5)
+    # stability at +-1000
+    xs, cs = (1, 1, 2, 1), (1, 1, 1, 1)
+    l = host(B.loss_forward(dev([1000, -1000], xs), dev([2], cs)))[0]
+    assert np.isfinite(l) and abs(l - 2000) < 1e-2
+
+
+def test_label_errors():
+    xs, cs = (1, 1, 3, 1), (1, 1, 1, 1)
+    with pytest.raises(B.DataError, match="not an integer"):
+        B.loss_forward(dev([0, 0, 0], xs), dev([1.5], cs))
+    with pytest.raises(B.DataError, match="out of range"):
+        B.loss_forward(dev([0, 0, 0], xs), dev([4], cs))
+    with pytest.raises(B.ShapeError, match="classification labels"):
+        B.loss_forward(dev([0, 0, 0], xs), dev([1, 1], (1, 1, 1, 2)))
+
+
+def test_sgd_bitexact():
+    r = O.Rng(38)
+    n = 10007
+    w, v, g = r.uniform(n), r.uniform(n), r.uniform(n)
+    wt, vt, gt = (torch.from_numpy(a.copy()).cuda() for a in (w, v, g))
+    B.sgd_step(wt, vt, gt, 0.01, 0.9, 5e-4)
+    w_ref, v_ref = O.sgd_step(w, v, g, 0.01, 0.9, 5e-4)
+    assert np.array_equal(host(vt), v_ref)
+    assert np.array_equal(host(wt), w_ref)

@@ -1,0 +1,98 @@
+"""Whole-network parity: the device DAG engine (engine.cu) vs the oracle
+chain (oracle/chain.py, the reference DAG semantics of graph.cpp:494-598)
+on the BASELINE.json networks at small batch, plus size-independent
+properties at the full AlexNet batch."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    floor = 1e-2 * np.sqrt(np.mean(b * b)) + 1e-30
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(a) + np.abs(b), floor)))
+
+
+def device_graph(net, math):
+    from paper_1412_4564_b200.graph import Graph
+    g = Graph(math=math)
+    net.build(g)
+    g.finalize()
+    return g
+
+
+@pytest.mark.parametrize("math", ["fp32", "tf32"])
+@pytest.mark.parametrize("name,batch,kw", [("lenet", 4, {}), ("cifar", 4, {}), ("alexnet", 2, {}),
+                                           ("vgg16bn", 2, {"image": 32})])
+def test_network_fwd_bwd(name, batch, kw, math):
+    import chain
+    from paper_1412_4564_b200 import nets
+    net = nets.NETS[name](batch=batch, **kw)
+    params, inputs = net.init_params(), net.init_inputs()
+    if name == "vgg16bn":  # make the deep net's logits non-degenerate
+        params = {k: (v * 20 if k.endswith("f") else v) for k, v in params.items()}
+    vals, derivs = chain.run(net, params, inputs)
+    g = device_graph(net, math)
+    for k, v in {**params, **inputs}.items():
+        g.set(k, v)
+    g.forward()
+    g.backward("objective")
+    loss = g.get("objective")[0]
+    tol = 1e-4 if math == "fp32" else 1e-2
+    assert abs(loss - vals["objective"][0]) <= tol * abs(vals["objective"][0])
+    for pname, _, _ in net.params:
+        assert rel(g.get(pname, deriv=True), derivs[pname]) < (2e-3 if math == "fp32" else 5e-2), pname
+    assert rel(g.get("data", deriv=True), derivs["data"]) < (2e-3 if math == "fp32" else 5e-2)
+    assert g.last_launches > 0
+
+
+def test_trainer_step_matches_oracle_sgd():
+    import chain
+    from paper_1412_4564_b200 import nets
+    from paper_1412_4564_b200.graph import Trainer
+    net = nets.lenet(batch=8)
+    params, inputs = net.init_params(), net.init_inputs()
+    vals, derivs = chain.run(net, params, inputs)
+    g = device_graph(net, "fp32")
+    for k, v in {**params, **inputs}.items():
+        g.set(k, v)
+    t = Trainer(g, lr=0.01, momentum=0.9, weight_decay=5e-4)
+    loss = t.step()
+    assert abs(loss - vals["objective"][0]) < 1e-4 * vals["objective"][0]
+    for pname, _, _ in net.params:
+        w_ref, _ = O.sgd_step(params[pname], np.zeros_like(params[pname]),
+                              derivs[pname].astype(np.float32), 0.01, 0.9, 5e-4)
+        assert rel(g.get(pname), w_ref) < 1e-4, pname
+    # a few steps reduce the loss on a fixed batch
+    for _ in range(5):
+        last = t.step()
+    assert last < loss
+
+
+def test_alexnet_full_batch_properties():
+    """Full BASELINE size (b=256): properties the oracle need not run."""
+    from paper_1412_4564_b200 import nets
+    net = nets.alexnet(batch=256)
+    g = device_graph(net, "tf32")
+    for k, v in {**net.init_params(), **net.init_inputs()}.items():
+        g.set(k, v)
+    g.forward()
+    g.backward("objective")
+    loss = g.get("objective")[0]
+    # random init: logits ~0 -> loss ~ 256 ln 1000
+    assert abs(loss - 256 * np.log(1000)) < 0.01 * 256 * np.log(1000)
+    # softmaxlog derivative sums to zero per image (loss.cpp:263-275)
+    d8 = g.get("f8", deriv=True).reshape(256, 1000)
+    assert np.abs(d8.sum(axis=1)).max() < 1e-4
+    # max-pool backward conserves mass: sum dx = sum dy
+    assert abs(g.get("r5", deriv=True).sum(dtype=np.float64) -
+               g.get("p5", deriv=True).sum(dtype=np.float64)) < 1e-3 * (
+                   np.abs(g.get("p5", deriv=True)).sum() + 1e-12)
+    # relu backward is a mask of its input's sign
+    r6, c6 = g.get("r6", deriv=True), g.get("f6")
+    assert np.all(g.get("f6", deriv=True)[c6 <= 0] == 0)
+    assert np.isfinite(g.get("conv1f", deriv=True)).all()
