@@ -119,7 +119,7 @@ class Handle:
         self.device = device
 
     def __del__(self):
-        if getattr(self, "h", None) and _lib._lib is not None:
+        if getattr(self, "h", None) and _lib is not None and _lib._lib is not None:
             _lib._lib.ck_destroy(self.h)
             self.h = None
 

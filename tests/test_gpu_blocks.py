@@ -36,9 +36,15 @@ def host(t):
 
 
 def rel(a, b):
+    """Per-element relative error with the denominator floored at 1% of the
+    tensor's scale (fd_rel_err's floor, graph.cpp:685-689, made scale-aware):
+    near-zero outputs produced by cancellation are judged against the
+    tensor's magnitude, not their own.  Also bounds the normwise error."""
     a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
-    floor = 1e-2 * np.sqrt(np.mean(b * b)) + 1e-30
-    return float(np.max(np.abs(a - b) / np.maximum(np.abs(a) + np.abs(b), floor)))
+    floor = 1e-2 * np.max(np.abs(b)) + 1e-30
+    elem = float(np.max(np.abs(a - b) / np.maximum(np.abs(a) + np.abs(b), floor)))
+    norm = float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
+    return max(elem, 10 * norm)
 
 
 TOL = {"fp32": 1e-4, "tf32": 1e-2}
@@ -138,7 +144,8 @@ def test_pool_bitexact(xs, pg):
         return
     r = O.Rng(33)
     x = r.uniform(O.size(xs))
-    x[::5] = x[2::5][: len(x[::5])]  # ties
+    if x.size > 20:
+        x[::5] = x[2::5][: len(x[::5])]  # ties
     geom = B.PoolGeom(*pg[:8], mode="max" if pg[8] == 0 else "avg")
     y_ref, ys = O.pool_forward(x, xs, pg)
     y = B.pool_forward(dev(x, xs), geom)
