@@ -12,6 +12,7 @@
 // shared memory with register double buffering.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "ck_internal.hpp"
@@ -189,6 +190,35 @@ struct WgradProb {
   }
 };
 
+// Fully-connected dgrad (H'' = W'' = 1, no padding): dX[q, n] = sum_k F[q, k] dY[k, n],
+// a plain GEMM instead of the 1-valid-tap-in-H*W gather of DgradProb.
+struct FcDgradProb {
+  const float* dy;
+  const float* f;
+  float* dx;
+  ConvDims d;
+  __device__ int64_t Q() const { return (int64_t)d.H * d.W * d.C; }
+  __device__ int64_t M() const { return Q(); }
+  __device__ int64_t N() const { return d.N; }
+  __device__ int64_t K() const { return d.K; }
+  struct RowCtx {
+    int64_t q;
+    bool valid;
+  };
+  __device__ RowCtx row(int64_t m, int) const { return RowCtx{m, m < M()}; }
+  __device__ float a(const RowCtx& r, int64_t k) const {
+    return (r.valid && k < K()) ? f[r.q + Q() * k] : 0.f;
+  }
+  __device__ float b(int64_t k, int64_t n, int) const {
+    return (k < K() && n < N()) ? dy[k + (int64_t)d.K * n] : 0.f;
+  }
+  __device__ void store(int64_t m, int64_t n, int, float v, int acc) const {
+    if (m >= M() || n >= N()) return;
+    float* dst = dx + m + Q() * n;
+    *dst = acc ? __fadd_rn(*dst, v) : v;
+  }
+};
+
 // ---- the tiled kernel ------------------------------------------------------------
 
 template <class P, bool kSplit>
@@ -305,6 +335,45 @@ __global__ void bgrad_k(const float* __restrict__ dy, float* db, int OHW, int K,
   }
 }
 
+// Strided dgrad in gather form with the stride-phase decomposition: for dx
+// pixel i only taps fi = (i + pt) mod s (+ s, + 2s, ...) hit an output row, so
+// each thread visits ceil(fh/s) x ceil(fw/s) taps instead of fh x fw.  One
+// thread per dx element, consecutive threads along H.
+template <bool kAcc>
+__global__ void dgrad_strided_k(const float* __restrict__ dy, const float* __restrict__ f,
+                                float* dx, ConvDims d) {
+  const int64_t total = (int64_t)d.H * d.W * d.C * d.N;
+  const int Kg = d.Kg();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % d.H);
+    int64_t r = e / d.H;
+    const int j = (int)(r % d.W);
+    r /= d.W;
+    const int c = (int)(r % d.C);
+    const int n = (int)(r / d.C);
+    const int g = c / d.Cg, cl = c - g * d.Cg;
+    const int ri = (i + d.pt) % d.sh, rj = (j + d.pl) % d.sw;
+    float acc = 0.f;
+    for (int fj = rj; fj < d.fw; fj += d.sw) {
+      const int oj = (j + d.pl - fj) / d.sw;
+      if (j + d.pl - fj < 0 || oj >= d.OW) continue;
+      for (int fi = ri; fi < d.fh; fi += d.sh) {
+        const int oi = (i + d.pt - fi) / d.sh;
+        if (i + d.pt - fi < 0 || oi >= d.OH) continue;
+        const float* yp = dy + ((int64_t)n * d.K + (int64_t)g * Kg) * d.OH * d.OW + oi +
+                          (int64_t)d.OH * oj;
+        const float* fp = f + fi + (int64_t)d.fh * (fj + (int64_t)d.fw * (cl * d.fsc));
+        const int64_t fstep = (int64_t)d.fh * d.fw * d.fsk;
+        const float* fpk = fp + (int64_t)g * Kg * (int64_t)d.fh * d.fw * d.fsk;
+        for (int k = 0; k < Kg; ++k)
+          acc = fmaf(yp[(int64_t)k * d.OH * d.OW], fpk[k * fstep], acc);
+      }
+    }
+    dx[e] = kAcc ? __fadd_rn(dx[e], acc) : acc;
+  }
+}
+
 int wgrad_splits(const ConvDims& d) {
   int64_t rows = (int64_t)d.fh * d.fw * d.Cg, cols = d.Kg();
   int64_t tiles = ((rows + BM - 1) / BM) * ((cols + BN - 1) / BN) * d.groups;
@@ -330,6 +399,26 @@ void conv_fwd_fp32(const float* x, const float* f, const float* bias, float* y,
 
 void conv_dgrad_fp32(const float* dy, const float* f, float* dx, const ConvDims& d, int acc,
                      cudaStream_t s) {
+  const bool fc = d.OH == 1 && d.OW == 1 && d.fh == d.H && d.fw == d.W && d.pt == 0 &&
+                  d.pl == 0 && d.groups == 1 && d.fsc == 1;
+  if (fc) {
+    FcDgradProb p{dy, f, dx, d};
+    int64_t Q = (int64_t)d.H * d.W * d.C;
+    dim3 grid((unsigned)((Q + BM - 1) / BM), (unsigned)((d.N + BN - 1) / BN), 1);
+    count_launch();
+    simt_gemm_k<FcDgradProb, false><<<grid, NT, 0, s>>>(p, 1, acc);
+    return;
+  }
+  if (d.sh > 1 || d.sw > 1) {
+    int64_t total = (int64_t)d.H * d.W * d.C * d.N;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    count_launch();
+    if (acc)
+      dgrad_strided_k<true><<<blocks, 256, 0, s>>>(dy, f, dx, d);
+    else
+      dgrad_strided_k<false><<<blocks, 256, 0, s>>>(dy, f, dx, d);
+    return;
+  }
   DgradProb p{dy, f, dx, d};
   int64_t M = (int64_t)d.N * d.H * d.W;
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((d.Cg + BN - 1) / BN), d.groups);

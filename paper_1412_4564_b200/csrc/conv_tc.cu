@@ -1,14 +1,849 @@
-// conv_tc.cu -- tcgen05 / TMEM / TMA TF32 convolution kernels (sm_100a).
-// (placeholder until the tensor-core path lands: every entry declines.)
+// conv_tc.cu -- the CK_MATH_TF32 convolution path: tcgen05 tensor cores with
+// TMEM accumulators, operands staged by TMA (sm_100a).
+//
+// One warp-specialised GEMM kernel,  C[m, n] = sum_k A[m, k] B[n, k],  serves
+// every pass of conv.cpp:193-280:
+//
+//   pass            A (rows m)                  B (rows n)               K
+//   conv fprop      im2col(x) pixels  [TMA im2col, K-major]  filters [tiled]  (tap, c)
+//   conv dgrad      im2col(dy) pixels [TMA im2col, K-major]  flipped filters  (tap, k)
+//   conv wgrad      dy^T filters      [tiled, MN-major]      im2col(x) [TMA im2col, MN-major]  pixels
+//   fc fprop        filters [tiled K] images x [tiled K]                      q = (i, j, c)
+//   fc dgrad        filters [tiled MN] dy [tiled K]                           k
+//   fc wgrad        x [tiled MN]       dy [tiled MN]                          images
+//
+// The reference layout HWCN has odd spatial pitches (27, 13, ...) that TMA
+// cannot address (global strides must be multiples of 16 bytes), so conv
+// operands go through a "pixel-major" layout -- [n][w][h][c], channels
+// innermost, padded per group to a multiple of 32 -- produced by a transpose
+// kernel; TMA's im2col mode then walks output pixels across image boundaries
+// with zero-fill for the padding, which is the reference's im2row
+// (conv.cpp:35-59) done by the copy engine with no buffer.  FC layers (the
+// H''=W''=1 special case) need no transform at all.
+//
+// Pipeline (per CTA, one 128 x BN output tile):
+//   warp 0     : TMA producer, STAGES-deep ring of (A 16 KB, B BN*128 B) stages
+//   warp 1     : TMEM allocator + single-thread tcgen05.mma.kind::tf32 issuer
+//   warps 2..5 : epilogue, tcgen05.ld 32x32b -> registers -> global
+// Operand tiles are 128-byte swizzled (SWIZZLE_128B) in both K-major and
+// MN-major forms; K per stage = 32 fp32, 4 MMAs of K = 8.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
 #include "ck_handle.hpp"
+#include "ck_internal.hpp"
 
 namespace ck {
-bool conv_tc_available() { return false; }
-bool conv_tc_forward(ck_handle*, const float*, const float*, const float*, float*,
-                     const ConvDims&, int, cudaStream_t) { return false; }
-bool conv_tc_dgrad(ck_handle*, const float*, const float*, float*, const ConvDims&, int,
-                   cudaStream_t) { return false; }
-bool conv_tc_wgrad(ck_handle*, const float*, const float*, float*, const ConvDims&, int,
-                   cudaStream_t) { return false; }
-void conv_tc_release(ck_handle*) {}
+
+// ============================================================================
+//                               device helpers
+// ============================================================================
+namespace tc {
+
+enum OpKind : int {
+  OP_TILED_K = 0,     // 2D tensor (K inner, MN outer), box (32, rows)
+  OP_TILED_MN = 1,    // 2D tensor (MN inner, K outer), boxes (32, 32) x rows/32
+  OP_IM2COL_K = 2,    // 4D im2col over a pixel-major tensor, box 128 px x 32 ch
+  OP_IM2COL_MN = 3,   // 4D im2col, boxes 32 px x 32 ch, one per 32 rows of n
+};
+
+enum EpiKind : int {
+  EPI_PIX = 0,     // row m = output pixel (n, ow, oh) of an HWCN tensor, col = channel
+  EPI_LINEAR = 1,  // addr = row + col * ld
+};
+
+struct GemmParams {
+  int M, N, K;            // problem (per group), K in elements (multiple of 32)
+  int BN;                 // tile N (multiple of 16, <= 256)
+  int stages;
+  int splits;             // split-K factor (grid.z = groups * splits)
+  // im2col geometry (for OP_IM2COL_*): output pixel decode and origin
+  int OH, OW;             // output spatial extent walked by the TMA
+  int sh, sw, pt, pl;     // traversal stride and pad (start = o*s - p)
+  int fh;                 // taps are t = fi + fh * fj
+  int cchunks;            // channel chunks of 32 per tap (Cgp / 32)
+  int a_grp_c, b_grp_c;   // per-group channel offset of the im2col tensor (Cgp / Kgp)
+  int a_grp_mn, b_grp_mn; // per-group offset along MN for tiled operands
+  int a_grp_k, b_grp_k;   // per-group offset along K for tiled operands
+  // epilogue
+  int epi;
+  float* out;
+  int64_t ld;             // EPI_LINEAR: column stride; EPI_PIX: OH*OW
+  int64_t img_stride;     // EPI_PIX: K_total * OH * OW
+  int64_t grp_col;        // column offset per group (EPI_PIX channel / EPI_LINEAR col)
+  int64_t grp_out;        // element offset per group (EPI_LINEAR)
+  int64_t split_stride;   // elements between split partials (splits > 1)
+  int epi_OHW;            // EPI_PIX: pixels per image of the output
+  const float* bias;      // per col (EPI_PIX) or per row (EPI_LINEAR)
+  int relu, acc;
+  int n_valid;            // columns < n_valid are stored
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_im2col_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                              int c, int h, int w, int n, uint16_t oh,
+                                              uint16_t ow) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c), "r"(h), "r"(w), "r"(n), "h"(oh), "h"(ow)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor (sm_100 "version 1"), SWIZZLE_128B = 2.
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, M = 128.
+__device__ __forceinline__ uint32_t idesc_tf32(int n, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+#define CK_LD32(r, taddr)                                                                   \
+  asm volatile(                                                                             \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "                                             \
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22," \
+      "%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                                        \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),          \
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),       \
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),       \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),       \
+        "=r"(r[31])                                                                         \
+      : "r"(taddr));
+
+constexpr int kThreads = 192;
+constexpr int kStageA = 128 * 128;  // 128 rows x 128 B
+
+// ============================================================================
+//                                 the kernel
+// ============================================================================
+template <int AK, int BK>
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
+                   const __grid_constant__ CUtensorMap tma_b, const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int S = p.stages;
+  const int stage_b = p.BN * 128;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * kStageA;
+  uint64_t* full = (uint64_t*)(sB + S * stage_b);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int m0 = blockIdx.x * 128, n0 = blockIdx.y * p.BN;
+  const int grp = blockIdx.z / p.splits, split = blockIdx.z % p.splits;
+  const int nkb_total = p.K / 32;
+  const int per = (nkb_total + p.splits - 1) / p.splits;
+  const int kb0 = split * per;
+  const int kb1 = min(nkb_total, kb0 + per);
+  const int ncols = p.BN <= 32 ? 32 : p.BN <= 64 ? 64 : p.BN <= 128 ? 128 : 256;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_b) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer --
+    if (lane == 0) {
+      // im2col origin of this M tile (first output pixel)
+      int a_h = 0, a_w = 0, a_n = 0;
+      if (AK == OP_IM2COL_K) {
+        const int ohw = p.OH * p.OW;
+        a_n = m0 / ohw;
+        const int r = m0 - a_n * ohw;
+        a_w = r / p.OH;
+        a_h = r - a_w * p.OH;
+        a_h = a_h * p.sh - p.pt;
+        a_w = a_w * p.sw - p.pl;
+      }
+      const uint32_t bytes = kStageA + stage_b;
+      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+        const int s = i % S;
+        const uint32_t ph = (i / S) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], bytes);
+        uint8_t* a = sA + s * kStageA;
+        uint8_t* b = sB + s * stage_b;
+        const int k0 = kb * 32;
+        // ---- A ----
+        if (AK == OP_TILED_K) {
+          tma_2d(a, &tma_a, &full[s], k0 + grp * p.a_grp_k, m0 + grp * p.a_grp_mn);
+        } else if (AK == OP_TILED_MN) {
+          for (int j = 0; j < 4; ++j)
+            tma_2d(a + j * 4096, &tma_a, &full[s], m0 + grp * p.a_grp_mn + 32 * j,
+                   k0 + grp * p.a_grp_k);
+        } else {  // OP_IM2COL_K: kb = tap * cchunks + cc
+          const int tap = kb / p.cchunks, cc = kb - tap * p.cchunks;
+          const int fj = tap / p.fh, fi = tap - fj * p.fh;
+          tma_im2col_4d(a, &tma_a, &full[s], grp * p.a_grp_c + cc * 32, a_h, a_w, a_n,
+                        (uint16_t)fi, (uint16_t)fj);
+        }
+        // ---- B ----
+        if (BK == OP_TILED_K) {
+          tma_2d(b, &tma_b, &full[s], k0 + grp * p.b_grp_k, n0 + grp * p.b_grp_mn);
+        } else if (BK == OP_TILED_MN) {
+          for (int j = 0; j < p.BN / 32; ++j)
+            tma_2d(b + j * 4096, &tma_b, &full[s], n0 + grp * p.b_grp_mn + 32 * j,
+                   k0 + grp * p.b_grp_k);
+        } else {  // OP_IM2COL_MN: K = output pixels, rows n = (tap, c)
+          const int ohw = p.OH * p.OW;
+          const int pn = k0 / ohw;
+          const int r = k0 - pn * ohw;
+          const int pw = r / p.OH;
+          const int phh = r - pw * p.OH;
+          const int h = phh * p.sh - p.pt, w = pw * p.sw - p.pl;
+          for (int j = 0; j < p.BN / 32; ++j) {
+            const int nn = n0 + 32 * j;
+            const int tap = nn / (p.cchunks * 32), c = nn - tap * p.cchunks * 32;
+            const int fj = tap / p.fh, fi = tap - fj * p.fh;
+            tma_im2col_4d(b + j * 4096, &tma_b, &full[s], grp * p.b_grp_c + c, h, w, pn,
+                          (uint16_t)fi, (uint16_t)fj);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // --------------------------------------------------------- MMA issuer --
+    if (lane == 0) {
+      const uint32_t idesc = idesc_tf32(p.BN, AK == OP_TILED_MN ? 1 : 0,
+                                        (BK == OP_TILED_MN || BK == OP_IM2COL_MN) ? 1 : 0);
+      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
+        const int s = i % S;
+        const uint32_t ph = (i / S) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t a = smem_u32(sA + s * kStageA);
+        const uint32_t b = smem_u32(sB + s * stage_b);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          // K-major SW128: K step = +32 B within the 128-B row, SBO = 1024 (8 rows).
+          // MN-major SW128: K step = +1024 B (8 rows of 128 B), LBO = 4096 (32-elem MN chunk).
+          const uint64_t ad = (AK == OP_TILED_MN) ? sdesc(a + k * 1024, 4096, 1024)
+                                                  : sdesc(a + k * 32, 16, 1024);
+          const uint64_t bd = (BK == OP_TILED_MN || BK == OP_IM2COL_MN)
+                                  ? sdesc(b + k * 1024, 4096, 1024)
+                                  : sdesc(b + k * 32, 16, 1024);
+          mma_tf32(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(tfull);
+    }
+  } else {
+    // ----------------------------------------------------------- epilogue --
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = q * 32 + lane;
+    const int m = m0 + row;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    const bool row_ok = m < p.M;
+    int64_t row_base = 0;
+    float rbias = 0.f;
+    if (p.epi == EPI_PIX) {
+      const int img = m / p.epi_OHW;
+      const int sp = m - img * p.epi_OHW;
+      row_base = (int64_t)img * p.img_stride + sp + (int64_t)grp * p.grp_col * p.ld;
+    } else {
+      row_base = (int64_t)m + (int64_t)grp * p.grp_out;
+      if (p.bias && p.splits == 1 && row_ok) rbias = p.bias[m + grp * p.grp_col];
+    }
+    float* out = p.out;
+    const bool partial = p.splits > 1;
+    if (partial) out += (int64_t)split * p.split_stride;
+    for (int c0 = 0; c0 < p.BN; c0 += 32) {
+      uint32_t r[32];
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
+      CK_LD32(r, taddr);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row_ok) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = n0 + c0 + j;
+          if (col < p.n_valid) {
+            float v = __uint_as_float(r[j]);
+            float* dst = out + row_base + (int64_t)col * p.ld;
+            if (!partial) {
+              if (p.epi == EPI_PIX) {
+                if (p.bias) v = __fadd_rn(v, p.bias[col + grp * p.grp_col]);
+              } else if (p.bias) {
+                v = __fadd_rn(v, rbias);
+              }
+              if (p.relu) v = v > 0.f ? v : 0.f;
+              if (p.acc) v = __fadd_rn(*dst, v);
+            }
+            *dst = v;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
+  }
+}
+
+// ============================================================================
+//                          layout transforms (HBM bound)
+// ============================================================================
+
+// HWCN x[n][c][w][h] -> pixel-major xT[n][w][h][cp], channel c of group g at
+// cp = g*Cgp + (c - g*Cg), zeros in the per-group padding.  32x32 smem tile.
+__global__ void to_pixel_major_k(const float* __restrict__ x, float* __restrict__ xt, int HW,
+                                 int C, int Cg, int Cgp, int groups) {
+  __shared__ float tile[32][33];
+  const int n = blockIdx.z;
+  const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;  // c0 over padded channels
+  const int Cp = Cgp * groups;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 256 threads: ty 0..7
+  // read: rows = padded channel, cols = pixel (coalesced along pixels)
+  for (int r = ty; r < 32; r += 8) {
+    const int cp = c0 + r;
+    const int g = cp / Cgp, cl = cp - g * Cgp;
+    const int p = p0 + tx;
+    float v = 0.f;
+    if (cp < Cp && cl < Cg && p < HW) v = x[((int64_t)n * C + g * Cg + cl) * HW + p];
+    tile[r][tx] = v;
+  }
+  __syncthreads();
+  // write: rows = pixel, cols = padded channel (coalesced along channels)
+  for (int r = ty; r < 32; r += 8) {
+    const int p = p0 + r, cp = c0 + tx;
+    if (p < HW && cp < Cp) xt[((int64_t)n * HW + p) * Cp + cp] = tile[tx][r];
+  }
+}
+
+// fprop filters: fT[k][tap][cpos] (tap = fi + fh*fj), from the reference
+// filter bank f[fi + fh*(fj + fw*(c*fsc + k*fsk))]; zeros for channel pads.
+__global__ void repack_fprop_k(const float* __restrict__ f, float* __restrict__ ft, int fh, int fw,
+                               int Cg, int Cgp, int K, int64_t fsc, int64_t fsk) {
+  const int64_t taps = (int64_t)fh * fw;
+  const int64_t total = (int64_t)K * taps * Cgp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int cp = (int)(e % Cgp);
+    const int64_t r = e / Cgp;
+    const int tap = (int)(r % taps);
+    const int64_t k = r / taps;
+    float v = 0.f;
+    if (cp < Cg) {
+      const int fi = tap % fh, fj = tap / fh;
+      v = f[fi + (int64_t)fh * (fj + (int64_t)fw * (cp * fsc + k * fsk))];
+    }
+    ft[e] = v;
+  }
+}
+
+// dgrad filters: gT[c][tap'][kpos], kpos = per-group padded filter index,
+// tap' = flipped tap: g[fi', fj', k, c] = f[fh-1-fi', fw-1-fj', c, k].
+__global__ void repack_dgrad_k(const float* __restrict__ f, float* __restrict__ gt, int fh, int fw,
+                               int Cg, int Kg, int Kgp, int groups, int64_t fsc, int64_t fsk) {
+  const int64_t taps = (int64_t)fh * fw;
+  const int64_t total = (int64_t)Cg * groups * taps * Kgp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int kp = (int)(e % Kgp);
+    const int64_t r = e / Kgp;
+    const int tap = (int)(r % taps);
+    const int64_t cc = r / taps;  // 0 .. Cg*groups-1
+    const int g = (int)(cc / Cg);
+    const int c = (int)(cc - (int64_t)g * Cg);
+    float v = 0.f;
+    if (kp < Kg) {
+      const int fi = fh - 1 - tap % fh, fj = fw - 1 - tap / fh;
+      const int64_t k = (int64_t)g * Kg + kp;
+      v = f[fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + k * fsk))];
+    }
+    gt[e] = v;
+  }
+}
+
+// wgrad: df[fi,fj,c,k] (+)= sum_s part[s][g][n = tap*Cgp + cpos][k]  (fixed order)
+__global__ void wgrad_finish_k(const float* __restrict__ part, float* df, int fh, int fw, int Cg,
+                               int Cgp, int Kg, int groups, int splits, int64_t split_stride,
+                               int64_t fsc, int64_t fsk, int acc) {
+  const int64_t taps = (int64_t)fh * fw;
+  const int64_t total = (int64_t)groups * Kg * taps * Cg;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    // e enumerates (k fastest) so reads of part are coalesced
+    const int k = (int)(e % Kg);
+    int64_t r = e / Kg;
+    const int c = (int)(r % Cg);
+    r /= Cg;
+    const int tap = (int)(r % taps);
+    const int g = (int)(r / taps);
+    const int64_t n = (int64_t)tap * Cgp + c;
+    const int64_t src = ((int64_t)g * taps * Cgp + n) * Kg + k;
+    float s = 0.f;
+    for (int sp = 0; sp < splits; ++sp) s += part[sp * split_stride + src];
+    const int fi = tap % fh, fj = tap / fh;
+    const int64_t kk = (int64_t)g * Kg + k;
+    float* dst = df + fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + kk * fsk));
+    *dst = acc ? *dst + s : s;
+  }
+}
+
+// generic split-K finisher for EPI_LINEAR outputs: out[row + col*ld]
+__global__ void splitk_finish_k(const float* __restrict__ part, float* out, int rows, int cols,
+                                int64_t ld, int splits, int64_t split_stride,
+                                const float* __restrict__ bias, int relu, int acc) {
+  const int64_t total = (int64_t)rows * cols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int row = (int)(e % rows);
+    const int64_t col = e / rows;
+    const int64_t a = row + col * ld;
+    float s = 0.f;
+    for (int sp = 0; sp < splits; ++sp) s += part[sp * split_stride + a];
+    if (bias) s = __fadd_rn(s, bias[row]);
+    if (relu) s = s > 0.f ? s : 0.f;
+    out[a] = acc ? __fadd_rn(out[a], s) : s;
+  }
+}
+
+}  // namespace tc
+
+// ============================================================================
+//                                  host side
+// ============================================================================
+
+using namespace tc;
+
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*PFN_encodeIm2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                     const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                     cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                     CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled g_encode_tiled = nullptr;
+static PFN_encodeIm2col g_encode_im2col = nullptr;
+static bool g_tc_ok = false;
+
+static bool load_driver() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f1, cudaEnableDefault, &q1) !=
+            cudaSuccess ||
+        cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f2, cudaEnableDefault, &q2) !=
+            cudaSuccess)
+      return;
+    g_encode_tiled = (PFN_encodeTiled)f1;
+    g_encode_im2col = (PFN_encodeIm2col)f2;
+    int dev = 0, major = 0, minor = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+    g_tc_ok = g_encode_tiled && g_encode_im2col && major == 10 && minor == 0;
+  });
+  return g_tc_ok;
+}
+
+bool conv_tc_available() { return load_driver(); }
+
+struct TcState {
+  Workspace xt, dyt, ft, part;
+};
+
+static TcState* state(ck_handle* h) {
+  if (!h->tc) h->tc = new TcState();
+  return h->tc;
+}
+
+void conv_tc_release(ck_handle* h) {
+  if (!h->tc) return;
+  h->tc->xt.release();
+  h->tc->dyt.release();
+  h->tc->ft.release();
+  h->tc->part.release();
+  delete h->tc;
+  h->tc = nullptr;
+}
+
+static inline int rup(int v, int m) { return (v + m - 1) / m * m; }
+
+// 2D tiled map over a row-major [outer][inner] fp32 matrix, box (32, box_outer), SW128.
+static CUtensorMap map_2d(const float* base, uint64_t inner, uint64_t outer, uint64_t ld_elems,
+                          uint32_t box_outer) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {ld_elems * 4};
+  cuuint32_t box[2] = {32, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides,
+                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Err(CK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+// 4D im2col map over a pixel-major tensor (Cp, H, W, N).
+static CUtensorMap map_im2col(const float* base, int Cp, int H, int W, int N, int lo_h, int lo_w,
+                              int up_h, int up_w, int sh, int sw, int pixels) {
+  CUtensorMap m;
+  cuuint64_t dims[4] = {(cuuint64_t)Cp, (cuuint64_t)H, (cuuint64_t)W, (cuuint64_t)N};
+  cuuint64_t strides[3] = {(cuuint64_t)Cp * 4, (cuuint64_t)Cp * H * 4, (cuuint64_t)Cp * H * W * 4};
+  int lower[2] = {lo_h, lo_w};
+  int upper[2] = {up_h, up_w};
+  cuuint32_t es[4] = {1, (cuuint32_t)sh, (cuuint32_t)sw, 1};
+  CUresult r = g_encode_im2col(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides,
+                               lower, upper, 32, (cuuint32_t)pixels, es,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Err(CK_ERR_CUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")");
+  return m;
+}
+
+static int pick_bn(int n) {
+  // largest MMA N (multiple of 16, <= 256) that tiles n with little waste
+  if (n <= 256) return rup(n, 16);
+  const int cands[] = {256, 192, 128};
+  int best = 128;
+  double best_w = 1e9;
+  for (int c : cands) {
+    double waste = (double)rup(n, c) / n;
+    if (waste < best_w - 1e-9) {
+      best_w = waste;
+      best = c;
+    }
+  }
+  return best;
+}
+
+template <int AK, int BK>
+static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int grid_m,
+                   int grid_n, int grid_z, cudaStream_t s) {
+  const int stage_bytes = kStageA + p.BN * 128;
+  const int budget = 227 * 1024 - 1024 - 256;
+  p.stages = std::min(8, budget / stage_bytes);
+  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + 256;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(tc_gemm_kernel<AK, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    configured = true;
+  }
+  count_launch();
+  tc_gemm_kernel<AK, BK><<<dim3(grid_m, grid_n, grid_z), kThreads, smem, s>>>(a, b, p);
+}
+
+static int split_for(int tiles, int kblocks) {
+  // fill ~1 wave of 148 SMs; keep >= 8 k-blocks per split
+  int s = 1;
+  while (tiles * s * 2 <= 148 && kblocks / (s * 2) >= 8) s *= 2;
+  return s;
+}
+
+static void* grow(Workspace& w, size_t bytes, cudaStream_t s) {
+  void* p = w.get(bytes, s);
+  if (!p) throw Err(CK_ERR_CUDA, "workspace allocation failed");
+  return p;
+}
+
+static void to_pm(const float* x, float* xt, int H, int W, int C, int N, int Cg, int Cgp,
+                  int groups, cudaStream_t s) {
+  const int HW = H * W;
+  dim3 grid((HW + 31) / 32, (Cgp * groups + 31) / 32, N);
+  count_launch();
+  to_pixel_major_k<<<grid, 256, 0, s>>>(x, xt, HW, C, Cg, Cgp, groups);
+}
+
+static bool is_fc(const ConvDims& d) {
+  return d.OH == 1 && d.OW == 1 && d.fh == d.H && d.fw == d.W && d.pt == 0 && d.pb == 0 &&
+         d.pl == 0 && d.pr == 0 && d.groups == 1 && d.fsc == 1;
+}
+
+// ---------------------------------------------------------------- fprop ----
+bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
+                     const ConvDims& d, int relu, cudaStream_t s) {
+  if (!load_driver()) return false;
+  const int Kg = d.Kg();
+  if (is_fc(d)) {
+    // Y[k, n] = sum_q F[q, k] X[q, n]   (A = filters, B = images, both K-major)
+    const int Q = d.H * d.W * d.C;
+    if (Q % 4 || d.K < 16) return false;
+    const int BN = pick_bn(std::min(d.N, 256));
+    const int gm = (d.K + 127) / 128, gn = (d.N + BN - 1) / BN;
+    const int splits = split_for(gm * gn, rup(Q, 32) / 32);
+    GemmParams p{};
+    p.M = d.K; p.N = d.N; p.K = rup(Q, 32); p.BN = BN; p.splits = splits;
+    p.epi = EPI_LINEAR; p.ld = d.K; p.n_valid = d.N; p.relu = relu; p.bias = bias;
+    CUtensorMap ta = map_2d(f, Q, d.K, Q, 128);
+    CUtensorMap tb = map_2d(x, Q, d.N, Q, BN);
+    if (splits > 1) {
+      const int64_t per = (int64_t)d.K * d.N;
+      float* part = (float*)grow(state(h)->part, sizeof(float) * per * splits, s);
+      p.out = part; p.split_stride = per;
+      launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, splits, s);
+      count_launch();
+      splitk_finish_k<<<std::min<int64_t>((per + 255) / 256, 148 * 8), 256, 0, s>>>(
+          part, y, d.K, d.N, d.K, splits, per, bias, relu, 0);
+    } else {
+      p.out = y;
+      launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
+    }
+    return true;
+  }
+  if (d.Cg < 16 || Kg < 16) return false;
+  const int Cgp = rup(d.Cg, 32), Cp = Cgp * d.groups;
+  const int taps = d.fh * d.fw;
+  if (d.pt > 127 || d.pl > 127 || d.fh > 128 || d.fw > 128) return false;
+  TcState* st = state(h);
+  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
+  float* ft = (float*)grow(st->ft, sizeof(float) * (size_t)d.K * taps * Cgp, s);
+  to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
+  count_launch();
+  repack_fprop_k<<<std::min<int64_t>(((int64_t)d.K * taps * Cgp + 255) / 256, 148 * 8), 256, 0, s>>>(
+      f, ft, d.fh, d.fw, d.Cg, Cgp, d.K, d.fsc, d.fsk);
+  GemmParams p{};
+  p.M = d.N * d.OH * d.OW;
+  p.N = Kg;
+  p.K = taps * Cgp;
+  p.BN = pick_bn(Kg);
+  p.splits = 1;
+  p.OH = d.OH; p.OW = d.OW; p.sh = d.sh; p.sw = d.sw; p.pt = d.pt; p.pl = d.pl; p.fh = d.fh;
+  p.cchunks = Cgp / 32;
+  p.a_grp_c = Cgp;
+  p.b_grp_mn = Kg;
+  p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+  p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg; p.epi_OHW = d.OH * d.OW;
+  p.bias = bias; p.relu = relu; p.acc = 0; p.n_valid = Kg;
+  CUtensorMap ta = map_im2col(xt, Cp, d.H, d.W, d.N, -d.pt, -d.pl, d.pb - (d.fh - 1),
+                              d.pr - (d.fw - 1), d.sh, d.sw, 128);
+  CUtensorMap tb = map_2d(ft, (uint64_t)taps * Cgp, d.K, (uint64_t)taps * Cgp, p.BN);
+  launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (Kg + p.BN - 1) / p.BN, d.groups,
+                                  s);
+  return true;
+}
+
+// ---------------------------------------------------------------- dgrad ----
+bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, const ConvDims& d,
+                   int acc, cudaStream_t s) {
+  if (!load_driver()) return false;
+  const int Kg = d.Kg();
+  if (is_fc(d)) {
+    // dX[q, n] = sum_k F[q, k] dY[k, n]   (A = F MN-major, B = dY K-major)
+    const int Q = d.H * d.W * d.C;
+    if (Q % 4 || d.K % 4) return false;
+    const int BN = pick_bn(std::min(d.N, 256));
+    const int gm = (Q + 127) / 128, gn = (d.N + BN - 1) / BN;
+    const int splits = split_for(gm * gn, rup(d.K, 32) / 32);
+    GemmParams p{};
+    p.M = Q; p.N = d.N; p.K = rup(d.K, 32); p.BN = BN; p.splits = splits;
+    p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.N; p.acc = acc;
+    CUtensorMap ta = map_2d(f, Q, d.K, Q, 32);       // F as [k][q]: MN (q) inner
+    CUtensorMap tb = map_2d(dy, d.K, d.N, d.K, BN);  // dY as [n][k]: K inner
+    if (splits > 1) {
+      const int64_t per = (int64_t)Q * d.N;
+      float* part = (float*)grow(state(h)->part, sizeof(float) * per * splits, s);
+      p.out = part; p.split_stride = per;
+      launch<OP_TILED_MN, OP_TILED_K>(ta, tb, p, gm, gn, splits, s);
+      count_launch();
+      splitk_finish_k<<<std::min<int64_t>((per + 255) / 256, 148 * 8), 256, 0, s>>>(
+          part, dx, Q, d.N, Q, splits, per, nullptr, 0, acc);
+    } else {
+      p.out = dx;
+      launch<OP_TILED_MN, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
+    }
+    return true;
+  }
+  // stride-1 conv of dy with the flipped bank, padding fh-1-pt (SPEC.md:151 adjoint)
+  if (d.sh != 1 || d.sw != 1) return false;
+  if (d.Cg < 16 || Kg < 16) return false;
+  if (d.pt > d.fh - 1 || d.pb > d.fh - 1 || d.pl > d.fw - 1 || d.pr > d.fw - 1) return false;
+  const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
+  const int taps = d.fh * d.fw;
+  TcState* st = state(h);
+  float* dyt = (float*)grow(st->dyt, sizeof(float) * (size_t)d.N * d.OH * d.OW * Kp, s);
+  float* gt = (float*)grow(st->ft, sizeof(float) * (size_t)d.C * taps * Kgp, s);
+  to_pm(dy, dyt, d.OH, d.OW, d.K, d.N, Kg, Kgp, d.groups, s);
+  count_launch();
+  repack_dgrad_k<<<std::min<int64_t>(((int64_t)d.C * taps * Kgp + 255) / 256, 148 * 8), 256, 0, s>>>(
+      f, gt, d.fh, d.fw, d.Cg, Kg, Kgp, d.groups, d.fsc, d.fsk);
+  const int qt = d.fh - 1 - d.pt, qb = d.fh - 1 - d.pb, ql = d.fw - 1 - d.pl, qr = d.fw - 1 - d.pr;
+  GemmParams p{};
+  p.M = d.N * d.H * d.W;
+  p.N = d.Cg;
+  p.K = taps * Kgp;
+  p.BN = pick_bn(d.Cg);
+  p.splits = 1;
+  p.OH = d.H; p.OW = d.W; p.sh = 1; p.sw = 1; p.pt = qt; p.pl = ql; p.fh = d.fh;
+  p.cchunks = Kgp / 32;
+  p.a_grp_c = Kgp;
+  p.b_grp_mn = d.Cg;
+  p.epi = EPI_PIX; p.out = dx; p.ld = (int64_t)d.H * d.W;
+  p.img_stride = (int64_t)d.C * d.H * d.W; p.grp_col = d.Cg; p.epi_OHW = d.H * d.W;
+  p.bias = nullptr; p.relu = 0; p.acc = acc; p.n_valid = d.Cg;
+  CUtensorMap ta = map_im2col(dyt, Kp, d.OH, d.OW, d.N, -qt, -ql, qb - (d.fh - 1),
+                              qr - (d.fw - 1), 1, 1, 128);
+  CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kgp, d.C, (uint64_t)taps * Kgp, p.BN);
+  launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.Cg + p.BN - 1) / p.BN,
+                                  d.groups, s);
+  return true;
+}
+
+// ---------------------------------------------------------------- wgrad ----
+bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, const ConvDims& d,
+                   int acc, cudaStream_t s) {
+  if (!load_driver()) return false;
+  const int Kg = d.Kg();
+  if (is_fc(d)) {
+    // dF[q, k] = sum_n X[q, n] dY[k, n]   (A = X MN-major, B = dY MN-major)
+    const int Q = d.H * d.W * d.C;
+    if (Q % 4 || d.K % 4) return false;
+    const int BN = d.K >= 256 ? 256 : rup(d.K, 32);
+    const int gm = (Q + 127) / 128, gn = (d.K + BN - 1) / BN;
+    GemmParams p{};
+    p.M = Q; p.N = d.K; p.K = rup(d.N, 32); p.BN = BN; p.splits = 1;
+    p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.K; p.acc = acc; p.out = df;
+    CUtensorMap ta = map_2d(x, Q, d.N, Q, 32);
+    CUtensorMap tb = map_2d(dy, d.K, d.N, d.K, 32);
+    launch<OP_TILED_MN, OP_TILED_MN>(ta, tb, p, gm, gn, 1, s);
+    return true;
+  }
+  if (d.Cg < 16 || Kg < 16) return false;
+  if (d.pt > 127 || d.pl > 127) return false;
+  const int Cgp = rup(d.Cg, 32), Cp = Cgp * d.groups;
+  const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
+  const int taps = d.fh * d.fw;
+  const int P = d.N * d.OH * d.OW;  // K blocks of 32 output pixels, tail zero-filled
+  TcState* st = state(h);
+  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
+  float* dyt = (float*)grow(st->dyt, sizeof(float) * (size_t)P * Kp, s);
+  to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
+  to_pm(dy, dyt, d.OH, d.OW, d.K, d.N, Kg, Kgp, d.groups, s);
+  const int Ntot = taps * Cgp;  // GEMM N = (tap, c) per group
+  const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
+  const int gm = (Kg + 127) / 128, gn = (Ntot + BN - 1) / BN;
+  const int splits = split_for(gm * gn * d.groups, rup(P, 32) / 32);
+  const int64_t per_grp = (int64_t)Ntot * Kg;
+  const int64_t per = per_grp * d.groups;
+  float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
+  GemmParams p{};
+  p.M = Kg; p.N = Ntot; p.K = rup(P, 32); p.BN = BN; p.splits = splits;
+  p.OH = d.OH; p.OW = d.OW; p.sh = d.sh; p.sw = d.sw; p.pt = d.pt; p.pl = d.pl; p.fh = d.fh;
+  p.cchunks = Cgp / 32;
+  p.b_grp_c = Cgp;
+  p.a_grp_mn = Kgp;
+  p.epi = EPI_LINEAR; p.out = part; p.ld = Kg; p.grp_out = per_grp; p.n_valid = Ntot;
+  // partial for split s: part[s*per + g*per_grp + n*Kg + k]
+  p.split_stride = per;
+  if (splits == 1) p.splits = 1;
+  CUtensorMap ta = map_2d(dyt, Kp, P, Kp, 32);  // dy^T as [pixel][k]: k inner (MN-major)
+  CUtensorMap tb = map_im2col(xt, Cp, d.H, d.W, d.N, -d.pt, -d.pl, d.pb - (d.fh - 1),
+                              d.pr - (d.fw - 1), d.sh, d.sw, 32);
+  // the epilogue must write raw partials even when splits == 1
+  GemmParams q = p;
+  q.bias = nullptr; q.relu = 0; q.acc = 0;
+  launch<OP_TILED_MN, OP_IM2COL_MN>(ta, tb, q, gm, gn, d.groups * splits, s);
+  const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
+  count_launch();
+  wgrad_finish_k<<<std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
+      part, df, d.fh, d.fw, d.Cg, Cgp, Kg, d.groups, splits, per, d.fsc, d.fsk, acc);
+  return true;
+}
+
 }  // namespace ck
