@@ -45,11 +45,15 @@ namespace ck {
 // ============================================================================
 namespace tc {
 
+// Every operand is K-major (K contiguous in a 128-byte swizzled row): the
+// "transpose" (MN-major) bit of the kind::tf32 instruction descriptor reads
+// as zeros on this part (probed, tools/tc_probe.py), so layouts that would
+// need it are produced K-major by the transform kernels instead.
 enum OpKind : int {
   OP_TILED_K = 0,     // 2D tensor (K inner, MN outer), box (32, rows)
-  OP_TILED_MN = 1,    // 2D tensor (MN inner, K outer), boxes (32, 32) x rows/32
   OP_IM2COL_K = 2,    // 4D im2col over a pixel-major tensor, box 128 px x 32 ch
-  OP_IM2COL_MN = 3,   // 4D im2col, boxes 32 px x 32 ch, one per 32 rows of n
+  OP_SHIFT_K = 4,     // wgrad B: boxes (32 px, 32 ch) of a channel-major padded
+                      // tensor, K coordinate shifted by the tap: p' + fi + Hp*fj
 };
 
 enum EpiKind : int {
@@ -82,6 +86,9 @@ struct GemmParams {
   const float* bias;      // per col (EPI_PIX) or per row (EPI_LINEAR)
   int relu, acc;
   int n_valid;            // columns < n_valid are stored
+  int Hp;                 // OP_SHIFT_K: padded plane height (tap shift = fi + Hp*fj)
+  int b_grp_row;          // OP_SHIFT_K: per-group row (channel) offset
+  int exp;                // debug experiments (CK_TC_EXP)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -260,10 +267,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- A ----
         if (AK == OP_TILED_K) {
           tma_2d(a, &tma_a, &full[s], k0 + grp * p.a_grp_k, m0 + grp * p.a_grp_mn);
-        } else if (AK == OP_TILED_MN) {
-          for (int j = 0; j < 4; ++j)
-            tma_2d(a + j * 4096, &tma_a, &full[s], m0 + grp * p.a_grp_mn + 32 * j,
-                   k0 + grp * p.a_grp_k);
         } else {  // OP_IM2COL_K: kb = tap * cchunks + cc
           const int tap = kb / p.cchunks, cc = kb - tap * p.cchunks;
           const int fj = tap / p.fh, fi = tap - fj * p.fh;
@@ -273,23 +276,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---- B ----
         if (BK == OP_TILED_K) {
           tma_2d(b, &tma_b, &full[s], k0 + grp * p.b_grp_k, n0 + grp * p.b_grp_mn);
-        } else if (BK == OP_TILED_MN) {
-          for (int j = 0; j < p.BN / 32; ++j)
-            tma_2d(b + j * 4096, &tma_b, &full[s], n0 + grp * p.b_grp_mn + 32 * j,
-                   k0 + grp * p.b_grp_k);
-        } else {  // OP_IM2COL_MN: K = output pixels, rows n = (tap, c)
-          const int ohw = p.OH * p.OW;
-          const int pn = k0 / ohw;
-          const int r = k0 - pn * ohw;
-          const int pw = r / p.OH;
-          const int phh = r - pw * p.OH;
-          const int h = phh * p.sh - p.pt, w = pw * p.sw - p.pl;
+        } else {  // OP_SHIFT_K: rows n = (tap, c), K = padded-grid pixels p'
           for (int j = 0; j < p.BN / 32; ++j) {
             const int nn = n0 + 32 * j;
             const int tap = nn / (p.cchunks * 32), c = nn - tap * p.cchunks * 32;
             const int fj = tap / p.fh, fi = tap - fj * p.fh;
-            tma_im2col_4d(b + j * 4096, &tma_b, &full[s], grp * p.b_grp_c + c, h, w, pn,
-                          (uint16_t)fi, (uint16_t)fj);
+            tma_2d(b + j * 4096, &tma_b, &full[s], k0 + fi + p.Hp * fj, grp * p.b_grp_row + c);
           }
         }
       }
@@ -297,8 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer --
     if (lane == 0) {
-      const uint32_t idesc = idesc_tf32(p.BN, AK == OP_TILED_MN ? 1 : 0,
-                                        (BK == OP_TILED_MN || BK == OP_IM2COL_MN) ? 1 : 0);
+      const uint32_t idesc = idesc_tf32(p.BN, 0, 0);
       for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
         const int s = i % S;
         const uint32_t ph = (i / S) & 1;
@@ -309,13 +300,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           // K-major SW128: K step = +32 B within the 128-B row, SBO = 1024 (8 rows).
-          // MN-major SW128: K step = +1024 B (8 rows of 128 B), LBO = 4096 (32-elem MN chunk).
-          const uint64_t ad = (AK == OP_TILED_MN) ? sdesc(a + k * 1024, 4096, 1024)
-                                                  : sdesc(a + k * 32, 16, 1024);
-          const uint64_t bd = (BK == OP_TILED_MN || BK == OP_IM2COL_MN)
-                                  ? sdesc(b + k * 1024, 4096, 1024)
-                                  : sdesc(b + k * 32, 16, 1024);
-          mma_tf32(tmem, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+          mma_tf32(tmem, sdesc(a + k * 32, 16, 1024), sdesc(b + k * 32, 16, 1024), idesc,
+                   (i > 0 || k > 0) ? 1u : 0u);
         }
         mma_commit(&empty[s]);
       }
@@ -496,6 +482,44 @@ __global__ void splitk_finish_k(const float* __restrict__ part, float* out, int 
   }
 }
 
+// out[c * ldo + r] = in[r * ldi + c] for an R x Cc matrix (32x32 smem tiles).
+__global__ void transpose_k(const float* __restrict__ in, float* __restrict__ out, int R, int Cc,
+                            int64_t ldi, int64_t ldo) {
+  __shared__ float tile[32][33];
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  for (int k = ty; k < 32; k += 8) {
+    const int r = r0 + k, c = c0 + tx;
+    tile[k][tx] = (r < R && c < Cc) ? in[(int64_t)r * ldi + c] : 0.f;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int c = c0 + k, r = r0 + tx;
+    if (c < Cc && r < R) out[(int64_t)c * ldo + r] = tile[tx][k];
+  }
+}
+
+// Channel-major padded planes for the wgrad operands: out[c][n][Wp][Hp] holds
+// in[n][c][W][H] at offset (oh, ow) and zeros elsewhere (zero padding for x,
+// zero "junk" rows/columns of the padded output grid for dy).
+__global__ void pad_planes_k(const float* __restrict__ in, float* __restrict__ out, int H, int W,
+                             int Hp, int Wp, int oh, int ow, int C, int N, int64_t ld) {
+  const int64_t plane = (int64_t)Hp * Wp;
+  const int64_t per_c = plane * N;
+  const int64_t total = per_c * C;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / per_c);
+    const int64_t q = e - c * per_c;  // n * plane + r
+    const int n = (int)(q / plane);
+    const int r = (int)(q - n * plane);
+    const int j = r / Hp - ow, i = r % Hp - oh;
+    float v = 0.f;
+    if (i >= 0 && i < H && j >= 0 && j < W) v = in[((int64_t)n * C + c) * H * W + i + (int64_t)H * j];
+    out[c * ld + q] = v;
+  }
+}
+
 }  // namespace tc
 
 // ============================================================================
@@ -616,6 +640,8 @@ static int pick_bn(int n) {
 template <int AK, int BK>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int grid_m,
                    int grid_n, int grid_z, cudaStream_t s) {
+  static const int exp = getenv("CK_TC_EXP") ? atoi(getenv("CK_TC_EXP")) : 0;
+  p.exp = exp;
   const int stage_bytes = kStageA + p.BN * 128;
   const int budget = 227 * 1024 - 1024 - 256;
   p.stages = std::min(8, budget / stage_bytes);
@@ -649,6 +675,21 @@ static void to_pm(const float* x, float* xt, int H, int W, int C, int N, int Cg,
   dim3 grid((HW + 31) / 32, (Cgp * groups + 31) / 32, N);
   count_launch();
   to_pixel_major_k<<<grid, 256, 0, s>>>(x, xt, HW, C, Cg, Cgp, groups);
+}
+
+static void transpose(const float* in, float* out, int R, int Cc, int64_t ldi, int64_t ldo,
+                      cudaStream_t s) {
+  dim3 grid((Cc + 31) / 32, (R + 31) / 32);
+  count_launch();
+  transpose_k<<<grid, 256, 0, s>>>(in, out, R, Cc, ldi, ldo);
+}
+
+static void pad_planes(const float* in, float* out, int H, int W, int Hp, int Wp, int oh, int ow,
+                       int C, int N, int64_t ld, cudaStream_t s) {
+  const int64_t total = (int64_t)Hp * Wp * N * C;
+  count_launch();
+  pad_planes_k<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
+      in, out, H, W, Hp, Wp, oh, ow, C, N, ld);
 }
 
 static bool is_fc(const ConvDims& d) {
@@ -725,28 +766,30 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   if (!load_driver()) return false;
   const int Kg = d.Kg();
   if (is_fc(d)) {
-    // dX[q, n] = sum_k F[q, k] dY[k, n]   (A = F MN-major, B = dY K-major)
+    // dX[q, n] = sum_k F^T[q, k] dY[k, n]: A = F^T (transposed to K-major), B = dY
     const int Q = d.H * d.W * d.C;
     if (Q % 4 || d.K % 4) return false;
+    float* ft = (float*)grow(state(h)->ft, sizeof(float) * (size_t)Q * d.K, s);
+    transpose(f, ft, d.K, Q, Q, d.K, s);
     const int BN = pick_bn(std::min(d.N, 256));
     const int gm = (Q + 127) / 128, gn = (d.N + BN - 1) / BN;
     const int splits = split_for(gm * gn, rup(d.K, 32) / 32);
     GemmParams p{};
     p.M = Q; p.N = d.N; p.K = rup(d.K, 32); p.BN = BN; p.splits = splits;
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.N; p.acc = acc;
-    CUtensorMap ta = map_2d(f, Q, d.K, Q, 32);       // F as [k][q]: MN (q) inner
-    CUtensorMap tb = map_2d(dy, d.K, d.N, d.K, BN);  // dY as [n][k]: K inner
+    CUtensorMap ta = map_2d(ft, d.K, Q, d.K, 128);   // F^T as [q][k]
+    CUtensorMap tb = map_2d(dy, d.K, d.N, d.K, BN);  // dY as [n][k]
     if (splits > 1) {
       const int64_t per = (int64_t)Q * d.N;
       float* part = (float*)grow(state(h)->part, sizeof(float) * per * splits, s);
       p.out = part; p.split_stride = per;
-      launch<OP_TILED_MN, OP_TILED_K>(ta, tb, p, gm, gn, splits, s);
+      launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, splits, s);
       count_launch();
       splitk_finish_k<<<std::min<int64_t>((per + 255) / 256, 148 * 8), 256, 0, s>>>(
           part, dx, Q, d.N, Q, splits, per, nullptr, 0, acc);
     } else {
       p.out = dx;
-      launch<OP_TILED_MN, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
+      launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
     }
     return true;
   }
@@ -791,54 +834,62 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   if (!load_driver()) return false;
   const int Kg = d.Kg();
   if (is_fc(d)) {
-    // dF[q, k] = sum_n X[q, n] dY[k, n]   (A = X MN-major, B = dY MN-major)
+    // dF[q, k] = sum_n X^T[q, n] dY^T[k, n]: both operands transposed to K-major
     const int Q = d.H * d.W * d.C;
     if (Q % 4 || d.K % 4) return false;
+    const int Np = rup(d.N, 4);
+    TcState* st = state(h);
+    float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)Q * Np, s);
+    float* dyt = (float*)grow(st->dyt, sizeof(float) * (size_t)d.K * Np, s);
+    transpose(x, xt, d.N, Q, Q, Np, s);
+    transpose(dy, dyt, d.N, d.K, d.K, Np, s);
     const int BN = d.K >= 256 ? 256 : rup(d.K, 32);
     const int gm = (Q + 127) / 128, gn = (d.K + BN - 1) / BN;
     GemmParams p{};
     p.M = Q; p.N = d.K; p.K = rup(d.N, 32); p.BN = BN; p.splits = 1;
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.K; p.acc = acc; p.out = df;
-    CUtensorMap ta = map_2d(x, Q, d.N, Q, 32);
-    CUtensorMap tb = map_2d(dy, d.K, d.N, d.K, 32);
-    launch<OP_TILED_MN, OP_TILED_MN>(ta, tb, p, gm, gn, 1, s);
+    CUtensorMap ta = map_2d(xt, d.N, Q, Np, 128);
+    CUtensorMap tb = map_2d(dyt, d.N, d.K, Np, BN);
+    launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
     return true;
   }
+  // Stride-1 convolutions: reduce over the output pixels p' of the padded grid
+  // (Hp x Wp per image).  dy is laid channel-major with zeros at the junk
+  // positions of that grid; x channel-major and zero padded, so the im2row
+  // column of tap (fi, fj) is x shifted by fi + Hp*fj -- a K-major 2D TMA box.
+  if (d.sh != 1 || d.sw != 1) return false;
   if (d.Cg < 16 || Kg < 16) return false;
-  if (d.pt > 127 || d.pl > 127) return false;
-  const int Cgp = rup(d.Cg, 32), Cp = Cgp * d.groups;
-  const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
+  const int Cgp = rup(d.Cg, 32);
   const int taps = d.fh * d.fw;
-  const int P = d.N * d.OH * d.OW;  // K blocks of 32 output pixels, tail zero-filled
+  const int Hp = d.H + d.pt + d.pb, Wp = d.W + d.pl + d.pr;
+  const int64_t P = (int64_t)d.N * Hp * Wp;
+  const int64_t ldp = rup((int)std::min<int64_t>(P, INT32_MAX), 4);
   TcState* st = state(h);
-  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
-  float* dyt = (float*)grow(st->dyt, sizeof(float) * (size_t)P * Kp, s);
-  to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
-  to_pm(dy, dyt, d.OH, d.OW, d.K, d.N, Kg, Kgp, d.groups, s);
+  float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)ldp * d.C, s);
+  float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)ldp * d.K, s);
+  pad_planes(x, xp, d.H, d.W, Hp, Wp, d.pt, d.pl, d.C, d.N, ldp, s);
+  pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, ldp, s);
   const int Ntot = taps * Cgp;  // GEMM N = (tap, c) per group
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
   const int gm = (Kg + 127) / 128, gn = (Ntot + BN - 1) / BN;
-  const int splits = split_for(gm * gn * d.groups, rup(P, 32) / 32);
+  const int kblocks = (int)((P + 31) / 32);
+  const int splits = split_for(gm * gn * d.groups, kblocks);
   const int64_t per_grp = (int64_t)Ntot * Kg;
   const int64_t per = per_grp * d.groups;
   float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
   GemmParams p{};
-  p.M = Kg; p.N = Ntot; p.K = rup(P, 32); p.BN = BN; p.splits = splits;
-  p.OH = d.OH; p.OW = d.OW; p.sh = d.sh; p.sw = d.sw; p.pt = d.pt; p.pl = d.pl; p.fh = d.fh;
+  p.M = Kg; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.splits = splits;
+  p.fh = d.fh; p.Hp = Hp;
   p.cchunks = Cgp / 32;
-  p.b_grp_c = Cgp;
-  p.a_grp_mn = Kgp;
+  p.a_grp_mn = Kg;
+  p.b_grp_row = d.Cg;
+  // raw partials: part[s*per + g*per_grp + n*Kg + k]
   p.epi = EPI_LINEAR; p.out = part; p.ld = Kg; p.grp_out = per_grp; p.n_valid = Ntot;
-  // partial for split s: part[s*per + g*per_grp + n*Kg + k]
   p.split_stride = per;
-  if (splits == 1) p.splits = 1;
-  CUtensorMap ta = map_2d(dyt, Kp, P, Kp, 32);  // dy^T as [pixel][k]: k inner (MN-major)
-  CUtensorMap tb = map_im2col(xt, Cp, d.H, d.W, d.N, -d.pt, -d.pl, d.pb - (d.fh - 1),
-                              d.pr - (d.fw - 1), d.sh, d.sw, 32);
-  // the epilogue must write raw partials even when splits == 1
-  GemmParams q = p;
-  q.bias = nullptr; q.relu = 0; q.acc = 0;
-  launch<OP_TILED_MN, OP_IM2COL_MN>(ta, tb, q, gm, gn, d.groups * splits, s);
+  p.bias = nullptr; p.relu = 0; p.acc = 0;
+  CUtensorMap ta = map_2d(dyp, (uint64_t)P, d.K, ldp, 128);  // rows k, K = p'
+  CUtensorMap tb = map_2d(xp, (uint64_t)P, d.C, ldp, 32);    // rows c, K = p' + shift
+  launch<OP_TILED_K, OP_SHIFT_K>(ta, tb, p, gm, gn, d.groups * splits, s);
   const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
   count_launch();
   wgrad_finish_k<<<std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(

@@ -46,9 +46,16 @@ def test_network_fwd_bwd(name, batch, kw, math):
     loss = g.get("objective")[0]
     tol = 1e-4 if math == "fp32" else 1e-2
     assert abs(loss - vals["objective"][0]) <= tol * abs(vals["objective"][0])
+    def err(a, b):
+        if math == "fp32":
+            return rel(a, b)
+        a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)  # normwise (TF32)
+        return max(float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30)),
+                   float(np.max(np.abs(a - b)) / (np.max(np.abs(b)) + 1e-30)))
+
     for pname, _, _ in net.params:
-        assert rel(g.get(pname, deriv=True), derivs[pname]) < (2e-3 if math == "fp32" else 5e-2), pname
-    assert rel(g.get("data", deriv=True), derivs["data"]) < (2e-3 if math == "fp32" else 5e-2)
+        assert err(g.get(pname, deriv=True), derivs[pname]) < (2e-3 if math == "fp32" else 3e-2), pname
+    assert err(g.get("data", deriv=True), derivs["data"]) < (2e-3 if math == "fp32" else 3e-2)
     assert g.last_launches > 0
 
 
