@@ -340,8 +340,8 @@ class Rng:
         self._h = C.c_void_p(lib().cko_rng_new(seed))
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().cko_rng_free(self._h)
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.cko_rng_free(self._h)
             self._h = None
 
     def next(self) -> int:

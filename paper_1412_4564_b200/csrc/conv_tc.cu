@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 
@@ -123,6 +124,15 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 
@@ -279,13 +289,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {  // OP_SHIFT_K: rows n = (tap, c), K = padded-grid pixels p'
           for (int j = 0; j < p.BN / 32; ++j) {
             const int nn = n0 + 32 * j;
-            const int tap = nn / (p.cchunks * 32), c = nn - tap * p.cchunks * 32;
+            const int tap = nn / (p.cchunks * 32);
+            const int c = nn - tap * p.cchunks * 32;
             const int fj = tap / p.fh, fi = tap - fj * p.fh;
-            tma_2d(b + j * 4096, &tma_b, &full[s], k0 + fi + p.Hp * fj, grp * p.b_grp_row + c);
+            const int shift = fi + p.Hp * fj, r = shift & 3;  // copy r keeps 16-B alignment
+            tma_3d(b + j * 4096, &tma_b, &full[s], k0 + shift - r, grp * p.b_grp_row + c, r);
           }
         }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer --
     if (lane == 0) {
@@ -307,12 +320,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mma_commit(tfull);
     }
+    __syncwarp();
   } else {
     // ----------------------------------------------------------- epilogue --
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const int row = q * 32 + lane;
     const int m = m0 + row;
-    mbar_wait(tfull, 0);
+    const bool empty_split = kb0 >= kb1;  // no MMA issued: the tile is zero
+    if (!empty_split) mbar_wait(tfull, 0);
     tc_fence_after();
     const bool row_ok = m < p.M;
     int64_t row_base = 0;
@@ -333,6 +348,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
       CK_LD32(r, taddr);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (empty_split)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = 0u;
       if (row_ok) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -502,21 +520,29 @@ __global__ void transpose_k(const float* __restrict__ in, float* __restrict__ ou
 // Channel-major padded planes for the wgrad operands: out[c][n][Wp][Hp] holds
 // in[n][c][W][H] at offset (oh, ow) and zeros elsewhere (zero padding for x,
 // zero "junk" rows/columns of the padded output grid for dy).
+// `copies` > 1 also writes copy r = 1..copies-1 shifted left by r elements
+// (out[(r*C + c)*ld + q] = plane value at q + r): TMA box starts must be
+// 16-byte aligned, so a tap shift s is served from copy s % 4 at s - s % 4.
 __global__ void pad_planes_k(const float* __restrict__ in, float* __restrict__ out, int H, int W,
-                             int Hp, int Wp, int oh, int ow, int C, int N, int64_t ld) {
+                             int Hp, int Wp, int oh, int ow, int C, int N, int64_t ld,
+                             int copies) {
   const int64_t plane = (int64_t)Hp * Wp;
   const int64_t per_c = plane * N;
-  const int64_t total = per_c * C;
+  const int64_t total = ld * C * copies;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e / per_c);
-    const int64_t q = e - c * per_c;  // n * plane + r
-    const int n = (int)(q / plane);
-    const int r = (int)(q - n * plane);
-    const int j = r / Hp - ow, i = r % Hp - oh;
+    const int64_t rc = e / ld;  // r * C + c
+    const int64_t q = e - rc * ld + rc / C;  // position in the unshifted row
+    const int c = (int)(rc % C);
     float v = 0.f;
-    if (i >= 0 && i < H && j >= 0 && j < W) v = in[((int64_t)n * C + c) * H * W + i + (int64_t)H * j];
-    out[c * ld + q] = v;
+    if (q < per_c) {
+      const int n = (int)(q / plane);
+      const int r = (int)(q - n * plane);
+      const int j = r / Hp - ow, i = r % Hp - oh;
+      if (i >= 0 && i < H && j >= 0 && j < W)
+        v = in[((int64_t)n * C + c) * H * W + i + (int64_t)H * j];
+    }
+    out[e] = v;
   }
 }
 
@@ -658,6 +684,8 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
 
 static int split_for(int tiles, int kblocks) {
   // fill ~1 wave of 148 SMs; keep >= 8 k-blocks per split
+  static const int force = getenv("CK_TC_SPLITS") ? atoi(getenv("CK_TC_SPLITS")) : 0;
+  if (force > 0) return std::min(force, std::max(1, kblocks));
   int s = 1;
   while (tiles * s * 2 <= 148 && kblocks / (s * 2) >= 8) s *= 2;
   return s;
@@ -685,11 +713,27 @@ static void transpose(const float* in, float* out, int R, int Cc, int64_t ldi, i
 }
 
 static void pad_planes(const float* in, float* out, int H, int W, int Hp, int Wp, int oh, int ow,
-                       int C, int N, int64_t ld, cudaStream_t s) {
-  const int64_t total = (int64_t)Hp * Wp * N * C;
+                       int C, int N, int64_t ld, int copies, cudaStream_t s) {
+  const int64_t total = ld * C * copies;
   count_launch();
   pad_planes_k<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
-      in, out, H, W, Hp, Wp, oh, ow, C, N, ld);
+      in, out, H, W, Hp, Wp, oh, ow, C, N, ld, copies);
+}
+
+// 3D tiled map over copies of a channel-major [copy][row][ld] tensor, box (32, 32, 1).
+static CUtensorMap map_3d_copies(const float* base, uint64_t inner, uint64_t rows,
+                                 uint64_t copies, uint64_t ld_elems) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {inner, rows, copies};
+  cuuint64_t strides[2] = {ld_elems * 4, ld_elems * rows * 4};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides,
+                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Err(CK_ERR_CUDA, "cuTensorMapEncodeTiled (3d) failed");
+  return m;
 }
 
 static bool is_fc(const ConvDims& d) {
@@ -856,19 +900,24 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   // Stride-1 convolutions: reduce over the output pixels p' of the padded grid
   // (Hp x Wp per image).  dy is laid channel-major with zeros at the junk
   // positions of that grid; x channel-major and zero padded, so the im2row
-  // column of tap (fi, fj) is x shifted by fi + Hp*fj -- a K-major 2D TMA box.
+  // column of tap (fi, fj) is x shifted by fi + Hp*fj -- a K-major TMA box.
+  // Hp is rounded to a multiple of 4 so the shift is fi (mod 4); TMA box
+  // starts must be 16-byte aligned, so x is written in min(4, fh) copies
+  // pre-shifted by 0..3 elements.
   if (d.sh != 1 || d.sw != 1) return false;
   if (d.Cg < 16 || Kg < 16) return false;
   const int Cgp = rup(d.Cg, 32);
   const int taps = d.fh * d.fw;
-  const int Hp = d.H + d.pt + d.pb, Wp = d.W + d.pl + d.pr;
+  const int Hp = rup(d.H + d.pt + d.pb, 4), Wp = d.W + d.pl + d.pr;
   const int64_t P = (int64_t)d.N * Hp * Wp;
-  const int64_t ldp = rup((int)std::min<int64_t>(P, INT32_MAX), 4);
+  if (P + 128 > INT32_MAX) return false;
+  const int64_t ldp = P;  // multiple of 4 since Hp is
+  const int copies = std::min(4, d.fh);
   TcState* st = state(h);
-  float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)ldp * d.C, s);
+  float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)ldp * d.C * copies, s);
   float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)ldp * d.K, s);
-  pad_planes(x, xp, d.H, d.W, Hp, Wp, d.pt, d.pl, d.C, d.N, ldp, s);
-  pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, ldp, s);
+  pad_planes(x, xp, d.H, d.W, Hp, Wp, d.pt, d.pl, d.C, d.N, ldp, copies, s);
+  pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, ldp, 1, s);
   const int Ntot = taps * Cgp;  // GEMM N = (tap, c) per group
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
   const int gm = (Kg + 127) / 128, gn = (Ntot + BN - 1) / BN;
@@ -888,8 +937,18 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   p.split_stride = per;
   p.bias = nullptr; p.relu = 0; p.acc = 0;
   CUtensorMap ta = map_2d(dyp, (uint64_t)P, d.K, ldp, 128);  // rows k, K = p'
-  CUtensorMap tb = map_2d(xp, (uint64_t)P, d.C, ldp, 32);    // rows c, K = p' + shift
-  launch<OP_TILED_K, OP_SHIFT_K>(ta, tb, p, gm, gn, d.groups * splits, s);
+  CUtensorMap tb = map_3d_copies(xp, (uint64_t)P, d.C, copies, ldp);  // [copy][c][p']
+  static const int dbg = getenv("CK_TC_DBG") ? atoi(getenv("CK_TC_DBG")) : 0;
+  if (dbg & 4) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    fprintf(stderr, "[wgrad] before gemm: %s  P=%lld ldp=%lld BN=%d gm=%d gn=%d splits=%d K=%d\n",
+            cudaGetErrorString(e), (long long)P, (long long)ldp, BN, gm, gn, splits, p.K);
+  }
+  if (!(dbg & 1)) launch<OP_TILED_K, OP_SHIFT_K>(ta, tb, p, gm, gn, d.groups * splits, s);
+  if (dbg & 4) {
+    cudaError_t e = cudaStreamSynchronize(s);
+    fprintf(stderr, "[wgrad] after gemm: %s\n", cudaGetErrorString(e));
+  }
   const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
   count_launch();
   wgrad_finish_k<<<std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
