@@ -245,9 +245,9 @@ def vgg16_bn(batch=64, image=224) -> Net:
         x = n.pool(f"pool{gi + 1}", x, f"p{gi + 1}", 2, 2)
     side = image // 32
     x = n.conv("fc6", x, "f6", side, side, 512, 4096)
-    x = n.relu("relu6", x, "r6")
+    x = n.relu("relu_fc6", x, "rf6")
     x = n.conv("fc7", x, "f7", 1, 1, 4096, 4096)
-    x = n.relu("relu7", x, "r7")
+    x = n.relu("relu_fc7", x, "rf7")
     x = n.conv("fc8", x, "f8", 1, 1, 4096, 1000)
     n.loss(x)
     return n

@@ -53,3 +53,14 @@ def test_host_rng_known_values():
     assert u.dtype == np.float32 and np.all((u >= -1) & (u < 1))
     lab = Rng(3).labels(1000, 10)
     assert set(np.unique(lab)) <= set(range(1, 11))
+
+
+def test_nets_are_well_formed():
+    """Every variable has at most one producer (graph.cpp Graph::finalize)."""
+    from paper_1412_4564_b200 import nets
+    for name, make in nets.NETS.items():
+        net = make(batch=2) if name != "vgg16bn" else make(batch=2, image=64)
+        produced = [o for _, _, _, outs, _ in net.layers for o in outs]
+        assert len(produced) == len(set(produced)), name
+        names = [l[1] for l in net.layers]
+        assert len(names) == len(set(names)), name
