@@ -60,6 +60,7 @@ enum OpKind : int {
 enum EpiKind : int {
   EPI_PIX = 0,     // row m = output pixel (n, ow, oh) of an HWCN tensor, col = channel
   EPI_LINEAR = 1,  // addr = row + col * ld
+  EPI_S2D = 2,     // row m = s2d pixel (n, v, u), col c' = (a, b, c) -> x[s*u+a, s*v+b, c]
 };
 
 struct GemmParams {
@@ -89,6 +90,7 @@ struct GemmParams {
   int n_valid;            // columns < n_valid are stored
   int Hp;                 // OP_SHIFT_K: padded plane height (tap shift = fi + Hp*fj)
   int b_grp_row;          // OP_SHIFT_K: per-group row (channel) offset
+  int s2d, s2d_U, s2d_H, s2d_W, s2d_C;  // EPI_S2D: factor, grid height, target dims
   int exp;                // debug experiments (CK_TC_EXP)
 };
 
@@ -332,7 +334,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool row_ok = m < p.M;
     int64_t row_base = 0;
     float rbias = 0.f;
-    if (p.epi == EPI_PIX) {
+    int s_i = 0, s_j = 0;  // EPI_S2D: top-left target pixel of this row's s x s block
+    if (p.epi == EPI_S2D) {
+      const int img = m / p.epi_OHW;
+      const int r = m - img * p.epi_OHW;
+      const int v = r / p.s2d_U, u = r - v * p.s2d_U;
+      s_i = p.s2d * u;
+      s_j = p.s2d * v;
+      row_base = (int64_t)img * p.s2d_C * p.s2d_H * p.s2d_W;
+    } else if (p.epi == EPI_PIX) {
       const int img = m / p.epi_OHW;
       const int sp = m - img * p.epi_OHW;
       row_base = (int64_t)img * p.img_stride + sp + (int64_t)grp * p.grp_col * p.ld;
@@ -357,7 +367,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int col = n0 + c0 + j;
           if (col < p.n_valid) {
             float v = __uint_as_float(r[j]);
-            float* dst = out + row_base + (int64_t)col * p.ld;
+            float* dst;
+            if (p.epi == EPI_S2D) {
+              const int cg = p.s2d_C, ab = col / cg, c = col - ab * cg;
+              const int i = s_i + ab % p.s2d, jj = s_j + ab / p.s2d;
+              if (i >= p.s2d_H || jj >= p.s2d_W) continue;
+              dst = out + row_base + i + (int64_t)p.s2d_H * (jj + (int64_t)p.s2d_W * c);
+            } else {
+              dst = out + row_base + (int64_t)col * p.ld;
+            }
             if (!partial) {
               if (p.epi == EPI_PIX) {
                 if (p.bias) v = __fadd_rn(v, p.bias[col + grp * p.grp_col]);
@@ -543,6 +561,124 @@ __global__ void pad_planes_k(const float* __restrict__ in, float* __restrict__ o
         v = in[((int64_t)n * C + c) * H * W + i + (int64_t)H * j];
     }
     out[e] = v;
+  }
+}
+
+// ---- space-to-depth (strided convolutions, e.g. AlexNet conv1 s=4) ---------
+// A stride-s conv equals a stride-1 conv over x_s2d[u][v][c'] =
+// x[s*u + a, s*v + b, c], c' = c + Cg*(a + s*b), with taps (t, t2) and filter
+// G[t, t2, c', k] = f[a + s*t, b + s*t2, c, k] (zero past the filter edge).
+
+__device__ __forceinline__ float s2d_read(const float* x, int H, int W, int C, int s, int Cg,
+                                          int n, int u, int v, int cp) {
+  const int c = cp % Cg, ab = cp / Cg;
+  const int a = ab % s, b = ab / s;
+  const int i = s * u + a, j = s * v + b;
+  if (i >= H || j >= W) return 0.f;
+  return x[((int64_t)n * C + c) * H * W + i + (int64_t)H * j];
+}
+
+// pixel-major s2d tensor [n][v][u][c'p] for the fprop im2col operand
+__global__ void s2d_pm_k(const float* __restrict__ x, float* __restrict__ out, int H, int W, int C,
+                         int N, int s, int U, int V, int Cs, int Csp) {
+  const int64_t total = (int64_t)N * V * U * Csp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int cp = (int)(e % Csp);
+    int64_t r = e / Csp;
+    const int u = (int)(r % U);
+    r /= U;
+    const int v = (int)(r % V);
+    const int n = (int)(r / V);
+    out[e] = cp < Cs ? s2d_read(x, H, W, C, s, C, n, u, v, cp) : 0.f;
+  }
+}
+
+// channel-major padded copies of the s2d tensor (wgrad B operand), same
+// conventions as pad_planes_k: out[(r*Cs + c')*ld + q] = plane value at q + r.
+__global__ void s2d_planes_k(const float* __restrict__ x, float* __restrict__ out, int H, int W,
+                             int C, int N, int s, int U, int V, int Hp, int Wp, int Cs, int64_t ld,
+                             int copies) {
+  const int64_t plane = (int64_t)Hp * Wp;
+  const int64_t per_c = plane * N;
+  const int64_t total = ld * Cs * copies;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rc = e / ld;
+    const int64_t q = e - rc * ld + rc / Cs;
+    const int cp = (int)(rc % Cs);
+    float v = 0.f;
+    if (q < per_c) {
+      const int n = (int)(q / plane);
+      const int r = (int)(q - n * plane);
+      const int vv = r / Hp, uu = r % Hp;
+      if (uu < U && vv < V) v = s2d_read(x, H, W, C, s, C, n, uu, vv, cp);
+    }
+    out[e] = v;
+  }
+}
+
+// fprop filters of the s2d conv: fT[k][tap = t + Th*t2][c'p]
+__global__ void s2d_repack_fprop_k(const float* __restrict__ f, float* __restrict__ ft, int fh,
+                                   int fw, int Cg, int K, int s, int Th, int Tw, int Csp) {
+  const int64_t total = (int64_t)K * Th * Tw * Csp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int cp = (int)(e % Csp);
+    int64_t r = e / Csp;
+    const int tap = (int)(r % (Th * Tw));
+    const int64_t k = r / (Th * Tw);
+    float v = 0.f;
+    if (cp < s * s * Cg) {
+      const int c = cp % Cg, ab = cp / Cg, a = ab % s, b = ab / s;
+      const int fi = a + s * (tap % Th), fj = b + s * (tap / Th);
+      if (fi < fh && fj < fw) v = f[fi + (int64_t)fh * (fj + (int64_t)fw * (c + (int64_t)Cg * k))];
+    }
+    ft[e] = v;
+  }
+}
+
+// dgrad filters of the s2d conv (flipped taps): gT[c'][tap'][kp]
+__global__ void s2d_repack_dgrad_k(const float* __restrict__ f, float* __restrict__ gt, int fh,
+                                   int fw, int Cg, int K, int Kp, int s, int Th, int Tw) {
+  const int Cs = s * s * Cg;
+  const int64_t total = (int64_t)Cs * Th * Tw * Kp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int kp = (int)(e % Kp);
+    int64_t r = e / Kp;
+    const int tap = (int)(r % (Th * Tw));
+    const int cp = (int)(r / (Th * Tw));
+    float v = 0.f;
+    if (kp < K) {
+      const int c = cp % Cg, ab = cp / Cg, a = ab % s, b = ab / s;
+      const int t = Th - 1 - tap % Th, t2 = Tw - 1 - tap / Th;
+      const int fi = a + s * t, fj = b + s * t2;
+      if (fi < fh && fj < fw) v = f[fi + (int64_t)fh * (fj + (int64_t)fw * (c + (int64_t)Cg * kp))];
+    }
+    gt[e] = v;
+  }
+}
+
+// wgrad finish of the s2d conv: df[fi,fj,c,k] = sum_s part[s][(tap, c'p)][k]
+__global__ void s2d_wgrad_finish_k(const float* __restrict__ part, float* df, int fh, int fw,
+                                   int Cg, int K, int s, int Th, int Csp, int splits,
+                                   int64_t split_stride, int acc) {
+  const int64_t total = (int64_t)K * fh * fw * Cg;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(e % K);
+    int64_t r = e / K;
+    const int c = (int)(r % Cg);
+    r /= Cg;
+    const int fi = (int)(r % fh);
+    const int fj = (int)(r / fh);
+    const int t = fi / s, a = fi % s, t2 = fj / s, b = fj % s;
+    const int64_t n = (int64_t)(t + Th * t2) * Csp + c + (int64_t)Cg * (a + s * b);
+    float v = 0.f;
+    for (int sp = 0; sp < splits; ++sp) v += part[sp * split_stride + n * K + k];
+    float* dst = df + fi + (int64_t)fh * (fj + (int64_t)fw * (c + (int64_t)Cg * k));
+    *dst = acc ? *dst + v : v;
   }
 }
 
@@ -736,6 +872,110 @@ static CUtensorMap map_3d_copies(const float* base, uint64_t inner, uint64_t row
   return m;
 }
 
+// ---- space-to-depth path for strided convolutions --------------------------
+struct S2D {
+  int s, U, V, Th, Tw, Cs, Csp;
+};
+
+static bool s2d_plan(const ConvDims& d, S2D& z) {
+  if (d.sh != d.sw || d.sh < 2 || d.groups != 1 || d.fsc != 1) return false;
+  if (d.pt || d.pb || d.pl || d.pr) return false;
+  z.s = d.sh;
+  z.U = (d.H + z.s - 1) / z.s;
+  z.V = (d.W + z.s - 1) / z.s;
+  z.Th = (d.fh + z.s - 1) / z.s;
+  z.Tw = (d.fw + z.s - 1) / z.s;
+  if (z.U - z.Th + 1 != d.OH || z.V - z.Tw + 1 != d.OW) return false;
+  z.Cs = z.s * z.s * d.C;
+  z.Csp = rup(z.Cs, 32);
+  return d.K >= 16 && z.Cs >= 16;
+}
+
+static int blocks_for(int64_t total) { return (int)std::min<int64_t>((total + 255) / 256, 148 * 16); }
+
+template <int AK, int BK>
+static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int grid_m,
+                   int grid_n, int grid_z, cudaStream_t s);
+
+static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
+                      const ConvDims& d, const S2D& z, int relu, cudaStream_t s) {
+  TcState* st = state(h);
+  const int taps = z.Th * z.Tw;
+  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * z.U * z.V * z.Csp, s);
+  float* ft = (float*)grow(st->ft, sizeof(float) * (size_t)d.K * taps * z.Csp, s);
+  count_launch(2);
+  s2d_pm_k<<<blocks_for((int64_t)d.N * z.U * z.V * z.Csp), 256, 0, s>>>(
+      x, xt, d.H, d.W, d.C, d.N, z.s, z.U, z.V, z.Cs, z.Csp);
+  s2d_repack_fprop_k<<<blocks_for((int64_t)d.K * taps * z.Csp), 256, 0, s>>>(
+      f, ft, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Tw, z.Csp);
+  GemmParams p{};
+  p.M = d.N * d.OH * d.OW; p.N = d.K; p.K = taps * z.Csp; p.BN = pick_bn(d.K); p.splits = 1;
+  p.OH = d.OH; p.OW = d.OW; p.sh = 1; p.sw = 1; p.pt = 0; p.pl = 0; p.fh = z.Th;
+  p.cchunks = z.Csp / 32;
+  p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+  p.img_stride = (int64_t)d.K * d.OH * d.OW; p.epi_OHW = d.OH * d.OW;
+  p.bias = bias; p.relu = relu; p.n_valid = d.K;
+  CUtensorMap ta = map_im2col(xt, z.Csp, z.U, z.V, d.N, 0, 0, -(z.Th - 1), -(z.Tw - 1), 1, 1, 128);
+  CUtensorMap tb = map_2d(ft, (uint64_t)taps * z.Csp, d.K, (uint64_t)taps * z.Csp, p.BN);
+  launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.K + p.BN - 1) / p.BN, 1, s);
+}
+
+static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, const ConvDims& d,
+                      const S2D& z, int acc, cudaStream_t s) {
+  TcState* st = state(h);
+  const int taps = z.Th * z.Tw;
+  const int Kp = rup(d.K, 32);
+  float* dyt = (float*)grow(st->dyt, sizeof(float) * (size_t)d.N * d.OH * d.OW * Kp, s);
+  float* gt = (float*)grow(st->ft, sizeof(float) * (size_t)z.Cs * taps * Kp, s);
+  to_pm(dy, dyt, d.OH, d.OW, d.K, d.N, d.K, Kp, 1, s);
+  count_launch();
+  s2d_repack_dgrad_k<<<blocks_for((int64_t)z.Cs * taps * Kp), 256, 0, s>>>(
+      f, gt, d.fh, d.fw, d.C, d.K, Kp, z.s, z.Th, z.Tw);
+  GemmParams p{};
+  p.M = d.N * z.U * z.V; p.N = z.Cs; p.K = taps * Kp; p.BN = pick_bn(z.Cs); p.splits = 1;
+  p.OH = z.U; p.OW = z.V; p.sh = 1; p.sw = 1; p.pt = z.Th - 1; p.pl = z.Tw - 1; p.fh = z.Th;
+  p.cchunks = Kp / 32;
+  p.epi = EPI_S2D; p.out = dx; p.epi_OHW = z.U * z.V;
+  p.s2d = z.s; p.s2d_U = z.U; p.s2d_H = d.H; p.s2d_W = d.W; p.s2d_C = d.C;
+  p.acc = acc; p.n_valid = z.Cs;
+  CUtensorMap ta = map_im2col(dyt, Kp, d.OH, d.OW, d.N, -(z.Th - 1), -(z.Tw - 1),
+                              z.U - d.OH - z.Th + 1, z.V - d.OW - z.Tw + 1, 1, 1, 128);
+  CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kp, z.Cs, (uint64_t)taps * Kp, p.BN);
+  launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (z.Cs + p.BN - 1) / p.BN, 1, s);
+}
+
+static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, const ConvDims& d,
+                      const S2D& z, int acc, cudaStream_t s) {
+  TcState* st = state(h);
+  const int taps = z.Th * z.Tw;
+  const int Hp = rup(z.U, 4), Wp = z.V;
+  const int64_t P = (int64_t)d.N * Hp * Wp;
+  const int copies = std::min(4, z.Th);
+  float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)P * z.Cs * copies, s);
+  float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)P * d.K, s);
+  count_launch();
+  s2d_planes_k<<<blocks_for(P * z.Cs * copies), 256, 0, s>>>(x, xp, d.H, d.W, d.C, d.N, z.s, z.U,
+                                                             z.V, Hp, Wp, z.Cs, P, copies);
+  pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, P, 1, s);
+  const int Ntot = taps * z.Csp;
+  const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
+  const int gm = (d.K + 127) / 128, gn = (Ntot + BN - 1) / BN;
+  const int kblocks = (int)((P + 31) / 32);
+  const int splits = split_for(gm * gn, kblocks);
+  const int64_t per = (int64_t)Ntot * d.K;
+  float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
+  GemmParams p{};
+  p.M = d.K; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.splits = splits;
+  p.fh = z.Th; p.Hp = Hp; p.cchunks = z.Csp / 32;
+  p.epi = EPI_LINEAR; p.out = part; p.ld = d.K; p.n_valid = Ntot; p.split_stride = per;
+  CUtensorMap ta = map_2d(dyp, (uint64_t)P, d.K, P, 128);
+  CUtensorMap tb = map_3d_copies(xp, (uint64_t)P, z.Cs, copies, P);
+  launch<OP_TILED_K, OP_SHIFT_K>(ta, tb, p, gm, gn, splits, s);
+  count_launch();
+  s2d_wgrad_finish_k<<<blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s>>>(
+      part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc);
+}
+
 static bool is_fc(const ConvDims& d) {
   return d.OH == 1 && d.OW == 1 && d.fh == d.H && d.fw == d.W && d.pt == 0 && d.pb == 0 &&
          d.pl == 0 && d.pr == 0 && d.groups == 1 && d.fsc == 1;
@@ -770,6 +1010,12 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
       p.out = y;
       launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
     }
+    return true;
+  }
+  if ((d.sh > 1 || d.sw > 1) && d.Cg < 16) {
+    S2D z;
+    if (!s2d_plan(d, z)) return false;
+    s2d_fprop(h, x, f, bias, y, d, z, relu, s);
     return true;
   }
   if (d.Cg < 16 || Kg < 16) return false;
@@ -838,7 +1084,12 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     return true;
   }
   // stride-1 conv of dy with the flipped bank, padding fh-1-pt (SPEC.md:151 adjoint)
-  if (d.sh != 1 || d.sw != 1) return false;
+  if (d.sh != 1 || d.sw != 1) {
+    S2D z;
+    if (!s2d_plan(d, z)) return false;
+    s2d_dgrad(h, dy, f, dx, d, z, acc, s);
+    return true;
+  }
   if (d.Cg < 16 || Kg < 16) return false;
   if (d.pt > d.fh - 1 || d.pb > d.fh - 1 || d.pl > d.fw - 1 || d.pr > d.fw - 1) return false;
   const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
@@ -904,7 +1155,12 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   // Hp is rounded to a multiple of 4 so the shift is fi (mod 4); TMA box
   // starts must be 16-byte aligned, so x is written in min(4, fh) copies
   // pre-shifted by 0..3 elements.
-  if (d.sh != 1 || d.sw != 1) return false;
+  if (d.sh != 1 || d.sw != 1) {
+    S2D z;
+    if (!s2d_plan(d, z)) return false;
+    s2d_wgrad(h, x, dy, df, d, z, acc, s);
+    return true;
+  }
   if (d.Cg < 16 || Kg < 16) return false;
   const int Cgp = rup(d.Cg, 32);
   const int taps = d.fh * d.fw;
