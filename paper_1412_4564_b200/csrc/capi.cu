@@ -322,7 +322,11 @@ ck_status ck_conv_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* f,
   }
   cudaStream_t s = (cudaStream_t)stream;
   ConvDims d = conv_dims(x->shape, f->shape, ys, *g);
-  if (db) conv_bgrad(dy->data, db->data, (int)(ys.h * ys.w), (int)ys.c, (int)ys.n, accumulate, s);
+  if (db) {
+    void* bws = h->scratch.get(conv_bgrad_ws_bytes((int)ys.c, (int)ys.n), s);
+    if (!bws) throw Err(CK_ERR_CUDA, "workspace allocation failed");
+    conv_bgrad(dy->data, db->data, (int)(ys.h * ys.w), (int)ys.c, (int)ys.n, accumulate, bws, s);
+  }
   if (df) conv_wgrad_dispatch(h, x->data, dy->data, df->data, d, accumulate, math, s);
   if (dx) conv_dgrad_dispatch(h, dy->data, f->data, dx->data, d, accumulate, math, s);
   after_launch();

@@ -316,13 +316,17 @@ __global__ void wgrad_reduce_k(const float* __restrict__ part, float* df, ConvDi
   }
 }
 
-// db[k] = sum_n sum_p dy[p, k, n] (conv.cpp:246-252), one block per filter.
-__global__ void bgrad_k(const float* __restrict__ dy, float* db, int OHW, int K, int N, int acc) {
-  const int k = blockIdx.x;
+// db[k] = sum_n sum_p dy[p, k, n] (conv.cpp:246-252).  Grid (K, S): block
+// (k, s) reduces images s, s+S, ... of filter k into partial[s][k] (double);
+// bgrad_finish_k sums the S partials in a fixed order (deterministic).
+__global__ void bgrad_part_k(const float* __restrict__ dy, double* part, int OHW, int K, int N) {
+  const int k = blockIdx.x, s = blockIdx.y, S = gridDim.y;
   double a = 0;
-  for (int n = 0; n < N; ++n) {
+  for (int n = s; n < N; n += S) {
     const float* p = dy + ((int64_t)n * K + k) * OHW;
-    for (int i = threadIdx.x; i < OHW; i += blockDim.x) a += p[i];
+    float f = 0.f;
+    for (int i = threadIdx.x; i < OHW; i += blockDim.x) f += p[i];
+    a += f;
   }
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   __shared__ double red[32];
@@ -331,8 +335,16 @@ __global__ void bgrad_k(const float* __restrict__ dy, float* db, int OHW, int K,
   if (threadIdx.x == 0) {
     double t = 0;
     for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += red[w];
-    db[k] = acc ? db[k] + (float)t : (float)t;
+    part[(int64_t)s * K + k] = t;
   }
+}
+
+__global__ void bgrad_finish_k(const double* part, float* db, int K, int S, int acc) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double t = 0;
+  for (int s = 0; s < S; ++s) t += part[(int64_t)s * K + k];
+  db[k] = acc ? db[k] + (float)t : (float)t;
 }
 
 // Strided dgrad in gather form with the stride-phase decomposition: for dx
@@ -447,9 +459,18 @@ void conv_wgrad_fp32(const float* x, const float* dy, float* df, const ConvDims&
   wgrad_reduce_k<<<blocks, 256, 0, s>>>((const float*)ws, df, d, splits, acc);
 }
 
-void conv_bgrad(const float* dy, float* db, int OHW, int K, int N, int acc, cudaStream_t s) {
-  count_launch();
-  bgrad_k<<<K, 256, 0, s>>>(dy, db, OHW, K, N, acc);
+size_t conv_bgrad_ws_bytes(int K, int N) {
+  return sizeof(double) * (size_t)K * std::min(N, 64);
+}
+
+void conv_bgrad(const float* dy, float* db, int OHW, int K, int N, int acc, void* ws,
+                cudaStream_t s) {
+  // enough blocks to fill the machine ~4x, at most one image per split
+  int S = std::max(1, std::min(N, (148 * 8 + K - 1) / K));
+  S = std::min(S, 64);
+  count_launch(2);
+  bgrad_part_k<<<dim3(K, S), 256, 0, s>>>(dy, (double*)ws, OHW, K, N);
+  bgrad_finish_k<<<(K + 127) / 128, 128, 0, s>>>((const double*)ws, db, K, S, acc);
 }
 
 }  // namespace ck

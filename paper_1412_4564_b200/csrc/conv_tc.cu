@@ -92,6 +92,9 @@ struct GemmParams {
   int b_grp_row;          // OP_SHIFT_K: per-group row (channel) offset
   int s2d, s2d_U, s2d_H, s2d_W, s2d_C;  // EPI_S2D: factor, grid height, target dims
   int exp;                // debug experiments (CK_TC_EXP)
+  int BM;                 // 128 or 256 (two M=128 MMAs sharing the B tile)
+  int nacc;               // TMEM accumulator buffers (2: epilogue overlaps mainloop)
+  int groups;             // tiles = ceil(M/BM) * ceil(N/BN) * groups * splits
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -203,11 +206,41 @@ __device__ __forceinline__ void tc_fence_before() {
       : "r"(taddr));
 
 constexpr int kThreads = 192;
-constexpr int kStageA = 128 * 128;  // 128 rows x 128 B
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Tile decomposition shared by the three roles of a persistent CTA.
+struct Tile {
+  int m0, n0, grp, split, kb0, kb1;
+};
+
+__device__ __forceinline__ Tile tile_at(const GemmParams& p, int t) {
+  Tile r;
+  const int tm = (p.M + p.BM - 1) / p.BM, tn = (p.N + p.BN - 1) / p.BN;
+  const int mt = t % tm;
+  const int rest = t / tm;
+  const int nt = rest % tn;
+  const int z = rest / tn;
+  r.m0 = mt * p.BM;
+  r.n0 = nt * p.BN;
+  r.grp = z / p.splits;
+  r.split = z % p.splits;
+  const int nkb = p.K / 32;
+  const int per = (nkb + p.splits - 1) / p.splits;
+  r.kb0 = r.split * per;
+  r.kb1 = min(nkb, r.kb0 + per);
+  return r;
+}
 
 // ============================================================================
 //                                 the kernel
 // ============================================================================
+// Persistent: CTA b processes tiles b, b + gridDim.x, ...  Each tile is
+// BM (128 or 256, i.e. 1 or 2 M=128 MMAs sharing the B tile) x BN.  The
+// accumulator lives in TMEM, double buffered (nacc = 2) when it fits, so the
+// epilogue of tile i overlaps the mainloop of tile i+1.
 template <int AK, int BK>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
@@ -215,29 +248,33 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = p.stages;
+  const int halves = p.BM / 128;
+  const int stage_a = p.BM * 128;
   const int stage_b = p.BN * 128;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + S * kStageA;
+  uint8_t* sB = smem + S * stage_a;
   uint64_t* full = (uint64_t*)(sB + S * stage_b);
   uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
-  uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
+  uint64_t* tfull = empty + S;       // [nacc]
+  uint64_t* tempty = tfull + 2;      // [nacc]
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.x * 128, n0 = blockIdx.y * p.BN;
-  const int grp = blockIdx.z / p.splits, split = blockIdx.z % p.splits;
-  const int nkb_total = p.K / 32;
-  const int per = (nkb_total + p.splits - 1) / p.splits;
-  const int kb0 = split * per;
-  const int kb1 = min(nkb_total, kb0 + per);
-  const int ncols = p.BN <= 32 ? 32 : p.BN <= 64 ? 64 : p.BN <= 128 ? 128 : 256;
+  const int tm = (p.M + p.BM - 1) / p.BM, tn = (p.N + p.BN - 1) / p.BN;
+  const int total = tm * tn * p.groups * p.splits;
+  const int acc_cols = halves * p.BN;  // TMEM columns per accumulator buffer
+  const int need = p.nacc * acc_cols;
+  const int ncols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_b) : "memory");
@@ -256,46 +293,50 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------------------------------------------------- producer --
     if (lane == 0) {
-      // im2col origin of this M tile (first output pixel)
-      int a_h = 0, a_w = 0, a_n = 0;
-      if (AK == OP_IM2COL_K) {
-        const int ohw = p.OH * p.OW;
-        a_n = m0 / ohw;
-        const int r = m0 - a_n * ohw;
-        a_w = r / p.OH;
-        a_h = r - a_w * p.OH;
-        a_h = a_h * p.sh - p.pt;
-        a_w = a_w * p.sw - p.pl;
-      }
-      const uint32_t bytes = kStageA + stage_b;
-      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
-        const int s = i % S;
-        const uint32_t ph = (i / S) & 1;
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], bytes);
-        uint8_t* a = sA + s * kStageA;
-        uint8_t* b = sB + s * stage_b;
-        const int k0 = kb * 32;
-        // ---- A ----
-        if (AK == OP_TILED_K) {
-          tma_2d(a, &tma_a, &full[s], k0 + grp * p.a_grp_k, m0 + grp * p.a_grp_mn);
-        } else {  // OP_IM2COL_K: kb = tap * cchunks + cc
-          const int tap = kb / p.cchunks, cc = kb - tap * p.cchunks;
-          const int fj = tap / p.fh, fi = tap - fj * p.fh;
-          tma_im2col_4d(a, &tma_a, &full[s], grp * p.a_grp_c + cc * 32, a_h, a_w, a_n,
-                        (uint16_t)fi, (uint16_t)fj);
+      const uint32_t bytes = stage_a + stage_b;
+      int it = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const Tile T = tile_at(p, t);
+        // im2col origin of this M tile (first output pixel)
+        int a_h = 0, a_w = 0, a_n = 0;
+        if (AK == OP_IM2COL_K) {
+          const int ohw = p.OH * p.OW;
+          a_n = T.m0 / ohw;
+          const int r = T.m0 - a_n * ohw;
+          a_w = r / p.OH;
+          a_h = r - a_w * p.OH;
+          a_h = a_h * p.sh - p.pt;
+          a_w = a_w * p.sw - p.pl;
         }
-        // ---- B ----
-        if (BK == OP_TILED_K) {
-          tma_2d(b, &tma_b, &full[s], k0 + grp * p.b_grp_k, n0 + grp * p.b_grp_mn);
-        } else {  // OP_SHIFT_K: rows n = (tap, c), K = padded-grid pixels p'
-          for (int j = 0; j < p.BN / 32; ++j) {
-            const int nn = n0 + 32 * j;
-            const int tap = nn / (p.cchunks * 32);
-            const int c = nn - tap * p.cchunks * 32;
+        for (int kb = T.kb0; kb < T.kb1; ++kb, ++it) {
+          const int s = it % S;
+          const uint32_t ph = (it / S) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], bytes);
+          uint8_t* a = sA + s * stage_a;
+          uint8_t* b = sB + s * stage_b;
+          const int k0 = kb * 32;
+          // ---- A (BM rows) ----
+          if (AK == OP_TILED_K) {
+            tma_2d(a, &tma_a, &full[s], k0 + T.grp * p.a_grp_k, T.m0 + T.grp * p.a_grp_mn);
+          } else {  // OP_IM2COL_K: kb = tap * cchunks + cc; one box walks BM pixels
+            const int tap = kb / p.cchunks, cc = kb - tap * p.cchunks;
             const int fj = tap / p.fh, fi = tap - fj * p.fh;
-            const int shift = fi + p.Hp * fj, r = shift & 3;  // copy r keeps 16-B alignment
-            tma_3d(b + j * 4096, &tma_b, &full[s], k0 + shift - r, grp * p.b_grp_row + c, r);
+            tma_im2col_4d(a, &tma_a, &full[s], T.grp * p.a_grp_c + cc * 32, a_h, a_w, a_n,
+                          (uint16_t)fi, (uint16_t)fj);
+          }
+          // ---- B (BN rows) ----
+          if (BK == OP_TILED_K) {
+            tma_2d(b, &tma_b, &full[s], k0 + T.grp * p.b_grp_k, T.n0 + T.grp * p.b_grp_mn);
+          } else {  // OP_SHIFT_K: rows n = (tap, c), K = padded-grid pixels p'
+            for (int j = 0; j < p.BN / 32; ++j) {
+              const int nn = T.n0 + 32 * j;
+              const int tap = nn / (p.cchunks * 32);
+              const int c = nn - tap * p.cchunks * 32;
+              const int fj = tap / p.fh, fi = tap - fj * p.fh;
+              const int shift = fi + p.Hp * fj, r = shift & 3;  // copy r keeps 16-B alignment
+              tma_3d(b + j * 4096, &tma_b, &full[s], k0 + shift - r, T.grp * p.b_grp_row + c, r);
+            }
           }
         }
       }
@@ -305,95 +346,119 @@ __global__ void __launch_bounds__(kThreads, 1)
     // --------------------------------------------------------- MMA issuer --
     if (lane == 0) {
       const uint32_t idesc = idesc_tf32(p.BN, 0, 0);
-      for (int kb = kb0, i = 0; kb < kb1; ++kb, ++i) {
-        const int s = i % S;
-        const uint32_t ph = (i / S) & 1;
-        mbar_wait(&full[s], ph);
+      int it = 0, tc = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
+        const Tile T = tile_at(p, t);
+        const int ab = tc % p.nacc;
+        const uint32_t aph = (tc / p.nacc) & 1;
+        mbar_wait(&tempty[ab], aph ^ 1);  // epilogue drained this accumulator
         tc_fence_after();
-        const uint32_t a = smem_u32(sA + s * kStageA);
-        const uint32_t b = smem_u32(sB + s * stage_b);
+        const uint32_t dcol = tmem + (uint32_t)(ab * acc_cols);
+        for (int kb = T.kb0; kb < T.kb1; ++kb, ++it) {
+          const int s = it % S;
+          const uint32_t ph = (it / S) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a = smem_u32(sA + s * stage_a);
+          const uint32_t b = smem_u32(sB + s * stage_b);
+          const bool first = kb == T.kb0;
+          for (int h = 0; h < halves; ++h) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          // K-major SW128: K step = +32 B within the 128-B row, SBO = 1024 (8 rows).
-          mma_tf32(tmem, sdesc(a + k * 32, 16, 1024), sdesc(b + k * 32, 16, 1024), idesc,
-                   (i > 0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < 4; ++k) {
+              // K-major SW128: K step = +32 B within the 128-B row, SBO = 1024 (8 rows).
+              mma_tf32(dcol + h * p.BN, sdesc(a + h * 16384 + k * 32, 16, 1024),
+                       sdesc(b + k * 32, 16, 1024), idesc, (!first || k > 0) ? 1u : 0u);
+            }
+          }
+          mma_commit(&empty[s]);
         }
-        mma_commit(&empty[s]);
+        mma_commit(&tfull[ab]);
       }
-      mma_commit(tfull);
     }
     __syncwarp();
   } else {
     // ----------------------------------------------------------- epilogue --
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    const int row = q * 32 + lane;
-    const int m = m0 + row;
-    const bool empty_split = kb0 >= kb1;  // no MMA issued: the tile is zero
-    if (!empty_split) mbar_wait(tfull, 0);
-    tc_fence_after();
-    const bool row_ok = m < p.M;
-    int64_t row_base = 0;
-    float rbias = 0.f;
-    int s_i = 0, s_j = 0;  // EPI_S2D: top-left target pixel of this row's s x s block
-    if (p.epi == EPI_S2D) {
-      const int img = m / p.epi_OHW;
-      const int r = m - img * p.epi_OHW;
-      const int v = r / p.s2d_U, u = r - v * p.s2d_U;
-      s_i = p.s2d * u;
-      s_j = p.s2d * v;
-      row_base = (int64_t)img * p.s2d_C * p.s2d_H * p.s2d_W;
-    } else if (p.epi == EPI_PIX) {
-      const int img = m / p.epi_OHW;
-      const int sp = m - img * p.epi_OHW;
-      row_base = (int64_t)img * p.img_stride + sp + (int64_t)grp * p.grp_col * p.ld;
-    } else {
-      row_base = (int64_t)m + (int64_t)grp * p.grp_out;
-      if (p.bias && p.splits == 1 && row_ok) rbias = p.bias[m + grp * p.grp_col];
-    }
-    float* out = p.out;
-    const bool partial = p.splits > 1;
-    if (partial) out += (int64_t)split * p.split_stride;
-    for (int c0 = 0; c0 < p.BN; c0 += 32) {
-      uint32_t r[32];
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0;
-      CK_LD32(r, taddr);
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (empty_split)
+    int tc = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
+      const Tile T = tile_at(p, t);
+      const int ab = tc % p.nacc;
+      const uint32_t aph = (tc / p.nacc) & 1;
+      const bool empty_split = T.kb0 >= T.kb1;  // no MMA issued: the tile is zero
+      mbar_wait(&tfull[ab], aph);
+      tc_fence_after();
+      float* out = p.out;
+      const bool partial = p.splits > 1;
+      if (partial) out += (int64_t)T.split * p.split_stride;
+      for (int h = 0; h < halves; ++h) {
+        const int m = T.m0 + h * 128 + q * 32 + lane;
+        const bool row_ok = m < p.M;
+        int64_t row_base = 0;
+        float rbias = 0.f;
+        int s_i = 0, s_j = 0;  // EPI_S2D: top-left target pixel of this row's s x s block
+        if (p.epi == EPI_S2D) {
+          const int img = m / p.epi_OHW;
+          const int r = m - img * p.epi_OHW;
+          const int v = r / p.s2d_U, u = r - v * p.s2d_U;
+          s_i = p.s2d * u;
+          s_j = p.s2d * v;
+          row_base = (int64_t)img * p.s2d_C * p.s2d_H * p.s2d_W;
+        } else if (p.epi == EPI_PIX) {
+          const int img = m / p.epi_OHW;
+          const int sp = m - img * p.epi_OHW;
+          row_base = (int64_t)img * p.img_stride + sp + (int64_t)T.grp * p.grp_col * p.ld;
+        } else {
+          row_base = (int64_t)m + (int64_t)T.grp * p.grp_out;
+          if (p.bias && !partial && row_ok) rbias = p.bias[m + T.grp * p.grp_col];
+        }
+        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) +
+                                 (uint32_t)(ab * acc_cols + h * p.BN + c0);
+          CK_LD32(r, taddr);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (empty_split)
 #pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = 0u;
-      if (row_ok) {
+            for (int j = 0; j < 32; ++j) r[j] = 0u;
+          if (row_ok) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int col = n0 + c0 + j;
-          if (col < p.n_valid) {
-            float v = __uint_as_float(r[j]);
-            float* dst;
-            if (p.epi == EPI_S2D) {
-              const int cg = p.s2d_C, ab = col / cg, c = col - ab * cg;
-              const int i = s_i + ab % p.s2d, jj = s_j + ab / p.s2d;
-              if (i >= p.s2d_H || jj >= p.s2d_W) continue;
-              dst = out + row_base + i + (int64_t)p.s2d_H * (jj + (int64_t)p.s2d_W * c);
-            } else {
-              dst = out + row_base + (int64_t)col * p.ld;
-            }
-            if (!partial) {
-              if (p.epi == EPI_PIX) {
-                if (p.bias) v = __fadd_rn(v, p.bias[col + grp * p.grp_col]);
-              } else if (p.bias) {
-                v = __fadd_rn(v, rbias);
+            for (int j = 0; j < 32; ++j) {
+              const int col = T.n0 + c0 + j;
+              if (col < p.n_valid) {
+                float v = __uint_as_float(r[j]);
+                float* dst;
+                if (p.epi == EPI_S2D) {
+                  const int cg = p.s2d_C, abc = col / cg, c = col - abc * cg;
+                  const int i = s_i + abc % p.s2d, jj = s_j + abc / p.s2d;
+                  if (i >= p.s2d_H || jj >= p.s2d_W) continue;
+                  dst = out + row_base + i + (int64_t)p.s2d_H * (jj + (int64_t)p.s2d_W * c);
+                } else {
+                  dst = out + row_base + (int64_t)col * p.ld;
+                }
+                if (!partial) {
+                  if (p.epi == EPI_PIX) {
+                    if (p.bias) v = __fadd_rn(v, p.bias[col + T.grp * p.grp_col]);
+                  } else if (p.bias) {
+                    v = __fadd_rn(v, rbias);
+                  }
+                  if (p.relu) v = v > 0.f ? v : 0.f;
+                  if (p.acc) v = __fadd_rn(*dst, v);
+                }
+                *dst = v;
               }
-              if (p.relu) v = v > 0.f ? v : 0.f;
-              if (p.acc) v = __fadd_rn(*dst, v);
             }
-            *dst = v;
           }
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
+    __syncwarp();
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
   }
@@ -541,27 +606,31 @@ __global__ void transpose_k(const float* __restrict__ in, float* __restrict__ ou
 // `copies` > 1 also writes copy r = 1..copies-1 shifted left by r elements
 // (out[(r*C + c)*ld + q] = plane value at q + r): TMA box starts must be
 // 16-byte aligned, so a tap shift s is served from copy s % 4 at s - s % 4.
+// Grid (column groups, N, copies * C), block (32, 8): threads walk (row ii,
+// column jj) of one padded plane -- no per-element division.  ld == N*Hp*Wp.
 __global__ void pad_planes_k(const float* __restrict__ in, float* __restrict__ out, int H, int W,
                              int Hp, int Wp, int oh, int ow, int C, int N, int64_t ld,
                              int copies) {
-  const int64_t plane = (int64_t)Hp * Wp;
-  const int64_t per_c = plane * N;
-  const int64_t total = ld * C * copies;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rc = e / ld;  // r * C + c
-    const int64_t q = e - rc * ld + rc / C;  // position in the unshifted row
-    const int c = (int)(rc % C);
-    float v = 0.f;
-    if (q < per_c) {
-      const int n = (int)(q / plane);
-      const int r = (int)(q - n * plane);
-      const int j = r / Hp - ow, i = r % Hp - oh;
-      if (i >= 0 && i < H && j >= 0 && j < W)
-        v = in[((int64_t)n * C + c) * H * W + i + (int64_t)H * j];
+  const int rc = blockIdx.z;
+  const int r = rc / C, c = rc - r * C;
+  const int n = blockIdx.y;
+  float* o = out + (int64_t)rc * ld + (int64_t)n * Hp * Wp;
+  for (int jj = blockIdx.x * blockDim.y + threadIdx.y; jj < Wp; jj += gridDim.x * blockDim.y)
+    for (int ii = threadIdx.x; ii < Hp; ii += blockDim.x) {
+      int si = ii + r, sj = jj, sn = n;  // source = flat position + r
+      if (si >= Hp) {
+        si -= Hp;
+        if (++sj >= Wp) {
+          sj = 0;
+          ++sn;
+        }
+      }
+      float v = 0.f;
+      const int i = si - oh, j = sj - ow;
+      if (sn < N && i >= 0 && i < H && j >= 0 && j < W)
+        v = in[((int64_t)sn * C + c) * H * W + i + (int64_t)H * j];
+      o[jj * Hp + ii] = v;
     }
-    out[e] = v;
-  }
 }
 
 // ---- space-to-depth (strided convolutions, e.g. AlexNet conv1 s=4) ---------
@@ -599,23 +668,24 @@ __global__ void s2d_pm_k(const float* __restrict__ x, float* __restrict__ out, i
 __global__ void s2d_planes_k(const float* __restrict__ x, float* __restrict__ out, int H, int W,
                              int C, int N, int s, int U, int V, int Hp, int Wp, int Cs, int64_t ld,
                              int copies) {
-  const int64_t plane = (int64_t)Hp * Wp;
-  const int64_t per_c = plane * N;
-  const int64_t total = ld * Cs * copies;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rc = e / ld;
-    const int64_t q = e - rc * ld + rc / Cs;
-    const int cp = (int)(rc % Cs);
-    float v = 0.f;
-    if (q < per_c) {
-      const int n = (int)(q / plane);
-      const int r = (int)(q - n * plane);
-      const int vv = r / Hp, uu = r % Hp;
-      if (uu < U && vv < V) v = s2d_read(x, H, W, C, s, C, n, uu, vv, cp);
+  const int rc = blockIdx.z;
+  const int r = rc / Cs, cp = rc - r * Cs;
+  const int n = blockIdx.y;
+  float* o = out + (int64_t)rc * ld + (int64_t)n * Hp * Wp;
+  for (int jj = blockIdx.x * blockDim.y + threadIdx.y; jj < Wp; jj += gridDim.x * blockDim.y)
+    for (int ii = threadIdx.x; ii < Hp; ii += blockDim.x) {
+      int si = ii + r, sj = jj, sn = n;
+      if (si >= Hp) {
+        si -= Hp;
+        if (++sj >= Wp) {
+          sj = 0;
+          ++sn;
+        }
+      }
+      float v = 0.f;
+      if (sn < N && si < U && sj < V) v = s2d_read(x, H, W, C, s, C, sn, si, sj, cp);
+      o[jj * Hp + ii] = v;
     }
-    out[e] = v;
-  }
 }
 
 // fprop filters of the s2d conv: fT[k][tap = t + Th*t2][c'p]
@@ -799,12 +869,21 @@ static int pick_bn(int n) {
   return best;
 }
 
+// Tile M: two M=128 MMAs per CTA (sharing each B tile) once M is large.
+static int pick_bm(int64_t M) { return M >= 4096 ? 256 : 128; }
+
 template <int AK, int BK>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int grid_m,
                    int grid_n, int grid_z, cudaStream_t s) {
+  (void)grid_m;
+  (void)grid_n;
   static const int exp = getenv("CK_TC_EXP") ? atoi(getenv("CK_TC_EXP")) : 0;
   p.exp = exp;
-  const int stage_bytes = kStageA + p.BN * 128;
+  if (p.BM != 128 && p.BM != 256) p.BM = 128;
+  p.groups = grid_z / p.splits;
+  const int halves = p.BM / 128;
+  p.nacc = (2 * halves * p.BN <= 512) ? 2 : 1;
+  const int stage_bytes = p.BM * 128 + p.BN * 128;
   const int budget = 227 * 1024 - 1024 - 256;
   p.stages = std::min(8, budget / stage_bytes);
   const size_t smem = 1024 + (size_t)p.stages * stage_bytes + 256;
@@ -814,8 +893,10 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
                          227 * 1024);
     configured = true;
   }
+  const int tiles = ((p.M + p.BM - 1) / p.BM) * ((p.N + p.BN - 1) / p.BN) * grid_z;
+  const int grid = std::min(tiles, 148);
   count_launch();
-  tc_gemm_kernel<AK, BK><<<dim3(grid_m, grid_n, grid_z), kThreads, smem, s>>>(a, b, p);
+  tc_gemm_kernel<AK, BK><<<grid, kThreads, smem, s>>>(a, b, p);
 }
 
 static int split_for(int tiles, int kblocks) {
@@ -850,9 +931,8 @@ static void transpose(const float* in, float* out, int R, int Cc, int64_t ldi, i
 
 static void pad_planes(const float* in, float* out, int H, int W, int Hp, int Wp, int oh, int ow,
                        int C, int N, int64_t ld, int copies, cudaStream_t s) {
-  const int64_t total = ld * C * copies;
   count_launch();
-  pad_planes_k<<<(int)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
+  pad_planes_k<<<dim3((Wp + 7) / 8, N, C * copies), dim3(32, 8), 0, s>>>(
       in, out, H, W, Hp, Wp, oh, ow, C, N, ld, copies);
 }
 
@@ -915,7 +995,8 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.n_valid = d.K;
-  CUtensorMap ta = map_im2col(xt, z.Csp, z.U, z.V, d.N, 0, 0, -(z.Th - 1), -(z.Tw - 1), 1, 1, 128);
+  p.BM = pick_bm(p.M);
+  CUtensorMap ta = map_im2col(xt, z.Csp, z.U, z.V, d.N, 0, 0, -(z.Th - 1), -(z.Tw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(ft, (uint64_t)taps * z.Csp, d.K, (uint64_t)taps * z.Csp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.K + p.BN - 1) / p.BN, 1, s);
 }
@@ -938,8 +1019,9 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   p.epi = EPI_S2D; p.out = dx; p.epi_OHW = z.U * z.V;
   p.s2d = z.s; p.s2d_U = z.U; p.s2d_H = d.H; p.s2d_W = d.W; p.s2d_C = d.C;
   p.acc = acc; p.n_valid = z.Cs;
+  p.BM = pick_bm(p.M);
   CUtensorMap ta = map_im2col(dyt, Kp, d.OH, d.OW, d.N, -(z.Th - 1), -(z.Tw - 1),
-                              z.U - d.OH - z.Th + 1, z.V - d.OW - z.Tw + 1, 1, 1, 128);
+                              z.U - d.OH - z.Th + 1, z.V - d.OW - z.Tw + 1, 1, 1, p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kp, z.Cs, (uint64_t)taps * Kp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (z.Cs + p.BN - 1) / p.BN, 1, s);
 }
@@ -954,8 +1036,8 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)P * z.Cs * copies, s);
   float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)P * d.K, s);
   count_launch();
-  s2d_planes_k<<<blocks_for(P * z.Cs * copies), 256, 0, s>>>(x, xp, d.H, d.W, d.C, d.N, z.s, z.U,
-                                                             z.V, Hp, Wp, z.Cs, P, copies);
+  s2d_planes_k<<<dim3((Wp + 7) / 8, d.N, z.Cs * copies), dim3(32, 8), 0, s>>>(
+      x, xp, d.H, d.W, d.C, d.N, z.s, z.U, z.V, Hp, Wp, z.Cs, P, copies);
   pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, P, 1, s);
   const int Ntot = taps * z.Csp;
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
@@ -968,7 +1050,8 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   p.M = d.K; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.splits = splits;
   p.fh = z.Th; p.Hp = Hp; p.cchunks = z.Csp / 32;
   p.epi = EPI_LINEAR; p.out = part; p.ld = d.K; p.n_valid = Ntot; p.split_stride = per;
-  CUtensorMap ta = map_2d(dyp, (uint64_t)P, d.K, P, 128);
+  p.BM = pick_bm(p.M);
+  CUtensorMap ta = map_2d(dyp, (uint64_t)P, d.K, P, p.BM);
   CUtensorMap tb = map_3d_copies(xp, (uint64_t)P, z.Cs, copies, P);
   launch<OP_TILED_K, OP_SHIFT_K>(ta, tb, p, gm, gn, splits, s);
   count_launch();
@@ -996,7 +1079,8 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
     GemmParams p{};
     p.M = d.K; p.N = d.N; p.K = rup(Q, 32); p.BN = BN; p.splits = splits;
     p.epi = EPI_LINEAR; p.ld = d.K; p.n_valid = d.N; p.relu = relu; p.bias = bias;
-    CUtensorMap ta = map_2d(f, Q, d.K, Q, 128);
+    p.BM = pick_bm(p.M);
+    CUtensorMap ta = map_2d(f, Q, d.K, Q, p.BM);
     CUtensorMap tb = map_2d(x, Q, d.N, Q, BN);
     if (splits > 1) {
       const int64_t per = (int64_t)d.K * d.N;
@@ -1042,8 +1126,9 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
   p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.acc = 0; p.n_valid = Kg;
+  p.BM = pick_bm(p.M);
   CUtensorMap ta = map_im2col(xt, Cp, d.H, d.W, d.N, -d.pt, -d.pl, d.pb - (d.fh - 1),
-                              d.pr - (d.fw - 1), d.sh, d.sw, 128);
+                              d.pr - (d.fw - 1), d.sh, d.sw, p.BM);
   CUtensorMap tb = map_2d(ft, (uint64_t)taps * Cgp, d.K, (uint64_t)taps * Cgp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (Kg + p.BN - 1) / p.BN, d.groups,
                                   s);
@@ -1067,7 +1152,8 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     GemmParams p{};
     p.M = Q; p.N = d.N; p.K = rup(d.K, 32); p.BN = BN; p.splits = splits;
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.N; p.acc = acc;
-    CUtensorMap ta = map_2d(ft, d.K, Q, d.K, 128);   // F^T as [q][k]
+    p.BM = pick_bm(p.M);
+    CUtensorMap ta = map_2d(ft, d.K, Q, d.K, p.BM);   // F^T as [q][k]
     CUtensorMap tb = map_2d(dy, d.K, d.N, d.K, BN);  // dY as [n][k]
     if (splits > 1) {
       const int64_t per = (int64_t)Q * d.N;
@@ -1115,8 +1201,9 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   p.epi = EPI_PIX; p.out = dx; p.ld = (int64_t)d.H * d.W;
   p.img_stride = (int64_t)d.C * d.H * d.W; p.grp_col = d.Cg; p.epi_OHW = d.H * d.W;
   p.bias = nullptr; p.relu = 0; p.acc = acc; p.n_valid = d.Cg;
+  p.BM = pick_bm(p.M);
   CUtensorMap ta = map_im2col(dyt, Kp, d.OH, d.OW, d.N, -qt, -ql, qb - (d.fh - 1),
-                              qr - (d.fw - 1), 1, 1, 128);
+                              qr - (d.fw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kgp, d.C, (uint64_t)taps * Kgp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.Cg + p.BN - 1) / p.BN,
                                   d.groups, s);
@@ -1143,7 +1230,8 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
     GemmParams p{};
     p.M = Q; p.N = d.K; p.K = rup(d.N, 32); p.BN = BN; p.splits = 1;
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.K; p.acc = acc; p.out = df;
-    CUtensorMap ta = map_2d(xt, d.N, Q, Np, 128);
+    p.BM = pick_bm(p.M);
+    CUtensorMap ta = map_2d(xt, d.N, Q, Np, p.BM);
     CUtensorMap tb = map_2d(dyt, d.N, d.K, Np, BN);
     launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
     return true;

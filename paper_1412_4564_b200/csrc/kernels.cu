@@ -204,6 +204,65 @@ __global__ void pool_bwd_k(const float* __restrict__ x, const float* __restrict_
   }
 }
 
+// Plane-tiled variant: one block per (c, n) plane.  The x plane is staged in
+// shared memory, each window's argmax (same first-strict-max rule) is
+// computed ONCE, then every input element gathers its windows in (oj, oi)
+// order -- identical float sums to pool_bwd_k, ~9x fewer loads.
+template <bool kAcc>
+__global__ void pool_bwd_plane_k(const float* __restrict__ x, const float* __restrict__ dy,
+                                 float* dx, PoolDims d) {
+  extern __shared__ float psm[];
+  const int HW = d.H * d.W, OHW = d.OH * d.OW;
+  float* xs = psm;                     // [HW]
+  float* ds = xs + HW;                 // [OHW] dy, or dy/area for avg
+  int* arg = (int*)(ds + OHW);         // [OHW] argmax (max mode)
+  const int64_t plane = blockIdx.x;    // c + C*n
+  const float* xp = x + plane * HW;
+  const float* dyp = dy + plane * OHW;
+  for (int e = threadIdx.x; e < HW; e += blockDim.x) xs[e] = xp[e];
+  __syncthreads();
+  for (int w = threadIdx.x; w < OHW; w += blockDim.x) {
+    const int oi = w % d.OH, oj = w / d.OH;
+    Win b = window_at(d, oi, oj);
+    const float p = dyp[w];
+    if (d.mode == 0) {
+      int best_e = b.i0 + d.H * b.j0;
+      float best = xs[best_e];
+      for (int j = b.j0; j < b.j1; ++j)
+        for (int i = b.i0; i < b.i1; ++i) {
+          float v = xs[i + d.H * j];
+          if (v > best) {
+            best = v;
+            best_e = i + d.H * j;
+          }
+        }
+      arg[w] = best_e;
+      ds[w] = p;
+    } else {
+      float area = (float)((b.i1 - b.i0) * (b.j1 - b.j0));
+      ds[w] = __fdiv_rn(p, area);
+    }
+  }
+  __syncthreads();
+  float* dxp = dx + plane * HW;
+  for (int e = threadIdx.x; e < HW; e += blockDim.x) {
+    const int i = e % d.H, j = e / d.H;
+    int oi_lo = i + d.pt - d.wh + 1;
+    oi_lo = oi_lo <= 0 ? 0 : (oi_lo + d.sh - 1) / d.sh;
+    const int oi_hi = min(d.OH - 1, (i + d.pt) / d.sh);
+    int oj_lo = j + d.pl - d.ww + 1;
+    oj_lo = oj_lo <= 0 ? 0 : (oj_lo + d.sw - 1) / d.sw;
+    const int oj_hi = min(d.OW - 1, (j + d.pl) / d.sw);
+    float acc = 0.f;
+    for (int oj = oj_lo; oj <= oj_hi; ++oj)
+      for (int oi = oi_lo; oi <= oi_hi; ++oi) {
+        const int w = oi + d.OH * oj;
+        if (d.mode != 0 || arg[w] == e) acc = __fadd_rn(acc, ds[w]);
+      }
+    dxp[e] = kAcc ? __fadd_rn(dxp[e], acc) : acc;
+  }
+}
+
 // ----------------------------------------------------------------- LRN ----
 // normalize.cpp:18-22 lrn_group: [k - (n-1)/2, k + n-1-(n-1)/2] clipped.
 // A block owns kLrnPix consecutive pixels of one image and stages all their
@@ -620,6 +679,23 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
   int64_t total = (int64_t)d.H * d.W * d.C * d.N;
   if (total == 0) return;
   count_launch();
+  const size_t smem = sizeof(float) * ((size_t)d.H * d.W + 2 * (size_t)d.OH * d.OW);
+  if (smem <= 96 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(pool_bwd_plane_k<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           96 * 1024);
+      cudaFuncSetAttribute(pool_bwd_plane_k<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           96 * 1024);
+      configured = true;
+    }
+    const unsigned planes = (unsigned)((int64_t)d.C * d.N);
+    if (acc)
+      pool_bwd_plane_k<true><<<planes, 256, smem, s>>>(x, dy, dx, d);
+    else
+      pool_bwd_plane_k<false><<<planes, 256, smem, s>>>(x, dy, dx, d);
+    return;
+  }
   if (acc)
     pool_bwd_k<true><<<blocks_for(total, 256), 256, 0, s>>>(x, dy, dx, d);
   else
