@@ -53,8 +53,9 @@ namespace tc {
 enum OpKind : int {
   OP_TILED_K = 0,     // 2D tensor (K inner, MN outer), box (32, rows)
   OP_IM2COL_K = 2,    // 4D im2col over a pixel-major tensor, box 128 px x 32 ch
-  OP_SHIFT_K = 4,     // wgrad B: boxes (32 px, 32 ch) of a channel-major padded
-                      // tensor, K coordinate shifted by the tap: p' + fi + Hp*fj
+  OP_SHIFT_K = 4,     // wgrad B: boxes (32 px, 32 ch, 1, 1) of padded planes
+                      // [copy][n][c][PL], pixel coordinate shifted by the tap
+  OP_PLANE_K = 5,     // wgrad A: box (32 px, rows, 1) of padded planes [n][k][PL]
 };
 
 enum EpiKind : int {
@@ -95,6 +96,7 @@ struct GemmParams {
   int BM;                 // 128 or 256 (two M=128 MMAs sharing the B tile)
   int nacc;               // TMEM accumulator buffers (2: epilogue overlaps mainloop)
   int groups;             // tiles = ceil(M/BM) * ceil(N/BN) * groups * splits
+  int kpp;                // OP_PLANE_K / OP_SHIFT_K: K blocks (32 px) per image plane
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -129,6 +131,15 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 
@@ -319,6 +330,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           // ---- A (BM rows) ----
           if (AK == OP_TILED_K) {
             tma_2d(a, &tma_a, &full[s], k0 + T.grp * p.a_grp_k, T.m0 + T.grp * p.a_grp_mn);
+          } else if (AK == OP_PLANE_K) {
+            const int n = kb / p.kpp, q0 = (kb - n * p.kpp) * 32;
+            tma_3d(a, &tma_a, &full[s], q0, T.m0 + T.grp * p.a_grp_mn, n);
           } else {  // OP_IM2COL_K: kb = tap * cchunks + cc; one box walks BM pixels
             const int tap = kb / p.cchunks, cc = kb - tap * p.cchunks;
             const int fj = tap / p.fh, fi = tap - fj * p.fh;
@@ -328,14 +342,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           // ---- B (BN rows) ----
           if (BK == OP_TILED_K) {
             tma_2d(b, &tma_b, &full[s], k0 + T.grp * p.b_grp_k, T.n0 + T.grp * p.b_grp_mn);
-          } else {  // OP_SHIFT_K: rows n = (tap, c), K = padded-grid pixels p'
+          } else {  // OP_SHIFT_K: rows n = (tap, c), K = pixels of image plane img
+            const int img = kb / p.kpp, q0 = (kb - img * p.kpp) * 32;
             for (int j = 0; j < p.BN / 32; ++j) {
               const int nn = T.n0 + 32 * j;
               const int tap = nn / (p.cchunks * 32);
               const int c = nn - tap * p.cchunks * 32;
               const int fj = tap / p.fh, fi = tap - fj * p.fh;
               const int shift = fi + p.Hp * fj, r = shift & 3;  // copy r keeps 16-B alignment
-              tma_3d(b + j * 4096, &tma_b, &full[s], k0 + shift - r, T.grp * p.b_grp_row + c, r);
+              tma_4d(b + j * 4096, &tma_b, &full[s], q0 + shift - r, T.grp * p.b_grp_row + c,
+                     img, r);
             }
           }
         }
@@ -600,37 +616,30 @@ __global__ void transpose_k(const float* __restrict__ in, float* __restrict__ ou
   }
 }
 
-// Channel-major padded planes for the wgrad operands: out[c][n][Wp][Hp] holds
-// in[n][c][W][H] at offset (oh, ow) and zeros elsewhere (zero padding for x,
-// zero "junk" rows/columns of the padded output grid for dy).
-// `copies` > 1 also writes copy r = 1..copies-1 shifted left by r elements
-// (out[(r*C + c)*ld + q] = plane value at q + r): TMA box starts must be
-// 16-byte aligned, so a tap shift s is served from copy s % 4 at s - s % 4.
-// Grid (column groups, N, copies * C), block (32, 8): threads walk (row ii,
-// column jj) of one padded plane -- no per-element division.  ld == N*Hp*Wp.
+// Padded planes for the wgrad operands, layout [copy][n][c][PL] (PL = Hp*Wp
+// rounded up to 32): plane (n, c) holds in[n][c][W][H] at offset (oh, ow),
+// zeros elsewhere (zero padding for x, zero "junk" rows/columns of the output
+// grid for dy).  Copy r is the plane shifted left by r elements: TMA box
+// starts must be 16-byte aligned, so a tap shift t is read from copy t % 4 at
+// t - t % 4.  Grid (ceil(PL/256), C, copies*N).
 __global__ void pad_planes_k(const float* __restrict__ in, float* __restrict__ out, int H, int W,
-                             int Hp, int Wp, int oh, int ow, int C, int N, int64_t ld,
-                             int copies) {
-  const int rc = blockIdx.z;
-  const int r = rc / C, c = rc - r * C;
-  const int n = blockIdx.y;
-  float* o = out + (int64_t)rc * ld + (int64_t)n * Hp * Wp;
-  for (int jj = blockIdx.x * blockDim.y + threadIdx.y; jj < Wp; jj += gridDim.x * blockDim.y)
-    for (int ii = threadIdx.x; ii < Hp; ii += blockDim.x) {
-      int si = ii + r, sj = jj, sn = n;  // source = flat position + r
-      if (si >= Hp) {
-        si -= Hp;
-        if (++sj >= Wp) {
-          sj = 0;
-          ++sn;
-        }
-      }
-      float v = 0.f;
-      const int i = si - oh, j = sj - ow;
-      if (sn < N && i >= 0 && i < H && j >= 0 && j < W)
-        v = in[((int64_t)sn * C + c) * H * W + i + (int64_t)H * j];
-      o[jj * Hp + ii] = v;
+                             int Hp, int Wp, int oh, int ow, int C, int N, int PL) {
+  const int c = blockIdx.y;
+  const int rn = blockIdx.z;
+  const int r = rn / N, n = rn - r * N;
+  const float* src = in + ((int64_t)n * C + c) * H * W;
+  float* o = out + ((int64_t)rn * C + c) * PL;
+  const int plane = Hp * Wp;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < PL; q += gridDim.x * blockDim.x) {
+    const int pos = q + r;
+    float v = 0.f;
+    if (pos < plane) {
+      const int jj = pos / Hp, ii = pos - jj * Hp;
+      const int i = ii - oh, j = jj - ow;
+      if (i >= 0 && i < H && j >= 0 && j < W) v = src[i + (int64_t)H * j];
     }
+    o[q] = v;
+  }
 }
 
 // ---- space-to-depth (strided convolutions, e.g. AlexNet conv1 s=4) ---------
@@ -663,29 +672,23 @@ __global__ void s2d_pm_k(const float* __restrict__ x, float* __restrict__ out, i
   }
 }
 
-// channel-major padded copies of the s2d tensor (wgrad B operand), same
-// conventions as pad_planes_k: out[(r*Cs + c')*ld + q] = plane value at q + r.
+// Padded planes of the s2d tensor, same layout and copies as pad_planes_k.
 __global__ void s2d_planes_k(const float* __restrict__ x, float* __restrict__ out, int H, int W,
-                             int C, int N, int s, int U, int V, int Hp, int Wp, int Cs, int64_t ld,
-                             int copies) {
-  const int rc = blockIdx.z;
-  const int r = rc / Cs, cp = rc - r * Cs;
-  const int n = blockIdx.y;
-  float* o = out + (int64_t)rc * ld + (int64_t)n * Hp * Wp;
-  for (int jj = blockIdx.x * blockDim.y + threadIdx.y; jj < Wp; jj += gridDim.x * blockDim.y)
-    for (int ii = threadIdx.x; ii < Hp; ii += blockDim.x) {
-      int si = ii + r, sj = jj, sn = n;
-      if (si >= Hp) {
-        si -= Hp;
-        if (++sj >= Wp) {
-          sj = 0;
-          ++sn;
-        }
-      }
-      float v = 0.f;
-      if (sn < N && si < U && sj < V) v = s2d_read(x, H, W, C, s, C, sn, si, sj, cp);
-      o[jj * Hp + ii] = v;
+                             int C, int N, int s, int U, int V, int Hp, int Wp, int Cs, int PL) {
+  const int cp = blockIdx.y;
+  const int rn = blockIdx.z;
+  const int r = rn / N, n = rn - r * N;
+  float* o = out + ((int64_t)rn * Cs + cp) * PL;
+  const int plane = Hp * Wp;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < PL; q += gridDim.x * blockDim.x) {
+    const int pos = q + r;
+    float v = 0.f;
+    if (pos < plane) {
+      const int vv = pos / Hp, uu = pos - vv * Hp;
+      if (uu < U && vv < V) v = s2d_read(x, H, W, C, s, C, n, uu, vv, cp);
     }
+    o[q] = v;
+  }
 }
 
 // fprop filters of the s2d conv: fT[k][tap = t + Th*t2][c'p]
@@ -908,6 +911,15 @@ static int split_for(int tiles, int kblocks) {
   return s;
 }
 
+// wgrad: reductions over ~1e5-1e6 pixels; split so every SM has ~2 tiles.
+static int wgrad_splits_for(int tiles, int kblocks) {
+  static const int force = getenv("CK_TC_SPLITS") ? atoi(getenv("CK_TC_SPLITS")) : 0;
+  if (force > 0) return std::min(force, std::max(1, kblocks));
+  int sp = (2 * 148 + tiles - 1) / tiles;
+  sp = std::min(sp, std::max(1, kblocks / 16));
+  return std::max(1, std::min(sp, 64));
+}
+
 static void* grow(Workspace& w, size_t bytes, cudaStream_t s) {
   void* p = w.get(bytes, s);
   if (!p) throw Err(CK_ERR_CUDA, "workspace allocation failed");
@@ -930,26 +942,40 @@ static void transpose(const float* in, float* out, int R, int Cc, int64_t ldi, i
 }
 
 static void pad_planes(const float* in, float* out, int H, int W, int Hp, int Wp, int oh, int ow,
-                       int C, int N, int64_t ld, int copies, cudaStream_t s) {
+                       int C, int N, int PL, int copies, cudaStream_t s) {
   count_launch();
-  pad_planes_k<<<dim3((Wp + 7) / 8, N, C * copies), dim3(32, 8), 0, s>>>(
-      in, out, H, W, Hp, Wp, oh, ow, C, N, ld, copies);
+  pad_planes_k<<<dim3((PL + 255) / 256, C, copies * N), 256, 0, s>>>(in, out, H, W, Hp, Wp, oh,
+                                                                      ow, C, N, PL);
 }
 
-// 3D tiled map over copies of a channel-major [copy][row][ld] tensor, box (32, 32, 1).
-static CUtensorMap map_3d_copies(const float* base, uint64_t inner, uint64_t rows,
-                                 uint64_t copies, uint64_t ld_elems) {
+static CUtensorMap encode_tiled(const float* base, int rank, const cuuint64_t* dims,
+                                const cuuint64_t* strides_bytes, const cuuint32_t* box) {
   CUtensorMap m;
-  cuuint64_t dims[3] = {inner, rows, copies};
-  cuuint64_t strides[2] = {ld_elems * 4, ld_elems * rows * 4};
-  cuuint32_t box[3] = {32, 32, 1};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = g_encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides,
-                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, (void*)base, dims,
+                              strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw Err(CK_ERR_CUDA, "cuTensorMapEncodeTiled (3d) failed");
+  if (r != CUDA_SUCCESS)
+    throw Err(CK_ERR_CUDA, "cuTensorMapEncodeTiled (rank " + std::to_string(rank) + ") failed");
   return m;
+}
+
+// wgrad A: planes [n][rows][PL], box (32 px, box_rows, 1)
+static CUtensorMap map_planes(const float* base, int PL, int rows, int N, int box_rows) {
+  cuuint64_t dims[3] = {(cuuint64_t)PL, (cuuint64_t)rows, (cuuint64_t)N};
+  cuuint64_t strides[2] = {(cuuint64_t)PL * 4, (cuuint64_t)PL * rows * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+  return encode_tiled(base, 3, dims, strides, box);
+}
+
+// wgrad B: shifted copies [copy][n][c][PL], box (32 px, 32 ch, 1, 1)
+static CUtensorMap map_plane_copies(const float* base, int PL, int C, int N, int copies) {
+  cuuint64_t dims[4] = {(cuuint64_t)PL, (cuuint64_t)C, (cuuint64_t)N, (cuuint64_t)copies};
+  cuuint64_t strides[3] = {(cuuint64_t)PL * 4, (cuuint64_t)PL * C * 4,
+                           (cuuint64_t)PL * C * N * 4};
+  cuuint32_t box[4] = {32, 32, 1, 1};
+  return encode_tiled(base, 4, dims, strides, box);
 }
 
 // ---- space-to-depth path for strided convolutions --------------------------
@@ -1031,29 +1057,28 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   TcState* st = state(h);
   const int taps = z.Th * z.Tw;
   const int Hp = rup(z.U, 4), Wp = z.V;
-  const int64_t P = (int64_t)d.N * Hp * Wp;
+  const int PL = rup(Hp * Wp, 32);
   const int copies = std::min(4, z.Th);
-  float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)P * z.Cs * copies, s);
-  float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)P * d.K, s);
+  float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)PL * d.N * z.Cs * copies, s);
+  float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)PL * d.N * d.K, s);
   count_launch();
-  s2d_planes_k<<<dim3((Wp + 7) / 8, d.N, z.Cs * copies), dim3(32, 8), 0, s>>>(
-      x, xp, d.H, d.W, d.C, d.N, z.s, z.U, z.V, Hp, Wp, z.Cs, P, copies);
-  pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, P, 1, s);
+  s2d_planes_k<<<dim3((PL + 255) / 256, z.Cs, copies * d.N), 256, 0, s>>>(
+      x, xp, d.H, d.W, d.C, d.N, z.s, z.U, z.V, Hp, Wp, z.Cs, PL);
+  pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, PL, 1, s);
   const int Ntot = taps * z.Csp;
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
-  const int gm = (d.K + 127) / 128, gn = (Ntot + BN - 1) / BN;
-  const int kblocks = (int)((P + 31) / 32);
-  const int splits = split_for(gm * gn, kblocks);
+  const int BM = pick_bm(d.K);
+  const int kblocks = d.N * (PL / 32);
+  const int splits = wgrad_splits_for(((d.K + BM - 1) / BM) * ((Ntot + BN - 1) / BN), kblocks);
   const int64_t per = (int64_t)Ntot * d.K;
   float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
   GemmParams p{};
-  p.M = d.K; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.splits = splits;
-  p.fh = z.Th; p.Hp = Hp; p.cchunks = z.Csp / 32;
+  p.M = d.K; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.BM = BM; p.splits = splits;
+  p.fh = z.Th; p.Hp = Hp; p.cchunks = z.Csp / 32; p.kpp = PL / 32;
   p.epi = EPI_LINEAR; p.out = part; p.ld = d.K; p.n_valid = Ntot; p.split_stride = per;
-  p.BM = pick_bm(p.M);
-  CUtensorMap ta = map_2d(dyp, (uint64_t)P, d.K, P, p.BM);
-  CUtensorMap tb = map_3d_copies(xp, (uint64_t)P, z.Cs, copies, P);
-  launch<OP_TILED_K, OP_SHIFT_K>(ta, tb, p, gm, gn, splits, s);
+  CUtensorMap ta = map_planes(dyp, PL, d.K, d.N, BM);
+  CUtensorMap tb = map_plane_copies(xp, PL, z.Cs, d.N, copies);
+  launch<OP_PLANE_K, OP_SHIFT_K>(ta, tb, p, 0, 0, splits, s);
   count_launch();
   s2d_wgrad_finish_k<<<blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s>>>(
       part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc);
@@ -1253,26 +1278,26 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   const int Cgp = rup(d.Cg, 32);
   const int taps = d.fh * d.fw;
   const int Hp = rup(d.H + d.pt + d.pb, 4), Wp = d.W + d.pl + d.pr;
-  const int64_t P = (int64_t)d.N * Hp * Wp;
-  if (P + 128 > INT32_MAX) return false;
-  const int64_t ldp = P;  // multiple of 4 since Hp is
+  const int PL = rup(Hp * Wp, 32);
+  if ((int64_t)PL * d.N * std::max(d.C, d.K) * 4 > INT32_MAX) return false;
   const int copies = std::min(4, d.fh);
   TcState* st = state(h);
-  float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)ldp * d.C * copies, s);
-  float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)ldp * d.K, s);
-  pad_planes(x, xp, d.H, d.W, Hp, Wp, d.pt, d.pl, d.C, d.N, ldp, copies, s);
-  pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, ldp, 1, s);
+  float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)PL * d.N * d.C * copies, s);
+  float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)PL * d.N * d.K, s);
+  pad_planes(x, xp, d.H, d.W, Hp, Wp, d.pt, d.pl, d.C, d.N, PL, copies, s);
+  pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, PL, 1, s);
   const int Ntot = taps * Cgp;  // GEMM N = (tap, c) per group
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
-  const int gm = (Kg + 127) / 128, gn = (Ntot + BN - 1) / BN;
-  const int kblocks = (int)((P + 31) / 32);
-  const int splits = split_for(gm * gn * d.groups, kblocks);
+  const int BM = pick_bm(Kg);
+  const int kblocks = d.N * (PL / 32);
+  const int splits = wgrad_splits_for(
+      ((Kg + BM - 1) / BM) * ((Ntot + BN - 1) / BN) * d.groups, kblocks);
   const int64_t per_grp = (int64_t)Ntot * Kg;
   const int64_t per = per_grp * d.groups;
   float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
   GemmParams p{};
-  p.M = Kg; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.splits = splits;
-  p.fh = d.fh; p.Hp = Hp;
+  p.M = Kg; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.BM = BM; p.splits = splits;
+  p.fh = d.fh; p.Hp = Hp; p.kpp = PL / 32;
   p.cchunks = Cgp / 32;
   p.a_grp_mn = Kg;
   p.b_grp_row = d.Cg;
@@ -1280,19 +1305,9 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   p.epi = EPI_LINEAR; p.out = part; p.ld = Kg; p.grp_out = per_grp; p.n_valid = Ntot;
   p.split_stride = per;
   p.bias = nullptr; p.relu = 0; p.acc = 0;
-  CUtensorMap ta = map_2d(dyp, (uint64_t)P, d.K, ldp, 128);  // rows k, K = p'
-  CUtensorMap tb = map_3d_copies(xp, (uint64_t)P, d.C, copies, ldp);  // [copy][c][p']
-  static const int dbg = getenv("CK_TC_DBG") ? atoi(getenv("CK_TC_DBG")) : 0;
-  if (dbg & 4) {
-    cudaError_t e = cudaStreamSynchronize(s);
-    fprintf(stderr, "[wgrad] before gemm: %s  P=%lld ldp=%lld BN=%d gm=%d gn=%d splits=%d K=%d\n",
-            cudaGetErrorString(e), (long long)P, (long long)ldp, BN, gm, gn, splits, p.K);
-  }
-  if (!(dbg & 1)) launch<OP_TILED_K, OP_SHIFT_K>(ta, tb, p, gm, gn, d.groups * splits, s);
-  if (dbg & 4) {
-    cudaError_t e = cudaStreamSynchronize(s);
-    fprintf(stderr, "[wgrad] after gemm: %s\n", cudaGetErrorString(e));
-  }
+  CUtensorMap ta = map_planes(dyp, PL, d.K, d.N, BM);            // rows k, K = plane pixels
+  CUtensorMap tb = map_plane_copies(xp, PL, d.C, d.N, copies);   // rows c, shifted by tap
+  launch<OP_PLANE_K, OP_SHIFT_K>(ta, tb, p, 0, 0, d.groups * splits, s);
   const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
   count_launch();
   wgrad_finish_k<<<std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
