@@ -324,9 +324,18 @@ __global__ void bgrad_part_k(const float* __restrict__ dy, double* part, int OHW
   double a = 0;
   for (int n = s; n < N; n += S) {
     const float* p = dy + ((int64_t)n * K + k) * OHW;
-    float f = 0.f;
-    for (int i = threadIdx.x; i < OHW; i += blockDim.x) f += p[i];
-    a += f;
+    // four independent accumulators keep 4 loads in flight per thread
+    float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f;
+    const int step = blockDim.x;
+    int i = threadIdx.x;
+    for (; i + 3 * step < OHW; i += 4 * step) {
+      f0 += p[i];
+      f1 += p[i + step];
+      f2 += p[i + 2 * step];
+      f3 += p[i + 3 * step];
+    }
+    for (; i < OHW; i += step) f0 += p[i];
+    a += (double)((f0 + f1) + (f2 + f3));
   }
   for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
   __shared__ double red[32];
@@ -466,7 +475,7 @@ size_t conv_bgrad_ws_bytes(int K, int N) {
 void conv_bgrad(const float* dy, float* db, int OHW, int K, int N, int acc, void* ws,
                 cudaStream_t s) {
   // enough blocks to fill the machine ~4x, at most one image per split
-  int S = std::max(1, std::min(N, (148 * 8 + K - 1) / K));
+  int S = std::max(1, std::min(N, (148 * 32 + K - 1) / K));
   S = std::min(S, 64);
   count_launch(2);
   bgrad_part_k<<<dim3(K, S), 256, 0, s>>>(dy, (double*)ws, OHW, K, N);

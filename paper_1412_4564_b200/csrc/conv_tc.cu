@@ -642,6 +642,42 @@ __global__ void pad_planes_k(const float* __restrict__ in, float* __restrict__ o
   }
 }
 
+// Same result as pad_planes_k, one block per (n, c) source plane: the plane is
+// read once into shared memory and all `copies` shifted planes are written
+// from it with coalesced stores (no per-element division).
+__global__ void pad_planes_smem_k(const float* __restrict__ in, float* __restrict__ out, int H,
+                                  int W, int Hp, int Wp, int oh, int ow, int C, int N, int PL,
+                                  int copies) {
+  extern __shared__ float pl_src[];
+  const int64_t nc = blockIdx.x;  // n * C + c
+  const int n = (int)(nc / C), c = (int)(nc - (int64_t)n * C);
+  const float* src = in + nc * H * W;
+  for (int e = threadIdx.x; e < H * W; e += blockDim.x) pl_src[e] = src[e];
+  __syncthreads();
+  const int plane = Hp * Wp;
+  const int si = blockDim.x % Hp, sj = blockDim.x / Hp;  // (ii, jj) step of q += blockDim
+  for (int r = 0; r < copies; ++r) {
+    float* o = out + (((int64_t)r * N + n) * C + c) * PL;
+    int pos = threadIdx.x + r;
+    int jj = pos / Hp, ii = pos - jj * Hp;
+    for (int q = threadIdx.x; q < PL; q += blockDim.x) {
+      float v = 0.f;
+      if (pos < plane) {
+        const int i = ii - oh, j = jj - ow;
+        if (i >= 0 && i < H && j >= 0 && j < W) v = pl_src[i + H * j];
+      }
+      o[q] = v;
+      pos += blockDim.x;
+      ii += si;
+      jj += sj;
+      if (ii >= Hp) {
+        ii -= Hp;
+        ++jj;
+      }
+    }
+  }
+}
+
 // ---- space-to-depth (strided convolutions, e.g. AlexNet conv1 s=4) ---------
 // A stride-s conv equals a stride-1 conv over x_s2d[u][v][c'] =
 // x[s*u + a, s*v + b, c], c' = c + Cg*(a + s*b), with taps (t, t2) and filter
@@ -944,6 +980,12 @@ static void transpose(const float* in, float* out, int R, int Cc, int64_t ldi, i
 static void pad_planes(const float* in, float* out, int H, int W, int Hp, int Wp, int oh, int ow,
                        int C, int N, int PL, int copies, cudaStream_t s) {
   count_launch();
+  const size_t smem = sizeof(float) * (size_t)H * W;
+  if (smem <= 48 * 1024) {
+    pad_planes_smem_k<<<(unsigned)((int64_t)N * C), 256, smem, s>>>(in, out, H, W, Hp, Wp, oh, ow,
+                                                                  C, N, PL, copies);
+    return;
+  }
   pad_planes_k<<<dim3((PL + 255) / 256, C, copies * N), 256, 0, s>>>(in, out, H, W, Hp, Wp, oh,
                                                                       ow, C, N, PL);
 }
