@@ -260,11 +260,11 @@ def main():
     inputs = net.init_inputs(data_seed=1 + rank, label_seed=3 + rank)
     for k, v in inputs.items():
         g.set(k, v)
-    tr = Trainer(g, lr=1e-3, momentum=0.9, weight_decay=5e-4)
+    # cnn_train scales the step by the batch: the loss is a SUM over images
+    tr = Trainer(g, lr=0.01 / args.batch, momentum=0.9, weight_decay=5e-4)
     if world > 1:
-        uid = [Trainer.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        tr.init_dp(uid[0], rank, world)
+        from paper_1412_4564_b200 import dp
+        tr.init_dp(dp.share_unique_id(Trainer.unique_id, rank), rank, world)
     stream = torch.cuda.Stream()
     sp = stream.cuda_stream
 
