@@ -909,7 +909,9 @@ static int pick_bn(int n) {
 }
 
 // Tile M: two M=128 MMAs per CTA (sharing each B tile) once M is large.
-static int pick_bm(int64_t M) { return M >= 4096 ? 256 : 128; }
+// Keep TMEM double-buffered (2 x BM/128 x BN <= 512 columns) so the epilogue
+// of one tile overlaps the next tile's mainloop.
+static int pick_bm(int64_t M, int BN) { return (M >= 4096 && BN <= 128) ? 256 : 128; }
 
 template <int AK, int BK>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int grid_m,
@@ -1063,7 +1065,7 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.n_valid = d.K;
-  p.BM = pick_bm(p.M);
+  p.BM = pick_bm(p.M, p.BN);
   CUtensorMap ta = map_im2col(xt, z.Csp, z.U, z.V, d.N, 0, 0, -(z.Th - 1), -(z.Tw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(ft, (uint64_t)taps * z.Csp, d.K, (uint64_t)taps * z.Csp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.K + p.BN - 1) / p.BN, 1, s);
@@ -1087,7 +1089,7 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   p.epi = EPI_S2D; p.out = dx; p.epi_OHW = z.U * z.V;
   p.s2d = z.s; p.s2d_U = z.U; p.s2d_H = d.H; p.s2d_W = d.W; p.s2d_C = d.C;
   p.acc = acc; p.n_valid = z.Cs;
-  p.BM = pick_bm(p.M);
+  p.BM = pick_bm(p.M, p.BN);
   CUtensorMap ta = map_im2col(dyt, Kp, d.OH, d.OW, d.N, -(z.Th - 1), -(z.Tw - 1),
                               z.U - d.OH - z.Th + 1, z.V - d.OW - z.Tw + 1, 1, 1, p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kp, z.Cs, (uint64_t)taps * Kp, p.BN);
@@ -1109,7 +1111,7 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, PL, 1, s);
   const int Ntot = taps * z.Csp;
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
-  const int BM = pick_bm(d.K);
+  const int BM = pick_bm(d.K, BN);
   const int kblocks = d.N * (PL / 32);
   const int splits = wgrad_splits_for(((d.K + BM - 1) / BM) * ((Ntot + BN - 1) / BN), kblocks);
   const int64_t per = (int64_t)Ntot * d.K;
@@ -1146,7 +1148,7 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
     GemmParams p{};
     p.M = d.K; p.N = d.N; p.K = rup(Q, 32); p.BN = BN; p.splits = splits;
     p.epi = EPI_LINEAR; p.ld = d.K; p.n_valid = d.N; p.relu = relu; p.bias = bias;
-    p.BM = pick_bm(p.M);
+    p.BM = pick_bm(p.M, p.BN);
     CUtensorMap ta = map_2d(f, Q, d.K, Q, p.BM);
     CUtensorMap tb = map_2d(x, Q, d.N, Q, BN);
     if (splits > 1) {
@@ -1193,7 +1195,7 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
   p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.acc = 0; p.n_valid = Kg;
-  p.BM = pick_bm(p.M);
+  p.BM = pick_bm(p.M, p.BN);
   CUtensorMap ta = map_im2col(xt, Cp, d.H, d.W, d.N, -d.pt, -d.pl, d.pb - (d.fh - 1),
                               d.pr - (d.fw - 1), d.sh, d.sw, p.BM);
   CUtensorMap tb = map_2d(ft, (uint64_t)taps * Cgp, d.K, (uint64_t)taps * Cgp, p.BN);
@@ -1219,7 +1221,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     GemmParams p{};
     p.M = Q; p.N = d.N; p.K = rup(d.K, 32); p.BN = BN; p.splits = splits;
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.N; p.acc = acc;
-    p.BM = pick_bm(p.M);
+    p.BM = pick_bm(p.M, p.BN);
     CUtensorMap ta = map_2d(ft, d.K, Q, d.K, p.BM);   // F^T as [q][k]
     CUtensorMap tb = map_2d(dy, d.K, d.N, d.K, BN);  // dY as [n][k]
     if (splits > 1) {
@@ -1268,7 +1270,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   p.epi = EPI_PIX; p.out = dx; p.ld = (int64_t)d.H * d.W;
   p.img_stride = (int64_t)d.C * d.H * d.W; p.grp_col = d.Cg; p.epi_OHW = d.H * d.W;
   p.bias = nullptr; p.relu = 0; p.acc = acc; p.n_valid = d.Cg;
-  p.BM = pick_bm(p.M);
+  p.BM = pick_bm(p.M, p.BN);
   CUtensorMap ta = map_im2col(dyt, Kp, d.OH, d.OW, d.N, -qt, -ql, qb - (d.fh - 1),
                               qr - (d.fw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kgp, d.C, (uint64_t)taps * Kgp, p.BN);
@@ -1297,7 +1299,7 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
     GemmParams p{};
     p.M = Q; p.N = d.K; p.K = rup(d.N, 32); p.BN = BN; p.splits = 1;
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.K; p.acc = acc; p.out = df;
-    p.BM = pick_bm(p.M);
+    p.BM = pick_bm(p.M, p.BN);
     CUtensorMap ta = map_2d(xt, d.N, Q, Np, p.BM);
     CUtensorMap tb = map_2d(dyt, d.N, d.K, Np, BN);
     launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
@@ -1330,7 +1332,7 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, PL, 1, s);
   const int Ntot = taps * Cgp;  // GEMM N = (tap, c) per group
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
-  const int BM = pick_bm(Kg);
+  const int BM = pick_bm(Kg, BN);
   const int kblocks = d.N * (PL / 32);
   const int splits = wgrad_splits_for(
       ((Kg + BM - 1) / BM) * ((Ntot + BN - 1) / BN) * d.groups, kblocks);

@@ -345,6 +345,120 @@ __global__ void lrn_bwd_k(const float* __restrict__ x, const float* __restrict__
   }
 }
 
+// Register-streaming LRN for group sizes 1..9: one thread per pixel walks the
+// channels (coalesced across threads), holding the channel window in
+// compile-time-indexed shift registers.  Out-of-range window slots hold 0,
+// and 0 + a == a exactly, so every sum is performed in the reference's
+// order (normalize.cpp:55-62, :85-111) and matches lrn_fwd_k / lrn_bwd_k.
+template <int NW>
+__global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y, int HW, int C,
+                              int64_t pixels, float kappa, float alpha, float nbeta) {
+  constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pixels;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = e / HW;
+    const int p = (int)(e - n * HW);
+    const float* xp = x + n * C * HW + p;
+    float* yp = y + n * C * HW + p;
+    float sq[NW], xv[NW];  // window k-DOWN .. k+UP
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      const int t = i - DOWN;
+      const float v = (t >= 0 && t < C) ? xp[(int64_t)t * HW] : 0.f;
+      xv[i] = v;
+      sq[i] = __fmul_rn(v, v);
+    }
+    for (int k = 0; k < C; ++k) {
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
+      const float scale = powf(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
+      yp[(int64_t)k * HW] = __fmul_rn(xv[DOWN], scale);
+      const int t = k + UP + 1;
+      const float v = t < C ? xp[(int64_t)t * HW] : 0.f;
+#pragma unroll
+      for (int i = 0; i < NW - 1; ++i) {
+        sq[i] = sq[i + 1];
+        xv[i] = xv[i + 1];
+      }
+      xv[NW - 1] = v;
+      sq[NW - 1] = __fmul_rn(v, v);
+    }
+  }
+}
+
+template <int NW, bool kAcc>
+__global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
+                              int HW, int C, int64_t pixels, float kappa, float alpha, float beta) {
+  constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
+  const float nb1 = -beta - 1.f, nb = -beta;
+  const float c2ab = __fmul_rn(__fmul_rn(2.f, alpha), beta);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pixels;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = e / HW;
+    const int p = (int)(e - n * HW);
+    const int64_t base = n * C * HW + p;
+    const float* xp = x + base;
+    const float* gp = dy + base;
+    float* dp = dx + base;
+    // squares for the lead index j: sq[i] = x[j - DOWN + i]^2
+    float sq[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      const int t = i - DOWN;
+      const float v = (t >= 0 && t < C) ? xp[(int64_t)t * HW] : 0.f;
+      sq[i] = __fmul_rn(v, v);
+    }
+    float eta[NW];  // eta of indices j-NW+1 .. j (0 outside [0, C))
+    float Ls[DOWN + 1], xs[DOWN + 1], gs[DOWN + 1];  // indices j-DOWN .. j
+#pragma unroll
+    for (int i = 0; i < NW; ++i) eta[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i <= DOWN; ++i) Ls[i] = xs[i] = gs[i] = 0.f;
+    for (int j = 0; j < C + DOWN; ++j) {
+      float L = 0.f, xj = 0.f, gj = 0.f, et = 0.f;
+      if (j < C) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
+        L = __fadd_rn(kappa, __fmul_rn(alpha, acc));
+        xj = xp[(int64_t)j * HW];
+        gj = gp[(int64_t)j * HW];
+        et = __fmul_rn(__fmul_rn(gj, powf(L, nb1)), xj);
+      }
+#pragma unroll
+      for (int i = 0; i < NW - 1; ++i) eta[i] = eta[i + 1];
+      eta[NW - 1] = et;
+#pragma unroll
+      for (int i = 0; i < DOWN; ++i) {
+        Ls[i] = Ls[i + 1];
+        xs[i] = xs[i + 1];
+        gs[i] = gs[i + 1];
+      }
+      Ls[DOWN] = L;
+      xs[DOWN] = xj;
+      gs[DOWN] = gj;
+      const int d = j - DOWN;
+      if (d >= 0) {
+        // k in [d-UP, d+DOWN] = [j-NW+1, j]: the whole eta window, ascending
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, eta[i]);
+        const float r = __fadd_rn(__fmul_rn(gs[0], powf(Ls[0], nb)),
+                                  -__fmul_rn(__fmul_rn(c2ab, xs[0]), acc));
+        float* o = dp + (int64_t)d * HW;
+        *o = kAcc ? __fadd_rn(*o, r) : r;
+      }
+      // advance the square window to lead index j + 1
+      const int t = j + UP + 1;
+      const float v = t < C ? xp[(int64_t)t * HW] : 0.f;
+#pragma unroll
+      for (int i = 0; i < NW - 1; ++i) sq[i] = sq[i + 1];
+      sq[NW - 1] = __fmul_rn(v, v);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- bnorm ---
 // Per-channel moments over H*W*N (normalize.cpp:132-161).  Grid (C, splits):
 // each block reduces a contiguous run of images of one channel in double and
@@ -714,23 +828,63 @@ static void lrn_smem_check(int C, int arrays) {
   }
 }
 
+template <int NW>
+static void lrn_fwd_reg(const float* x, float* y, int HW, int C, int N, float kappa, float alpha,
+                        float beta, cudaStream_t s) {
+  const int64_t pixels = (int64_t)HW * N;
+  lrn_fwd_reg_k<NW><<<blocks_for(pixels, 128, 32), 128, 0, s>>>(x, y, HW, C, pixels, kappa, alpha,
+                                                                 -beta);
+}
+
+template <int NW>
+static void lrn_bwd_reg(const float* x, const float* dy, float* dx, int HW, int C, int N,
+                        float kappa, float alpha, float beta, int acc, cudaStream_t s) {
+  const int64_t pixels = (int64_t)HW * N;
+  if (acc)
+    lrn_bwd_reg_k<NW, true><<<blocks_for(pixels, 128, 32), 128, 0, s>>>(x, dy, dx, HW, C, pixels,
+                                                                         kappa, alpha, beta);
+  else
+    lrn_bwd_reg_k<NW, false><<<blocks_for(pixels, 128, 32), 128, 0, s>>>(x, dy, dx, HW, C, pixels,
+                                                                          kappa, alpha, beta);
+}
+
+#define CK_LRN_SWITCH(size, CALL) \
+  switch (size) {                 \
+    case 1: CALL(1); return;      \
+    case 2: CALL(2); return;      \
+    case 3: CALL(3); return;      \
+    case 4: CALL(4); return;      \
+    case 5: CALL(5); return;      \
+    case 6: CALL(6); return;      \
+    case 7: CALL(7); return;      \
+    case 8: CALL(8); return;      \
+    case 9: CALL(9); return;      \
+    default: break;               \
+  }
+
 void lrn_forward(const float* x, float* y, int H, int W, int C, int N, int size, float kappa,
                  float alpha, float beta, cudaStream_t s) {
   const int HW = H * W;
+  count_launch();
+#define CK_FWD(NW) lrn_fwd_reg<NW>(x, y, HW, C, N, kappa, alpha, beta, s)
+  CK_LRN_SWITCH(size, CK_FWD)
+#undef CK_FWD
   dim3 grid((HW + kLrnPix - 1) / kLrnPix, N);
   size_t smem = (size_t)C * kLrnPix * sizeof(float);
   lrn_smem_check(C, 1);
-  count_launch();
   lrn_fwd_k<<<grid, 256, smem, s>>>(x, y, HW, C, size, kappa, alpha, -beta);
 }
 
 void lrn_backward(const float* x, const float* dy, float* dx, int H, int W, int C, int N, int size,
                   float kappa, float alpha, float beta, int acc, cudaStream_t s) {
   const int HW = H * W;
+  count_launch();
+#define CK_BWD(NW) lrn_bwd_reg<NW>(x, dy, dx, HW, C, N, kappa, alpha, beta, acc, s)
+  CK_LRN_SWITCH(size, CK_BWD)
+#undef CK_BWD
   dim3 grid((HW + kLrnPix - 1) / kLrnPix, N);
   size_t smem = (size_t)3 * C * kLrnPix * sizeof(float);
   lrn_smem_check(C, 3);
-  count_launch();
   if (acc)
     lrn_bwd_k<true><<<grid, 256, smem, s>>>(x, dy, dx, HW, C, size, kappa, alpha, beta);
   else
