@@ -35,6 +35,7 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <numeric>
 
 #include "ck_handle.hpp"
 #include "ck_internal.hpp"
@@ -97,6 +98,7 @@ struct GemmParams {
   int nacc;               // TMEM accumulator buffers (2: epilogue overlaps mainloop)
   int groups;             // tiles = ceil(M/BM) * ceil(N/BN) * groups * splits
   int kpp;                // OP_PLANE_K / OP_SHIFT_K: K blocks (32 px) per image plane
+  int b_rows;             // OP_SHIFT_K: channel rows per TMA box (divides Cgp and BN)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -344,14 +346,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_2d(b, &tma_b, &full[s], k0 + T.grp * p.b_grp_k, T.n0 + T.grp * p.b_grp_mn);
           } else {  // OP_SHIFT_K: rows n = (tap, c), K = pixels of image plane img
             const int img = kb / p.kpp, q0 = (kb - img * p.kpp) * 32;
-            for (int j = 0; j < p.BN / 32; ++j) {
-              const int nn = T.n0 + 32 * j;
+            for (int j = 0; j < p.BN / p.b_rows; ++j) {
+              const int nn = T.n0 + p.b_rows * j;
               const int tap = nn / (p.cchunks * 32);
               const int c = nn - tap * p.cchunks * 32;
               const int fj = tap / p.fh, fi = tap - fj * p.fh;
               const int shift = fi + p.Hp * fj, r = shift & 3;  // copy r keeps 16-B alignment
-              tma_4d(b + j * 4096, &tma_b, &full[s], q0 + shift - r, T.grp * p.b_grp_row + c,
-                     img, r);
+              tma_4d(b + j * p.b_rows * 128, &tma_b, &full[s], q0 + shift - r,
+                     T.grp * p.b_grp_row + c, img, r);
             }
           }
         }
@@ -678,6 +680,49 @@ __global__ void pad_planes_smem_k(const float* __restrict__ in, float* __restric
   }
 }
 
+// Same result again, P planes per block.  Planes nc0..nc0+P-1 are contiguous
+// in the source and, for every copy r, in the output ([copy][n*C + c][PL]),
+// so a block streams P*H*W floats in and P*PL floats per copy out (float4
+// stores).  A per-block table maps a padded-plane position to its source
+// offset (-1 = zero), which removes the per-element division.
+__global__ void pad_planes_multi_k(const float* __restrict__ in, float* __restrict__ out, int H,
+                                   int W, int Hp, int Wp, int oh, int ow, int64_t NC, int PL,
+                                   int copies, int P) {
+  extern __shared__ float sm_pp[];
+  int* tbl = reinterpret_cast<int*>(sm_pp);  // PL + 4 entries
+  float* src = sm_pp + PL + 4;
+  const int HW = H * W, plane = Hp * Wp;
+  const int64_t nc0 = (int64_t)blockIdx.x * P;
+  const int np = (int)(NC - nc0 < P ? NC - nc0 : P);
+  for (int q = threadIdx.x; q < PL + 4; q += blockDim.x) {
+    int v = -1;
+    if (q < plane) {
+      const int jj = q / Hp, ii = q - jj * Hp;
+      const int i = ii - oh, j = jj - ow;
+      if (i >= 0 && i < H && j >= 0 && j < W) v = i + H * j;
+    }
+    tbl[q] = v;
+  }
+  const float* s = in + nc0 * HW;
+  for (int e = threadIdx.x; e < np * HW; e += blockDim.x) src[e] = __ldg(s + e);
+  __syncthreads();
+  const int n4 = np * PL / 4;
+  for (int r = 0; r < copies; ++r) {
+    float4* o = reinterpret_cast<float4*>(out + ((int64_t)r * NC + nc0) * PL);
+    for (int e4 = threadIdx.x; e4 < n4; e4 += blockDim.x) {
+      const int e = e4 * 4, p = e / PL, q = e - p * PL + r;
+      const float* sp = src + p * HW;
+      int t;
+      float4 v;
+      t = tbl[q];     v.x = t >= 0 ? sp[t] : 0.f;
+      t = tbl[q + 1]; v.y = t >= 0 ? sp[t] : 0.f;
+      t = tbl[q + 2]; v.z = t >= 0 ? sp[t] : 0.f;
+      t = tbl[q + 3]; v.w = t >= 0 ? sp[t] : 0.f;
+      o[e4] = v;
+    }
+  }
+}
+
 // ---- space-to-depth (strided convolutions, e.g. AlexNet conv1 s=4) ---------
 // A stride-s conv equals a stride-1 conv over x_s2d[u][v][c'] =
 // x[s*u + a, s*v + b, c], c' = c + Cg*(a + s*b), with taps (t, t2) and filter
@@ -705,6 +750,94 @@ __global__ void s2d_pm_k(const float* __restrict__ x, float* __restrict__ out, i
     const int v = (int)(r % V);
     const int n = (int)(r / V);
     out[e] = cp < Cs ? s2d_read(x, H, W, C, s, C, n, u, v, cp) : 0.f;
+  }
+}
+
+// Strip-staged s2d transforms.  A block stages x columns [s*v0, s*(v0+VB))
+// of one or all channels of image n in shared memory (row pitch Hs = s*U >=
+// H, zero past the edges), so every global read is a coalesced column read
+// and every write a contiguous run of the output.
+__device__ __forceinline__ void s2d_stage_strip(const float* __restrict__ x, float* strip, int H,
+                                                int W, int c_first, int c_count, int C, int n,
+                                                int j0, int cols, int Hs) {
+  const int per = Hs * cols;
+  for (int e = threadIdx.x; e < c_count * per; e += blockDim.x) {
+    const int cc = e / per, rem = e - cc * per;
+    const int jl = rem / Hs, i = rem - jl * Hs, j = j0 + jl;
+    strip[e] = (i < H && j < W)
+                   ? __ldg(x + (((int64_t)n * C + c_first + cc) * W + j) * H + i)
+                   : 0.f;
+  }
+}
+
+// pixel-major s2d tensor [n][v][u][c'p]; block = (v strip of VB columns, n)
+__global__ void s2d_pm_strip_k(const float* __restrict__ x, float* __restrict__ out, int H, int W,
+                               int C, int s, int U, int V, int Cs, int Csp, int VB) {
+  extern __shared__ float strip_pm[];
+  const int n = blockIdx.y, v0 = blockIdx.x * VB;
+  const int vb = min(VB, V - v0);
+  const int Hs = s * U;
+  s2d_stage_strip(x, strip_pm, H, W, 0, C, C, n, s * v0, s * vb, Hs);
+  __syncthreads();
+  const int per_c = Hs * s * vb;
+  const int c4 = Csp / 4, total = vb * U * c4;
+  float4* o = reinterpret_cast<float4*>(out + (((int64_t)n * V + v0) * U) * Csp);
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    const int cq = e % c4, pix = e / c4;
+    const int vl = pix / U, u = pix - vl * U;
+    float r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int cp = cq * 4 + k;
+      float v = 0.f;
+      if (cp < Cs) {
+        const int c = cp % C, ab = cp / C, a = ab % s, b = ab / s;
+        v = strip_pm[c * per_c + (s * u + a) + Hs * (s * vl + b)];
+      }
+      r[k] = v;
+    }
+    o[e] = make_float4(r[0], r[1], r[2], r[3]);
+  }
+}
+
+// padded s2d planes [copy][n][c'][PL] (c' < Cs), block = (v strip, c, n)
+__global__ void s2d_planes_strip_k(const float* __restrict__ x, float* __restrict__ out, int H,
+                                   int W, int C, int N, int s, int U, int V, int Hp, int Wp,
+                                   int Cs, int PL, int copies, int VB) {
+  extern __shared__ float strip_pl[];
+  const int c = blockIdx.y, n = blockIdx.z, v0 = blockIdx.x * VB;
+  const int vb = min(VB, Wp - v0);
+  const int Hs = s * U;
+  int* tbl = reinterpret_cast<int*>(strip_pl);  // VB*Hp entries
+  float* strip = strip_pl + VB * Hp;
+  for (int l = threadIdx.x; l < vb * Hp; l += blockDim.x) {
+    const int vl = l / Hp, uu = l - vl * Hp;
+    tbl[l] = (uu < U && v0 + vl < V) ? s * uu + Hs * s * vl : -1;
+  }
+  s2d_stage_strip(x, strip, H, W, c, 1, C, n, s * v0, s * vb, Hs);
+  __syncthreads();
+  const int pos0 = v0 * Hp, len = vb * Hp;
+  const bool last = v0 + vb >= Wp;
+  const int planes = s * s;
+  for (int r = 0; r < copies; ++r) {
+    // positions [pos0, pos0 + len) land at q = pos - r (q >= 0)
+    const int skip = pos0 - r < 0 ? r - pos0 : 0;
+    const int span = len - skip;
+    for (int e = threadIdx.x; e < planes * span; e += blockDim.x) {
+      const int ab = e / span, l = e - ab * span + skip;
+      const int a = ab % s, b = ab / s;
+      const int t = tbl[l];
+      const float v = t >= 0 ? strip[t + a + Hs * b] : 0.f;
+      const int cp = c + C * ab;
+      out[(((int64_t)r * N + n) * Cs + cp) * PL + pos0 + l - r] = v;
+    }
+    if (last) {  // zero tail q in [Hp*Wp - r, PL)
+      const int t0 = Hp * Wp - r, tl = PL - t0;
+      for (int e = threadIdx.x; e < planes * tl; e += blockDim.x) {
+        const int ab = e / tl, q = t0 + (e - ab * tl);
+        out[(((int64_t)r * N + n) * Cs + c + C * ab) * PL + q] = 0.f;
+      }
+    }
   }
 }
 
@@ -950,12 +1083,24 @@ static int split_for(int tiles, int kblocks) {
 }
 
 // wgrad: reductions over ~1e5-1e6 pixels; split so every SM has ~2 tiles.
+// Split-K factor for the wgrad GEMMs: minimise the persistent kernel's
+// makespan, waves * (K blocks per split + a per-tile fill/epilogue cost of
+// ~24 K blocks), over splits that keep >= 16 K blocks per split.
 static int wgrad_splits_for(int tiles, int kblocks) {
   static const int force = getenv("CK_TC_SPLITS") ? atoi(getenv("CK_TC_SPLITS")) : 0;
   if (force > 0) return std::min(force, std::max(1, kblocks));
-  int sp = (2 * 148 + tiles - 1) / tiles;
-  sp = std::min(sp, std::max(1, kblocks / 16));
-  return std::max(1, std::min(sp, 64));
+  const int max_sp = std::max(1, std::min(64, kblocks / 16));
+  int best = 1;
+  int64_t best_cost = INT64_MAX;
+  for (int sp = 1; sp <= max_sp; ++sp) {
+    const int64_t waves = ((int64_t)tiles * sp + 147) / 148;
+    const int64_t cost = waves * ((kblocks + sp - 1) / sp + 24);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
+  return best;
 }
 
 static void* grow(Workspace& w, size_t bytes, cudaStream_t s) {
@@ -983,6 +1128,14 @@ static void pad_planes(const float* in, float* out, int H, int W, int Hp, int Wp
                        int C, int N, int PL, int copies, cudaStream_t s) {
   count_launch();
   const size_t smem = sizeof(float) * (size_t)H * W;
+  const size_t tbl = sizeof(float) * (size_t)(PL + 4);
+  if (tbl + smem <= 40 * 1024) {
+    const int64_t NC = (int64_t)N * C;
+    const int P = (int)std::min<int64_t>({64, NC, (int64_t)((40 * 1024 - tbl) / smem)});
+    pad_planes_multi_k<<<(unsigned)((NC + P - 1) / P), 256, tbl + P * smem, s>>>(
+        in, out, H, W, Hp, Wp, oh, ow, NC, PL, copies, P);
+    return;
+  }
   if (smem <= 48 * 1024) {
     pad_planes_smem_k<<<(unsigned)((int64_t)N * C), 256, smem, s>>>(in, out, H, W, Hp, Wp, oh, ow,
                                                                   C, N, PL, copies);
@@ -1014,11 +1167,12 @@ static CUtensorMap map_planes(const float* base, int PL, int rows, int N, int bo
 }
 
 // wgrad B: shifted copies [copy][n][c][PL], box (32 px, 32 ch, 1, 1)
-static CUtensorMap map_plane_copies(const float* base, int PL, int C, int N, int copies) {
+static CUtensorMap map_plane_copies(const float* base, int PL, int C, int N, int copies,
+                                    int rows) {
   cuuint64_t dims[4] = {(cuuint64_t)PL, (cuuint64_t)C, (cuuint64_t)N, (cuuint64_t)copies};
   cuuint64_t strides[3] = {(cuuint64_t)PL * 4, (cuuint64_t)PL * C * 4,
                            (cuuint64_t)PL * C * N * 4};
-  cuuint32_t box[4] = {32, 32, 1, 1};
+  cuuint32_t box[4] = {32, (cuuint32_t)rows, 1, 1};
   return encode_tiled(base, 4, dims, strides, box);
 }
 
@@ -1054,8 +1208,14 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * z.U * z.V * z.Csp, s);
   float* ft = (float*)grow(st->ft, sizeof(float) * (size_t)d.K * taps * z.Csp, s);
   count_launch(2);
-  s2d_pm_k<<<blocks_for((int64_t)d.N * z.U * z.V * z.Csp), 256, 0, s>>>(
-      x, xt, d.H, d.W, d.C, d.N, z.s, z.U, z.V, z.Cs, z.Csp);
+  const int col_bytes = (int)sizeof(float) * d.C * z.s * z.U * z.s;  // one s2d column, all c
+  const int VB = std::min(z.V, (44 * 1024) / col_bytes);
+  if (VB >= 1)
+    s2d_pm_strip_k<<<dim3((z.V + VB - 1) / VB, d.N), 256, (size_t)VB * col_bytes, s>>>(
+        x, xt, d.H, d.W, d.C, z.s, z.U, z.V, z.Cs, z.Csp, VB);
+  else
+    s2d_pm_k<<<blocks_for((int64_t)d.N * z.U * z.V * z.Csp), 256, 0, s>>>(
+        x, xt, d.H, d.W, d.C, d.N, z.s, z.U, z.V, z.Cs, z.Csp);
   s2d_repack_fprop_k<<<blocks_for((int64_t)d.K * taps * z.Csp), 256, 0, s>>>(
       f, ft, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Tw, z.Csp);
   GemmParams p{};
@@ -1106,8 +1266,16 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)PL * d.N * z.Cs * copies, s);
   float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)PL * d.N * d.K, s);
   count_launch();
-  s2d_planes_k<<<dim3((PL + 255) / 256, z.Cs, copies * d.N), 256, 0, s>>>(
-      x, xp, d.H, d.W, d.C, d.N, z.s, z.U, z.V, Hp, Wp, z.Cs, PL);
+  {
+    const int col_bytes = (int)sizeof(float) * (z.s * z.U * z.s + Hp);  // strip + table
+    const int VB = std::min(Wp, (40 * 1024) / col_bytes);
+    if (VB >= 1)
+      s2d_planes_strip_k<<<dim3((Wp + VB - 1) / VB, d.C, d.N), 256, (size_t)VB * col_bytes, s>>>(
+          x, xp, d.H, d.W, d.C, d.N, z.s, z.U, z.V, Hp, Wp, z.Cs, PL, copies, VB);
+    else
+      s2d_planes_k<<<dim3((PL + 255) / 256, z.Cs, copies * d.N), 256, 0, s>>>(
+          x, xp, d.H, d.W, d.C, d.N, z.s, z.U, z.V, Hp, Wp, z.Cs, PL);
+  }
   pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, PL, 1, s);
   const int Ntot = taps * z.Csp;
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
@@ -1119,9 +1287,10 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   GemmParams p{};
   p.M = d.K; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.BM = BM; p.splits = splits;
   p.fh = z.Th; p.Hp = Hp; p.cchunks = z.Csp / 32; p.kpp = PL / 32;
+  p.b_rows = std::gcd(z.Csp, BN);
   p.epi = EPI_LINEAR; p.out = part; p.ld = d.K; p.n_valid = Ntot; p.split_stride = per;
   CUtensorMap ta = map_planes(dyp, PL, d.K, d.N, BM);
-  CUtensorMap tb = map_plane_copies(xp, PL, z.Cs, d.N, copies);
+  CUtensorMap tb = map_plane_copies(xp, PL, z.Cs, d.N, copies, p.b_rows);
   launch<OP_PLANE_K, OP_SHIFT_K>(ta, tb, p, 0, 0, splits, s);
   count_launch();
   s2d_wgrad_finish_k<<<blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s>>>(
@@ -1343,6 +1512,7 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   p.M = Kg; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.BM = BM; p.splits = splits;
   p.fh = d.fh; p.Hp = Hp; p.kpp = PL / 32;
   p.cchunks = Cgp / 32;
+  p.b_rows = std::gcd(Cgp, BN);
   p.a_grp_mn = Kg;
   p.b_grp_row = d.Cg;
   // raw partials: part[s*per + g*per_grp + n*Kg + k]
@@ -1350,7 +1520,7 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   p.split_stride = per;
   p.bias = nullptr; p.relu = 0; p.acc = 0;
   CUtensorMap ta = map_planes(dyp, PL, d.K, d.N, BM);            // rows k, K = plane pixels
-  CUtensorMap tb = map_plane_copies(xp, PL, d.C, d.N, copies);   // rows c, shifted by tap
+  CUtensorMap tb = map_plane_copies(xp, PL, d.C, d.N, copies, p.b_rows);   // rows c, shifted by tap
   launch<OP_PLANE_K, OP_SHIFT_K>(ta, tb, p, 0, 0, d.groups * splits, s);
   const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
   count_launch();
