@@ -323,7 +323,7 @@ ck_status ck_conv_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* f,
   cudaStream_t s = (cudaStream_t)stream;
   ConvDims d = conv_dims(x->shape, f->shape, ys, *g);
   if (db) {
-    void* bws = h->scratch.get(conv_bgrad_ws_bytes((int)ys.c, (int)ys.n), s);
+    void* bws = h->scratch.get(conv_bgrad_ws_bytes((int)ys.c, (int)ys.n, (int)(ys.h * ys.w)), s);
     if (!bws) throw Err(CK_ERR_CUDA, "workspace allocation failed");
     conv_bgrad(dy->data, db->data, (int)(ys.h * ys.w), (int)ys.c, (int)ys.n, accumulate, bws, s);
   }

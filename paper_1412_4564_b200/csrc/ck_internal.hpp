@@ -101,7 +101,7 @@ void conv_dgrad_fp32(const float* dy, const float* f, float* dx, const ConvDims&
 size_t conv_wgrad_ws_bytes(const ConvDims& d);
 void conv_wgrad_fp32(const float* x, const float* dy, float* df, const ConvDims& d, int acc,
                      void* ws, cudaStream_t s);
-size_t conv_bgrad_ws_bytes(int K, int N);
+size_t conv_bgrad_ws_bytes(int K, int N, int OHW);
 void conv_bgrad(const float* dy, float* db, int OHW, int K, int N, int acc, void* ws,
                 cudaStream_t s);
 

@@ -316,44 +316,45 @@ __global__ void wgrad_reduce_k(const float* __restrict__ part, float* df, ConvDi
   }
 }
 
-// db[k] = sum_n sum_p dy[p, k, n] (conv.cpp:246-252).  Grid (K, S): block
-// (k, s) reduces images s, s+S, ... of filter k into partial[s][k] (double);
-// bgrad_finish_k sums the S partials in a fixed order (deterministic).
-__global__ void bgrad_part_k(const float* __restrict__ dy, double* part, int OHW, int K, int N) {
-  const int k = blockIdx.x, s = blockIdx.y, S = gridDim.y;
-  double a = 0;
-  for (int n = s; n < N; n += S) {
-    const float* p = dy + ((int64_t)n * K + k) * OHW;
-    // four independent accumulators keep 4 loads in flight per thread
-    float f0 = 0.f, f1 = 0.f, f2 = 0.f, f3 = 0.f;
-    const int step = blockDim.x;
-    int i = threadIdx.x;
-    for (; i + 3 * step < OHW; i += 4 * step) {
-      f0 += p[i];
-      f1 += p[i + step];
-      f2 += p[i + 2 * step];
-      f3 += p[i + 3 * step];
+// db[k] = sum_n sum_p dy[p, k, n] (conv.cpp:246-252).  Each image's dy is
+// K*OHW contiguous floats, so thread j of [0, K*OHW) sums element j over the
+// images of its split (n = s, s+S, ...) with perfectly coalesced loads and
+// four images in flight; bgrad_finish_k then reduces the S*OHW partials of
+// channel k in a fixed order (deterministic, double accumulation).
+__global__ void bgrad_part_k(const float* __restrict__ dy, double* part, int64_t KP, int N) {
+  const int s = blockIdx.y, S = gridDim.y;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < KP;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const float* p = dy + j;
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    int n = s;
+    for (; n + 3 * S < N; n += 4 * S) {
+      const float v0 = __ldg(p + (int64_t)n * KP), v1 = __ldg(p + (int64_t)(n + S) * KP);
+      const float v2 = __ldg(p + (int64_t)(n + 2 * S) * KP), v3 = __ldg(p + (int64_t)(n + 3 * S) * KP);
+      a0 += v0; a1 += v1; a2 += v2; a3 += v3;
     }
-    for (; i < OHW; i += step) f0 += p[i];
-    a += (double)((f0 + f1) + (f2 + f3));
-  }
-  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-  __shared__ double red[32];
-  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = a;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0;
-    for (int w = 0; w < (int)(blockDim.x / 32); ++w) t += red[w];
-    part[(int64_t)s * K + k] = t;
+    for (; n < N; n += S) a0 += __ldg(p + (int64_t)n * KP);
+    part[(int64_t)s * KP + j] = (a0 + a1) + (a2 + a3);
   }
 }
 
-__global__ void bgrad_finish_k(const double* part, float* db, int K, int S, int acc) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
+__global__ void bgrad_finish_k(const double* part, float* db, int K, int OHW, int S, int acc) {
+  const int k = blockIdx.x;
+  const int64_t KP = (int64_t)K * OHW;
   double t = 0;
-  for (int s = 0; s < S; ++s) t += part[(int64_t)s * K + k];
-  db[k] = acc ? db[k] + (float)t : (float)t;
+  for (int e = threadIdx.x; e < S * OHW; e += blockDim.x) {
+    const int sp = e / OHW, q = e - sp * OHW;
+    t += part[sp * KP + (int64_t)k * OHW + q];
+  }
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __shared__ double red[32];
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) u += red[w];
+    db[k] = acc ? db[k] + (float)u : (float)u;
+  }
 }
 
 // Strided dgrad in gather form with the stride-phase decomposition: for dx
@@ -468,18 +469,25 @@ void conv_wgrad_fp32(const float* x, const float* dy, float* df, const ConvDims&
   wgrad_reduce_k<<<blocks, 256, 0, s>>>((const float*)ws, df, d, splits, acc);
 }
 
-size_t conv_bgrad_ws_bytes(int K, int N) {
-  return sizeof(double) * (size_t)K * std::min(N, 64);
+static int bgrad_splits(int64_t KP, int N) {
+  // ~148 SMs x 2048 threads in flight; at most one image per split
+  const int64_t want = (148 * 2048 + KP - 1) / KP;
+  return (int)std::max<int64_t>(1, std::min<int64_t>({want, (int64_t)N, 64}));
+}
+
+size_t conv_bgrad_ws_bytes(int K, int N, int OHW) {
+  const int64_t KP = (int64_t)K * OHW;
+  return sizeof(double) * (size_t)KP * bgrad_splits(KP, N);
 }
 
 void conv_bgrad(const float* dy, float* db, int OHW, int K, int N, int acc, void* ws,
                 cudaStream_t s) {
-  // enough blocks to fill the machine ~4x, at most one image per split
-  int S = std::max(1, std::min(N, (148 * 32 + K - 1) / K));
-  S = std::min(S, 64);
+  const int64_t KP = (int64_t)K * OHW;
+  const int S = bgrad_splits(KP, N);
+  const int blocks = (int)std::min<int64_t>((KP + 255) / 256, 148 * 8);
   count_launch(2);
-  bgrad_part_k<<<dim3(K, S), 256, 0, s>>>(dy, (double*)ws, OHW, K, N);
-  bgrad_finish_k<<<(K + 127) / 128, 128, 0, s>>>((const double*)ws, db, K, S, acc);
+  bgrad_part_k<<<dim3(blocks, S), 256, 0, s>>>(dy, (double*)ws, KP, N);
+  bgrad_finish_k<<<K, 256, 0, s>>>((const double*)ws, db, K, OHW, S, acc);
 }
 
 }  // namespace ck

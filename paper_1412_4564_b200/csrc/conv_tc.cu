@@ -57,6 +57,7 @@ enum OpKind : int {
   OP_SHIFT_K = 4,     // wgrad B: boxes (32 px, 32 ch, 1, 1) of padded planes
                       // [copy][n][c][PL], pixel coordinate shifted by the tap
   OP_PLANE_K = 5,     // wgrad A: box (32 px, rows, 1) of padded planes [n][k][PL]
+  OP_TILED_MN = 6,    // MN-major 2D tensor [K][MN] (MN inner): 32x32 boxes, SW128_32B atoms
 };
 
 enum EpiKind : int {
@@ -99,6 +100,7 @@ struct GemmParams {
   int groups;             // tiles = ceil(M/BM) * ceil(N/BN) * groups * splits
   int kpp;                // OP_PLANE_K / OP_SHIFT_K: K blocks (32 px) per image plane
   int b_rows;             // OP_SHIFT_K: channel rows per TMA box (divides Cgp and BN)
+  int a_mn3d, b_mn3d;     // OP_TILED_MN: one 3D box per stage (MN % 32 == 0) vs R/32 2D boxes
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -165,14 +167,28 @@ __device__ __forceinline__ void tma_im2col_4d(void* dst, const CUtensorMap* map,
 }
 
 // UMMA shared-memory descriptor (sm_100 "version 1"), SWIZZLE_128B = 2.
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                          uint32_t layout = 2) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)layout << 61;
   return d;
+}
+
+// Operand descriptor for K step k (of 8) in M/N half h of a stage.
+//   K-major, SWIZZLE_128B (layout 2): rows of 128 B = 32 k; K step +32 B;
+//     8-row groups 1024 B apart (SBO).
+//   MN-major, SWIZZLE_128B_BASE32B (layout 1; the only MN-major layout for
+//     tf32): k-rows of 128 B = 32 m/n, 32-B chunks swizzled by k & 3; 4-k
+//     groups 512 B apart (SBO), 32-wide MN blocks 4096 B apart (LBO); K step
+//     of 8 = +1024 B.  (tools/mn_probe.cu checks both against a CPU GEMM.)
+template <bool MN>
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int h, int k) {
+  return MN ? sdesc(base + h * 16384 + k * 1024, 4096, 512, 1)
+            : sdesc(base + h * 16384 + k * 32, 16, 1024, 2);
 }
 
 // kind::tf32 instruction descriptor: D f32, A/B tf32, M = 128.
@@ -332,6 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           // ---- A (BM rows) ----
           if (AK == OP_TILED_K) {
             tma_2d(a, &tma_a, &full[s], k0 + T.grp * p.a_grp_k, T.m0 + T.grp * p.a_grp_mn);
+          } else if (AK == OP_TILED_MN) {
+            if (p.a_mn3d)
+              tma_3d(a, &tma_a, &full[s], 0, k0, T.m0 / 32);
+            else
+              for (int j = 0; j < p.BM / 32; ++j)
+                tma_2d(a + j * 4096, &tma_a, &full[s], T.m0 + 32 * j, k0);
           } else if (AK == OP_PLANE_K) {
             const int n = kb / p.kpp, q0 = (kb - n * p.kpp) * 32;
             tma_3d(a, &tma_a, &full[s], q0, T.m0 + T.grp * p.a_grp_mn, n);
@@ -344,6 +366,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           // ---- B (BN rows) ----
           if (BK == OP_TILED_K) {
             tma_2d(b, &tma_b, &full[s], k0 + T.grp * p.b_grp_k, T.n0 + T.grp * p.b_grp_mn);
+          } else if (BK == OP_TILED_MN) {
+            if (p.b_mn3d)
+              tma_3d(b, &tma_b, &full[s], 0, k0, T.n0 / 32);
+            else
+              for (int j = 0; j < p.BN / 32; ++j)
+                tma_2d(b + j * 4096, &tma_b, &full[s], T.n0 + 32 * j, k0);
           } else {  // OP_SHIFT_K: rows n = (tap, c), K = pixels of image plane img
             const int img = kb / p.kpp, q0 = (kb - img * p.kpp) * 32;
             for (int j = 0; j < p.BN / p.b_rows; ++j) {
@@ -363,7 +391,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer --
     if (lane == 0) {
-      const uint32_t idesc = idesc_tf32(p.BN, 0, 0);
+      constexpr bool a_mn = AK == OP_TILED_MN, b_mn = BK == OP_TILED_MN;
+      const uint32_t idesc = idesc_tf32(p.BN, a_mn, b_mn);
       int it = 0, tc = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
         const Tile T = tile_at(p, t);
@@ -383,9 +412,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int h = 0; h < halves; ++h) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              // K-major SW128: K step = +32 B within the 128-B row, SBO = 1024 (8 rows).
-              mma_tf32(dcol + h * p.BN, sdesc(a + h * 16384 + k * 32, 16, 1024),
-                       sdesc(b + k * 32, 16, 1024), idesc, (!first || k > 0) ? 1u : 0u);
+              mma_tf32(dcol + h * p.BN, op_desc<a_mn>(a, h, k), op_desc<b_mn>(b, 0, k), idesc,
+                       (!first || k > 0) ? 1u : 0u);
             }
           }
           mma_commit(&empty[s]);
@@ -1146,16 +1174,36 @@ static void pad_planes(const float* in, float* out, int H, int W, int Hp, int Wp
 }
 
 static CUtensorMap encode_tiled(const float* base, int rank, const cuuint64_t* dims,
-                                const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+                                const cuuint64_t* strides_bytes, const cuuint32_t* box,
+                                CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
   CUresult r = g_encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, (void*)base, dims,
-                              strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                              strides_bytes, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw Err(CK_ERR_CUDA, "cuTensorMapEncodeTiled (rank " + std::to_string(rank) + ") failed");
   return m;
+}
+
+// MN-major operand: matrix [K rows][MN cols], row pitch ld elements (MN
+// contiguous).  With MN % 32 == 0 a 3D view {32, K, MN/32} loads a whole
+// R-row tile (R/32 blocks of 32 k-rows x 128 B) in one box; otherwise R/32
+// 2D boxes of 32 x 32.  Swizzle 128B_ATOM_32B = the UMMA SW128_32B layout.
+static CUtensorMap map_mn(const float* base, uint64_t K, uint64_t MN, uint64_t ld, int R,
+                          int* is3d) {
+  if (MN % 32 == 0) {
+    *is3d = 1;
+    cuuint64_t dims[3] = {32, K, MN / 32};
+    cuuint64_t strides[2] = {ld * 4, 128};
+    cuuint32_t box[3] = {32, 32, (cuuint32_t)(R / 32)};
+    return encode_tiled(base, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  }
+  *is3d = 0;
+  cuuint64_t dims[2] = {MN, K};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {32, 32};
+  return encode_tiled(base, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
 // wgrad A: planes [n][rows][PL], box (32 px, box_rows, 1)
@@ -1379,11 +1427,10 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   if (!load_driver()) return false;
   const int Kg = d.Kg();
   if (is_fc(d)) {
-    // dX[q, n] = sum_k F^T[q, k] dY[k, n]: A = F^T (transposed to K-major), B = dY
+    // dX[q, n] = sum_k F[q, k] dY[k, n]: A = F read MN-major in place
+    // (F[q + Q*k], q contiguous), B = dY K-major ([n][k]).
     const int Q = d.H * d.W * d.C;
     if (Q % 4 || d.K % 4) return false;
-    float* ft = (float*)grow(state(h)->ft, sizeof(float) * (size_t)Q * d.K, s);
-    transpose(f, ft, d.K, Q, Q, d.K, s);
     const int BN = pick_bn(std::min(d.N, 256));
     const int gm = (Q + 127) / 128, gn = (d.N + BN - 1) / BN;
     const int splits = split_for(gm * gn, rup(d.K, 32) / 32);
@@ -1391,19 +1438,19 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     p.M = Q; p.N = d.N; p.K = rup(d.K, 32); p.BN = BN; p.splits = splits;
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.N; p.acc = acc;
     p.BM = pick_bm(p.M, p.BN);
-    CUtensorMap ta = map_2d(ft, d.K, Q, d.K, p.BM);   // F^T as [q][k]
+    CUtensorMap ta = map_mn(f, d.K, Q, Q, p.BM, &p.a_mn3d);
     CUtensorMap tb = map_2d(dy, d.K, d.N, d.K, BN);  // dY as [n][k]
     if (splits > 1) {
       const int64_t per = (int64_t)Q * d.N;
       float* part = (float*)grow(state(h)->part, sizeof(float) * per * splits, s);
       p.out = part; p.split_stride = per;
-      launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, splits, s);
+      launch<OP_TILED_MN, OP_TILED_K>(ta, tb, p, gm, gn, splits, s);
       count_launch();
       splitk_finish_k<<<std::min<int64_t>((per + 255) / 256, 148 * 8), 256, 0, s>>>(
           part, dx, Q, d.N, Q, splits, per, nullptr, 0, acc);
     } else {
       p.out = dx;
-      launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
+      launch<OP_TILED_MN, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
     }
     return true;
   }
@@ -1454,24 +1501,19 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   if (!load_driver()) return false;
   const int Kg = d.Kg();
   if (is_fc(d)) {
-    // dF[q, k] = sum_n X^T[q, n] dY^T[k, n]: both operands transposed to K-major
+    // dF[q, k] = sum_n X[q, n] dY[k, n]: both operands read MN-major in place
+    // (X[q + Q*n], dY[k + K*n]); the reduction runs over the batch.
     const int Q = d.H * d.W * d.C;
     if (Q % 4 || d.K % 4) return false;
-    const int Np = rup(d.N, 4);
-    TcState* st = state(h);
-    float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)Q * Np, s);
-    float* dyt = (float*)grow(st->dyt, sizeof(float) * (size_t)d.K * Np, s);
-    transpose(x, xt, d.N, Q, Q, Np, s);
-    transpose(dy, dyt, d.N, d.K, d.K, Np, s);
     const int BN = d.K >= 256 ? 256 : rup(d.K, 32);
     const int gm = (Q + 127) / 128, gn = (d.K + BN - 1) / BN;
     GemmParams p{};
     p.M = Q; p.N = d.K; p.K = rup(d.N, 32); p.BN = BN; p.splits = 1;
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.K; p.acc = acc; p.out = df;
     p.BM = pick_bm(p.M, p.BN);
-    CUtensorMap ta = map_2d(xt, d.N, Q, Np, p.BM);
-    CUtensorMap tb = map_2d(dyt, d.N, d.K, Np, BN);
-    launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
+    CUtensorMap ta = map_mn(x, d.N, Q, Q, p.BM, &p.a_mn3d);
+    CUtensorMap tb = map_mn(dy, d.N, d.K, d.K, BN, &p.b_mn3d);
+    launch<OP_TILED_MN, OP_TILED_MN>(ta, tb, p, gm, gn, 1, s);
     return true;
   }
   // Stride-1 convolutions: reduce over the output pixels p' of the padded grid

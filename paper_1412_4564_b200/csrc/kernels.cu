@@ -221,45 +221,51 @@ __global__ void pool_bwd_plane_k(const float* __restrict__ x, const float* __res
   const float* dyp = dy + plane * OHW;
   for (int e = threadIdx.x; e < HW; e += blockDim.x) xs[e] = xp[e];
   __syncthreads();
-  for (int w = threadIdx.x; w < OHW; w += blockDim.x) {
-    const int oi = w % d.OH, oj = w / d.OH;
-    Win b = window_at(d, oi, oj);
-    const float p = dyp[w];
-    if (d.mode == 0) {
-      int best_e = b.i0 + d.H * b.j0;
-      float best = xs[best_e];
-      for (int j = b.j0; j < b.j1; ++j)
-        for (int i = b.i0; i < b.i1; ++i) {
-          float v = xs[i + d.H * j];
-          if (v > best) {
-            best = v;
-            best_e = i + d.H * j;
+  // (oj, oi) and (j, i) loops: warps over columns, lanes down a column (no
+  // per-element division; loads/stores coalesced along H).
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int oj = warp; oj < d.OW; oj += nw)
+    for (int oi = lane; oi < d.OH; oi += 32) {
+      const int w = oi + d.OH * oj;
+      Win b = window_at(d, oi, oj);
+      const float p = dyp[w];
+      if (d.mode == 0) {
+        int best_e = b.i0 + d.H * b.j0;
+        float best = xs[best_e];
+        for (int j = b.j0; j < b.j1; ++j)
+          for (int i = b.i0; i < b.i1; ++i) {
+            float v = xs[i + d.H * j];
+            if (v > best) {
+              best = v;
+              best_e = i + d.H * j;
+            }
           }
-        }
-      arg[w] = best_e;
-      ds[w] = p;
-    } else {
-      float area = (float)((b.i1 - b.i0) * (b.j1 - b.j0));
-      ds[w] = __fdiv_rn(p, area);
+        arg[w] = best_e;
+        ds[w] = p;
+      } else {
+        float area = (float)((b.i1 - b.i0) * (b.j1 - b.j0));
+        ds[w] = __fdiv_rn(p, area);
+      }
     }
-  }
   __syncthreads();
   float* dxp = dx + plane * HW;
-  for (int e = threadIdx.x; e < HW; e += blockDim.x) {
-    const int i = e % d.H, j = e / d.H;
-    int oi_lo = i + d.pt - d.wh + 1;
-    oi_lo = oi_lo <= 0 ? 0 : (oi_lo + d.sh - 1) / d.sh;
-    const int oi_hi = min(d.OH - 1, (i + d.pt) / d.sh);
+  for (int j = warp; j < d.W; j += nw) {
     int oj_lo = j + d.pl - d.ww + 1;
     oj_lo = oj_lo <= 0 ? 0 : (oj_lo + d.sw - 1) / d.sw;
     const int oj_hi = min(d.OW - 1, (j + d.pl) / d.sw);
-    float acc = 0.f;
-    for (int oj = oj_lo; oj <= oj_hi; ++oj)
-      for (int oi = oi_lo; oi <= oi_hi; ++oi) {
-        const int w = oi + d.OH * oj;
-        if (d.mode != 0 || arg[w] == e) acc = __fadd_rn(acc, ds[w]);
-      }
-    dxp[e] = kAcc ? __fadd_rn(dxp[e], acc) : acc;
+    for (int i = lane; i < d.H; i += 32) {
+      const int e = i + d.H * j;
+      int oi_lo = i + d.pt - d.wh + 1;
+      oi_lo = oi_lo <= 0 ? 0 : (oi_lo + d.sh - 1) / d.sh;
+      const int oi_hi = min(d.OH - 1, (i + d.pt) / d.sh);
+      float acc = 0.f;
+      for (int oj = oj_lo; oj <= oj_hi; ++oj)
+        for (int oi = oi_lo; oi <= oi_hi; ++oi) {
+          const int w = oi + d.OH * oj;
+          if (d.mode != 0 || arg[w] == e) acc = __fadd_rn(acc, ds[w]);
+        }
+      dxp[e] = kAcc ? __fadd_rn(dxp[e], acc) : acc;
+    }
   }
 }
 

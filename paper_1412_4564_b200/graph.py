@@ -118,6 +118,65 @@ class Graph:
         return out
 
 
+class Feeder:
+    """cnn_train's batch prefetch (cnn_train.m ``opts.prefetch``) for a
+    device-resident graph: the next batch's pinned host tensors are copied to
+    device staging buffers on a copy stream while the current step computes;
+    ``take`` (on the compute stream) waits for them and moves them into the
+    graph's input variables (one device-to-device copy each).  ``result``
+    queues an asynchronous device->host read of a variable (e.g. the
+    objective) into pinned memory, read back by ``collect``."""
+
+    def __init__(self, graph: Graph, names, stream):
+        self.g, self.names, self.stream = graph, list(names), stream
+        self.copy = torch.cuda.Stream(device=stream.device)
+        self.views = {n: graph.view(n) for n in self.names}
+        self.stage = {}
+        for n, v in self.views.items():
+            s = v.shape
+            self.stage[n] = torch.empty(s.h * s.w * s.c * s.n, dtype=torch.float32,
+                                        device=stream.device)
+        self.ready = torch.cuda.Event()
+        self.free = torch.cuda.Event()
+        self.free.record(stream)
+        self.pending = []
+        self.h2d_bytes = sum(4 * t.numel() for t in self.stage.values())
+
+    def put(self, host: dict):
+        """Queue the H2D copy of one batch (pinned host tensors by name)."""
+        self.copy.wait_event(self.free)
+        cs = C.c_void_p(self.copy.cuda_stream)
+        for n in self.names:
+            src = host[n]
+            assert src.is_pinned() and src.numel() == self.stage[n].numel(), n
+            self.g._check(lib().ck_memcpy(self.g.hd.h, self.stage[n].data_ptr(), src.data_ptr(),
+                                          4 * src.numel(), cs))
+        self.ready.record(self.copy)
+
+    def take(self):
+        """On the compute stream: wait for the staged batch, load it into the graph."""
+        self.stream.wait_event(self.ready)
+        s = C.c_void_p(self.stream.cuda_stream)
+        for n in self.names:
+            self.g._check(lib().ck_memcpy(self.g.hd.h, self.views[n].data,
+                                          self.stage[n].data_ptr(), 4 * self.stage[n].numel(), s))
+        self.free.record(self.stream)
+
+    def result(self, name="objective"):
+        v = self.g.view(name)
+        out = torch.empty(v.shape.h * v.shape.w * v.shape.c * v.shape.n, dtype=torch.float32,
+                          pin_memory=True)
+        self.g._check(lib().ck_memcpy(self.g.hd.h, out.data_ptr(), v.data, 4 * out.numel(),
+                                      C.c_void_p(self.stream.cuda_stream)))
+        self.pending.append(out)
+        return out
+
+    def collect(self):
+        self.stream.synchronize()
+        out, self.pending = [t.numpy().copy() for t in self.pending], []
+        return out
+
+
 class Trainer:
     """cnn_train's SGD step with optional NCCL data parallelism."""
 

@@ -75,6 +75,8 @@ CONV_CASES = [
     ((13, 13, 384, 2), (3, 3, 192, 256), (1, 1, 1, 1, 1, 1, 2)),
     ((6, 6, 256, 4), (6, 6, 256, 512), (1, 1, 0, 0, 0, 0, 1)),
     ((1, 1, 512, 4), (1, 1, 512, 100), (1, 1, 0, 0, 0, 0, 1)),
+    # FC with a ragged batch and a non-multiple-of-32 output count (MN-major tails)
+    ((2, 2, 64, 3), (2, 2, 64, 40), (1, 1, 0, 0, 0, 0, 1)),
 ]
 
 
