@@ -23,6 +23,7 @@ struct ck_handle {
   int* flag = nullptr;    // device label-error flag (loss.cpp:14-18, :101-106)
   int64_t last_classes = 0;
   ck::TcState* tc = nullptr;
+  uint64_t call = 0;      // API call id: scopes transform caches to one call
 };
 
 namespace ck {
@@ -37,6 +38,7 @@ struct Err : std::runtime_error {
 struct HandleScope {
   LaunchCounter* prev;
   explicit HandleScope(ck_handle* h) : prev(g_counter) {
+    ++h->call;
     cudaSetDevice(h->device);
     g_counter = &h->counter;
   }

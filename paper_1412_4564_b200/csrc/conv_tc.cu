@@ -58,6 +58,7 @@ enum OpKind : int {
                       // [copy][n][c][PL], pixel coordinate shifted by the tap
   OP_PLANE_K = 5,     // wgrad A: box (32 px, rows, 1) of padded planes [n][k][PL]
   OP_TILED_MN = 6,    // MN-major 2D tensor [K][MN] (MN inner): 32x32 boxes, SW128_32B atoms
+  OP_IM2COL_MN = 7,   // wgrad B: im2col boxes of 32 px (K) x 32 ch (MN) per (tap, c block)
 };
 
 enum EpiKind : int {
@@ -101,6 +102,7 @@ struct GemmParams {
   int kpp;                // OP_PLANE_K / OP_SHIFT_K: K blocks (32 px) per image plane
   int b_rows;             // OP_SHIFT_K: channel rows per TMA box (divides Cgp and BN)
   int a_mn3d, b_mn3d;     // OP_TILED_MN: one 3D box per stage (MN % 32 == 0) vs R/32 2D boxes
+  int taps;               // OP_IM2COL_MN: fh * fw
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -234,7 +236,8 @@ __device__ __forceinline__ void tc_fence_before() {
         "=r"(r[31])                                                                         \
       : "r"(taddr));
 
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;                  // epilogue warps (multiple of 4)
+constexpr int kThreads = 32 * (2 + kEpiWarps);  // + producer + MMA issuer
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_a) : "memory");
@@ -349,11 +352,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (AK == OP_TILED_K) {
             tma_2d(a, &tma_a, &full[s], k0 + T.grp * p.a_grp_k, T.m0 + T.grp * p.a_grp_mn);
           } else if (AK == OP_TILED_MN) {
+            const int mn0 = T.m0 + T.grp * p.a_grp_mn;
             if (p.a_mn3d)
-              tma_3d(a, &tma_a, &full[s], 0, k0, T.m0 / 32);
+              tma_3d(a, &tma_a, &full[s], 0, k0, mn0 / 32);
             else
               for (int j = 0; j < p.BM / 32; ++j)
-                tma_2d(a + j * 4096, &tma_a, &full[s], T.m0 + 32 * j, k0);
+                tma_2d(a + j * 4096, &tma_a, &full[s], mn0 + 32 * j, k0);
           } else if (AK == OP_PLANE_K) {
             const int n = kb / p.kpp, q0 = (kb - n * p.kpp) * 32;
             tma_3d(a, &tma_a, &full[s], q0, T.m0 + T.grp * p.a_grp_mn, n);
@@ -367,11 +371,28 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (BK == OP_TILED_K) {
             tma_2d(b, &tma_b, &full[s], k0 + T.grp * p.b_grp_k, T.n0 + T.grp * p.b_grp_mn);
           } else if (BK == OP_TILED_MN) {
+            const int mn0 = T.n0 + T.grp * p.b_grp_mn;
             if (p.b_mn3d)
-              tma_3d(b, &tma_b, &full[s], 0, k0, T.n0 / 32);
+              tma_3d(b, &tma_b, &full[s], 0, k0, mn0 / 32);
             else
               for (int j = 0; j < p.BN / 32; ++j)
-                tma_2d(b + j * 4096, &tma_b, &full[s], T.n0 + 32 * j, k0);
+                tma_2d(b + j * 4096, &tma_b, &full[s], mn0 + 32 * j, k0);
+          } else if (BK == OP_IM2COL_MN) {
+            // K block = 32 consecutive output pixels (h fastest, then w, n);
+            // MN block j = 32 channels of tap (fi, fj): one im2col box each.
+            const int ohw = p.OH * p.OW;
+            const int n = k0 / ohw, r = k0 - n * ohw;
+            const int ow = r / p.OH, oh = r - ow * p.OH;
+            const int h0 = oh * p.sh - p.pt, w0 = ow * p.sw - p.pl;
+            for (int j = 0; j < p.BN / 32; ++j) {
+              const int nn = T.n0 + 32 * j;
+              int tap = nn / (p.cchunks * 32);
+              const int c = nn - tap * p.cchunks * 32;
+              tap = min(tap, p.taps - 1);  // columns past the last tap are masked
+              const int fj = tap / p.fh, fi = tap - fj * p.fh;
+              tma_im2col_4d(b + j * 4096, &tma_b, &full[s], T.grp * p.b_grp_c + c, h0, w0, n,
+                            (uint16_t)fi, (uint16_t)fj);
+            }
           } else {  // OP_SHIFT_K: rows n = (tap, c), K = pixels of image plane img
             const int img = kb / p.kpp, q0 = (kb - img * p.kpp) * 32;
             for (int j = 0; j < p.BN / p.b_rows; ++j) {
@@ -391,7 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer --
     if (lane == 0) {
-      constexpr bool a_mn = AK == OP_TILED_MN, b_mn = BK == OP_TILED_MN;
+      constexpr bool a_mn = AK == OP_TILED_MN, b_mn = BK == OP_TILED_MN || BK == OP_IM2COL_MN;
       const uint32_t idesc = idesc_tf32(p.BN, a_mn, b_mn);
       int it = 0, tc = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
@@ -424,7 +445,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ----------------------------------------------------------- epilogue --
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    // kEpiWarps warps: warp w reads TMEM lane quarter w & 3 (hardware rule)
+    // and every (kEpiWarps/4)-th 32-column chunk, so two warps share a quarter.
+    const int q = warp & 3;
+    const int cpart = (warp - 2) / 4, cparts = kEpiWarps / 4;
     int tc = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
       const Tile T = tile_at(p, t);
@@ -436,6 +460,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* out = p.out;
       const bool partial = p.splits > 1;
       if (partial) out += (int64_t)T.split * p.split_stride;
+      // plain stores: split-K partials, or no bias / relu / accumulate
+      const bool plain = partial || (!p.bias && !p.relu && !p.acc);
+      const int64_t ld = p.ld;
       for (int h = 0; h < halves; ++h) {
         const int m = T.m0 + h * 128 + q * 32 + lane;
         const bool row_ok = m < p.M;
@@ -457,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           row_base = (int64_t)m + (int64_t)T.grp * p.grp_out;
           if (p.bias && !partial && row_ok) rbias = p.bias[m + T.grp * p.grp_col];
         }
-        for (int c0 = 0; c0 < p.BN; c0 += 32) {
+        for (int c0 = 32 * cpart; c0 < p.BN; c0 += 32 * cparts) {
           uint32_t r[32];
           const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) +
                                  (uint32_t)(ab * acc_cols + h * p.BN + c0);
@@ -466,34 +493,44 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (empty_split)
 #pragma unroll
             for (int j = 0; j < 32; ++j) r[j] = 0u;
-          if (row_ok) {
+          const int col0 = T.n0 + c0;
+          // columns of this chunk inside both the tile and the matrix
+          const int lim = min(min(32, p.BN - c0), p.n_valid - col0);
+          if (row_ok && lim > 0 && p.epi == EPI_S2D) {
+            for (int j = 0; j < lim; ++j) {
+              const int col = col0 + j;
+              const int cg = p.s2d_C, abc = col / cg, c = col - abc * cg;
+              const int i = s_i + abc % p.s2d, jj = s_j + abc / p.s2d;
+              if (i >= p.s2d_H || jj >= p.s2d_W) continue;
+              float* dst = out + row_base + i + (int64_t)p.s2d_H * (jj + (int64_t)p.s2d_W * c);
+              float v = __uint_as_float(r[j]);
+              if (!partial && p.acc) v = __fadd_rn(*dst, v);
+              *dst = v;
+            }
+          } else if (row_ok && lim > 0) {
+          float* dst = out + row_base + (int64_t)col0 * ld;
+          if (plain && lim == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) dst[j * ld] = __uint_as_float(r[j]);
+          } else if (plain) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < lim) dst[j * ld] = __uint_as_float(r[j]);
+          } else {
+            const float* bcol = p.bias ? p.bias + col0 + T.grp * p.grp_col : nullptr;
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              const int col = T.n0 + c0 + j;
-              if (col < p.n_valid) {
+              if (j < lim) {
                 float v = __uint_as_float(r[j]);
-                float* dst;
-                if (p.epi == EPI_S2D) {
-                  const int cg = p.s2d_C, abc = col / cg, c = col - abc * cg;
-                  const int i = s_i + abc % p.s2d, jj = s_j + abc / p.s2d;
-                  if (i >= p.s2d_H || jj >= p.s2d_W) continue;
-                  dst = out + row_base + i + (int64_t)p.s2d_H * (jj + (int64_t)p.s2d_W * c);
-                } else {
-                  dst = out + row_base + (int64_t)col * p.ld;
-                }
-                if (!partial) {
-                  if (p.epi == EPI_PIX) {
-                    if (p.bias) v = __fadd_rn(v, p.bias[col + T.grp * p.grp_col]);
-                  } else if (p.bias) {
-                    v = __fadd_rn(v, rbias);
-                  }
-                  if (p.relu) v = v > 0.f ? v : 0.f;
-                  if (p.acc) v = __fadd_rn(*dst, v);
-                }
-                *dst = v;
+                if (p.bias) v = __fadd_rn(v, p.epi == EPI_PIX ? __ldg(bcol + j) : rbias);
+                if (p.relu) v = v > 0.f ? v : 0.f;
+                if (p.acc) v = __fadd_rn(dst[j * ld], v);
+                dst[j * ld] = v;
               }
             }
           }
+          }
+          __syncwarp();  // reconverge before the next warp-wide tcgen05.ld
         }
       }
       tc_fence_before();
@@ -1000,6 +1037,11 @@ bool conv_tc_available() { return load_driver(); }
 
 struct TcState {
   Workspace xt, dyt, ft, part;
+  // dy in pixel-major layout is shared by wgrad and dgrad of one
+  // ck_conv_backward call: cached by (source, geometry, call id).
+  const float* dyt_src = nullptr;
+  uint64_t dyt_call = 0;
+  int64_t dyt_key = 0;
 };
 
 static TcState* state(ck_handle* h) {
@@ -1037,7 +1079,8 @@ static CUtensorMap map_2d(const float* base, uint64_t inner, uint64_t outer, uin
 
 // 4D im2col map over a pixel-major tensor (Cp, H, W, N).
 static CUtensorMap map_im2col(const float* base, int Cp, int H, int W, int N, int lo_h, int lo_w,
-                              int up_h, int up_w, int sh, int sw, int pixels) {
+                              int up_h, int up_w, int sh, int sw, int pixels,
+                              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   cuuint64_t dims[4] = {(cuuint64_t)Cp, (cuuint64_t)H, (cuuint64_t)W, (cuuint64_t)N};
   cuuint64_t strides[3] = {(cuuint64_t)Cp * 4, (cuuint64_t)Cp * H * 4, (cuuint64_t)Cp * H * W * 4};
@@ -1046,7 +1089,7 @@ static CUtensorMap map_im2col(const float* base, int Cp, int H, int W, int N, in
   cuuint32_t es[4] = {1, (cuuint32_t)sh, (cuuint32_t)sw, 1};
   CUresult r = g_encode_im2col(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)base, dims, strides,
                                lower, upper, 32, (cuuint32_t)pixels, es,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Err(CK_ERR_CUDA, "cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")");
@@ -1143,6 +1186,23 @@ static void to_pm(const float* x, float* xt, int H, int W, int C, int N, int Cg,
   dim3 grid((HW + 31) / 32, (Cgp * groups + 31) / 32, N);
   count_launch();
   to_pixel_major_k<<<grid, 256, 0, s>>>(x, xt, HW, C, Cg, Cgp, groups);
+}
+
+// dy in pixel-major layout [n][ow][oh][groups * Kgp]; wgrad and dgrad of one
+// ck_conv_backward call share it (same source, geometry and call id).
+static float* dy_pm(ck_handle* h, const float* dy, const ConvDims& d, int Kg, int Kgp, int groups,
+                    cudaStream_t s) {
+  TcState* st = state(h);
+  const int64_t key =
+      ((((int64_t)d.OH * 4099 + d.OW) * 65537 + d.K) * 131071 + d.N) * 1031 + Kgp * 17 + groups;
+  float* buf =
+      (float*)grow(st->dyt, sizeof(float) * (size_t)d.N * d.OH * d.OW * Kgp * groups, s);
+  if (st->dyt_src == dy && st->dyt_call == h->call && st->dyt_key == key) return buf;
+  to_pm(dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, s);
+  st->dyt_src = dy;
+  st->dyt_call = h->call;
+  st->dyt_key = key;
+  return buf;
 }
 
 static void transpose(const float* in, float* out, int R, int Cc, int64_t ldi, int64_t ldo,
@@ -1249,13 +1309,8 @@ template <int AK, int BK>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int grid_m,
                    int grid_n, int grid_z, cudaStream_t s);
 
-static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
-                      const ConvDims& d, const S2D& z, int relu, cudaStream_t s) {
-  TcState* st = state(h);
-  const int taps = z.Th * z.Tw;
-  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * z.U * z.V * z.Csp, s);
-  float* ft = (float*)grow(st->ft, sizeof(float) * (size_t)d.K * taps * z.Csp, s);
-  count_launch(2);
+static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, cudaStream_t s) {
+  count_launch();
   const int col_bytes = (int)sizeof(float) * d.C * z.s * z.U * z.s;  // one s2d column, all c
   const int VB = std::min(z.V, (44 * 1024) / col_bytes);
   if (VB >= 1)
@@ -1264,6 +1319,16 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   else
     s2d_pm_k<<<blocks_for((int64_t)d.N * z.U * z.V * z.Csp), 256, 0, s>>>(
         x, xt, d.H, d.W, d.C, d.N, z.s, z.U, z.V, z.Cs, z.Csp);
+}
+
+static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
+                      const ConvDims& d, const S2D& z, int relu, cudaStream_t s) {
+  TcState* st = state(h);
+  const int taps = z.Th * z.Tw;
+  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * z.U * z.V * z.Csp, s);
+  float* ft = (float*)grow(st->ft, sizeof(float) * (size_t)d.K * taps * z.Csp, s);
+  s2d_pm(x, xt, d, z, s);
+  count_launch();
   s2d_repack_fprop_k<<<blocks_for((int64_t)d.K * taps * z.Csp), 256, 0, s>>>(
       f, ft, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Tw, z.Csp);
   GemmParams p{};
@@ -1284,9 +1349,8 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   TcState* st = state(h);
   const int taps = z.Th * z.Tw;
   const int Kp = rup(d.K, 32);
-  float* dyt = (float*)grow(st->dyt, sizeof(float) * (size_t)d.N * d.OH * d.OW * Kp, s);
+  float* dyt = dy_pm(h, dy, d, d.K, Kp, 1, s);
   float* gt = (float*)grow(st->ft, sizeof(float) * (size_t)z.Cs * taps * Kp, s);
-  to_pm(dy, dyt, d.OH, d.OW, d.K, d.N, d.K, Kp, 1, s);
   count_launch();
   s2d_repack_dgrad_k<<<blocks_for((int64_t)z.Cs * taps * Kp), 256, 0, s>>>(
       f, gt, d.fh, d.fw, d.C, d.K, Kp, z.s, z.Th, z.Tw);
@@ -1304,42 +1368,35 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (z.Cs + p.BN - 1) / p.BN, 1, s);
 }
 
+static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, cudaStream_t s);
+
+// Strided wgrad through space-to-depth: the stride-1 im2col wgrad (see
+// conv_tc_wgrad) over the s2d pixel-major input, then the s2d filter scatter.
 static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, const ConvDims& d,
                       const S2D& z, int acc, cudaStream_t s) {
   TcState* st = state(h);
   const int taps = z.Th * z.Tw;
-  const int Hp = rup(z.U, 4), Wp = z.V;
-  const int PL = rup(Hp * Wp, 32);
-  const int copies = std::min(4, z.Th);
-  float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)PL * d.N * z.Cs * copies, s);
-  float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)PL * d.N * d.K, s);
-  count_launch();
-  {
-    const int col_bytes = (int)sizeof(float) * (z.s * z.U * z.s + Hp);  // strip + table
-    const int VB = std::min(Wp, (40 * 1024) / col_bytes);
-    if (VB >= 1)
-      s2d_planes_strip_k<<<dim3((Wp + VB - 1) / VB, d.C, d.N), 256, (size_t)VB * col_bytes, s>>>(
-          x, xp, d.H, d.W, d.C, d.N, z.s, z.U, z.V, Hp, Wp, z.Cs, PL, copies, VB);
-    else
-      s2d_planes_k<<<dim3((PL + 255) / 256, z.Cs, copies * d.N), 256, 0, s>>>(
-          x, xp, d.H, d.W, d.C, d.N, z.s, z.U, z.V, Hp, Wp, z.Cs, PL);
-  }
-  pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, PL, 1, s);
+  const int Kp = rup(d.K, 32);
+  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * z.U * z.V * z.Csp, s);
+  s2d_pm(x, xt, d, z, s);
+  float* dyt = dy_pm(h, dy, d, d.K, Kp, 1, s);
   const int Ntot = taps * z.Csp;
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
   const int BM = pick_bm(d.K, BN);
-  const int kblocks = d.N * (PL / 32);
+  const int64_t pix = (int64_t)d.N * d.OH * d.OW;
+  const int kblocks = (int)((pix + 31) / 32);
   const int splits = wgrad_splits_for(((d.K + BM - 1) / BM) * ((Ntot + BN - 1) / BN), kblocks);
   const int64_t per = (int64_t)Ntot * d.K;
   float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
   GemmParams p{};
   p.M = d.K; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.BM = BM; p.splits = splits;
-  p.fh = z.Th; p.Hp = Hp; p.cchunks = z.Csp / 32; p.kpp = PL / 32;
-  p.b_rows = std::gcd(z.Csp, BN);
+  p.OH = d.OH; p.OW = d.OW; p.sh = 1; p.sw = 1; p.pt = 0; p.pl = 0; p.fh = z.Th; p.taps = taps;
+  p.cchunks = z.Csp / 32;
   p.epi = EPI_LINEAR; p.out = part; p.ld = d.K; p.n_valid = Ntot; p.split_stride = per;
-  CUtensorMap ta = map_planes(dyp, PL, d.K, d.N, BM);
-  CUtensorMap tb = map_plane_copies(xp, PL, z.Cs, d.N, copies, p.b_rows);
-  launch<OP_PLANE_K, OP_SHIFT_K>(ta, tb, p, 0, 0, splits, s);
+  CUtensorMap ta = map_mn(dyt, (uint64_t)pix, Kp, Kp, BM, &p.a_mn3d);
+  CUtensorMap tb = map_im2col(xt, z.Csp, z.U, z.V, d.N, 0, 0, -(z.Th - 1), -(z.Tw - 1), 1, 1, 32,
+                              CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  launch<OP_TILED_MN, OP_IM2COL_MN>(ta, tb, p, 0, 0, splits, s);
   count_launch();
   s2d_wgrad_finish_k<<<blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s>>>(
       part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc);
@@ -1466,9 +1523,8 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
   const int taps = d.fh * d.fw;
   TcState* st = state(h);
-  float* dyt = (float*)grow(st->dyt, sizeof(float) * (size_t)d.N * d.OH * d.OW * Kp, s);
+  float* dyt = dy_pm(h, dy, d, Kg, Kgp, d.groups, s);
   float* gt = (float*)grow(st->ft, sizeof(float) * (size_t)d.C * taps * Kgp, s);
-  to_pm(dy, dyt, d.OH, d.OW, d.K, d.N, Kg, Kgp, d.groups, s);
   count_launch();
   repack_dgrad_k<<<std::min<int64_t>(((int64_t)d.C * taps * Kgp + 255) / 256, 148 * 8), 256, 0, s>>>(
       f, gt, d.fh, d.fw, d.Cg, Kg, Kgp, d.groups, d.fsc, d.fsk);
@@ -1516,13 +1572,10 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
     launch<OP_TILED_MN, OP_TILED_MN>(ta, tb, p, gm, gn, 1, s);
     return true;
   }
-  // Stride-1 convolutions: reduce over the output pixels p' of the padded grid
-  // (Hp x Wp per image).  dy is laid channel-major with zeros at the junk
-  // positions of that grid; x channel-major and zero padded, so the im2row
-  // column of tap (fi, fj) is x shifted by fi + Hp*fj -- a K-major TMA box.
-  // Hp is rounded to a multiple of 4 so the shift is fi (mod 4); TMA box
-  // starts must be 16-byte aligned, so x is written in min(4, fh) copies
-  // pre-shifted by 0..3 elements.
+  // dF[k, (tap, c)] = sum_q dY[q, k] X[q + tap, c] over all output pixels q:
+  // A = dY pixel-major, read MN-major ([q][k], k contiguous); B = X pixel-major
+  // through im2col boxes (32 pixels x 32 channels of one tap), also MN-major.
+  // Split-K over the pixels; partials reduced by wgrad_finish_k.
   if (d.sh != 1 || d.sw != 1) {
     S2D z;
     if (!s2d_plan(d, z)) return false;
@@ -1530,21 +1583,19 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
     return true;
   }
   if (d.Cg < 16 || Kg < 16) return false;
-  const int Cgp = rup(d.Cg, 32);
+  if (d.pt > 127 || d.pl > 127 || d.fh > 128 || d.fw > 128) return false;
+  const int Cgp = rup(d.Cg, 32), Cp = Cgp * d.groups;
+  const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
   const int taps = d.fh * d.fw;
-  const int Hp = rup(d.H + d.pt + d.pb, 4), Wp = d.W + d.pl + d.pr;
-  const int PL = rup(Hp * Wp, 32);
-  if ((int64_t)PL * d.N * std::max(d.C, d.K) * 4 > INT32_MAX) return false;
-  const int copies = std::min(4, d.fh);
   TcState* st = state(h);
-  float* xp = (float*)grow(st->xt, sizeof(float) * (size_t)PL * d.N * d.C * copies, s);
-  float* dyp = (float*)grow(st->dyt, sizeof(float) * (size_t)PL * d.N * d.K, s);
-  pad_planes(x, xp, d.H, d.W, Hp, Wp, d.pt, d.pl, d.C, d.N, PL, copies, s);
-  pad_planes(dy, dyp, d.OH, d.OW, Hp, Wp, 0, 0, d.K, d.N, PL, 1, s);
+  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
+  to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
+  float* dyt = dy_pm(h, dy, d, Kg, Kgp, d.groups, s);
   const int Ntot = taps * Cgp;  // GEMM N = (tap, c) per group
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
   const int BM = pick_bm(Kg, BN);
-  const int kblocks = d.N * (PL / 32);
+  const int64_t pix = (int64_t)d.N * d.OH * d.OW;
+  const int kblocks = (int)((pix + 31) / 32);
   const int splits = wgrad_splits_for(
       ((Kg + BM - 1) / BM) * ((Ntot + BN - 1) / BN) * d.groups, kblocks);
   const int64_t per_grp = (int64_t)Ntot * Kg;
@@ -1552,18 +1603,17 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
   GemmParams p{};
   p.M = Kg; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.BM = BM; p.splits = splits;
-  p.fh = d.fh; p.Hp = Hp; p.kpp = PL / 32;
-  p.cchunks = Cgp / 32;
-  p.b_rows = std::gcd(Cgp, BN);
-  p.a_grp_mn = Kg;
-  p.b_grp_row = d.Cg;
+  p.OH = d.OH; p.OW = d.OW; p.sh = 1; p.sw = 1; p.pt = d.pt; p.pl = d.pl; p.fh = d.fh;
+  p.taps = taps; p.cchunks = Cgp / 32;
+  p.a_grp_mn = Kgp;
+  p.b_grp_c = Cgp;
   // raw partials: part[s*per + g*per_grp + n*Kg + k]
   p.epi = EPI_LINEAR; p.out = part; p.ld = Kg; p.grp_out = per_grp; p.n_valid = Ntot;
   p.split_stride = per;
-  p.bias = nullptr; p.relu = 0; p.acc = 0;
-  CUtensorMap ta = map_planes(dyp, PL, d.K, d.N, BM);            // rows k, K = plane pixels
-  CUtensorMap tb = map_plane_copies(xp, PL, d.C, d.N, copies, p.b_rows);   // rows c, shifted by tap
-  launch<OP_PLANE_K, OP_SHIFT_K>(ta, tb, p, 0, 0, d.groups * splits, s);
+  CUtensorMap ta = map_mn(dyt, (uint64_t)pix, Kp, Kp, BM, &p.a_mn3d);
+  CUtensorMap tb = map_im2col(xt, Cp, d.H, d.W, d.N, -d.pt, -d.pl, d.pb - (d.fh - 1),
+                              d.pr - (d.fw - 1), 1, 1, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  launch<OP_TILED_MN, OP_IM2COL_MN>(ta, tb, p, 0, 0, d.groups * splits, s);
   const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
   count_launch();
   wgrad_finish_k<<<std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(

@@ -67,6 +67,11 @@ CONV_CASES = [
     ((11, 10, 2, 2), (5, 4, 2, 3), (3, 2, 2, 0, 1, 3, 1)),
     ((8, 8, 6, 2), (1, 1, 2, 6), (1, 1, 0, 0, 0, 0, 3)),
     ((5, 5, 2, 1), (3, 3, 2, 3), (2, 2, 0, 1, 0, 1, 1)),
+    # tensor-core paths at odd sizes: channel padding, asymmetric pad, groups,
+    # space-to-depth stride 2
+    ((9, 7, 32, 3), (3, 2, 32, 48), (1, 1, 1, 0, 1, 1, 1)),
+    ((6, 5, 40, 2), (3, 3, 20, 36), (1, 1, 1, 1, 1, 1, 2)),
+    ((23, 21, 5, 2), (5, 5, 5, 24), (2, 2, 0, 0, 0, 0, 1)),
     # AlexNet layer shapes at batch 2
     ((227, 227, 3, 2), (11, 11, 3, 96), (4, 4, 0, 0, 0, 0, 1)),
     ((27, 27, 96, 2), (5, 5, 48, 256), (1, 1, 2, 2, 2, 2, 2)),
