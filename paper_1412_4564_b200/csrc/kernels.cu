@@ -269,6 +269,103 @@ __global__ void pool_bwd_plane_k(const float* __restrict__ x, const float* __res
   }
 }
 
+// Compile-time window / stride max pooling (AlexNet 3x3/2, LeNet and VGG
+// 2x2/2): unrolled windows, one runtime division per element.  Same rules
+// as pool_fwd_k / pool_bwd_plane_k (first strict maximum, (oj, oi) order).
+template <int WH, int WW, int SH, int SW>
+__global__ void pool_max_fwd_t(const float* __restrict__ x, float* __restrict__ y, PoolDims d) {
+  const int OHW = d.OH * d.OW, HW = d.H * d.W;
+  const int64_t total = (int64_t)OHW * d.C * d.N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t plane = e / OHW;
+    const int w = (int)(e - plane * OHW);
+    const int oj = w / d.OH, oi = w - oj * d.OH;
+    const int si = oi * SH - d.pt, sj = oj * SW - d.pl;
+    const float* xp = x + plane * HW;
+    float best = 0.f;
+    bool have = false;
+#pragma unroll
+    for (int b = 0; b < WW; ++b) {
+      const int j = sj + b;
+#pragma unroll
+      for (int a = 0; a < WH; ++a) {
+        const int i = si + a;
+        if (i >= 0 && i < d.H && j >= 0 && j < d.W) {
+          const float v = __ldg(xp + i + d.H * j);
+          if (!have || v > best) {
+            best = v;
+            have = true;
+          }
+        }
+      }
+    }
+    y[e] = best;
+  }
+}
+
+template <int WH, int WW, int SH, int SW, bool kAcc>
+__global__ void pool_max_bwd_t(const float* __restrict__ x, const float* __restrict__ dy,
+                               float* dx, PoolDims d) {
+  extern __shared__ float psm[];
+  const int HW = d.H * d.W, OHW = d.OH * d.OW;
+  float* xs = psm;              // [HW]
+  float* ds = xs + HW;          // [OHW]
+  int* arg = (int*)(ds + OHW);  // [OHW]
+  const int64_t plane = blockIdx.x;
+  const float* xp = x + plane * HW;
+  const float* dyp = dy + plane * OHW;
+  for (int e = threadIdx.x; e < HW; e += blockDim.x) xs[e] = __ldg(xp + e);
+  __syncthreads();
+  for (int w = threadIdx.x; w < OHW; w += blockDim.x) {
+    const int oj = w / d.OH, oi = w - oj * d.OH;
+    const int si = oi * SH - d.pt, sj = oj * SW - d.pl;
+    float best = 0.f;
+    int best_e = -1;
+#pragma unroll
+    for (int b = 0; b < WW; ++b) {
+      const int j = sj + b;
+#pragma unroll
+      for (int a = 0; a < WH; ++a) {
+        const int i = si + a;
+        if (i >= 0 && i < d.H && j >= 0 && j < d.W) {
+          const float v = xs[i + d.H * j];
+          if (best_e < 0 || v > best) {
+            best = v;
+            best_e = i + d.H * j;
+          }
+        }
+      }
+    }
+    arg[w] = best_e;
+    ds[w] = __ldg(dyp + w);
+  }
+  __syncthreads();
+  constexpr int NI = (WH + SH - 1) / SH, NJ = (WW + SW - 1) / SW;
+  float* dxp = dx + plane * HW;
+  for (int e = threadIdx.x; e < HW; e += blockDim.x) {
+    const int j = e / d.H, i = e - j * d.H;
+    const int ti = i + d.pt, tj = j + d.pl;
+    const int oi_hi = min(d.OH - 1, ti / SH), oj_hi = min(d.OW - 1, tj / SW);
+    const int oi_lo = ti - WH + 1 <= 0 ? 0 : (ti - WH + SH) / SH;
+    const int oj_lo = tj - WW + 1 <= 0 ? 0 : (tj - WW + SW) / SW;
+    float acc = 0.f;
+#pragma unroll
+    for (int b = 0; b < NJ; ++b) {
+      const int oj = oj_lo + b;
+#pragma unroll
+      for (int a = 0; a < NI; ++a) {
+        const int oi = oi_lo + a;
+        if (oj <= oj_hi && oi <= oi_hi) {
+          const int w = oi + d.OH * oj;
+          if (arg[w] == e) acc = __fadd_rn(acc, ds[w]);
+        }
+      }
+    }
+    dxp[e] = kAcc ? __fadd_rn(dxp[e], acc) : acc;
+  }
+}
+
 // ----------------------------------------------------------------- LRN ----
 // normalize.cpp:18-22 lrn_group: [k - (n-1)/2, k + n-1-(n-1)/2] clipped.
 // A block owns kLrnPix consecutive pixels of one image and stages all their
@@ -360,35 +457,45 @@ template <int NW>
 __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y, int HW, int C,
                               int64_t pixels, float kappa, float alpha, float nbeta) {
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
+  constexpr int P = 4;  // prefetch distance (channels)
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pixels;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = e / HW;
     const int p = (int)(e - n * HW);
     const float* xp = x + n * C * HW + p;
     float* yp = y + n * C * HW + p;
+    auto ldx = [&](int t) { return (t >= 0 && t < C) ? __ldg(xp + (int64_t)t * HW) : 0.f; };
     float sq[NW], xv[NW];  // window k-DOWN .. k+UP
 #pragma unroll
     for (int i = 0; i < NW; ++i) {
-      const int t = i - DOWN;
-      const float v = (t >= 0 && t < C) ? xp[(int64_t)t * HW] : 0.f;
-      xv[i] = v;
-      sq[i] = __fmul_rn(v, v);
+      xv[i] = ldx(i - DOWN);
+      sq[i] = __fmul_rn(xv[i], xv[i]);
     }
-    for (int k = 0; k < C; ++k) {
-      float acc = 0.f;
+    float xpre[P];  // x[k + UP + 1 + u]
 #pragma unroll
-      for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
-      const float scale = powf(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
-      yp[(int64_t)k * HW] = __fmul_rn(xv[DOWN], scale);
-      const int t = k + UP + 1;
-      const float v = t < C ? xp[(int64_t)t * HW] : 0.f;
+    for (int u = 0; u < P; ++u) xpre[u] = ldx(UP + 1 + u);
+    for (int k0 = 0; k0 < C; k0 += P) {
 #pragma unroll
-      for (int i = 0; i < NW - 1; ++i) {
-        sq[i] = sq[i + 1];
-        xv[i] = xv[i + 1];
+      for (int u = 0; u < P; ++u) {
+        const int k = k0 + u;
+        const float v = xpre[u];
+        xpre[u] = ldx(k + P + UP + 1);
+        if (k < C) {
+          float acc = 0.f;
+#pragma unroll
+          for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
+          // fast-math power (MUFU lg2/ex2, a few ulp; normalize.cpp uses std::pow)
+          const float scale = __powf(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
+          yp[(int64_t)k * HW] = __fmul_rn(xv[DOWN], scale);
+#pragma unroll
+          for (int i = 0; i < NW - 1; ++i) {
+            sq[i] = sq[i + 1];
+            xv[i] = xv[i + 1];
+          }
+          xv[NW - 1] = v;
+          sq[NW - 1] = __fmul_rn(v, v);
+        }
       }
-      xv[NW - 1] = v;
-      sq[NW - 1] = __fmul_rn(v, v);
     }
   }
 }
@@ -397,7 +504,8 @@ template <int NW, bool kAcc>
 __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
                               int HW, int C, int64_t pixels, float kappa, float alpha, float beta) {
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
-  const float nb1 = -beta - 1.f, nb = -beta;
+  constexpr int P = 4;  // prefetch distance (channels): 2P loads in flight per thread
+  const float nb = -beta;
   const float c2ab = __fmul_rn(__fmul_rn(2.f, alpha), beta);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pixels;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -407,60 +515,79 @@ __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restri
     const float* xp = x + base;
     const float* gp = dy + base;
     float* dp = dx + base;
-    // squares for the lead index j: sq[i] = x[j - DOWN + i]^2
-    float sq[NW];
+    auto ldx = [&](int t) { return (t >= 0 && t < C) ? __ldg(xp + (int64_t)t * HW) : 0.f; };
+    auto ldg = [&](int t) { return t < C ? __ldg(gp + (int64_t)t * HW) : 0.f; };
+    // x window of the lead index j: xw[i] = x[j - DOWN + i], sq = its squares
+    float xw[NW], sq[NW];
 #pragma unroll
     for (int i = 0; i < NW; ++i) {
-      const int t = i - DOWN;
-      const float v = (t >= 0 && t < C) ? xp[(int64_t)t * HW] : 0.f;
-      sq[i] = __fmul_rn(v, v);
+      xw[i] = ldx(i - DOWN);
+      sq[i] = __fmul_rn(xw[i], xw[i]);
+    }
+    float xpre[P], gpre[P];  // x[j + UP + 1 + u], dy[j + u] for the next P steps
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      xpre[u] = ldx(UP + 1 + u);
+      gpre[u] = ldg(u);
     }
     float eta[NW];  // eta of indices j-NW+1 .. j (0 outside [0, C))
-    float Ls[DOWN + 1], xs[DOWN + 1], gs[DOWN + 1];  // indices j-DOWN .. j
+    float Ls[DOWN + 1], xs[DOWN + 1], gs[DOWN + 1];  // L^-beta, x, dy of j-DOWN .. j
 #pragma unroll
     for (int i = 0; i < NW; ++i) eta[i] = 0.f;
 #pragma unroll
     for (int i = 0; i <= DOWN; ++i) Ls[i] = xs[i] = gs[i] = 0.f;
-    for (int j = 0; j < C + DOWN; ++j) {
-      float L = 0.f, xj = 0.f, gj = 0.f, et = 0.f;
-      if (j < C) {
-        float acc = 0.f;
+    for (int j0 = 0; j0 < C + DOWN; j0 += P) {
 #pragma unroll
-        for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
-        L = __fadd_rn(kappa, __fmul_rn(alpha, acc));
-        xj = xp[(int64_t)j * HW];
-        gj = gp[(int64_t)j * HW];
-        et = __fmul_rn(__fmul_rn(gj, powf(L, nb1)), xj);
+      for (int u = 0; u < P; ++u) {
+        const int j = j0 + u;
+        const float xlead = xpre[u], gj_in = gpre[u];
+        xpre[u] = ldx(j + P + UP + 1);
+        gpre[u] = ldg(j + P);
+        if (j < C + DOWN) {
+          float L = 0.f, xj = 0.f, gj = 0.f, et = 0.f;
+          if (j < C) {
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
+            const float Lj = __fadd_rn(kappa, __fmul_rn(alpha, acc));
+            L = __powf(Lj, nb);  // L^-beta; L^(-beta-1) = L^-beta / L
+            xj = xw[DOWN];
+            gj = gj_in;
+            et = __fmul_rn(__fmul_rn(gj, __fdividef(L, Lj)), xj);
+          }
+#pragma unroll
+          for (int i = 0; i < NW - 1; ++i) eta[i] = eta[i + 1];
+          eta[NW - 1] = et;
+#pragma unroll
+          for (int i = 0; i < DOWN; ++i) {
+            Ls[i] = Ls[i + 1];
+            xs[i] = xs[i + 1];
+            gs[i] = gs[i + 1];
+          }
+          Ls[DOWN] = L;
+          xs[DOWN] = xj;
+          gs[DOWN] = gj;
+          const int d = j - DOWN;
+          if (d >= 0) {
+            // k in [d-UP, d+DOWN] = [j-NW+1, j]: the whole eta window, ascending
+            float acc = 0.f;
+#pragma unroll
+            for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, eta[i]);
+            const float r = __fadd_rn(__fmul_rn(gs[0], Ls[0]),
+                                      -__fmul_rn(__fmul_rn(c2ab, xs[0]), acc));
+            float* o = dp + (int64_t)d * HW;
+            *o = kAcc ? __fadd_rn(*o, r) : r;
+          }
+          // advance the x window to lead index j + 1
+#pragma unroll
+          for (int i = 0; i < NW - 1; ++i) {
+            xw[i] = xw[i + 1];
+            sq[i] = sq[i + 1];
+          }
+          xw[NW - 1] = xlead;
+          sq[NW - 1] = __fmul_rn(xlead, xlead);
+        }
       }
-#pragma unroll
-      for (int i = 0; i < NW - 1; ++i) eta[i] = eta[i + 1];
-      eta[NW - 1] = et;
-#pragma unroll
-      for (int i = 0; i < DOWN; ++i) {
-        Ls[i] = Ls[i + 1];
-        xs[i] = xs[i + 1];
-        gs[i] = gs[i + 1];
-      }
-      Ls[DOWN] = L;
-      xs[DOWN] = xj;
-      gs[DOWN] = gj;
-      const int d = j - DOWN;
-      if (d >= 0) {
-        // k in [d-UP, d+DOWN] = [j-NW+1, j]: the whole eta window, ascending
-        float acc = 0.f;
-#pragma unroll
-        for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, eta[i]);
-        const float r = __fadd_rn(__fmul_rn(gs[0], powf(Ls[0], nb)),
-                                  -__fmul_rn(__fmul_rn(c2ab, xs[0]), acc));
-        float* o = dp + (int64_t)d * HW;
-        *o = kAcc ? __fadd_rn(*o, r) : r;
-      }
-      // advance the square window to lead index j + 1
-      const int t = j + UP + 1;
-      const float v = t < C ? xp[(int64_t)t * HW] : 0.f;
-#pragma unroll
-      for (int i = 0; i < NW - 1; ++i) sq[i] = sq[i + 1];
-      sq[NW - 1] = __fmul_rn(v, v);
     }
   }
 }
@@ -787,11 +914,29 @@ void sgd_step(float* w, float* v, const float* g, int64_t n, float lr, float mom
   sgd_k<<<blocks_for(n, 256), 256, 0, s>>>(w, v, g, n, lr, mom, wd);
 }
 
+template <int WH, int WW, int SH, int SW>
+static void pool_max_fwd_launch(const float* x, float* y, const PoolDims& d, cudaStream_t s) {
+  const int64_t total = (int64_t)d.OH * d.OW * d.C * d.N;
+  pool_max_fwd_t<WH, WW, SH, SW><<<blocks_for(total, 256), 256, 0, s>>>(x, y, d);
+}
+
+// compile-time window/stride of a max pooling, or 0
+static int pool_fixed(const PoolDims& d) {
+  if (d.mode != 0) return 0;
+  if (d.wh == 3 && d.ww == 3 && d.sh == 2 && d.sw == 2) return 3;
+  if (d.wh == 2 && d.ww == 2 && d.sh == 2 && d.sw == 2) return 2;
+  return 0;
+}
+
 void pool_forward(const float* x, float* y, const PoolDims& d, cudaStream_t s) {
   int64_t total = (int64_t)d.OH * d.OW * d.C * d.N;
   if (total == 0) return;
   count_launch();
-  pool_fwd_k<<<blocks_for(total, 256), 256, 0, s>>>(x, y, d);
+  switch (pool_fixed(d)) {
+    case 3: pool_max_fwd_launch<3, 3, 2, 2>(x, y, d, s); return;
+    case 2: pool_max_fwd_launch<2, 2, 2, 2>(x, y, d, s); return;
+    default: pool_fwd_k<<<blocks_for(total, 256), 256, 0, s>>>(x, y, d);
+  }
 }
 
 void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d, int acc,
@@ -810,6 +955,14 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
       configured = true;
     }
     const unsigned planes = (unsigned)((int64_t)d.C * d.N);
+    const int fx = pool_fixed(d);
+    if (fx && smem <= 48 * 1024) {
+      if (fx == 3 && acc) pool_max_bwd_t<3, 3, 2, 2, true><<<planes, 256, smem, s>>>(x, dy, dx, d);
+      if (fx == 3 && !acc) pool_max_bwd_t<3, 3, 2, 2, false><<<planes, 256, smem, s>>>(x, dy, dx, d);
+      if (fx == 2 && acc) pool_max_bwd_t<2, 2, 2, 2, true><<<planes, 256, smem, s>>>(x, dy, dx, d);
+      if (fx == 2 && !acc) pool_max_bwd_t<2, 2, 2, 2, false><<<planes, 256, smem, s>>>(x, dy, dx, d);
+      return;
+    }
     if (acc)
       pool_bwd_plane_k<true><<<planes, 256, smem, s>>>(x, dy, dx, d);
     else

@@ -174,6 +174,23 @@ def test_pool_bitexact(xs, pg):
     assert np.array_equal(host(dx), O.pool_backward(x, xs, pg, dy))
 
 
+@pytest.mark.parametrize("pg", POOLS[:3])
+def test_pool_shared_argmax_order(pg):
+    """Spikes at window corners are the argmax of up to 4 overlapping windows:
+    dx sums >= 3 contributions, so the (oj, oi) accumulation order shows."""
+    xs = (27, 27, 4, 3)
+    r = O.Rng(34)
+    x = r.uniform(O.size(xs), -0.01, 0.01).reshape(xs[::-1])
+    x[:, :, ::2, ::2] += 1.0 + r.uniform(x[:, :, ::2, ::2].size).reshape(x[:, :, ::2, ::2].shape)
+    x = x.ravel()
+    geom = B.PoolGeom(*pg[:8], mode="max" if pg[8] == 0 else "avg")
+    y_ref, ys = O.pool_forward(x, xs, pg)
+    assert np.array_equal(host(B.pool_forward(dev(x, xs), geom)), y_ref)
+    dy = r.uniform(O.size(ys), -1e3, 1e3) * r.uniform(O.size(ys), 0.5, 1.5) ** 20
+    dx = B.pool_backward(dev(x, xs), geom, dev(dy, ys))
+    assert np.array_equal(host(dx), O.pool_backward(x, xs, pg, dy))
+
+
 def test_relu_bitexact():
     r = O.Rng(34)
     for n in (1000, 1001, 4096 * 7 + 3):
