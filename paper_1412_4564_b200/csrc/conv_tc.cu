@@ -59,6 +59,7 @@ enum OpKind : int {
   OP_PLANE_K = 5,     // wgrad A: box (32 px, rows, 1) of padded planes [n][k][PL]
   OP_TILED_MN = 6,    // MN-major 2D tensor [K][MN] (MN inner): 32x32 boxes, SW128_32B atoms
   OP_IM2COL_MN = 7,   // wgrad B: im2col boxes of 32 px (K) x 32 ch (MN) per (tap, c block)
+  OP_SHIFT_MN = 8,    // wgrad B: 3D boxes {32 ch, 32 grid rows + tap shift, b_rows/32 blocks}
 };
 
 enum EpiKind : int {
@@ -102,7 +103,14 @@ struct GemmParams {
   int kpp;                // OP_PLANE_K / OP_SHIFT_K: K blocks (32 px) per image plane
   int b_rows;             // OP_SHIFT_K: channel rows per TMA box (divides Cgp and BN)
   int a_mn3d, b_mn3d;     // OP_TILED_MN: one 3D box per stage (MN % 32 == 0) vs R/32 2D boxes
-  int taps;               // OP_IM2COL_MN: fh * fw
+  int taps;               // OP_IM2COL_MN / halo kernel: fh * fw
+  // halo kernel (stride-1 conv on a padded pixel-major grid, see halo_conv_kernel)
+  int hg, hw_grid;        // grid pitch (rows per column) and rows per image; 0 = not a grid
+  int ohv, owv;           // valid output extent on the grid
+  int arows, abox, anbox; // halo rows per A stage, rows per A box, A boxes per stage
+  int TT;                 // taps per B stage
+  int SA, SB;             // A / B ring depths
+  unsigned long long* prof;  // debug (CK_HALO_PROF): per-CTA wait-cycle counters
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -210,6 +218,37 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// 3D box multicast to the CTAs of ctaMask (same smem offset, same mbarrier
+// offset in every destination CTA).
+__device__ __forceinline__ void tma_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                          int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+
+// MMA completion -> arrive on the mbarrier at this offset in every CTA of mask.
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -264,6 +303,102 @@ __device__ __forceinline__ Tile tile_at(const GemmParams& p, int t) {
   r.kb0 = r.split * per;
   r.kb1 = min(nkb, r.kb0 + per);
   return r;
+}
+
+// One output tile of the accumulator at TMEM column `tacc` -> global.
+// kEpiWarps warps: warp w reads TMEM lane quarter w & 3 (hardware rule) and
+// every (kEpiWarps/4)-th 32-column chunk, so two warps share a quarter.
+// Rows are GEMM rows m; with p.hg > 0 (halo kernels) m is a position on a
+// padded grid of pitch hg (hw_grid rows per image) and only positions with
+// (u, v) < (ohv, owv) are real outputs, at pixel u + ohv * v.
+__device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T, uint32_t tacc,
+                                              bool empty_split, int halves, int warp, int lane) {
+  const int q = warp & 3;
+  const int cpart = (warp - 2) / 4, cparts = kEpiWarps / 4;
+  float* out = p.out;
+  const bool partial = p.splits > 1;
+  if (partial) out += (int64_t)T.split * p.split_stride;
+  // plain stores: split-K partials, or no bias / relu / accumulate
+  const bool plain = partial || (!p.bias && !p.relu && !p.acc);
+  const int64_t ld = p.ld;
+  for (int h = 0; h < halves; ++h) {
+    int m = T.m0 + h * 128 + q * 32 + lane;
+    bool row_ok = m < p.M;
+    int img = 0, pix = 0;
+    if (p.hg > 0) {
+      img = m / p.hw_grid;
+      const int r = m - img * p.hw_grid;
+      const int v = r / p.hg, u = r - v * p.hg;
+      row_ok = row_ok && u < p.ohv && v < p.owv;
+      pix = u + p.ohv * v;
+    } else if (p.epi != EPI_LINEAR) {
+      img = m / p.epi_OHW;
+      pix = m - img * p.epi_OHW;
+    }
+    int64_t row_base = 0;
+    float rbias = 0.f;
+    int s_i = 0, s_j = 0;  // EPI_S2D: top-left target pixel of this row's s x s block
+    if (p.epi == EPI_S2D) {
+      const int v = pix / p.s2d_U, u = pix - v * p.s2d_U;
+      s_i = p.s2d * u;
+      s_j = p.s2d * v;
+      row_base = (int64_t)img * p.s2d_C * p.s2d_H * p.s2d_W;
+    } else if (p.epi == EPI_PIX) {
+      row_base = (int64_t)img * p.img_stride + pix + (int64_t)T.grp * p.grp_col * p.ld;
+    } else {
+      row_base = (int64_t)m + (int64_t)T.grp * p.grp_out;
+      if (p.bias && !partial && row_ok) rbias = p.bias[m + T.grp * p.grp_col];
+    }
+    for (int c0 = 32 * cpart; c0 < p.BN; c0 += 32 * cparts) {
+      uint32_t r[32];
+      const uint32_t taddr = tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * p.BN + c0);
+      CK_LD32(r, taddr);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (empty_split)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = 0u;
+      const int col0 = T.n0 + c0;
+      // columns of this chunk inside both the tile and the matrix
+      const int lim = min(min(32, p.BN - c0), p.n_valid - col0);
+      if (row_ok && lim > 0 && p.epi == EPI_S2D) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {  // static r[] indexing: keeps r in registers
+          const int col = col0 + j;
+          const int cg = p.s2d_C, abc = col / cg, c = col - abc * cg;
+          const int i = s_i + abc % p.s2d, jj = s_j + abc / p.s2d;
+          if (j < lim && i < p.s2d_H && jj < p.s2d_W) {
+            float* dst = out + row_base + i + (int64_t)p.s2d_H * (jj + (int64_t)p.s2d_W * c);
+            float v = __uint_as_float(r[j]);
+            if (!partial && p.acc) v = __fadd_rn(*dst, v);
+            *dst = v;
+          }
+        }
+      } else if (row_ok && lim > 0) {
+        float* dst = out + row_base + (int64_t)col0 * ld;
+        if (plain && lim == 32) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) dst[j * ld] = __uint_as_float(r[j]);
+        } else if (plain) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < lim) dst[j * ld] = __uint_as_float(r[j]);
+        } else {
+          const float* bcol = p.bias ? p.bias + col0 + T.grp * p.grp_col : nullptr;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (j < lim) {
+              float v = __uint_as_float(r[j]);
+              if (p.bias) v = __fadd_rn(v, p.epi == EPI_PIX ? __ldg(bcol + j) : rbias);
+              if (p.relu) v = v > 0.f ? v : 0.f;
+              if (p.acc) v = __fadd_rn(dst[j * ld], v);
+              dst[j * ld] = v;
+            }
+          }
+        }
+      }
+      __syncwarp();  // reconverge before the next warp-wide tcgen05.ld
+    }
+  }
 }
 
 // ============================================================================
@@ -377,6 +512,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             else
               for (int j = 0; j < p.BN / 32; ++j)
                 tma_2d(b + j * 4096, &tma_b, &full[s], mn0 + 32 * j, k0);
+          } else if (BK == OP_SHIFT_MN) {
+            // K block = 32 rows of the padded grid (pitch Hp); MN = (tap, c):
+            // one 3D box per tap, b_rows channels, rows shifted by the tap.
+            for (int j = 0; j < p.BN / p.b_rows; ++j) {
+              const int nn = T.n0 + j * p.b_rows;
+              int tap = nn / (p.cchunks * 32);
+              const int c = nn - tap * p.cchunks * 32;
+              tap = min(tap, p.taps - 1);  // columns past the last tap are masked
+              const int fj = tap / p.fh, fi = tap - fj * p.fh;
+              tma_3d(b + j * p.b_rows * 128, &tma_b, &full[s], 0, k0 + fi + p.Hp * fj,
+                     (T.grp * p.b_grp_c + c) / 32);
+            }
           } else if (BK == OP_IM2COL_MN) {
             // K block = 32 consecutive output pixels (h fastest, then w, n);
             // MN block j = 32 channels of tap (fi, fj): one im2col box each.
@@ -412,7 +559,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer --
     if (lane == 0) {
-      constexpr bool a_mn = AK == OP_TILED_MN, b_mn = BK == OP_TILED_MN || BK == OP_IM2COL_MN;
+      constexpr bool a_mn = AK == OP_TILED_MN,
+                     b_mn = BK == OP_TILED_MN || BK == OP_IM2COL_MN || BK == OP_SHIFT_MN;
       const uint32_t idesc = idesc_tf32(p.BN, a_mn, b_mn);
       int it = 0, tc = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
@@ -445,94 +593,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // ----------------------------------------------------------- epilogue --
-    // kEpiWarps warps: warp w reads TMEM lane quarter w & 3 (hardware rule)
-    // and every (kEpiWarps/4)-th 32-column chunk, so two warps share a quarter.
-    const int q = warp & 3;
-    const int cpart = (warp - 2) / 4, cparts = kEpiWarps / 4;
     int tc = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
       const Tile T = tile_at(p, t);
       const int ab = tc % p.nacc;
       const uint32_t aph = (tc / p.nacc) & 1;
-      const bool empty_split = T.kb0 >= T.kb1;  // no MMA issued: the tile is zero
       mbar_wait(&tfull[ab], aph);
       tc_fence_after();
-      float* out = p.out;
-      const bool partial = p.splits > 1;
-      if (partial) out += (int64_t)T.split * p.split_stride;
-      // plain stores: split-K partials, or no bias / relu / accumulate
-      const bool plain = partial || (!p.bias && !p.relu && !p.acc);
-      const int64_t ld = p.ld;
-      for (int h = 0; h < halves; ++h) {
-        const int m = T.m0 + h * 128 + q * 32 + lane;
-        const bool row_ok = m < p.M;
-        int64_t row_base = 0;
-        float rbias = 0.f;
-        int s_i = 0, s_j = 0;  // EPI_S2D: top-left target pixel of this row's s x s block
-        if (p.epi == EPI_S2D) {
-          const int img = m / p.epi_OHW;
-          const int r = m - img * p.epi_OHW;
-          const int v = r / p.s2d_U, u = r - v * p.s2d_U;
-          s_i = p.s2d * u;
-          s_j = p.s2d * v;
-          row_base = (int64_t)img * p.s2d_C * p.s2d_H * p.s2d_W;
-        } else if (p.epi == EPI_PIX) {
-          const int img = m / p.epi_OHW;
-          const int sp = m - img * p.epi_OHW;
-          row_base = (int64_t)img * p.img_stride + sp + (int64_t)T.grp * p.grp_col * p.ld;
-        } else {
-          row_base = (int64_t)m + (int64_t)T.grp * p.grp_out;
-          if (p.bias && !partial && row_ok) rbias = p.bias[m + T.grp * p.grp_col];
-        }
-        for (int c0 = 32 * cpart; c0 < p.BN; c0 += 32 * cparts) {
-          uint32_t r[32];
-          const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) +
-                                 (uint32_t)(ab * acc_cols + h * p.BN + c0);
-          CK_LD32(r, taddr);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (empty_split)
-#pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = 0u;
-          const int col0 = T.n0 + c0;
-          // columns of this chunk inside both the tile and the matrix
-          const int lim = min(min(32, p.BN - c0), p.n_valid - col0);
-          if (row_ok && lim > 0 && p.epi == EPI_S2D) {
-            for (int j = 0; j < lim; ++j) {
-              const int col = col0 + j;
-              const int cg = p.s2d_C, abc = col / cg, c = col - abc * cg;
-              const int i = s_i + abc % p.s2d, jj = s_j + abc / p.s2d;
-              if (i >= p.s2d_H || jj >= p.s2d_W) continue;
-              float* dst = out + row_base + i + (int64_t)p.s2d_H * (jj + (int64_t)p.s2d_W * c);
-              float v = __uint_as_float(r[j]);
-              if (!partial && p.acc) v = __fadd_rn(*dst, v);
-              *dst = v;
-            }
-          } else if (row_ok && lim > 0) {
-          float* dst = out + row_base + (int64_t)col0 * ld;
-          if (plain && lim == 32) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) dst[j * ld] = __uint_as_float(r[j]);
-          } else if (plain) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (j < lim) dst[j * ld] = __uint_as_float(r[j]);
-          } else {
-            const float* bcol = p.bias ? p.bias + col0 + T.grp * p.grp_col : nullptr;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j < lim) {
-                float v = __uint_as_float(r[j]);
-                if (p.bias) v = __fadd_rn(v, p.epi == EPI_PIX ? __ldg(bcol + j) : rbias);
-                if (p.relu) v = v > 0.f ? v : 0.f;
-                if (p.acc) v = __fadd_rn(dst[j * ld], v);
-                dst[j * ld] = v;
-              }
-            }
-          }
-          }
-          __syncwarp();  // reconverge before the next warp-wide tcgen05.ld
-        }
-      }
+      epilogue_tile(p, T, tmem + (uint32_t)(ab * acc_cols), T.kb0 >= T.kb1, halves, warp, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
@@ -540,6 +608,214 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
+  }
+}
+
+// ============================================================================
+//                      halo kernel (stride-1 implicit GEMM)
+// ============================================================================
+// A stride-1 convolution over a zero-padded pixel-major grid P[row][Cp]
+// (row = n * hw_grid + i + hg * j) is
+//     Y[q, k] = sum_{tap, c} P[q + fi + hg * fj, c] * F[k, tap, c]
+// for grid rows q (rows whose (u, v) fall outside the valid output extent
+// are computed and dropped).  Per 32-channel chunk a CTA loads ONE halo tile
+// of rows [q0, q0 + BM + maxshift) and feeds every tap from it by moving the
+// UMMA descriptor start by shift * 128 B (the SWIZZLE_128B pattern is keyed
+// on address bits, tools/shift_probe.cu) -- the activation operand is read
+// once per chunk instead of once per tap.  Filters stream as 3D boxes of TT
+// taps x BN rows x 32 channels from F laid [row][tap][Cgp].
+// Warp roles as tc_gemm_kernel; A and B have separate mbarrier rings.
+// CS = 2: clusters of two CTAs on vertically adjacent M tiles share every
+// filter stage -- each loads half the taps of the stage and multicasts it
+// to both, and a stage is refilled once both CTAs' MMAs released it.
+template <int CS>
+__global__ void __launch_bounds__(kThreads, 1)
+    halo_conv_kernel(const __grid_constant__ CUtensorMap tma_a,
+                     const __grid_constant__ CUtensorMap tma_b, const GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int halves = p.BM / 128;
+  const int stage_a = p.anbox * p.abox * 128;
+  const int stage_b = p.TT * p.BN * 128;
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + p.SA * stage_a;
+  uint64_t* fullA = (uint64_t*)(sB + p.SB * stage_b);
+  uint64_t* emptyA = fullA + p.SA;
+  uint64_t* fullB = emptyA + p.SA;
+  uint64_t* emptyB = fullB + p.SB;
+  uint64_t* tfull = emptyB + p.SB;  // [2]
+  uint64_t* tempty = tfull + 2;     // [2]
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tm = (p.M + p.BM - 1) / p.BM, tn = (p.N + p.BN - 1) / p.BN;
+  const int tmc = (tm + CS - 1) / CS;  // M tiles per cluster row
+  const int total = tmc * tn * p.groups;  // cluster work items
+  const int rank = CS > 1 ? (int)cluster_rank() : 0;
+  const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+  const uint16_t cmask = (uint16_t)((1u << CS) - 1);
+  const int acc_cols = halves * p.BN;
+  const int need = p.nacc * acc_cols;
+  const int ncols = need <= 32 ? 32 : need <= 64 ? 64 : need <= 128 ? 128 : need <= 256 ? 256 : 512;
+  const int chunks = p.cchunks;
+  const int ntg = (p.taps + p.TT - 1) / p.TT;
+  const int tt_part = p.TT / CS;  // taps of each stage this CTA loads
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < p.SA; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 1);
+    }
+    for (int s = 0; s < p.SB; ++s) {
+      mbar_init(&fullB[s], 1);
+      mbar_init(&emptyB[s], CS);  // released by the MMAs of every CTA it feeds
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tma_b) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (CS > 1) cluster_sync();  // peers' barriers are initialised before any multicast
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  auto tile_of = [&](int t) {
+    Tile T;
+    const int mt = (t % tmc) * CS + rank, rest = t / tmc;
+    T.m0 = mt * p.BM;
+    T.n0 = (rest % tn) * p.BN;
+    T.grp = rest / tn;
+    T.split = 0;
+    T.kb0 = 0;
+    T.kb1 = 1;
+    return T;
+  };
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer --
+    if (lane == 0) {
+      int ia = 0, ib = 0;
+      for (int t = cid; t < total; t += ncl) {
+        const Tile T = tile_of(t);
+        for (int cc = 0; cc < chunks; ++cc) {
+          const int sa = ia % p.SA;
+          mbar_wait(&emptyA[sa], ((ia / p.SA) & 1) ^ 1);
+          mbar_expect_tx(&fullA[sa], stage_a);
+          const int c = T.grp * p.a_grp_c + cc * 32;
+          for (int bx = 0; bx < p.anbox; ++bx)
+            tma_2d(sA + sa * stage_a + bx * p.abox * 128, &tma_a, &fullA[sa], c,
+                   T.m0 + bx * p.abox);
+          ++ia;
+          for (int tg = 0; tg < ntg; ++tg) {
+            const int sb = ib % p.SB;
+            mbar_wait(&emptyB[sb], ((ib / p.SB) & 1) ^ 1);
+            mbar_expect_tx(&fullB[sb], stage_b);
+            if (CS > 1)
+              tma_3d_mc(sB + sb * stage_b + rank * tt_part * p.BN * 128, &tma_b, &fullB[sb],
+                        cc * 32, T.n0 + T.grp * p.b_grp_row, tg * p.TT + rank * tt_part, cmask);
+            else
+              tma_3d(sB + sb * stage_b, &tma_b, &fullB[sb], cc * 32, T.n0 + T.grp * p.b_grp_row,
+                     tg * p.TT);
+            ++ib;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // --------------------------------------------------------- MMA issuer --
+    if (lane == 0) {
+      const uint32_t idesc = idesc_tf32(p.BN, 0, 0);
+      int ia = 0, ib = 0, tc = 0;
+      unsigned long long w_t = 0, w_a = 0, w_b = 0, t_start = clock64();
+      for (int t = cid; t < total; t += ncl, ++tc) {
+        const int ab = tc % p.nacc;
+        unsigned long long c0 = clock64();
+        mbar_wait(&tempty[ab], ((tc / p.nacc) & 1) ^ 1);
+        w_t += clock64() - c0;
+        tc_fence_after();
+        const uint32_t dcol = tmem + (uint32_t)(ab * acc_cols);
+        for (int cc = 0; cc < chunks; ++cc) {
+          const int sa = ia % p.SA;
+          unsigned long long c1 = clock64();
+          mbar_wait(&fullA[sa], (ia / p.SA) & 1);
+          w_a += clock64() - c1;
+          tc_fence_after();
+          const uint32_t a = smem_u32(sA + sa * stage_a);
+          for (int tg = 0; tg < ntg; ++tg) {
+            const int sb = ib % p.SB;
+            unsigned long long c2 = clock64();
+            mbar_wait(&fullB[sb], (ib / p.SB) & 1);
+            w_b += clock64() - c2;
+            tc_fence_after();
+            const uint32_t b = smem_u32(sB + sb * stage_b);
+            for (int u = 0; u < p.TT; ++u) {
+              const int tap = tg * p.TT + u;
+              if (tap >= p.taps) break;
+              const int fj = tap / p.fh, fi = tap - fj * p.fh;
+              const uint32_t shift = (uint32_t)(fi + p.hg * fj) * 128u;
+              for (int h = 0; h < halves; ++h) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint32_t acc = (cc > 0 || tap > 0 || k > 0) ? 1u : 0u;
+                  mma_tf32(dcol + h * p.BN,
+                           sdesc(a + (uint32_t)h * 16384u + shift + k * 32, 16, 1024),
+                           sdesc(b + (uint32_t)(u * p.BN * 128) + k * 32, 16, 1024), idesc, acc);
+                }
+              }
+            }
+            if (CS > 1)
+              mma_commit_mc(&emptyB[sb], cmask);
+            else
+              mma_commit(&emptyB[sb]);
+            ++ib;
+          }
+          mma_commit(&emptyA[sa]);
+          ++ia;
+        }
+        mma_commit(&tfull[ab]);
+      }
+      if (p.prof) {
+        unsigned long long* o = p.prof + blockIdx.x * 4;
+        o[0] = clock64() - t_start;
+        o[1] = w_t;
+        o[2] = w_a;
+        o[3] = w_b;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ----------------------------------------------------------- epilogue --
+    int tc = 0;
+    for (int t = cid; t < total; t += ncl, ++tc) {
+      const Tile T = tile_of(t);
+      const int ab = tc % p.nacc;
+      mbar_wait(&tfull[ab], (tc / p.nacc) & 1);
+      tc_fence_after();
+      epilogue_tile(p, T, tmem + (uint32_t)(ab * acc_cols), false, halves, warp, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[ab]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (CS > 1) cluster_sync();  // no CTA leaves while a peer may still signal its barriers
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
@@ -574,6 +850,53 @@ __global__ void to_pixel_major_k(const float* __restrict__ x, float* __restrict_
   for (int r = ty; r < 32; r += 8) {
     const int p = p0 + r, cp = c0 + tx;
     if (p < HW && cp < Cp) xt[((int64_t)n * HW + p) * Cp + cp] = tile[tx][r];
+  }
+}
+
+// HWCN x[n][c][w][h] -> padded pixel-major grid xg[n][Wg][Hg][cp]: pixel
+// (i, j) at grid position (i + oh, j + ow), channel c of group g at
+// cp = g*Cgp + (c - g*Cgp_local); zero borders and channel pads (the input of
+// halo_conv_kernel).  32 x 32 smem tile transpose.
+__global__ void to_grid_pm_k(const float* __restrict__ x, float* __restrict__ xg, int H, int W,
+                             int C, int Cg, int Cgp, int groups, int Hg, int Wg, int oh, int ow) {
+  // tile: 64 grid pixels x 32 padded channels; loads coalesced along pixels
+  // (two per channel row per thread), stores as float4 along channels.
+  __shared__ float tile[32][65];
+  const int n = blockIdx.z;
+  const int p0 = blockIdx.x * 64, c0 = blockIdx.y * 32;
+  const int Cp = Cgp * groups, HWg = Hg * Wg;
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  int64_t src[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int P = p0 + lane + 32 * k;
+    const int jj = P / Hg, ii = P - jj * Hg;
+    const int i = ii - oh, j = jj - ow;
+    src[k] = (P < HWg && i >= 0 && i < H && j >= 0 && j < W) ? (int64_t)j * H + i : -1;
+  }
+  const float* xn = x + (int64_t)n * C * H * W;
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = warp + 8 * rr;
+    const int cp = c0 + r;
+    const int g = cp / Cgp, cl = cp - g * Cgp;
+    const bool ch_ok = cp < Cp && cl < Cg;
+    const float* xc = xn + (int64_t)(g * Cg + cl) * H * W;
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      tile[r][lane + 32 * k] = (ch_ok && src[k] >= 0) ? __ldg(xc + src[k]) : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int idx = threadIdx.x + 256 * k;
+    const int pr = idx / 8, q = idx % 8;
+    const int P = p0 + pr, cp = c0 + 4 * q;
+    if (P < HWg && cp < Cp) {
+      const float4 v = make_float4(tile[4 * q][pr], tile[4 * q + 1][pr], tile[4 * q + 2][pr],
+                                   tile[4 * q + 3][pr]);
+      *reinterpret_cast<float4*>(xg + ((int64_t)n * HWg + P) * Cp + cp) = v;
+    }
   }
 }
 
@@ -1036,7 +1359,7 @@ static bool load_driver() {
 bool conv_tc_available() { return load_driver(); }
 
 struct TcState {
-  Workspace xt, dyt, ft, part;
+  Workspace xt, dyt, ft, part, dyg;
   // dy in pixel-major layout is shared by wgrad and dgrad of one
   // ck_conv_backward call: cached by (source, geometry, call id).
   const float* dyt_src = nullptr;
@@ -1055,6 +1378,7 @@ void conv_tc_release(ck_handle* h) {
   h->tc->dyt.release();
   h->tc->ft.release();
   h->tc->part.release();
+  h->tc->dyg.release();
   delete h->tc;
   h->tc = nullptr;
 }
@@ -1115,7 +1439,12 @@ static int pick_bn(int n) {
 // Tile M: two M=128 MMAs per CTA (sharing each B tile) once M is large.
 // Keep TMEM double-buffered (2 x BM/128 x BN <= 512 columns) so the epilogue
 // of one tile overlaps the next tile's mainloop.
-static int pick_bm(int64_t M, int BN) { return (M >= 4096 && BN <= 128) ? 256 : 128; }
+static int pick_bm(int64_t M, int BN) {
+  static const int mode = getenv("CK_TC_BM") ? atoi(getenv("CK_TC_BM")) : 0;  // experiments
+  if (mode == 256) return M >= 4096 ? 256 : 128;
+  if (mode == 128) return 128;
+  return (M >= 4096 && BN <= 128) ? 256 : 128;
+}
 
 template <int AK, int BK>
 static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int grid_m,
@@ -1180,12 +1509,13 @@ static void* grow(Workspace& w, size_t bytes, cudaStream_t s) {
   return p;
 }
 
+static void to_grid_pm(const float* x, float* xg, int H, int W, int C, int N, int Cg, int Cgp,
+                       int groups, int Hg, int Wg, int oh, int ow, cudaStream_t s);
+
+// pixel-major [n][w][h][cp] = the padding-free grid
 static void to_pm(const float* x, float* xt, int H, int W, int C, int N, int Cg, int Cgp,
                   int groups, cudaStream_t s) {
-  const int HW = H * W;
-  dim3 grid((HW + 31) / 32, (Cgp * groups + 31) / 32, N);
-  count_launch();
-  to_pixel_major_k<<<grid, 256, 0, s>>>(x, xt, HW, C, Cg, Cgp, groups);
+  to_grid_pm(x, xt, H, W, C, N, Cg, Cgp, groups, H, W, 0, 0, s);
 }
 
 // dy in pixel-major layout [n][ow][oh][groups * Kgp]; wgrad and dgrad of one
@@ -1203,6 +1533,169 @@ static float* dy_pm(ck_handle* h, const float* dy, const ConvDims& d, int Kg, in
   st->dyt_call = h->call;
   st->dyt_key = key;
   return buf;
+}
+
+static void to_grid_pm(const float* x, float* xg, int H, int W, int C, int N, int Cg, int Cgp,
+                       int groups, int Hg, int Wg, int oh, int ow, cudaStream_t s) {
+  dim3 grid((Hg * Wg + 63) / 64, (Cgp * groups + 31) / 32, N);
+  count_launch();
+  to_grid_pm_k<<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow);
+}
+
+static bool halo_enabled() {
+  // Off by default: measured slower than the im2col kernels on AlexNet
+  // (junk grid rows + per-tap filter streaming), kept for experiments.
+  static const int on = getenv("CK_TC_HALO") ? atoi(getenv("CK_TC_HALO")) : 0;
+  return on != 0;
+}
+
+static CUtensorMap encode_tiled(const float* base, int rank, const cuuint64_t* dims,
+                                const cuuint64_t* strides_bytes, const cuuint32_t* box,
+                                CUtensorMapSwizzle swz);
+
+// Operands of one halo_conv_kernel launch: the padded grid (A) and the
+// filter bank laid [row][tap][Cgp] (B), with `rows` output channels per group.
+struct HaloConv {
+  const float* grid;
+  int Cp, Hg, Wg, N;   // grid [N][Wg][Hg][Cp]
+  const float* filt;
+  int Cgp, taps, fh, fw, rows, groups;
+  int ohv, owv;        // valid output extent on the grid
+};
+
+// Whether halo_launch can run this shape (same sizing rules).
+static bool halo_ok(int rows, int fh, int fw, int Hg) {
+  if (!halo_enabled()) return false;
+  const int BN = pick_bn(rows);
+  if (BN > 256 || BN % 16) return false;
+  const int arows = rup(256 + (fh - 1) + Hg * (fw - 1), 8);  // BM <= 256
+  const int anbox = (arows + 255) / 256;
+  const int stage_a = anbox * rup((arows + anbox - 1) / anbox, 8) * 128;
+  return 227 * 1024 - 2048 - 2 * stage_a >= 2 * BN * 128;
+}
+
+// p carries the epilogue fields (epi, out, ld, img_stride, grp_col, bias, relu,
+// acc, s2d_*); returns false when the shape does not fit the kernel.
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+static bool halo_launch(const HaloConv& hc, GemmParams p, cudaStream_t s) {
+  if (!halo_enabled()) return false;
+  static const int bm_env = env_int("CK_HALO_BM", 256), sb_env = env_int("CK_HALO_SB", 3),
+                   tt_env = env_int("CK_HALO_TT", 0), cs_env = env_int("CK_HALO_CS", 2),
+                   bn_env = env_int("CK_HALO_BN", 0);
+  const int BM = bm_env == 128 ? 128 : 256, halves = BM / 128;
+  const int BN = bn_env > 0 && bn_env < hc.rows ? bn_env : pick_bn(hc.rows);
+  if (BN > 256 || BN % 16) return false;
+  const int maxshift = (hc.fh - 1) + hc.Hg * (hc.fw - 1);
+  const int arows = rup(BM + maxshift, 8);
+  const int anbox = (arows + 255) / 256;
+  const int abox = rup((arows + anbox - 1) / anbox, 8);
+  const int stage_a = anbox * abox * 128;
+  const int budget = 227 * 1024 - 2048;
+  const int SA = 2;
+  const int bud_b = budget - SA * stage_a;
+  int SB = sb_env;
+  int tt_max = bud_b / (SB * BN * 128);
+  if (tt_max < 1) {
+    SB = 2;
+    tt_max = bud_b / (SB * BN * 128);
+  }
+  if (tt_max < 1) return false;
+  tt_max = std::min(tt_max, hc.taps);
+  if (tt_env > 0) tt_max = std::min(tt_max, tt_env);
+  const int ngroups = (hc.taps + tt_max - 1) / tt_max;
+  int TT = (hc.taps + ngroups - 1) / ngroups;
+  // clusters of 2 split every filter stage in two tap halves: TT even
+  const int CS = (cs_env == 2 && tt_max >= 2) ? 2 : 1;
+  if (CS == 2 && TT % 2) TT = TT + 1 <= tt_max ? TT + 1 : TT - 1;
+  const int64_t rows_total = (int64_t)hc.N * hc.Hg * hc.Wg;
+  if (rows_total + abox * anbox > INT32_MAX) return false;
+  p.M = (int)rows_total;
+  p.N = hc.rows;
+  p.BM = BM;
+  p.BN = BN;
+  p.splits = 1;
+  p.groups = hc.groups;
+  p.nacc = (2 * halves * BN <= 512) ? 2 : 1;
+  p.hg = hc.Hg;
+  p.hw_grid = hc.Hg * hc.Wg;
+  p.ohv = hc.ohv;
+  p.owv = hc.owv;
+  p.cchunks = hc.Cgp / 32;
+  p.a_grp_c = hc.Cgp;
+  p.b_grp_row = hc.rows;
+  p.taps = hc.taps;
+  p.fh = hc.fh;
+  p.TT = TT;
+  p.SA = SA;
+  p.SB = SB;
+  p.arows = arows;
+  p.abox = abox;
+  p.anbox = anbox;
+  p.n_valid = hc.rows;
+  CUtensorMap ta = map_2d(hc.grid, hc.Cp, (uint64_t)rows_total, hc.Cp, abox);
+  cuuint64_t dims[3] = {(cuuint64_t)hc.Cgp, (cuuint64_t)hc.rows * hc.groups, (cuuint64_t)hc.taps};
+  cuuint64_t strides[2] = {(cuuint64_t)hc.taps * hc.Cgp * 4, (cuuint64_t)hc.Cgp * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)BN, (cuuint32_t)(TT / CS)};
+  CUtensorMap tb = encode_tiled(hc.filt, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  const size_t smem = 1024 + (size_t)SA * stage_a + (size_t)SB * TT * BN * 128 + 256;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(halo_conv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    cudaFuncSetAttribute(halo_conv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    configured = true;
+  }
+  const int tm = (p.M + BM - 1) / BM;
+  const int items = ((tm + CS - 1) / CS) * ((p.N + BN - 1) / BN) * hc.groups;
+  static const int prof = env_int("CK_HALO_PROF", 0);
+  static unsigned long long* prof_buf = nullptr;
+  if (prof && !prof_buf) cudaMalloc(&prof_buf, 148 * 4 * sizeof(unsigned long long));
+  p.prof = prof ? prof_buf : nullptr;
+  if (prof) cudaMemsetAsync(prof_buf, 0, 148 * 4 * sizeof(unsigned long long), s);
+  struct ProfDump {
+    unsigned long long* buf;
+    cudaStream_t s;
+    int M, N, BN, TT, SB;
+    ~ProfDump() {
+      if (!buf) return;
+      unsigned long long h[148 * 4];
+      cudaStreamSynchronize(s);
+      cudaMemcpy(h, buf, sizeof(h), cudaMemcpyDeviceToHost);
+      double tot = 0, wt = 0, wa = 0, wb = 0;
+      int n = 0;
+      for (int i = 0; i < 148; ++i)
+        if (h[i * 4]) {
+          tot += h[i * 4]; wt += h[i * 4 + 1]; wa += h[i * 4 + 2]; wb += h[i * 4 + 3]; ++n;
+        }
+      fprintf(stderr, "[halo] M=%d N=%d BN=%d TT=%d SB=%d ctas=%d mma-thread cycles %.0f: wait tempty %.1f%% fullA %.1f%% fullB %.1f%%\n",
+              M, N, BN, TT, SB, n, tot / n, 100 * wt / tot, 100 * wa / tot, 100 * wb / tot);
+    }
+  } dump{prof ? prof_buf : nullptr, s, p.M, p.N, BN, TT, SB};
+  count_launch();
+  if (CS == 1) {
+    halo_conv_kernel<1><<<std::min(items, 148), kThreads, smem, s>>>(ta, tb, p);
+    return true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * std::min(items, 74));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, halo_conv_kernel<2>, ta, tb, p) != cudaSuccess)
+    throw Err(CK_ERR_CUDA, "halo_conv_kernel cluster launch failed");
+  return true;
 }
 
 static void transpose(const float* in, float* out, int R, int Cc, int64_t ldi, int64_t ldo,
@@ -1331,6 +1824,15 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   count_launch();
   s2d_repack_fprop_k<<<blocks_for((int64_t)d.K * taps * z.Csp), 256, 0, s>>>(
       f, ft, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Tw, z.Csp);
+  if (halo_ok(d.K, z.Th, z.Tw, z.U)) {
+    // the s2d pixel-major tensor is already a (pad-free) grid of pitch U
+    GemmParams p{};
+    p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+    p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = d.K;
+    p.bias = bias; p.relu = relu; p.acc = 0;
+    HaloConv hc{xt, z.Csp, z.U, z.V, d.N, ft, z.Csp, taps, z.Th, z.Tw, d.K, 1, d.OH, d.OW};
+    if (halo_launch(hc, p, s)) return;
+  }
   GemmParams p{};
   p.M = d.N * d.OH * d.OW; p.N = d.K; p.K = taps * z.Csp; p.BN = pick_bn(d.K); p.splits = 1;
   p.OH = d.OH; p.OW = d.OW; p.sh = 1; p.sw = 1; p.pt = 0; p.pl = 0; p.fh = z.Th;
@@ -1349,11 +1851,24 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   TcState* st = state(h);
   const int taps = z.Th * z.Tw;
   const int Kp = rup(d.K, 32);
-  float* dyt = dy_pm(h, dy, d, d.K, Kp, 1, s);
   float* gt = (float*)grow(st->ft, sizeof(float) * (size_t)z.Cs * taps * Kp, s);
   count_launch();
   s2d_repack_dgrad_k<<<blocks_for((int64_t)z.Cs * taps * Kp), 256, 0, s>>>(
       f, gt, d.fh, d.fw, d.C, d.K, Kp, z.s, z.Th, z.Tw);
+  const int Hq = d.OH + 2 * (z.Th - 1), Wq = d.OW + 2 * (z.Tw - 1);
+  if (halo_ok(z.Cs, z.Th, z.Tw, Hq)) {
+    // dx_s2d = stride-1 conv of dy zero-padded by (Th-1, Tw-1) with the
+    // flipped bank, on a grid of pitch Hq; EPI_S2D scatters back to x.
+    float* dyg = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hq * Wq * Kp, s);
+    to_grid_pm(dy, dyg, d.OH, d.OW, d.K, d.N, d.K, Kp, 1, Hq, Wq, z.Th - 1, z.Tw - 1, s);
+    GemmParams p{};
+    p.epi = EPI_S2D; p.out = dx;
+    p.s2d = z.s; p.s2d_U = z.U; p.s2d_H = d.H; p.s2d_W = d.W; p.s2d_C = d.C;
+    p.acc = acc;
+    HaloConv hc{dyg, Kp, Hq, Wq, d.N, gt, Kp, taps, z.Th, z.Tw, z.Cs, 1, z.U, z.V};
+    if (halo_launch(hc, p, s)) return;
+  }
+  float* dyt = dy_pm(h, dy, d, d.K, Kp, 1, s);
   GemmParams p{};
   p.M = d.N * z.U * z.V; p.N = z.Cs; p.K = taps * Kp; p.BN = pick_bn(z.Cs); p.splits = 1;
   p.OH = z.U; p.OW = z.V; p.sh = 1; p.sw = 1; p.pt = z.Th - 1; p.pl = z.Tw - 1; p.fh = z.Th;
@@ -1370,6 +1885,52 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
 
 static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, cudaStream_t s);
 
+static bool wgrid_enabled() {
+  static const int on = getenv("CK_TC_WGRID") ? atoi(getenv("CK_TC_WGRID")) : 1;
+  return on != 0;
+}
+
+// Weight gradient on a padded grid (stride-1 conv; x at its padding offset in
+// an Hg x Wg grid, dy at (0, 0) of the same grid with zeros elsewhere):
+//   part[s][g][(tap, c)][k] = sum_{grid rows q of split s} dYg[q, k] Xg[q + fi + Hg*fj, c]
+// A = dYg read MN-major (one 3D box of BM channels x 32 rows); B = Xg rows
+// shifted by the tap, one 3D box per tap of b_rows channels (tiled TMA, no
+// im2col).  Junk grid rows carry dy = 0.  Returns the split count.
+static int grid_wgrad(ck_handle* h, const float* xg, int Cp, int Cgp, const float* dyg, int Kp,
+                      int Kgp, int Kg, int groups, int N, int Hg, int Wg, int fh, int fw,
+                      float** part_out, int64_t* per_out, cudaStream_t s) {
+  TcState* st = state(h);
+  const int taps = fh * fw;
+  const int Ntot = taps * Cgp;  // GEMM N = (tap, c) per group
+  const int BN = (Cgp >= 128 && Cgp <= 256) ? Cgp : std::min(256, rup(Ntot, 32));
+  const int b_rows = std::min(256, std::gcd(Cgp, BN));
+  const int BM = pick_bm(Kg, BN);
+  const int64_t rows = (int64_t)N * Hg * Wg;
+  const int kblocks = (int)((rows + 31) / 32);
+  const int splits = wgrad_splits_for(((Kg + BM - 1) / BM) * ((Ntot + BN - 1) / BN) * groups,
+                                      kblocks);
+  const int64_t per_grp = (int64_t)Ntot * Kg;
+  const int64_t per = per_grp * groups;
+  float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
+  GemmParams p{};
+  p.M = Kg; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.BM = BM; p.splits = splits;
+  p.Hp = Hg; p.fh = fh; p.taps = taps; p.cchunks = Cgp / 32; p.b_rows = b_rows;
+  p.a_grp_mn = Kgp;
+  p.b_grp_c = Cgp;
+  // raw partials: part[s*per + g*per_grp + n*Kg + k]
+  p.epi = EPI_LINEAR; p.out = part; p.ld = Kg; p.grp_out = per_grp; p.n_valid = Ntot;
+  p.split_stride = per;
+  CUtensorMap ta = map_mn(dyg, (uint64_t)rows, Kp, Kp, BM, &p.a_mn3d);
+  cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(Cp / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)Cp * 4, 128};
+  cuuint32_t box[3] = {32, 32, (cuuint32_t)(b_rows / 32)};
+  CUtensorMap tb = encode_tiled(xg, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  launch<OP_TILED_MN, OP_SHIFT_MN>(ta, tb, p, 0, 0, groups * splits, s);
+  *part_out = part;
+  *per_out = per;
+  return splits;
+}
+
 // Strided wgrad through space-to-depth: the stride-1 im2col wgrad (see
 // conv_tc_wgrad) over the s2d pixel-major input, then the s2d filter scatter.
 static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, const ConvDims& d,
@@ -1379,6 +1940,19 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   const int Kp = rup(d.K, 32);
   float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * z.U * z.V * z.Csp, s);
   s2d_pm(x, xt, d, z, s);
+  if (wgrid_enabled()) {
+    // the s2d tensor is a pad-free grid of pitch U; dy goes to (0, 0) of it
+    float* dyg = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * z.U * z.V * Kp, s);
+    to_grid_pm(dy, dyg, d.OH, d.OW, d.K, d.N, d.K, Kp, 1, z.U, z.V, 0, 0, s);
+    float* part;
+    int64_t per;
+    const int splits = grid_wgrad(h, xt, z.Csp, z.Csp, dyg, Kp, Kp, d.K, 1, d.N, z.U, z.V, z.Th,
+                                  z.Tw, &part, &per, s);
+    count_launch();
+    s2d_wgrad_finish_k<<<blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s>>>(
+        part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc);
+    return;
+  }
   float* dyt = dy_pm(h, dy, d, d.K, Kp, 1, s);
   const int Ntot = taps * z.Csp;
   const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
@@ -1450,12 +2024,24 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
   const int taps = d.fh * d.fw;
   if (d.pt > 127 || d.pl > 127 || d.fh > 128 || d.fw > 128) return false;
   TcState* st = state(h);
-  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
   float* ft = (float*)grow(st->ft, sizeof(float) * (size_t)d.K * taps * Cgp, s);
-  to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
   count_launch();
   repack_fprop_k<<<std::min<int64_t>(((int64_t)d.K * taps * Cgp + 255) / 256, 148 * 8), 256, 0, s>>>(
       f, ft, d.fh, d.fw, d.Cg, Cgp, d.K, d.fsc, d.fsk);
+  const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
+  if (d.sh == 1 && d.sw == 1 && halo_ok(Kg, d.fh, d.fw, Hg)) {
+    // halo kernel over the zero-padded pixel-major grid (Hg x Wg per image)
+    float* xg = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * Hg * Wg * Cp, s);
+    to_grid_pm(x, xg, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, Hg, Wg, d.pt, d.pl, s);
+    GemmParams p{};
+    p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+    p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg;
+    p.bias = bias; p.relu = relu; p.acc = 0;
+    HaloConv hc{xg, Cp, Hg, Wg, d.N, ft, Cgp, taps, d.fh, d.fw, Kg, d.groups, d.OH, d.OW};
+    if (halo_launch(hc, p, s)) return true;
+  }
+  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
+  to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
   GemmParams p{};
   p.M = d.N * d.OH * d.OW;
   p.N = Kg;
@@ -1523,12 +2109,25 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
   const int taps = d.fh * d.fw;
   TcState* st = state(h);
-  float* dyt = dy_pm(h, dy, d, Kg, Kgp, d.groups, s);
   float* gt = (float*)grow(st->ft, sizeof(float) * (size_t)d.C * taps * Kgp, s);
   count_launch();
   repack_dgrad_k<<<std::min<int64_t>(((int64_t)d.C * taps * Kgp + 255) / 256, 148 * 8), 256, 0, s>>>(
       f, gt, d.fh, d.fw, d.Cg, Kg, Kgp, d.groups, d.fsc, d.fsk);
   const int qt = d.fh - 1 - d.pt, qb = d.fh - 1 - d.pb, ql = d.fw - 1 - d.pl, qr = d.fw - 1 - d.pr;
+  const int Hq = d.OH + qt + qb, Wq = d.OW + ql + qr;
+  if (halo_ok(d.Cg, d.fh, d.fw, Hq)) {
+    // halo kernel: dy zero-padded by (fh-1-pt, ...) on a grid of pitch Hq,
+    // convolved with the flipped bank; the valid rows are the H x W of dx.
+    float* dyg = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hq * Wq * Kp, s);
+    to_grid_pm(dy, dyg, d.OH, d.OW, d.K, d.N, Kg, Kgp, d.groups, Hq, Wq, qt, ql, s);
+    GemmParams p{};
+    p.epi = EPI_PIX; p.out = dx; p.ld = (int64_t)d.H * d.W;
+    p.img_stride = (int64_t)d.C * d.H * d.W; p.grp_col = d.Cg;
+    p.bias = nullptr; p.relu = 0; p.acc = acc;
+    HaloConv hc{dyg, Kp, Hq, Wq, d.N, gt, Kgp, taps, d.fh, d.fw, d.Cg, d.groups, d.H, d.W};
+    if (halo_launch(hc, p, s)) return true;
+  }
+  float* dyt = dy_pm(h, dy, d, Kg, Kgp, d.groups, s);
   GemmParams p{};
   p.M = d.N * d.H * d.W;
   p.N = d.Cg;
@@ -1588,6 +2187,22 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
   const int taps = d.fh * d.fw;
   TcState* st = state(h);
+  if (wgrid_enabled()) {
+    const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
+    float* xg = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * Hg * Wg * Cp, s);
+    to_grid_pm(x, xg, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, Hg, Wg, d.pt, d.pl, s);
+    float* dyg = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hg * Wg * Kp, s);
+    to_grid_pm(dy, dyg, d.OH, d.OW, d.K, d.N, Kg, Kgp, d.groups, Hg, Wg, 0, 0, s);
+    float* part;
+    int64_t per;
+    const int splits = grid_wgrad(h, xg, Cp, Cgp, dyg, Kp, Kgp, Kg, d.groups, d.N, Hg, Wg, d.fh,
+                                  d.fw, &part, &per, s);
+    const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
+    count_launch();
+    wgrad_finish_k<<<std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
+        part, df, d.fh, d.fw, d.Cg, Cgp, Kg, d.groups, splits, per, d.fsc, d.fsk, acc);
+    return true;
+  }
   float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
   to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
   float* dyt = dy_pm(h, dy, d, Kg, Kgp, d.groups, s);

@@ -1,0 +1,173 @@
+// Probe: can a K-major SWIZZLE_128B UMMA operand start at an arbitrary ROW of
+// a swizzled tile (start address + r0*128 B), i.e. can one halo tile feed
+// several filter taps?  A is written as TMA would (row r at r*128, 16-B chunk
+// c stored at c ^ (r & 7), tile base 1024-B aligned); the MMA reads rows
+// r0 .. r0+127.  Variants: descriptor base_offset field = 0 or (r0 & 7).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -o tools/shift_probe.bin tools/shift_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <cmath>
+#include <vector>
+#include <cuda_runtime.h>
+
+constexpr int M = 128, N = 64, K = 32, MR = M + 16;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t base_off) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(base_off & 7) << 49;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+__device__ __forceinline__ uint32_t off_k(int r, int k) {
+  return (uint32_t)(r * 128 + (((k >> 2) ^ (r & 7)) << 4) + (k & 3) * 4);
+}
+
+__global__ void probe(const float* A, const float* B, float* D, int r0, int boff_mode) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = sm;              // MR rows x 128 B
+  uint8_t* sB = sm + 32768;      // N rows x 128 B
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int e = tid; e < MR * K; e += blockDim.x) {
+    const int m = e / K, k = e % K;
+    *(float*)(sA + off_k(m, k)) = A[m * K + k];
+  }
+  for (int e = tid; e < N * K; e += blockDim.x) {
+    const int n = e / K, k = e % K;
+    *(float*)(sB + off_k(n, k)) = B[n * K + k];
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(64));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+  if (tid == 0) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+    for (int j = 0; j < K / 8; ++j) {
+      const uint32_t boff = boff_mode == 0 ? 0u : boff_mode == 1 ? (uint32_t)(r0 & 7) : (uint32_t)((8 - (r0 & 7)) & 7);
+      const uint64_t da = sdesc(su32(sA) + r0 * 128 + j * 32, 16, 1024, boff);
+      const uint64_t db = sdesc(su32(sB) + j * 32, 16, 1024, 0);
+      const uint32_t acc = j > 0;
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                   "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                   ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
+  }
+  asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}\n" ::"r"(su32(&bar)) : "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  for (int c0 = 0; c0 < N; c0 += 8) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(tmem + ((uint32_t)(warp * 32) << 16) + c0));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int m = warp * 32 + (tid & 31);
+    for (int j = 0; j < 8; ++j) D[m * N + c0 + j] = __uint_as_float(r[j]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
+  }
+}
+
+// Timing: 2048 MMAs (M=128, N=NT, K=8) from one thread with the A start at
+// row r0; returns cycles per MMA.
+template <int NT>
+__global__ void mma_rate(int r0, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid / 32;
+  for (int e = tid; e < 65536 / 4; e += blockDim.x) ((float*)sm)[e] = 0.001f * (e & 7);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+  if (tid == 0) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t a = su32(sm), b = su32(sm + 32768);
+    long long t0 = clock64();
+    for (int i = 0; i < 2048; ++i) {
+      const uint64_t da = sdesc(a + r0 * 128 + (i & 3) * 32, 16, 1024, 0);
+      const uint64_t db = sdesc(b + (i & 3) * 32, 16, 1024, 0);
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                   "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                   ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(1u));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
+    asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}\n" ::"r"(su32(&bar)) : "memory");
+    long long t1 = clock64();
+    out[0] = (t1 - t0) / 2048;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
+int main() {
+  {
+    long long* d; cudaMalloc(&d, 8);
+    cudaFuncSetAttribute(mma_rate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(mma_rate<192>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(mma_rate<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    for (int r0 : {0, 1, 2, 3, 4, 8, 15, 16, 17}) {
+      long long c[3];
+      mma_rate<256><<<1, 128, 100 * 1024>>>(r0, d); cudaDeviceSynchronize(); cudaMemcpy(&c[0], d, 8, cudaMemcpyDeviceToHost);
+      mma_rate<192><<<1, 128, 100 * 1024>>>(r0, d); cudaDeviceSynchronize(); cudaMemcpy(&c[1], d, 8, cudaMemcpyDeviceToHost);
+      mma_rate<64><<<1, 128, 100 * 1024>>>(r0, d); cudaDeviceSynchronize(); cudaMemcpy(&c[2], d, 8, cudaMemcpyDeviceToHost);
+      printf("A start row %2d: cycles/MMA N=256 %lld  N=192 %lld  N=64 %lld\n", r0, c[0], c[1], c[2]);
+    }
+  }
+  std::vector<float> A(MR * K), B(N * K), D(M * N);
+  uint32_t s = 777;
+  auto rnd = [&]() { s = s * 1664525u + 1013904223u; return ((s >> 8) & 0xFFFF) / 32768.0f - 1.0f; };
+  for (auto& v : A) v = rnd();
+  for (auto& v : B) v = rnd();
+  float *dA, *dB, *dD;
+  cudaMalloc(&dA, 4 * A.size()); cudaMalloc(&dB, 4 * B.size()); cudaMalloc(&dD, 4 * D.size());
+  cudaMemcpy(dA, A.data(), 4 * A.size(), cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, B.data(), 4 * B.size(), cudaMemcpyHostToDevice);
+  cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  for (int mode = 0; mode < 3; ++mode)
+    for (int r0 = 0; r0 < 12; ++r0) {
+      probe<<<1, 128, 48 * 1024>>>(dA, dB, dD, r0, mode);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("r0=%d mode=%d CUDA error %s\n", r0, mode, cudaGetErrorString(e)); return 1; }
+      cudaMemcpy(D.data(), dD, 4 * D.size(), cudaMemcpyDeviceToHost);
+      double err = 0, mx = 0;
+      for (int m = 0; m < M; ++m)
+        for (int n = 0; n < N; ++n) {
+          double ref = 0;
+          for (int k = 0; k < K; ++k) ref += (double)A[(m + r0) * K + k] * B[n * K + k];
+          err = fmax(err, fabs(D[m * N + n] - ref));
+          mx = fmax(mx, fabs(ref));
+        }
+      printf("base_off mode %d  r0=%2d  max|err| %.3e (max|ref| %.2f)\n", mode, r0, err, mx);
+    }
+  return 0;
+}
