@@ -1148,13 +1148,14 @@ __global__ void s2d_pm_k(const float* __restrict__ x, float* __restrict__ out, i
 __device__ __forceinline__ void s2d_stage_strip(const float* __restrict__ x, float* strip, int H,
                                                 int W, int c_first, int c_count, int C, int n,
                                                 int j0, int cols, int Hs) {
-  const int per = Hs * cols;
-  for (int e = threadIdx.x; e < c_count * per; e += blockDim.x) {
-    const int cc = e / per, rem = e - cc * per;
-    const int jl = rem / Hs, i = rem - jl * Hs, j = j0 + jl;
-    strip[e] = (i < H && j < W)
-                   ? __ldg(x + (((int64_t)n * C + c_first + cc) * W + j) * H + i)
-                   : 0.f;
+  // one warp per (channel, column): coalesced column reads, no division
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+  for (int cj = warp; cj < c_count * cols; cj += nw) {
+    const int cc = cj / cols, jl = cj - cc * cols, j = j0 + jl;
+    const float* col = x + (((int64_t)n * C + c_first + cc) * W + j) * H;
+    float* dst = strip + (int64_t)cj * Hs;
+    const bool jok = j < W;
+    for (int i = lane; i < Hs; i += 32) dst[i] = (jok && i < H) ? __ldg(col + i) : 0.f;
   }
 }
 
@@ -1162,27 +1163,32 @@ __device__ __forceinline__ void s2d_stage_strip(const float* __restrict__ x, flo
 __global__ void s2d_pm_strip_k(const float* __restrict__ x, float* __restrict__ out, int H, int W,
                                int C, int s, int U, int V, int Cs, int Csp, int VB) {
   extern __shared__ float strip_pm[];
+  __shared__ int offs[256];  // s2d channel c' -> strip offset of (c, a, b), -1 = pad
   const int n = blockIdx.y, v0 = blockIdx.x * VB;
   const int vb = min(VB, V - v0);
   const int Hs = s * U;
+  const int per_c = Hs * s * vb;
+  for (int cp = threadIdx.x; cp < Csp; cp += blockDim.x) {
+    int o = -1;
+    if (cp < Cs) {
+      const int c = cp % C, ab = cp / C, a = ab % s, b = ab / s;
+      o = c * per_c + a + Hs * b;
+    }
+    offs[cp] = o;
+  }
   s2d_stage_strip(x, strip_pm, H, W, 0, C, C, n, s * v0, s * vb, Hs);
   __syncthreads();
-  const int per_c = Hs * s * vb;
   const int c4 = Csp / 4, total = vb * U * c4;
   float4* o = reinterpret_cast<float4*>(out + (((int64_t)n * V + v0) * U) * Csp);
   for (int e = threadIdx.x; e < total; e += blockDim.x) {
     const int cq = e % c4, pix = e / c4;
     const int vl = pix / U, u = pix - vl * U;
+    const int base = s * u + Hs * s * vl;
     float r[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const int cp = cq * 4 + k;
-      float v = 0.f;
-      if (cp < Cs) {
-        const int c = cp % C, ab = cp / C, a = ab % s, b = ab / s;
-        v = strip_pm[c * per_c + (s * u + a) + Hs * (s * vl + b)];
-      }
-      r[k] = v;
+      const int off = offs[cq * 4 + k];
+      r[k] = off >= 0 ? strip_pm[off + base] : 0.f;
     }
     o[e] = make_float4(r[0], r[1], r[2], r[3]);
   }
@@ -1365,6 +1371,10 @@ struct TcState {
   const float* dyt_src = nullptr;
   uint64_t dyt_call = 0;
   int64_t dyt_key = 0;
+  // same for dy on the padded grid (dyg): shared by grid wgrad and im2col dgrad
+  const float* dyg_src = nullptr;
+  uint64_t dyg_call = 0;
+  int64_t dyg_key = 0;
 };
 
 static TcState* state(ck_handle* h) {
@@ -1542,6 +1552,8 @@ static void to_grid_pm(const float* x, float* xg, int H, int W, int C, int N, in
   to_grid_pm_k<<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow);
 }
 
+static bool wgrid_enabled();
+
 static bool halo_enabled() {
   // Off by default: measured slower than the im2col kernels on AlexNet
   // (junk grid rows + per-tap filter streaming), kept for experiments.
@@ -1696,6 +1708,23 @@ static bool halo_launch(const HaloConv& hc, GemmParams p, cudaStream_t s) {
   if (cudaLaunchKernelEx(&cfg, halo_conv_kernel<2>, ta, tb, p) != cudaSuccess)
     throw Err(CK_ERR_CUDA, "halo_conv_kernel cluster launch failed");
   return true;
+}
+
+// dy at (0, 0) of an Hg x Wg zero grid, pixel-major [n][Wg][Hg][groups*Kgp]:
+// the wgrad A operand and (through im2col with negative corners) the dgrad
+// input of one ck_conv_backward call -- transformed once per call.
+static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, int Kgp,
+                      int groups, int Hg, int Wg, cudaStream_t s) {
+  TcState* st = state(h);
+  const int64_t key = ((((int64_t)Hg * 4099 + Wg) * 65537 + d.K) * 131071 + d.N) * 1031 +
+                      Kgp * 17 + groups + ((int64_t)d.OH << 40) + ((int64_t)d.OW << 50);
+  float* buf = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hg * Wg * Kgp * groups, s);
+  if (st->dyg_src == dy && st->dyg_call == h->call && st->dyg_key == key) return buf;
+  to_grid_pm(dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, Hg, Wg, 0, 0, s);
+  st->dyg_src = dy;
+  st->dyg_call = h->call;
+  st->dyg_key = key;
+  return buf;
 }
 
 static void transpose(const float* in, float* out, int R, int Cc, int64_t ldi, int64_t ldo,
@@ -1860,6 +1889,7 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
     // dx_s2d = stride-1 conv of dy zero-padded by (Th-1, Tw-1) with the
     // flipped bank, on a grid of pitch Hq; EPI_S2D scatters back to x.
     float* dyg = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hq * Wq * Kp, s);
+    st->dyg_src = nullptr;
     to_grid_pm(dy, dyg, d.OH, d.OW, d.K, d.N, d.K, Kp, 1, Hq, Wq, z.Th - 1, z.Tw - 1, s);
     GemmParams p{};
     p.epi = EPI_S2D; p.out = dx;
@@ -1868,7 +1898,9 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
     HaloConv hc{dyg, Kp, Hq, Wq, d.N, gt, Kp, taps, z.Th, z.Tw, z.Cs, 1, z.U, z.V};
     if (halo_launch(hc, p, s)) return;
   }
-  float* dyt = dy_pm(h, dy, d, d.K, Kp, 1, s);
+  // im2col over dy at (0, 0) of the U x V grid (shared with the wgrad): the
+  // negative corner supplies the top/left padding, the grid's zero rows the rest
+  float* dyt = dy_grid(h, dy, d, d.K, Kp, 1, z.U, z.V, s);
   GemmParams p{};
   p.M = d.N * z.U * z.V; p.N = z.Cs; p.K = taps * Kp; p.BN = pick_bn(z.Cs); p.splits = 1;
   p.OH = z.U; p.OW = z.V; p.sh = 1; p.sw = 1; p.pt = z.Th - 1; p.pl = z.Tw - 1; p.fh = z.Th;
@@ -1877,8 +1909,8 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   p.s2d = z.s; p.s2d_U = z.U; p.s2d_H = d.H; p.s2d_W = d.W; p.s2d_C = d.C;
   p.acc = acc; p.n_valid = z.Cs;
   p.BM = pick_bm(p.M, p.BN);
-  CUtensorMap ta = map_im2col(dyt, Kp, d.OH, d.OW, d.N, -(z.Th - 1), -(z.Tw - 1),
-                              z.U - d.OH - z.Th + 1, z.V - d.OW - z.Tw + 1, 1, 1, p.BM);
+  CUtensorMap ta = map_im2col(dyt, Kp, z.U, z.V, d.N, -(z.Th - 1), -(z.Tw - 1), -(z.Th - 1),
+                              -(z.Tw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kp, z.Cs, (uint64_t)taps * Kp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (z.Cs + p.BN - 1) / p.BN, 1, s);
 }
@@ -1942,8 +1974,7 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   s2d_pm(x, xt, d, z, s);
   if (wgrid_enabled()) {
     // the s2d tensor is a pad-free grid of pitch U; dy goes to (0, 0) of it
-    float* dyg = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * z.U * z.V * Kp, s);
-    to_grid_pm(dy, dyg, d.OH, d.OW, d.K, d.N, d.K, Kp, 1, z.U, z.V, 0, 0, s);
+    float* dyg = dy_grid(h, dy, d, d.K, Kp, 1, z.U, z.V, s);
     float* part;
     int64_t per;
     const int splits = grid_wgrad(h, xt, z.Csp, z.Csp, dyg, Kp, Kp, d.K, 1, d.N, z.U, z.V, z.Th,
@@ -2119,6 +2150,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     // halo kernel: dy zero-padded by (fh-1-pt, ...) on a grid of pitch Hq,
     // convolved with the flipped bank; the valid rows are the H x W of dx.
     float* dyg = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hq * Wq * Kp, s);
+    st->dyg_src = nullptr;
     to_grid_pm(dy, dyg, d.OH, d.OW, d.K, d.N, Kg, Kgp, d.groups, Hq, Wq, qt, ql, s);
     GemmParams p{};
     p.epi = EPI_PIX; p.out = dx; p.ld = (int64_t)d.H * d.W;
@@ -2127,7 +2159,12 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     HaloConv hc{dyg, Kp, Hq, Wq, d.N, gt, Kgp, taps, d.fh, d.fw, d.Cg, d.groups, d.H, d.W};
     if (halo_launch(hc, p, s)) return true;
   }
-  float* dyt = dy_pm(h, dy, d, Kg, Kgp, d.groups, s);
+  // dy: on the wgrad's zero grid (Hg x Wg, dy at (0, 0); shared within the
+  // call) when that path is on, else compact pixel-major.
+  const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
+  const bool on_grid = wgrid_enabled();
+  float* dyt = on_grid ? dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s)
+                       : dy_pm(h, dy, d, Kg, Kgp, d.groups, s);
   GemmParams p{};
   p.M = d.N * d.H * d.W;
   p.N = d.Cg;
@@ -2142,8 +2179,11 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   p.img_stride = (int64_t)d.C * d.H * d.W; p.grp_col = d.Cg; p.epi_OHW = d.H * d.W;
   p.bias = nullptr; p.relu = 0; p.acc = acc; p.n_valid = d.Cg;
   p.BM = pick_bm(p.M, p.BN);
-  CUtensorMap ta = map_im2col(dyt, Kp, d.OH, d.OW, d.N, -qt, -ql, qb - (d.fh - 1),
-                              qr - (d.fw - 1), 1, 1, p.BM);
+  CUtensorMap ta = on_grid
+                       ? map_im2col(dyt, Kp, Hg, Wg, d.N, -qt, -ql, d.H - Hg - qt, d.W - Wg - ql,
+                                    1, 1, p.BM)
+                       : map_im2col(dyt, Kp, d.OH, d.OW, d.N, -qt, -ql, qb - (d.fh - 1),
+                                    qr - (d.fw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kgp, d.C, (uint64_t)taps * Kgp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.Cg + p.BN - 1) / p.BN,
                                   d.groups, s);
@@ -2191,8 +2231,7 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
     const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
     float* xg = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * Hg * Wg * Cp, s);
     to_grid_pm(x, xg, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, Hg, Wg, d.pt, d.pl, s);
-    float* dyg = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hg * Wg * Kp, s);
-    to_grid_pm(dy, dyg, d.OH, d.OW, d.K, d.N, Kg, Kgp, d.groups, Hg, Wg, 0, 0, s);
+    float* dyg = dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s);
     float* part;
     int64_t per;
     const int splits = grid_wgrad(h, xg, Cp, Cgp, dyg, Kp, Kgp, Kg, d.groups, d.N, Hg, Wg, d.fh,
