@@ -24,6 +24,7 @@ struct ck_handle {
   int64_t last_classes = 0;
   ck::TcState* tc = nullptr;
   uint64_t call = 0;      // API call id: scopes transform caches to one call
+  ck::ConvCache* conv_cache = nullptr;  // set by the graph engine around conv calls
 };
 
 namespace ck {

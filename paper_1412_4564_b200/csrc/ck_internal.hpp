@@ -42,6 +42,17 @@ struct Workspace {
   void release();
 };
 
+// A conv layer's input in the tensor-core layout (padded pixel-major grid or
+// space-to-depth tensor), written by the forward and reused by the weight
+// gradient of the same graph step.  Owned by the graph engine, one per conv
+// layer; the engine invalidates it at the start of every forward pass.
+struct ConvCache {
+  Workspace buf;
+  const float* src = nullptr;
+  int64_t key = 0;
+  bool valid = false;
+};
+
 struct LaunchCounter {
   int64_t n = 0;
 };

@@ -1727,6 +1727,26 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
   return buf;
 }
 
+// x on its zero-padded grid (Hg x Wg, x at (pt, pl)), pixel-major: the fprop
+// im2col input and the wgrad B operand.  Inside a graph step the engine's
+// per-layer ConvCache carries it from the forward to the weight gradient.
+static float* x_grid(ck_handle* h, const float* x, const ConvDims& d, int Cgp, int Hg, int Wg,
+                     cudaStream_t s) {
+  ConvCache* c = h->conv_cache;
+  const int64_t key = (((((int64_t)Hg * 4099 + Wg) * 65537 + d.C) * 131071 + d.N) * 1031 +
+                       Cgp * 17 + d.groups) ^ ((int64_t)(d.pt * 64 + d.pl) << 52) ^ 0x1;
+  const size_t bytes = sizeof(float) * (size_t)d.N * Hg * Wg * Cgp * d.groups;
+  float* buf = (float*)grow(c ? c->buf : state(h)->xt, bytes, s);
+  if (c && c->valid && c->src == x && c->key == key) return buf;
+  to_grid_pm(x, buf, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, Hg, Wg, d.pt, d.pl, s);
+  if (c) {
+    c->valid = true;
+    c->src = x;
+    c->key = key;
+  }
+  return buf;
+}
+
 static void transpose(const float* in, float* out, int R, int Cc, int64_t ldi, int64_t ldo,
                       cudaStream_t s) {
   dim3 grid((Cc + 31) / 32, (R + 31) / 32);
@@ -1843,13 +1863,30 @@ static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, c
         x, xt, d.H, d.W, d.C, d.N, z.s, z.U, z.V, z.Cs, z.Csp);
 }
 
+// the space-to-depth input (a pad-free grid of pitch U), cached like x_grid
+static float* x_s2d(ck_handle* h, const float* x, const ConvDims& d, const S2D& z,
+                    cudaStream_t s) {
+  ConvCache* c = h->conv_cache;
+  const int64_t key = ((((int64_t)z.U * 4099 + z.V) * 65537 + d.C) * 131071 + d.N) * 1031 +
+                      z.Csp * 17 + z.s + 0x2;
+  float* buf = (float*)grow(c ? c->buf : state(h)->xt,
+                            sizeof(float) * (size_t)d.N * z.U * z.V * z.Csp, s);
+  if (c && c->valid && c->src == x && c->key == key) return buf;
+  s2d_pm(x, buf, d, z, s);
+  if (c) {
+    c->valid = true;
+    c->src = x;
+    c->key = key;
+  }
+  return buf;
+}
+
 static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
                       const ConvDims& d, const S2D& z, int relu, cudaStream_t s) {
   TcState* st = state(h);
   const int taps = z.Th * z.Tw;
-  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * z.U * z.V * z.Csp, s);
+  float* xt = x_s2d(h, x, d, z, s);
   float* ft = (float*)grow(st->ft, sizeof(float) * (size_t)d.K * taps * z.Csp, s);
-  s2d_pm(x, xt, d, z, s);
   count_launch();
   s2d_repack_fprop_k<<<blocks_for((int64_t)d.K * taps * z.Csp), 256, 0, s>>>(
       f, ft, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Tw, z.Csp);
@@ -1970,8 +2007,7 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   TcState* st = state(h);
   const int taps = z.Th * z.Tw;
   const int Kp = rup(d.K, 32);
-  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * z.U * z.V * z.Csp, s);
-  s2d_pm(x, xt, d, z, s);
+  float* xt = x_s2d(h, x, d, z, s);
   if (wgrid_enabled()) {
     // the s2d tensor is a pad-free grid of pitch U; dy goes to (0, 0) of it
     float* dyg = dy_grid(h, dy, d, d.K, Kp, 1, z.U, z.V, s);
@@ -2071,8 +2107,16 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
     HaloConv hc{xg, Cp, Hg, Wg, d.N, ft, Cgp, taps, d.fh, d.fw, Kg, d.groups, d.OH, d.OW};
     if (halo_launch(hc, p, s)) return true;
   }
-  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
-  to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
+  // stride 1: im2col over the padded grid (shared with the wgrad); else over
+  // the compact pixel-major tensor with the padding in the im2col corners
+  const bool on_grid = d.sh == 1 && d.sw == 1 && wgrid_enabled();
+  float* xt;
+  if (on_grid) {
+    xt = x_grid(h, x, d, Cgp, Hg, Wg, s);
+  } else {
+    xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
+    to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
+  }
   GemmParams p{};
   p.M = d.N * d.OH * d.OW;
   p.N = Kg;
@@ -2087,8 +2131,11 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.acc = 0; p.n_valid = Kg;
   p.BM = pick_bm(p.M, p.BN);
-  CUtensorMap ta = map_im2col(xt, Cp, d.H, d.W, d.N, -d.pt, -d.pl, d.pb - (d.fh - 1),
-                              d.pr - (d.fw - 1), d.sh, d.sw, p.BM);
+  if (on_grid) p.pt = p.pl = 0;
+  CUtensorMap ta = on_grid ? map_im2col(xt, Cp, Hg, Wg, d.N, 0, 0, -(d.fh - 1), -(d.fw - 1), 1,
+                                        1, p.BM)
+                           : map_im2col(xt, Cp, d.H, d.W, d.N, -d.pt, -d.pl, d.pb - (d.fh - 1),
+                                        d.pr - (d.fw - 1), d.sh, d.sw, p.BM);
   CUtensorMap tb = map_2d(ft, (uint64_t)taps * Cgp, d.K, (uint64_t)taps * Cgp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (Kg + p.BN - 1) / p.BN, d.groups,
                                   s);
@@ -2229,8 +2276,7 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   TcState* st = state(h);
   if (wgrid_enabled()) {
     const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
-    float* xg = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * Hg * Wg * Cp, s);
-    to_grid_pm(x, xg, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, Hg, Wg, d.pt, d.pl, s);
+    float* xg = x_grid(h, x, d, Cgp, Hg, Wg, s);
     float* dyg = dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s);
     float* part;
     int64_t per;

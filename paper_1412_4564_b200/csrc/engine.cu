@@ -69,6 +69,7 @@ struct Layer {
   std::vector<int> in, out;
   std::vector<double> p;
   float* aux = nullptr;  // bnorm moments (K x 2), graph.cpp:306
+  ConvCache cache;       // conv input transform shared by forward and wgrad
 };
 
 static std::vector<std::string> split_csv(const char* s) {
@@ -115,6 +116,7 @@ struct ck_graph {
     return (int)vars.size() - 1;
   }
   ~ck_graph() {
+    for (auto& l : layers) l.cache.buf.release();
     for (void* p : allocs) cudaFree(p);
     for (auto e : prof_ev) cudaEventDestroy(e);
   }
@@ -306,7 +308,9 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
       ck_tensor x = V(0), f = V(1), b;
       if (l.in.size() > 2) b = V(2);
       ck_conv_geom cg = conv_geom_of(l);
+      h->conv_cache = &l.cache;
       st = ck_conv_forward(h, &x, &f, l.in.size() > 2 ? &b : nullptr, &cg, &y, g->math, s);
+      h->conv_cache = nullptr;
       break;
     }
     case Kind::convt: {
@@ -374,6 +378,11 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
       // Independent accumulate flags per output: run the three passes
       // separately when they differ.
       int a0 = acc(0), a1 = acc(1), a2 = l.in.size() > 2 ? acc(2) : a1;
+      h->conv_cache = &l.cache;  // the forward's transformed input (valid this step)
+      struct Reset {
+        ck_handle* h;
+        ~Reset() { h->conv_cache = nullptr; }
+      } reset{h};
       if (a0 == a1 && a1 == a2) {
         st = ck_conv_backward(h, &x, &f, &cg, &dy, &dx, &df, l.in.size() > 2 ? &db : nullptr, a0,
                               g->math, s);
@@ -460,6 +469,7 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
 
 // graph.cpp:494-545 forward (train mode).
 static void run_forward(ck_graph* g, cudaStream_t s) {
+  for (auto& l : g->layers) l.cache.valid = false;
   for (int li : g->order) {
     g->prof(li, 0, s);
     layer_forward(g, g->layers[li], s);
