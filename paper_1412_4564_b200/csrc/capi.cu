@@ -322,6 +322,11 @@ ck_status ck_conv_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* f,
   }
   cudaStream_t s = (cudaStream_t)stream;
   ConvDims d = conv_dims(x->shape, f->shape, ys, *g);
+  // TF32 conv layers with a tensor-core grid path reduce db inside the dy
+  // transform their dgrad/wgrad reuse; everything else uses conv_bgrad.
+  if (db && math == CK_MATH_TF32 && (dx || df) &&
+      conv_tc_bias(h, dy->data, db->data, d, accumulate, s))
+    db = nullptr;
   if (db) {
     void* bws = h->scratch.get(conv_bgrad_ws_bytes((int)ys.c, (int)ys.n, (int)(ys.h * ys.w)), s);
     if (!bws) throw Err(CK_ERR_CUDA, "workspace allocation failed");

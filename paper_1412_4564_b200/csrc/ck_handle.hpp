@@ -74,6 +74,8 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
                    int acc, cudaStream_t s);
 bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, const ConvDims& d,
                    int acc, cudaStream_t s);
+bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, int acc,
+                  cudaStream_t s);
 void conv_tc_release(ck_handle* h);
 
 }  // namespace ck

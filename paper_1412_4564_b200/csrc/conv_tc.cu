@@ -858,7 +858,8 @@ __global__ void to_pixel_major_k(const float* __restrict__ x, float* __restrict_
 // cp = g*Cgp + (c - g*Cgp_local); zero borders and channel pads (the input of
 // halo_conv_kernel).  32 x 32 smem tile transpose.
 __global__ void to_grid_pm_k(const float* __restrict__ x, float* __restrict__ xg, int H, int W,
-                             int C, int Cg, int Cgp, int groups, int Hg, int Wg, int oh, int ow) {
+                             int C, int Cg, int Cgp, int groups, int Hg, int Wg, int oh, int ow,
+                             double* __restrict__ bpart) {
   // tile: 64 grid pixels x 32 padded channels; loads coalesced along pixels
   // (two per channel row per thread), stores as float4 along channels.
   __shared__ float tile[32][65];
@@ -882,9 +883,18 @@ __global__ void to_grid_pm_k(const float* __restrict__ x, float* __restrict__ xg
     const int g = cp / Cgp, cl = cp - g * Cgp;
     const bool ch_ok = cp < Cp && cl < Cg;
     const float* xc = xn + (int64_t)(g * Cg + cl) * H * W;
+    float v[2];
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
-      tile[r][lane + 32 * k] = (ch_ok && src[k] >= 0) ? __ldg(xc + src[k]) : 0.f;
+    for (int k = 0; k < 2; ++k) {
+      v[k] = (ch_ok && src[k] >= 0) ? __ldg(xc + src[k]) : 0.f;
+      tile[r][lane + 32 * k] = v[k];
+    }
+    if (bpart) {  // fused bias gradient: this tile's per-channel sum (double, fixed order)
+      double t = (double)v[0] + (double)v[1];
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (lane == 0 && cp < Cp)
+        bpart[((int64_t)n * gridDim.x + blockIdx.x) * Cp + cp] = t;
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -1365,7 +1375,7 @@ static bool load_driver() {
 bool conv_tc_available() { return load_driver(); }
 
 struct TcState {
-  Workspace xt, dyt, ft, part, dyg;
+  Workspace xt, dyt, ft, part, dyg, bpart;
   // dy in pixel-major layout is shared by wgrad and dgrad of one
   // ck_conv_backward call: cached by (source, geometry, call id).
   const float* dyt_src = nullptr;
@@ -1389,6 +1399,7 @@ void conv_tc_release(ck_handle* h) {
   h->tc->ft.release();
   h->tc->part.release();
   h->tc->dyg.release();
+  h->tc->bpart.release();
   delete h->tc;
   h->tc = nullptr;
 }
@@ -1549,7 +1560,7 @@ static void to_grid_pm(const float* x, float* xg, int H, int W, int C, int N, in
                        int groups, int Hg, int Wg, int oh, int ow, cudaStream_t s) {
   dim3 grid((Hg * Wg + 63) / 64, (Cgp * groups + 31) / 32, N);
   count_launch();
-  to_grid_pm_k<<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow);
+  to_grid_pm_k<<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow, nullptr);
 }
 
 static bool wgrid_enabled();
@@ -1713,14 +1724,44 @@ static bool halo_launch(const HaloConv& hc, GemmParams p, cudaStream_t s) {
 // dy at (0, 0) of an Hg x Wg zero grid, pixel-major [n][Wg][Hg][groups*Kgp]:
 // the wgrad A operand and (through im2col with negative corners) the dgrad
 // input of one ck_conv_backward call -- transformed once per call.
+__global__ void grid_bias_finish_k(const double* __restrict__ bpart, float* db, int K, int Kg,
+                                   int Kgp, int Cp, int rows, int acc) {
+  const int k = blockIdx.x;
+  const int g = k / Kg, cp = g * Kgp + (k - g * Kg);
+  double t = 0;
+  for (int r = threadIdx.x; r < rows; r += blockDim.x) t += bpart[(int64_t)r * Cp + cp];
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  __shared__ double red[32];
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double u = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) u += red[w];
+    db[k] = acc ? db[k] + (float)u : (float)u;
+  }
+}
+
+// With db != nullptr the transform also reduces db[k] = sum over all dy
+// pixels (conv.cpp:246-252), fused into the same read of dy.
 static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, int Kgp,
-                      int groups, int Hg, int Wg, cudaStream_t s) {
+                      int groups, int Hg, int Wg, cudaStream_t s, float* db = nullptr,
+                      int db_acc = 0) {
   TcState* st = state(h);
   const int64_t key = ((((int64_t)Hg * 4099 + Wg) * 65537 + d.K) * 131071 + d.N) * 1031 +
                       Kgp * 17 + groups + ((int64_t)d.OH << 40) + ((int64_t)d.OW << 50);
   float* buf = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hg * Wg * Kgp * groups, s);
-  if (st->dyg_src == dy && st->dyg_call == h->call && st->dyg_key == key) return buf;
-  to_grid_pm(dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, Hg, Wg, 0, 0, s);
+  if (!db && st->dyg_src == dy && st->dyg_call == h->call && st->dyg_key == key) return buf;
+  if (db) {
+    const int Cp = Kgp * groups, nb = (Hg * Wg + 63) / 64;
+    double* bpart = (double*)grow(st->bpart, sizeof(double) * (size_t)d.N * nb * Cp, s);
+    dim3 grid(nb, (Cp + 31) / 32, d.N);
+    count_launch(2);
+    to_grid_pm_k<<<grid, 256, 0, s>>>(dy, buf, d.OH, d.OW, d.K, Kg, Kgp, groups, Hg, Wg, 0, 0,
+                                      bpart);
+    grid_bias_finish_k<<<d.K, 256, 0, s>>>(bpart, db, d.K, Kg, Kgp, Cp, d.N * nb, db_acc);
+  } else {
+    to_grid_pm(dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, Hg, Wg, 0, 0, s);
+  }
   st->dyg_src = dy;
   st->dyg_call = h->call;
   st->dyg_key = key;
@@ -2234,6 +2275,25 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kgp, d.C, (uint64_t)taps * Kgp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.Cg + p.BN - 1) / p.BN,
                                   d.groups, s);
+  return true;
+}
+
+// Bias gradient fused into the dy-grid transform that the dgrad / wgrad of
+// the same ck_conv_backward call then reuse.  False when the shape does not
+// use the grid (FC layers, strided convs without space-to-depth).
+bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, int acc,
+                  cudaStream_t s) {
+  if (!load_driver() || !wgrid_enabled() || is_fc(d)) return false;
+  const int Kg = d.Kg();
+  if (d.sh == 1 && d.sw == 1) {
+    if (d.Cg < 16 || Kg < 16) return false;
+    const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
+    dy_grid(h, dy, d, Kg, rup(Kg, 32), d.groups, Hg, Wg, s, db, acc);
+    return true;
+  }
+  S2D z;
+  if (!s2d_plan(d, z)) return false;
+  dy_grid(h, dy, d, d.K, rup(d.K, 32), 1, z.U, z.V, s, db, acc);
   return true;
 }
 
