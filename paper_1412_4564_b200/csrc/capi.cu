@@ -413,7 +413,8 @@ ck_status ck_pool_forward(ck_handle* h, const ck_tensor* x, const ck_pool_geom* 
   if (!g) throw Err(CK_ERR_ARG, "null geometry");
   ck_shape ys = pool_output_shape(x->shape, *g);
   check_out(y, ys, "y");
-  pool_forward(x->data, y->data, pool_dims(x->shape, ys, *g), (cudaStream_t)stream);
+  pool_forward(x->data, y->data, pool_dims(x->shape, ys, *g), (cudaStream_t)stream,
+               h->conv_cache);
   after_launch();
   CK_API_END(h)
 }
@@ -431,7 +432,7 @@ ck_status ck_pool_backward(ck_handle* h, const ck_tensor* x, const ck_pool_geom*
                                 " does not match output " + shape_str(ys));
   check_out(dx, x->shape, "dx");
   pool_backward(x->data, dy->data, dx->data, pool_dims(x->shape, ys, *g), accumulate,
-                (cudaStream_t)stream);
+                (cudaStream_t)stream, h->conv_cache);
   after_launch();
   CK_API_END(h)
 }

@@ -69,9 +69,11 @@ void axpy_inplace(float* y, const float* x, int64_t n, cudaStream_t s);  // y +=
 void sgd_step(float* w, float* v, const float* g, int64_t n, float lr, float mom, float wd,
               cudaStream_t s);
 
-void pool_forward(const float* x, float* y, const PoolDims& d, cudaStream_t s);
+struct ConvCache;
+void pool_forward(const float* x, float* y, const PoolDims& d, cudaStream_t s,
+                  ConvCache* cache = nullptr);
 void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d, int acc,
-                   cudaStream_t s);
+                   cudaStream_t s, ConvCache* cache = nullptr);
 
 void lrn_forward(const float* x, float* y, int H, int W, int C, int N, int size, float kappa,
                  float alpha, float beta, cudaStream_t s);

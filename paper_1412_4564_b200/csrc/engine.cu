@@ -322,7 +322,9 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
     case Kind::pool: {
       ck_tensor x = V(0);
       ck_pool_geom pg = pool_geom_of(l);
+      h->conv_cache = &l.cache;  // records the argmax for this step's backward
       st = ck_pool_forward(h, &x, &pg, &y, s);
+      h->conv_cache = nullptr;
       break;
     }
     case Kind::relu: {
@@ -412,7 +414,9 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
     case Kind::pool: {
       ck_tensor x = V(0), dx = D(0);
       ck_pool_geom pg = pool_geom_of(l);
+      h->conv_cache = &l.cache;
       st = ck_pool_backward(h, &x, &pg, &dy, &dx, acc(0), s);
+      h->conv_cache = nullptr;
       mark(0);
       break;
     }

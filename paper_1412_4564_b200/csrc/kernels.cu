@@ -270,43 +270,150 @@ __global__ void pool_bwd_plane_k(const float* __restrict__ x, const float* __res
 }
 
 // Compile-time window / stride max pooling (AlexNet 3x3/2, LeNet and VGG
-// 2x2/2): unrolled windows, one runtime division per element.  Same rules
-// as pool_fwd_k / pool_bwd_plane_k (first strict maximum, (oj, oi) order).
-template <int WH, int WW, int SH, int SW>
-__global__ void pool_max_fwd_t(const float* __restrict__ x, float* __restrict__ y, PoolDims d) {
+// 2x2/2): unrolled windows; index splits by multiply-shift (FastDiv) instead
+// of integer division; INSIDE = every window lies inside the input (no
+// padding, no clipping), which drops all bounds tests.  Same rules as
+// pool_fwd_k / pool_bwd_plane_k (first strict maximum, (oj, oi) order).
+struct FastDiv {  // n / d == (n * m) >> 40 for n * d < 2^39
+  uint64_t m;
+  explicit FastDiv(int d = 1) : m(((1ull << 40) + (uint64_t)d - 1) / (uint64_t)d) {}
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return (uint32_t)(((uint64_t)n * m) >> 40);
+  }
+};
+
+template <int WH, int WW, int SH, int SW, bool INSIDE>
+__global__ void pool_max_fwd_t(const float* __restrict__ x, float* __restrict__ y, PoolDims d,
+                               FastDiv by_ohw, FastDiv by_oh, uint8_t* __restrict__ argout) {
   const int OHW = d.OH * d.OW, HW = d.H * d.W;
-  const int64_t total = (int64_t)OHW * d.C * d.N;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t plane = e / OHW;
+  const uint32_t total = (uint32_t)OHW * d.C * d.N;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += gridDim.x * blockDim.x) {
+    const uint32_t plane = by_ohw.div(e);
     const int w = (int)(e - plane * OHW);
-    const int oj = w / d.OH, oi = w - oj * d.OH;
+    const int oj = (int)by_oh.div(w), oi = w - oj * d.OH;
     const int si = oi * SH - d.pt, sj = oj * SW - d.pl;
-    const float* xp = x + plane * HW;
+    const float* xp = x + (size_t)plane * HW;
     float best = 0.f;
     bool have = false;
+    int code = 0;  // window offset a + WH*b of the winner
 #pragma unroll
     for (int b = 0; b < WW; ++b) {
       const int j = sj + b;
 #pragma unroll
       for (int a = 0; a < WH; ++a) {
         const int i = si + a;
-        if (i >= 0 && i < d.H && j >= 0 && j < d.W) {
+        if (INSIDE || (i >= 0 && i < d.H && j >= 0 && j < d.W)) {
           const float v = __ldg(xp + i + d.H * j);
-          if (!have || v > best) {
+          if ((INSIDE && a == 0 && b == 0) || (!INSIDE && !have) || v > best) {
             best = v;
-            have = true;
+            code = a + WH * b;
           }
+          have = true;
         }
       }
     }
     y[e] = best;
+    if (argout) argout[e] = (uint8_t)code;
   }
 }
 
+// Backward from the argmax the forward recorded (one byte per window): no
+// re-read of x, one thread per dx element gathering its <= ceil(W/S)^2
+// windows in the reference's (oj, oi) order.
 template <int WH, int WW, int SH, int SW, bool kAcc>
+__global__ void pool_max_bwd_arg_t(const uint8_t* __restrict__ arg, const float* __restrict__ dy,
+                                   float* dx, PoolDims d, FastDiv by_hw, FastDiv by_h) {
+  constexpr int NI = (WH + SH - 1) / SH, NJ = (WW + SW - 1) / SW;
+  const int HW = d.H * d.W, OHW = d.OH * d.OW;
+  const uint32_t total = (uint32_t)HW * d.C * d.N;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += gridDim.x * blockDim.x) {
+    const uint32_t plane = by_hw.div(e);
+    const int pix = (int)(e - plane * HW);
+    const int j = (int)by_h.div(pix), i = pix - j * d.H;
+    const int ti = i + d.pt, tj = j + d.pl;
+    const int oi_hi = min(d.OH - 1, ti / SH), oj_hi = min(d.OW - 1, tj / SW);
+    const int oi_lo = ti - WH + 1 <= 0 ? 0 : (ti - WH + SH) / SH;
+    const int oj_lo = tj - WW + 1 <= 0 ? 0 : (tj - WW + SW) / SW;
+    const uint8_t* ap = arg + (size_t)plane * OHW;
+    const float* dp = dy + (size_t)plane * OHW;
+    float acc = 0.f;
+#pragma unroll
+    for (int b = 0; b < NJ; ++b) {
+      const int oj = oj_lo + b;
+#pragma unroll
+      for (int a = 0; a < NI; ++a) {
+        const int oi = oi_lo + a;
+        if (oj <= oj_hi && oi <= oi_hi) {
+          const int w = oi + d.OH * oj;
+          const int code = __ldg(ap + w);
+          const int ai = code % WH, bj = code / WH;
+          if (oi * SH - d.pt + ai == i && oj * SW - d.pl + bj == j)
+            acc = __fadd_rn(acc, __ldg(dp + w));
+        }
+      }
+    }
+    dx[e] = kAcc ? __fadd_rn(dx[e], acc) : acc;
+  }
+}
+
+// 3x3 / stride 2 from the recorded argmax, one thread per 2x2 block of dx in
+// padded coordinates (ti, tj) = (2a + di, 2b + dj): the four elements share
+// the candidate windows oi in {a-1, a}, oj in {b-1, b}, whose codes and dy
+// are loaded once; each element adds the dy of the windows routed to it in
+// the reference's (oj, oi) order.
+template <bool kAcc>
+__global__ void pool_max3s2_bwd_arg_k(const uint8_t* __restrict__ arg,
+                                      const float* __restrict__ dy, float* dx, PoolDims d,
+                                      int A, int B, FastDiv by_a, FastDiv by_ab) {
+  const int HW = d.H * d.W, OHW = d.OH * d.OW;
+  const uint32_t total = (uint32_t)A * B * d.C * d.N;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += gridDim.x * blockDim.x) {
+    const uint32_t plane = by_ab.div(e);
+    const int r = (int)(e - plane * (uint32_t)(A * B));
+    const int b = (int)by_a.div(r), a = r - b * A;
+    const uint8_t* ap = arg + (size_t)plane * OHW;
+    const float* dp = dy + (size_t)plane * OHW;
+    int code[2][2];
+    float g[2][2];
+#pragma unroll
+    for (int wb = 0; wb < 2; ++wb)
+#pragma unroll
+      for (int wa = 0; wa < 2; ++wa) {
+        const int oi = a - 1 + wa, oj = b - 1 + wb;
+        const bool ok = oi >= 0 && oi < d.OH && oj >= 0 && oj < d.OW;
+        code[wb][wa] = ok ? __ldg(ap + oi + d.OH * oj) : -1;
+        g[wb][wa] = ok ? __ldg(dp + oi + d.OH * oj) : 0.f;
+      }
+    float* dxp = dx + (size_t)plane * HW;
+#pragma unroll
+    for (int dj = 0; dj < 2; ++dj)
+#pragma unroll
+      for (int di = 0; di < 2; ++di) {
+        const int i = 2 * a + di - d.pt, j = 2 * b + dj - d.pl;
+        if (i < 0 || i >= d.H || j < 0 || j >= d.W) continue;
+        float acc = 0.f;
+#pragma unroll
+        for (int wb = 0; wb < 2; ++wb)
+#pragma unroll
+          for (int wa = 0; wa < 2; ++wa) {
+            // window (a-1+wa, b-1+wb) starts at padded (2a-2+2wa, 2b-2+2wb): this
+            // element is its offset (di+2-2wa, dj+2-2wb) if that lies in 0..2
+            const int ai = di + 2 - 2 * wa, bj = dj + 2 - 2 * wb;
+            if (ai <= 2 && bj <= 2 && code[wb][wa] == ai + 3 * bj)
+              acc = __fadd_rn(acc, g[wb][wa]);
+          }
+        float* o = dxp + i + d.H * j;
+        *o = kAcc ? __fadd_rn(*o, acc) : acc;
+      }
+  }
+}
+
+template <int WH, int WW, int SH, int SW, bool INSIDE, bool kAcc>
 __global__ void pool_max_bwd_t(const float* __restrict__ x, const float* __restrict__ dy,
-                               float* dx, PoolDims d) {
+                               float* dx, PoolDims d, FastDiv by_oh, FastDiv by_h) {
   extern __shared__ float psm[];
   const int HW = d.H * d.W, OHW = d.OH * d.OW;
   float* xs = psm;              // [HW]
@@ -316,9 +423,10 @@ __global__ void pool_max_bwd_t(const float* __restrict__ x, const float* __restr
   const float* xp = x + plane * HW;
   const float* dyp = dy + plane * OHW;
   for (int e = threadIdx.x; e < HW; e += blockDim.x) xs[e] = __ldg(xp + e);
+  for (int w = threadIdx.x; w < OHW; w += blockDim.x) ds[w] = __ldg(dyp + w);
   __syncthreads();
   for (int w = threadIdx.x; w < OHW; w += blockDim.x) {
-    const int oj = w / d.OH, oi = w - oj * d.OH;
+    const int oj = (int)by_oh.div(w), oi = w - oj * d.OH;
     const int si = oi * SH - d.pt, sj = oj * SW - d.pl;
     float best = 0.f;
     int best_e = -1;
@@ -328,23 +436,23 @@ __global__ void pool_max_bwd_t(const float* __restrict__ x, const float* __restr
 #pragma unroll
       for (int a = 0; a < WH; ++a) {
         const int i = si + a;
-        if (i >= 0 && i < d.H && j >= 0 && j < d.W) {
-          const float v = xs[i + d.H * j];
-          if (best_e < 0 || v > best) {
+        if (INSIDE || (i >= 0 && i < d.H && j >= 0 && j < d.W)) {
+          const int e = i + d.H * j;
+          const float v = xs[e];
+          if ((INSIDE && a == 0 && b == 0) || (!INSIDE && best_e < 0) || v > best) {
             best = v;
-            best_e = i + d.H * j;
+            best_e = e;
           }
         }
       }
     }
     arg[w] = best_e;
-    ds[w] = __ldg(dyp + w);
   }
   __syncthreads();
   constexpr int NI = (WH + SH - 1) / SH, NJ = (WW + SW - 1) / SW;
   float* dxp = dx + plane * HW;
   for (int e = threadIdx.x; e < HW; e += blockDim.x) {
-    const int j = e / d.H, i = e - j * d.H;
+    const int j = (int)by_h.div(e), i = e - j * d.H;
     const int ti = i + d.pt, tj = j + d.pl;
     const int oi_hi = min(d.OH - 1, ti / SH), oj_hi = min(d.OW - 1, tj / SW);
     const int oi_lo = ti - WH + 1 <= 0 ? 0 : (ti - WH + SH) / SH;
@@ -914,10 +1022,57 @@ void sgd_step(float* w, float* v, const float* g, int64_t n, float lr, float mom
   sgd_k<<<blocks_for(n, 256), 256, 0, s>>>(w, v, g, n, lr, mom, wd);
 }
 
+// every window inside the input: no padding and the last window ends in it
+static bool pool_inside(const PoolDims& d) {
+  return d.pt == 0 && d.pl == 0 && (d.OH - 1) * d.sh + d.wh <= d.H &&
+         (d.OW - 1) * d.sw + d.ww <= d.W;
+}
+
 template <int WH, int WW, int SH, int SW>
-static void pool_max_fwd_launch(const float* x, float* y, const PoolDims& d, cudaStream_t s) {
+static void pool_max_fwd_launch(const float* x, float* y, const PoolDims& d, uint8_t* arg,
+                                cudaStream_t s) {
   const int64_t total = (int64_t)d.OH * d.OW * d.C * d.N;
-  pool_max_fwd_t<WH, WW, SH, SW><<<blocks_for(total, 256), 256, 0, s>>>(x, y, d);
+  const FastDiv a(d.OH * d.OW), b(d.OH);
+  if (pool_inside(d))
+    pool_max_fwd_t<WH, WW, SH, SW, true><<<blocks_for(total, 256), 256, 0, s>>>(x, y, d, a, b,
+                                                                                arg);
+  else
+    pool_max_fwd_t<WH, WW, SH, SW, false><<<blocks_for(total, 256), 256, 0, s>>>(x, y, d, a, b,
+                                                                                 arg);
+}
+
+template <int WH, int WW, int SH, int SW>
+static void pool_max_bwd_arg_launch(const uint8_t* arg, const float* dy, float* dx,
+                                    const PoolDims& d, int acc, cudaStream_t s) {
+  const int64_t total = (int64_t)d.H * d.W * d.C * d.N;
+  const FastDiv a(d.H * d.W), b(d.H);
+  if (acc)
+    pool_max_bwd_arg_t<WH, WW, SH, SW, true><<<blocks_for(total, 256), 256, 0, s>>>(arg, dy, dx,
+                                                                                     d, a, b);
+  else
+    pool_max_bwd_arg_t<WH, WW, SH, SW, false><<<blocks_for(total, 256), 256, 0, s>>>(arg, dy, dx,
+                                                                                      d, a, b);
+}
+
+static int64_t pool_arg_key(const float* x, const PoolDims& d) {
+  return (int64_t)(((((((uint64_t)d.H * 4099 + d.W) * 65537 + d.C) * 131071 + d.N) * 31 + d.wh) *
+                        31 + d.sh) * 31 + d.pt) ^ (uint64_t)(uintptr_t)x;
+}
+
+template <int WH, int WW, int SH, int SW>
+static void pool_max_bwd_launch(const float* x, const float* dy, float* dx, const PoolDims& d,
+                                int acc, size_t smem, cudaStream_t s) {
+  const unsigned planes = (unsigned)((int64_t)d.C * d.N);
+  const FastDiv a(d.OH), b(d.H);
+  const bool in = pool_inside(d);
+  if (in && acc)
+    pool_max_bwd_t<WH, WW, SH, SW, true, true><<<planes, 256, smem, s>>>(x, dy, dx, d, a, b);
+  else if (in)
+    pool_max_bwd_t<WH, WW, SH, SW, true, false><<<planes, 256, smem, s>>>(x, dy, dx, d, a, b);
+  else if (acc)
+    pool_max_bwd_t<WH, WW, SH, SW, false, true><<<planes, 256, smem, s>>>(x, dy, dx, d, a, b);
+  else
+    pool_max_bwd_t<WH, WW, SH, SW, false, false><<<planes, 256, smem, s>>>(x, dy, dx, d, a, b);
 }
 
 // compile-time window/stride of a max pooling, or 0
@@ -928,22 +1083,58 @@ static int pool_fixed(const PoolDims& d) {
   return 0;
 }
 
-void pool_forward(const float* x, float* y, const PoolDims& d, cudaStream_t s) {
+// With a layer cache (graph engine) the fixed-window max path also records
+// each window's argmax for the backward of the same step.
+void pool_forward(const float* x, float* y, const PoolDims& d, cudaStream_t s, ConvCache* cache) {
   int64_t total = (int64_t)d.OH * d.OW * d.C * d.N;
   if (total == 0) return;
   count_launch();
-  switch (pool_fixed(d)) {
-    case 3: pool_max_fwd_launch<3, 3, 2, 2>(x, y, d, s); return;
-    case 2: pool_max_fwd_launch<2, 2, 2, 2>(x, y, d, s); return;
+  // FastDiv and 32-bit indices: total * OH*OW < 2^39
+  const int fx = total < (1ll << 31) && total * d.OH * d.OW < (1ll << 39) ? pool_fixed(d) : 0;
+  uint8_t* arg = nullptr;
+  if (fx && cache) {
+    arg = (uint8_t*)cache->buf.get((size_t)total, s);
+    if (arg) {
+      cache->valid = true;
+      cache->src = x;
+      cache->key = pool_arg_key(x, d);
+    }
+  }
+  switch (fx) {
+    case 3: pool_max_fwd_launch<3, 3, 2, 2>(x, y, d, arg, s); return;
+    case 2: pool_max_fwd_launch<2, 2, 2, 2>(x, y, d, arg, s); return;
     default: pool_fwd_k<<<blocks_for(total, 256), 256, 0, s>>>(x, y, d);
   }
 }
 
 void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d, int acc,
-                   cudaStream_t s) {
+                   cudaStream_t s, ConvCache* cache) {
   int64_t total = (int64_t)d.H * d.W * d.C * d.N;
   if (total == 0) return;
   count_launch();
+  const int fx = pool_fixed(d);
+  if (fx && cache && cache->valid && cache->src == x && cache->key == pool_arg_key(x, d) &&
+      total < (1ll << 31) && total * d.H * d.W < (1ll << 39)) {
+    const uint8_t* arg = (const uint8_t*)cache->buf.ptr;
+    if (fx == 3) {
+      const int A = (d.H + d.pt + 1) / 2, B = (d.W + d.pl + 1) / 2;
+      const int64_t blocks = (int64_t)A * B * d.C * d.N;
+      const FastDiv by_a(A), by_ab(A * B);
+      if (blocks * A * B < (1ll << 39)) {
+        if (acc)
+          pool_max3s2_bwd_arg_k<true><<<blocks_for(blocks, 256), 256, 0, s>>>(arg, dy, dx, d, A,
+                                                                              B, by_a, by_ab);
+        else
+          pool_max3s2_bwd_arg_k<false><<<blocks_for(blocks, 256), 256, 0, s>>>(arg, dy, dx, d, A,
+                                                                               B, by_a, by_ab);
+        return;
+      }
+      pool_max_bwd_arg_launch<3, 3, 2, 2>(arg, dy, dx, d, acc, s);
+    } else {
+      pool_max_bwd_arg_launch<2, 2, 2, 2>(arg, dy, dx, d, acc, s);
+    }
+    return;
+  }
   const size_t smem = sizeof(float) * ((size_t)d.H * d.W + 2 * (size_t)d.OH * d.OW);
   if (smem <= 96 * 1024) {
     static bool configured = false;
@@ -956,11 +1147,10 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
     }
     const unsigned planes = (unsigned)((int64_t)d.C * d.N);
     const int fx = pool_fixed(d);
-    if (fx && smem <= 48 * 1024) {
-      if (fx == 3 && acc) pool_max_bwd_t<3, 3, 2, 2, true><<<planes, 256, smem, s>>>(x, dy, dx, d);
-      if (fx == 3 && !acc) pool_max_bwd_t<3, 3, 2, 2, false><<<planes, 256, smem, s>>>(x, dy, dx, d);
-      if (fx == 2 && acc) pool_max_bwd_t<2, 2, 2, 2, true><<<planes, 256, smem, s>>>(x, dy, dx, d);
-      if (fx == 2 && !acc) pool_max_bwd_t<2, 2, 2, 2, false><<<planes, 256, smem, s>>>(x, dy, dx, d);
+    // FastDiv needs n * d < 2^39 (n < HW, d <= H)
+    if (fx && smem <= 48 * 1024 && (int64_t)d.H * d.W * d.H < (1ll << 39)) {
+      if (fx == 3) pool_max_bwd_launch<3, 3, 2, 2>(x, dy, dx, d, acc, smem, s);
+      else pool_max_bwd_launch<2, 2, 2, 2>(x, dy, dx, d, acc, smem, s);
       return;
     }
     if (acc)

@@ -119,3 +119,34 @@ def test_alexnet_full_batch_properties():
     r6, c6 = g.get("r6", deriv=True), g.get("f6")
     assert np.all(g.get("f6", deriv=True)[c6 <= 0] == 0)
     assert np.isfinite(g.get("conv1f", deriv=True)).all()
+
+
+@pytest.mark.parametrize("pad", [(0, 0, 0, 0), (0, 1, 0, 1)])
+def test_engine_pool_argmax_route_bitexact(pad):
+    """In a graph the max pool records its argmax in the forward and the
+    backward routes from it (engine.cu / kernels.cu pool_max_bwd_arg_t): dx
+    must equal the oracle pool backward (pool.cpp:83-126) of the same dy
+    bit for bit, spikes making >= 3 windows share an argmax."""
+    from paper_1412_4564_b200.graph import Graph
+    xs, n = (27, 27, 4, 3), 3
+    r = O.Rng(41)
+    x = r.uniform(O.size(xs), -0.01, 0.01).reshape(xs[::-1])
+    x[:, :, ::2, ::2] += 1.0 + r.uniform(x[:, :, ::2, ::2].size).reshape(x[:, :, ::2, ::2].shape)
+    x = x.ravel()
+    pg = (3, 3, 2, 2, *pad, 0)
+    _, ps = O.pool_forward(x, xs, pg)
+    g = Graph(math="fp32")
+    g.add_input("x", xs)
+    g.add_input("label", (1, 1, 1, n))
+    g.add_layer("pool", "pool1", ["x"], ["p1"], list(pg))
+    # average the pooled map to 1x1 so every window gets a gradient
+    g.add_layer("pool", "pool2", ["p1"], ["p2"], [ps[0], ps[1], 1, 1, 0, 0, 0, 0, 1])
+    g.add_layer("loss", "loss", ["p2", "label"], ["objective"], [])
+    g.finalize()
+    g.set("x", x)
+    g.set("label", np.array([1, 3, 2], np.float32))
+    g.forward()
+    g.backward("objective")
+    dp1 = g.get("p1", deriv=True)
+    assert np.abs(dp1).max() > 0
+    assert np.array_equal(g.get("x", deriv=True), O.pool_backward(x, xs, pg, dp1))
