@@ -92,6 +92,15 @@ const char* ck_last_error(const ck_handle* h);
 const char* ck_version(void);
 /* Number of kernels this handle launched since creation (bench evidence). */
 int64_t ck_launch_count(const ck_handle* h);
+/* Per-launch timing of the tensor-core GEMM kernels (bench roofline): while
+ * on, every GEMM launch is bracketed by CUDA events on its stream and recorded
+ * with a label and its algorithmic FLOP count (2*N*OH*OW*K*fh*fw*C/groups).
+ * ck_kernel_profile_get synchronises the record's end event. */
+ck_status ck_set_kernel_profiling(ck_handle* h, int on);
+int ck_kernel_profile_count(const ck_handle* h);
+ck_status ck_kernel_profile_get(ck_handle* h, int i, const char** label, float* ms,
+                                double* flops);
+ck_status ck_kernel_profile_clear(ck_handle* h);
 /* Stream-ordered copy between any host / device pointers (UVA). */
 ck_status ck_memcpy(ck_handle* h, void* dst, const void* src, int64_t bytes, ck_stream stream);
 

@@ -56,6 +56,11 @@ SIGNATURES = {
     "ck_last_error": (C.c_char_p, [P]),
     "ck_version": (C.c_char_p, []),
     "ck_launch_count": (C.c_int64, [P]),
+    "ck_set_kernel_profiling": (C.c_int, [P, C.c_int]),
+    "ck_kernel_profile_count": (C.c_int, [P]),
+    "ck_kernel_profile_get": (C.c_int, [P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_float),
+                                        C.POINTER(C.c_double)]),
+    "ck_kernel_profile_clear": (C.c_int, [P]),
     "ck_memcpy": (S, [P, P, P, C.c_int64, P]),
     "ck_conv_output_shape": (S, [P, ck_shape, ck_shape, C.POINTER(ck_conv_geom), C.POINTER(ck_shape)]),
     "ck_convt_output_shape": (S, [P, ck_shape, ck_shape, C.POINTER(ck_convt_geom), C.POINTER(ck_shape)]),

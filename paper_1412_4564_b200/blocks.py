@@ -130,6 +130,21 @@ class Handle:
     def launches(self) -> int:
         return lib().ck_launch_count(self.h)
 
+    def kernel_profiling(self, on: bool):
+        """Time every tensor-core GEMM launch (ck_set_kernel_profiling)."""
+        self.check(lib().ck_kernel_profile_clear(self.h))
+        self.check(lib().ck_set_kernel_profiling(self.h, int(on)))
+
+    def kernel_profile(self):
+        """[(label, ms, algorithmic flops)] of the GEMM launches recorded so far."""
+        out = []
+        for i in range(lib().ck_kernel_profile_count(self.h)):
+            lab, ms, fl = C.c_char_p(), C.c_float(), C.c_double()
+            self.check(lib().ck_kernel_profile_get(self.h, i, C.byref(lab), C.byref(ms),
+                                                   C.byref(fl)))
+            out.append((lab.value.decode(), ms.value, fl.value))
+        return out
+
 
 def handle(device: int | None = None) -> Handle:
     device = torch.cuda.current_device() if device is None else device

@@ -169,21 +169,29 @@ void after_launch() { check_cuda(cudaPeekAtLastError(), "kernel launch"); }
 
 // ---- conv dispatch (shared by the C ABI and the graph engine) ----------------
 
+// a profiler label left by a tensor-core path that declined the shape
+static void prof_drop() {
+  if (g_prof) g_prof->label.clear();
+}
+
 void conv_forward_dispatch(ck_handle* h, const float* x, const float* f, const float* bias,
                            float* y, const ConvDims& d, int relu, ck_math math, cudaStream_t s) {
   if (math == CK_MATH_TF32 && conv_tc_forward(h, x, f, bias, y, d, relu, s)) return;
+  prof_drop();
   conv_fwd_fp32(x, f, bias, y, d, relu, s);
 }
 
 void conv_dgrad_dispatch(ck_handle* h, const float* dy, const float* f, float* dx,
                          const ConvDims& d, int acc, ck_math math, cudaStream_t s) {
   if (math == CK_MATH_TF32 && conv_tc_dgrad(h, dy, f, dx, d, acc, s)) return;
+  prof_drop();
   conv_dgrad_fp32(dy, f, dx, d, acc, s);
 }
 
 void conv_wgrad_dispatch(ck_handle* h, const float* x, const float* dy, float* df,
                          const ConvDims& d, int acc, ck_math math, cudaStream_t s) {
   if (math == CK_MATH_TF32 && conv_tc_wgrad(h, x, dy, df, d, acc, s)) return;
+  prof_drop();
   void* ws = h->ws.get(conv_wgrad_ws_bytes(d), s);
   if (!ws) throw Err(CK_ERR_CUDA, "workspace allocation failed");
   conv_wgrad_fp32(x, dy, df, d, acc, ws, s);
@@ -242,6 +250,35 @@ void ck_destroy(ck_handle* h) {
 const char* ck_last_error(const ck_handle* h) { return h ? h->err.c_str() : "null handle"; }
 
 int64_t ck_launch_count(const ck_handle* h) { return h ? h->counter.n : 0; }
+
+ck_status ck_set_kernel_profiling(ck_handle* h, int on) {
+  CK_API_BEGIN(h)
+  h->prof.on = on != 0;
+  h->prof.label.clear();
+  CK_API_END(h)
+}
+
+int ck_kernel_profile_count(const ck_handle* h) { return h ? (int)h->prof.recs.size() : 0; }
+
+ck_status ck_kernel_profile_get(ck_handle* h, int i, const char** label, float* ms,
+                                double* flops) {
+  CK_API_BEGIN(h)
+  if (i < 0 || i >= (int)h->prof.recs.size()) throw Err(CK_ERR_ARG, "profile index out of range");
+  auto& r = h->prof.recs[(size_t)i];
+  check_cuda(cudaEventSynchronize(r.b), "event sync");
+  float t = 0;
+  check_cuda(cudaEventElapsedTime(&t, r.a, r.b), "event time");
+  if (label) *label = r.label.c_str();
+  if (ms) *ms = t;
+  if (flops) *flops = r.flops;
+  CK_API_END(h)
+}
+
+ck_status ck_kernel_profile_clear(ck_handle* h) {
+  CK_API_BEGIN(h)
+  h->prof.clear();
+  CK_API_END(h)
+}
 
 ck_status ck_memcpy(ck_handle* h, void* dst, const void* src, int64_t bytes, ck_stream stream) {
   CK_API_BEGIN(h)

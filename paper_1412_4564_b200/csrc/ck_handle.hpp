@@ -25,6 +25,7 @@ struct ck_handle {
   ck::TcState* tc = nullptr;
   uint64_t call = 0;      // API call id: scopes transform caches to one call
   ck::ConvCache* conv_cache = nullptr;  // set by the graph engine around conv calls
+  ck::KernelProfiler prof;
 };
 
 namespace ck {
@@ -38,12 +39,17 @@ struct Err : std::runtime_error {
 // Binds the device and the launch counter for the duration of one API call.
 struct HandleScope {
   LaunchCounter* prev;
-  explicit HandleScope(ck_handle* h) : prev(g_counter) {
+  KernelProfiler* prev_prof;
+  explicit HandleScope(ck_handle* h) : prev(g_counter), prev_prof(g_prof) {
     ++h->call;
     cudaSetDevice(h->device);
     g_counter = &h->counter;
+    g_prof = &h->prof;
   }
-  ~HandleScope() { g_counter = prev; }
+  ~HandleScope() {
+    g_counter = prev;
+    g_prof = prev_prof;
+  }
 };
 
 std::string shape_str(const ck_shape& s);

@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "ck/ck.h"
 
@@ -59,6 +60,34 @@ struct LaunchCounter {
 
 // ---- launchers (kernels.cu / conv_simt.cu / conv_tc.cu) -------------------
 extern thread_local LaunchCounter* g_counter;  // counts kernel launches
+
+// Optional per-launch timing of the GEMM kernels (ck_set_kernel_profiling).
+struct KernelProfiler {
+  bool on = false;
+  std::string label;  // pending label / FLOP count for the next GEMM launch
+  double flops = 0;
+  struct Rec {
+    std::string label;
+    double flops;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  void clear() {
+    for (auto& r : recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    recs.clear();
+  }
+  ~KernelProfiler() { clear(); }
+};
+extern thread_local KernelProfiler* g_prof;
+inline void prof_next(const std::string& label, double flops) {
+  if (g_prof && g_prof->on) {
+    g_prof->label = label;
+    g_prof->flops = flops;
+  }
+}
 inline void count_launch(int k = 1) {
   if (g_counter) g_counter->n += k;
 }

@@ -1460,11 +1460,14 @@ static int pick_bn(int n) {
 // Tile M: two M=128 MMAs per CTA (sharing each B tile) once M is large.
 // Keep TMEM double-buffered (2 x BM/128 x BN <= 512 columns) so the epilogue
 // of one tile overlaps the next tile's mainloop.
-static int pick_bm(int64_t M, int BN) {
+// BM = 256 (two M=128 MMAs sharing each B tile) halves the B traffic per
+// FLOP; for the conv im2col GEMMs it wins even without TMEM double buffering
+// (BN > 128), for the FC GEMMs only when the accumulators stay double-buffered.
+static int pick_bm(int64_t M, int BN, bool conv = false) {
   static const int mode = getenv("CK_TC_BM") ? atoi(getenv("CK_TC_BM")) : 0;  // experiments
   if (mode == 256) return M >= 4096 ? 256 : 128;
   if (mode == 128) return 128;
-  return (M >= 4096 && BN <= 128) ? 256 : 128;
+  return (M >= 4096 && (conv || BN <= 128)) ? 256 : 128;
 }
 
 template <int AK, int BK>
@@ -1491,7 +1494,30 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
   const int tiles = ((p.M + p.BM - 1) / p.BM) * ((p.N + p.BN - 1) / p.BN) * grid_z;
   const int grid = std::min(tiles, 148);
   count_launch();
+  KernelProfiler* pr = (g_prof && g_prof->on && !g_prof->label.empty()) ? g_prof : nullptr;
+  KernelProfiler::Rec rec;
+  if (pr) {
+    rec.label = pr->label;
+    rec.flops = pr->flops;
+    pr->label.clear();
+    cudaEventCreate(&rec.a);
+    cudaEventCreate(&rec.b);
+    cudaEventRecord(rec.a, s);
+  }
   tc_gemm_kernel<AK, BK><<<grid, kThreads, smem, s>>>(a, b, p);
+  if (pr) {
+    cudaEventRecord(rec.b, s);
+    pr->recs.push_back(rec);
+  }
+}
+
+// label + algorithmic FLOP (2*N*OH*OW*K*fh*fw*C/g) of a conv pass for the profiler
+static void prof_conv(const char* pass, const ConvDims& d) {
+  if (!g_prof || !g_prof->on) return;
+  char buf[160];
+  snprintf(buf, sizeof buf, "%s %dx%dx%d->%d f%dx%d s%d g%d N%d", pass, d.H, d.W, d.C, d.K, d.fh,
+           d.fw, d.sh, d.groups, d.N);
+  prof_next(buf, 2.0 * d.N * d.OH * d.OW * (double)d.K * d.fh * d.fw * d.Cg);
 }
 
 static int split_for(int tiles, int kblocks) {
@@ -1947,7 +1973,7 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.n_valid = d.K;
-  p.BM = pick_bm(p.M, p.BN);
+  p.BM = pick_bm(p.M, p.BN, true);
   CUtensorMap ta = map_im2col(xt, z.Csp, z.U, z.V, d.N, 0, 0, -(z.Th - 1), -(z.Tw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(ft, (uint64_t)taps * z.Csp, d.K, (uint64_t)taps * z.Csp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.K + p.BN - 1) / p.BN, 1, s);
@@ -1986,7 +2012,7 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   p.epi = EPI_S2D; p.out = dx; p.epi_OHW = z.U * z.V;
   p.s2d = z.s; p.s2d_U = z.U; p.s2d_H = d.H; p.s2d_W = d.W; p.s2d_C = d.C;
   p.acc = acc; p.n_valid = z.Cs;
-  p.BM = pick_bm(p.M, p.BN);
+  p.BM = pick_bm(p.M, p.BN, true);
   CUtensorMap ta = map_im2col(dyt, Kp, z.U, z.V, d.N, -(z.Th - 1), -(z.Tw - 1), -(z.Th - 1),
                               -(z.Tw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kp, z.Cs, (uint64_t)taps * Kp, p.BN);
@@ -2093,6 +2119,7 @@ static bool is_fc(const ConvDims& d) {
 bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
                      const ConvDims& d, int relu, cudaStream_t s) {
   if (!load_driver()) return false;
+  prof_conv("fprop", d);
   const int Kg = d.Kg();
   if (is_fc(d)) {
     // Y[k, n] = sum_q F[q, k] X[q, n]   (A = filters, B = images, both K-major)
@@ -2171,7 +2198,7 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
   p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.acc = 0; p.n_valid = Kg;
-  p.BM = pick_bm(p.M, p.BN);
+  p.BM = pick_bm(p.M, p.BN, true);
   if (on_grid) p.pt = p.pl = 0;
   CUtensorMap ta = on_grid ? map_im2col(xt, Cp, Hg, Wg, d.N, 0, 0, -(d.fh - 1), -(d.fw - 1), 1,
                                         1, p.BM)
@@ -2187,6 +2214,7 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
 bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, const ConvDims& d,
                    int acc, cudaStream_t s) {
   if (!load_driver()) return false;
+  prof_conv("dgrad", d);
   const int Kg = d.Kg();
   if (is_fc(d)) {
     // dX[q, n] = sum_k F[q, k] dY[k, n]: A = F read MN-major in place
@@ -2266,7 +2294,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   p.epi = EPI_PIX; p.out = dx; p.ld = (int64_t)d.H * d.W;
   p.img_stride = (int64_t)d.C * d.H * d.W; p.grp_col = d.Cg; p.epi_OHW = d.H * d.W;
   p.bias = nullptr; p.relu = 0; p.acc = acc; p.n_valid = d.Cg;
-  p.BM = pick_bm(p.M, p.BN);
+  p.BM = pick_bm(p.M, p.BN, true);
   CUtensorMap ta = on_grid
                        ? map_im2col(dyt, Kp, Hg, Wg, d.N, -qt, -ql, d.H - Hg - qt, d.W - Wg - ql,
                                     1, 1, p.BM)
@@ -2301,6 +2329,7 @@ bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, i
 bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, const ConvDims& d,
                    int acc, cudaStream_t s) {
   if (!load_driver()) return false;
+  prof_conv("wgrad", d);
   const int Kg = d.Kg();
   if (is_fc(d)) {
     // dF[q, k] = sum_n X[q, n] dY[k, n]: both operands read MN-major in place

@@ -18,6 +18,7 @@
 namespace ck {
 
 thread_local LaunchCounter* g_counter = nullptr;
+thread_local KernelProfiler* g_prof = nullptr;
 
 namespace {
 
@@ -104,6 +105,26 @@ __global__ void sgd_k(float* w, float* v, const float* __restrict__ g, int64_t n
     float vi = __fadd_rn(__fmul_rn(mom, v[i]), -__fmul_rn(lr, t));
     v[i] = vi;
     w[i] = __fadd_rn(wi, vi);
+  }
+}
+
+// float4 variant (16-byte aligned arrays, n % 4 == 0): same rounding per lane.
+__global__ void sgd_v4_k(float4* w, float4* v, const float4* __restrict__ g, int64_t n4,
+                         float lr, float mom, float wd) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 wi = w[i], vi0 = v[i], gi = __ldg(g + i);
+    float4 vo, wo;
+#define CK_SGD_LANE(c)                                                        \
+  {                                                                           \
+    const float t = __fadd_rn(gi.c, __fmul_rn(wd, wi.c));                     \
+    vo.c = __fadd_rn(__fmul_rn(mom, vi0.c), -__fmul_rn(lr, t));               \
+    wo.c = __fadd_rn(wi.c, vo.c);                                             \
+  }
+    CK_SGD_LANE(x) CK_SGD_LANE(y) CK_SGD_LANE(z) CK_SGD_LANE(w)
+#undef CK_SGD_LANE
+    v[i] = vo;
+    w[i] = wo;
   }
 }
 
@@ -1019,6 +1040,11 @@ void sgd_step(float* w, float* v, const float* g, int64_t n, float lr, float mom
               cudaStream_t s) {
   if (n == 0) return;
   count_launch();
+  if (n % 4 == 0 && (((uintptr_t)w | (uintptr_t)v | (uintptr_t)g) & 15) == 0) {
+    sgd_v4_k<<<blocks_for(n / 4, 256), 256, 0, s>>>((float4*)w, (float4*)v, (const float4*)g,
+                                                     n / 4, lr, mom, wd);
+    return;
+  }
   sgd_k<<<blocks_for(n, 256), 256, 0, s>>>(w, v, g, n, lr, mom, wd);
 }
 
