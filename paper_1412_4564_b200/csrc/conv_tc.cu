@@ -47,18 +47,13 @@ namespace ck {
 // ============================================================================
 namespace tc {
 
-// Every operand is K-major (K contiguous in a 128-byte swizzled row): the
-// "transpose" (MN-major) bit of the kind::tf32 instruction descriptor reads
-// as zeros on this part (probed, tools/tc_probe.py), so layouts that would
-// need it are produced K-major by the transform kernels instead.
+// Operand kinds.  K-major operands use SWIZZLE_128B rows of 32 k; MN-major
+// ones (tf32 allows them only in the SWIZZLE_128B_BASE32B layout,
+// tools/mn_probe.cu) rows of 32 m/n per k.
 enum OpKind : int {
   OP_TILED_K = 0,     // 2D tensor (K inner, MN outer), box (32, rows)
-  OP_IM2COL_K = 2,    // 4D im2col over a pixel-major tensor, box 128 px x 32 ch
-  OP_SHIFT_K = 4,     // wgrad B: boxes (32 px, 32 ch, 1, 1) of padded planes
-                      // [copy][n][c][PL], pixel coordinate shifted by the tap
-  OP_PLANE_K = 5,     // wgrad A: box (32 px, rows, 1) of padded planes [n][k][PL]
+  OP_IM2COL_K = 2,    // 4D im2col over a pixel-major tensor, box BM px x 32 ch
   OP_TILED_MN = 6,    // MN-major 2D tensor [K][MN] (MN inner): 32x32 boxes, SW128_32B atoms
-  OP_IM2COL_MN = 7,   // wgrad B: im2col boxes of 32 px (K) x 32 ch (MN) per (tap, c block)
   OP_SHIFT_MN = 8,    // wgrad B: 3D boxes {32 ch, 32 grid rows + tap shift, b_rows/32 blocks}
 };
 
@@ -93,17 +88,16 @@ struct GemmParams {
   const float* bias;      // per col (EPI_PIX) or per row (EPI_LINEAR)
   int relu, acc;
   int n_valid;            // columns < n_valid are stored
-  int Hp;                 // OP_SHIFT_K: padded plane height (tap shift = fi + Hp*fj)
-  int b_grp_row;          // OP_SHIFT_K: per-group row (channel) offset
+  int Hp;                 // OP_SHIFT_MN: grid pitch (tap shift = fi + Hp*fj)
+  int b_grp_row;          // halo kernel: per-group filter row offset
   int s2d, s2d_U, s2d_H, s2d_W, s2d_C;  // EPI_S2D: factor, grid height, target dims
   int exp;                // debug experiments (CK_TC_EXP)
   int BM;                 // 128 or 256 (two M=128 MMAs sharing the B tile)
   int nacc;               // TMEM accumulator buffers (2: epilogue overlaps mainloop)
   int groups;             // tiles = ceil(M/BM) * ceil(N/BN) * groups * splits
-  int kpp;                // OP_PLANE_K / OP_SHIFT_K: K blocks (32 px) per image plane
-  int b_rows;             // OP_SHIFT_K: channel rows per TMA box (divides Cgp and BN)
+  int b_rows;             // OP_SHIFT_MN: channels per TMA box (divides Cgp and BN)
   int a_mn3d, b_mn3d;     // OP_TILED_MN: one 3D box per stage (MN % 32 == 0) vs R/32 2D boxes
-  int taps;               // OP_IM2COL_MN / halo kernel: fh * fw
+  int taps;               // OP_SHIFT_MN / halo kernel: fh * fw
   // halo kernel (stride-1 conv on a padded pixel-major grid, see halo_conv_kernel)
   int hg, hw_grid;        // grid pitch (rows per column) and rows per image; 0 = not a grid
   int ohv, owv;           // valid output extent on the grid
@@ -493,9 +487,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             else
               for (int j = 0; j < p.BM / 32; ++j)
                 tma_2d(a + j * 4096, &tma_a, &full[s], mn0 + 32 * j, k0);
-          } else if (AK == OP_PLANE_K) {
-            const int n = kb / p.kpp, q0 = (kb - n * p.kpp) * 32;
-            tma_3d(a, &tma_a, &full[s], q0, T.m0 + T.grp * p.a_grp_mn, n);
           } else {  // OP_IM2COL_K: kb = tap * cchunks + cc; one box walks BM pixels
             const int tap = kb / p.cchunks, cc = kb - tap * p.cchunks;
             const int fj = tap / p.fh, fi = tap - fj * p.fh;
@@ -524,33 +515,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_3d(b + j * p.b_rows * 128, &tma_b, &full[s], 0, k0 + fi + p.Hp * fj,
                      (T.grp * p.b_grp_c + c) / 32);
             }
-          } else if (BK == OP_IM2COL_MN) {
-            // K block = 32 consecutive output pixels (h fastest, then w, n);
-            // MN block j = 32 channels of tap (fi, fj): one im2col box each.
-            const int ohw = p.OH * p.OW;
-            const int n = k0 / ohw, r = k0 - n * ohw;
-            const int ow = r / p.OH, oh = r - ow * p.OH;
-            const int h0 = oh * p.sh - p.pt, w0 = ow * p.sw - p.pl;
-            for (int j = 0; j < p.BN / 32; ++j) {
-              const int nn = T.n0 + 32 * j;
-              int tap = nn / (p.cchunks * 32);
-              const int c = nn - tap * p.cchunks * 32;
-              tap = min(tap, p.taps - 1);  // columns past the last tap are masked
-              const int fj = tap / p.fh, fi = tap - fj * p.fh;
-              tma_im2col_4d(b + j * 4096, &tma_b, &full[s], T.grp * p.b_grp_c + c, h0, w0, n,
-                            (uint16_t)fi, (uint16_t)fj);
-            }
-          } else {  // OP_SHIFT_K: rows n = (tap, c), K = pixels of image plane img
-            const int img = kb / p.kpp, q0 = (kb - img * p.kpp) * 32;
-            for (int j = 0; j < p.BN / p.b_rows; ++j) {
-              const int nn = T.n0 + p.b_rows * j;
-              const int tap = nn / (p.cchunks * 32);
-              const int c = nn - tap * p.cchunks * 32;
-              const int fj = tap / p.fh, fi = tap - fj * p.fh;
-              const int shift = fi + p.Hp * fj, r = shift & 3;  // copy r keeps 16-B alignment
-              tma_4d(b + j * p.b_rows * 128, &tma_b, &full[s], q0 + shift - r,
-                     T.grp * p.b_grp_row + c, img, r);
-            }
           }
         }
       }
@@ -560,7 +524,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // --------------------------------------------------------- MMA issuer --
     if (lane == 0) {
       constexpr bool a_mn = AK == OP_TILED_MN,
-                     b_mn = BK == OP_TILED_MN || BK == OP_IM2COL_MN || BK == OP_SHIFT_MN;
+                     b_mn = BK == OP_TILED_MN || BK == OP_SHIFT_MN;
       const uint32_t idesc = idesc_tf32(p.BN, a_mn, b_mn);
       int it = 0, tc = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
@@ -827,32 +791,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 //                          layout transforms (HBM bound)
 // ============================================================================
 
-// HWCN x[n][c][w][h] -> pixel-major xT[n][w][h][cp], channel c of group g at
-// cp = g*Cgp + (c - g*Cg), zeros in the per-group padding.  32x32 smem tile.
-__global__ void to_pixel_major_k(const float* __restrict__ x, float* __restrict__ xt, int HW,
-                                 int C, int Cg, int Cgp, int groups) {
-  __shared__ float tile[32][33];
-  const int n = blockIdx.z;
-  const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;  // c0 over padded channels
-  const int Cp = Cgp * groups;
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 256 threads: ty 0..7
-  // read: rows = padded channel, cols = pixel (coalesced along pixels)
-  for (int r = ty; r < 32; r += 8) {
-    const int cp = c0 + r;
-    const int g = cp / Cgp, cl = cp - g * Cgp;
-    const int p = p0 + tx;
-    float v = 0.f;
-    if (cp < Cp && cl < Cg && p < HW) v = x[((int64_t)n * C + g * Cg + cl) * HW + p];
-    tile[r][tx] = v;
-  }
-  __syncthreads();
-  // write: rows = pixel, cols = padded channel (coalesced along channels)
-  for (int r = ty; r < 32; r += 8) {
-    const int p = p0 + r, cp = c0 + tx;
-    if (p < HW && cp < Cp) xt[((int64_t)n * HW + p) * Cp + cp] = tile[tx][r];
-  }
-}
-
 // HWCN x[n][c][w][h] -> padded pixel-major grid xg[n][Wg][Hg][cp]: pixel
 // (i, j) at grid position (i + oh, j + ow), channel c of group g at
 // cp = g*Cgp + (c - g*Cgp_local); zero borders and channel pads (the input of
@@ -999,128 +937,6 @@ __global__ void splitk_finish_k(const float* __restrict__ part, float* out, int 
   }
 }
 
-// out[c * ldo + r] = in[r * ldi + c] for an R x Cc matrix (32x32 smem tiles).
-__global__ void transpose_k(const float* __restrict__ in, float* __restrict__ out, int R, int Cc,
-                            int64_t ldi, int64_t ldo) {
-  __shared__ float tile[32][33];
-  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
-  for (int k = ty; k < 32; k += 8) {
-    const int r = r0 + k, c = c0 + tx;
-    tile[k][tx] = (r < R && c < Cc) ? in[(int64_t)r * ldi + c] : 0.f;
-  }
-  __syncthreads();
-  for (int k = ty; k < 32; k += 8) {
-    const int c = c0 + k, r = r0 + tx;
-    if (c < Cc && r < R) out[(int64_t)c * ldo + r] = tile[tx][k];
-  }
-}
-
-// Padded planes for the wgrad operands, layout [copy][n][c][PL] (PL = Hp*Wp
-// rounded up to 32): plane (n, c) holds in[n][c][W][H] at offset (oh, ow),
-// zeros elsewhere (zero padding for x, zero "junk" rows/columns of the output
-// grid for dy).  Copy r is the plane shifted left by r elements: TMA box
-// starts must be 16-byte aligned, so a tap shift t is read from copy t % 4 at
-// t - t % 4.  Grid (ceil(PL/256), C, copies*N).
-__global__ void pad_planes_k(const float* __restrict__ in, float* __restrict__ out, int H, int W,
-                             int Hp, int Wp, int oh, int ow, int C, int N, int PL) {
-  const int c = blockIdx.y;
-  const int rn = blockIdx.z;
-  const int r = rn / N, n = rn - r * N;
-  const float* src = in + ((int64_t)n * C + c) * H * W;
-  float* o = out + ((int64_t)rn * C + c) * PL;
-  const int plane = Hp * Wp;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < PL; q += gridDim.x * blockDim.x) {
-    const int pos = q + r;
-    float v = 0.f;
-    if (pos < plane) {
-      const int jj = pos / Hp, ii = pos - jj * Hp;
-      const int i = ii - oh, j = jj - ow;
-      if (i >= 0 && i < H && j >= 0 && j < W) v = src[i + (int64_t)H * j];
-    }
-    o[q] = v;
-  }
-}
-
-// Same result as pad_planes_k, one block per (n, c) source plane: the plane is
-// read once into shared memory and all `copies` shifted planes are written
-// from it with coalesced stores (no per-element division).
-__global__ void pad_planes_smem_k(const float* __restrict__ in, float* __restrict__ out, int H,
-                                  int W, int Hp, int Wp, int oh, int ow, int C, int N, int PL,
-                                  int copies) {
-  extern __shared__ float pl_src[];
-  const int64_t nc = blockIdx.x;  // n * C + c
-  const int n = (int)(nc / C), c = (int)(nc - (int64_t)n * C);
-  const float* src = in + nc * H * W;
-  for (int e = threadIdx.x; e < H * W; e += blockDim.x) pl_src[e] = src[e];
-  __syncthreads();
-  const int plane = Hp * Wp;
-  const int si = blockDim.x % Hp, sj = blockDim.x / Hp;  // (ii, jj) step of q += blockDim
-  for (int r = 0; r < copies; ++r) {
-    float* o = out + (((int64_t)r * N + n) * C + c) * PL;
-    int pos = threadIdx.x + r;
-    int jj = pos / Hp, ii = pos - jj * Hp;
-    for (int q = threadIdx.x; q < PL; q += blockDim.x) {
-      float v = 0.f;
-      if (pos < plane) {
-        const int i = ii - oh, j = jj - ow;
-        if (i >= 0 && i < H && j >= 0 && j < W) v = pl_src[i + H * j];
-      }
-      o[q] = v;
-      pos += blockDim.x;
-      ii += si;
-      jj += sj;
-      if (ii >= Hp) {
-        ii -= Hp;
-        ++jj;
-      }
-    }
-  }
-}
-
-// Same result again, P planes per block.  Planes nc0..nc0+P-1 are contiguous
-// in the source and, for every copy r, in the output ([copy][n*C + c][PL]),
-// so a block streams P*H*W floats in and P*PL floats per copy out (float4
-// stores).  A per-block table maps a padded-plane position to its source
-// offset (-1 = zero), which removes the per-element division.
-__global__ void pad_planes_multi_k(const float* __restrict__ in, float* __restrict__ out, int H,
-                                   int W, int Hp, int Wp, int oh, int ow, int64_t NC, int PL,
-                                   int copies, int P) {
-  extern __shared__ float sm_pp[];
-  int* tbl = reinterpret_cast<int*>(sm_pp);  // PL + 4 entries
-  float* src = sm_pp + PL + 4;
-  const int HW = H * W, plane = Hp * Wp;
-  const int64_t nc0 = (int64_t)blockIdx.x * P;
-  const int np = (int)(NC - nc0 < P ? NC - nc0 : P);
-  for (int q = threadIdx.x; q < PL + 4; q += blockDim.x) {
-    int v = -1;
-    if (q < plane) {
-      const int jj = q / Hp, ii = q - jj * Hp;
-      const int i = ii - oh, j = jj - ow;
-      if (i >= 0 && i < H && j >= 0 && j < W) v = i + H * j;
-    }
-    tbl[q] = v;
-  }
-  const float* s = in + nc0 * HW;
-  for (int e = threadIdx.x; e < np * HW; e += blockDim.x) src[e] = __ldg(s + e);
-  __syncthreads();
-  const int n4 = np * PL / 4;
-  for (int r = 0; r < copies; ++r) {
-    float4* o = reinterpret_cast<float4*>(out + ((int64_t)r * NC + nc0) * PL);
-    for (int e4 = threadIdx.x; e4 < n4; e4 += blockDim.x) {
-      const int e = e4 * 4, p = e / PL, q = e - p * PL + r;
-      const float* sp = src + p * HW;
-      int t;
-      float4 v;
-      t = tbl[q];     v.x = t >= 0 ? sp[t] : 0.f;
-      t = tbl[q + 1]; v.y = t >= 0 ? sp[t] : 0.f;
-      t = tbl[q + 2]; v.z = t >= 0 ? sp[t] : 0.f;
-      t = tbl[q + 3]; v.w = t >= 0 ? sp[t] : 0.f;
-      o[e4] = v;
-    }
-  }
-}
-
 // ---- space-to-depth (strided convolutions, e.g. AlexNet conv1 s=4) ---------
 // A stride-s conv equals a stride-1 conv over x_s2d[u][v][c'] =
 // x[s*u + a, s*v + b, c], c' = c + Cg*(a + s*b), with taps (t, t2) and filter
@@ -1201,66 +1017,6 @@ __global__ void s2d_pm_strip_k(const float* __restrict__ x, float* __restrict__ 
       r[k] = off >= 0 ? strip_pm[off + base] : 0.f;
     }
     o[e] = make_float4(r[0], r[1], r[2], r[3]);
-  }
-}
-
-// padded s2d planes [copy][n][c'][PL] (c' < Cs), block = (v strip, c, n)
-__global__ void s2d_planes_strip_k(const float* __restrict__ x, float* __restrict__ out, int H,
-                                   int W, int C, int N, int s, int U, int V, int Hp, int Wp,
-                                   int Cs, int PL, int copies, int VB) {
-  extern __shared__ float strip_pl[];
-  const int c = blockIdx.y, n = blockIdx.z, v0 = blockIdx.x * VB;
-  const int vb = min(VB, Wp - v0);
-  const int Hs = s * U;
-  int* tbl = reinterpret_cast<int*>(strip_pl);  // VB*Hp entries
-  float* strip = strip_pl + VB * Hp;
-  for (int l = threadIdx.x; l < vb * Hp; l += blockDim.x) {
-    const int vl = l / Hp, uu = l - vl * Hp;
-    tbl[l] = (uu < U && v0 + vl < V) ? s * uu + Hs * s * vl : -1;
-  }
-  s2d_stage_strip(x, strip, H, W, c, 1, C, n, s * v0, s * vb, Hs);
-  __syncthreads();
-  const int pos0 = v0 * Hp, len = vb * Hp;
-  const bool last = v0 + vb >= Wp;
-  const int planes = s * s;
-  for (int r = 0; r < copies; ++r) {
-    // positions [pos0, pos0 + len) land at q = pos - r (q >= 0)
-    const int skip = pos0 - r < 0 ? r - pos0 : 0;
-    const int span = len - skip;
-    for (int e = threadIdx.x; e < planes * span; e += blockDim.x) {
-      const int ab = e / span, l = e - ab * span + skip;
-      const int a = ab % s, b = ab / s;
-      const int t = tbl[l];
-      const float v = t >= 0 ? strip[t + a + Hs * b] : 0.f;
-      const int cp = c + C * ab;
-      out[(((int64_t)r * N + n) * Cs + cp) * PL + pos0 + l - r] = v;
-    }
-    if (last) {  // zero tail q in [Hp*Wp - r, PL)
-      const int t0 = Hp * Wp - r, tl = PL - t0;
-      for (int e = threadIdx.x; e < planes * tl; e += blockDim.x) {
-        const int ab = e / tl, q = t0 + (e - ab * tl);
-        out[(((int64_t)r * N + n) * Cs + c + C * ab) * PL + q] = 0.f;
-      }
-    }
-  }
-}
-
-// Padded planes of the s2d tensor, same layout and copies as pad_planes_k.
-__global__ void s2d_planes_k(const float* __restrict__ x, float* __restrict__ out, int H, int W,
-                             int C, int N, int s, int U, int V, int Hp, int Wp, int Cs, int PL) {
-  const int cp = blockIdx.y;
-  const int rn = blockIdx.z;
-  const int r = rn / N, n = rn - r * N;
-  float* o = out + ((int64_t)rn * Cs + cp) * PL;
-  const int plane = Hp * Wp;
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < PL; q += gridDim.x * blockDim.x) {
-    const int pos = q + r;
-    float v = 0.f;
-    if (pos < plane) {
-      const int vv = pos / Hp, uu = pos - vv * Hp;
-      if (uu < U && vv < V) v = s2d_read(x, H, W, C, s, C, n, uu, vv, cp);
-    }
-    o[q] = v;
   }
 }
 
@@ -1375,13 +1131,9 @@ static bool load_driver() {
 bool conv_tc_available() { return load_driver(); }
 
 struct TcState {
-  Workspace xt, dyt, ft, part, dyg, bpart;
-  // dy in pixel-major layout is shared by wgrad and dgrad of one
-  // ck_conv_backward call: cached by (source, geometry, call id).
-  const float* dyt_src = nullptr;
-  uint64_t dyt_call = 0;
-  int64_t dyt_key = 0;
-  // same for dy on the padded grid (dyg): shared by grid wgrad and im2col dgrad
+  Workspace xt, ft, part, dyg, bpart;
+  // dy on the padded grid (dyg) is shared by the grid wgrad and the im2col
+  // dgrad of one ck_conv_backward call: cached by (source, geometry, call id)
   const float* dyg_src = nullptr;
   uint64_t dyg_call = 0;
   int64_t dyg_key = 0;
@@ -1395,7 +1147,6 @@ static TcState* state(ck_handle* h) {
 void conv_tc_release(ck_handle* h) {
   if (!h->tc) return;
   h->tc->xt.release();
-  h->tc->dyt.release();
   h->tc->ft.release();
   h->tc->part.release();
   h->tc->dyg.release();
@@ -1565,31 +1316,12 @@ static void to_pm(const float* x, float* xt, int H, int W, int C, int N, int Cg,
   to_grid_pm(x, xt, H, W, C, N, Cg, Cgp, groups, H, W, 0, 0, s);
 }
 
-// dy in pixel-major layout [n][ow][oh][groups * Kgp]; wgrad and dgrad of one
-// ck_conv_backward call share it (same source, geometry and call id).
-static float* dy_pm(ck_handle* h, const float* dy, const ConvDims& d, int Kg, int Kgp, int groups,
-                    cudaStream_t s) {
-  TcState* st = state(h);
-  const int64_t key =
-      ((((int64_t)d.OH * 4099 + d.OW) * 65537 + d.K) * 131071 + d.N) * 1031 + Kgp * 17 + groups;
-  float* buf =
-      (float*)grow(st->dyt, sizeof(float) * (size_t)d.N * d.OH * d.OW * Kgp * groups, s);
-  if (st->dyt_src == dy && st->dyt_call == h->call && st->dyt_key == key) return buf;
-  to_pm(dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, s);
-  st->dyt_src = dy;
-  st->dyt_call = h->call;
-  st->dyt_key = key;
-  return buf;
-}
-
 static void to_grid_pm(const float* x, float* xg, int H, int W, int C, int N, int Cg, int Cgp,
                        int groups, int Hg, int Wg, int oh, int ow, cudaStream_t s) {
   dim3 grid((Hg * Wg + 63) / 64, (Cgp * groups + 31) / 32, N);
   count_launch();
   to_grid_pm_k<<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow, nullptr);
 }
-
-static bool wgrid_enabled();
 
 static bool halo_enabled() {
   // Off by default: measured slower than the im2col kernels on AlexNet
@@ -1814,34 +1546,6 @@ static float* x_grid(ck_handle* h, const float* x, const ConvDims& d, int Cgp, i
   return buf;
 }
 
-static void transpose(const float* in, float* out, int R, int Cc, int64_t ldi, int64_t ldo,
-                      cudaStream_t s) {
-  dim3 grid((Cc + 31) / 32, (R + 31) / 32);
-  count_launch();
-  transpose_k<<<grid, 256, 0, s>>>(in, out, R, Cc, ldi, ldo);
-}
-
-static void pad_planes(const float* in, float* out, int H, int W, int Hp, int Wp, int oh, int ow,
-                       int C, int N, int PL, int copies, cudaStream_t s) {
-  count_launch();
-  const size_t smem = sizeof(float) * (size_t)H * W;
-  const size_t tbl = sizeof(float) * (size_t)(PL + 4);
-  if (tbl + smem <= 40 * 1024) {
-    const int64_t NC = (int64_t)N * C;
-    const int P = (int)std::min<int64_t>({64, NC, (int64_t)((40 * 1024 - tbl) / smem)});
-    pad_planes_multi_k<<<(unsigned)((NC + P - 1) / P), 256, tbl + P * smem, s>>>(
-        in, out, H, W, Hp, Wp, oh, ow, NC, PL, copies, P);
-    return;
-  }
-  if (smem <= 48 * 1024) {
-    pad_planes_smem_k<<<(unsigned)((int64_t)N * C), 256, smem, s>>>(in, out, H, W, Hp, Wp, oh, ow,
-                                                                  C, N, PL, copies);
-    return;
-  }
-  pad_planes_k<<<dim3((PL + 255) / 256, C, copies * N), 256, 0, s>>>(in, out, H, W, Hp, Wp, oh,
-                                                                      ow, C, N, PL);
-}
-
 static CUtensorMap encode_tiled(const float* base, int rank, const cuuint64_t* dims,
                                 const cuuint64_t* strides_bytes, const cuuint32_t* box,
                                 CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
@@ -1873,24 +1577,6 @@ static CUtensorMap map_mn(const float* base, uint64_t K, uint64_t MN, uint64_t l
   cuuint64_t strides[1] = {ld * 4};
   cuuint32_t box[2] = {32, 32};
   return encode_tiled(base, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-}
-
-// wgrad A: planes [n][rows][PL], box (32 px, box_rows, 1)
-static CUtensorMap map_planes(const float* base, int PL, int rows, int N, int box_rows) {
-  cuuint64_t dims[3] = {(cuuint64_t)PL, (cuuint64_t)rows, (cuuint64_t)N};
-  cuuint64_t strides[2] = {(cuuint64_t)PL * 4, (cuuint64_t)PL * rows * 4};
-  cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
-  return encode_tiled(base, 3, dims, strides, box);
-}
-
-// wgrad B: shifted copies [copy][n][c][PL], box (32 px, 32 ch, 1, 1)
-static CUtensorMap map_plane_copies(const float* base, int PL, int C, int N, int copies,
-                                    int rows) {
-  cuuint64_t dims[4] = {(cuuint64_t)PL, (cuuint64_t)C, (cuuint64_t)N, (cuuint64_t)copies};
-  cuuint64_t strides[3] = {(cuuint64_t)PL * 4, (cuuint64_t)PL * C * 4,
-                           (cuuint64_t)PL * C * N * 4};
-  cuuint32_t box[4] = {32, (cuuint32_t)rows, 1, 1};
-  return encode_tiled(base, 4, dims, strides, box);
 }
 
 // ---- space-to-depth path for strided convolutions --------------------------
@@ -2021,11 +1707,6 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
 
 static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, cudaStream_t s);
 
-static bool wgrid_enabled() {
-  static const int on = getenv("CK_TC_WGRID") ? atoi(getenv("CK_TC_WGRID")) : 1;
-  return on != 0;
-}
-
 // Weight gradient on a padded grid (stride-1 conv; x at its padding offset in
 // an Hg x Wg grid, dy at (0, 0) of the same grid with zeros elsewhere):
 //   part[s][g][(tap, c)][k] = sum_{grid rows q of split s} dYg[q, k] Xg[q + fi + Hg*fj, c]
@@ -2067,44 +1748,17 @@ static int grid_wgrad(ck_handle* h, const float* xg, int Cp, int Cgp, const floa
   return splits;
 }
 
-// Strided wgrad through space-to-depth: the stride-1 im2col wgrad (see
-// conv_tc_wgrad) over the s2d pixel-major input, then the s2d filter scatter.
+// Strided wgrad through space-to-depth: the grid wgrad over the s2d input (a
+// pad-free grid of pitch U, dy at (0, 0) of it), then the s2d filter scatter.
 static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, const ConvDims& d,
                       const S2D& z, int acc, cudaStream_t s) {
-  TcState* st = state(h);
-  const int taps = z.Th * z.Tw;
   const int Kp = rup(d.K, 32);
   float* xt = x_s2d(h, x, d, z, s);
-  if (wgrid_enabled()) {
-    // the s2d tensor is a pad-free grid of pitch U; dy goes to (0, 0) of it
-    float* dyg = dy_grid(h, dy, d, d.K, Kp, 1, z.U, z.V, s);
-    float* part;
-    int64_t per;
-    const int splits = grid_wgrad(h, xt, z.Csp, z.Csp, dyg, Kp, Kp, d.K, 1, d.N, z.U, z.V, z.Th,
-                                  z.Tw, &part, &per, s);
-    count_launch();
-    s2d_wgrad_finish_k<<<blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s>>>(
-        part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc);
-    return;
-  }
-  float* dyt = dy_pm(h, dy, d, d.K, Kp, 1, s);
-  const int Ntot = taps * z.Csp;
-  const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
-  const int BM = pick_bm(d.K, BN);
-  const int64_t pix = (int64_t)d.N * d.OH * d.OW;
-  const int kblocks = (int)((pix + 31) / 32);
-  const int splits = wgrad_splits_for(((d.K + BM - 1) / BM) * ((Ntot + BN - 1) / BN), kblocks);
-  const int64_t per = (int64_t)Ntot * d.K;
-  float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
-  GemmParams p{};
-  p.M = d.K; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.BM = BM; p.splits = splits;
-  p.OH = d.OH; p.OW = d.OW; p.sh = 1; p.sw = 1; p.pt = 0; p.pl = 0; p.fh = z.Th; p.taps = taps;
-  p.cchunks = z.Csp / 32;
-  p.epi = EPI_LINEAR; p.out = part; p.ld = d.K; p.n_valid = Ntot; p.split_stride = per;
-  CUtensorMap ta = map_mn(dyt, (uint64_t)pix, Kp, Kp, BM, &p.a_mn3d);
-  CUtensorMap tb = map_im2col(xt, z.Csp, z.U, z.V, d.N, 0, 0, -(z.Th - 1), -(z.Tw - 1), 1, 1, 32,
-                              CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  launch<OP_TILED_MN, OP_IM2COL_MN>(ta, tb, p, 0, 0, splits, s);
+  float* dyg = dy_grid(h, dy, d, d.K, Kp, 1, z.U, z.V, s);
+  float* part;
+  int64_t per;
+  const int splits = grid_wgrad(h, xt, z.Csp, z.Csp, dyg, Kp, Kp, d.K, 1, d.N, z.U, z.V, z.Th,
+                                z.Tw, &part, &per, s);
   count_launch();
   s2d_wgrad_finish_k<<<blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s>>>(
       part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc);
@@ -2177,7 +1831,7 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
   }
   // stride 1: im2col over the padded grid (shared with the wgrad); else over
   // the compact pixel-major tensor with the padding in the im2col corners
-  const bool on_grid = d.sh == 1 && d.sw == 1 && wgrid_enabled();
+  const bool on_grid = d.sh == 1 && d.sw == 1;
   float* xt;
   if (on_grid) {
     xt = x_grid(h, x, d, Cgp, Hg, Wg, s);
@@ -2275,12 +1929,11 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     HaloConv hc{dyg, Kp, Hq, Wq, d.N, gt, Kgp, taps, d.fh, d.fw, d.Cg, d.groups, d.H, d.W};
     if (halo_launch(hc, p, s)) return true;
   }
-  // dy: on the wgrad's zero grid (Hg x Wg, dy at (0, 0); shared within the
-  // call) when that path is on, else compact pixel-major.
+  // dy on the wgrad's zero grid (Hg x Wg, dy at (0, 0); shared within the
+  // call): the negative im2col corners supply the top/left padding, the grid's
+  // zero rows the bottom/right
   const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
-  const bool on_grid = wgrid_enabled();
-  float* dyt = on_grid ? dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s)
-                       : dy_pm(h, dy, d, Kg, Kgp, d.groups, s);
+  float* dyt = dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s);
   GemmParams p{};
   p.M = d.N * d.H * d.W;
   p.N = d.Cg;
@@ -2295,11 +1948,8 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   p.img_stride = (int64_t)d.C * d.H * d.W; p.grp_col = d.Cg; p.epi_OHW = d.H * d.W;
   p.bias = nullptr; p.relu = 0; p.acc = acc; p.n_valid = d.Cg;
   p.BM = pick_bm(p.M, p.BN, true);
-  CUtensorMap ta = on_grid
-                       ? map_im2col(dyt, Kp, Hg, Wg, d.N, -qt, -ql, d.H - Hg - qt, d.W - Wg - ql,
-                                    1, 1, p.BM)
-                       : map_im2col(dyt, Kp, d.OH, d.OW, d.N, -qt, -ql, qb - (d.fh - 1),
-                                    qr - (d.fw - 1), 1, 1, p.BM);
+  CUtensorMap ta = map_im2col(dyt, Kp, Hg, Wg, d.N, -qt, -ql, d.H - Hg - qt, d.W - Wg - ql, 1, 1,
+                              p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kgp, d.C, (uint64_t)taps * Kgp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.Cg + p.BN - 1) / p.BN,
                                   d.groups, s);
@@ -2311,7 +1961,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
 // use the grid (FC layers, strided convs without space-to-depth).
 bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, int acc,
                   cudaStream_t s) {
-  if (!load_driver() || !wgrid_enabled() || is_fc(d)) return false;
+  if (!load_driver() || is_fc(d)) return false;
   const int Kg = d.Kg();
   if (d.sh == 1 && d.sw == 1) {
     if (d.Cg < 16 || Kg < 16) return false;
@@ -2362,47 +2012,13 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   const int Cgp = rup(d.Cg, 32), Cp = Cgp * d.groups;
   const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
   const int taps = d.fh * d.fw;
-  TcState* st = state(h);
-  if (wgrid_enabled()) {
-    const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
-    float* xg = x_grid(h, x, d, Cgp, Hg, Wg, s);
-    float* dyg = dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s);
-    float* part;
-    int64_t per;
-    const int splits = grid_wgrad(h, xg, Cp, Cgp, dyg, Kp, Kgp, Kg, d.groups, d.N, Hg, Wg, d.fh,
-                                  d.fw, &part, &per, s);
-    const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
-    count_launch();
-    wgrad_finish_k<<<std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
-        part, df, d.fh, d.fw, d.Cg, Cgp, Kg, d.groups, splits, per, d.fsc, d.fsk, acc);
-    return true;
-  }
-  float* xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
-  to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
-  float* dyt = dy_pm(h, dy, d, Kg, Kgp, d.groups, s);
-  const int Ntot = taps * Cgp;  // GEMM N = (tap, c) per group
-  const int BN = Ntot >= 256 ? 256 : rup(Ntot, 32);
-  const int BM = pick_bm(Kg, BN);
-  const int64_t pix = (int64_t)d.N * d.OH * d.OW;
-  const int kblocks = (int)((pix + 31) / 32);
-  const int splits = wgrad_splits_for(
-      ((Kg + BM - 1) / BM) * ((Ntot + BN - 1) / BN) * d.groups, kblocks);
-  const int64_t per_grp = (int64_t)Ntot * Kg;
-  const int64_t per = per_grp * d.groups;
-  float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
-  GemmParams p{};
-  p.M = Kg; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.BM = BM; p.splits = splits;
-  p.OH = d.OH; p.OW = d.OW; p.sh = 1; p.sw = 1; p.pt = d.pt; p.pl = d.pl; p.fh = d.fh;
-  p.taps = taps; p.cchunks = Cgp / 32;
-  p.a_grp_mn = Kgp;
-  p.b_grp_c = Cgp;
-  // raw partials: part[s*per + g*per_grp + n*Kg + k]
-  p.epi = EPI_LINEAR; p.out = part; p.ld = Kg; p.grp_out = per_grp; p.n_valid = Ntot;
-  p.split_stride = per;
-  CUtensorMap ta = map_mn(dyt, (uint64_t)pix, Kp, Kp, BM, &p.a_mn3d);
-  CUtensorMap tb = map_im2col(xt, Cp, d.H, d.W, d.N, -d.pt, -d.pl, d.pb - (d.fh - 1),
-                              d.pr - (d.fw - 1), 1, 1, 32, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-  launch<OP_TILED_MN, OP_IM2COL_MN>(ta, tb, p, 0, 0, d.groups * splits, s);
+  const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
+  float* xg = x_grid(h, x, d, Cgp, Hg, Wg, s);
+  float* dyg = dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s);
+  float* part;
+  int64_t per;
+  const int splits = grid_wgrad(h, xg, Cp, Cgp, dyg, Kp, Kgp, Kg, d.groups, d.N, Hg, Wg, d.fh,
+                                d.fw, &part, &per, s);
   const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
   count_launch();
   wgrad_finish_k<<<std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
