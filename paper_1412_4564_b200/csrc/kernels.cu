@@ -586,7 +586,7 @@ template <int NW>
 __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y, int HW, int C,
                               int64_t pixels, float kappa, float alpha, float nbeta) {
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
-  constexpr int P = 4;  // prefetch distance (channels)
+  constexpr int P = 8;  // prefetch distance (channels)
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pixels;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = e / HW;
@@ -633,7 +633,7 @@ template <int NW, bool kAcc>
 __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
                               int HW, int C, int64_t pixels, float kappa, float alpha, float beta) {
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
-  constexpr int P = 4;  // prefetch distance (channels): 2P loads in flight per thread
+  constexpr int P = 8;  // prefetch distance (channels): 2P loads in flight per thread
   const float nb = -beta;
   const float c2ab = __fmul_rn(__fmul_rn(2.f, alpha), beta);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pixels;
