@@ -98,6 +98,7 @@ struct GemmParams {
   int b_rows;             // OP_SHIFT_MN: channels per TMA box (divides Cgp and BN)
   int a_mn3d, b_mn3d;     // OP_TILED_MN: one 3D box per stage (MN % 32 == 0) vs R/32 2D boxes
   int taps;               // OP_SHIFT_MN / halo kernel: fh * fw
+  int kstage;             // K per pipeline stage: 32, or 64 (both operands MN-major)
   // halo kernel (stride-1 conv on a padded pixel-major grid, see halo_conv_kernel)
   int hg, hw_grid;        // grid pitch (rows per column) and rows per image; 0 = not a grid
   int ohv, owv;           // valid output extent on the grid
@@ -189,9 +190,11 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 //     tf32): k-rows of 128 B = 32 m/n, 32-B chunks swizzled by k & 3; 4-k
 //     groups 512 B apart (SBO), 32-wide MN blocks 4096 B apart (LBO); K step
 //     of 8 = +1024 B.  (tools/mn_probe.cu checks both against a CPU GEMM.)
+// ks = K rows per stage (32, or 64 when both operands are MN-major: each
+// 32-wide MN block then holds ks k-rows, LBO = ks * 128).
 template <bool MN>
-__device__ __forceinline__ uint64_t op_desc(uint32_t base, int h, int k) {
-  return MN ? sdesc(base + h * 16384 + k * 1024, 4096, 512, 1)
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int h, int k, int ks = 32) {
+  return MN ? sdesc(base + h * ks * 512 + k * 1024, ks * 128, 512, 1)
             : sdesc(base + h * 16384 + k * 32, 16, 1024, 2);
 }
 
@@ -292,7 +295,7 @@ __device__ __forceinline__ Tile tile_at(const GemmParams& p, int t) {
   r.n0 = nt * p.BN;
   r.grp = z / p.splits;
   r.split = z % p.splits;
-  const int nkb = p.K / 32;
+  const int nkb = p.K / p.kstage;
   const int per = (nkb + p.splits - 1) / p.splits;
   r.kb0 = r.split * per;
   r.kb1 = min(nkb, r.kb0 + per);
@@ -410,8 +413,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = p.stages;
   const int halves = p.BM / 128;
-  const int stage_a = p.BM * 128;
-  const int stage_b = p.BN * 128;
+  const int KS = p.kstage;
+  const int stage_a = p.BM * KS * 4;
+  const int stage_b = p.BN * KS * 4;
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * stage_a;
   uint64_t* full = (uint64_t*)(sB + S * stage_b);
@@ -476,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(&full[s], bytes);
           uint8_t* a = sA + s * stage_a;
           uint8_t* b = sB + s * stage_b;
-          const int k0 = kb * 32;
+          const int k0 = kb * KS;
           // ---- A (BM rows) ----
           if (AK == OP_TILED_K) {
             tma_2d(a, &tma_a, &full[s], k0 + T.grp * p.a_grp_k, T.m0 + T.grp * p.a_grp_mn);
@@ -486,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_3d(a, &tma_a, &full[s], 0, k0, mn0 / 32);
             else
               for (int j = 0; j < p.BM / 32; ++j)
-                tma_2d(a + j * 4096, &tma_a, &full[s], mn0 + 32 * j, k0);
+                tma_2d(a + j * KS * 128, &tma_a, &full[s], mn0 + 32 * j, k0);
           } else {  // OP_IM2COL_K: kb = tap * cchunks + cc; one box walks BM pixels
             const int tap = kb / p.cchunks, cc = kb - tap * p.cchunks;
             const int fj = tap / p.fh, fi = tap - fj * p.fh;
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_3d(b, &tma_b, &full[s], 0, k0, mn0 / 32);
             else
               for (int j = 0; j < p.BN / 32; ++j)
-                tma_2d(b + j * 4096, &tma_b, &full[s], mn0 + 32 * j, k0);
+                tma_2d(b + j * KS * 128, &tma_b, &full[s], mn0 + 32 * j, k0);
           } else if (BK == OP_SHIFT_MN) {
             // K block = 32 rows of the padded grid (pitch Hp); MN = (tap, c):
             // one 3D box per tap, b_rows channels, rows shifted by the tap.
@@ -512,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int c = nn - tap * p.cchunks * 32;
               tap = min(tap, p.taps - 1);  // columns past the last tap are masked
               const int fj = tap / p.fh, fi = tap - fj * p.fh;
-              tma_3d(b + j * p.b_rows * 128, &tma_b, &full[s], 0, k0 + fi + p.Hp * fj,
+              tma_3d(b + j * p.b_rows * KS * 4, &tma_b, &full[s], 0, k0 + fi + p.Hp * fj,
                      (T.grp * p.b_grp_c + c) / 32);
             }
           }
@@ -527,31 +531,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                      b_mn = BK == OP_TILED_MN || BK == OP_SHIFT_MN;
       const uint32_t idesc = idesc_tf32(p.BN, a_mn, b_mn);
       int it = 0, tc = 0;
+      unsigned long long w_t = 0, w_f = 0, t_start = clock64();
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
         const Tile T = tile_at(p, t);
         const int ab = tc % p.nacc;
         const uint32_t aph = (tc / p.nacc) & 1;
+        unsigned long long c0 = clock64();
         mbar_wait(&tempty[ab], aph ^ 1);  // epilogue drained this accumulator
+        w_t += clock64() - c0;
         tc_fence_after();
         const uint32_t dcol = tmem + (uint32_t)(ab * acc_cols);
         for (int kb = T.kb0; kb < T.kb1; ++kb, ++it) {
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
+          unsigned long long c1 = clock64();
           mbar_wait(&full[s], ph);
+          w_f += clock64() - c1;
           tc_fence_after();
           const uint32_t a = smem_u32(sA + s * stage_a);
           const uint32_t b = smem_u32(sB + s * stage_b);
           const bool first = kb == T.kb0;
           for (int h = 0; h < halves; ++h) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              mma_tf32(dcol + h * p.BN, op_desc<a_mn>(a, h, k), op_desc<b_mn>(b, 0, k), idesc,
-                       (!first || k > 0) ? 1u : 0u);
+            for (int k = 0; k < KS / 8; ++k) {
+              mma_tf32(dcol + h * p.BN, op_desc<a_mn>(a, h, k, KS), op_desc<b_mn>(b, 0, k, KS),
+                       idesc, (!first || k > 0) ? 1u : 0u);
             }
           }
           mma_commit(&empty[s]);
         }
         mma_commit(&tfull[ab]);
+      }
+      if (p.prof) {
+        unsigned long long* o = p.prof + blockIdx.x * 4;
+        o[0] = clock64() - t_start;
+        o[1] = w_t;
+        o[2] = w_f;
+        o[3] = it;
       }
     }
     __syncwarp();
@@ -1232,7 +1247,8 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
   p.groups = grid_z / p.splits;
   const int halves = p.BM / 128;
   p.nacc = (2 * halves * p.BN <= 512) ? 2 : 1;
-  const int stage_bytes = p.BM * 128 + p.BN * 128;
+  if (p.kstage != 64) p.kstage = 32;
+  const int stage_bytes = (p.BM + p.BN) * p.kstage * 4;
   const int budget = 227 * 1024 - 1024 - 256;
   p.stages = std::min(8, budget / stage_bytes);
   const size_t smem = 1024 + (size_t)p.stages * stage_bytes + 256;
@@ -1245,6 +1261,11 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
   const int tiles = ((p.M + p.BM - 1) / p.BM) * ((p.N + p.BN - 1) / p.BN) * grid_z;
   const int grid = std::min(tiles, 148);
   count_launch();
+  static const int mprof = getenv("CK_TC_PROF") ? atoi(getenv("CK_TC_PROF")) : 0;
+  static unsigned long long* mbuf = nullptr;
+  if (mprof && !mbuf) cudaMalloc(&mbuf, 148 * 4 * sizeof(unsigned long long));
+  p.prof = mprof ? mbuf : nullptr;
+  if (mprof) cudaMemsetAsync(mbuf, 0, 148 * 4 * sizeof(unsigned long long), s);
   KernelProfiler* pr = (g_prof && g_prof->on && !g_prof->label.empty()) ? g_prof : nullptr;
   KernelProfiler::Rec rec;
   if (pr) {
@@ -1256,6 +1277,22 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
     cudaEventRecord(rec.a, s);
   }
   tc_gemm_kernel<AK, BK><<<grid, kThreads, smem, s>>>(a, b, p);
+  if (mprof) {  // debug: where the MMA thread of each CTA spent its time
+    unsigned long long hbuf[148 * 4];
+    cudaStreamSynchronize(s);
+    cudaMemcpy(hbuf, mbuf, sizeof(hbuf), cudaMemcpyDeviceToHost);
+    double tot = 0, wt = 0, wf = 0, kb = 0;
+    int n = 0;
+    for (int i = 0; i < 148; ++i)
+      if (hbuf[i * 4]) {
+        tot += hbuf[i * 4]; wt += hbuf[i * 4 + 1]; wf += hbuf[i * 4 + 2]; kb += hbuf[i * 4 + 3];
+        ++n;
+      }
+    if (n)
+      fprintf(stderr, "[gemm<%d,%d>] M=%d N=%d K=%d BM=%d BN=%d S=%d nacc=%d ctas=%d: mma-thread %.0f cyc, "
+              "%.0f cyc/kblock, wait tempty %.1f%% full %.1f%%\n", AK, BK, p.M, p.N, p.K, p.BM, p.BN,
+              p.stages, p.nacc, n, tot / n, tot / (kb / n), 100 * wt / tot, 100 * wf / tot);
+  }
   if (pr) {
     cudaEventRecord(rec.b, s);
     pr->recs.push_back(rec);
@@ -1564,18 +1601,18 @@ static CUtensorMap encode_tiled(const float* base, int rank, const cuuint64_t* d
 // R-row tile (R/32 blocks of 32 k-rows x 128 B) in one box; otherwise R/32
 // 2D boxes of 32 x 32.  Swizzle 128B_ATOM_32B = the UMMA SW128_32B layout.
 static CUtensorMap map_mn(const float* base, uint64_t K, uint64_t MN, uint64_t ld, int R,
-                          int* is3d) {
+                          int* is3d, int ks = 32) {
   if (MN % 32 == 0) {
     *is3d = 1;
     cuuint64_t dims[3] = {32, K, MN / 32};
     cuuint64_t strides[2] = {ld * 4, 128};
-    cuuint32_t box[3] = {32, 32, (cuuint32_t)(R / 32)};
+    cuuint32_t box[3] = {32, (cuuint32_t)ks, (cuuint32_t)(R / 32)};
     return encode_tiled(base, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   }
   *is3d = 0;
   cuuint64_t dims[2] = {MN, K};
   cuuint64_t strides[1] = {ld * 4};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {32, (cuuint32_t)ks};
   return encode_tiled(base, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
 }
 
@@ -1723,24 +1760,28 @@ static int grid_wgrad(ck_handle* h, const float* xg, int Cp, int Cgp, const floa
   const int b_rows = std::min(256, std::gcd(Cgp, BN));
   const int BM = pick_bm(Kg, BN);
   const int64_t rows = (int64_t)N * Hg * Wg;
-  const int kblocks = (int)((rows + 31) / 32);
+  // 64 grid rows per stage: half the TMA boxes per FLOP (both operands MN-major)
+  static const int ks_env = getenv("CK_TC_WKS") ? atoi(getenv("CK_TC_WKS")) : 64;
+  const int KS = ks_env == 32 ? 32 : 64;
+  const int kblocks = (int)((rows + KS - 1) / KS);
   const int splits = wgrad_splits_for(((Kg + BM - 1) / BM) * ((Ntot + BN - 1) / BN) * groups,
                                       kblocks);
   const int64_t per_grp = (int64_t)Ntot * Kg;
   const int64_t per = per_grp * groups;
   float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
   GemmParams p{};
-  p.M = Kg; p.N = Ntot; p.K = kblocks * 32; p.BN = BN; p.BM = BM; p.splits = splits;
+  p.M = Kg; p.N = Ntot; p.K = kblocks * KS; p.BN = BN; p.BM = BM; p.splits = splits;
+  p.kstage = KS;
   p.Hp = Hg; p.fh = fh; p.taps = taps; p.cchunks = Cgp / 32; p.b_rows = b_rows;
   p.a_grp_mn = Kgp;
   p.b_grp_c = Cgp;
   // raw partials: part[s*per + g*per_grp + n*Kg + k]
   p.epi = EPI_LINEAR; p.out = part; p.ld = Kg; p.grp_out = per_grp; p.n_valid = Ntot;
   p.split_stride = per;
-  CUtensorMap ta = map_mn(dyg, (uint64_t)rows, Kp, Kp, BM, &p.a_mn3d);
+  CUtensorMap ta = map_mn(dyg, (uint64_t)rows, Kp, Kp, BM, &p.a_mn3d, KS);
   cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(Cp / 32)};
   cuuint64_t strides[2] = {(cuuint64_t)Cp * 4, 128};
-  cuuint32_t box[3] = {32, 32, (cuuint32_t)(b_rows / 32)};
+  cuuint32_t box[3] = {32, (cuuint32_t)KS, (cuuint32_t)(b_rows / 32)};
   CUtensorMap tb = encode_tiled(xg, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   launch<OP_TILED_MN, OP_SHIFT_MN>(ta, tb, p, 0, 0, groups * splits, s);
   *part_out = part;

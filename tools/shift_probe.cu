@@ -129,7 +129,69 @@ __global__ void mma_rate(int r0, long long* out) {
   }
 }
 
+// Streaming variant: S stages of (A 16 KB = 128 rows x 32 k, B NT rows x 32 k),
+// each MMA reads a different stage / k-slice, as in the GEMM mainloop.
+template <int NT, int S>
+__global__ void mma_stream(long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid / 32;
+  const int stage = 16384 + NT * 128;
+  for (int e = tid; e < S * stage / 4; e += blockDim.x) ((float*)sm)[e] = 0.001f * (e & 7);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_base;
+  if (tid == 0) {
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    long long t0 = clock64();
+    for (int i = 0; i < 2048; ++i) {
+      const int st = (i / 4) % S, k = i & 3;
+      const uint32_t a = su32(sm + st * stage), b = a + 16384;
+      const uint64_t da = sdesc(a + k * 32, 16, 1024, 0);
+      const uint64_t db = sdesc(b + k * 32, 16, 1024, 0);
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                   "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                   ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(1u));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
+    asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}\n" ::"r"(su32(&bar)) : "memory");
+    long long t1 = clock64();
+    out[0] = (t1 - t0) / 2048;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) {
+    __syncwarp();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+  }
+}
+
+template <int NT, int S>
+static long long run_stream(long long* d) {
+  const int smem = S * (16384 + NT * 128) + 2048;
+  cudaFuncSetAttribute(mma_stream<NT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_stream<NT, S><<<1, 128, smem>>>(d);
+  cudaDeviceSynchronize();
+  long long c; cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+  return c;
+}
+
 int main() {
+  {
+    long long* d; cudaMalloc(&d, 8);
+    printf("streaming MMA (M=128, K=8 tf32) cycles/MMA: N=256 S1 %lld S4 %lld | N=192 S1 %lld S4 %lld | N=96 S1 %lld S6 %lld | N=48 S1 %lld S6 %lld\n",
+           run_stream<256, 1>(d), run_stream<256, 4>(d), run_stream<192, 1>(d), run_stream<192, 4>(d),
+           run_stream<96, 1>(d), run_stream<96, 6>(d), run_stream<48, 1>(d), run_stream<48, 6>(d));
+  }
   {
     long long* d; cudaMalloc(&d, 8);
     cudaFuncSetAttribute(mma_rate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
