@@ -552,9 +552,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t b = smem_u32(sB + s * stage_b);
           const bool first = kb == T.kb0;
           for (int h = 0; h < halves; ++h) {
-            for (int k = 0; k < KS / 8; ++k) {
-              mma_tf32(dcol + h * p.BN, op_desc<a_mn>(a, h, k, KS), op_desc<b_mn>(b, 0, k, KS),
-                       idesc, (!first || k > 0) ? 1u : 0u);
+            if (KS == 32) {  // fully unrolled issue: the MMA thread is on the critical path
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_tf32(dcol + h * p.BN, op_desc<a_mn>(a, h, k, 32), op_desc<b_mn>(b, 0, k, 32),
+                         idesc, (!first || k > 0) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                mma_tf32(dcol + h * p.BN, op_desc<a_mn>(a, h, k, 64), op_desc<b_mn>(b, 0, k, 64),
+                         idesc, (!first || k > 0) ? 1u : 0u);
             }
           }
           mma_commit(&empty[s]);
