@@ -246,6 +246,30 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
+// Warp-converged variants: all 32 lanes execute the issue loop and one
+// elected lane issues (no per-instruction divergence handling in SASS).
+__device__ __forceinline__ void mma_tf32_elect(uint32_t tmem_d, uint64_t a, uint64_t b,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -526,7 +550,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer --
-    if (lane == 0) {
+    // the whole warp walks the loop; one elected lane issues each MMA/commit
+    {
       constexpr bool a_mn = AK == OP_TILED_MN,
                      b_mn = BK == OP_TILED_MN || BK == OP_SHIFT_MN;
       const uint32_t idesc = idesc_tf32(p.BN, a_mn, b_mn);
@@ -555,20 +580,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (KS == 32) {  // fully unrolled issue: the MMA thread is on the critical path
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                mma_tf32(dcol + h * p.BN, op_desc<a_mn>(a, h, k, 32), op_desc<b_mn>(b, 0, k, 32),
-                         idesc, (!first || k > 0) ? 1u : 0u);
+                mma_tf32_elect(dcol + h * p.BN, op_desc<a_mn>(a, h, k, 32),
+                               op_desc<b_mn>(b, 0, k, 32), idesc, (!first || k > 0) ? 1u : 0u);
             } else {
 #pragma unroll
               for (int k = 0; k < 8; ++k)
-                mma_tf32(dcol + h * p.BN, op_desc<a_mn>(a, h, k, 64), op_desc<b_mn>(b, 0, k, 64),
-                         idesc, (!first || k > 0) ? 1u : 0u);
+                mma_tf32_elect(dcol + h * p.BN, op_desc<a_mn>(a, h, k, 64),
+                               op_desc<b_mn>(b, 0, k, 64), idesc, (!first || k > 0) ? 1u : 0u);
             }
           }
-          mma_commit(&empty[s]);
+          mma_commit_elect(&empty[s]);
         }
-        mma_commit(&tfull[ab]);
+        mma_commit_elect(&tfull[ab]);
       }
-      if (p.prof) {
+      if (p.prof && lane == 0) {
         unsigned long long* o = p.prof + blockIdx.x * 4;
         o[0] = clock64() - t_start;
         o[1] = w_t;
