@@ -143,6 +143,57 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, uint64
       : "memory");
 }
 
+// ---- predicated forms for a warp-converged producer: every lane runs the
+// loop, the lane with pred != 0 (elect_one) issues -- no divergent branch
+// around the async-proxy instructions.
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\nselp.u32 %0, 1, 0, e;\n}\n"
+      : "=r"(p));
+  return p;
+}
+
+__device__ __forceinline__ void mbar_expect_tx_p(uint64_t* bar, uint32_t bytes, uint32_t pred) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n"
+      "@q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(bytes), "r"(pred)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_2d_p(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                         int c1, uint32_t pred) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %5, 0;\n"
+      "@q cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];\n}\n" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(pred)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_3d_p(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                         int c1, int c2, uint32_t pred) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %6, 0;\n"
+      "@q cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5}], [%2];\n}\n" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(pred)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_im2col_4d_p(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int c, int h, int w, int n, uint16_t oh,
+                                                uint16_t ow, uint32_t pred) {
+  asm volatile(
+      "{\n.reg .pred q;\nsetp.ne.u32 q, %9, 0;\n"
+      "@q cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};\n}\n" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(c), "r"(h), "r"(w), "r"(n), "h"(oh), "h"(ow),
+      "r"(pred)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                        int c1, int c2, int c3) {
   asm volatile(
@@ -481,7 +532,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ---------------------------------------------------------- producer --
-    if (lane == 0) {
+    // warp-converged: all lanes walk the loop, the elected lane issues
+    {
+      const uint32_t lead = elect_one();
       const uint32_t bytes = stage_a + stage_b;
       int it = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -501,36 +554,36 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], bytes);
+          mbar_expect_tx_p(&full[s], bytes, lead);
           uint8_t* a = sA + s * stage_a;
           uint8_t* b = sB + s * stage_b;
           const int k0 = kb * KS;
           // ---- A (BM rows) ----
           if (AK == OP_TILED_K) {
-            tma_2d(a, &tma_a, &full[s], k0 + T.grp * p.a_grp_k, T.m0 + T.grp * p.a_grp_mn);
+            tma_2d_p(a, &tma_a, &full[s], k0 + T.grp * p.a_grp_k, T.m0 + T.grp * p.a_grp_mn, lead);
           } else if (AK == OP_TILED_MN) {
             const int mn0 = T.m0 + T.grp * p.a_grp_mn;
             if (p.a_mn3d)
-              tma_3d(a, &tma_a, &full[s], 0, k0, mn0 / 32);
+              tma_3d_p(a, &tma_a, &full[s], 0, k0, mn0 / 32, lead);
             else
               for (int j = 0; j < p.BM / 32; ++j)
-                tma_2d(a + j * KS * 128, &tma_a, &full[s], mn0 + 32 * j, k0);
+                tma_2d_p(a + j * KS * 128, &tma_a, &full[s], mn0 + 32 * j, k0, lead);
           } else {  // OP_IM2COL_K: kb = tap * cchunks + cc; one box walks BM pixels
             const int tap = kb / p.cchunks, cc = kb - tap * p.cchunks;
             const int fj = tap / p.fh, fi = tap - fj * p.fh;
-            tma_im2col_4d(a, &tma_a, &full[s], T.grp * p.a_grp_c + cc * 32, a_h, a_w, a_n,
-                          (uint16_t)fi, (uint16_t)fj);
+            tma_im2col_4d_p(a, &tma_a, &full[s], T.grp * p.a_grp_c + cc * 32, a_h, a_w, a_n,
+                          (uint16_t)fi, (uint16_t)fj, lead);
           }
           // ---- B (BN rows) ----
           if (BK == OP_TILED_K) {
-            tma_2d(b, &tma_b, &full[s], k0 + T.grp * p.b_grp_k, T.n0 + T.grp * p.b_grp_mn);
+            tma_2d_p(b, &tma_b, &full[s], k0 + T.grp * p.b_grp_k, T.n0 + T.grp * p.b_grp_mn, lead);
           } else if (BK == OP_TILED_MN) {
             const int mn0 = T.n0 + T.grp * p.b_grp_mn;
             if (p.b_mn3d)
-              tma_3d(b, &tma_b, &full[s], 0, k0, mn0 / 32);
+              tma_3d_p(b, &tma_b, &full[s], 0, k0, mn0 / 32, lead);
             else
               for (int j = 0; j < p.BN / 32; ++j)
-                tma_2d(b + j * KS * 128, &tma_b, &full[s], mn0 + 32 * j, k0);
+                tma_2d_p(b + j * KS * 128, &tma_b, &full[s], mn0 + 32 * j, k0, lead);
           } else if (BK == OP_SHIFT_MN) {
             // K block = 32 rows of the padded grid (pitch Hp); MN = (tap, c):
             // one 3D box per tap, b_rows channels, rows shifted by the tap.
@@ -540,8 +593,8 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int c = nn - tap * p.cchunks * 32;
               tap = min(tap, p.taps - 1);  // columns past the last tap are masked
               const int fj = tap / p.fh, fi = tap - fj * p.fh;
-              tma_3d(b + j * p.b_rows * KS * 4, &tma_b, &full[s], 0, k0 + fi + p.Hp * fj,
-                     (T.grp * p.b_grp_c + c) / 32);
+              tma_3d_p(b + j * p.b_rows * KS * 4, &tma_b, &full[s], 0, k0 + fi + p.Hp * fj,
+                     (T.grp * p.b_grp_c + c) / 32, lead);
             }
           }
         }
@@ -556,22 +609,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                      b_mn = BK == OP_TILED_MN || BK == OP_SHIFT_MN;
       const uint32_t idesc = idesc_tf32(p.BN, a_mn, b_mn);
       int it = 0, tc = 0;
+#ifdef CK_TC_PROFILE  // build with -DCK_TC_PROFILE and run with CK_TC_PROF=1
       unsigned long long w_t = 0, w_f = 0, t_start = clock64();
+#define CK_PROF_T0(v) unsigned long long v = clock64()
+#define CK_PROF_ADD(acc, v) acc += clock64() - v
+#else
+#define CK_PROF_T0(v)
+#define CK_PROF_ADD(acc, v)
+#endif
       for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
         const Tile T = tile_at(p, t);
         const int ab = tc % p.nacc;
         const uint32_t aph = (tc / p.nacc) & 1;
-        unsigned long long c0 = clock64();
+        CK_PROF_T0(c0);
         mbar_wait(&tempty[ab], aph ^ 1);  // epilogue drained this accumulator
-        w_t += clock64() - c0;
+        CK_PROF_ADD(w_t, c0);
         tc_fence_after();
         const uint32_t dcol = tmem + (uint32_t)(ab * acc_cols);
         for (int kb = T.kb0; kb < T.kb1; ++kb, ++it) {
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
-          unsigned long long c1 = clock64();
+          CK_PROF_T0(c1);
           mbar_wait(&full[s], ph);
-          w_f += clock64() - c1;
+          CK_PROF_ADD(w_f, c1);
           tc_fence_after();
           const uint32_t a = smem_u32(sA + s * stage_a);
           const uint32_t b = smem_u32(sB + s * stage_b);
@@ -593,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit_elect(&tfull[ab]);
       }
+#ifdef CK_TC_PROFILE
       if (p.prof && lane == 0) {
         unsigned long long* o = p.prof + blockIdx.x * 4;
         o[0] = clock64() - t_start;
@@ -600,6 +661,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         o[2] = w_f;
         o[3] = it;
       }
+#endif
+#undef CK_PROF_T0
+#undef CK_PROF_ADD
     }
     __syncwarp();
   } else {
