@@ -41,6 +41,7 @@ def parse():
     p.add_argument("--math", default="tf32", choices=["tf32", "fp32"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-graph", action="store_true", help="launch every kernel (no CUDA graph)")
     p.add_argument("--profile-layers", action="store_true", help="print per-layer times to stderr")
     # internal: CPU sample run in a subprocess
     p.add_argument("--cpu-sample", type=int, default=0)
@@ -282,6 +283,9 @@ def main():
         return float(t.item())
 
     # ---- device-resident throughput -------------------------------------
+    # CUDA-graph replay of the step: warm-up step 1 runs eagerly (sizes every
+    # workspace), step 2 is captured, the rest (and the timed steps) replay it.
+    tr.set_graph(not args.no_graph)
     for _ in range(max(args.warmup, 3)):
         tr.step(want_loss=False, stream=sp)
     barrier()
@@ -414,7 +418,7 @@ def main():
                "data": "synthetic (xoshiro256**: U[-1,1) data, 0.01 N(0,1) weights, random labels)",
                "config": {"workload": WORKLOAD, "global_batch": world * args.batch,
                           "per_gpu_batch": args.batch, "parallelism": f"dp{world}",
-                          "math": args.math,
+                          "math": args.math, "cuda_graph": not args.no_graph,
                           "l2": "inputs larger than L2: the step streams ~4 GB of activations "
                                 "(input batch alone 158 MB > 126 MB L2)",
                           "vs_baseline_ref": "MatConvNet CuDNN v2 AlexNet b=256 on 1x Titan "

@@ -232,6 +232,10 @@ ck_status ck_trainer_init_dp(ck_trainer* t, const char id[128], int rank, int wo
 /* forward + backward + gradient allreduce (overlapped) + SGD on `stream`.
  * If loss_host != NULL the step's objective is copied back (synchronising). */
 ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream);
+/* Replay each step as one CUDA graph: captured on the first graph step after
+ * an eager one (same stream; profiling steps stay eager). Graph memory and
+ * tensor maps are fixed at capture: shapes and buffers must not change. */
+ck_status ck_trainer_set_graph(ck_trainer* t, int on);
 
 /* ---- synthetic data (host): the reference generator, xoshiro256** seeded
  * via splitmix64 (rng.hpp:9-36, rng.cpp:10-59) ---------------------------- */

@@ -56,6 +56,7 @@ SIGNATURES = {
     "ck_last_error": (C.c_char_p, [P]),
     "ck_version": (C.c_char_p, []),
     "ck_launch_count": (C.c_int64, [P]),
+    "ck_trainer_set_graph": (C.c_int, [P, C.c_int]),
     "ck_set_kernel_profiling": (C.c_int, [P, C.c_int]),
     "ck_kernel_profile_count": (C.c_int, [P]),
     "ck_kernel_profile_get": (C.c_int, [P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_float),

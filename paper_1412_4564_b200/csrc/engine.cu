@@ -540,6 +540,12 @@ struct ck_trainer : ck::LayerDone {
   cudaEvent_t comm_done = nullptr;
   std::vector<std::vector<int>> layer_params;  // params finished by layer li
   float* loss_dev = nullptr;
+  // CUDA-graph replay of the whole step (ck_trainer_set_graph)
+  bool use_graph = false;
+  int eager_steps = 0;                 // workspaces are sized by one eager step
+  cudaGraphExec_t exec = nullptr;
+  cudaStream_t graph_stream = nullptr;
+  int64_t graph_launches = 0;          // kernels in the captured step
 
   void done(int li, cudaStream_t s) override {
     const auto& ps = layer_params[li];
@@ -572,7 +578,13 @@ struct ck_trainer : ck::LayerDone {
                                wd, s);
     if (st != CK_OK) throw Err(st, g->h->err);
   }
+  void drop_graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    graph_stream = nullptr;
+  }
   ~ck_trainer() override {
+    drop_graph();
     for (float* m : mom) cudaFree(m);
     for (auto e : ev) cudaEventDestroy(e);
     if (comm_done) cudaEventDestroy(comm_done);
@@ -794,12 +806,10 @@ ck_status ck_trainer_init_dp(ck_trainer* t, const char id[128], int rank, int wo
   CKG_END(g)
 }
 
-ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
-  if (!t) return CK_ERR_ARG;
+// One training step's device work on stream s: forward, backward with the
+// per-layer gradient allreduce + SGD, objective to loss_dev.
+static void trainer_body(ck_trainer* t, cudaStream_t s) {
   ck_graph* g = t->g;
-  CKG_BEGIN(g)
-  cudaStream_t s = (cudaStream_t)stream;
-  int64_t before = g->h->counter.n;
   run_forward(g, s);
   run_backward(g, t->objective, s, t);
   if (t->comm) {
@@ -816,6 +826,52 @@ ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
     Var& obj = g->vars[t->objective];
     check_cuda(cudaMemcpyAsync(t->loss_dev, obj.value, sizeof(float), cudaMemcpyDeviceToDevice, s),
                "copy");
+  }
+}
+
+ck_status ck_trainer_set_graph(ck_trainer* t, int on) {
+  if (!t) return CK_ERR_ARG;
+  ck_graph* g = t->g;
+  CKG_BEGIN(g)
+  t->use_graph = on != 0;
+  t->drop_graph();
+  CKG_END(g)
+}
+
+ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
+  if (!t) return CK_ERR_ARG;
+  ck_graph* g = t->g;
+  CKG_BEGIN(g)
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t before = g->h->counter.n;
+  // (the legacy default stream cannot be captured: such steps stay eager)
+  if (t->use_graph && s != nullptr && !g->profiling && !g->h->prof.on && t->eager_steps > 0) {
+    // Replay: the step's ~100 launches become one graph launch.  Captured on
+    // the first graph step (after an eager step sized every workspace); the
+    // captured kernel count keeps ck_launch_count honest.
+    if (!t->exec || t->graph_stream != s) {
+      t->drop_graph();
+      cudaGraph_t graph;
+      check_cuda(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+      try {
+        trainer_body(t, s);
+      } catch (...) {
+        cudaStreamEndCapture(s, &graph);
+        throw;
+      }
+      check_cuda(cudaStreamEndCapture(s, &graph), "end capture");
+      const cudaError_t e = cudaGraphInstantiate(&t->exec, graph, 0);
+      cudaGraphDestroy(graph);
+      check_cuda(e, "graph instantiate");
+      t->graph_stream = s;
+      t->graph_launches = g->h->counter.n - before;
+    } else {
+      g->h->counter.n += t->graph_launches;
+    }
+    check_cuda(cudaGraphLaunch(t->exec, s), "graph launch");
+  } else {
+    trainer_body(t, s);
+    ++t->eager_steps;
   }
   if (loss_host) {
     check_cuda(cudaMemcpyAsync(loss_host, t->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, s),

@@ -202,6 +202,10 @@ class Trainer:
     def init_dp(self, uid: bytes, rank: int, world: int):
         self.graph._check(lib().ck_trainer_init_dp(self.t, uid, rank, world))
 
+    def set_graph(self, on: bool):
+        """Replay each step as one CUDA graph (ck_trainer_set_graph)."""
+        self.graph._check(lib().ck_trainer_set_graph(self.t, int(on)))
+
     def step(self, want_loss=True, stream=None):
         s = C.c_void_p(stream if stream is not None else torch.cuda.current_stream().cuda_stream)
         if want_loss:

@@ -150,3 +150,28 @@ def test_engine_pool_argmax_route_bitexact(pad):
     dp1 = g.get("p1", deriv=True)
     assert np.abs(dp1).max() > 0
     assert np.array_equal(g.get("x", deriv=True), O.pool_backward(x, xs, pg, dp1))
+
+
+def test_trainer_cuda_graph_replay_matches_eager():
+    """ck_trainer_set_graph: the captured step replays the same deterministic
+    kernels, so parameters after 4 steps are bit-identical to eager steps."""
+    from paper_1412_4564_b200 import nets
+    from paper_1412_4564_b200.graph import Trainer
+    net = nets.cifar(batch=8)
+    params, inputs = net.init_params(), net.init_inputs()
+    results = []
+    for graph_mode in (False, True):
+        g = device_graph(net, "tf32")
+        for k, v in {**params, **inputs}.items():
+            g.set(k, v)
+        t = Trainer(g, lr=0.01, momentum=0.9, weight_decay=5e-4)
+        t.set_graph(graph_mode)
+        before = g.hd.launches
+        stream = torch.cuda.Stream()  # graph capture needs a non-default stream
+        losses = [t.step(stream=stream.cuda_stream) for _ in range(4)]
+        assert g.hd.launches - before > 4 * 10  # replayed launches are still counted
+        results.append((losses, {p: g.get(p) for p, _, _ in net.params}))
+    (l0, p0), (l1, p1) = results
+    assert l0 == l1
+    for k in p0:
+        assert np.array_equal(p0[k], p1[k]), k
