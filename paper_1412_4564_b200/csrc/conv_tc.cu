@@ -925,24 +925,28 @@ __global__ void to_grid_pm_k(const float* __restrict__ x, float* __restrict__ xg
     src[k] = (P < HWg && i >= 0 && i < H && j >= 0 && j < W) ? (int64_t)j * H + i : -1;
   }
   const float* xn = x + (int64_t)n * C * H * W;
+  // all eight loads first (independent, in flight together), then the tile
+  float v[4][2];
 #pragma unroll
   for (int rr = 0; rr < 4; ++rr) {
-    const int r = warp + 8 * rr;
-    const int cp = c0 + r;
+    const int cp = c0 + warp + 8 * rr;
     const int g = cp / Cgp, cl = cp - g * Cgp;
     const bool ch_ok = cp < Cp && cl < Cg;
     const float* xc = xn + (int64_t)(g * Cg + cl) * H * W;
-    float v[2];
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      v[k] = (ch_ok && src[k] >= 0) ? __ldg(xc + src[k]) : 0.f;
-      tile[r][lane + 32 * k] = v[k];
-    }
-    if (bpart) {  // fused bias gradient: this tile's per-channel sum (double, fixed order)
-      double t = (double)v[0] + (double)v[1];
+    for (int k = 0; k < 2; ++k) v[rr][k] = (ch_ok && src[k] >= 0) ? __ldg(xc + src[k]) : 0.f;
+  }
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+    for (int k = 0; k < 2; ++k) tile[warp + 8 * rr][lane + 32 * k] = v[rr][k];
+  if (bpart) {  // fused bias gradient: this tile's per-channel sums (double, fixed order)
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) {
+      const int cp = c0 + warp + 8 * rr;
+      double t = (double)v[rr][0] + (double)v[rr][1];
       for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane == 0 && cp < Cp)
-        bpart[((int64_t)n * gridDim.x + blockIdx.x) * Cp + cp] = t;
+      if (lane == 0 && cp < Cp) bpart[((int64_t)n * gridDim.x + blockIdx.x) * Cp + cp] = t;
     }
   }
   __syncthreads();
@@ -1615,20 +1619,40 @@ static bool halo_launch(const HaloConv& hc, GemmParams p, cudaStream_t s) {
 // dy at (0, 0) of an Hg x Wg zero grid, pixel-major [n][Wg][Hg][groups*Kgp]:
 // the wgrad A operand and (through im2col with negative corners) the dgrad
 // input of one ck_conv_backward call -- transformed once per call.
-__global__ void grid_bias_finish_k(const double* __restrict__ bpart, float* db, int K, int Kg,
-                                   int Kgp, int Cp, int rows, int acc) {
-  const int k = blockIdx.x;
-  const int g = k / Kg, cp = g * Kgp + (k - g * Kg);
+// db from the per-(image, pixel tile) partials [rows][Cp], in two fixed-order
+// stages (deterministic): grid_bias_part_k -- block (32 channels, row chunk
+// of 8*RPW rows) -> part2[chunk][Cp]; grid_bias_finish_k sums the chunks.
+constexpr int kBiasRowsPerWarp = 8;
+__global__ void grid_bias_part_k(const double* __restrict__ bpart, double* __restrict__ part2,
+                                 int Cp, int rows) {
+  __shared__ double red[8][32];
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  const int cp = blockIdx.x * 32 + lane;
+  const int r0 = blockIdx.y * 8 * kBiasRowsPerWarp + warp * kBiasRowsPerWarp;
   double t = 0;
-  for (int r = threadIdx.x; r < rows; r += blockDim.x) t += bpart[(int64_t)r * Cp + cp];
-  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-  __shared__ double red[32];
-  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = t;
+  if (cp < Cp)
+#pragma unroll
+    for (int r = r0; r < r0 + kBiasRowsPerWarp; ++r)
+      if (r < rows) t += bpart[(int64_t)r * Cp + cp];
+  red[warp][lane] = t;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (warp == 0 && cp < Cp) {
     double u = 0;
-    for (int w = 0; w < (int)(blockDim.x / 32); ++w) u += red[w];
-    db[k] = acc ? db[k] + (float)u : (float)u;
+    for (int w = 0; w < 8; ++w) u += red[w][lane];
+    part2[(int64_t)blockIdx.y * Cp + cp] = u;
+  }
+}
+
+__global__ void grid_bias_finish_k(const double* __restrict__ part2, float* db, int K, int Kg,
+                                   int Kgp, int Cp, int chunks, int acc) {
+  const int cp = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cp >= Cp) return;
+  double u = 0;
+  for (int c = 0; c < chunks; ++c) u += part2[(int64_t)c * Cp + cp];
+  const int g = cp / Kgp, kl = cp - g * Kgp;
+  if (kl < Kg) {
+    const int k = g * Kg + kl;
+    if (k < K) db[k] = acc ? db[k] + (float)u : (float)u;
   }
 }
 
@@ -1644,12 +1668,17 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
   if (!db && st->dyg_src == dy && st->dyg_call == h->call && st->dyg_key == key) return buf;
   if (db) {
     const int Cp = Kgp * groups, nb = (Hg * Wg + 63) / 64;
-    double* bpart = (double*)grow(st->bpart, sizeof(double) * (size_t)d.N * nb * Cp, s);
+    const int rows = d.N * nb, chunks = (rows + 8 * kBiasRowsPerWarp - 1) / (8 * kBiasRowsPerWarp);
+    double* bpart =
+        (double*)grow(st->bpart, sizeof(double) * ((size_t)rows + chunks) * Cp, s);
+    double* part2 = bpart + (size_t)rows * Cp;
     dim3 grid(nb, (Cp + 31) / 32, d.N);
-    count_launch(2);
+    count_launch(3);
     to_grid_pm_k<<<grid, 256, 0, s>>>(dy, buf, d.OH, d.OW, d.K, Kg, Kgp, groups, Hg, Wg, 0, 0,
                                       bpart);
-    grid_bias_finish_k<<<d.K, 256, 0, s>>>(bpart, db, d.K, Kg, Kgp, Cp, d.N * nb, db_acc);
+    grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(bpart, part2, Cp, rows);
+    grid_bias_finish_k<<<(Cp + 127) / 128, 128, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
+                                                        db_acc);
   } else {
     to_grid_pm(dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, Hg, Wg, 0, 0, s);
   }
