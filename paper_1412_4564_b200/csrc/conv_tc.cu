@@ -53,6 +53,8 @@ namespace tc {
 enum OpKind : int {
   OP_TILED_K = 0,     // 2D tensor (K inner, MN outer), box (32, rows)
   OP_IM2COL_K = 2,    // 4D im2col over a pixel-major tensor, box BM px x 32 ch
+  OP_SHIFT_K = 4,     // fprop/dgrad A: 3D box {32 ch, BM grid rows + tap shift, KS/32 chunks}
+  OP_TILED_K3 = 5,    // B for OP_SHIFT_K: 3D box {32 k, BN rows, KS/32 chunks} of [row][K]
   OP_TILED_MN = 6,    // MN-major 2D tensor [K][MN] (MN inner): 32x32 boxes, SW128_32B atoms
   OP_SHIFT_MN = 8,    // wgrad B: 3D boxes {32 ch, 32 grid rows + tap shift, b_rows/32 blocks}
 };
@@ -88,7 +90,8 @@ struct GemmParams {
   const float* bias;      // per col (EPI_PIX) or per row (EPI_LINEAR)
   int relu, acc;
   int n_valid;            // columns < n_valid are stored
-  int Hp;                 // OP_SHIFT_MN: grid pitch (tap shift = fi + Hp*fj)
+  int Hp;                 // OP_SHIFT_MN / OP_SHIFT_K: grid pitch (tap shift = fi + Hp*fj)
+  int base_shift;         // OP_SHIFT_K: row offset added to every tap shift (dgrad: -(qt+Hp*ql))
   int b_grp_row;          // halo kernel: per-group filter row offset
   int s2d, s2d_U, s2d_H, s2d_W, s2d_C;  // EPI_S2D: factor, grid height, target dims
   int exp;                // debug experiments (CK_TC_EXP)
@@ -98,7 +101,7 @@ struct GemmParams {
   int b_rows;             // OP_SHIFT_MN: channels per TMA box (divides Cgp and BN)
   int a_mn3d, b_mn3d;     // OP_TILED_MN: one 3D box per stage (MN % 32 == 0) vs R/32 2D boxes
   int taps;               // OP_SHIFT_MN / halo kernel: fh * fw
-  int kstage;             // K per pipeline stage: 32, or 64 (both operands MN-major)
+  int kstage;             // K per pipeline stage: 32, or 64 (MN-major pair, or SHIFT_K/TILED_K3)
   // halo kernel (stride-1 conv on a padded pixel-major grid, see halo_conv_kernel)
   int hg, hw_grid;        // grid pitch (rows per column) and rows per image; 0 = not a grid
   int ohv, owv;           // valid output extent on the grid
@@ -568,6 +571,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             else
               for (int j = 0; j < p.BM / 32; ++j)
                 tma_2d_p(a + j * KS * 128, &tma_a, &full[s], mn0 + 32 * j, k0, lead);
+          } else if (AK == OP_SHIFT_K) {
+            // K block = KS channels of one tap (KS divides Cgp): BM consecutive
+            // grid rows shifted by the tap, one 3D box of KS/32 channel chunks
+            const int kc = k0 / 32;  // first 32-channel chunk of this K block
+            const int tap = kc / p.cchunks, cc = kc - tap * p.cchunks;
+            const int fj = tap / p.fh, fi = tap - fj * p.fh;
+            tma_3d_p(a, &tma_a, &full[s], 0, T.m0 + p.base_shift + fi + p.Hp * fj,
+                     (T.grp * p.a_grp_c) / 32 + cc, lead);
           } else {  // OP_IM2COL_K: kb = tap * cchunks + cc; one box walks BM pixels
             const int tap = kb / p.cchunks, cc = kb - tap * p.cchunks;
             const int fj = tap / p.fh, fi = tap - fj * p.fh;
@@ -575,7 +586,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                           (uint16_t)fi, (uint16_t)fj, lead);
           }
           // ---- B (BN rows) ----
-          if (BK == OP_TILED_K) {
+          if (BK == OP_TILED_K3) {
+            tma_3d_p(b, &tma_b, &full[s], 0, T.n0 + T.grp * p.b_grp_mn, k0 / 32, lead);
+          } else if (BK == OP_TILED_K) {
             tma_2d_p(b, &tma_b, &full[s], k0 + T.grp * p.b_grp_k, T.n0 + T.grp * p.b_grp_mn, lead);
           } else if (BK == OP_TILED_MN) {
             const int mn0 = T.n0 + T.grp * p.b_grp_mn;
@@ -642,6 +655,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int k = 0; k < 4; ++k)
                 mma_tf32_elect(dcol + h * p.BN, op_desc<a_mn>(a, h, k, 32),
                                op_desc<b_mn>(b, 0, k, 32), idesc, (!first || k > 0) ? 1u : 0u);
+            } else if (AK == OP_SHIFT_K) {
+              // K-major, two 32-k chunks per stage: chunk c of A at c*BM*128 B,
+              // of B at c*BN*128 B, each an ordinary SW128 K-major tile
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+                mma_tf32_elect(dcol + h * p.BN,
+                               op_desc<false>(a + (k / 4) * p.BM * 128, h, k % 4),
+                               op_desc<false>(b + (k / 4) * p.BN * 128, 0, k % 4), idesc,
+                               (!first || k > 0) ? 1u : 0u);
             } else {
 #pragma unroll
               for (int k = 0; k < 8; ++k)
@@ -1796,6 +1818,56 @@ static float* x_s2d(ck_handle* h, const float* x, const ConvDims& d, const S2D& 
   return buf;
 }
 
+// Off by default: correct, but on AlexNet the junk grid rows (25-33 %) cost
+// more than the cheaper tiled boxes save -- these GEMMs are bound by shared-
+// memory operand traffic, not TMA issue.  CK_TC_SHIFT=1.
+static bool shift_enabled() {
+  static const int on = getenv("CK_TC_SHIFT") ? atoi(getenv("CK_TC_SHIFT")) : 0;
+  return on != 0;
+}
+
+// Stride-1 implicit GEMM on a zero-padded pixel-major grid G[N*Hg*Wg][Cp]
+// with tiled (not im2col) TMA: output grid row q accumulates
+//   sum_{tap, c} G[q + base_shift + fi + Hg*fj, c] * F[row][tap][c],
+// the A tile of a K block being BM consecutive grid rows shifted by the tap --
+// one 3D box of KS/32 channel chunks (half the TMA time of an im2col box per
+// byte, tools/tma_probe.cu).  Rows whose (u, v) lie outside (ohv, owv) are
+// junk and dropped by the epilogue; p carries the epilogue fields.
+static void shift_conv(const float* G, int Cp, int Hg, int Wg, int N, int base_shift,
+                       const float* F, int Cgp, int taps, int fh, int rows, int groups, int ohv,
+                       int owv, GemmParams p, cudaStream_t s) {
+  const int64_t M = (int64_t)N * Hg * Wg;
+  p.M = (int)M;
+  p.N = rows;
+  p.K = taps * Cgp;
+  p.BN = pick_bn(rows);
+  p.splits = 1;
+  p.BM = pick_bm(M, p.BN, true);
+  const int KS = (Cgp % 64 == 0 && 3 * (p.BM + p.BN) * 64 * 4 <= 224 * 1024) ? 64 : 32;
+  p.kstage = KS;
+  p.Hp = Hg;
+  p.base_shift = base_shift;
+  p.fh = fh;
+  p.cchunks = Cgp / 32;
+  p.a_grp_c = Cgp;
+  p.b_grp_mn = rows;
+  p.hg = Hg;
+  p.hw_grid = Hg * Wg;
+  p.ohv = ohv;
+  p.owv = owv;
+  p.n_valid = rows;
+  cuuint64_t adims[3] = {32, (cuuint64_t)M, (cuuint64_t)(Cp / 32)};
+  cuuint64_t astr[2] = {(cuuint64_t)Cp * 4, 128};
+  cuuint32_t abox[3] = {32, (cuuint32_t)p.BM, (cuuint32_t)(KS / 32)};
+  CUtensorMap ta = encode_tiled(G, 3, adims, astr, abox, CU_TENSOR_MAP_SWIZZLE_128B);
+  const int64_t kt = (int64_t)taps * Cgp;
+  cuuint64_t bdims[3] = {32, (cuuint64_t)rows * groups, (cuuint64_t)(kt / 32)};
+  cuuint64_t bstr[2] = {(cuuint64_t)kt * 4, 128};
+  cuuint32_t bbox[3] = {32, (cuuint32_t)p.BN, (cuuint32_t)(KS / 32)};
+  CUtensorMap tb = encode_tiled(F, 3, bdims, bstr, bbox, CU_TENSOR_MAP_SWIZZLE_128B);
+  launch<OP_SHIFT_K, OP_TILED_K3>(ta, tb, p, 0, 0, groups, s);
+}
+
 static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
                       const ConvDims& d, const S2D& z, int relu, cudaStream_t s) {
   TcState* st = state(h);
@@ -1813,6 +1885,14 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
     p.bias = bias; p.relu = relu; p.acc = 0;
     HaloConv hc{xt, z.Csp, z.U, z.V, d.N, ft, z.Csp, taps, z.Th, z.Tw, d.K, 1, d.OH, d.OW};
     if (halo_launch(hc, p, s)) return;
+  }
+  if (shift_enabled()) {
+    GemmParams p{};
+    p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+    p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = d.K;
+    p.bias = bias; p.relu = relu; p.acc = 0;
+    shift_conv(xt, z.Csp, z.U, z.V, d.N, 0, ft, z.Csp, taps, z.Th, d.K, 1, d.OH, d.OW, p, s);
+    return;
   }
   GemmParams p{};
   p.M = d.N * d.OH * d.OW; p.N = d.K; p.K = taps * z.Csp; p.BN = pick_bn(d.K); p.splits = 1;
@@ -1853,6 +1933,17 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   // im2col over dy at (0, 0) of the U x V grid (shared with the wgrad): the
   // negative corner supplies the top/left padding, the grid's zero rows the rest
   float* dyt = dy_grid(h, dy, d, d.K, Kp, 1, z.U, z.V, s);
+  if (shift_enabled()) {
+    // output s2d pixel (u, v) at grid row u + U*v reads dy rows shifted by
+    // fi - (Th-1) + U*(fj - (Tw-1)); the grid's zero rows/columns are the padding
+    GemmParams p{};
+    p.epi = EPI_S2D; p.out = dx;
+    p.s2d = z.s; p.s2d_U = z.U; p.s2d_H = d.H; p.s2d_W = d.W; p.s2d_C = d.C;
+    p.acc = acc;
+    shift_conv(dyt, Kp, z.U, z.V, d.N, -((z.Th - 1) + z.U * (z.Tw - 1)), gt, Kp, taps, z.Th, z.Cs,
+               1, z.U, z.V, p, s);
+    return;
+  }
   GemmParams p{};
   p.M = d.N * z.U * z.V; p.N = z.Cs; p.K = taps * Kp; p.BN = pick_bn(z.Cs); p.splits = 1;
   p.OH = z.U; p.OW = z.V; p.sh = 1; p.sw = 1; p.pt = z.Th - 1; p.pl = z.Tw - 1; p.fh = z.Th;
@@ -2001,6 +2092,14 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
   float* xt;
   if (on_grid) {
     xt = x_grid(h, x, d, Cgp, Hg, Wg, s);
+    if (shift_enabled()) {
+      GemmParams p{};
+      p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+      p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg;
+      p.bias = bias; p.relu = relu; p.acc = 0;
+      shift_conv(xt, Cp, Hg, Wg, d.N, 0, ft, Cgp, taps, d.fh, Kg, d.groups, d.OH, d.OW, p, s);
+      return true;
+    }
   } else {
     xt = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * d.H * d.W * Cp, s);
     to_pm(x, xt, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, s);
@@ -2100,6 +2199,16 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   // zero rows the bottom/right
   const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
   float* dyt = dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s);
+  if (shift_enabled()) {
+    // dx (i, j) at grid row i + Hg*j reads dy rows shifted by fi - qt + Hg*(fj - ql)
+    GemmParams p{};
+    p.epi = EPI_PIX; p.out = dx; p.ld = (int64_t)d.H * d.W;
+    p.img_stride = (int64_t)d.C * d.H * d.W; p.grp_col = d.Cg;
+    p.bias = nullptr; p.relu = 0; p.acc = acc;
+    shift_conv(dyt, Kp, Hg, Wg, d.N, -(qt + Hg * ql), gt, Kgp, taps, d.fh, d.Cg, d.groups, d.H,
+               d.W, p, s);
+    return true;
+  }
   GemmParams p{};
   p.M = d.N * d.H * d.W;
   p.N = d.Cg;

@@ -1,3 +1,3 @@
-timeout 300 python -m pytest tests/test_gpu_blocks.py -x -q -k "conv" 2>&1 | tail -1
-python tools/conv_layer_bench.py --passes w
-CK_TC_WKS=32 python tools/conv_layer_bench.py --passes w --layers conv1,conv2,conv3
+timeout 600 python -m pytest tests/test_gpu_blocks.py -x -q -k "conv" 2>&1 | tail -3
+python tools/conv_layer_bench.py --passes f,d
+CK_TC_SHIFT=0 python tools/conv_layer_bench.py --passes f,d

@@ -19,7 +19,7 @@ __global__ void stream_k(const __grid_constant__ CUtensorMap map, const __grid_c
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t full[8];
-  const int stage_bytes = boxes_per_stage * R * 128 + (mode >= 2 ? R2 * 128 : 0);
+  const int stage_bytes = boxes_per_stage * R * 128 * (mode == 4 ? R2 : 1) + (mode == 2 || mode == 3 ? R2 * 128 : 0);
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&full[s])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -36,15 +36,18 @@ __global__ void stream_k(const __grid_constant__ CUtensorMap map, const __grid_c
     }
     if (it >= iters) continue;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(stage_bytes) : "memory");
-    if (mode >= 2) {  // second operand: one tiled box of R2 rows
+    if (mode == 2 || mode == 3) {  // second operand: one tiled box of R2 rows
       uint8_t* dst = sm + s * stage_bytes + boxes_per_stage * R * 128;
       asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
                    ::"r"(su32(dst)), "l"((uint64_t)&map2), "r"(su32(&full[s])), "r"(32), "r"((int)((pix * 7) % npix)) : "memory");
     }
     for (int b = 0; b < boxes_per_stage; ++b) {
-      uint8_t* dst = sm + s * stage_bytes + b * R * 128;
+      uint8_t* dst = sm + s * stage_bytes + b * R * 128 * (mode == 4 ? R2 : 1);
       const int c = (b % 4) * 32;
-      if (mode == 0 || mode == 3) {
+      if (mode == 4) {
+        asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+                     ::"r"(su32(dst)), "l"((uint64_t)&map), "r"(su32(&full[s])), "r"(0), "r"((int)(pix % npix)), "r"(0) : "memory");
+      } else if (mode == 0 || mode == 3) {
         asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
                      ::"r"(su32(dst)), "l"((uint64_t)&map), "r"(su32(&full[s])), "r"(c), "r"((int)(pix % npix)) : "memory");
       } else {
@@ -90,6 +93,15 @@ int main() {
           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return m;
   };
+  auto tiled3 = [&](int R, int D) {
+    CUtensorMap m; cuuint32_t es[3] = {1, 1, 1};
+    cuuint64_t dims[3] = {32, (cuuint64_t)npix, (cuuint64_t)(C / 32)};
+    cuuint64_t str[2] = {(cuuint64_t)C * 4, 128};
+    cuuint32_t box[3] = {32, (cuuint32_t)R, (cuuint32_t)D};
+    enc_t(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, buf, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return m;
+  };
   auto im2col = [&](int R) {
     CUtensorMap m; cuuint32_t es[4] = {1, 1, 1, 1};
     cuuint64_t dims[4] = {(cuuint64_t)C, (cuuint64_t)H, (cuuint64_t)W, (cuuint64_t)N};
@@ -109,11 +121,13 @@ int main() {
       {"im2col256+tiled192 S3", 2, 256, 1, 192, 3}, {"im2col256+tiled256 S3", 2, 256, 1, 256, 3},
       {"tiled128+tiled256 S4", 3, 128, 1, 256, 4}, {"tiled256+tiled256 S3", 3, 256, 1, 256, 3},
       {"im2col32x8+tiled128 S4", 2, 32, 8, 128, 4},
+      {"tiled3d 256x2 S3", 4, 256, 1, 2, 3}, {"tiled3d 128x2 S4", 4, 128, 1, 2, 4},
+      {"tiled3d 256x1 S4", 4, 256, 1, 1, 4}, {"tiled3d 128x4 S3", 4, 128, 1, 4, 3},
   };
   for (const Cfg& c : cfgs) {
-    CUtensorMap m = (c.mode == 1 || c.mode == 2) ? im2col(c.R) : tiled(c.R);
-    CUtensorMap m2 = tiled(c.R2 ? c.R2 : 32);
-    const int stage_bytes = c.bps * c.R * 128 + (c.mode >= 2 ? c.R2 * 128 : 0);
+    CUtensorMap m = c.mode == 4 ? tiled3(c.R, c.R2) : (c.mode == 1 || c.mode == 2) ? im2col(c.R) : tiled(c.R);
+    CUtensorMap m2 = tiled(c.mode == 4 ? 32 : (c.R2 ? c.R2 : 32));
+    const int stage_bytes = c.bps * c.R * 128 * (c.mode == 4 ? c.R2 : 1) + (c.mode == 2 || c.mode == 3 ? c.R2 * 128 : 0);
     const int iters = (int)((256LL << 20) / 148 / stage_bytes);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     stream_k<<<148, 32, c.S * stage_bytes + 1024>>>(m, m2, c.mode, c.R, c.bps, c.R2, iters, npix, H, W, N, c.S, sink);
