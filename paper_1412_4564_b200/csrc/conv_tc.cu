@@ -1485,8 +1485,8 @@ static void to_grid_pm(const float* x, float* xg, int H, int W, int C, int N, in
 static bool halo_enabled() {
   // Off by default: measured slower than the im2col kernels on AlexNet
   // (junk grid rows + per-tap filter streaming), kept for experiments.
-  static const int on = getenv("CK_TC_HALO") ? atoi(getenv("CK_TC_HALO")) : 0;
-  return on != 0;
+  const char* v = getenv("CK_TC_HALO");  // read per call: tests toggle it
+  return v && atoi(v) != 0;
 }
 
 static CUtensorMap encode_tiled(const float* base, int rank, const cuuint64_t* dims,
@@ -1822,8 +1822,8 @@ static float* x_s2d(ck_handle* h, const float* x, const ConvDims& d, const S2D& 
 // more than the cheaper tiled boxes save -- these GEMMs are bound by shared-
 // memory operand traffic, not TMA issue.  CK_TC_SHIFT=1.
 static bool shift_enabled() {
-  static const int on = getenv("CK_TC_SHIFT") ? atoi(getenv("CK_TC_SHIFT")) : 0;
-  return on != 0;
+  const char* v = getenv("CK_TC_SHIFT");  // read per call: tests toggle it
+  return v && atoi(v) != 0;
 }
 
 // Stride-1 implicit GEMM on a zero-padded pixel-major grid G[N*Hg*Wg][Cp]

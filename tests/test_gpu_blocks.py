@@ -275,3 +275,23 @@ def test_sgd_bitexact():
     w_ref, v_ref = O.sgd_step(w, v, g, 0.01, 0.9, 5e-4)
     assert np.array_equal(host(vt), v_ref)
     assert np.array_equal(host(wt), w_ref)
+
+
+@pytest.mark.parametrize("path", ["CK_TC_SHIFT", "CK_TC_HALO"])
+@pytest.mark.parametrize("xs,fs,g", [CONV_CASES[5], CONV_CASES[7], CONV_CASES[9], CONV_CASES[8]])
+def test_conv_experimental_paths(xs, fs, g, path, monkeypatch):
+    """The experimental shifted-grid and halo-reuse kernels (off by default,
+    conv_tc.cu) stay within the TF32 tolerance of the oracle."""
+    monkeypatch.setenv(path, "1")
+    r = O.Rng(sum(xs) + sum(fs) + 7)
+    x = r.uniform(O.size(xs))
+    f = r.uniform(O.size(fs), -0.1, 0.1)
+    b = r.uniform(fs[3])
+    geom = B.ConvGeom(*g)
+    y_ref, ys = O.conv_forward(x, xs, f, fs, b, g)
+    y = B.conv_forward(dev(x, xs), dev(f, fs), torch.from_numpy(b).cuda(), geom, math="tf32")
+    assert err(host(y), y_ref, "tf32") < TOL["tf32"]
+    dy = r.uniform(O.size(ys))
+    dx_ref, _, _ = O.conv_backward(x, xs, f, fs, g, dy)
+    dx, _, _ = B.conv_backward(dev(x, xs), dev(f, fs), geom, dev(dy, ys), math="tf32")
+    assert err(host(dx), dx_ref, "tf32") < TOL["tf32"]
