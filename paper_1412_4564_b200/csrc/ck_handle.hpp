@@ -25,6 +25,8 @@ struct ck_handle {
   ck::TcState* tc = nullptr;
   uint64_t call = 0;      // API call id: scopes transform caches to one call
   ck::ConvCache* conv_cache = nullptr;  // set by the graph engine around conv calls
+  float* fuse_relu = nullptr;  // engine: conv forward may also write relu(y) here
+  bool fuse_relu_done = false; // ... and reports whether it did
   ck::KernelProfiler prof;
 };
 

@@ -89,6 +89,7 @@ struct GemmParams {
   int epi_OHW;            // EPI_PIX: pixels per image of the output
   const float* bias;      // per col (EPI_PIX) or per row (EPI_LINEAR)
   int relu, acc;
+  float* out2;            // EPI_PIX / EPI_LINEAR (non-partial): also store relu(v) here
   int n_valid;            // columns < n_valid are stored
   int Hp;                 // OP_SHIFT_MN / OP_SHIFT_K: grid pitch (tap shift = fi + Hp*fj)
   int base_shift;         // OP_SHIFT_K: row offset added to every tap shift (dgrad: -(qt+Hp*ql))
@@ -394,7 +395,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
   const bool partial = p.splits > 1;
   if (partial) out += (int64_t)T.split * p.split_stride;
   // plain stores: split-K partials, or no bias / relu / accumulate
-  const bool plain = partial || (!p.bias && !p.relu && !p.acc);
+  const bool plain = partial || (!p.bias && !p.relu && !p.acc && !p.out2);
   const int64_t ld = p.ld;
   for (int h = 0; h < halves; ++h) {
     int m = T.m0 + h * 128 + q * 32 + lane;
@@ -459,6 +460,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
             if (j < lim) dst[j * ld] = __uint_as_float(r[j]);
         } else {
           const float* bcol = p.bias ? p.bias + col0 + T.grp * p.grp_col : nullptr;
+          float* dst2 = p.out2 ? p.out2 + row_base + (int64_t)col0 * ld : nullptr;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (j < lim) {
@@ -467,6 +469,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
               if (p.relu) v = v > 0.f ? v : 0.f;
               if (p.acc) v = __fadd_rn(dst[j * ld], v);
               dst[j * ld] = v;
+              if (dst2) dst2[j * ld] = v > 0.f ? v : 0.f;  // fused relu layer
             }
           }
         }
@@ -1059,7 +1062,8 @@ __global__ void wgrad_finish_k(const float* __restrict__ part, float* df, int fh
 // generic split-K finisher for EPI_LINEAR outputs: out[row + col*ld]
 __global__ void splitk_finish_k(const float* __restrict__ part, float* out, int rows, int cols,
                                 int64_t ld, int splits, int64_t split_stride,
-                                const float* __restrict__ bias, int relu, int acc) {
+                                const float* __restrict__ bias, int relu, int acc,
+                                float* __restrict__ out2) {
   const int64_t total = (int64_t)rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -1071,6 +1075,7 @@ __global__ void splitk_finish_k(const float* __restrict__ part, float* out, int 
     if (bias) s = __fadd_rn(s, bias[row]);
     if (relu) s = s > 0.f ? s : 0.f;
     out[a] = acc ? __fadd_rn(out[a], s) : s;
+    if (out2) out2[a] = s > 0.f ? s : 0.f;  // fused relu layer (acc is 0 then)
   }
 }
 
@@ -1880,7 +1885,7 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   if (halo_ok(d.K, z.Th, z.Tw, z.U)) {
     // the s2d pixel-major tensor is already a (pad-free) grid of pitch U
     GemmParams p{};
-    p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+    p.epi = EPI_PIX; p.out = y; p.out2 = h->fuse_relu; p.ld = (int64_t)d.OH * d.OW;
     p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = d.K;
     p.bias = bias; p.relu = relu; p.acc = 0;
     HaloConv hc{xt, z.Csp, z.U, z.V, d.N, ft, z.Csp, taps, z.Th, z.Tw, d.K, 1, d.OH, d.OW};
@@ -1888,7 +1893,7 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   }
   if (shift_enabled()) {
     GemmParams p{};
-    p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+    p.epi = EPI_PIX; p.out = y; p.out2 = h->fuse_relu; p.ld = (int64_t)d.OH * d.OW;
     p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = d.K;
     p.bias = bias; p.relu = relu; p.acc = 0;
     shift_conv(xt, z.Csp, z.U, z.V, d.N, 0, ft, z.Csp, taps, z.Th, d.K, 1, d.OH, d.OW, p, s);
@@ -1898,7 +1903,7 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   p.M = d.N * d.OH * d.OW; p.N = d.K; p.K = taps * z.Csp; p.BN = pick_bn(d.K); p.splits = 1;
   p.OH = d.OH; p.OW = d.OW; p.sh = 1; p.sw = 1; p.pt = 0; p.pl = 0; p.fh = z.Th;
   p.cchunks = z.Csp / 32;
-  p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+  p.epi = EPI_PIX; p.out = y; p.out2 = h->fuse_relu; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.n_valid = d.K;
   p.BM = pick_bm(p.M, p.BN, true);
@@ -2027,8 +2032,8 @@ static bool is_fc(const ConvDims& d) {
 }
 
 // ---------------------------------------------------------------- fprop ----
-bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
-                     const ConvDims& d, int relu, cudaStream_t s) {
+static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, const float* bias,
+                                 float* y, const ConvDims& d, int relu, cudaStream_t s) {
   if (!load_driver()) return false;
   prof_conv("fprop", d);
   const int Kg = d.Kg();
@@ -2042,6 +2047,7 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
     GemmParams p{};
     p.M = d.K; p.N = d.N; p.K = rup(Q, 32); p.BN = BN; p.splits = splits;
     p.epi = EPI_LINEAR; p.ld = d.K; p.n_valid = d.N; p.relu = relu; p.bias = bias;
+    p.out2 = h->fuse_relu;
     p.BM = pick_bm(p.M, p.BN);
     CUtensorMap ta = map_2d(f, Q, d.K, Q, p.BM);
     CUtensorMap tb = map_2d(x, Q, d.N, Q, BN);
@@ -2052,7 +2058,7 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
       launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, splits, s);
       count_launch();
       splitk_finish_k<<<std::min<int64_t>((per + 255) / 256, 148 * 8), 256, 0, s>>>(
-          part, y, d.K, d.N, d.K, splits, per, bias, relu, 0);
+          part, y, d.K, d.N, d.K, splits, per, bias, relu, 0, h->fuse_relu);
     } else {
       p.out = y;
       launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);
@@ -2080,7 +2086,7 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
     float* xg = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * Hg * Wg * Cp, s);
     to_grid_pm(x, xg, d.H, d.W, d.C, d.N, d.Cg, Cgp, d.groups, Hg, Wg, d.pt, d.pl, s);
     GemmParams p{};
-    p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+    p.epi = EPI_PIX; p.out = y; p.out2 = h->fuse_relu; p.ld = (int64_t)d.OH * d.OW;
     p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg;
     p.bias = bias; p.relu = relu; p.acc = 0;
     HaloConv hc{xg, Cp, Hg, Wg, d.N, ft, Cgp, taps, d.fh, d.fw, Kg, d.groups, d.OH, d.OW};
@@ -2094,7 +2100,7 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
     xt = x_grid(h, x, d, Cgp, Hg, Wg, s);
     if (shift_enabled()) {
       GemmParams p{};
-      p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+      p.epi = EPI_PIX; p.out = y; p.out2 = h->fuse_relu; p.ld = (int64_t)d.OH * d.OW;
       p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg;
       p.bias = bias; p.relu = relu; p.acc = 0;
       shift_conv(xt, Cp, Hg, Wg, d.N, 0, ft, Cgp, taps, d.fh, Kg, d.groups, d.OH, d.OW, p, s);
@@ -2114,7 +2120,7 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
   p.cchunks = Cgp / 32;
   p.a_grp_c = Cgp;
   p.b_grp_mn = Kg;
-  p.epi = EPI_PIX; p.out = y; p.ld = (int64_t)d.OH * d.OW;
+  p.epi = EPI_PIX; p.out = y; p.out2 = h->fuse_relu; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.acc = 0; p.n_valid = Kg;
   p.BM = pick_bm(p.M, p.BN, true);
@@ -2127,6 +2133,15 @@ bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* 
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (Kg + p.BN - 1) / p.BN, d.groups,
                                   s);
   return true;
+}
+
+// With h->fuse_relu set (graph engine, conv -> relu) every forward epilogue
+// also writes relu(y) there; fuse_relu_done tells the engine it happened.
+bool conv_tc_forward(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
+                     const ConvDims& d, int relu, cudaStream_t s) {
+  const bool ok = conv_tc_forward_impl(h, x, f, bias, y, d, relu, s);
+  if (ok && h->fuse_relu) h->fuse_relu_done = true;
+  return ok;
 }
 
 // ---------------------------------------------------------------- dgrad ----
@@ -2156,7 +2171,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
       launch<OP_TILED_MN, OP_TILED_K>(ta, tb, p, gm, gn, splits, s);
       count_launch();
       splitk_finish_k<<<std::min<int64_t>((per + 255) / 256, 148 * 8), 256, 0, s>>>(
-          part, dx, Q, d.N, Q, splits, per, nullptr, 0, acc);
+          part, dx, Q, d.N, Q, splits, per, nullptr, 0, acc, nullptr);
     } else {
       p.out = dx;
       launch<OP_TILED_MN, OP_TILED_K>(ta, tb, p, gm, gn, 1, s);

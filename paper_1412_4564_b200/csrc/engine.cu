@@ -70,6 +70,12 @@ struct Layer {
   std::vector<double> p;
   float* aux = nullptr;  // bnorm moments (K x 2), graph.cpp:306
   ConvCache cache;       // conv input transform shared by forward and wgrad
+  // conv -> relu fusion: the conv's epilogue also writes relu(y) (the relu
+  // layer's output) when its output feeds only that relu; the relu forward
+  // then has nothing to do.  fused_by = producing conv layer, or -1.
+  int relu_out = -1;     // conv: var index of the fused relu output
+  int fused_by = -1;     // relu: index of the conv layer that writes its output
+  bool fused_done = false;
 };
 
 static std::vector<std::string> split_csv(const char* s) {
@@ -295,6 +301,17 @@ static void finalize(ck_graph* g) {
   }
   for (auto& l : g->layers)
     if (l.kind == Kind::bnorm) l.aux = alloc(2 * (size_t)g->vars[l.in[0]].shape.c);
+  // conv -> relu pairs whose intermediate has no other reader
+  for (size_t li = 0; li < g->layers.size(); ++li) {
+    Layer& r = g->layers[li];
+    if (r.kind != Kind::relu) continue;
+    const Var& v = g->vars[r.in[0]];
+    if (v.producer < 0 || v.consumers.size() != 1) continue;
+    Layer& c = g->layers[v.producer];
+    if (c.kind != Kind::conv || c.relu_out >= 0) continue;
+    c.relu_out = r.out[0];
+    r.fused_by = v.producer;
+  }
   g->finalized = true;
 }
 
@@ -309,8 +326,15 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
       if (l.in.size() > 2) b = V(2);
       ck_conv_geom cg = conv_geom_of(l);
       h->conv_cache = &l.cache;
+      h->fuse_relu = l.relu_out >= 0 ? g->vars[l.relu_out].value : nullptr;
+      h->fuse_relu_done = false;
       st = ck_conv_forward(h, &x, &f, l.in.size() > 2 ? &b : nullptr, &cg, &y, g->math, s);
       h->conv_cache = nullptr;
+      h->fuse_relu = nullptr;
+      if (l.relu_out >= 0) {
+        Layer& r = g->layers[g->vars[l.relu_out].producer];
+        r.fused_done = st == CK_OK && h->fuse_relu_done;
+      }
       break;
     }
     case Kind::convt: {
@@ -328,6 +352,7 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
       break;
     }
     case Kind::relu: {
+      if (l.fused_by >= 0 && l.fused_done) break;  // written by the conv epilogue
       ck_tensor x = V(0);
       st = ck_relu_forward(h, &x, &y, s);
       break;
