@@ -175,3 +175,32 @@ def test_trainer_cuda_graph_replay_matches_eager():
     assert l0 == l1
     for k in p0:
         assert np.array_equal(p0[k], p1[k]), k
+
+
+@pytest.mark.parametrize("graph_mode", [False, True])
+def test_trainer_nccl_single_rank(graph_mode):
+    """The data-parallel step on a one-rank NCCL communicator (the only
+    topology one GPU allows): per-layer ncclAllReduce on the comm stream,
+    event hand-off, SGD, loss allreduce -- eagerly and captured into a CUDA
+    graph -- must equal the plain single-GPU step bit for bit (a sum over one
+    rank is the identity)."""
+    from paper_1412_4564_b200 import nets
+    from paper_1412_4564_b200.graph import Trainer
+    net = nets.lenet(batch=8)
+    params, inputs = net.init_params(), net.init_inputs()
+    out = []
+    for dp in (False, True):
+        g = device_graph(net, "tf32")
+        for k, v in {**params, **inputs}.items():
+            g.set(k, v)
+        t = Trainer(g, lr=0.01, momentum=0.9, weight_decay=5e-4)
+        if dp:
+            t.init_dp(Trainer.unique_id(), 0, 1)
+        t.set_graph(graph_mode)
+        stream = torch.cuda.Stream()
+        losses = [t.step(stream=stream.cuda_stream) for _ in range(3)]
+        out.append((losses, {p: g.get(p) for p, _, _ in net.params}))
+    (l0, p0), (l1, p1) = out
+    assert l0 == l1
+    for k in p0:
+        assert np.array_equal(p0[k], p1[k]), k
