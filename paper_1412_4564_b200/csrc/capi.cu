@@ -361,9 +361,17 @@ ck_status ck_conv_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* f,
   ConvDims d = conv_dims(x->shape, f->shape, ys, *g);
   // TF32 conv layers with a tensor-core grid path reduce db inside the dy
   // transform their dgrad/wgrad reuse; everything else uses conv_bgrad.
+  // With the engine's fused conv -> relu, dy is first produced from the relu
+  // output derivative (inside the transform when the grid path runs).
+  const float* rx = h->fuse_relu_x;
+  const float* rdy = h->fuse_relu_dy;
+  bool gated = false;
   if (db && math == CK_MATH_TF32 && (dx || df) &&
-      conv_tc_bias(h, dy->data, db->data, d, accumulate, s))
+      conv_tc_bias(h, dy->data, db->data, d, accumulate, s, rx, rdy)) {
     db = nullptr;
+    gated = rx != nullptr;
+  }
+  if (rx && !gated) relu_backward(rx, rdy, dy->data, elems(dy->shape), 0, s);
   if (db) {
     void* bws = h->scratch.get(conv_bgrad_ws_bytes((int)ys.c, (int)ys.n, (int)(ys.h * ys.w)), s);
     if (!bws) throw Err(CK_ERR_CUDA, "workspace allocation failed");

@@ -27,6 +27,10 @@ struct ck_handle {
   ck::ConvCache* conv_cache = nullptr;  // set by the graph engine around conv calls
   float* fuse_relu = nullptr;  // engine: conv forward may also write relu(y) here
   bool fuse_relu_done = false; // ... and reports whether it did
+  // engine, conv backward of a fused conv -> relu: dy (the conv output's
+  // derivative) is relu_x > 0 ? relu_dy : 0, produced inside the call
+  const float* fuse_relu_x = nullptr;
+  const float* fuse_relu_dy = nullptr;
   ck::KernelProfiler prof;
 };
 
@@ -83,7 +87,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
 bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, const ConvDims& d,
                    int acc, cudaStream_t s);
 bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, int acc,
-                  cudaStream_t s);
+                  cudaStream_t s, const float* relu_x = nullptr, const float* relu_dy = nullptr);
 void conv_tc_release(ck_handle* h);
 
 }  // namespace ck

@@ -931,9 +931,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 // (i, j) at grid position (i + oh, j + ow), channel c of group g at
 // cp = g*Cgp + (c - g*Cgp_local); zero borders and channel pads (the input of
 // halo_conv_kernel).  32 x 32 smem tile transpose.
+// With gate != nullptr the source is relu-gated first (v = gate > 0 ? x : 0,
+// the relu backward, activation.cpp:14-22, bit-exact with relu_bwd_v4) and the
+// gated HWCN value is also stored to gout: the conv backward consumes the
+// relu backward in the same pass over memory.
 __global__ void to_grid_pm_k(const float* __restrict__ x, float* __restrict__ xg, int H, int W,
                              int C, int Cg, int Cgp, int groups, int Hg, int Wg, int oh, int ow,
-                             double* __restrict__ bpart) {
+                             double* __restrict__ bpart, const float* __restrict__ gate,
+                             float* __restrict__ gout) {
   // tile: 64 grid pixels x 32 padded channels; loads coalesced along pixels
   // (two per channel row per thread), stores as float4 along channels.
   __shared__ float tile[32][65];
@@ -960,6 +965,16 @@ __global__ void to_grid_pm_k(const float* __restrict__ x, float* __restrict__ xg
     const float* xc = xn + (int64_t)(g * Cg + cl) * H * W;
 #pragma unroll
     for (int k = 0; k < 2; ++k) v[rr][k] = (ch_ok && src[k] >= 0) ? __ldg(xc + src[k]) : 0.f;
+    if (gate) {
+      const int64_t off = (int64_t)n * C * H * W + (int64_t)(g * Cg + cl) * H * W;
+#pragma unroll
+      for (int k = 0; k < 2; ++k)
+        if (ch_ok && src[k] >= 0) {
+          const float gv = __ldg(gate + off + src[k]) > 0.f ? v[rr][k] : 0.f;
+          v[rr][k] = gv;
+          gout[off + src[k]] = gv;
+        }
+    }
   }
 #pragma unroll
   for (int rr = 0; rr < 4; ++rr)
@@ -1484,7 +1499,8 @@ static void to_grid_pm(const float* x, float* xg, int H, int W, int C, int N, in
                        int groups, int Hg, int Wg, int oh, int ow, cudaStream_t s) {
   dim3 grid((Hg * Wg + 63) / 64, (Cgp * groups + 31) / 32, N);
   count_launch();
-  to_grid_pm_k<<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow, nullptr);
+  to_grid_pm_k<<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow, nullptr,
+                                    nullptr, nullptr);
 }
 
 static bool halo_enabled() {
@@ -1685,9 +1701,12 @@ __global__ void grid_bias_finish_k(const double* __restrict__ part2, float* db, 
 
 // With db != nullptr the transform also reduces db[k] = sum over all dy
 // pixels (conv.cpp:246-252), fused into the same read of dy.
+// With relu_x != nullptr, dy is produced here: dy = relu_x > 0 ? relu_dy : 0
+// (the engine's fused conv -> relu backward); the grid is built from it.
 static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, int Kgp,
                       int groups, int Hg, int Wg, cudaStream_t s, float* db = nullptr,
-                      int db_acc = 0) {
+                      int db_acc = 0, const float* relu_x = nullptr,
+                      const float* relu_dy = nullptr) {
   TcState* st = state(h);
   const int64_t key = ((((int64_t)Hg * 4099 + Wg) * 65537 + d.K) * 131071 + d.N) * 1031 +
                       Kgp * 17 + groups + ((int64_t)d.OH << 40) + ((int64_t)d.OW << 50);
@@ -1701,8 +1720,9 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
     double* part2 = bpart + (size_t)rows * Cp;
     dim3 grid(nb, (Cp + 31) / 32, d.N);
     count_launch(3);
-    to_grid_pm_k<<<grid, 256, 0, s>>>(dy, buf, d.OH, d.OW, d.K, Kg, Kgp, groups, Hg, Wg, 0, 0,
-                                      bpart);
+    to_grid_pm_k<<<grid, 256, 0, s>>>(relu_x ? relu_dy : dy, buf, d.OH, d.OW, d.K, Kg, Kgp,
+                                      groups, Hg, Wg, 0, 0, bpart, relu_x,
+                                      relu_x ? const_cast<float*>(dy) : nullptr);
     grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(bpart, part2, Cp, rows);
     grid_bias_finish_k<<<(Cp + 127) / 128, 128, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
                                                         db_acc);
@@ -2250,18 +2270,18 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
 // the same ck_conv_backward call then reuse.  False when the shape does not
 // use the grid (FC layers, strided convs without space-to-depth).
 bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, int acc,
-                  cudaStream_t s) {
+                  cudaStream_t s, const float* relu_x, const float* relu_dy) {
   if (!load_driver() || is_fc(d)) return false;
   const int Kg = d.Kg();
   if (d.sh == 1 && d.sw == 1) {
     if (d.Cg < 16 || Kg < 16) return false;
     const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
-    dy_grid(h, dy, d, Kg, rup(Kg, 32), d.groups, Hg, Wg, s, db, acc);
+    dy_grid(h, dy, d, Kg, rup(Kg, 32), d.groups, Hg, Wg, s, db, acc, relu_x, relu_dy);
     return true;
   }
   S2D z;
   if (!s2d_plan(d, z)) return false;
-  dy_grid(h, dy, d, d.K, rup(d.K, 32), 1, z.U, z.V, s, db, acc);
+  dy_grid(h, dy, d, d.K, rup(d.K, 32), 1, z.U, z.V, s, db, acc, relu_x, relu_dy);
   return true;
 }
 

@@ -76,6 +76,8 @@ struct Layer {
   int relu_out = -1;     // conv: var index of the fused relu output
   int fused_by = -1;     // relu: index of the conv layer that writes its output
   bool fused_done = false;
+  bool fused_bwd = false;  // relu backward may be left to the producing conv's backward
+  bool bwd_deferred = false;  // ... and was, in the current backward pass
 };
 
 static std::vector<std::string> split_csv(const char* s) {
@@ -311,6 +313,7 @@ static void finalize(ck_graph* g) {
     if (c.kind != Kind::conv || c.relu_out >= 0) continue;
     c.relu_out = r.out[0];
     r.fused_by = v.producer;
+    r.fused_bwd = true;
   }
   g->finalized = true;
 }
@@ -406,9 +409,18 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
       // separately when they differ.
       int a0 = acc(0), a1 = acc(1), a2 = l.in.size() > 2 ? acc(2) : a1;
       h->conv_cache = &l.cache;  // the forward's transformed input (valid this step)
+      if (l.relu_out >= 0 && g->layers[g->vars[l.relu_out].producer].bwd_deferred) {
+        // fused relu backward: this call derives dy from the relu output's derivative
+        h->fuse_relu_x = g->vars[l.out[0]].value;
+        h->fuse_relu_dy = g->vars[l.relu_out].deriv;
+      }
       struct Reset {
         ck_handle* h;
-        ~Reset() { h->conv_cache = nullptr; }
+        ~Reset() {
+          h->conv_cache = nullptr;
+          h->fuse_relu_x = nullptr;
+          h->fuse_relu_dy = nullptr;
+        }
       } reset{h};
       if (a0 == a1 && a1 == a2) {
         st = ck_conv_backward(h, &x, &f, &cg, &dy, &dx, &df, l.in.size() > 2 ? &db : nullptr, a0,
@@ -446,6 +458,13 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
       break;
     }
     case Kind::relu: {
+      l.bwd_deferred = l.fused_by >= 0 && l.fused_bwd && !acc(0);
+      if (l.bwd_deferred) {
+        // the producing conv's backward derives this derivative itself
+        // (ck_conv_backward with fuse_relu_x / fuse_relu_dy)
+        mark(0);
+        break;
+      }
       ck_tensor x = V(0), dx = D(0);
       st = ck_relu_backward(h, &x, &dy, &dx, acc(0), s);
       mark(0);
@@ -517,6 +536,7 @@ struct LayerDone {
 // graph.cpp:548-598 backward with d(objective) = 1.
 static void run_backward(ck_graph* g, int objective, cudaStream_t s, LayerDone* cb) {
   for (auto& v : g->vars) v.deriv_live = false;
+  for (auto& l : g->layers) l.bwd_deferred = false;
   Var& obj = g->vars[objective];
   if (elems(obj.shape) != 1) throw Err(CK_ERR_ARG, "objective '" + obj.name + "' is not a scalar");
   const float one = 1.0f;
