@@ -582,6 +582,11 @@ __global__ void lrn_bwd_k(const float* __restrict__ x, const float* __restrict__
 // compile-time-indexed shift registers.  Out-of-range window slots hold 0,
 // and 0 + a == a exactly, so every sum is performed in the reference's
 // order (normalize.cpp:55-62, :85-111) and matches lrn_fwd_k / lrn_bwd_k.
+// LRN with the channel window in registers, one pixel per thread (loads and
+// stores coalesced along the pixels of a warp).  Loads run P channels ahead;
+// the steady state (all prefetches in range) runs without bounds tests and
+// walks the channel planes with pointer increments -- these kernels are
+// instruction-bound otherwise.
 template <int NW>
 __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y, int HW, int C,
                               int64_t pixels, float kappa, float alpha, float nbeta) {
@@ -592,7 +597,7 @@ __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y
     const int64_t n = e / HW;
     const int p = (int)(e - n * HW);
     const float* xp = x + n * C * HW + p;
-    float* yp = y + n * C * HW + p;
+    float* yq = y + n * C * HW + p;
     auto ldx = [&](int t) { return (t >= 0 && t < C) ? __ldg(xp + (int64_t)t * HW) : 0.f; };
     float sq[NW], xv[NW];  // window k-DOWN .. k+UP
 #pragma unroll
@@ -603,27 +608,42 @@ __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y
     float xpre[P];  // x[k + UP + 1 + u]
 #pragma unroll
     for (int u = 0; u < P; ++u) xpre[u] = ldx(UP + 1 + u);
-    for (int k0 = 0; k0 < C; k0 += P) {
+    const float* lp = xp + (int64_t)(P + UP + 1) * HW;  // prefetch address of step k
+    auto step = [&](float v) {
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
+      // fast-math power (MUFU lg2/ex2, a few ulp; normalize.cpp uses std::pow)
+      const float scale = __powf(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
+      *yq = __fmul_rn(xv[DOWN], scale);
+#pragma unroll
+      for (int i = 0; i < NW - 1; ++i) {
+        sq[i] = sq[i + 1];
+        xv[i] = xv[i + 1];
+      }
+      xv[NW - 1] = v;
+      sq[NW - 1] = __fmul_rn(v, v);
+    };
+    int k0 = 0;
+    for (; k0 + 2 * P + UP + 1 <= C; k0 += P) {  // steady state: no bounds tests
+#pragma unroll
+      for (int u = 0; u < P; ++u) {
+        const float v = xpre[u];
+        xpre[u] = __ldg(lp);
+        lp += HW;
+        step(v);
+        yq += HW;
+      }
+    }
+    for (; k0 < C; k0 += P) {
 #pragma unroll
       for (int u = 0; u < P; ++u) {
         const int k = k0 + u;
         const float v = xpre[u];
-        xpre[u] = ldx(k + P + UP + 1);
-        if (k < C) {
-          float acc = 0.f;
-#pragma unroll
-          for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
-          // fast-math power (MUFU lg2/ex2, a few ulp; normalize.cpp uses std::pow)
-          const float scale = __powf(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
-          yp[(int64_t)k * HW] = __fmul_rn(xv[DOWN], scale);
-#pragma unroll
-          for (int i = 0; i < NW - 1; ++i) {
-            sq[i] = sq[i + 1];
-            xv[i] = xv[i + 1];
-          }
-          xv[NW - 1] = v;
-          sq[NW - 1] = __fmul_rn(v, v);
-        }
+        xpre[u] = k + P + UP + 1 < C ? __ldg(lp) : 0.f;
+        lp += HW;
+        if (k < C) step(v);
+        yq += HW;
       }
     }
   }
@@ -643,7 +663,6 @@ __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restri
     const int64_t base = n * C * HW + p;
     const float* xp = x + base;
     const float* gp = dy + base;
-    float* dp = dx + base;
     auto ldx = [&](int t) { return (t >= 0 && t < C) ? __ldg(xp + (int64_t)t * HW) : 0.f; };
     auto ldg = [&](int t) { return t < C ? __ldg(gp + (int64_t)t * HW) : 0.f; };
     // x window of the lead index j: xw[i] = x[j - DOWN + i], sq = its squares
@@ -659,63 +678,99 @@ __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restri
       xpre[u] = ldx(UP + 1 + u);
       gpre[u] = ldg(u);
     }
+    const float* lx = xp + (int64_t)(P + UP + 1) * HW;  // prefetch addresses of step j
+    const float* lg = gp + (int64_t)P * HW;
+    float* dq = dx + base - (int64_t)DOWN * HW;  // store address of step j (d = j - DOWN)
     float eta[NW];  // eta of indices j-NW+1 .. j (0 outside [0, C))
     float Ls[DOWN + 1], xs[DOWN + 1], gs[DOWN + 1];  // L^-beta, x, dy of j-DOWN .. j
 #pragma unroll
     for (int i = 0; i < NW; ++i) eta[i] = 0.f;
 #pragma unroll
     for (int i = 0; i <= DOWN; ++i) Ls[i] = xs[i] = gs[i] = 0.f;
-    for (int j0 = 0; j0 < C + DOWN; j0 += P) {
+    // one channel step; `full`: j < C and the store index j - DOWN >= 0
+    auto step = [&](int j, float xlead, float gj_in, bool compute, bool store) {
+      float L = 0.f, xj = 0.f, gj = 0.f, et = 0.f;
+      if (compute) {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
+        const float Lj = __fadd_rn(kappa, __fmul_rn(alpha, acc));
+        L = __powf(Lj, nb);  // L^-beta; L^(-beta-1) = L^-beta / L
+        xj = xw[DOWN];
+        gj = gj_in;
+        et = __fmul_rn(__fmul_rn(gj, __fdividef(L, Lj)), xj);
+      }
+#pragma unroll
+      for (int i = 0; i < NW - 1; ++i) eta[i] = eta[i + 1];
+      eta[NW - 1] = et;
+#pragma unroll
+      for (int i = 0; i < DOWN; ++i) {
+        Ls[i] = Ls[i + 1];
+        xs[i] = xs[i + 1];
+        gs[i] = gs[i + 1];
+      }
+      Ls[DOWN] = L;
+      xs[DOWN] = xj;
+      gs[DOWN] = gj;
+      if (store) {
+        // k in [d-UP, d+DOWN] = [j-NW+1, j]: the whole eta window, ascending
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, eta[i]);
+        const float r = __fadd_rn(__fmul_rn(gs[0], Ls[0]),
+                                  -__fmul_rn(__fmul_rn(c2ab, xs[0]), acc));
+        *dq = kAcc ? __fadd_rn(*dq, r) : r;
+      }
+      // advance the x window to lead index j + 1
+#pragma unroll
+      for (int i = 0; i < NW - 1; ++i) {
+        xw[i] = xw[i + 1];
+        sq[i] = sq[i + 1];
+      }
+      xw[NW - 1] = xlead;
+      sq[NW - 1] = __fmul_rn(xlead, xlead);
+      (void)j;
+    };
+    const int J = C + DOWN;  // steps
+    int j0 = 0;
+    // head group(s): stores not yet due, checked loads
+    for (; j0 < J && (j0 < DOWN || j0 + 2 * P + UP + 1 > C); j0 += P) {
 #pragma unroll
       for (int u = 0; u < P; ++u) {
         const int j = j0 + u;
-        const float xlead = xpre[u], gj_in = gpre[u];
-        xpre[u] = ldx(j + P + UP + 1);
-        gpre[u] = ldg(j + P);
-        if (j < C + DOWN) {
-          float L = 0.f, xj = 0.f, gj = 0.f, et = 0.f;
-          if (j < C) {
-            float acc = 0.f;
+        const float xl = xpre[u], gi = gpre[u];
+        xpre[u] = j + P + UP + 1 < C ? __ldg(lx) : 0.f;
+        gpre[u] = j + P < C ? __ldg(lg) : 0.f;
+        lx += HW;
+        lg += HW;
+        if (j < J) step(j, xl, gi, j < C, j >= DOWN);
+        dq += HW;
+      }
+    }
+    // steady state: every load in range, every step computes and stores
+    for (; j0 + 2 * P + UP + 1 <= C; j0 += P) {
 #pragma unroll
-            for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
-            const float Lj = __fadd_rn(kappa, __fmul_rn(alpha, acc));
-            L = __powf(Lj, nb);  // L^-beta; L^(-beta-1) = L^-beta / L
-            xj = xw[DOWN];
-            gj = gj_in;
-            et = __fmul_rn(__fmul_rn(gj, __fdividef(L, Lj)), xj);
-          }
+      for (int u = 0; u < P; ++u) {
+        const float xl = xpre[u], gi = gpre[u];
+        xpre[u] = __ldg(lx);
+        gpre[u] = __ldg(lg);
+        lx += HW;
+        lg += HW;
+        step(j0 + u, xl, gi, true, true);
+        dq += HW;
+      }
+    }
+    for (; j0 < J; j0 += P) {
 #pragma unroll
-          for (int i = 0; i < NW - 1; ++i) eta[i] = eta[i + 1];
-          eta[NW - 1] = et;
-#pragma unroll
-          for (int i = 0; i < DOWN; ++i) {
-            Ls[i] = Ls[i + 1];
-            xs[i] = xs[i + 1];
-            gs[i] = gs[i + 1];
-          }
-          Ls[DOWN] = L;
-          xs[DOWN] = xj;
-          gs[DOWN] = gj;
-          const int d = j - DOWN;
-          if (d >= 0) {
-            // k in [d-UP, d+DOWN] = [j-NW+1, j]: the whole eta window, ascending
-            float acc = 0.f;
-#pragma unroll
-            for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, eta[i]);
-            const float r = __fadd_rn(__fmul_rn(gs[0], Ls[0]),
-                                      -__fmul_rn(__fmul_rn(c2ab, xs[0]), acc));
-            float* o = dp + (int64_t)d * HW;
-            *o = kAcc ? __fadd_rn(*o, r) : r;
-          }
-          // advance the x window to lead index j + 1
-#pragma unroll
-          for (int i = 0; i < NW - 1; ++i) {
-            xw[i] = xw[i + 1];
-            sq[i] = sq[i + 1];
-          }
-          xw[NW - 1] = xlead;
-          sq[NW - 1] = __fmul_rn(xlead, xlead);
-        }
+      for (int u = 0; u < P; ++u) {
+        const int j = j0 + u;
+        const float xl = xpre[u], gi = gpre[u];
+        xpre[u] = j + P + UP + 1 < C ? __ldg(lx) : 0.f;
+        gpre[u] = j + P < C ? __ldg(lg) : 0.f;
+        lx += HW;
+        lg += HW;
+        if (j < J) step(j, xl, gi, j < C, j >= DOWN);
+        dq += HW;
       }
     }
   }
