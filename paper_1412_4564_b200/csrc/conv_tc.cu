@@ -560,6 +560,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
           mbar_wait(&empty[s], ph ^ 1);
+          if (p.exp == 2) {  // experiment: no operand loads (measures MMA + smem reads)
+            if (lead) mbar_arrive(&full[s]);
+            continue;
+          }
           mbar_expect_tx_p(&full[s], bytes, lead);
           uint8_t* a = sA + s * stage_a;
           uint8_t* b = sB + s * stage_b;
@@ -652,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t a = smem_u32(sA + s * stage_a);
           const uint32_t b = smem_u32(sB + s * stage_b);
           const bool first = kb == T.kb0;
-          for (int h = 0; h < halves; ++h) {
+          for (int h = 0; h < halves && p.exp != 1; ++h) {  // exp 1: no MMAs (TMA only)
             if (KS == 32) {  // fully unrolled issue: the MMA thread is on the critical path
 #pragma unroll
               for (int k = 0; k < 4; ++k)
@@ -1351,6 +1355,8 @@ static CUtensorMap map_im2col(const float* base, int Cp, int H, int W, int N, in
 
 static int pick_bn(int n) {
   // largest MMA N (multiple of 16, <= 256) that tiles n with little waste
+  static const int force = getenv("CK_TC_BN") ? atoi(getenv("CK_TC_BN")) : 0;  // experiments
+  if (force > 0 && force < n) return force;
   if (n <= 256) return rup(n, 16);
   const int cands[] = {256, 192, 128};
   int best = 128;

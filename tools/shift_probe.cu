@@ -131,14 +131,15 @@ __global__ void mma_rate(int r0, long long* out) {
 
 // Streaming variant: S stages of (A 16 KB = 128 rows x 32 k, B NT rows x 32 k),
 // each MMA reads a different stage / k-slice, as in the GEMM mainloop.
-template <int NT, int S>
+template <int NT, int S, int CE = 0, int NACC = 1>
 __global__ void mma_stream(long long* out) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, bar2[8];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid / 32;
   const int stage = 16384 + NT * 128;
+  if (tid < 8) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar2[tid])));
   for (int e = tid; e < S * stage / 4; e += blockDim.x) ((float*)sm)[e] = 0.001f * (e & 7);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_base)), "r"(256));
@@ -158,9 +159,12 @@ __global__ void mma_stream(long long* out) {
       const uint32_t a = su32(sm + st * stage), b = a + 16384;
       const uint64_t da = sdesc(a + k * 32, 16, 1024, 0);
       const uint64_t db = sdesc(b + k * 32, 16, 1024, 0);
+      const uint32_t dacc = tmem + (uint32_t)(((i / 4) % NACC) * NT);
       asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
-                   ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(1u));
+                   ::"r"(dacc), "l"(da), "l"(db), "r"(idesc), "r"(1u));
+      if (CE && (i % CE) == CE - 1)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar2[(i / CE) % 8])) : "memory");
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(&bar)) : "memory");
     asm volatile("{\n.reg .pred p;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W;\n}\n" ::"r"(su32(&bar)) : "memory");
@@ -175,11 +179,11 @@ __global__ void mma_stream(long long* out) {
   }
 }
 
-template <int NT, int S>
+template <int NT, int S, int CE = 0, int NACC = 1>
 static long long run_stream(long long* d) {
   const int smem = S * (16384 + NT * 128) + 2048;
-  cudaFuncSetAttribute(mma_stream<NT, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  mma_stream<NT, S><<<1, 128, smem>>>(d);
+  cudaFuncSetAttribute(mma_stream<NT, S, CE, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  mma_stream<NT, S, CE, NACC><<<1, 128, smem>>>(d);
   cudaDeviceSynchronize();
   long long c; cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
   return c;
@@ -191,6 +195,11 @@ int main() {
     printf("streaming MMA (M=128, K=8 tf32) cycles/MMA: N=256 S1 %lld S4 %lld | N=192 S1 %lld S4 %lld | N=96 S1 %lld S6 %lld | N=48 S1 %lld S6 %lld\n",
            run_stream<256, 1>(d), run_stream<256, 4>(d), run_stream<192, 1>(d), run_stream<192, 4>(d),
            run_stream<96, 1>(d), run_stream<96, 6>(d), run_stream<48, 1>(d), run_stream<48, 6>(d));
+    printf("N=192 S4: commit every 8 %lld, every 4 %lld, 2 accumulators %lld, 2 acc + commit/8 %lld\n",
+           run_stream<192, 4, 8, 1>(d), run_stream<192, 4, 4, 1>(d), run_stream<192, 4, 0, 2>(d),
+           run_stream<192, 4, 8, 2>(d));
+    printf("N=128 S4: plain %lld, 2 acc + commit/8 %lld | N=96 2 acc + commit/8 %lld\n",
+           run_stream<128, 4>(d), run_stream<128, 4, 8, 2>(d), run_stream<96, 4, 8, 2>(d));
   }
   {
     long long* d; cudaMalloc(&d, 8);
