@@ -35,7 +35,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     inc_nccl, lib_nccl = nccl_paths()
     common = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc_nccl,
-              "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3"]
+              "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
+              *os.environ.get("CK_EXTRA_NVCC", "").split()]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "ck", "ck.h"))
     hdr_mtime = max(os.path.getmtime(h) for h in headers)

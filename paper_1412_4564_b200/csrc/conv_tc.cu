@@ -315,6 +315,36 @@ __device__ __forceinline__ void mma_tf32_elect(uint32_t tmem_d, uint64_t a, uint
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// Four MMAs of one stage from one elected lane: A/B descriptors advance by
+// astep/bstep (16-byte units) per MMA; the first accumulates iff acc != 0.
+// One asm block keeps the per-kblock issue path short -- the issue loop is
+// latency-bound on its own instruction count otherwise (~160 instructions
+// per 4 MMAs took longer than the MMAs themselves).
+__device__ __forceinline__ void mma4_elect(uint32_t d, uint64_t a, uint32_t astep, uint64_t b,
+                                           uint32_t bstep, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t;\n"
+      ".reg .b64 a1, a2, a3, b1, b2, b3, sa, sb;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "setp.ne.b32 t, %3, 0;\n"  // idesc != 0: constant true
+      "cvt.u64.u32 sa, %4;\n"
+      "cvt.u64.u32 sb, %5;\n"
+      "add.s64 a1, %1, sa;\n"
+      "add.s64 b1, %2, sb;\n"
+      "add.s64 a2, a1, sa;\n"
+      "add.s64 b2, b1, sb;\n"
+      "add.s64 a3, a2, sa;\n"
+      "add.s64 b3, b2, sb;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], a1, b1, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], a2, b2, %3, t;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], a3, b3, %3, t;\n"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(astep), "r"(bstep), "r"(acc));
+}
+
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n"
@@ -479,6 +509,45 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
   }
 }
 
+// The MMA issuer's K loop for one tile: NG groups of four MMAs per stage
+// (group g: A/B descriptor offsets ga/gb, accumulator column offset gd; bit g
+// of first_mask = group g starts an accumulator, so it overwrites on the
+// tile's first stage).  Straight-line per stage: wait full, issue, commit.
+struct Ring {
+  int s;
+  uint32_t ph;
+};
+template <int NG>
+__device__ __forceinline__ void mma_tile(uint64_t* full, uint64_t* empty, int S, Ring& r, int nkb,
+                                         uint32_t dcol, uint64_t da0, uint64_t db0, uint32_t sa16,
+                                         uint32_t sb16, uint32_t ak, uint32_t bk, const uint32_t* ga,
+                                         const uint32_t* gb, const uint32_t* gd, uint32_t first_mask,
+                                         uint32_t idesc, bool wait_full, bool do_mma) {
+  uint32_t oa[NG], ob[NG], od[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    oa[g] = ga[g];
+    ob[g] = gb[g];
+    od[g] = dcol + gd[g];
+  }
+  for (int i = 0; i < nkb; ++i) {
+    if (wait_full) mbar_wait(&full[r.s], r.ph);
+    tc_fence_after();
+    const uint64_t da = da0 + (uint64_t)(r.s * sa16), db = db0 + (uint64_t)(r.s * sb16);
+    if (do_mma) {
+#pragma unroll
+      for (int g = 0; g < NG; ++g)
+        mma4_elect(od[g], da + oa[g], ak, db + ob[g], bk, idesc,
+                   (i > 0 || !((first_mask >> g) & 1)) ? 1u : 0u);
+    }
+    mma_commit_elect(&empty[r.s]);
+    if (++r.s == S) {
+      r.s = 0;
+      r.ph ^= 1;
+    }
+  }
+}
+
 // ============================================================================
 //                                 the kernel
 // ============================================================================
@@ -542,7 +611,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     {
       const uint32_t lead = elect_one();
       const uint32_t bytes = stage_a + stage_b;
-      int it = 0;
+      const int kc_step = KS / 32;  // 32-channel chunks per K block
+      int s = 0;
+      uint32_t ph = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const Tile T = tile_at(p, t);
         // im2col origin of this M tile (first output pixel)
@@ -556,66 +627,96 @@ __global__ void __launch_bounds__(kThreads, 1)
           a_h = a_h * p.sh - p.pt;
           a_w = a_w * p.sw - p.pl;
         }
-        for (int kb = T.kb0; kb < T.kb1; ++kb, ++it) {
-          const int s = it % S;
-          const uint32_t ph = (it / S) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
+        // (tap, chunk) walk of the A operand, advanced incrementally per K block:
+        // OP_IM2COL_K: K block kb = tap * cchunks + cc;
+        // OP_SHIFT_K:  32-channel chunk kc = kb * KS / 32 = tap * cchunks + cc
+        int cc = 0, fi = 0, fj = 0;
+        if (AK == OP_IM2COL_K || AK == OP_SHIFT_K) {
+          const int kc = AK == OP_IM2COL_K ? T.kb0 : T.kb0 * kc_step;
+          const int tap = kc / p.cchunks;
+          cc = kc - tap * p.cchunks;
+          fj = tap / p.fh;
+          fi = tap - fj * p.fh;
+        }
+        // OP_SHIFT_MN B boxes: per-tile (row shift, channel block) of each box
+        int b_shift[8], b_cb[8];
+        const int nbox = BK == OP_SHIFT_MN ? p.BN / p.b_rows : 0;
+        if (BK == OP_SHIFT_MN) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int nn = T.n0 + j * p.b_rows;
+            int tap = nn / (p.cchunks * 32);
+            const int c = nn - tap * p.cchunks * 32;
+            tap = min(tap, p.taps - 1);  // columns past the last tap are masked
+            const int jj = tap / p.fh, ii = tap - jj * p.fh;
+            b_shift[j] = ii + p.Hp * jj;
+            b_cb[j] = (T.grp * p.b_grp_c + c) / 32;
+          }
+        }
+        for (int kb = T.kb0; kb < T.kb1; ++kb) {
+          if (p.exp != 5) mbar_wait(&empty[s], ph ^ 1);  // exp 5: no producer
           if (p.exp == 2) {  // experiment: no operand loads (measures MMA + smem reads)
             if (lead) mbar_arrive(&full[s]);
-            continue;
-          }
-          mbar_expect_tx_p(&full[s], bytes, lead);
-          uint8_t* a = sA + s * stage_a;
-          uint8_t* b = sB + s * stage_b;
-          const int k0 = kb * KS;
-          // ---- A (BM rows) ----
-          if (AK == OP_TILED_K) {
-            tma_2d_p(a, &tma_a, &full[s], k0 + T.grp * p.a_grp_k, T.m0 + T.grp * p.a_grp_mn, lead);
-          } else if (AK == OP_TILED_MN) {
-            const int mn0 = T.m0 + T.grp * p.a_grp_mn;
-            if (p.a_mn3d)
-              tma_3d_p(a, &tma_a, &full[s], 0, k0, mn0 / 32, lead);
-            else
-              for (int j = 0; j < p.BM / 32; ++j)
-                tma_2d_p(a + j * KS * 128, &tma_a, &full[s], mn0 + 32 * j, k0, lead);
-          } else if (AK == OP_SHIFT_K) {
-            // K block = KS channels of one tap (KS divides Cgp): BM consecutive
-            // grid rows shifted by the tap, one 3D box of KS/32 channel chunks
-            const int kc = k0 / 32;  // first 32-channel chunk of this K block
-            const int tap = kc / p.cchunks, cc = kc - tap * p.cchunks;
-            const int fj = tap / p.fh, fi = tap - fj * p.fh;
-            tma_3d_p(a, &tma_a, &full[s], 0, T.m0 + p.base_shift + fi + p.Hp * fj,
-                     (T.grp * p.a_grp_c) / 32 + cc, lead);
-          } else {  // OP_IM2COL_K: kb = tap * cchunks + cc; one box walks BM pixels
-            const int tap = kb / p.cchunks, cc = kb - tap * p.cchunks;
-            const int fj = tap / p.fh, fi = tap - fj * p.fh;
-            tma_im2col_4d_p(a, &tma_a, &full[s], T.grp * p.a_grp_c + cc * 32, a_h, a_w, a_n,
-                          (uint16_t)fi, (uint16_t)fj, lead);
-          }
-          // ---- B (BN rows) ----
-          if (BK == OP_TILED_K3) {
-            tma_3d_p(b, &tma_b, &full[s], 0, T.n0 + T.grp * p.b_grp_mn, k0 / 32, lead);
-          } else if (BK == OP_TILED_K) {
-            tma_2d_p(b, &tma_b, &full[s], k0 + T.grp * p.b_grp_k, T.n0 + T.grp * p.b_grp_mn, lead);
-          } else if (BK == OP_TILED_MN) {
-            const int mn0 = T.n0 + T.grp * p.b_grp_mn;
-            if (p.b_mn3d)
-              tma_3d_p(b, &tma_b, &full[s], 0, k0, mn0 / 32, lead);
-            else
-              for (int j = 0; j < p.BN / 32; ++j)
-                tma_2d_p(b + j * KS * 128, &tma_b, &full[s], mn0 + 32 * j, k0, lead);
-          } else if (BK == OP_SHIFT_MN) {
-            // K block = 32 rows of the padded grid (pitch Hp); MN = (tap, c):
-            // one 3D box per tap, b_rows channels, rows shifted by the tap.
-            for (int j = 0; j < p.BN / p.b_rows; ++j) {
-              const int nn = T.n0 + j * p.b_rows;
-              int tap = nn / (p.cchunks * 32);
-              const int c = nn - tap * p.cchunks * 32;
-              tap = min(tap, p.taps - 1);  // columns past the last tap are masked
-              const int fj = tap / p.fh, fi = tap - fj * p.fh;
-              tma_3d_p(b + j * p.b_rows * KS * 4, &tma_b, &full[s], 0, k0 + fi + p.Hp * fj,
-                     (T.grp * p.b_grp_c + c) / 32, lead);
+          } else if (p.exp != 5) {
+            mbar_expect_tx_p(&full[s], bytes, lead);
+            uint8_t* a = sA + s * stage_a;
+            uint8_t* b = sB + s * stage_b;
+            const int k0 = kb * KS;
+            // ---- A (BM rows) ----
+            if (AK == OP_TILED_K) {
+              tma_2d_p(a, &tma_a, &full[s], k0 + T.grp * p.a_grp_k, T.m0 + T.grp * p.a_grp_mn, lead);
+            } else if (AK == OP_TILED_MN) {
+              const int mn0 = T.m0 + T.grp * p.a_grp_mn;
+              if (p.a_mn3d)
+                tma_3d_p(a, &tma_a, &full[s], 0, k0, mn0 / 32, lead);
+              else
+                for (int j = 0; j < p.BM / 32; ++j)
+                  tma_2d_p(a + j * KS * 128, &tma_a, &full[s], mn0 + 32 * j, k0, lead);
+            } else if (AK == OP_SHIFT_K) {
+              // K block = KS channels of one tap (KS divides Cgp): BM consecutive
+              // grid rows shifted by the tap, one 3D box of KS/32 channel chunks
+              tma_3d_p(a, &tma_a, &full[s], 0, T.m0 + p.base_shift + fi + p.Hp * fj,
+                       (T.grp * p.a_grp_c) / 32 + cc, lead);
+            } else {  // OP_IM2COL_K: one box walks BM pixels
+              tma_im2col_4d_p(a, &tma_a, &full[s], T.grp * p.a_grp_c + cc * 32, a_h, a_w, a_n,
+                              (uint16_t)fi, (uint16_t)fj, lead);
             }
+            // ---- B (BN rows) ----
+            if (BK == OP_TILED_K3) {
+              tma_3d_p(b, &tma_b, &full[s], 0, T.n0 + T.grp * p.b_grp_mn, k0 / 32, lead);
+            } else if (BK == OP_TILED_K) {
+              tma_2d_p(b, &tma_b, &full[s], k0 + T.grp * p.b_grp_k, T.n0 + T.grp * p.b_grp_mn, lead);
+            } else if (BK == OP_TILED_MN) {
+              const int mn0 = T.n0 + T.grp * p.b_grp_mn;
+              if (p.b_mn3d)
+                tma_3d_p(b, &tma_b, &full[s], 0, k0, mn0 / 32, lead);
+              else
+                for (int j = 0; j < p.BN / 32; ++j)
+                  tma_2d_p(b + j * KS * 128, &tma_b, &full[s], mn0 + 32 * j, k0, lead);
+            } else if (BK == OP_SHIFT_MN) {
+              // K block = KS rows of the padded grid (pitch Hp); MN = (tap, c):
+              // one 3D box per tap, b_rows channels, rows shifted by the tap.
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (j < nbox)
+                  tma_3d_p(b + j * p.b_rows * KS * 4, &tma_b, &full[s], 0, k0 + b_shift[j], b_cb[j],
+                           lead);
+            }
+          }
+          // advance the (tap, chunk) walk and the stage ring
+          if (AK == OP_IM2COL_K || AK == OP_SHIFT_K) {
+            cc += AK == OP_IM2COL_K ? 1 : kc_step;
+            if (cc >= p.cchunks) {
+              cc -= p.cchunks;
+              if (++fi == p.fh) {
+                fi = 0;
+                ++fj;
+              }
+            }
+          }
+          if (++s == S) {
+            s = 0;
+            ph ^= 1;
           }
         }
       }
@@ -629,8 +730,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                      b_mn = BK == OP_TILED_MN || BK == OP_SHIFT_MN;
       const uint32_t idesc = idesc_tf32(p.BN, a_mn, b_mn);
       int it = 0, tc = 0;
+      // descriptors of stage 0 / half 0 / k 0, advanced in 16-byte units:
+      //   K-major SW128: k +32 B, half +16 KB (128 rows), 32-k chunk +rows*128 B
+      //   MN-major SW128_32B: k +1024 B, half +KS*512 B
+      const uint64_t da0 = a_mn ? sdesc(smem_u32(sA), KS * 128, 512, 1) : sdesc(smem_u32(sA), 16, 1024, 2);
+      const uint64_t db0 = b_mn ? sdesc(smem_u32(sB), KS * 128, 512, 1) : sdesc(smem_u32(sB), 16, 1024, 2);
+      const uint32_t ak = a_mn ? 64 : 2, bk = b_mn ? 64 : 2;
+      const uint32_t ah = a_mn ? KS * 32 : 1024;
+      const uint32_t sa16 = stage_a >> 4, sb16 = stage_b >> 4;
+      const bool do_mma = p.exp != 1;      // exp 1: no MMAs (TMA only)
+      const bool wait_full = p.exp != 5;   // exp 5: MMAs only (no operand handshake)
+      // MMA groups per stage: (half h, 32-k chunk c) -> g = h * chunks + c
+      const int chunks = KS / 32, ng = halves * chunks;
+      uint32_t ga[4] = {0, 0, 0, 0}, gb[4] = {0, 0, 0, 0}, gd[4] = {0, 0, 0, 0}, first_mask = 0;
+      for (int h = 0; h < halves; ++h)
+        for (int c = 0; c < chunks; ++c) {
+          const int g = h * chunks + c;
+          const uint32_t ca = AK == OP_SHIFT_K ? p.BM * 8 : 4 * ak;  // 32-k chunk step of A
+          const uint32_t cb = AK == OP_SHIFT_K ? p.BN * 8 : 4 * bk;
+          ga[g] = h * ah + c * ca;
+          gb[g] = c * cb;
+          gd[g] = h * p.BN;
+          if (c == 0) first_mask |= 1u << g;
+        }
+      Ring ring{0, 0};
 #ifdef CK_TC_PROFILE  // build with -DCK_TC_PROFILE and run with CK_TC_PROF=1
-      unsigned long long w_t = 0, w_f = 0, t_start = clock64();
+      unsigned long long w_t = 0, w_f = 0, t_start = clock64(), g_start;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
 #define CK_PROF_T0(v) unsigned long long v = clock64()
 #define CK_PROF_ADD(acc, v) acc += clock64() - v
 #else
@@ -646,49 +772,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         CK_PROF_ADD(w_t, c0);
         tc_fence_after();
         const uint32_t dcol = tmem + (uint32_t)(ab * acc_cols);
-        for (int kb = T.kb0; kb < T.kb1; ++kb, ++it) {
-          const int s = it % S;
-          const uint32_t ph = (it / S) & 1;
-          CK_PROF_T0(c1);
-          mbar_wait(&full[s], ph);
-          CK_PROF_ADD(w_f, c1);
-          tc_fence_after();
-          const uint32_t a = smem_u32(sA + s * stage_a);
-          const uint32_t b = smem_u32(sB + s * stage_b);
-          const bool first = kb == T.kb0;
-          for (int h = 0; h < halves && p.exp != 1; ++h) {  // exp 1: no MMAs (TMA only)
-            if (KS == 32) {  // fully unrolled issue: the MMA thread is on the critical path
-#pragma unroll
-              for (int k = 0; k < 4; ++k)
-                mma_tf32_elect(dcol + h * p.BN, op_desc<a_mn>(a, h, k, 32),
-                               op_desc<b_mn>(b, 0, k, 32), idesc, (!first || k > 0) ? 1u : 0u);
-            } else if (AK == OP_SHIFT_K) {
-              // K-major, two 32-k chunks per stage: chunk c of A at c*BM*128 B,
-              // of B at c*BN*128 B, each an ordinary SW128 K-major tile
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                mma_tf32_elect(dcol + h * p.BN,
-                               op_desc<false>(a + (k / 4) * p.BM * 128, h, k % 4),
-                               op_desc<false>(b + (k / 4) * p.BN * 128, 0, k % 4), idesc,
-                               (!first || k > 0) ? 1u : 0u);
-            } else {
-#pragma unroll
-              for (int k = 0; k < 8; ++k)
-                mma_tf32_elect(dcol + h * p.BN, op_desc<a_mn>(a, h, k, 64),
-                               op_desc<b_mn>(b, 0, k, 64), idesc, (!first || k > 0) ? 1u : 0u);
-            }
-          }
-          mma_commit_elect(&empty[s]);
-        }
+        const int nkb = T.kb1 - T.kb0;
+        if (ng == 1)
+          mma_tile<1>(full, empty, S, ring, nkb, dcol, da0, db0, sa16, sb16, ak, bk, ga, gb, gd,
+                      first_mask, idesc, wait_full, do_mma);
+        else if (ng == 2)
+          mma_tile<2>(full, empty, S, ring, nkb, dcol, da0, db0, sa16, sb16, ak, bk, ga, gb, gd,
+                      first_mask, idesc, wait_full, do_mma);
+        else
+          mma_tile<4>(full, empty, S, ring, nkb, dcol, da0, db0, sa16, sb16, ak, bk, ga, gb, gd,
+                      first_mask, idesc, wait_full, do_mma);
+        it += nkb;
         mma_commit_elect(&tfull[ab]);
       }
 #ifdef CK_TC_PROFILE
       if (p.prof && lane == 0) {
-        unsigned long long* o = p.prof + blockIdx.x * 4;
+        unsigned long long* o = p.prof + blockIdx.x * 8;
+        unsigned long long g_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
         o[0] = clock64() - t_start;
         o[1] = w_t;
         o[2] = w_f;
         o[3] = it;
+        o[4] = g_end - g_start;
       }
 #endif
 #undef CK_PROF_T0
@@ -698,17 +804,37 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ----------------------------------------------------------- epilogue --
     int tc = 0;
+#ifdef CK_TC_PROFILE
+    unsigned long long e_w = 0, e_b = 0;
+#endif
     for (int t = blockIdx.x; t < total; t += gridDim.x, ++tc) {
       const Tile T = tile_at(p, t);
       const int ab = tc % p.nacc;
       const uint32_t aph = (tc / p.nacc) & 1;
+#ifdef CK_TC_PROFILE
+      unsigned long long e0 = clock64();
+#endif
       mbar_wait(&tfull[ab], aph);
       tc_fence_after();
-      epilogue_tile(p, T, tmem + (uint32_t)(ab * acc_cols), T.kb0 >= T.kb1, halves, warp, lane);
+#ifdef CK_TC_PROFILE
+      unsigned long long e1 = clock64();
+      e_w += e1 - e0;
+#endif
+      if (p.exp != 5)  // exp 5: no epilogue work
+        epilogue_tile(p, T, tmem + (uint32_t)(ab * acc_cols), T.kb0 >= T.kb1, halves, warp, lane);
       tc_fence_before();
       __syncwarp();
+#ifdef CK_TC_PROFILE
+      e_b += clock64() - e1;
+#endif
       if (lane == 0) mbar_arrive(&tempty[ab]);
     }
+#ifdef CK_TC_PROFILE
+    if (p.prof && warp == 2 && lane == 0) {
+      p.prof[blockIdx.x * 8 + 5] = e_w;
+      p.prof[blockIdx.x * 8 + 6] = e_b;
+    }
+#endif
   }
   tc_fence_before();
   __syncthreads();
@@ -1371,17 +1497,23 @@ static int pick_bn(int n) {
   return best;
 }
 
-// Tile M: two M=128 MMAs per CTA (sharing each B tile) once M is large.
-// Keep TMEM double-buffered (2 x BM/128 x BN <= 512 columns) so the epilogue
-// of one tile overlaps the next tile's mainloop.
-// BM = 256 (two M=128 MMAs sharing each B tile) halves the B traffic per
-// FLOP; for the conv im2col GEMMs it wins even without TMEM double buffering
-// (BN > 128), for the FC GEMMs only when the accumulators stay double-buffered.
-static int pick_bm(int64_t M, int BN, bool conv = false) {
+// Tile M: one or two M=128 MMAs per CTA (BM = 256 shares each B tile between
+// two MMAs, halving the B traffic per FLOP).  For the implicit-GEMM convs
+// (nt = N tiles x groups) pick the BM with the smaller modelled makespan:
+// waves x per-tile work, with BM = 256 charged 25 % when its accumulators
+// cannot be double-buffered in TMEM (2 x 2 x BN > 512 columns: the epilogue
+// then serialises with the next tile) and BM = 128 charged 8 % for its extra
+// B traffic.  FC / wgrad GEMMs: BM = 256 only when TMEM stays double-buffered.
+static int pick_bm(int64_t M, int BN, bool conv = false, int nt = 1) {
   static const int mode = getenv("CK_TC_BM") ? atoi(getenv("CK_TC_BM")) : 0;  // experiments
   if (mode == 256) return M >= 4096 ? 256 : 128;
   if (mode == 128) return 128;
-  return (M >= 4096 && (conv || BN <= 128)) ? 256 : 128;
+  if (M < 4096) return 128;
+  if (!conv) return BN <= 128 ? 256 : 128;
+  const int64_t t256 = (M + 255) / 256 * nt, t128 = (M + 127) / 128 * nt;
+  const double c256 = (double)((t256 + 147) / 148) * 2.0 * (BN <= 128 ? 1.0 : 1.25);
+  const double c128 = (double)((t128 + 147) / 148) * 1.08;
+  return c128 < c256 ? 128 : 256;
 }
 
 template <int AK, int BK>
@@ -1411,9 +1543,9 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
   count_launch();
   static const int mprof = getenv("CK_TC_PROF") ? atoi(getenv("CK_TC_PROF")) : 0;
   static unsigned long long* mbuf = nullptr;
-  if (mprof && !mbuf) cudaMalloc(&mbuf, 148 * 4 * sizeof(unsigned long long));
+  if (mprof && !mbuf) cudaMalloc(&mbuf, (148 * 8 + 512) * sizeof(unsigned long long));
   p.prof = mprof ? mbuf : nullptr;
-  if (mprof) cudaMemsetAsync(mbuf, 0, 148 * 4 * sizeof(unsigned long long), s);
+  if (mprof) cudaMemsetAsync(mbuf, 0, (148 * 8 + 512) * sizeof(unsigned long long), s);
   KernelProfiler* pr = (g_prof && g_prof->on && !g_prof->label.empty()) ? g_prof : nullptr;
   KernelProfiler::Rec rec;
   if (pr) {
@@ -1426,20 +1558,28 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
   }
   tc_gemm_kernel<AK, BK><<<grid, kThreads, smem, s>>>(a, b, p);
   if (mprof) {  // debug: where the MMA thread of each CTA spent its time
-    unsigned long long hbuf[148 * 4];
+    unsigned long long hbuf[148 * 8 + 512];
     cudaStreamSynchronize(s);
     cudaMemcpy(hbuf, mbuf, sizeof(hbuf), cudaMemcpyDeviceToHost);
-    double tot = 0, wt = 0, wf = 0, kb = 0;
+    double tot = 0, wt = 0, wf = 0, kb = 0, ew = 0, eb = 0, ns = 0;
     int n = 0;
     for (int i = 0; i < 148; ++i)
-      if (hbuf[i * 4]) {
-        tot += hbuf[i * 4]; wt += hbuf[i * 4 + 1]; wf += hbuf[i * 4 + 2]; kb += hbuf[i * 4 + 3];
+      if (hbuf[i * 8]) {
+        tot += hbuf[i * 8]; wt += hbuf[i * 8 + 1]; wf += hbuf[i * 8 + 2]; kb += hbuf[i * 8 + 3];
+        ns += hbuf[i * 8 + 4]; ew += hbuf[i * 8 + 5]; eb += hbuf[i * 8 + 6];
         ++n;
       }
     if (n)
-      fprintf(stderr, "[gemm<%d,%d>] M=%d N=%d K=%d BM=%d BN=%d S=%d nacc=%d ctas=%d: mma-thread %.0f cyc, "
-              "%.0f cyc/kblock, wait tempty %.1f%% full %.1f%%\n", AK, BK, p.M, p.N, p.K, p.BM, p.BN,
-              p.stages, p.nacc, n, tot / n, tot / (kb / n), 100 * wt / tot, 100 * wf / tot);
+      fprintf(stderr, "[gemm<%d,%d>] M=%d N=%d K=%d BM=%d BN=%d S=%d nacc=%d ctas=%d: mma-thread %.0f cyc "
+              "%.1f us (%.0f MHz), %.0f cyc/kblock, wait tempty %.1f%% full %.1f%%; epilogue busy %.0f "
+              "wait %.0f cyc\n", AK, BK, p.M, p.N, p.K, p.BM, p.BN, p.stages, p.nacc, n, tot / n,
+              ns / n / 1e3, tot / ns * 1e3, tot / kb, 100 * wt / tot, 100 * wf / tot, eb / n, ew / n);
+    if (mprof == 2) {  // per-kblock issue-start deltas of CTA 0
+      fprintf(stderr, "  kblock deltas:");
+      for (int i = 1; i < 512 && hbuf[148 * 8 + i]; ++i)
+        fprintf(stderr, " %lld", (long long)(hbuf[148 * 8 + i] - hbuf[148 * 8 + i - 1]));
+      fprintf(stderr, "\n");
+    }
   }
   if (pr) {
     cudaEventRecord(rec.b, s);
@@ -1873,7 +2013,7 @@ static void shift_conv(const float* G, int Cp, int Hg, int Wg, int N, int base_s
   p.K = taps * Cgp;
   p.BN = pick_bn(rows);
   p.splits = 1;
-  p.BM = pick_bm(M, p.BN, true);
+  p.BM = pick_bm(M, p.BN, true, (rows + p.BN - 1) / p.BN * groups);
   const int KS = (Cgp % 64 == 0 && 3 * (p.BM + p.BN) * 64 * 4 <= 224 * 1024) ? 64 : 32;
   p.kstage = KS;
   p.Hp = Hg;
@@ -1932,7 +2072,7 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   p.epi = EPI_PIX; p.out = y; p.out2 = h->fuse_relu; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.n_valid = d.K;
-  p.BM = pick_bm(p.M, p.BN, true);
+  p.BM = pick_bm(p.M, p.BN, true, (d.K + p.BN - 1) / p.BN);
   CUtensorMap ta = map_im2col(xt, z.Csp, z.U, z.V, d.N, 0, 0, -(z.Th - 1), -(z.Tw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(ft, (uint64_t)taps * z.Csp, d.K, (uint64_t)taps * z.Csp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.K + p.BN - 1) / p.BN, 1, s);
@@ -1982,7 +2122,7 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   p.epi = EPI_S2D; p.out = dx; p.epi_OHW = z.U * z.V;
   p.s2d = z.s; p.s2d_U = z.U; p.s2d_H = d.H; p.s2d_W = d.W; p.s2d_C = d.C;
   p.acc = acc; p.n_valid = z.Cs;
-  p.BM = pick_bm(p.M, p.BN, true);
+  p.BM = pick_bm(p.M, p.BN, true, (z.Cs + p.BN - 1) / p.BN);
   CUtensorMap ta = map_im2col(dyt, Kp, z.U, z.V, d.N, -(z.Th - 1), -(z.Tw - 1), -(z.Th - 1),
                               -(z.Tw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kp, z.Cs, (uint64_t)taps * Kp, p.BN);
@@ -2149,7 +2289,7 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
   p.epi = EPI_PIX; p.out = y; p.out2 = h->fuse_relu; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.grp_col = Kg; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.acc = 0; p.n_valid = Kg;
-  p.BM = pick_bm(p.M, p.BN, true);
+  p.BM = pick_bm(p.M, p.BN, true, (Kg + p.BN - 1) / p.BN * d.groups);
   if (on_grid) p.pt = p.pl = 0;
   CUtensorMap ta = on_grid ? map_im2col(xt, Cp, Hg, Wg, d.N, 0, 0, -(d.fh - 1), -(d.fw - 1), 1,
                                         1, p.BM)
@@ -2263,7 +2403,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   p.epi = EPI_PIX; p.out = dx; p.ld = (int64_t)d.H * d.W;
   p.img_stride = (int64_t)d.C * d.H * d.W; p.grp_col = d.Cg; p.epi_OHW = d.H * d.W;
   p.bias = nullptr; p.relu = 0; p.acc = acc; p.n_valid = d.Cg;
-  p.BM = pick_bm(p.M, p.BN, true);
+  p.BM = pick_bm(p.M, p.BN, true, (d.Cg + p.BN - 1) / p.BN * d.groups);
   CUtensorMap ta = map_im2col(dyt, Kp, Hg, Wg, d.N, -qt, -ql, d.H - Hg - qt, d.W - Wg - ql, 1, 1,
                               p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kgp, d.C, (uint64_t)taps * Kgp, p.BN);

@@ -11,8 +11,15 @@ LAYERS = {
     "conv4": ((13, 13, 384), (3, 3, 192, 384), (1, 1, 1, 1, 1, 1, 2)),
     "conv5": ((13, 13, 384), (3, 3, 192, 256), (1, 1, 1, 1, 1, 1, 2)),
 }
+import argparse
+ap = argparse.ArgumentParser()
+ap.add_argument("--only", default="")
+ap.add_argument("--fwd-only", action="store_true")
+a = ap.parse_args()
 hd = B.handle()
 for name, ((H, W, C), fs, g) in LAYERS.items():
+    if a.only and name != a.only:
+        continue
     x = B.from_hwcn((H, W, C, 256)).uniform_(-1, 1)
     f = B.from_hwcn(fs).uniform_(-0.1, 0.1)
     geom = B.ConvGeom(*g)
@@ -21,12 +28,14 @@ for name, ((H, W, C), fs, g) in LAYERS.items():
     dx, df = torch.empty_like(x), torch.empty_like(f)
     for _ in range(2):
         B.conv_forward(x, f, None, geom)
-        B.conv_backward(x, f, geom, dy, out=(dx, df, None))
+        if not a.fwd_only:
+            B.conv_backward(x, f, geom, dy, out=(dx, df, None))
     torch.cuda.synchronize()
     hd.kernel_profiling(True)
     for _ in range(3):
         B.conv_forward(x, f, None, geom)
-        B.conv_backward(x, f, geom, dy, out=(dx, df, None))
+        if not a.fwd_only:
+            B.conv_backward(x, f, geom, dy, out=(dx, df, None))
     torch.cuda.synchronize()
     prof = hd.kernel_profile()
     hd.kernel_profiling(False)
