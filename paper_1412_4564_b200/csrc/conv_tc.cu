@@ -425,7 +425,9 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
   const bool partial = p.splits > 1;
   if (partial) out += (int64_t)T.split * p.split_stride;
   // plain stores: split-K partials, or no bias / relu / accumulate
-  const bool plain = partial || (!p.bias && !p.relu && !p.acc && !p.out2);
+  // per-column (EPI_PIX) bias is added to the TMEM values before the stores
+  const bool col_bias = p.bias && !partial && p.epi == EPI_PIX;
+  const bool plain = partial || ((!p.bias || col_bias) && !p.relu && !p.acc && !p.out2);
   const int64_t ld = p.ld;
   for (int h = 0; h < halves; ++h) {
     int m = T.m0 + h * 128 + q * 32 + lane;
@@ -458,14 +460,21 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
     for (int c0 = 32 * cpart; c0 < p.BN; c0 += 32 * cparts) {
       uint32_t r[32];
       const uint32_t taddr = tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * p.BN + c0);
+      const int col0 = T.n0 + c0;
+      // columns of this chunk inside both the tile and the matrix
+      const int lim = min(min(32, p.BN - c0), p.n_valid - col0);
+      // per-column bias: one coalesced load per chunk (lane j holds column j),
+      // issued before the TMEM load so its latency overlaps; broadcast by shuffle
+      const float lane_bias = col_bias && lane < lim ? __ldg(p.bias + col0 + T.grp * p.grp_col + lane) : 0.f;
       CK_LD32(r, taddr);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (empty_split)
 #pragma unroll
         for (int j = 0; j < 32; ++j) r[j] = 0u;
-      const int col0 = T.n0 + c0;
-      // columns of this chunk inside both the tile and the matrix
-      const int lim = min(min(32, p.BN - c0), p.n_valid - col0);
+      if (col_bias)  // warp-uniform: every lane shuffles
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          r[j] = __float_as_uint(__fadd_rn(__uint_as_float(r[j]), __shfl_sync(0xffffffffu, lane_bias, j)));
       if (row_ok && lim > 0 && p.epi == EPI_S2D) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {  // static r[] indexing: keeps r in registers
@@ -489,13 +498,12 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
           for (int j = 0; j < 32; ++j)
             if (j < lim) dst[j * ld] = __uint_as_float(r[j]);
         } else {
-          const float* bcol = p.bias ? p.bias + col0 + T.grp * p.grp_col : nullptr;
           float* dst2 = p.out2 ? p.out2 + row_base + (int64_t)col0 * ld : nullptr;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (j < lim) {
               float v = __uint_as_float(r[j]);
-              if (p.bias) v = __fadd_rn(v, p.epi == EPI_PIX ? __ldg(bcol + j) : rbias);
+              if (p.bias && !col_bias) v = __fadd_rn(v, rbias);
               if (p.relu) v = v > 0.f ? v : 0.f;
               if (p.acc) v = __fadd_rn(dst[j * ld], v);
               dst[j * ld] = v;
