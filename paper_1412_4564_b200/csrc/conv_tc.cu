@@ -1073,54 +1073,66 @@ __global__ void __launch_bounds__(kThreads, 1)
 // the relu backward, activation.cpp:14-22, bit-exact with relu_bwd_v4) and the
 // gated HWCN value is also stored to gout: the conv backward consumes the
 // relu backward in the same pass over memory.
-__global__ void to_grid_pm_k(const float* __restrict__ x, float* __restrict__ xg, int H, int W,
-                             int C, int Cg, int Cgp, int groups, int Hg, int Wg, int oh, int ow,
-                             double* __restrict__ bpart, const float* __restrict__ gate,
-                             float* __restrict__ gout) {
-  // tile: 64 grid pixels x 32 padded channels; loads coalesced along pixels
-  // (two per channel row per thread), stores as float4 along channels.
-  __shared__ float tile[32][65];
+template <int CH, bool GATE>
+__global__ void __launch_bounds__(256, CH == 32 ? 8 : 4) to_grid_pm_k(
+    const float* __restrict__ x, float* __restrict__ xg, int H, int W, int C, int Cg, int Cgp,
+    int groups, int Hg, int Wg, int oh, int ow, double* __restrict__ bpart,
+    const float* __restrict__ gate, float* __restrict__ gout) {
+  // tile: 64 grid pixels x CH padded channels; loads coalesced along pixels
+  // (two per channel row per thread, CH/8 rows per warp), stores as float4
+  // along channels.  Every load of the tile (and of the relu gate) is issued
+  // before any is consumed: the kernel is bound by bytes in flight.
+  constexpr int RR = CH / 8;
+  __shared__ float tile[CH][65];
   const int n = blockIdx.z;
-  const int p0 = blockIdx.x * 64, c0 = blockIdx.y * 32;
-  const int Cp = Cgp * groups, HWg = Hg * Wg;
+  const int p0 = blockIdx.x * 64, c0 = blockIdx.y * CH;
+  const int Cp = Cgp * groups, HWg = Hg * Wg, HW = H * W;
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-  int64_t src[2];
+  int src[2];
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int P = p0 + lane + 32 * k;
     const int jj = P / Hg, ii = P - jj * Hg;
     const int i = ii - oh, j = jj - ow;
-    src[k] = (P < HWg && i >= 0 && i < H && j >= 0 && j < W) ? (int64_t)j * H + i : -1;
+    src[k] = (P < HWg && i >= 0 && i < H && j >= 0 && j < W) ? j * H + i : -1;
   }
-  const float* xn = x + (int64_t)n * C * H * W;
-  // all eight loads first (independent, in flight together), then the tile
-  float v[4][2];
+  const int64_t img = (int64_t)n * C * HW;
+  const float* xn = x + img;
+  const float* gn = GATE ? gate + img : nullptr;
+  float v[RR][2], gv[RR][2];
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr) {
+  for (int rr = 0; rr < RR; ++rr) {
     const int cp = c0 + warp + 8 * rr;
     const int g = cp / Cgp, cl = cp - g * Cgp;
-    const bool ch_ok = cp < Cp && cl < Cg;
-    const float* xc = xn + (int64_t)(g * Cg + cl) * H * W;
+    const int coff = (cp < Cp && cl < Cg) ? (g * Cg + cl) * HW : -1;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) v[rr][k] = (ch_ok && src[k] >= 0) ? __ldg(xc + src[k]) : 0.f;
-    if (gate) {
-      const int64_t off = (int64_t)n * C * H * W + (int64_t)(g * Cg + cl) * H * W;
+    for (int k = 0; k < 2; ++k) {
+      const bool e = coff >= 0 && src[k] >= 0;
+      v[rr][k] = e ? __ldg(xn + coff + src[k]) : 0.f;
+      if (GATE) gv[rr][k] = e ? __ldg(gn + coff + src[k]) : 0.f;
+    }
+  }
+  if (GATE) {
+    float* go = gout + img;
 #pragma unroll
-      for (int k = 0; k < 2; ++k)
-        if (ch_ok && src[k] >= 0) {
-          const float gv = __ldg(gate + off + src[k]) > 0.f ? v[rr][k] : 0.f;
-          v[rr][k] = gv;
-          gout[off + src[k]] = gv;
-        }
+    for (int rr = 0; rr < RR; ++rr) {
+      const int cp = c0 + warp + 8 * rr;
+      const int g = cp / Cgp, cl = cp - g * Cgp;
+      const int coff = (cp < Cp && cl < Cg) ? (g * Cg + cl) * HW : -1;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        v[rr][k] = gv[rr][k] > 0.f ? v[rr][k] : 0.f;
+        if (coff >= 0 && src[k] >= 0) go[coff + src[k]] = v[rr][k];
+      }
     }
   }
 #pragma unroll
-  for (int rr = 0; rr < 4; ++rr)
+  for (int rr = 0; rr < RR; ++rr)
 #pragma unroll
     for (int k = 0; k < 2; ++k) tile[warp + 8 * rr][lane + 32 * k] = v[rr][k];
   if (bpart) {  // fused bias gradient: this tile's per-channel sums (double, fixed order)
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) {
+    for (int rr = 0; rr < RR; ++rr) {
       const int cp = c0 + warp + 8 * rr;
       double t = (double)v[rr][0] + (double)v[rr][1];
       for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -1128,16 +1140,42 @@ __global__ void to_grid_pm_k(const float* __restrict__ x, float* __restrict__ xg
     }
   }
   __syncthreads();
+  constexpr int Q = CH / 4;  // float4 per pixel row of the tile
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < CH / 16; ++k) {
     const int idx = threadIdx.x + 256 * k;
-    const int pr = idx / 8, q = idx % 8;
+    const int pr = idx / Q, q = idx % Q;
     const int P = p0 + pr, cp = c0 + 4 * q;
     if (P < HWg && cp < Cp) {
-      const float4 v = make_float4(tile[4 * q][pr], tile[4 * q + 1][pr], tile[4 * q + 2][pr],
+      const float4 w = make_float4(tile[4 * q][pr], tile[4 * q + 1][pr], tile[4 * q + 2][pr],
                                    tile[4 * q + 3][pr]);
-      *reinterpret_cast<float4*>(xg + ((int64_t)n * HWg + P) * Cp + cp) = v;
+      *reinterpret_cast<float4*>(xg + ((int64_t)n * HWg + P) * Cp + cp) = w;
     }
+  }
+}
+
+// launch of to_grid_pm_k: 64-channel tiles when the padded channels allow
+static void grid_pm_launch(const float* x, float* xg, int H, int W, int C, int N, int Cg, int Cgp,
+                           int groups, int Hg, int Wg, int oh, int ow, double* bpart,
+                           const float* gate, float* gout, cudaStream_t s) {
+  const int Cp = Cgp * groups;
+  static const int ch = getenv("CK_GRID_CH") ? atoi(getenv("CK_GRID_CH")) : 32;  // experiments
+  if (ch == 64 && Cp % 64 == 0) {
+    dim3 grid((Hg * Wg + 63) / 64, Cp / 64, N);
+    if (gate)
+      to_grid_pm_k<64, true><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
+                                                  bpart, gate, gout);
+    else
+      to_grid_pm_k<64, false><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
+                                                   bpart, gate, gout);
+  } else {
+    dim3 grid((Hg * Wg + 63) / 64, (Cp + 31) / 32, N);
+    if (gate)
+      to_grid_pm_k<32, true><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
+                                                  bpart, gate, gout);
+    else
+      to_grid_pm_k<32, false><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
+                                                   bpart, gate, gout);
   }
 }
 
@@ -1426,7 +1464,7 @@ static bool load_driver() {
 bool conv_tc_available() { return load_driver(); }
 
 struct TcState {
-  Workspace xt, ft, part, dyg, bpart;
+  Workspace xt, ft, part, dyg, bpart, s2dT;
   // dy on the padded grid (dyg) is shared by the grid wgrad and the im2col
   // dgrad of one ck_conv_backward call: cached by (source, geometry, call id)
   const float* dyg_src = nullptr;
@@ -1446,6 +1484,7 @@ void conv_tc_release(ck_handle* h) {
   h->tc->part.release();
   h->tc->dyg.release();
   h->tc->bpart.release();
+  h->tc->s2dT.release();
   delete h->tc;
   h->tc = nullptr;
 }
@@ -1651,10 +1690,8 @@ static void to_pm(const float* x, float* xt, int H, int W, int C, int N, int Cg,
 
 static void to_grid_pm(const float* x, float* xg, int H, int W, int C, int N, int Cg, int Cgp,
                        int groups, int Hg, int Wg, int oh, int ow, cudaStream_t s) {
-  dim3 grid((Hg * Wg + 63) / 64, (Cgp * groups + 31) / 32, N);
   count_launch();
-  to_grid_pm_k<<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow, nullptr,
-                                    nullptr, nullptr);
+  grid_pm_launch(x, xg, H, W, C, N, Cg, Cgp, groups, Hg, Wg, oh, ow, nullptr, nullptr, nullptr, s);
 }
 
 static bool halo_enabled() {
@@ -1872,11 +1909,9 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
     double* bpart =
         (double*)grow(st->bpart, sizeof(double) * ((size_t)rows + chunks) * Cp, s);
     double* part2 = bpart + (size_t)rows * Cp;
-    dim3 grid(nb, (Cp + 31) / 32, d.N);
     count_launch(3);
-    to_grid_pm_k<<<grid, 256, 0, s>>>(relu_x ? relu_dy : dy, buf, d.OH, d.OW, d.K, Kg, Kgp,
-                                      groups, Hg, Wg, 0, 0, bpart, relu_x,
-                                      relu_x ? const_cast<float*>(dy) : nullptr);
+    grid_pm_launch(relu_x ? relu_dy : dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, Hg, Wg, 0,
+                   0, bpart, relu_x, relu_x ? const_cast<float*>(dy) : nullptr, s);
     grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(bpart, part2, Cp, rows);
     grid_bias_finish_k<<<(Cp + 127) / 128, 128, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
                                                         db_acc);
@@ -2086,6 +2121,47 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (d.K + p.BN - 1) / p.BN, 1, s);
 }
 
+// dx[n][c][j][i] (+)= T[((a + s*b) * C + c) * M + (n * V + v) * U + u] with
+// (i, j) = (s*u + a, s*v + b): the s2d dgrad result, written by the GEMM
+// epilogue column-major (coalesced along the s2d pixels), scattered back to
+// the HWCN image.  One block row per (n, c, j); along i each warp reads s
+// planes of 32/s consecutive u -- whole 32-byte sectors.
+__global__ void __launch_bounds__(256) s2d_unpack_k(const float* __restrict__ T,
+                                                    float* __restrict__ dx, int H, int W, int C,
+                                                    int s, int U, int V, int64_t M, int rows,
+                                                    int acc) {
+  constexpr int R = 8;  // image rows (n, c, j) per block, loads of all in flight together
+  // per-row source plane base (32-bit index math, once per block row)
+  __shared__ int64_t base[R];
+  if (threadIdx.x < R) {
+    const int row = blockIdx.x * R + threadIdx.x;  // (n * C + c) * W + j
+    if (row < rows) {
+      const int j = row % W, nc = row / W;
+      const int c = nc % C, n = nc / C;
+      const int v = j / s, b = j - v * s;
+      base[threadIdx.x] = (int64_t)(s * b * C + c) * M + ((int64_t)n * V + v) * U;
+    }
+  }
+  __syncthreads();
+  const int64_t plane = (int64_t)C * M;  // T stride of one sub-pixel row a
+  for (int i = threadIdx.x; i < H; i += blockDim.x) {
+    const int u = i / s, a = i - u * s;
+    const int64_t off = a * plane + u;
+    float val[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      val[r] = blockIdx.x * R + r < rows ? __ldg(T + base[r] + off) : 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = blockIdx.x * R + r;
+      if (row < rows) {
+        float* d = dx + (int64_t)row * H + i;
+        *d = acc ? __fadd_rn(*d, val[r]) : val[r];
+      }
+    }
+  }
+}
+
 static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, const ConvDims& d,
                       const S2D& z, int acc, cudaStream_t s) {
   TcState* st = state(h);
@@ -2123,18 +2199,23 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
                1, z.U, z.V, p, s);
     return;
   }
+  // GEMM over the s2d pixels into T[c'][m] (column-major, coalesced epilogue
+  // stores), then one pass scatters T back to the HWCN image
   GemmParams p{};
   p.M = d.N * z.U * z.V; p.N = z.Cs; p.K = taps * Kp; p.BN = pick_bn(z.Cs); p.splits = 1;
   p.OH = z.U; p.OW = z.V; p.sh = 1; p.sw = 1; p.pt = z.Th - 1; p.pl = z.Tw - 1; p.fh = z.Th;
   p.cchunks = Kp / 32;
-  p.epi = EPI_S2D; p.out = dx; p.epi_OHW = z.U * z.V;
-  p.s2d = z.s; p.s2d_U = z.U; p.s2d_H = d.H; p.s2d_W = d.W; p.s2d_C = d.C;
-  p.acc = acc; p.n_valid = z.Cs;
+  float* T = (float*)grow(st->s2dT, sizeof(float) * (size_t)p.M * z.Cs, s);
+  p.epi = EPI_LINEAR; p.out = T; p.ld = p.M; p.acc = 0; p.n_valid = z.Cs;
   p.BM = pick_bm(p.M, p.BN, true, (z.Cs + p.BN - 1) / p.BN);
   CUtensorMap ta = map_im2col(dyt, Kp, z.U, z.V, d.N, -(z.Th - 1), -(z.Tw - 1), -(z.Th - 1),
                               -(z.Tw - 1), 1, 1, p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kp, z.Cs, (uint64_t)taps * Kp, p.BN);
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (z.Cs + p.BN - 1) / p.BN, 1, s);
+  count_launch();
+  const int rows = d.N * d.C * d.W;
+  s2d_unpack_k<<<(rows + 7) / 8, d.H <= 128 ? 128 : 256, 0, s>>>(T, dx, d.H, d.W, d.C, z.s, z.U,
+                                                                z.V, (int64_t)p.M, rows, acc);
 }
 
 static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, cudaStream_t s);
