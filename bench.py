@@ -330,10 +330,17 @@ def main():
     except OSError:
         pass
     bf16 = peaks.get("bf16_tflops_sustained") or 1400.0
-    tf32_peak = bf16 / 2.0 if args.math == "tf32" else 74.0
-    peak_src = ("0.5 x MEASURED_PEAKS.json bf16_tflops_sustained (TF32 = half the bf16 rate; "
-                "sustained: the kernel runs inside a long step)" if args.math == "tf32" else
-                "FP32 FFMA nominal 148 SM x 128 x 2 x 1.965 GHz")
+    tf32_peak, peak_src = bf16 / 2.0, ("0.5 x MEASURED_PEAKS.json bf16_tflops_sustained "
+                                       "(TF32 = half the bf16 rate)")
+    try:  # measured full-chip TF32 MMA rate (tools/shift_probe.cu full), sustained
+        tp = json.load(open(os.path.join(ROOT, "profiles", "tf32_peak.json")))
+        tf32_peak = tp["tf32_tflops_sustained"]
+        peak_src = ("profiles/tf32_peak.json tf32_tflops_sustained: measured full-chip "
+                    "tcgen05.mma.kind::tf32 stream, sustained (the kernel runs inside a long step)")
+    except (OSError, ValueError, KeyError):
+        pass
+    if args.math != "tf32":
+        tf32_peak, peak_src = 74.0, "FP32 FFMA nominal 148 SM x 128 x 2 x 1.965 GHz"
     if kprof:
         # dominant kernel = the GEMM launch with the largest time in the step
         lab, kms, kfl = max(kprof, key=lambda r: r[1])

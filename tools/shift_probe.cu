@@ -340,8 +340,8 @@ __global__ void mma_full(long long* out, int iters, int rnd) {
 }
 
 template <int NT, int MODE = 0, int R = 4, int P = 4>
-static void run_full(int rnd, int ctas, int big = 0) {
-  const int S = 4, iters = 400000;
+static void run_full(int rnd, int ctas, int big = 0, int iters = 400000) {
+  const int S = 4;
   const int smem = big ? 225 * 1024 : S * (16384 + NT * 128) + 2048;
   long long* d; cudaMalloc(&d, 1001 * 8);
   cudaFuncSetAttribute(mma_full<NT, S, MODE, R, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -371,7 +371,12 @@ static long long run_stream(long long* d) {
 
 int main(int argc, char** argv) {
   if (argc > 1) {
-    run_full<192, 12>(1, 1); run_full<192, 12>(1, 1, 1); run_full<192, 12>(1, 148, 1);
+    // full-chip TF32 peak: every SM streams back-to-back M=128 K=8 MMAs over
+    // random operands (the roofline denominator of bench.py)
+    run_full<256>(1, 148); run_full<192>(1, 148); run_full<128>(1, 148);
+    run_full<192, 9>(1, 148);  // with the GEMM's stage-ring handshake
+    // sustained: ~3 s of back-to-back launches (power/clock steady state)
+    for (int r = 0; r < 10; ++r) run_full<192, 9>(1, 148, 0, 4000000);
     return 0;
   }
   {
