@@ -1927,6 +1927,19 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
 // x on its zero-padded grid (Hg x Wg, x at (pt, pl)), pixel-major: the fprop
 // im2col input and the wgrad B operand.  Inside a graph step the engine's
 // per-layer ConvCache carries it from the forward to the weight gradient.
+// Padded pixel-major grid of a stride-1 conv: x at (pt, pl) of an Hg x Wg
+// image grid.  Adjacent columns share their zero halo (bottom pad of column j
+// = top pad of column j+1; right pad of image n = left pad of image n+1), so
+// Hg = H + max(pt, pb), Wg = W + max(pl, pr): every shifted read of x stays
+// on zeros or in TMA zero fill, and the dy grid (dy at (0, 0), OH <= Hg) has
+// fewer junk rows for the weight-gradient reduction.
+static void grid_dims(const ConvDims& d, int& Hg, int& Wg) {
+  const bool shared = std::min(d.pt, d.pb) < d.fh && std::min(d.pl, d.pr) < d.fw &&
+                      !getenv("CK_TC_FULLGRID");
+  Hg = d.H + (shared ? std::max(d.pt, d.pb) : d.pt + d.pb);
+  Wg = d.W + (shared ? std::max(d.pl, d.pr) : d.pl + d.pr);
+}
+
 static float* x_grid(ck_handle* h, const float* x, const ConvDims& d, int Cgp, int Hg, int Wg,
                      cudaStream_t s) {
   ConvCache* c = h->conv_cache;
@@ -2335,7 +2348,8 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
   count_launch();
   repack_fprop_k<<<std::min<int64_t>(((int64_t)d.K * taps * Cgp + 255) / 256, 148 * 8), 256, 0, s>>>(
       f, ft, d.fh, d.fw, d.Cg, Cgp, d.K, d.fsc, d.fsk);
-  const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
+  int Hg, Wg;
+  grid_dims(d, Hg, Wg);
   if (d.sh == 1 && d.sw == 1 && halo_ok(Kg, d.fh, d.fw, Hg)) {
     // halo kernel over the zero-padded pixel-major grid (Hg x Wg per image)
     float* xg = (float*)grow(st->xt, sizeof(float) * (size_t)d.N * Hg * Wg * Cp, s);
@@ -2380,7 +2394,11 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
   p.bias = bias; p.relu = relu; p.acc = 0; p.n_valid = Kg;
   p.BM = pick_bm(p.M, p.BN, true, (Kg + p.BN - 1) / p.BN * d.groups);
   if (on_grid) p.pt = p.pl = 0;
-  CUtensorMap ta = on_grid ? map_im2col(xt, Cp, Hg, Wg, d.N, 0, 0, -(d.fh - 1), -(d.fw - 1), 1,
+  // on the grid the output extent is (H + pt + pb) - fh + 1 whatever the grid
+  // pitch: rows read past a shared-halo grid's column end are TMA zero fill
+  CUtensorMap ta = on_grid ? map_im2col(xt, Cp, Hg, Wg, d.N, 0, 0,
+                                        (d.H + d.pt + d.pb - Hg) - (d.fh - 1),
+                                        (d.W + d.pl + d.pr - Wg) - (d.fw - 1), 1,
                                         1, p.BM)
                            : map_im2col(xt, Cp, d.H, d.W, d.N, -d.pt, -d.pl, d.pb - (d.fh - 1),
                                         d.pr - (d.fw - 1), d.sh, d.sw, p.BM);
@@ -2467,7 +2485,8 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   // dy on the wgrad's zero grid (Hg x Wg, dy at (0, 0); shared within the
   // call): the negative im2col corners supply the top/left padding, the grid's
   // zero rows the bottom/right
-  const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
+  int Hg, Wg;
+  grid_dims(d, Hg, Wg);
   float* dyt = dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s);
   if (shift_enabled()) {
     // dx (i, j) at grid row i + Hg*j reads dy rows shifted by fi - qt + Hg*(fj - ql)
@@ -2510,7 +2529,8 @@ bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, i
   const int Kg = d.Kg();
   if (d.sh == 1 && d.sw == 1) {
     if (d.Cg < 16 || Kg < 16) return false;
-    const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
+    int Hg, Wg;
+    grid_dims(d, Hg, Wg);
     dy_grid(h, dy, d, Kg, rup(Kg, 32), d.groups, Hg, Wg, s, db, acc, relu_x, relu_dy);
     return true;
   }
@@ -2557,7 +2577,8 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   const int Cgp = rup(d.Cg, 32), Cp = Cgp * d.groups;
   const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
   const int taps = d.fh * d.fw;
-  const int Hg = d.H + d.pt + d.pb, Wg = d.W + d.pl + d.pr;
+  int Hg, Wg;
+  grid_dims(d, Hg, Wg);
   float* xg = x_grid(h, x, d, Cgp, Hg, Wg, s);
   float* dyg = dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s);
   float* part;
