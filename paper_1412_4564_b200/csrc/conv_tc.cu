@@ -96,6 +96,8 @@ struct GemmParams {
   int b_grp_row;          // halo kernel: per-group filter row offset
   int s2d, s2d_U, s2d_H, s2d_W, s2d_C;  // EPI_S2D: factor, grid height, target dims
   int exp;                // debug experiments (CK_TC_EXP)
+  int last_k;             // OP_IM2COL_K: K=8 MMAs needed in a tap's last 32-channel chunk
+                          // (1..4; the rest of the chunk is channel padding = zeros)
   int BM;                 // 128 or 256 (two M=128 MMAs sharing the B tile)
   int nacc;               // TMEM accumulator buffers (2: epilogue overlaps mainloop)
   int groups;             // tiles = ceil(M/BM) * ceil(N/BN) * groups * splits
@@ -345,6 +347,37 @@ __device__ __forceinline__ void mma4_elect(uint32_t d, uint64_t a, uint32_t aste
       "l"(a), "l"(b), "r"(idesc), "r"(astep), "r"(bstep), "r"(acc));
 }
 
+// As mma4_elect, but only the first n (1..4) of the four MMAs: a tap's last
+// channel chunk whose tail is zero padding skips the all-zero K steps.
+__device__ __forceinline__ void mma4n_elect(uint32_t d, uint64_t a, uint32_t astep, uint64_t b,
+                                            uint32_t bstep, uint32_t idesc, uint32_t acc,
+                                            uint32_t n) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e, p, t, e1, e2, e3;\n"
+      ".reg .b64 a1, a2, a3, b1, b2, b3, sa, sb;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "setp.ne.b32 t, %3, 0;\n"
+      "setp.gt.and.u32 e1, %7, 1, e;\n"
+      "setp.gt.and.u32 e2, %7, 2, e;\n"
+      "setp.gt.and.u32 e3, %7, 3, e;\n"
+      "cvt.u64.u32 sa, %4;\n"
+      "cvt.u64.u32 sb, %5;\n"
+      "add.s64 a1, %1, sa;\n"
+      "add.s64 b1, %2, sb;\n"
+      "add.s64 a2, a1, sa;\n"
+      "add.s64 b2, b1, sb;\n"
+      "add.s64 a3, a2, sa;\n"
+      "add.s64 b3, b2, sb;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "@e1 tcgen05.mma.cta_group::1.kind::tf32 [%0], a1, b1, %3, t;\n"
+      "@e2 tcgen05.mma.cta_group::1.kind::tf32 [%0], a2, b2, %3, t;\n"
+      "@e3 tcgen05.mma.cta_group::1.kind::tf32 [%0], a3, b3, %3, t;\n"
+      "}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(astep), "r"(bstep), "r"(acc), "r"(n));
+}
+
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n"
@@ -525,12 +558,13 @@ struct Ring {
   int s;
   uint32_t ph;
 };
-template <int NG>
+template <int NG, bool SKIP>
 __device__ __forceinline__ void mma_tile(uint64_t* full, uint64_t* empty, int S, Ring& r, int nkb,
                                          uint32_t dcol, uint64_t da0, uint64_t db0, uint32_t sa16,
                                          uint32_t sb16, uint32_t ak, uint32_t bk, const uint32_t* ga,
                                          const uint32_t* gb, const uint32_t* gd, uint32_t first_mask,
-                                         uint32_t idesc, bool wait_full, bool do_mma) {
+                                         uint32_t idesc, bool wait_full, bool do_mma, int cc,
+                                         int cchunks, uint32_t last_k) {
   uint32_t oa[NG], ob[NG], od[NG];
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
@@ -543,11 +577,19 @@ __device__ __forceinline__ void mma_tile(uint64_t* full, uint64_t* empty, int S,
     tc_fence_after();
     const uint64_t da = da0 + (uint64_t)(r.s * sa16), db = db0 + (uint64_t)(r.s * sb16);
     if (do_mma) {
+      if (SKIP && cc == cchunks - 1) {  // tap's last chunk: skip the zero-padded K steps
 #pragma unroll
-      for (int g = 0; g < NG; ++g)
-        mma4_elect(od[g], da + oa[g], ak, db + ob[g], bk, idesc,
-                   (i > 0 || !((first_mask >> g) & 1)) ? 1u : 0u);
+        for (int g = 0; g < NG; ++g)
+          mma4n_elect(od[g], da + oa[g], ak, db + ob[g], bk, idesc,
+                      (i > 0 || !((first_mask >> g) & 1)) ? 1u : 0u, last_k);
+      } else {
+#pragma unroll
+        for (int g = 0; g < NG; ++g)
+          mma4_elect(od[g], da + oa[g], ak, db + ob[g], bk, idesc,
+                     (i > 0 || !((first_mask >> g) & 1)) ? 1u : 0u);
+      }
     }
+    if (SKIP && ++cc == cchunks) cc = 0;
     mma_commit_elect(&empty[r.s]);
     if (++r.s == S) {
       r.s = 0;
@@ -781,15 +823,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t dcol = tmem + (uint32_t)(ab * acc_cols);
         const int nkb = T.kb1 - T.kb0;
-        if (ng == 1)
-          mma_tile<1>(full, empty, S, ring, nkb, dcol, da0, db0, sa16, sb16, ak, bk, ga, gb, gd,
-                      first_mask, idesc, wait_full, do_mma);
-        else if (ng == 2)
-          mma_tile<2>(full, empty, S, ring, nkb, dcol, da0, db0, sa16, sb16, ak, bk, ga, gb, gd,
-                      first_mask, idesc, wait_full, do_mma);
-        else
-          mma_tile<4>(full, empty, S, ring, nkb, dcol, da0, db0, sa16, sb16, ak, bk, ga, gb, gd,
-                      first_mask, idesc, wait_full, do_mma);
+        // padded-chunk skipping: im2col convs only (kb = tap * cchunks + cc, KS = 32)
+        const bool skip = AK == OP_IM2COL_K && KS == 32 && p.last_k >= 1 && p.last_k < 4;
+        const int cch = skip ? p.cchunks : 1 << 30;
+        const int cc0 = skip ? T.kb0 % p.cchunks : 0;
+        const uint32_t lk = skip ? (uint32_t)p.last_k : 4u;
+#define CK_MMA_TILE(NG, SK)                                                                   \
+  mma_tile<NG, SK>(full, empty, S, ring, nkb, dcol, da0, db0, sa16, sb16, ak, bk, ga, gb, gd,   \
+                   first_mask, idesc, wait_full, do_mma, cc0, cch, lk)
+        if (skip) {
+          if (ng == 1) CK_MMA_TILE(1, true);
+          else CK_MMA_TILE(2, true);
+        } else if (ng == 1) {
+          CK_MMA_TILE(1, false);
+        } else if (ng == 2) {
+          CK_MMA_TILE(2, false);
+        } else {
+          CK_MMA_TILE(4, false);
+        }
+#undef CK_MMA_TILE
         it += nkb;
         mma_commit_elect(&tfull[ab]);
       }
@@ -2125,6 +2177,7 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   p.M = d.N * d.OH * d.OW; p.N = d.K; p.K = taps * z.Csp; p.BN = pick_bn(d.K); p.splits = 1;
   p.OH = d.OH; p.OW = d.OW; p.sh = 1; p.sw = 1; p.pt = 0; p.pl = 0; p.fh = z.Th;
   p.cchunks = z.Csp / 32;
+  p.last_k = z.Cs % 32 ? (z.Cs % 32 + 7) / 8 : 4;
   p.epi = EPI_PIX; p.out = y; p.out2 = h->fuse_relu; p.ld = (int64_t)d.OH * d.OW;
   p.img_stride = (int64_t)d.K * d.OH * d.OW; p.epi_OHW = d.OH * d.OW;
   p.bias = bias; p.relu = relu; p.n_valid = d.K;
@@ -2387,6 +2440,7 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
   p.splits = 1;
   p.OH = d.OH; p.OW = d.OW; p.sh = d.sh; p.sw = d.sw; p.pt = d.pt; p.pl = d.pl; p.fh = d.fh;
   p.cchunks = Cgp / 32;
+  p.last_k = d.Cg % 32 ? (d.Cg % 32 + 7) / 8 : 4;
   p.a_grp_c = Cgp;
   p.b_grp_mn = Kg;
   p.epi = EPI_PIX; p.out = y; p.out2 = h->fuse_relu; p.ld = (int64_t)d.OH * d.OW;
@@ -2506,6 +2560,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   p.splits = 1;
   p.OH = d.H; p.OW = d.W; p.sh = 1; p.sw = 1; p.pt = qt; p.pl = ql; p.fh = d.fh;
   p.cchunks = Kgp / 32;
+  p.last_k = Kg % 32 ? (Kg % 32 + 7) / 8 : 4;
   p.a_grp_c = Kgp;
   p.b_grp_mn = d.Cg;
   p.epi = EPI_PIX; p.out = dx; p.ld = (int64_t)d.H * d.W;
