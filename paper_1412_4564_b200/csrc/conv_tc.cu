@@ -1366,7 +1366,20 @@ __device__ __forceinline__ void s2d_stage_strip(const float* __restrict__ x, flo
     const float* col = x + (((int64_t)n * C + c_first + cc) * W + j) * H;
     float* dst = strip + (int64_t)cj * Hs;
     const bool jok = j < W;
-    for (int i = lane; i < Hs; i += 32) dst[i] = (jok && i < H) ? __ldg(col + i) : 0.f;
+    // eight loads in flight per lane before any store (the loop is latency-bound otherwise)
+    for (int i0 = 0; i0 < Hs; i0 += 256) {
+      float r[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + lane + 32 * k;
+        r[k] = (jok && i < H) ? __ldg(col + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int i = i0 + lane + 32 * k;
+        if (i < Hs) dst[i] = r[k];
+      }
+    }
   }
 }
 
