@@ -96,6 +96,7 @@ struct GemmParams {
   int b_grp_row;          // halo kernel: per-group filter row offset
   int s2d, s2d_U, s2d_H, s2d_W, s2d_C;  // EPI_S2D: factor, grid height, target dims
   int exp;                // debug experiments (CK_TC_EXP)
+  int snake;              // epilogue: snake-order (half, chunk) units (CK_EPI_SNAKE=0 disables)
   int last_k;             // OP_IM2COL_K: K=8 MMAs needed in a tap's last 32-channel chunk
                           // (1..4; the rest of the chunk is channel padding = zeros)
   int BM;                 // 128 or 256 (two M=128 MMAs sharing the B tile)
@@ -462,7 +463,13 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
   const bool col_bias = p.bias && !partial && p.epi == EPI_PIX;
   const bool plain = partial || ((!p.bias || col_bias) && !p.relu && !p.acc && !p.out2);
   const int64_t ld = p.ld;
-  for (int h = 0; h < halves; ++h) {
+  // (half, 32-column chunk) units dealt to the cparts warps of a lane quarter
+  // in snake order (odd halves walk the chunks backwards): balanced when a
+  // half has an odd number of chunks (BN = 96) or a short last chunk (BN = 48)
+  const int nch = (p.BN + 31) / 32, units = halves * nch;
+  for (int u = cpart; u < units; u += cparts) {
+    const int h = u / nch, ci = u - h * nch;
+    const int c0 = 32 * ((h & 1) && p.snake ? nch - 1 - ci : ci);
     int m = T.m0 + h * 128 + q * 32 + lane;
     bool row_ok = m < p.M;
     int img = 0, pix = 0;
@@ -490,7 +497,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
       row_base = (int64_t)m + (int64_t)T.grp * p.grp_out;
       if (p.bias && !partial && row_ok) rbias = p.bias[m + T.grp * p.grp_col];
     }
-    for (int c0 = 32 * cpart; c0 < p.BN; c0 += 32 * cparts) {
+    {
       uint32_t r[32];
       const uint32_t taddr = tacc + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * p.BN + c0);
       const int col0 = T.n0 + c0;
@@ -1635,6 +1642,8 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
   (void)grid_n;
   static const int exp = getenv("CK_TC_EXP") ? atoi(getenv("CK_TC_EXP")) : 0;
   p.exp = exp;
+  static const int snake = getenv("CK_EPI_SNAKE") ? atoi(getenv("CK_EPI_SNAKE")) : 1;
+  p.snake = snake;
   if (p.BM != 128 && p.BM != 256) p.BM = 128;
   p.groups = grid_z / p.splits;
   const int halves = p.BM / 128;
