@@ -293,6 +293,15 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+__device__ __forceinline__ void mma_commit_mc_elect(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
                    : "memory");
@@ -1036,63 +1045,58 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer --
-    if (lane == 0) {
+    // warp-converged; one elected lane issues four MMAs per asm block
+    // (mma4_elect), descriptors advanced by adds, division-free rings
+    {
       const uint32_t idesc = idesc_tf32(p.BN, 0, 0);
-      int ia = 0, ib = 0, tc = 0;
-      unsigned long long w_t = 0, w_a = 0, w_b = 0, t_start = clock64();
+      const uint64_t a_desc0 = sdesc(smem_u32(sA), 16, 1024, 2);
+      const uint64_t b_desc0 = sdesc(smem_u32(sB), 16, 1024, 2);
+      int sa = 0, sb = 0, tc = 0;
+      uint32_t pha = 0, phb = 0;
       for (int t = cid; t < total; t += ncl, ++tc) {
         const int ab = tc % p.nacc;
-        unsigned long long c0 = clock64();
         mbar_wait(&tempty[ab], ((tc / p.nacc) & 1) ^ 1);
-        w_t += clock64() - c0;
         tc_fence_after();
         const uint32_t dcol = tmem + (uint32_t)(ab * acc_cols);
         for (int cc = 0; cc < chunks; ++cc) {
-          const int sa = ia % p.SA;
-          unsigned long long c1 = clock64();
-          mbar_wait(&fullA[sa], (ia / p.SA) & 1);
-          w_a += clock64() - c1;
+          mbar_wait(&fullA[sa], pha);
           tc_fence_after();
-          const uint32_t a = smem_u32(sA + sa * stage_a);
+          const uint64_t da = a_desc0 + (uint64_t)((sa * stage_a) >> 4);
+          int fi = 0, fj = 0;
           for (int tg = 0; tg < ntg; ++tg) {
-            const int sb = ib % p.SB;
-            unsigned long long c2 = clock64();
-            mbar_wait(&fullB[sb], (ib / p.SB) & 1);
-            w_b += clock64() - c2;
+            mbar_wait(&fullB[sb], phb);
             tc_fence_after();
-            const uint32_t b = smem_u32(sB + sb * stage_b);
+            const uint64_t db = b_desc0 + (uint64_t)((sb * stage_b) >> 4);
             for (int u = 0; u < p.TT; ++u) {
               const int tap = tg * p.TT + u;
               if (tap >= p.taps) break;
-              const int fj = tap / p.fh, fi = tap - fj * p.fh;
-              const uint32_t shift = (uint32_t)(fi + p.hg * fj) * 128u;
-              for (int h = 0; h < halves; ++h) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  const uint32_t acc = (cc > 0 || tap > 0 || k > 0) ? 1u : 0u;
-                  mma_tf32(dcol + h * p.BN,
-                           sdesc(a + (uint32_t)h * 16384u + shift + k * 32, 16, 1024),
-                           sdesc(b + (uint32_t)(u * p.BN * 128) + k * 32, 16, 1024), idesc, acc);
-                }
+              // the tap's A operand starts (fi + hg*fj) rows into the halo tile
+              const uint32_t shift16 = (uint32_t)(fi + p.hg * fj) * 8u;
+              const uint32_t acc = (cc > 0 || tap > 0) ? 1u : 0u;
+              for (int h = 0; h < halves; ++h)
+                mma4_elect(dcol + h * p.BN, da + (uint64_t)(h * 1024 + shift16), 2u,
+                           db + (uint64_t)(u * p.BN * 8), 2u, idesc, acc);
+              if (++fi == p.fh) {
+                fi = 0;
+                ++fj;
               }
             }
             if (CS > 1)
-              mma_commit_mc(&emptyB[sb], cmask);
+              mma_commit_mc_elect(&emptyB[sb], cmask);
             else
-              mma_commit(&emptyB[sb]);
-            ++ib;
+              mma_commit_elect(&emptyB[sb]);
+            if (++sb == p.SB) {
+              sb = 0;
+              phb ^= 1;
+            }
           }
-          mma_commit(&emptyA[sa]);
-          ++ia;
+          mma_commit_elect(&emptyA[sa]);
+          if (++sa == p.SA) {
+            sa = 0;
+            pha ^= 1;
+          }
         }
-        mma_commit(&tfull[ab]);
-      }
-      if (p.prof) {
-        unsigned long long* o = p.prof + blockIdx.x * 4;
-        o[0] = clock64() - t_start;
-        o[1] = w_t;
-        o[2] = w_a;
-        o[3] = w_b;
+        mma_commit_elect(&tfull[ab]);
       }
     }
     __syncwarp();
