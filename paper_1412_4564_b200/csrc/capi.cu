@@ -181,9 +181,16 @@ void conv_forward_dispatch(ck_handle* h, const float* x, const float* f, const f
   conv_fwd_fp32(x, f, bias, y, d, relu, s);
 }
 
+void materialize_pending_dy(ck_handle* h, const float* dy, cudaStream_t s) {
+  if (!h->pending_dy || h->pending_dy != dy) return;
+  relu_backward(h->pending_rx, h->pending_rdy, const_cast<float*>(dy), h->pending_n, 0, s);
+  h->pending_dy = nullptr;
+}
+
 void conv_dgrad_dispatch(ck_handle* h, const float* dy, const float* f, float* dx,
                          const ConvDims& d, int acc, ck_math math, cudaStream_t s) {
   if (math == CK_MATH_TF32 && conv_tc_dgrad(h, dy, f, dx, d, acc, s)) return;
+  materialize_pending_dy(h, dy, s);
   prof_drop();
   conv_dgrad_fp32(dy, f, dx, d, acc, s);
 }
@@ -191,6 +198,7 @@ void conv_dgrad_dispatch(ck_handle* h, const float* dy, const float* f, float* d
 void conv_wgrad_dispatch(ck_handle* h, const float* x, const float* dy, float* df,
                          const ConvDims& d, int acc, ck_math math, cudaStream_t s) {
   if (math == CK_MATH_TF32 && conv_tc_wgrad(h, x, dy, df, d, acc, s)) return;
+  materialize_pending_dy(h, dy, s);
   prof_drop();
   void* ws = h->ws.get(conv_wgrad_ws_bytes(d), s);
   if (!ws) throw Err(CK_ERR_CUDA, "workspace allocation failed");
@@ -365,13 +373,28 @@ ck_status ck_conv_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* f,
   // output derivative (inside the transform when the grid path runs).
   const float* rx = h->fuse_relu_x;
   const float* rdy = h->fuse_relu_dy;
+  // the engine may let the gated transform skip storing dy itself (only its
+  // grid form is consumed): dy is then left pending, computed by any reader
+  // that needs it, and reported back through fuse_relu_pending
+  const bool lazy = h->fuse_relu_lazy && rx;
+  h->fuse_relu_pending = false;
   bool gated = false;
   if (db && math == CK_MATH_TF32 && (dx || df) &&
-      conv_tc_bias(h, dy->data, db->data, d, accumulate, s, rx, rdy)) {
+      conv_tc_bias(h, dy->data, db->data, d, accumulate, s, rx, rdy, lazy)) {
     db = nullptr;
     gated = rx != nullptr;
   }
   if (rx && !gated) relu_backward(rx, rdy, dy->data, elems(dy->shape), 0, s);
+  if (gated && lazy) {
+    h->pending_dy = dy->data;
+    h->pending_rx = rx;
+    h->pending_rdy = rdy;
+    h->pending_n = elems(dy->shape);
+  }
+  struct PendingReset {
+    ck_handle* h;
+    ~PendingReset() { h->pending_dy = nullptr; }
+  } pending_reset{h};
   if (db) {
     void* bws = h->scratch.get(conv_bgrad_ws_bytes((int)ys.c, (int)ys.n, (int)(ys.h * ys.w)), s);
     if (!bws) throw Err(CK_ERR_CUDA, "workspace allocation failed");
@@ -379,6 +402,7 @@ ck_status ck_conv_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* f,
   }
   if (df) conv_wgrad_dispatch(h, x->data, dy->data, df->data, d, accumulate, math, s);
   if (dx) conv_dgrad_dispatch(h, dy->data, f->data, dx->data, d, accumulate, math, s);
+  h->fuse_relu_pending = h->pending_dy == dy->data;  // still unmaterialized
   after_launch();
   CK_API_END(h)
 }

@@ -31,6 +31,16 @@ struct ck_handle {
   // derivative) is relu_x > 0 ? relu_dy : 0, produced inside the call
   const float* fuse_relu_x = nullptr;
   const float* fuse_relu_dy = nullptr;
+  // engine: the conv output's derivative itself need not be stored (only its
+  // grid form is consumed); set by ck_conv_backward when it was left pending
+  bool fuse_relu_lazy = false;
+  bool fuse_relu_pending = false;
+  // a dy left unmaterialized by the gated transform: any later reader of dy
+  // (a cache miss, a fallback path) first computes it (materialize_pending_dy)
+  const float* pending_dy = nullptr;
+  const float* pending_rx = nullptr;
+  const float* pending_rdy = nullptr;
+  int64_t pending_n = 0;
   ck::KernelProfiler prof;
 };
 
@@ -87,7 +97,10 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
 bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, const ConvDims& d,
                    int acc, cudaStream_t s);
 bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, int acc,
-                  cudaStream_t s, const float* relu_x = nullptr, const float* relu_dy = nullptr);
+                  cudaStream_t s, const float* relu_x = nullptr, const float* relu_dy = nullptr,
+                  bool skip_gout = false);
+// capi.cu: compute a dy the gated transform left pending (h->pending_dy == dy)
+void materialize_pending_dy(ck_handle* h, const float* dy, cudaStream_t s);
 void conv_tc_release(ck_handle* h);
 
 }  // namespace ck

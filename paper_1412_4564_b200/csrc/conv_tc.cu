@@ -1176,7 +1176,7 @@ __global__ void __launch_bounds__(256, CH == 32 ? 8 : 4) to_grid_pm_k(
     }
   }
   if (GATE) {
-    float* go = gout + img;
+    float* go = gout ? gout + img : nullptr;
 #pragma unroll
     for (int rr = 0; rr < RR; ++rr) {
       const int cp = c0 + warp + 8 * rr;
@@ -1185,7 +1185,7 @@ __global__ void __launch_bounds__(256, CH == 32 ? 8 : 4) to_grid_pm_k(
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         v[rr][k] = gv[rr][k] > 0.f ? v[rr][k] : 0.f;
-        if (coff >= 0 && src[k] >= 0) go[coff + src[k]] = v[rr][k];
+        if (gout && coff >= 0 && src[k] >= 0) go[coff + src[k]] = v[rr][k];
       }
     }
   }
@@ -1975,12 +1975,13 @@ __global__ void grid_bias_finish_k(const double* __restrict__ part2, float* db, 
 static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, int Kgp,
                       int groups, int Hg, int Wg, cudaStream_t s, float* db = nullptr,
                       int db_acc = 0, const float* relu_x = nullptr,
-                      const float* relu_dy = nullptr) {
+                      const float* relu_dy = nullptr, bool skip_gout = false) {
   TcState* st = state(h);
   const int64_t key = ((((int64_t)Hg * 4099 + Wg) * 65537 + d.K) * 131071 + d.N) * 1031 +
                       Kgp * 17 + groups + ((int64_t)d.OH << 40) + ((int64_t)d.OW << 50);
   float* buf = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hg * Wg * Kgp * groups, s);
   if (!db && st->dyg_src == dy && st->dyg_call == h->call && st->dyg_key == key) return buf;
+  if (!relu_x) materialize_pending_dy(h, dy, s);  // rebuilding from dy: it must exist
   if (db) {
     const int Cp = Kgp * groups, nb = (Hg * Wg + 63) / 64;
     const int rows = d.N * nb, chunks = (rows + 8 * kBiasRowsPerWarp - 1) / (8 * kBiasRowsPerWarp);
@@ -1989,7 +1990,7 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
     double* part2 = bpart + (size_t)rows * Cp;
     count_launch(3);
     grid_pm_launch(relu_x ? relu_dy : dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, Hg, Wg, 0,
-                   0, bpart, relu_x, relu_x ? const_cast<float*>(dy) : nullptr, s);
+                   0, bpart, relu_x, relu_x && !skip_gout ? const_cast<float*>(dy) : nullptr, s);
     grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(bpart, part2, Cp, rows);
     grid_bias_finish_k<<<(Cp + 127) / 128, 128, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
                                                         db_acc);
@@ -2269,6 +2270,7 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
     // flipped bank, on a grid of pitch Hq; EPI_S2D scatters back to x.
     float* dyg = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hq * Wq * Kp, s);
     st->dyg_src = nullptr;
+    materialize_pending_dy(h, dy, s);  // this path reads dy itself
     to_grid_pm(dy, dyg, d.OH, d.OW, d.K, d.N, d.K, Kp, 1, Hq, Wq, z.Th - 1, z.Tw - 1, s);
     GemmParams p{};
     p.epi = EPI_S2D; p.out = dx;
@@ -2516,6 +2518,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.N; p.acc = acc;
     p.BM = pick_bm(p.M, p.BN);
     CUtensorMap ta = map_mn(f, d.K, Q, Q, p.BM, &p.a_mn3d);
+    materialize_pending_dy(h, dy, s);  // this path reads dy itself
     CUtensorMap tb = map_2d(dy, d.K, d.N, d.K, BN);  // dY as [n][k]
     if (splits > 1) {
       const int64_t per = (int64_t)Q * d.N;
@@ -2554,6 +2557,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     // convolved with the flipped bank; the valid rows are the H x W of dx.
     float* dyg = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hq * Wq * Kp, s);
     st->dyg_src = nullptr;
+    materialize_pending_dy(h, dy, s);  // this path reads dy itself
     to_grid_pm(dy, dyg, d.OH, d.OW, d.K, d.N, Kg, Kgp, d.groups, Hq, Wq, qt, ql, s);
     GemmParams p{};
     p.epi = EPI_PIX; p.out = dx; p.ld = (int64_t)d.H * d.W;
@@ -2605,19 +2609,19 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
 // the same ck_conv_backward call then reuse.  False when the shape does not
 // use the grid (FC layers, strided convs without space-to-depth).
 bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, int acc,
-                  cudaStream_t s, const float* relu_x, const float* relu_dy) {
+                  cudaStream_t s, const float* relu_x, const float* relu_dy, bool skip_gout) {
   if (!load_driver() || is_fc(d)) return false;
   const int Kg = d.Kg();
   if (d.sh == 1 && d.sw == 1) {
     if (d.Cg < 16 || Kg < 16) return false;
     int Hg, Wg;
     grid_dims(d, Hg, Wg);
-    dy_grid(h, dy, d, Kg, rup(Kg, 32), d.groups, Hg, Wg, s, db, acc, relu_x, relu_dy);
+    dy_grid(h, dy, d, Kg, rup(Kg, 32), d.groups, Hg, Wg, s, db, acc, relu_x, relu_dy, skip_gout);
     return true;
   }
   S2D z;
   if (!s2d_plan(d, z)) return false;
-  dy_grid(h, dy, d, d.K, rup(d.K, 32), 1, z.U, z.V, s, db, acc, relu_x, relu_dy);
+  dy_grid(h, dy, d, d.K, rup(d.K, 32), 1, z.U, z.V, s, db, acc, relu_x, relu_dy, skip_gout);
   return true;
 }
 
@@ -2639,6 +2643,7 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.K; p.acc = acc; p.out = df;
     p.BM = pick_bm(p.M, p.BN);
     CUtensorMap ta = map_mn(x, d.N, Q, Q, p.BM, &p.a_mn3d);
+    materialize_pending_dy(h, dy, s);  // this path reads dy itself
     CUtensorMap tb = map_mn(dy, d.N, d.K, d.K, BN, &p.b_mn3d);
     launch<OP_TILED_MN, OP_TILED_MN>(ta, tb, p, gm, gn, 1, s);
     return true;

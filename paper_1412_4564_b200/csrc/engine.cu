@@ -61,6 +61,10 @@ struct Var {
   float* value = nullptr;
   float* deriv = nullptr;
   bool deriv_live = false;  // received a contribution in this backward
+  // derivative left unmaterialized by a fused conv -> relu backward (only its
+  // grid form was consumed): deriv = value(lazy_gate) > 0 ? deriv(lazy_src) : 0,
+  // computed when the derivative is requested (ck_graph_var)
+  int lazy_gate = -1, lazy_src = -1;
 };
 
 struct Layer {
@@ -409,10 +413,13 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
       // separately when they differ.
       int a0 = acc(0), a1 = acc(1), a2 = l.in.size() > 2 ? acc(2) : a1;
       h->conv_cache = &l.cache;  // the forward's transformed input (valid this step)
-      if (l.relu_out >= 0 && g->layers[g->vars[l.relu_out].producer].bwd_deferred) {
-        // fused relu backward: this call derives dy from the relu output's derivative
+      const bool fused = l.relu_out >= 0 && g->layers[g->vars[l.relu_out].producer].bwd_deferred;
+      if (fused) {
+        // fused relu backward: this call derives dy from the relu output's derivative;
+        // dy itself (the conv output's derivative) may stay unmaterialized
         h->fuse_relu_x = g->vars[l.out[0]].value;
         h->fuse_relu_dy = g->vars[l.relu_out].deriv;
+        h->fuse_relu_lazy = true;
       }
       struct Reset {
         ck_handle* h;
@@ -420,11 +427,17 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
           h->conv_cache = nullptr;
           h->fuse_relu_x = nullptr;
           h->fuse_relu_dy = nullptr;
+          h->fuse_relu_lazy = false;
+          h->fuse_relu_pending = false;
         }
       } reset{h};
       if (a0 == a1 && a1 == a2) {
         st = ck_conv_backward(h, &x, &f, &cg, &dy, &dx, &df, l.in.size() > 2 ? &db : nullptr, a0,
                               g->math, s);
+        if (st == CK_OK && fused && h->fuse_relu_pending) {
+          g->vars[l.out[0]].lazy_gate = l.out[0];
+          g->vars[l.out[0]].lazy_src = l.relu_out;
+        }
       } else {
         st = ck_conv_backward(h, &x, &f, &cg, &dy, &dx, nullptr, nullptr, a0, g->math, s);
         if (st == CK_OK) st = ck_conv_backward(h, &x, &f, &cg, &dy, nullptr, &df, nullptr, a1, g->math, s);
@@ -535,7 +548,10 @@ struct LayerDone {
 
 // graph.cpp:548-598 backward with d(objective) = 1.
 static void run_backward(ck_graph* g, int objective, cudaStream_t s, LayerDone* cb) {
-  for (auto& v : g->vars) v.deriv_live = false;
+  for (auto& v : g->vars) {
+    v.deriv_live = false;
+    v.lazy_gate = v.lazy_src = -1;
+  }
   for (auto& l : g->layers) l.bwd_deferred = false;
   Var& obj = g->vars[objective];
   if (elems(obj.shape) != 1) throw Err(CK_ERR_ARG, "objective '" + obj.name + "' is not a scalar");
@@ -722,6 +738,16 @@ ck_status ck_graph_var(ck_graph* g, const char* name, int deriv, ck_tensor* out)
   if (!g->finalized) throw Err(CK_ERR_ARG, "graph not finalized");
   if (!out) throw Err(CK_ERR_ARG, "null output");
   Var& v = g->vars[g->var(name ? name : "")];
+  if (deriv && v.lazy_gate >= 0) {
+    // a fused conv -> relu backward left this derivative unmaterialized:
+    // relu backward (activation.cpp:14-22) of the relu output's derivative,
+    // gated by this var's own value (x > 0), now, in order with all prior work
+    check_cuda(cudaDeviceSynchronize(), "synchronize");
+    relu_backward(g->vars[v.lazy_gate].value, g->vars[v.lazy_src].deriv, v.deriv,
+                  elems(v.shape), 0, 0);
+    check_cuda(cudaDeviceSynchronize(), "synchronize");
+    v.lazy_gate = v.lazy_src = -1;
+  }
   *out = tv(v, deriv != 0);
   CKG_END(g)
 }

@@ -121,6 +121,24 @@ def test_alexnet_full_batch_properties():
     assert np.isfinite(g.get("conv1f", deriv=True)).all()
 
 
+def test_fused_conv_relu_derivative_materialized_on_request():
+    """A fused conv -> relu backward leaves the conv output's derivative
+    unstored (only its grid form feeds the GEMMs); requesting it computes the
+    relu backward (activation.cpp:14-22) exactly: d(conv) = conv > 0 ? d(relu) : 0."""
+    from paper_1412_4564_b200 import nets
+    net = nets.alexnet(batch=32)
+    g = device_graph(net, "tf32")
+    for k, v in {**net.init_params(), **net.init_inputs()}.items():
+        g.set(k, v)
+    for _ in range(2):  # the second backward must not see the first one's derivative
+        g.forward()
+        g.backward("objective")
+        for c, r in [("c1", "r1"), ("c2", "r2"), ("c3", "r3"), ("c4", "r4"), ("c5", "r5"),
+                     ("f6", "r6"), ("f7", "r7")]:
+            dc, cv, dr = g.get(c, deriv=True), g.get(c), g.get(r, deriv=True)
+            assert np.array_equal(dc, np.where(cv > 0, dr, np.float32(0))), c
+
+
 @pytest.mark.parametrize("pad", [(0, 0, 0, 0), (0, 1, 0, 1)])
 def test_engine_pool_argmax_route_bitexact(pad):
     """In a graph the max pool records its argmax in the forward and the
