@@ -601,6 +601,13 @@ struct ck_trainer : ck::LayerDone {
   cudaEvent_t comm_done = nullptr;
   std::vector<std::vector<int>> layer_params;  // params finished by layer li
   float* loss_dev = nullptr;
+  // single GPU: each layer's SGD runs on an update stream as soon as that
+  // layer's backward is done, overlapping the rest of the backward (the
+  // streaming update fits beside a persistent GEMM's CTAs on the same SMs)
+  cudaStream_t upd_stream = nullptr;
+  std::vector<cudaEvent_t> upd_ev;
+  cudaEvent_t upd_done = nullptr;
+  bool upd_pending = false;
   // CUDA-graph replay of the whole step (ck_trainer_set_graph)
   bool use_graph = false;
   int eager_steps = 0;                 // workspaces are sized by one eager step
@@ -629,8 +636,25 @@ struct ck_trainer : ck::LayerDone {
         throw Err(CK_ERR_CUDA, "ncclAllReduce failed");
       for (int p : ps) sgd(p, comm_stream);
     } else {
-      for (int p : ps) sgd(p, s);
+      if (!upd_stream) {
+        ck::check_cuda(cudaStreamCreateWithFlags(&upd_stream, cudaStreamNonBlocking), "stream");
+        upd_ev.assign(g->layers.size(), nullptr);
+        for (auto& e : upd_ev)
+          ck::check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        ck::check_cuda(cudaEventCreateWithFlags(&upd_done, cudaEventDisableTiming), "event");
+      }
+      ck::check_cuda(cudaEventRecord(upd_ev[li], s), "event");
+      ck::check_cuda(cudaStreamWaitEvent(upd_stream, upd_ev[li], 0), "wait");
+      for (int p : ps) sgd(p, upd_stream);
+      upd_pending = true;
     }
+  }
+  // the step's parameters are final only after every queued update: join
+  void join_updates(cudaStream_t s) {
+    if (!upd_pending) return;
+    ck::check_cuda(cudaEventRecord(upd_done, upd_stream), "event");
+    ck::check_cuda(cudaStreamWaitEvent(s, upd_done, 0), "wait");
+    upd_pending = false;
   }
   void sgd(int p, cudaStream_t s) {
     ck::Var& v = g->vars[p];
@@ -649,6 +673,9 @@ struct ck_trainer : ck::LayerDone {
     for (float* m : mom) cudaFree(m);
     for (auto e : ev) cudaEventDestroy(e);
     if (comm_done) cudaEventDestroy(comm_done);
+    for (auto e : upd_ev) cudaEventDestroy(e);
+    if (upd_done) cudaEventDestroy(upd_done);
+    if (upd_stream) cudaStreamDestroy(upd_stream);
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (comm) ncclCommDestroy(comm);
     if (loss_dev) cudaFree(loss_dev);
@@ -897,6 +924,7 @@ static void trainer_body(ck_trainer* t, cudaStream_t s) {
     Var& obj = g->vars[t->objective];
     check_cuda(cudaMemcpyAsync(t->loss_dev, obj.value, sizeof(float), cudaMemcpyDeviceToDevice, s),
                "copy");
+    t->join_updates(s);
   }
 }
 
