@@ -41,6 +41,14 @@ struct ck_handle {
   const float* pending_rx = nullptr;
   const float* pending_rdy = nullptr;
   int64_t pending_n = 0;
+  // engine: a dy grid (and its bias-gradient partials) already built by the
+  // layer below's backward (lrn_backward_grid) for the conv backward of this
+  // call: used by dy_grid when (source, key) match
+  float* pre_dyg = nullptr;
+  const float* pre_dyg_src = nullptr;
+  int64_t pre_dyg_key = 0;
+  const double* pre_bpart = nullptr;
+  int pre_rows = 0;
   ck::KernelProfiler prof;
 };
 
@@ -99,6 +107,16 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
 bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, int acc,
                   cudaStream_t s, const float* relu_x = nullptr, const float* relu_dy = nullptr,
                   bool skip_gout = false);
+// The dy grid a TF32 conv backward consumes (dy at (0, 0) of an Hg x Wg grid,
+// Kgp padded channels per group): conv_tc_grid_plan says whether BOTH the
+// weight and data gradient of d read dy only through that grid, and how it
+// is laid out (key: dy_grid's cache key).
+struct GridPlan {
+  int Hg, Wg, Kg, Kgp, groups, OH, OW;
+  int64_t key;
+  size_t bytes;
+};
+bool conv_tc_grid_plan(const ConvDims& d, GridPlan* gp);
 // capi.cu: compute a dy the gated transform left pending (h->pending_dy == dy)
 void materialize_pending_dy(ck_handle* h, const float* dy, cudaStream_t s);
 void conv_tc_release(ck_handle* h);

@@ -108,6 +108,14 @@ void lrn_forward(const float* x, float* y, int H, int W, int C, int N, int size,
                  float alpha, float beta, cudaStream_t s);
 void lrn_backward(const float* x, const float* dy, float* dx, int H, int W, int C, int N, int size,
                   float kappa, float alpha, float beta, int acc, cudaStream_t s);
+// LRN backward whose output goes (ReLU-gated by x > 0) straight into the dy
+// grid of the conv below the ReLU that feeds the LRN, with per-warp bias
+// partials (bpart: lrn_grid_rows(H, W, N) x Kgp*groups doubles).  False when
+// the LRN size has no grid kernel (3 and 5 do).
+bool lrn_backward_grid(const float* x, const float* dy, float* grid, double* bpart, int H, int W,
+                       int C, int N, int size, float kappa, float alpha, float beta, int Hg, int Wg,
+                       int Kg, int Kgp, int groups, cudaStream_t s);
+int lrn_grid_rows(int H, int W, int N);
 
 // Per-channel sums in double: out[c] = {sum x, sum x^2, sum dy, sum dy*x}
 // (dy may be null).  partial: workspace of splits*C*4 doubles.

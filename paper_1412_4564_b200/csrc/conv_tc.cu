@@ -1972,13 +1972,33 @@ __global__ void grid_bias_finish_k(const double* __restrict__ part2, float* db, 
 // pixels (conv.cpp:246-252), fused into the same read of dy.
 // With relu_x != nullptr, dy is produced here: dy = relu_x > 0 ? relu_dy : 0
 // (the engine's fused conv -> relu backward); the grid is built from it.
+static int64_t dy_grid_key(const ConvDims& d, int Kgp, int groups, int Hg, int Wg) {
+  return ((((int64_t)Hg * 4099 + Wg) * 65537 + d.K) * 131071 + d.N) * 1031 + Kgp * 17 + groups +
+         ((int64_t)d.OH << 40) + ((int64_t)d.OW << 50);
+}
+
+static bool halo_enabled();
+static bool shift_enabled();
+
 static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, int Kgp,
                       int groups, int Hg, int Wg, cudaStream_t s, float* db = nullptr,
                       int db_acc = 0, const float* relu_x = nullptr,
                       const float* relu_dy = nullptr, bool skip_gout = false) {
   TcState* st = state(h);
-  const int64_t key = ((((int64_t)Hg * 4099 + Wg) * 65537 + d.K) * 131071 + d.N) * 1031 +
-                      Kgp * 17 + groups + ((int64_t)d.OH << 40) + ((int64_t)d.OW << 50);
+  const int64_t key = dy_grid_key(d, Kgp, groups, Hg, Wg);
+  if (h->pre_dyg && h->pre_dyg_src == dy && h->pre_dyg_key == key) {
+    // built (gated, bias partials included) by the engine's previous layer
+    if (db) {
+      const int Cp = Kgp * groups, rows = h->pre_rows;
+      const int chunks = (rows + 8 * kBiasRowsPerWarp - 1) / (8 * kBiasRowsPerWarp);
+      double* part2 = (double*)grow(st->bpart, sizeof(double) * (size_t)chunks * Cp, s);
+      count_launch(2);
+      grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(h->pre_bpart, part2, Cp, rows);
+      grid_bias_finish_k<<<(Cp + 127) / 128, 128, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
+                                                          db_acc);
+    }
+    return h->pre_dyg;
+  }
   float* buf = (float*)grow(st->dyg, sizeof(float) * (size_t)d.N * Hg * Wg * Kgp * groups, s);
   if (!db && st->dyg_src == dy && st->dyg_call == h->call && st->dyg_key == key) return buf;
   if (!relu_x) materialize_pending_dy(h, dy, s);  // rebuilding from dy: it must exist
@@ -2608,6 +2628,36 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
 // Bias gradient fused into the dy-grid transform that the dgrad / wgrad of
 // the same ck_conv_backward call then reuse.  False when the shape does not
 // use the grid (FC layers, strided convs without space-to-depth).
+// Mirrors the envelopes of conv_tc_bias / conv_tc_wgrad / conv_tc_dgrad: true
+// iff all three read dy only through dy_grid (no fallback, no experimental
+// path that transforms dy itself).
+bool conv_tc_grid_plan(const ConvDims& d, GridPlan* gp) {
+  if (!load_driver() || is_fc(d) || halo_enabled() || shift_enabled()) return false;
+  const int Kg = d.Kg();
+  if (d.sh == 1 && d.sw == 1) {
+    if (d.Cg < 16 || Kg < 16) return false;
+    if (d.pt > d.fh - 1 || d.pb > d.fh - 1 || d.pl > d.fw - 1 || d.pr > d.fw - 1) return false;
+    if (d.pt > 127 || d.pl > 127 || d.fh > 128 || d.fw > 128) return false;
+    grid_dims(d, gp->Hg, gp->Wg);
+    gp->Kg = Kg;
+    gp->Kgp = rup(Kg, 32);
+    gp->groups = d.groups;
+  } else {
+    S2D z;
+    if (!s2d_plan(d, z)) return false;
+    gp->Hg = z.U;
+    gp->Wg = z.V;
+    gp->Kg = d.K;
+    gp->Kgp = rup(d.K, 32);
+    gp->groups = 1;
+  }
+  gp->OH = d.OH;
+  gp->OW = d.OW;
+  gp->key = dy_grid_key(d, gp->Kgp, gp->groups, gp->Hg, gp->Wg);
+  gp->bytes = sizeof(float) * (size_t)d.N * gp->Hg * gp->Wg * gp->Kgp * gp->groups;
+  return true;
+}
+
 bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, int acc,
                   cudaStream_t s, const float* relu_x, const float* relu_dy, bool skip_gout) {
   if (!load_driver() || is_fc(d)) return false;

@@ -65,6 +65,9 @@ struct Var {
   // grid form was consumed): deriv = value(lazy_gate) > 0 ? deriv(lazy_src) : 0,
   // computed when the derivative is requested (ck_graph_var)
   int lazy_gate = -1, lazy_src = -1;
+  // derivative left unmaterialized because the LRN layer lazy_lrn wrote its
+  // consumer conv's dy grid directly: that LRN backward, computed on request
+  int lazy_lrn = -1;
 };
 
 struct Layer {
@@ -81,6 +84,12 @@ struct Layer {
   int fused_by = -1;     // relu: index of the conv layer that writes its output
   bool fused_done = false;
   bool fused_bwd = false;  // relu backward may be left to the producing conv's backward
+  // conv: its dy grid + bias partials prebuilt by the LRN above (lrn -> relu
+  // -> conv chain, see layer_backward), valid for the current backward
+  bool pre_grid = false;
+  GridPlan plan{};
+  Workspace dyg, bpart;
+  int pre_rows = 0;
   bool bwd_deferred = false;  // ... and was, in the current backward pass
 };
 
@@ -128,7 +137,11 @@ struct ck_graph {
     return (int)vars.size() - 1;
   }
   ~ck_graph() {
-    for (auto& l : layers) l.cache.buf.release();
+    for (auto& l : layers) {
+      l.cache.buf.release();
+      l.dyg.release();
+      l.bpart.release();
+    }
     for (void* p : allocs) cudaFree(p);
     for (auto e : prof_ev) cudaEventDestroy(e);
   }
@@ -395,6 +408,18 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
 
 // One layer's backward; contributions for input slot k go to derivs with
 // accumulate = deriv_live (graph.cpp:587-596 fused).
+// The relu output's derivative an LRN backward skipped (it wrote the conv's
+// dy grid instead): the ordinary LRN backward into it, now.
+static void materialize_lrn(ck_graph* g, Var& v, cudaStream_t s) {
+  if (v.lazy_lrn < 0) return;
+  Layer& l = g->layers[v.lazy_lrn];
+  ck_tensor x = tv(v, false), dx = tv(v, true), dy = tv(g->vars[l.out[0]], true);
+  const ck_lrn_params p = lrn_of(l);
+  const ck_status st = ck_lrn_backward(g->h, &x, &p, &dy, &dx, 0, s);
+  if (st != CK_OK) throw Err(st, g->h->err);
+  v.lazy_lrn = -1;
+}
+
 static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) {
   ck_handle* h = g->h;
   auto V = [&](int k) { return tv(g->vars[l.in[k]], false); };
@@ -414,6 +439,20 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
       int a0 = acc(0), a1 = acc(1), a2 = l.in.size() > 2 ? acc(2) : a1;
       h->conv_cache = &l.cache;  // the forward's transformed input (valid this step)
       const bool fused = l.relu_out >= 0 && g->layers[g->vars[l.relu_out].producer].bwd_deferred;
+      if (l.pre_grid) {
+        l.pre_grid = false;
+        if (fused && a0 == a1 && a1 == a2 && l.in.size() > 2) {
+          h->pre_dyg = (float*)l.dyg.ptr;
+          h->pre_dyg_src = dy.data;
+          h->pre_dyg_key = l.plan.key;
+          h->pre_bpart = (const double*)l.bpart.ptr;
+          h->pre_rows = l.pre_rows;
+        } else {
+          // cannot consume the prebuilt grid: materialize the relu output's
+          // derivative the LRN skipped, then take the ordinary path
+          materialize_lrn(g, g->vars[l.relu_out], s);
+        }
+      }
       if (fused) {
         // fused relu backward: this call derives dy from the relu output's derivative;
         // dy itself (the conv output's derivative) may stay unmaterialized
@@ -429,6 +468,9 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
           h->fuse_relu_dy = nullptr;
           h->fuse_relu_lazy = false;
           h->fuse_relu_pending = false;
+          h->pre_dyg = nullptr;
+          h->pre_dyg_src = nullptr;
+          h->pre_bpart = nullptr;
         }
       } reset{h};
       if (a0 == a1 && a1 == a2) {
@@ -486,6 +528,43 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
     case Kind::lrn: {
       ck_tensor x = V(0), dx = D(0);
       ck_lrn_params p = lrn_of(l);
+      // lrn <- relu <- conv with the relu fused into the conv (TF32 grid path):
+      // write the conv's ReLU-gated dy grid (+ bias partials) directly; the
+      // relu output's derivative is then computed only on request
+      Var& xv = g->vars[l.in[0]];
+      if (!acc(0) && g->math == CK_MATH_TF32 && xv.producer >= 0 && xv.consumers.size() == 1 &&
+          getenv("CK_NO_LRN_GRID") == nullptr) {
+        Layer& r = g->layers[xv.producer];
+        if (r.kind == Kind::relu && r.fused_by >= 0 && r.fused_bwd) {
+          Layer& c = g->layers[r.fused_by];
+          const Var& cx = g->vars[c.in[0]];
+          const Var& cf = g->vars[c.in[1]];
+          const ConvDims cd = conv_dims(cx.shape, cf.shape, g->vars[c.out[0]].shape,
+                                        conv_geom_of(c));
+          GridPlan gp;
+          if (c.in.size() > 2 && conv_tc_grid_plan(cd, &gp)) {
+            float* old = (float*)c.dyg.ptr;
+            float* grid = (float*)c.dyg.get(gp.bytes, s);
+            if (!grid) throw Err(CK_ERR_CUDA, "dy grid allocation failed");
+            if (grid != old)  // the grid's junk rows stay zero from here on
+              check_cuda(cudaMemsetAsync(grid, 0, c.dyg.bytes, s), "zero");
+            const int rows = lrn_grid_rows((int)x.shape.h, (int)x.shape.w, (int)x.shape.n);
+            double* bp = (double*)c.bpart.get(sizeof(double) * (size_t)rows * gp.Kgp * gp.groups, s);
+            if (!bp) throw Err(CK_ERR_CUDA, "bias partial allocation failed");
+            if (lrn_backward_grid(x.data, dy.data, grid, bp, (int)x.shape.h, (int)x.shape.w,
+                                  (int)x.shape.c, (int)x.shape.n, (int)p.group_size,
+                                  (float)p.kappa, (float)p.alpha, (float)p.beta, gp.Hg, gp.Wg,
+                                  gp.Kg, gp.Kgp, gp.groups, s)) {
+              c.pre_grid = true;
+              c.plan = gp;
+              c.pre_rows = rows;
+              xv.lazy_lrn = (int)(&l - &g->layers[0]);
+              mark(0);
+              break;
+            }
+          }
+        }
+      }
       st = ck_lrn_backward(h, &x, &p, &dy, &dx, acc(0), s);
       mark(0);
       break;
@@ -550,8 +629,9 @@ struct LayerDone {
 static void run_backward(ck_graph* g, int objective, cudaStream_t s, LayerDone* cb) {
   for (auto& v : g->vars) {
     v.deriv_live = false;
-    v.lazy_gate = v.lazy_src = -1;
+    v.lazy_gate = v.lazy_src = v.lazy_lrn = -1;
   }
+  for (auto& l : g->layers) l.pre_grid = false;
   for (auto& l : g->layers) l.bwd_deferred = false;
   Var& obj = g->vars[objective];
   if (elems(obj.shape) != 1) throw Err(CK_ERR_ARG, "objective '" + obj.name + "' is not a scalar");
@@ -765,6 +845,15 @@ ck_status ck_graph_var(ck_graph* g, const char* name, int deriv, ck_tensor* out)
   if (!g->finalized) throw Err(CK_ERR_ARG, "graph not finalized");
   if (!out) throw Err(CK_ERR_ARG, "null output");
   Var& v = g->vars[g->var(name ? name : "")];
+  if (deriv && v.lazy_lrn >= 0) {
+    check_cuda(cudaDeviceSynchronize(), "synchronize");
+    materialize_lrn(g, v, 0);
+    check_cuda(cudaDeviceSynchronize(), "synchronize");
+  }
+  if (deriv && v.lazy_gate >= 0 && g->vars[v.lazy_src].lazy_lrn >= 0) {
+    check_cuda(cudaDeviceSynchronize(), "synchronize");
+    materialize_lrn(g, g->vars[v.lazy_src], 0);
+  }
   if (deriv && v.lazy_gate >= 0) {
     // a fused conv -> relu backward left this derivative unmaterialized:
     // relu backward (activation.cpp:14-22) of the relu output's derivative,

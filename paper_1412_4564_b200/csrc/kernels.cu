@@ -649,17 +649,45 @@ __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y
   }
 }
 
-template <int NW, bool kAcc>
+// GRID: instead of dx, store relu_backward(x, dx) -- x is the output of the
+// ReLU feeding this LRN, so x > 0 is that ReLU's mask (activation.cpp:14-22)
+// -- straight into the pixel-major dy grid of the conv below that ReLU (dy at
+// (0, 0) of an Hg x Wg grid, channel g*Kgp + c of group g), with per-warp
+// per-channel sums of the stored values (the conv's bias gradient partials).
+struct LrnGridOut {
+  float* grid;
+  double* bpart;  // [pixel warp][Kgp * groups]
+  int H, Hg, Wg, Kg, Kgp, Cp;
+};
+
+template <int NW, bool kAcc, bool GRID = false>
 __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
-                              int HW, int C, int64_t pixels, float kappa, float alpha, float beta) {
+                              int HW, int C, int64_t pixels, float kappa, float alpha, float beta,
+                              LrnGridOut go = LrnGridOut{}) {
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
   constexpr int P = 8;  // prefetch distance (channels): 2P loads in flight per thread
   const float nb = -beta;
   const float c2ab = __fmul_rn(__fmul_rn(2.f, alpha), beta);
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pixels;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31, warp_in_block = threadIdx.x >> 5;
+  __shared__ float gsm[GRID ? 4 : 1][32][33];  // GRID: per-warp [pixel][channel] stage
+  __shared__ int64_t grs[GRID ? 4 : 1][32];     // GRID: per-warp pixel grid row offsets
+  // GRID: whole warps walk the pixels together (the bias partials are warp
+  // sums); lanes past the end repeat the last pixel and store nothing
+  for (int64_t eb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - (GRID ? lane : 0);
+       eb < pixels; eb += (int64_t)gridDim.x * blockDim.x) {
+    const bool live = !GRID || eb + lane < pixels;
+    const int64_t e = GRID ? (live ? eb + lane : pixels - 1) : eb;
     const int64_t n = e / HW;
     const int p = (int)(e - n * HW);
+    int64_t grow0 = 0;  // GRID: this pixel's grid row offset (floats)
+    int gch = 0, gcl = 0;  // GRID: (group, channel in group) of the next stored channel
+    if (GRID) {
+      const int i = p % go.H, jj = p / go.H;
+      grow0 = ((int64_t)n * go.Hg * go.Wg + i + (int64_t)go.Hg * jj) * go.Cp;
+      __syncwarp();  // the previous pixel group's flushes are done with grs
+      grs[warp_in_block][lane] = live ? grow0 : -1;
+      __syncwarp();
+    }
     const int64_t base = n * C * HW + p;
     const float* xp = x + base;
     const float* gp = dy + base;
@@ -688,7 +716,7 @@ __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restri
 #pragma unroll
     for (int i = 0; i <= DOWN; ++i) Ls[i] = xs[i] = gs[i] = 0.f;
     // one channel step; `full`: j < C and the store index j - DOWN >= 0
-    auto step = [&](int j, float xlead, float gj_in, bool compute, bool store) {
+    auto step = [&](int j, float xlead, float gj_in, bool compute, bool store, int slot) {
       float L = 0.f, xj = 0.f, gj = 0.f, et = 0.f;
       if (compute) {
         float acc = 0.f;
@@ -719,7 +747,36 @@ __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restri
         for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, eta[i]);
         const float r = __fadd_rn(__fmul_rn(gs[0], Ls[0]),
                                   -__fmul_rn(__fmul_rn(c2ab, xs[0]), acc));
-        *dq = kAcc ? __fadd_rn(*dq, r) : r;
+        if (GRID) {
+          // staged per warp as [pixel][channel mod 32]; every 32 channels the warp
+          // writes each of its pixels' 128-byte channel run with one coalesced store
+          const int c = j - DOWN, cpos = gch * go.Kgp + gcl;  // channel c of group gch
+          if (++gcl == go.Kg) {
+            gcl = 0;
+            ++gch;
+          }
+          const float v = (live && xs[0] > 0.f) ? r : 0.f;
+          gsm[warp_in_block][lane][c & 31] = v;
+          if ((c & 31) == 31) {
+            __syncwarp();
+            // lane = channel: store the 32 pixels' values of that channel, and
+            // their sum (the bias partial of this pixel group, pixels in order)
+            float* gb = go.grid + (cpos - 31 + lane);
+            double t = 0;
+#pragma unroll 8
+            for (int q = 0; q < 32; ++q) {
+              const int64_t rq = grs[warp_in_block][q];  // -1: lane q has no pixel
+              const float vq = gsm[warp_in_block][q][lane];
+              t += (double)vq;
+              if (rq >= 0) gb[rq] = vq;
+            }
+            go.bpart[(eb >> 5) * go.Cp + cpos - 31 + lane] = t;
+            __syncwarp();
+          }
+          (void)slot;
+        } else {
+          *dq = kAcc ? __fadd_rn(*dq, r) : r;
+        }
       }
       // advance the x window to lead index j + 1
 #pragma unroll
@@ -743,7 +800,7 @@ __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restri
         gpre[u] = j + P < C ? __ldg(lg) : 0.f;
         lx += HW;
         lg += HW;
-        if (j < J) step(j, xl, gi, j < C, j >= DOWN);
+        if (j < J) step(j, xl, gi, j < C, j >= DOWN, (u + 8 - DOWN) & 7);
         dq += HW;
       }
     }
@@ -756,7 +813,7 @@ __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restri
         gpre[u] = __ldg(lg);
         lx += HW;
         lg += HW;
-        step(j0 + u, xl, gi, true, true);
+        step(j0 + u, xl, gi, true, true, (u + 8 - DOWN) & 7);
         dq += HW;
       }
     }
@@ -769,7 +826,7 @@ __global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restri
         gpre[u] = j + P < C ? __ldg(lg) : 0.f;
         lx += HW;
         lg += HW;
-        if (j < J) step(j, xl, gi, j < C, j >= DOWN);
+        if (j < J) step(j, xl, gi, j < C, j >= DOWN, (u + 8 - DOWN) & 7);
         dq += HW;
       }
     }
@@ -1320,6 +1377,33 @@ void lrn_backward(const float* x, const float* dy, float* dx, int H, int W, int 
   else
     lrn_bwd_k<false><<<grid, 256, smem, s>>>(x, dy, dx, HW, C, size, kappa, alpha, beta);
 }
+
+bool lrn_backward_grid(const float* x, const float* dy, float* grid, double* bpart, int H, int W,
+                       int C, int N, int size, float kappa, float alpha, float beta, int Hg, int Wg,
+                       int Kg, int Kgp, int groups, cudaStream_t s) {
+  const int HW = H * W;
+  const int64_t pixels = (int64_t)HW * N;
+  // 32-channel runs never cross a group (and every run completes)
+  if (H > Hg || W > Wg || Kg * groups != C || Kg % 32 || C % 32) return false;
+  LrnGridOut go{grid, bpart, H, Hg, Wg, Kg, Kgp, Kgp * groups};
+  const dim3 grid_dim(blocks_for(pixels, 128, 32));
+  switch (size) {
+    case 3:
+      count_launch();
+      lrn_bwd_reg_k<3, false, true><<<grid_dim, 128, 0, s>>>(x, dy, nullptr, HW, C, pixels, kappa,
+                                                             alpha, beta, go);
+      return true;
+    case 5:
+      count_launch();
+      lrn_bwd_reg_k<5, false, true><<<grid_dim, 128, 0, s>>>(x, dy, nullptr, HW, C, pixels, kappa,
+                                                             alpha, beta, go);
+      return true;
+    default:
+      return false;
+  }
+}
+
+int lrn_grid_rows(int H, int W, int N) { return (int)(((int64_t)H * W * N + 31) / 32); }
 
 int bnorm_splits(int HW, int C, int N) {
   // Aim for ~4 blocks per SM overall.

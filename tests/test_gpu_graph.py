@@ -139,6 +139,38 @@ def test_fused_conv_relu_derivative_materialized_on_request():
             assert np.array_equal(dc, np.where(cv > 0, dr, np.float32(0))), c
 
 
+@pytest.mark.parametrize("net_name,batch", [("alexnet", 16), ("alexnet", 3), ("cifar", 8)])
+def test_lrn_writes_conv_dy_grid(net_name, batch, monkeypatch):
+    """conv -> relu -> lrn chains (TF32): the LRN backward writes the conv's
+    ReLU-gated dy grid and bias partials directly (lrn_backward_grid); the
+    relu output's and conv output's derivatives are computed on request.
+    Everything but the conv biases' gradients (summed in another fixed order,
+    in double) is bit-identical to the unfused engine; those agree to 1e-6."""
+    from paper_1412_4564_b200 import nets
+    net = nets.alexnet(batch=batch) if net_name == "alexnet" else nets.cifar(batch=batch)
+    out = []
+    for fuse in (True, False):
+        if fuse:
+            monkeypatch.delenv("CK_NO_LRN_GRID", raising=False)
+        else:
+            monkeypatch.setenv("CK_NO_LRN_GRID", "1")
+        g = device_graph(net, "tf32")
+        for k, v in {**net.init_params(), **net.init_inputs()}.items():
+            g.set(k, v)
+        g.forward()
+        g.backward("objective")
+        names = set(net.inputs) | {p[0] for p in net.params} | \
+            {o for layer in net.layers for o in layer[3]}
+        out.append({name: g.get(name, deriv=True) for name in sorted(names) if name != "label"})
+    biases = {p[0] for p in net.params if p[0].endswith("b")}
+    for name in out[1]:
+        a, b = out[0][name], out[1][name]
+        if name in biases:
+            assert np.abs(a - b).max() <= 1e-6 * (np.abs(b).max() + 1e-30), name
+        else:
+            assert np.array_equal(a, b), name
+
+
 @pytest.mark.parametrize("pad", [(0, 0, 0, 0), (0, 1, 0, 1)])
 def test_engine_pool_argmax_route_bitexact(pad):
     """In a graph the max pool records its argmax in the forward and the
