@@ -1934,17 +1934,22 @@ static bool halo_launch(const HaloConv& hc, GemmParams p, cudaStream_t s) {
 // db from the per-(image, pixel tile) partials [rows][Cp], in two fixed-order
 // stages (deterministic): grid_bias_part_k -- block (32 channels, row chunk
 // of 8*RPW rows) -> part2[chunk][Cp]; grid_bias_finish_k sums the chunks.
-constexpr int kBiasRowsPerWarp = 8;
+// rows of bias partials per warp: at least 8, and few enough block chunks
+// (<= 64) that the per-channel finish loop stays short
+static inline int bias_rows_per_warp(int rows) { return std::max(8, (rows + 511) / 512); }
+static inline int bias_chunks(int rows) {
+  const int rpw = bias_rows_per_warp(rows);
+  return (rows + 8 * rpw - 1) / (8 * rpw);
+}
 __global__ void grid_bias_part_k(const double* __restrict__ bpart, double* __restrict__ part2,
-                                 int Cp, int rows) {
+                                 int Cp, int rows, int rpw) {
   __shared__ double red[8][32];
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   const int cp = blockIdx.x * 32 + lane;
-  const int r0 = blockIdx.y * 8 * kBiasRowsPerWarp + warp * kBiasRowsPerWarp;
+  const int r0 = blockIdx.y * 8 * rpw + warp * rpw;
   double t = 0;
   if (cp < Cp)
-#pragma unroll
-    for (int r = r0; r < r0 + kBiasRowsPerWarp; ++r)
+    for (int r = r0; r < r0 + rpw; ++r)
       if (r < rows) t += bpart[(int64_t)r * Cp + cp];
   red[warp][lane] = t;
   __syncthreads();
@@ -1990,10 +1995,11 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
     // built (gated, bias partials included) by the engine's previous layer
     if (db) {
       const int Cp = Kgp * groups, rows = h->pre_rows;
-      const int chunks = (rows + 8 * kBiasRowsPerWarp - 1) / (8 * kBiasRowsPerWarp);
+      const int chunks = bias_chunks(rows);
       double* part2 = (double*)grow(st->bpart, sizeof(double) * (size_t)chunks * Cp, s);
       count_launch(2);
-      grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(h->pre_bpart, part2, Cp, rows);
+      grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(h->pre_bpart, part2, Cp, rows,
+                                                                     bias_rows_per_warp(rows));
       grid_bias_finish_k<<<(Cp + 127) / 128, 128, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
                                                           db_acc);
     }
@@ -2004,14 +2010,15 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
   if (!relu_x) materialize_pending_dy(h, dy, s);  // rebuilding from dy: it must exist
   if (db) {
     const int Cp = Kgp * groups, nb = (Hg * Wg + 63) / 64;
-    const int rows = d.N * nb, chunks = (rows + 8 * kBiasRowsPerWarp - 1) / (8 * kBiasRowsPerWarp);
+    const int rows = d.N * nb, chunks = bias_chunks(rows);
     double* bpart =
         (double*)grow(st->bpart, sizeof(double) * ((size_t)rows + chunks) * Cp, s);
     double* part2 = bpart + (size_t)rows * Cp;
     count_launch(3);
     grid_pm_launch(relu_x ? relu_dy : dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, Hg, Wg, 0,
                    0, bpart, relu_x, relu_x && !skip_gout ? const_cast<float*>(dy) : nullptr, s);
-    grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(bpart, part2, Cp, rows);
+    grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(bpart, part2, Cp, rows,
+                                                                   bias_rows_per_warp(rows));
     grid_bias_finish_k<<<(Cp + 127) / 128, 128, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
                                                         db_acc);
   } else {
