@@ -660,8 +660,11 @@ struct LrnGridOut {
   int H, Hg, Wg, Kg, Kgp, Cp;
 };
 
+#ifndef CK_LRN_GRID_MINB
+#define CK_LRN_GRID_MINB 5
+#endif
 template <int NW, bool kAcc, bool GRID = false>
-__global__ void lrn_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
+__global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
                               int HW, int C, int64_t pixels, float kappa, float alpha, float beta,
                               LrnGridOut go = LrnGridOut{}) {
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
