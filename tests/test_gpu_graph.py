@@ -171,6 +171,42 @@ def test_lrn_writes_conv_dy_grid(net_name, batch, monkeypatch):
             assert np.array_equal(a, b), name
 
 
+@pytest.mark.parametrize("cout,groups,size", [(64, 2, 5), (48, 1, 5), (96, 1, 3), (64, 1, 4)])
+def test_lrn_grid_envelope(cout, groups, size, monkeypatch):
+    """conv -> relu -> lrn -> pool -> fc on a small image: inside the fused
+    kernel's envelope (channels per group a multiple of 32, LRN size 3 or 5)
+    the LRN writes the conv's dy grid, outside it the engine falls back; both
+    agree with the unfused engine (bias gradients to 1e-6 relative)."""
+    from paper_1412_4564_b200.nets import Net
+    n = Net("lrnchain", 4, 10)
+    n.inputs = {"data": (15, 15, 16, 4), "label": (1, 1, 1, 4)}
+    x = n.conv("conv1", "data", "c1", 3, 3, 16, cout, pad=(1, 1, 1, 1), groups=groups)
+    x = n.relu("relu1", x, "r1")
+    x = n.lrn("norm1", x, "n1", size, 1.0, 1e-4, 0.75)
+    x = n.pool("pool1", x, "p1", 3, 2)
+    x = n.conv("fc", x, "f", 7, 7, cout, 10)
+    n.loss(x)
+    out = []
+    for fuse in (True, False):
+        if fuse:
+            monkeypatch.delenv("CK_NO_LRN_GRID", raising=False)
+        else:
+            monkeypatch.setenv("CK_NO_LRN_GRID", "1")
+        g = device_graph(n, "tf32")
+        for k, v in {**n.init_params(), **n.init_inputs()}.items():
+            g.set(k, v)
+        g.forward()
+        g.backward("objective")
+        names = set(n.inputs) | {p[0] for p in n.params} | {o for l in n.layers for o in l[3]}
+        out.append({name: g.get(name, deriv=True) for name in sorted(names) if name != "label"})
+    for name in out[1]:
+        a, b = out[0][name], out[1][name]
+        if name == "conv1b":
+            assert np.abs(a - b).max() <= 1e-6 * (np.abs(b).max() + 1e-30), name
+        else:
+            assert np.array_equal(a, b), name
+
+
 @pytest.mark.parametrize("pad", [(0, 0, 0, 0), (0, 1, 0, 1)])
 def test_engine_pool_argmax_route_bitexact(pad):
     """In a graph the max pool records its argmax in the forward and the
