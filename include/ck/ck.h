@@ -206,6 +206,13 @@ ck_status ck_graph_add_layer(ck_graph* g, const char* kind, const char* name,
 ck_status ck_graph_finalize(ck_graph* g, ck_math math);
 /* Device view of a variable's value (deriv == 0) or derivative (deriv != 0). */
 ck_status ck_graph_var(ck_graph* g, const char* name, int deriv, ck_tensor* out);
+
+/* Bind an input variable to caller-owned device memory (elements x 4 bytes,
+ * valid while bound; NULL restores the engine's own buffer).  A trainer step
+ * replays one captured CUDA graph per set of input bindings, so a caller can
+ * alternate two input buffers -- filling one while the step reads the other --
+ * with no device-to-device copy (graph.Feeder).  Not a reference entry point. */
+ck_status ck_graph_bind_input(ck_graph* g, const char* name, float* data);
 /* graph.cpp:494 forward (train mode) */
 ck_status ck_graph_forward(ck_graph* g, ck_stream stream);
 /* graph.cpp:548 backward with seed d(objective) = 1 */

@@ -92,6 +92,7 @@ SIGNATURES = {
                                C.POINTER(C.c_double), C.c_int]),
     "ck_graph_finalize": (S, [P, C.c_int]),
     "ck_graph_var": (S, [P, C.c_char_p, C.c_int, T]),
+    "ck_graph_bind_input": (S, [P, C.c_char_p, C.c_void_p]),
     "ck_graph_forward": (S, [P, P]),
     "ck_graph_backward": (S, [P, C.c_char_p, P]),
     "ck_graph_last_launches": (C.c_int64, [P]),

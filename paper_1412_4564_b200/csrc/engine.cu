@@ -59,6 +59,7 @@ struct Var {
   int producer = -1;
   std::vector<std::pair<int, int>> consumers;
   float* value = nullptr;
+  float* own_value = nullptr;  // the engine's buffer while an input is bound elsewhere
   float* deriv = nullptr;
   bool deriv_live = false;  // received a contribution in this backward
   // derivative left unmaterialized by a fused conv -> relu backward (only its
@@ -691,9 +692,15 @@ struct ck_trainer : ck::LayerDone {
   // CUDA-graph replay of the whole step (ck_trainer_set_graph)
   bool use_graph = false;
   int eager_steps = 0;                 // workspaces are sized by one eager step
-  cudaGraphExec_t exec = nullptr;
-  cudaStream_t graph_stream = nullptr;
-  int64_t graph_launches = 0;          // kernels in the captured step
+  // one captured step per (stream, input bindings): a caller alternating two
+  // bound input buffers (ck_graph_bind_input, graph.Feeder) replays two graphs
+  struct Captured {
+    cudaStream_t stream;
+    std::vector<float*> inputs;
+    cudaGraphExec_t exec;
+    int64_t launches;
+  };
+  std::vector<Captured> graphs;
 
   void done(int li, cudaStream_t s) override {
     const auto& ps = layer_params[li];
@@ -744,9 +751,8 @@ struct ck_trainer : ck::LayerDone {
     if (st != CK_OK) throw Err(st, g->h->err);
   }
   void drop_graph() {
-    if (exec) cudaGraphExecDestroy(exec);
-    exec = nullptr;
-    graph_stream = nullptr;
+    for (auto& c : graphs) cudaGraphExecDestroy(c.exec);
+    graphs.clear();
   }
   ~ck_trainer() override {
     drop_graph();
@@ -865,6 +871,16 @@ ck_status ck_graph_var(ck_graph* g, const char* name, int deriv, ck_tensor* out)
     v.lazy_gate = v.lazy_src = -1;
   }
   *out = tv(v, deriv != 0);
+  CKG_END(g)
+}
+
+ck_status ck_graph_bind_input(ck_graph* g, const char* name, float* data) {
+  CKG_BEGIN(g)
+  if (!g->finalized) throw Err(CK_ERR_ARG, "graph not finalized");
+  Var& v = g->vars[g->var(name ? name : "")];
+  if (v.role != 0) throw Err(CK_ERR_ARG, "'" + v.name + "' is not a graph input");
+  if (!v.own_value) v.own_value = v.value;
+  v.value = data ? data : v.own_value;
   CKG_END(g)
 }
 
@@ -1037,8 +1053,14 @@ ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
     // Replay: the step's ~100 launches become one graph launch.  Captured on
     // the first graph step (after an eager step sized every workspace); the
     // captured kernel count keeps ck_launch_count honest.
-    if (!t->exec || t->graph_stream != s) {
-      t->drop_graph();
+    std::vector<float*> inputs;
+    for (auto& v : g->vars)
+      if (v.role == 0) inputs.push_back(v.value);
+    ck_trainer::Captured* cap = nullptr;
+    for (auto& c : t->graphs)
+      if (c.stream == s && c.inputs == inputs) cap = &c;
+    if (!cap) {
+      if (t->graphs.size() >= 4) t->drop_graph();
       cudaGraph_t graph;
       check_cuda(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
       try {
@@ -1048,15 +1070,16 @@ ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
         throw;
       }
       check_cuda(cudaStreamEndCapture(s, &graph), "end capture");
-      const cudaError_t e = cudaGraphInstantiate(&t->exec, graph, 0);
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       check_cuda(e, "graph instantiate");
-      t->graph_stream = s;
-      t->graph_launches = g->h->counter.n - before;
+      t->graphs.push_back({s, inputs, exec, g->h->counter.n - before});
+      cap = &t->graphs.back();
     } else {
-      g->h->counter.n += t->graph_launches;
+      g->h->counter.n += cap->launches;
     }
-    check_cuda(cudaGraphLaunch(t->exec, s), "graph launch");
+    check_cuda(cudaGraphLaunch(cap->exec, s), "graph launch");
   } else {
     trainer_body(t, s);
     ++t->eager_steps;

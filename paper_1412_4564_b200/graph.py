@@ -120,47 +120,70 @@ class Graph:
 
 class Feeder:
     """cnn_train's batch prefetch (cnn_train.m ``opts.prefetch``) for a
-    device-resident graph: the next batch's pinned host tensors are copied to
-    device staging buffers on a copy stream while the current step computes;
-    ``take`` (on the compute stream) waits for them and moves them into the
-    graph's input variables (one device-to-device copy each).  ``result``
-    queues an asynchronous device->host read of a variable (e.g. the
-    objective) into pinned memory, read back by ``collect``."""
+    device-resident graph: two device buffers per input, alternated.  ``put``
+    copies the next batch's pinned host tensors into the free buffer on a copy
+    stream while the current step computes; ``take`` (on the compute stream)
+    waits for that copy and binds the graph's inputs to the buffer
+    (``ck_graph_bind_input``: no device-to-device copy; a trainer replays one
+    captured graph per binding).  ``result`` queues an asynchronous device->host
+    read of a variable (e.g. the objective) into pinned memory, read back by
+    ``collect``."""
 
     def __init__(self, graph: Graph, names, stream):
         self.g, self.names, self.stream = graph, list(names), stream
         self.copy = torch.cuda.Stream(device=stream.device)
-        self.views = {n: graph.view(n) for n in self.names}
-        self.stage = {}
-        for n, v in self.views.items():
-            s = v.shape
-            self.stage[n] = torch.empty(s.h * s.w * s.c * s.n, dtype=torch.float32,
-                                        device=stream.device)
-        self.ready = torch.cuda.Event()
-        self.free = torch.cuda.Event()
-        self.free.record(stream)
+        self.bufs = []
+        for _ in range(2):
+            bset = {}
+            for n in self.names:
+                s = graph.view(n).shape
+                bset[n] = torch.empty(s.h * s.w * s.c * s.n, dtype=torch.float32,
+                                      device=stream.device)
+            self.bufs.append(bset)
+        self.ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self.free = [torch.cuda.Event(), torch.cuda.Event()]
+        for e in self.free:
+            e.record(stream)
+        self.fill = 0        # buffer the next put() fills
+        self.queued = []     # filled buffers, oldest first
+        self.cur = None      # buffer bound to the graph now
         self.pending = []
-        self.h2d_bytes = sum(4 * t.numel() for t in self.stage.values())
+        self.h2d_bytes = sum(4 * t.numel() for t in self.bufs[0].values())
 
     def put(self, host: dict):
         """Queue the H2D copy of one batch (pinned host tensors by name)."""
-        self.copy.wait_event(self.free)
+        k = self.fill
+        self.copy.wait_event(self.free[k])  # the step that read buffer k is done
         cs = C.c_void_p(self.copy.cuda_stream)
         for n in self.names:
             src = host[n]
-            assert src.is_pinned() and src.numel() == self.stage[n].numel(), n
-            self.g._check(lib().ck_memcpy(self.g.hd.h, self.stage[n].data_ptr(), src.data_ptr(),
+            assert src.is_pinned() and src.numel() == self.bufs[k][n].numel(), n
+            self.g._check(lib().ck_memcpy(self.g.hd.h, self.bufs[k][n].data_ptr(), src.data_ptr(),
                                           4 * src.numel(), cs))
-        self.ready.record(self.copy)
+        self.ready[k].record(self.copy)
+        self.queued.append(k)
+        self.fill ^= 1
 
     def take(self):
-        """On the compute stream: wait for the staged batch, load it into the graph."""
-        self.stream.wait_event(self.ready)
-        s = C.c_void_p(self.stream.cuda_stream)
+        """On the compute stream: wait for the oldest filled buffer and bind the
+        graph's inputs to it; the previously bound buffer becomes free once the
+        work queued so far (the step that read it) completes."""
+        if self.cur is not None:
+            self.free[self.cur].record(self.stream)
+        k = self.queued.pop(0)
+        self.stream.wait_event(self.ready[k])
         for n in self.names:
-            self.g._check(lib().ck_memcpy(self.g.hd.h, self.views[n].data,
-                                          self.stage[n].data_ptr(), 4 * self.stage[n].numel(), s))
-        self.free.record(self.stream)
+            self.g._check(lib().ck_graph_bind_input(self.g.g, n.encode(),
+                                                    self.bufs[k][n].data_ptr()))
+        self.cur = k
+
+    def unbind(self):
+        """Restore the graph's own input buffers."""
+        for n in self.names:
+            self.g._check(lib().ck_graph_bind_input(self.g.g, n.encode(), None))
+        if self.cur is not None:
+            self.free[self.cur].record(self.stream)
+            self.cur = None
 
     def result(self, name="objective"):
         v = self.g.view(name)

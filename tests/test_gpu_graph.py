@@ -263,6 +263,52 @@ def test_trainer_cuda_graph_replay_matches_eager():
         assert np.array_equal(p0[k], p1[k]), k
 
 
+def test_feeder_bound_inputs_match_copied_inputs():
+    """graph.Feeder binds the graph's inputs to two alternating device buffers
+    (ck_graph_bind_input; one captured graph per binding): a replayed training
+    run over alternating batches is bit-identical to eager steps that copy each
+    batch into the graph's own input buffers."""
+    from paper_1412_4564_b200 import nets
+    from paper_1412_4564_b200.graph import Feeder, Trainer
+    net = nets.alexnet(batch=4)
+    params = net.init_params()
+    batches = [net.init_inputs(data_seed=1 + 100 * k, label_seed=3 + 100 * k) for k in range(2)]
+    hosts = [{n: torch.from_numpy(np.ascontiguousarray(b[n], np.float32)).pin_memory()
+              for n in ("data", "label")} for b in batches]
+    steps = 6
+    # eager reference: copy each batch in, one step each
+    g = device_graph(net, "tf32")
+    for k, v in params.items():
+        g.set(k, v)
+    t = Trainer(g, lr=0.01, momentum=0.9, weight_decay=5e-4)
+    ref = []
+    for i in range(steps):
+        for n, v in batches[i % 2].items():
+            g.set(n, v)
+        ref.append(t.step())
+    ref_params = {p: g.get(p) for p, _, _ in net.params}
+    # bound inputs + graph replay (after one eager step, as bench.py does)
+    g = device_graph(net, "tf32")
+    for k, v in params.items():
+        g.set(k, v)
+    t = Trainer(g, lr=0.01, momentum=0.9, weight_decay=5e-4)
+    t.set_graph(True)
+    stream = torch.cuda.Stream()
+    feed = Feeder(g, ["data", "label"], stream)
+    feed.put(hosts[0])
+    for i in range(steps):
+        feed.take()
+        if i + 1 < steps:
+            feed.put(hosts[(i + 1) % 2])
+        t.step(want_loss=False, stream=stream.cuda_stream)
+        feed.result("objective")
+    got = [float(v[0]) for v in feed.collect()]
+    feed.unbind()
+    assert got == ref
+    for p, _, _ in net.params:
+        assert np.array_equal(g.get(p), ref_params[p]), p
+
+
 @pytest.mark.parametrize("graph_mode", [False, True])
 def test_trainer_nccl_single_rank(graph_mode):
     """The data-parallel step on a one-rank NCCL communicator (the only
