@@ -460,8 +460,25 @@ __device__ __forceinline__ Tile tile_at(const GemmParams& p, int t) {
 // Rows are GEMM rows m; with p.hg > 0 (halo kernels) m is a position on a
 // padded grid of pitch hg (hw_grid rows per image) and only positions with
 // (u, v) < (ohv, owv) are real outputs, at pixel u + ohv * v.
+// Per-column bias of epilogue work unit u of this warp (lane j: column j of the
+// unit's 32-column chunk; 0 when the unit has no per-column bias).  Loaded one
+// unit ahead so the L2 latency hides behind the previous unit's stores (the
+// first unit's before the accumulator wait).
+__device__ __forceinline__ int epi_unit_c0(const GemmParams& p, int u, int nch) {
+  const int h = u / nch, ci = u - h * nch;
+  return 32 * ((h & 1) && p.snake ? nch - 1 - ci : ci);
+}
+__device__ __forceinline__ float epi_unit_bias(const GemmParams& p, const Tile& T, int u,
+                                               int units, int nch, int lane) {
+  if (u >= units || !p.bias || p.splits > 1 || p.epi != EPI_PIX) return 0.f;
+  const int c0 = epi_unit_c0(p, u, nch), col0 = T.n0 + c0;
+  const int lim = min(min(32, p.BN - c0), p.n_valid - col0);
+  return lane < lim ? __ldg(p.bias + col0 + T.grp * p.grp_col + lane) : 0.f;
+}
+
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T, uint32_t tacc,
-                                              bool empty_split, int halves, int warp, int lane) {
+                                              bool empty_split, int halves, int warp, int lane,
+                                              float bias_first) {
   const int q = warp & 3;
   const int cpart = (warp - 2) / 4, cparts = kEpiWarps / 4;
   float* out = p.out;
@@ -476,9 +493,12 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
   // in snake order (odd halves walk the chunks backwards): balanced when a
   // half has an odd number of chunks (BN = 96) or a short last chunk (BN = 48)
   const int nch = (p.BN + 31) / 32, units = halves * nch;
+  float bias_next = bias_first;
   for (int u = cpart; u < units; u += cparts) {
-    const int h = u / nch, ci = u - h * nch;
-    const int c0 = 32 * ((h & 1) && p.snake ? nch - 1 - ci : ci);
+    const int h = u / nch;
+    const int c0 = epi_unit_c0(p, u, nch);
+    const float lane_bias = bias_next;
+    bias_next = epi_unit_bias(p, T, u + cparts, units, nch, lane);  // next unit, in flight
     int m = T.m0 + h * 128 + q * 32 + lane;
     bool row_ok = m < p.M;
     int img = 0, pix = 0;
@@ -512,9 +532,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
       const int col0 = T.n0 + c0;
       // columns of this chunk inside both the tile and the matrix
       const int lim = min(min(32, p.BN - c0), p.n_valid - col0);
-      // per-column bias: one coalesced load per chunk (lane j holds column j),
-      // issued before the TMEM load so its latency overlaps; broadcast by shuffle
-      const float lane_bias = col_bias && lane < lim ? __ldg(p.bias + col0 + T.grp * p.grp_col + lane) : 0.f;
+      // per-column bias (lane j holds column j, loaded one unit ahead): broadcast by shuffle
       CK_LD32(r, taddr);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (empty_split)
@@ -890,6 +908,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef CK_TC_PROFILE
       unsigned long long e0 = clock64();
 #endif
+      const int nch = (p.BN + 31) / 32;
+      const float bias0 = epi_unit_bias(p, T, (warp - 2) / 4, halves * nch, nch, lane);
       mbar_wait(&tfull[ab], aph);
       tc_fence_after();
 #ifdef CK_TC_PROFILE
@@ -897,7 +917,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       e_w += e1 - e0;
 #endif
       if (p.exp != 5)  // exp 5: no epilogue work
-        epilogue_tile(p, T, tmem + (uint32_t)(ab * acc_cols), T.kb0 >= T.kb1, halves, warp, lane);
+        epilogue_tile(p, T, tmem + (uint32_t)(ab * acc_cols), T.kb0 >= T.kb1, halves, warp, lane,
+                      bias0);
       tc_fence_before();
       __syncwarp();
 #ifdef CK_TC_PROFILE
@@ -1108,7 +1129,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int ab = tc % p.nacc;
       mbar_wait(&tfull[ab], (tc / p.nacc) & 1);
       tc_fence_after();
-      epilogue_tile(p, T, tmem + (uint32_t)(ab * acc_cols), false, halves, warp, lane);
+      const int nch = (p.BN + 31) / 32;
+      epilogue_tile(p, T, tmem + (uint32_t)(ab * acc_cols), false, halves, warp, lane,
+                    epi_unit_bias(p, T, (warp - 2) / 4, halves * nch, nch, lane));
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[ab]);
