@@ -432,6 +432,85 @@ __global__ void pool_max3s2_bwd_arg_k(const uint8_t* __restrict__ arg,
   }
 }
 
+// Column-strip form of pool_max3s2_bwd_arg_k (identical matches and adds, in
+// the same (oj, oi) order): a segment of SEG lanes owns one plane, lane a
+// walks the block column b = 0..B-1.  Per step it loads only window (a, b);
+// window (a-1, b) comes from lane a-1 by shuffle and windows (., b-1) from
+// the previous step's registers -- 2 loads per 2x2 block instead of 8.  The
+// two output rows of a block column are stored as float2 when aligned.
+template <bool kAcc, int SEG>
+__global__ void __launch_bounds__(256) pool_max3s2_bwd_strip_k(const uint8_t* __restrict__ arg,
+                                                               const float* __restrict__ dy,
+                                                               float* __restrict__ dx, PoolDims d,
+                                                               int A, int B, int planes) {
+  const int lane = threadIdx.x & 31;
+  const int sub = lane % SEG;  // a
+  const int64_t plane = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / SEG;
+  const bool pl_ok = plane < planes;
+  const int a = sub;
+  const bool a_ok = pl_ok && a < A;
+  const uint8_t* ap = arg + (pl_ok ? plane : 0) * (int64_t)d.OH * d.OW;
+  const float* dp = dy + (pl_ok ? plane : 0) * (int64_t)d.OH * d.OW;
+  float* dxp = dx + (pl_ok ? plane : 0) * (int64_t)d.H * d.W;
+  const int oi = a;  // this lane's own window row (a, b)
+  // windows (a-1, b-1) and (a, b-1) from the previous step
+  int c_pl = -1, c_p = -1;
+  float g_pl = 0.f, g_p = 0.f;
+  const unsigned mask = 0xffffffffu;
+  for (int b = 0; b < B; ++b) {
+    const int oj = b;
+    const bool w_ok = a_ok && oi < d.OH && oj < d.OW;
+    const int code = w_ok ? __ldg(ap + oi + d.OH * oj) : -1;
+    const float g = w_ok ? __ldg(dp + oi + d.OH * oj) : 0.f;
+    // window (a-1, b): the left neighbour's (a = 0: none)
+    int code_l = __shfl_up_sync(mask, code, 1, SEG);
+    float g_l = __shfl_up_sync(mask, g, 1, SEG);
+    if (sub == 0) {
+      code_l = -1;
+      g_l = 0.f;
+    }
+    // codes[wb][wa] = window (a-1+wa, b-1+wb)
+    const int cd[2][2] = {{c_pl, c_p}, {code_l, code}};
+    const float gd[2][2] = {{g_pl, g_p}, {g_l, g}};
+    if (a_ok) {
+#pragma unroll
+      for (int dj = 0; dj < 2; ++dj) {
+        const int j = 2 * b + dj - d.pl;
+        float out[2];
+#pragma unroll
+        for (int di = 0; di < 2; ++di) {
+          float acc = 0.f;
+#pragma unroll
+          for (int wb = 0; wb < 2; ++wb)
+#pragma unroll
+            for (int wa = 0; wa < 2; ++wa) {
+              const int ai = di + 2 - 2 * wa, bj = dj + 2 - 2 * wb;
+              if (ai <= 2 && bj <= 2 && cd[wb][wa] == ai + 3 * bj) acc = __fadd_rn(acc, gd[wb][wa]);
+            }
+          out[di] = acc;
+        }
+        if (j < 0 || j >= d.W) continue;
+        const int i0 = 2 * a - d.pt;
+        float* o = dxp + (int64_t)d.H * j + i0;
+        const bool two = i0 >= 0 && i0 + 1 < d.H;
+        if (two && ((reinterpret_cast<uintptr_t>(o) & 7) == 0) && !kAcc) {
+          *reinterpret_cast<float2*>(o) = make_float2(out[0], out[1]);
+        } else {
+#pragma unroll
+          for (int di = 0; di < 2; ++di) {
+            const int i = i0 + di;
+            if (i >= 0 && i < d.H) o[di] = kAcc ? __fadd_rn(o[di], out[di]) : out[di];
+          }
+        }
+      }
+    }
+    c_pl = code_l;
+    g_pl = g_l;
+    c_p = code;
+    g_p = g;
+  }
+}
+
 template <int WH, int WW, int SH, int SW, bool INSIDE, bool kAcc>
 __global__ void pool_max_bwd_t(const float* __restrict__ x, const float* __restrict__ dy,
                                float* dx, PoolDims d, FastDiv by_oh, FastDiv by_h) {
@@ -1261,6 +1340,23 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
       const int A = (d.H + d.pt + 1) / 2, B = (d.W + d.pl + 1) / 2;
       const int64_t blocks = (int64_t)A * B * d.C * d.N;
       const FastDiv by_a(A), by_ab(A * B);
+      if (A <= 31 && !getenv("CK_POOL_BWD_FLAT")) {
+        // column strips: one lane segment (SEG >= A + 1 lanes) per plane
+        const int planes = d.C * d.N;
+        const int seg = A < 8 ? 8 : A < 16 ? 16 : 32;
+        const int64_t threads = (int64_t)planes * seg;
+        const unsigned grid = (unsigned)((threads + 255) / 256);
+#define CK_PSB(S)                                                                          \
+  do {                                                                                     \
+    if (acc) pool_max3s2_bwd_strip_k<true, S><<<grid, 256, 0, s>>>(arg, dy, dx, d, A, B, planes); \
+    else pool_max3s2_bwd_strip_k<false, S><<<grid, 256, 0, s>>>(arg, dy, dx, d, A, B, planes);   \
+  } while (0)
+        if (seg == 8) CK_PSB(8);
+        else if (seg == 16) CK_PSB(16);
+        else CK_PSB(32);
+#undef CK_PSB
+        return;
+      }
       if (blocks * A * B < (1ll << 39)) {
         if (acc)
           pool_max3s2_bwd_arg_k<true><<<blocks_for(blocks, 256), 256, 0, s>>>(arg, dy, dx, d, A,
