@@ -844,12 +844,12 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
             // lane = channel: store the 32 pixels' values of that channel, and
             // their sum (the bias partial of this pixel group, pixels in order)
             float* gb = go.grid + (cpos - 31 + lane);
-            double t = 0;
+            float t = 0.f;  // 32-pixel partial in float; partials summed in double
 #pragma unroll 8
             for (int q = 0; q < 32; ++q) {
               const int64_t rq = grs[warp_in_block][q];  // -1: lane q has no pixel
               const float vq = gsm[warp_in_block][q][lane];
-              t += (double)vq;
+              t += vq;
               if (rq >= 0) gb[rq] = vq;
             }
             go.bpart[(eb >> 5) * go.Cp + cpos - 31 + lane] = t;

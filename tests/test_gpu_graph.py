@@ -144,8 +144,9 @@ def test_lrn_writes_conv_dy_grid(net_name, batch, monkeypatch):
     """conv -> relu -> lrn chains (TF32): the LRN backward writes the conv's
     ReLU-gated dy grid and bias partials directly (lrn_backward_grid); the
     relu output's and conv output's derivatives are computed on request.
-    Everything but the conv biases' gradients (summed in another fixed order,
-    in double) is bit-identical to the unfused engine; those agree to 1e-6."""
+    Everything but the conv biases' gradients (32-pixel float partials, then
+    double, in another fixed order) is bit-identical to the unfused engine;
+    those agree to 1e-5 of the largest."""
     from paper_1412_4564_b200 import nets
     net = nets.alexnet(batch=batch) if net_name == "alexnet" else nets.cifar(batch=batch)
     out = []
@@ -166,7 +167,7 @@ def test_lrn_writes_conv_dy_grid(net_name, batch, monkeypatch):
     for name in out[1]:
         a, b = out[0][name], out[1][name]
         if name in biases:
-            assert np.abs(a - b).max() <= 1e-6 * (np.abs(b).max() + 1e-30), name
+            assert np.abs(a - b).max() <= 1e-5 * (np.abs(b).max() + 1e-30), name
         else:
             assert np.array_equal(a, b), name
 
@@ -176,7 +177,7 @@ def test_lrn_grid_envelope(cout, groups, size, monkeypatch):
     """conv -> relu -> lrn -> pool -> fc on a small image: inside the fused
     kernel's envelope (channels per group a multiple of 32, LRN size 3 or 5)
     the LRN writes the conv's dy grid, outside it the engine falls back; both
-    agree with the unfused engine (bias gradients to 1e-6 relative)."""
+    agree with the unfused engine (bias gradients to 1e-5 of the largest)."""
     from paper_1412_4564_b200.nets import Net
     n = Net("lrnchain", 4, 10)
     n.inputs = {"data": (15, 15, 16, 4), "label": (1, 1, 1, 4)}
@@ -202,7 +203,7 @@ def test_lrn_grid_envelope(cout, groups, size, monkeypatch):
     for name in out[1]:
         a, b = out[0][name], out[1][name]
         if name == "conv1b":
-            assert np.abs(a - b).max() <= 1e-6 * (np.abs(b).max() + 1e-30), name
+            assert np.abs(a - b).max() <= 1e-5 * (np.abs(b).max() + 1e-30), name
         else:
             assert np.array_equal(a, b), name
 
