@@ -1269,18 +1269,17 @@ static void grid_pm_launch(const float* x, float* xg, int H, int W, int C, int N
 // filter bank f[fi + fh*(fj + fw*(c*fsc + k*fsk))]; zeros for channel pads.
 __global__ void repack_fprop_k(const float* __restrict__ f, float* __restrict__ ft, int fh, int fw,
                                int Cg, int Cgp, int K, int64_t fsc, int64_t fsk) {
-  const int64_t taps = (int64_t)fh * fw;
-  const int64_t total = (int64_t)K * taps * Cgp;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int cp = (int)(e % Cgp);
-    const int64_t r = e / Cgp;
-    const int tap = (int)(r % taps);
-    const int64_t k = r / taps;
+  // 32-bit index math (the bank is far below 2^31 elements); the caller
+  // checks the 64-bit total
+  const int taps = fh * fw;
+  const int total = K * taps * Cgp;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int r = e / Cgp, cp = e - r * Cgp;
+    const int k = r / taps, tap = r - k * taps;
     float v = 0.f;
     if (cp < Cg) {
-      const int fi = tap % fh, fj = tap / fh;
-      v = f[fi + (int64_t)fh * (fj + (int64_t)fw * (cp * fsc + k * fsk))];
+      const int fj = tap / fh, fi = tap - fj * fh;
+      v = __ldg(f + fi + (int64_t)fh * (fj + (int64_t)fw * (cp * fsc + k * fsk)));
     }
     ft[e] = v;
   }
@@ -1290,21 +1289,18 @@ __global__ void repack_fprop_k(const float* __restrict__ f, float* __restrict__ 
 // tap' = flipped tap: g[fi', fj', k, c] = f[fh-1-fi', fw-1-fj', c, k].
 __global__ void repack_dgrad_k(const float* __restrict__ f, float* __restrict__ gt, int fh, int fw,
                                int Cg, int Kg, int Kgp, int groups, int64_t fsc, int64_t fsk) {
-  const int64_t taps = (int64_t)fh * fw;
-  const int64_t total = (int64_t)Cg * groups * taps * Kgp;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int kp = (int)(e % Kgp);
-    const int64_t r = e / Kgp;
-    const int tap = (int)(r % taps);
-    const int64_t cc = r / taps;  // 0 .. Cg*groups-1
-    const int g = (int)(cc / Cg);
-    const int c = (int)(cc - (int64_t)g * Cg);
+  const int taps = fh * fw;
+  const int total = Cg * groups * taps * Kgp;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int r = e / Kgp, kp = e - r * Kgp;
+    const int cc = r / taps, tap = r - cc * taps;  // cc: 0 .. Cg*groups-1
+    const int g = cc / Cg, c = cc - g * Cg;
     float v = 0.f;
     if (kp < Kg) {
-      const int fi = fh - 1 - tap % fh, fj = fw - 1 - tap / fh;
+      const int tj = tap / fh, ti = tap - tj * fh;
+      const int fi = fh - 1 - ti, fj = fw - 1 - tj;
       const int64_t k = (int64_t)g * Kg + kp;
-      v = f[fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + k * fsk))];
+      v = __ldg(f + fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + k * fsk)));
     }
     gt[e] = v;
   }
@@ -1314,22 +1310,20 @@ __global__ void repack_dgrad_k(const float* __restrict__ f, float* __restrict__ 
 __global__ void wgrad_finish_k(const float* __restrict__ part, float* df, int fh, int fw, int Cg,
                                int Cgp, int Kg, int groups, int splits, int64_t split_stride,
                                int64_t fsc, int64_t fsk, int acc) {
-  const int64_t taps = (int64_t)fh * fw;
-  const int64_t total = (int64_t)groups * Kg * taps * Cg;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
+  const int taps = fh * fw;
+  const int total = groups * Kg * taps * Cg;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     // e enumerates (k fastest) so reads of part are coalesced
-    const int k = (int)(e % Kg);
-    int64_t r = e / Kg;
-    const int c = (int)(r % Cg);
-    r /= Cg;
-    const int tap = (int)(r % taps);
-    const int g = (int)(r / taps);
-    const int64_t n = (int64_t)tap * Cgp + c;
-    const int64_t src = ((int64_t)g * taps * Cgp + n) * Kg + k;
+    int r = e / Kg;
+    const int k = e - r * Kg;
+    int r2 = r / Cg;
+    const int c = r - r2 * Cg;
+    const int g = r2 / taps, tap = r2 - g * taps;
+    const int64_t src = ((int64_t)g * taps * Cgp + (int64_t)tap * Cgp + c) * Kg + k;
     float s = 0.f;
-    for (int sp = 0; sp < splits; ++sp) s += part[sp * split_stride + src];
-    const int fi = tap % fh, fj = tap / fh;
+#pragma unroll 4
+    for (int sp = 0; sp < splits; ++sp) s += __ldg(part + sp * split_stride + src);
+    const int fj = tap / fh, fi = tap - fj * fh;
     const int64_t kk = (int64_t)g * Kg + k;
     float* dst = df + fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + kk * fsk));
     *dst = acc ? *dst + s : s;
@@ -1344,11 +1338,12 @@ __global__ void splitk_finish_k(const float* __restrict__ part, float* out, int 
   const int64_t total = (int64_t)rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int row = (int)(e % rows);
-    const int64_t col = e / rows;
+    const int col = (int)(total < (1ll << 31) ? (int)e / rows : e / rows);
+    const int row = (int)(e - (int64_t)col * rows);
     const int64_t a = row + col * ld;
     float s = 0.f;
-    for (int sp = 0; sp < splits; ++sp) s += part[sp * split_stride + a];
+#pragma unroll 4
+    for (int sp = 0; sp < splits; ++sp) s += __ldg(part + sp * split_stride + a);
     if (bias) s = __fadd_rn(s, bias[row]);
     if (relu) s = s > 0.f ? s : 0.f;
     out[a] = acc ? __fadd_rn(out[a], s) : s;
@@ -1972,6 +1967,7 @@ __global__ void grid_bias_part_k(const double* __restrict__ bpart, double* __res
   const int r0 = blockIdx.y * 8 * rpw + warp * rpw;
   double t = 0;
   if (cp < Cp)
+#pragma unroll 8
     for (int r = r0; r < r0 + rpw; ++r)
       if (r < rows) t += bpart[(int64_t)r * Cp + cp];
   red[warp][lane] = t;
@@ -1985,12 +1981,15 @@ __global__ void grid_bias_part_k(const double* __restrict__ bpart, double* __res
 
 __global__ void grid_bias_finish_k(const double* __restrict__ part2, float* db, int K, int Kg,
                                    int Kgp, int Cp, int chunks, int acc) {
-  const int cp = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per channel: lanes sum strided chunks, then a fixed shuffle tree
+  const int cp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (cp >= Cp) return;
   double u = 0;
-  for (int c = 0; c < chunks; ++c) u += part2[(int64_t)c * Cp + cp];
+  for (int c = lane; c < chunks; c += 32) u += part2[(int64_t)c * Cp + cp];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
   const int g = cp / Kgp, kl = cp - g * Kgp;
-  if (kl < Kg) {
+  if (lane == 0 && kl < Kg) {
     const int k = g * Kg + kl;
     if (k < K) db[k] = acc ? db[k] + (float)u : (float)u;
   }
@@ -2023,8 +2022,8 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
       count_launch(2);
       grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(h->pre_bpart, part2, Cp, rows,
                                                                      bias_rows_per_warp(rows));
-      grid_bias_finish_k<<<(Cp + 127) / 128, 128, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
-                                                          db_acc);
+      grid_bias_finish_k<<<(Cp * 32 + 255) / 256, 256, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp,
+                                                                chunks, db_acc);
     }
     return h->pre_dyg;
   }
@@ -2042,8 +2041,8 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
                    0, bpart, relu_x, relu_x && !skip_gout ? const_cast<float*>(dy) : nullptr, s);
     grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(bpart, part2, Cp, rows,
                                                                    bias_rows_per_warp(rows));
-    grid_bias_finish_k<<<(Cp + 127) / 128, 128, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
-                                                        db_acc);
+    grid_bias_finish_k<<<(Cp * 32 + 255) / 256, 256, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
+                                                              db_acc);
   } else {
     to_grid_pm(dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, Hg, Wg, 0, 0, s);
   }

@@ -1082,9 +1082,11 @@ __global__ void softmaxlog_fwd_k(const float* __restrict__ x, const float* __res
     int c = read_label(labels, s, C, flag);
     const float* xs = x + n * (int64_t)C * HW + p;
     float mx = -INFINITY;
+#pragma unroll 8
     for (int k = lane; k < C; k += 32) mx = fmaxf(mx, xs[(int64_t)k * HW]);
     mx = warp_max(mx);
     float sum = 0.f;
+#pragma unroll 8
     for (int k = lane; k < C; k += 32) sum += expf(xs[(int64_t)k * HW] - mx);
     sum = warp_sumf(sum);
     if (lane == 0) {
@@ -1132,12 +1134,15 @@ __global__ void softmaxlog_bwd_k(const float* __restrict__ x, const float* __res
       continue;
     }
     float mx = -INFINITY;
+#pragma unroll 8
     for (int k = lane; k < C; k += 32) mx = fmaxf(mx, xs[(int64_t)k * HW]);
     mx = warp_max(mx);
     float sum = 0.f;
+#pragma unroll 8
     for (int k = lane; k < C; k += 32) sum += expf(xs[(int64_t)k * HW] - mx);
     sum = warp_sumf(sum);
     const float scale = pscale * (weights ? weights[s] : 1.f);
+#pragma unroll 4
     for (int k = lane; k < C; k += 32) {
       float soft = expf(xs[(int64_t)k * HW] - mx) / sum;
       float r = scale * (soft - (k == c - 1 ? 1.f : 0.f));
