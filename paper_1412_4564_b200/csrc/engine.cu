@@ -722,6 +722,8 @@ struct ck_trainer : ck::LayerDone {
           ncclSuccess)
         throw Err(CK_ERR_CUDA, "ncclAllReduce failed");
       for (int p : ps) sgd(p, comm_stream);
+    } else if (getenv("CK_NO_UPDATE_STREAM")) {
+      for (int p : ps) sgd(p, s);
     } else {
       if (!upd_stream) {
         ck::check_cuda(cudaStreamCreateWithFlags(&upd_stream, cudaStreamNonBlocking), "stream");
