@@ -2375,7 +2375,23 @@ static int grid_wgrad(ck_handle* h, const float* xg, int Cp, int Cgp, const floa
   TcState* st = state(h);
   const int taps = fh * fw;
   const int Ntot = taps * Cgp;  // GEMM N = (tap, c) per group
-  const int BN = (Cgp >= 128 && Cgp <= 256) ? Cgp : std::min(256, rup(Ntot, 32));
+  // N tile: a whole tap's channels when they fit; else the multiple of 32 that
+  // wastes the fewest padded columns (conv1's s2d 576 = 3 x 192, conv2's 1600 =
+  // 10 x 160), larger on ties
+  int BN = Cgp;
+  if (Cgp < 128 || Cgp > 256) {
+    static const int force_bn = getenv("CK_TC_WBN") ? atoi(getenv("CK_TC_WBN")) : 0;
+    BN = 0;
+    int best = INT32_MAX;
+    for (int c = 256; c >= 64; c -= 32) {
+      const int padded = rup(Ntot, c);
+      if (padded < best) {
+        best = padded;
+        BN = c;
+      }
+    }
+    if (force_bn > 0 && force_bn % 32 == 0 && force_bn <= 256) BN = force_bn;
+  }
   const int b_rows = std::min(256, std::gcd(Cgp, BN));
   const int BM = pick_bm(Kg, BN);
   const int64_t rows = (int64_t)N * Hg * Wg;

@@ -1,4 +1,3 @@
-# scratch driver for gpurun experiments (edit freely): GPU tests, bench line, per-layer times
 timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python bench.py 2>/dev/null | tail -1 | cut -c1-250
-python bench.py --profile-layers --steps 20 2>&1 | grep -v "^{" | head -50
+for bn in 0 256 0 256; do echo "== WBN=$bn"; CK_TC_WBN=$bn python tools/gemm_exp.py 2>&1 | grep "conv1\|conv2" | sed 's/fprop.*wgrad/wgrad/; s/dgrad.*//'; done
+python bench.py --steps 50 --no-e2e --no-cpu-baseline 2>/dev/null | cut -c1-130
