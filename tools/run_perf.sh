@@ -1,3 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for bn in 0 256 0 256; do echo "== WBN=$bn"; CK_TC_WBN=$bn python tools/gemm_exp.py 2>&1 | grep "conv1\|conv2" | sed 's/fprop.*wgrad/wgrad/; s/dgrad.*//'; done
-python bench.py --steps 50 --no-e2e --no-cpu-baseline 2>/dev/null | cut -c1-130
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -1 gpurun_out/bench.json | cut -c1-200
+python bench.py --profile-layers --steps 20 2> gpurun_out/layers.txt > /dev/null
