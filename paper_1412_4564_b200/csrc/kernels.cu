@@ -739,6 +739,9 @@ struct LrnGridOut {
   int H, Hg, Wg, Kg, Kgp, Cp;
 };
 
+#ifndef CK_LRN_BWD_P
+#define CK_LRN_BWD_P 8
+#endif
 #ifndef CK_LRN_GRID_MINB
 #define CK_LRN_GRID_MINB 5
 #endif
@@ -747,7 +750,7 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
                               int HW, int C, int64_t pixels, float kappa, float alpha, float beta,
                               LrnGridOut go = LrnGridOut{}) {
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
-  constexpr int P = 8;  // prefetch distance (channels): 2P loads in flight per thread
+  constexpr int P = CK_LRN_BWD_P;  // prefetch distance (channels): 2P loads in flight per thread
   const float nb = -beta;
   const float c2ab = __fmul_rn(__fmul_rn(2.f, alpha), beta);
   const int lane = threadIdx.x & 31, warp_in_block = threadIdx.x >> 5;

@@ -7,6 +7,13 @@ k = collections.OrderedDict()
 for d in data:
     key = (d['ID'], d['Kernel Name'][:46])
     k.setdefault(key, {})[d['Metric Name']] = d['Metric Value']
+# one whole training step: the launches between the last two starts of a step
+# (the step's first kernel is the conv1 input transform)
+ids = list(k.keys())
+starts = [i for i, (_, n) in enumerate(ids) if 's2d_pm_strip_k' in n]
+if len(starts) >= 2:
+    keep = set(ids[starts[-2]:starts[-1]])
+    k = collections.OrderedDict((key, v) for key, v in k.items() if key in keep)
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
 for (i, name), m in k.items():
     t = float(m.get('gpu__time_duration.sum', 0)) / 1e3
