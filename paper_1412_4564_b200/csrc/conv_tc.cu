@@ -1160,18 +1160,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 // gated HWCN value is also stored to gout: the conv backward consumes the
 // relu backward in the same pass over memory.
 template <int CH, bool GATE>
-__global__ void __launch_bounds__(256, CH == 32 ? 8 : 4) to_grid_pm_k(
+__global__ void __launch_bounds__(256, CH == 32 ? (GATE ? 6 : 8) : 4) to_grid_pm_k(
     const float* __restrict__ x, float* __restrict__ xg, int H, int W, int C, int Cg, int Cgp,
     int groups, int Hg, int Wg, int oh, int ow, double* __restrict__ bpart,
-    const float* __restrict__ gate, float* __restrict__ gout) {
+    const float* __restrict__ gate, float* __restrict__ gout, int tpb) {
   // tile: 64 grid pixels x CH padded channels; loads coalesced along pixels
   // (two per channel row per thread, CH/8 rows per warp), stores as float4
-  // along channels.  Every load of the tile (and of the relu gate) is issued
-  // before any is consumed: the kernel is bound by bytes in flight.
+  // along channels.  Every load of a tile (and of the relu gate) is issued
+  // before any is consumed.  A block walks `tpb` consecutive channel tiles of
+  // its pixel tile, reusing the per-pixel source and destination arithmetic
+  // (the kernel is otherwise bound by its integer index math, not by HBM).
   constexpr int RR = CH / 8;
-  __shared__ float tile[CH][65];
+  __shared__ float tile[2][CH][65];
   const int n = blockIdx.z;
-  const int p0 = blockIdx.x * 64, c0 = blockIdx.y * CH;
+  const int p0 = blockIdx.x * 64;
   const int Cp = Cgp * groups, HWg = Hg * Wg, HW = H * W;
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   int src[2];
@@ -1185,57 +1187,65 @@ __global__ void __launch_bounds__(256, CH == 32 ? 8 : 4) to_grid_pm_k(
   const int64_t img = (int64_t)n * C * HW;
   const float* xn = x + img;
   const float* gn = GATE ? gate + img : nullptr;
-  float v[RR][2], gv[RR][2];
-#pragma unroll
-  for (int rr = 0; rr < RR; ++rr) {
-    const int cp = c0 + warp + 8 * rr;
-    const int g = cp / Cgp, cl = cp - g * Cgp;
-    const int coff = (cp < Cp && cl < Cg) ? (g * Cg + cl) * HW : -1;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const bool e = coff >= 0 && src[k] >= 0;
-      v[rr][k] = e ? __ldg(xn + coff + src[k]) : 0.f;
-      if (GATE) gv[rr][k] = e ? __ldg(gn + coff + src[k]) : 0.f;
-    }
-  }
-  if (GATE) {
-    float* go = gout ? gout + img : nullptr;
-#pragma unroll
-    for (int rr = 0; rr < RR; ++rr) {
-      const int cp = c0 + warp + 8 * rr;
-      const int g = cp / Cgp, cl = cp - g * Cgp;
-      const int coff = (cp < Cp && cl < Cg) ? (g * Cg + cl) * HW : -1;
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        v[rr][k] = gv[rr][k] > 0.f ? v[rr][k] : 0.f;
-        if (gout && coff >= 0 && src[k] >= 0) go[coff + src[k]] = v[rr][k];
-      }
-    }
-  }
-#pragma unroll
-  for (int rr = 0; rr < RR; ++rr)
-#pragma unroll
-    for (int k = 0; k < 2; ++k) tile[warp + 8 * rr][lane + 32 * k] = v[rr][k];
-  if (bpart) {  // fused bias gradient: this tile's per-channel sums (double, fixed order)
-#pragma unroll
-    for (int rr = 0; rr < RR; ++rr) {
-      const int cp = c0 + warp + 8 * rr;
-      double t = (double)v[rr][0] + (double)v[rr][1];
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-      if (lane == 0 && cp < Cp) bpart[((int64_t)n * gridDim.x + blockIdx.x) * Cp + cp] = t;
-    }
-  }
-  __syncthreads();
+  float* go = GATE && gout ? gout + img : nullptr;
+  // store side: thread -> (pixel row pr, float4 q) of the tile, CH/16 of them
   constexpr int Q = CH / 4;  // float4 per pixel row of the tile
+  float* dst[CH / 16];
 #pragma unroll
   for (int k = 0; k < CH / 16; ++k) {
     const int idx = threadIdx.x + 256 * k;
-    const int pr = idx / Q, q = idx % Q;
-    const int P = p0 + pr, cp = c0 + 4 * q;
-    if (P < HWg && cp < Cp) {
-      const float4 w = make_float4(tile[4 * q][pr], tile[4 * q + 1][pr], tile[4 * q + 2][pr],
-                                   tile[4 * q + 3][pr]);
-      *reinterpret_cast<float4*>(xg + ((int64_t)n * HWg + P) * Cp + cp) = w;
+    const int pr = idx / Q, q = idx % Q, P = p0 + pr;
+    dst[k] = P < HWg ? xg + ((int64_t)n * HWg + P) * Cp + 4 * q : nullptr;
+  }
+  for (int t = 0; t < tpb; ++t) {
+    const int c0 = (blockIdx.y * tpb + t) * CH;
+    if (c0 >= Cp) break;
+    float(*tl)[65] = tile[t & 1];
+    float v[RR][2];
+#pragma unroll
+    for (int rr = 0; rr < RR; ++rr) {
+      const int cp = c0 + warp + 8 * rr;
+      const int g = groups == 1 ? 0 : (groups == 2 ? (cp >= Cgp) : cp / Cgp);
+      const int cl = cp - g * Cgp;
+      const int coff = (cp < Cp && cl < Cg) ? (g * Cg + cl) * HW : -1;
+      float gv[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const bool e = coff >= 0 && src[k] >= 0;
+        v[rr][k] = e ? __ldg(xn + coff + src[k]) : 0.f;
+        if (GATE) gv[k] = e ? __ldg(gn + coff + src[k]) : 0.f;
+      }
+      if (GATE) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          v[rr][k] = gv[k] > 0.f ? v[rr][k] : 0.f;
+          if (go && coff >= 0 && src[k] >= 0) go[coff + src[k]] = v[rr][k];
+        }
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RR; ++rr)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) tl[warp + 8 * rr][lane + 32 * k] = v[rr][k];
+    if (bpart) {  // fused bias gradient: this tile's per-channel sums (double, fixed order)
+#pragma unroll
+      for (int rr = 0; rr < RR; ++rr) {
+        const int cp = c0 + warp + 8 * rr;
+        double s2 = (double)v[rr][0] + (double)v[rr][1];
+        for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        if (lane == 0 && cp < Cp) bpart[((int64_t)n * gridDim.x + blockIdx.x) * Cp + cp] = s2;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < CH / 16; ++k) {
+      const int idx = threadIdx.x + 256 * k;
+      const int pr = idx / Q, q = idx % Q;
+      if (dst[k] && c0 + 4 * q < Cp) {
+        const float4 w = make_float4(tl[4 * q][pr], tl[4 * q + 1][pr], tl[4 * q + 2][pr],
+                                     tl[4 * q + 3][pr]);
+        *reinterpret_cast<float4*>(dst[k] + c0) = w;
+      }
     }
   }
 }
@@ -1246,22 +1256,35 @@ static void grid_pm_launch(const float* x, float* xg, int H, int W, int C, int N
                            const float* gate, float* gout, cudaStream_t s) {
   const int Cp = Cgp * groups;
   static const int ch = getenv("CK_GRID_CH") ? atoi(getenv("CK_GRID_CH")) : 32;  // experiments
+  // channel tiles per block: enough blocks for ~8 resident per SM, each
+  // walking several tiles
+  static const int tpb_env = getenv("CK_GRID_TPB") ? atoi(getenv("CK_GRID_TPB")) : 0;
+  auto tiles_per_block = [&](int ctiles, int nb) {
+    if (tpb_env > 0) return std::min(tpb_env, ctiles);
+    int t = 1;
+    while (t < 4 && t * 2 <= ctiles && (int64_t)nb * N * ((ctiles + 2 * t - 1) / (2 * t)) >= 148 * 8 * 2)
+      t *= 2;
+    return t;
+  };
+  const int nb = (Hg * Wg + 63) / 64;
   if (ch == 64 && Cp % 64 == 0) {
-    dim3 grid((Hg * Wg + 63) / 64, Cp / 64, N);
+    const int ct = Cp / 64, t = tiles_per_block(ct, nb);
+    dim3 grid(nb, (ct + t - 1) / t, N);
     if (gate)
       to_grid_pm_k<64, true><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
-                                                  bpart, gate, gout);
+                                                  bpart, gate, gout, t);
     else
       to_grid_pm_k<64, false><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
-                                                   bpart, gate, gout);
+                                                   bpart, gate, gout, t);
   } else {
-    dim3 grid((Hg * Wg + 63) / 64, (Cp + 31) / 32, N);
+    const int ct = (Cp + 31) / 32, t = tiles_per_block(ct, nb);
+    dim3 grid(nb, (ct + t - 1) / t, N);
     if (gate)
       to_grid_pm_k<32, true><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
-                                                  bpart, gate, gout);
+                                                  bpart, gate, gout, t);
     else
       to_grid_pm_k<32, false><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
-                                                   bpart, gate, gout);
+                                                   bpart, gate, gout, t);
   }
 }
 
