@@ -1154,6 +1154,94 @@ __global__ void softmaxlog_bwd_k(const float* __restrict__ x, const float* __res
   }
 }
 
+// The same two kernels with a site's C <= 32*R scores held in registers: one
+// load pass with every load in flight instead of two (three) dependent
+// strided passes.  Per-lane order of the max / exp-sum and the warp
+// reductions are those of the kernels above, so results are bit-identical.
+template <int R>
+__global__ void softmaxlog_fwd_reg_k(const float* __restrict__ x, const float* __restrict__ labels,
+                                     const float* __restrict__ weights, float* site_loss,
+                                     int* flag, int HW, int C, int N) {
+  const int64_t sites = (int64_t)HW * N;
+  const int lane = threadIdx.x % 32;
+  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
+       s += (int64_t)gridDim.x * blockDim.x / 32) {
+    const int p = (int)(s % HW);
+    const int64_t n = s / HW;
+    const int c = read_label(labels, s, C, flag);
+    const float* xs = x + n * (int64_t)C * HW + p;
+    float v[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int k = lane + 32 * i;
+      v[i] = k < C ? __ldg(xs + (int64_t)k * HW) : -INFINITY;
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < R; ++i) mx = fmaxf(mx, v[i]);
+    mx = warp_max(mx);
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (lane + 32 * i < C) sum += expf(v[i] - mx);
+    sum = warp_sumf(sum);
+    if (lane == 0) {
+      float l = 0.f;
+      if (c > 0) {
+        float wgt = weights ? weights[s] : 1.f;
+        l = wgt * (-xs[(int64_t)(c - 1) * HW] + mx + logf(sum));
+      }
+      site_loss[s] = l;
+    }
+  }
+}
+
+template <int R, bool kAcc>
+__global__ void softmaxlog_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ labels,
+                                     const float* __restrict__ weights, float pscale, float* dx,
+                                     int* flag, int HW, int C, int N) {
+  const int64_t sites = (int64_t)HW * N;
+  const int lane = threadIdx.x % 32;
+  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
+       s += (int64_t)gridDim.x * blockDim.x / 32) {
+    const int p = (int)(s % HW);
+    const int64_t n = s / HW;
+    const int c = read_label(labels, s, C, flag);
+    const float* xs = x + n * (int64_t)C * HW + p;
+    float* ds = dx + n * (int64_t)C * HW + p;
+    if (c == 0) {  // ignored site: zero derivative (loss.cpp:252)
+      if (!kAcc)
+        for (int k = lane; k < C; k += 32) ds[(int64_t)k * HW] = 0.f;
+      continue;
+    }
+    float v[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int k = lane + 32 * i;
+      v[i] = k < C ? __ldg(xs + (int64_t)k * HW) : -INFINITY;
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < R; ++i) mx = fmaxf(mx, v[i]);
+    mx = warp_max(mx);
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+      if (lane + 32 * i < C) sum += expf(v[i] - mx);
+    sum = warp_sumf(sum);
+    const float scale = pscale * (weights ? weights[s] : 1.f);
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const int k = lane + 32 * i;
+      if (k < C) {
+        float soft = expf(v[i] - mx) / sum;
+        float r = scale * (soft - (k == c - 1 ? 1.f : 0.f));
+        ds[(int64_t)k * HW] = kAcc ? ds[(int64_t)k * HW] + r : r;
+      }
+    }
+  }
+}
+
 // classerror (loss.cpp:111-141; first strict maximum wins) and topk
 // (loss.cpp:142-149; rank = #{k : x_k >= x_c}), weighted, per site.
 __global__ void metrics_k(const float* __restrict__ x, const float* __restrict__ labels,
@@ -1561,8 +1649,12 @@ void softmaxlog_forward(const float* x, const float* labels, const float* weight
                         cudaStream_t s) {
   int64_t sites = (int64_t)HW * N;
   count_launch(2);
-  softmaxlog_fwd_k<<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, site_loss,
-                                                                flag, HW, C, N);
+  if (C <= 1024)
+    softmaxlog_fwd_reg_k<32><<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights,
+                                                                         site_loss, flag, HW, C, N);
+  else
+    softmaxlog_fwd_k<<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, site_loss,
+                                                                  flag, HW, C, N);
   sum_sites_k<<<1, 1024, 0, s>>>(site_loss, sites, loss);
 }
 
@@ -1570,6 +1662,15 @@ void softmaxlog_backward(const float* x, const float* labels, const float* weigh
                          float* dx, int* flag, int HW, int C, int N, int acc, cudaStream_t s) {
   int64_t sites = (int64_t)HW * N;
   count_launch();
+  if (C <= 1024) {
+    if (acc)
+      softmaxlog_bwd_reg_k<32, true><<<blocks_for(sites * 32, 256), 256, 0, s>>>(
+          x, labels, weights, p, dx, flag, HW, C, N);
+    else
+      softmaxlog_bwd_reg_k<32, false><<<blocks_for(sites * 32, 256), 256, 0, s>>>(
+          x, labels, weights, p, dx, flag, HW, C, N);
+    return;
+  }
   if (acc)
     softmaxlog_bwd_k<true><<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, p, dx,
                                                                         flag, HW, C, N);
