@@ -92,6 +92,9 @@ const char* ck_last_error(const ck_handle* h);
 const char* ck_version(void);
 /* Number of kernels this handle launched since creation (bench evidence). */
 int64_t ck_launch_count(const ck_handle* h);
+/* Of those, launches of the tcgen05 tensor-core GEMM (tc_gemm_kernel): lets a
+ * caller assert that a TF32 call really ran on the tensor cores. */
+int64_t ck_tc_launch_count(const ck_handle* h);
 /* Per-launch timing of the tensor-core GEMM kernels (bench roofline): while
  * on, every GEMM launch is bracketed by CUDA events on its stream and recorded
  * with a label and its algorithmic FLOP count (2*N*OH*OW*K*fh*fw*C/groups).
@@ -227,6 +230,10 @@ ck_status ck_graph_set_profiling(ck_graph* g, int enable);
 int ck_graph_layer_count(const ck_graph* g);
 const char* ck_graph_layer_name(const ck_graph* g, int layer);
 ck_status ck_graph_layer_ms(ck_graph* g, int layer, float* fwd_ms, float* bwd_ms);
+/* Engine options (not reference entry points):
+ *   "lrn_grid" (default 1): a TF32 conv -> relu -> lrn chain's LRN backward
+ *   writes the conv's ReLU-gated dy grid directly (0: the unfused blocks). */
+ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value);
 
 /* ---- cnn_train training step with multi-GPU data parallelism ------------ */
 typedef struct ck_trainer ck_trainer;
@@ -240,9 +247,20 @@ ck_status ck_trainer_init_dp(ck_trainer* t, const char id[128], int rank, int wo
  * If loss_host != NULL the step's objective is copied back (synchronising). */
 ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream);
 /* Replay each step as one CUDA graph: captured on the first graph step after
- * an eager one (same stream; profiling steps stay eager). Graph memory and
- * tensor maps are fixed at capture: shapes and buffers must not change. */
+ * an eager one (same stream; profiling steps stay eager).  A captured step is
+ * dropped and re-captured (after one eager step) whenever any workspace it
+ * points into was reallocated since, e.g. by a larger call on the handle. */
 ck_status ck_trainer_set_graph(ck_trainer* t, int on);
+/* Single GPU: run each layer's SGD on a side stream as soon as its
+ * derivatives are final (default 1), or in line on the step's stream (0). */
+ck_status ck_trainer_set_update_stream(ck_trainer* t, int on);
+/* Timing of the last profiled step (ck_graph_set_profiling on; such steps
+ * run eagerly): forward, backward, and the time from the end of backward to
+ * the completion of the last gradient allreduce + update (the exchange NOT
+ * hidden behind backward). */
+ck_status ck_trainer_last_timing(ck_trainer* t, float* fwd_ms, float* bwd_ms, float* tail_ms);
+/* NCCL allreduce groups issued by eager / captured steps (DP evidence). */
+int64_t ck_trainer_allreduce_count(const ck_trainer* t);
 
 /* ---- synthetic data (host): the reference generator, xoshiro256** seeded
  * via splitmix64 (rng.hpp:9-36, rng.cpp:10-59) ---------------------------- */

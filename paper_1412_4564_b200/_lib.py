@@ -56,6 +56,7 @@ SIGNATURES = {
     "ck_last_error": (C.c_char_p, [P]),
     "ck_version": (C.c_char_p, []),
     "ck_launch_count": (C.c_int64, [P]),
+    "ck_tc_launch_count": (C.c_int64, [P]),
     "ck_trainer_set_graph": (C.c_int, [P, C.c_int]),
     "ck_set_kernel_profiling": (C.c_int, [P, C.c_int]),
     "ck_kernel_profile_count": (C.c_int, [P]),
@@ -100,11 +101,16 @@ SIGNATURES = {
     "ck_graph_layer_count": (C.c_int, [P]),
     "ck_graph_layer_name": (C.c_char_p, [P, C.c_int]),
     "ck_graph_layer_ms": (S, [P, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "ck_graph_set_option": (S, [P, C.c_char_p, C.c_int64]),
     "ck_nccl_unique_id": (S, [C.c_char_p]),
     "ck_trainer_create": (S, [P, C.c_char_p, C.c_float, C.c_float, C.c_float, C.POINTER(P)]),
     "ck_trainer_destroy": (None, [P]),
     "ck_trainer_init_dp": (S, [P, C.c_char_p, C.c_int, C.c_int]),
     "ck_trainer_step": (S, [P, C.POINTER(C.c_float), P]),
+    "ck_trainer_set_update_stream": (S, [P, C.c_int]),
+    "ck_trainer_last_timing": (S, [P, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                                   C.POINTER(C.c_float)]),
+    "ck_trainer_allreduce_count": (C.c_int64, [P]),
     "ck_rng_create": (P, [C.c_uint64]),
     "ck_rng_destroy": (None, [P]),
     "ck_rng_uniform": (None, [P, P, C.c_int64, C.c_float, C.c_float]),

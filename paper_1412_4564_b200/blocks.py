@@ -130,6 +130,11 @@ class Handle:
     def launches(self) -> int:
         return lib().ck_launch_count(self.h)
 
+    @property
+    def tc_launches(self) -> int:
+        """tcgen05 GEMM launches (ck_tc_launch_count)."""
+        return lib().ck_tc_launch_count(self.h)
+
     def kernel_profiling(self, on: bool):
         """Time every tensor-core GEMM launch (ck_set_kernel_profiling)."""
         self.check(lib().ck_kernel_profile_clear(self.h))

@@ -6,6 +6,7 @@
 // Citations are to /root/reference/proj.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -19,8 +20,30 @@ using ck::Err;
 
 namespace ck {
 
+int knob(const char* name, int dflt) {
+#ifdef CK_EXPERIMENTS
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
+}
+
+bool experiments_build() {
+#ifdef CK_EXPERIMENTS
+  return true;
+#else
+  return false;
+#endif
+}
+
+static std::atomic<uint64_t> g_ws_gen{0};
+uint64_t workspace_generation() { return g_ws_gen.load(std::memory_order_relaxed); }
+
 void* Workspace::get(size_t want, cudaStream_t s) {
   if (want <= bytes) return ptr;
+  g_ws_gen.fetch_add(1, std::memory_order_relaxed);
   if (ptr) {
     cudaStreamSynchronize(s);
     cudaFree(ptr);
@@ -37,7 +60,10 @@ void* Workspace::get(size_t want, cudaStream_t s) {
 }
 
 void Workspace::release() {
-  if (ptr) cudaFree(ptr);
+  if (ptr) {
+    g_ws_gen.fetch_add(1, std::memory_order_relaxed);
+    cudaFree(ptr);
+  }
   ptr = nullptr;
   bytes = 0;
 }
@@ -167,6 +193,35 @@ void check_cuda(cudaError_t e, const char* what) {
 
 void after_launch() { check_cuda(cudaPeekAtLastError(), "kernel launch"); }
 
+// The device label/data flag (kernels.cu read_label): flag[0] bits, flag[1]
+// the first offending class label.  Messages are loss.cpp's (:14-18, :101-106,
+// :152-154, :201-203, :193-195).
+void throw_label_flag(int flag, int label, int64_t classes) {
+  if (flag & 1) throw Err(CK_ERR_DATA, "class label is not an integer");
+  if (flag & 2)
+    throw Err(CK_ERR_DATA, "class label " + std::to_string(label) + " out of range 1.." +
+                               std::to_string(classes));
+  if (flag & 4) throw Err(CK_ERR_DATA, "log loss needs a positive ground-truth score");
+  if (flag & 8) throw Err(CK_ERR_DATA, "attribute label is not an integer");
+  if (flag & 16) throw Err(CK_ERR_DATA, "attribute label must be -1, 0 or +1");
+  if (flag & 32) throw Err(CK_ERR_DATA, "binary log loss input must lie in [0,1]");
+}
+
+void reset_label_flag(ck_handle* h, cudaStream_t s) {
+  check_cuda(cudaMemsetAsync(h->flag, 0, 2 * sizeof(int), s), "flag");
+}
+
+void read_label_flag(ck_handle* h, cudaStream_t s) {
+  int flag[2] = {0, 0};
+  check_cuda(cudaMemcpyAsync(flag, h->flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, s), "flag");
+  check_cuda(cudaStreamSynchronize(s), "synchronize");
+  if (flag[0]) {
+    reset_label_flag(h, s);
+    throw_label_flag(flag[0], flag[1], h->last_classes);
+  }
+}
+
+
 // ---- conv dispatch (shared by the C ABI and the graph engine) ----------------
 
 // a profiler label left by a tensor-core path that declined the shape
@@ -227,7 +282,9 @@ using namespace ck;
 
 extern "C" {
 
-const char* ck_version(void) { return "ck 0.1 (sm_100a)"; }
+const char* ck_version(void) {
+  return ck::experiments_build() ? "ck 0.2 (sm_100a, CK_EXPERIMENTS)" : "ck 0.2 (sm_100a)";
+}
 
 ck_status ck_create(ck_handle** out, int device) {
   if (!out) return CK_ERR_ARG;
@@ -235,11 +292,11 @@ ck_status ck_create(ck_handle** out, int device) {
   if (cudaSetDevice(device) != cudaSuccess) return CK_ERR_CUDA;
   ck_handle* h = new ck_handle();
   h->device = device;
-  if (cudaMalloc(&h->flag, sizeof(int)) != cudaSuccess) {
+  if (cudaMalloc(&h->flag, 2 * sizeof(int)) != cudaSuccess) {
     delete h;
     return CK_ERR_CUDA;
   }
-  cudaMemset(h->flag, 0, sizeof(int));
+  cudaMemset(h->flag, 0, 2 * sizeof(int));
   *out = h;
   return CK_OK;
 }
@@ -256,6 +313,8 @@ void ck_destroy(ck_handle* h) {
 }
 
 const char* ck_last_error(const ck_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+int64_t ck_tc_launch_count(const ck_handle* h) { return h ? h->counter.tc : 0; }
 
 int64_t ck_launch_count(const ck_handle* h) { return h ? h->counter.n : 0; }
 
@@ -664,17 +723,6 @@ static void check_loss(const ck_tensor* x, const ck_tensor* labels, const ck_ten
                                 shape_str(cs));
 }
 
-static void read_label_flag(ck_handle* h, cudaStream_t s) {
-  int flag = 0;
-  check_cuda(cudaMemcpyAsync(&flag, h->flag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag");
-  check_cuda(cudaStreamSynchronize(s), "synchronize");
-  if (flag) {
-    cudaMemsetAsync(h->flag, 0, sizeof(int), s);
-    if (flag & 1) throw Err(CK_ERR_DATA, "class label is not an integer");
-    throw Err(CK_ERR_DATA, "class label out of range 1.." + std::to_string(h->last_classes));
-  }
-}
-
 ck_status ck_softmaxlog_forward(ck_handle* h, const ck_tensor* x, const ck_tensor* labels,
                                 const ck_tensor* weights, float* loss, int check_labels,
                                 ck_stream stream) {
@@ -687,6 +735,7 @@ ck_status ck_softmaxlog_forward(ck_handle* h, const ck_tensor* x, const ck_tenso
   float* site = (float*)h->scratch.get(sizeof(float) * sites, st);
   if (!site) throw Err(CK_ERR_CUDA, "workspace allocation failed");
   h->last_classes = s.c;
+  if (check_labels) reset_label_flag(h, st);  // no stale bit from an unchecked call
   softmaxlog_forward(x->data, labels->data, weights ? weights->data : nullptr, site, loss, h->flag,
                      (int)(s.h * s.w), (int)s.c, (int)s.n, st);
   after_launch();
@@ -702,8 +751,8 @@ ck_status ck_softmaxlog_backward(ck_handle* h, const ck_tensor* x, const ck_tens
   check_out(dx, x->shape, "dx");
   const ck_shape& s = x->shape;
   h->last_classes = s.c;
-  softmaxlog_backward(x->data, labels->data, weights ? weights->data : nullptr, p, dx->data,
-                      h->flag, (int)(s.h * s.w), (int)s.c, (int)s.n, accumulate,
+  softmaxlog_backward(x->data, labels->data, weights ? weights->data : nullptr, p, nullptr,
+                      dx->data, h->flag, (int)(s.h * s.w), (int)s.c, (int)s.n, accumulate,
                       (cudaStream_t)stream);
   after_launch();
   CK_API_END(h)

@@ -88,6 +88,11 @@ ConvDims conv_dims(const ck_shape& x, const ck_shape& f, const ck_shape& y, cons
 PoolDims pool_dims(const ck_shape& x, const ck_shape& y, const ck_pool_geom& g);
 void check_cuda(cudaError_t e, const char* what);
 void after_launch();
+// the device label/data-error flag of h (2 ints): reset, read (synchronising
+// s, throws CK_ERR_DATA with the reference's message), decode a copied value
+void reset_label_flag(ck_handle* h, cudaStream_t s);
+void read_label_flag(ck_handle* h, cudaStream_t s);
+void throw_label_flag(int flag, int label, int64_t classes);
 
 void conv_forward_dispatch(ck_handle* h, const float* x, const float* f, const float* bias,
                            float* y, const ConvDims& d, int relu, ck_math math, cudaStream_t s);

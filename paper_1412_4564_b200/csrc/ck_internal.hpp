@@ -35,6 +35,18 @@ struct PoolDims {
   int mode;  // 0 max, 1 avg
 };
 
+// Bumped whenever any Workspace frees or moves its buffer.  A captured CUDA
+// graph holds raw pointers into workspaces (and TMA descriptors encoding
+// them), so the trainer re-captures when the generation it captured under
+// is no longer current.
+uint64_t workspace_generation();
+
+// Tuning / experiment knobs (CK_* environment variables).  Product builds
+// ignore the environment and return dflt; only a -DCK_EXPERIMENTS build reads
+// them, so no variable can change what a production kernel computes.
+int knob(const char* name, int dflt);
+bool experiments_build();
+
 // Per-handle scratch owned by the C ABI / engine.
 struct Workspace {
   void* ptr = nullptr;
@@ -56,6 +68,7 @@ struct ConvCache {
 
 struct LaunchCounter {
   int64_t n = 0;
+  int64_t tc = 0;  // of which tcgen05 tensor-core GEMM launches (tc_gemm_kernel)
 };
 
 // ---- launchers (kernels.cu / conv_simt.cu / conv_tc.cu) -------------------
@@ -90,6 +103,9 @@ inline void prof_next(const std::string& label, double flops) {
 }
 inline void count_launch(int k = 1) {
   if (g_counter) g_counter->n += k;
+}
+inline void count_tc_launch() {
+  if (g_counter) g_counter->tc += 1;
 }
 
 void relu_forward(const float* x, float* y, int64_t n, cudaStream_t s);
@@ -133,8 +149,10 @@ void bnorm_backward_apply(const float* x, const float* dy, const float* w, const
 void softmaxlog_forward(const float* x, const float* labels, const float* weights,
                         float* site_loss, float* loss, int* flag, int HW, int C, int N,
                         cudaStream_t s);
+// p_dev (nullable): the projection read on the device instead of p.
 void softmaxlog_backward(const float* x, const float* labels, const float* weights, float p,
-                         float* dx, int* flag, int HW, int C, int N, int acc, cudaStream_t s);
+                         const float* p_dev, float* dx, int* flag, int HW, int C, int N, int acc,
+                         cudaStream_t s);
 void loss_metrics(const float* x, const float* labels, const float* weights, int top_k,
                   float* site_buf, float* top1, float* topk, int* flag, int HW, int C, int N,
                   cudaStream_t s);

@@ -65,6 +65,14 @@ enum EpiKind : int {
   EPI_S2D = 2,     // row m = s2d pixel (n, v, u), col c' = (a, b, c) -> x[s*u+a, s*v+b, c]
 };
 
+// Debug experiments that drop MMAs / loads / the epilogue exist only in
+// CK_EXPERIMENTS builds; a product kernel always does all of its work.
+#ifdef CK_EXPERIMENTS
+#define TC_EXP(p) ((p).exp)
+#else
+#define TC_EXP(p) 0
+#endif
+
 struct GemmParams {
   int M, N, K;            // problem (per group), K in elements (multiple of 32)
   int BN;                 // tile N (multiple of 16, <= 256)
@@ -738,10 +746,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         for (int kb = T.kb0; kb < T.kb1; ++kb) {
-          if (p.exp != 5) mbar_wait(&empty[s], ph ^ 1);  // exp 5: no producer
-          if (p.exp == 2) {  // experiment: no operand loads (measures MMA + smem reads)
+          if (TC_EXP(p) != 5) mbar_wait(&empty[s], ph ^ 1);  // exp 5: no producer
+          if (TC_EXP(p) == 2) {  // experiment: no operand loads (measures MMA + smem reads)
             if (lead) mbar_arrive(&full[s]);
-          } else if (p.exp != 5) {
+          } else if (TC_EXP(p) != 5) {
             mbar_expect_tx_p(&full[s], bytes, lead);
             uint8_t* a = sA + s * stage_a;
             uint8_t* b = sB + s * stage_b;
@@ -822,8 +830,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ak = a_mn ? 64 : 2, bk = b_mn ? 64 : 2;
       const uint32_t ah = a_mn ? KS * 32 : 1024;
       const uint32_t sa16 = stage_a >> 4, sb16 = stage_b >> 4;
-      const bool do_mma = p.exp != 1;      // exp 1: no MMAs (TMA only)
-      const bool wait_full = p.exp != 5;   // exp 5: MMAs only (no operand handshake)
+      const bool do_mma = TC_EXP(p) != 1;      // exp 1: no MMAs (TMA only)
+      const bool wait_full = TC_EXP(p) != 5;   // exp 5: MMAs only (no operand handshake)
       // MMA groups per stage: (half h, 32-k chunk c) -> g = h * chunks + c
       const int chunks = KS / 32, ng = halves * chunks;
       uint32_t ga[4] = {0, 0, 0, 0}, gb[4] = {0, 0, 0, 0}, gd[4] = {0, 0, 0, 0}, first_mask = 0;
@@ -916,7 +924,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       unsigned long long e1 = clock64();
       e_w += e1 - e0;
 #endif
-      if (p.exp != 5)  // exp 5: no epilogue work
+      if (TC_EXP(p) != 5)  // exp 5: no epilogue work
         epilogue_tile(p, T, tmem + (uint32_t)(ab * acc_cols), T.kb0 >= T.kb1, halves, warp, lane,
                       bias0);
       tc_fence_before();
@@ -942,6 +950,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+#ifdef CK_EXPERIMENTS  // measured slower than im2col: not in product builds
 // ============================================================================
 //                      halo kernel (stride-1 implicit GEMM)
 // ============================================================================
@@ -1153,6 +1162,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // HWCN x[n][c][w][h] -> padded pixel-major grid xg[n][Wg][Hg][cp]: pixel
 // (i, j) at grid position (i + oh, j + ow), channel c of group g at
+#endif  // CK_EXPERIMENTS
+
 // cp = g*Cgp + (c - g*Cgp_local); zero borders and channel pads (the input of
 // halo_conv_kernel).  32 x 32 smem tile transpose.
 // With gate != nullptr the source is relu-gated first (v = gate > 0 ? x : 0,
@@ -1255,10 +1266,10 @@ static void grid_pm_launch(const float* x, float* xg, int H, int W, int C, int N
                            int groups, int Hg, int Wg, int oh, int ow, double* bpart,
                            const float* gate, float* gout, cudaStream_t s) {
   const int Cp = Cgp * groups;
-  static const int ch = getenv("CK_GRID_CH") ? atoi(getenv("CK_GRID_CH")) : 32;  // experiments
+  static const int ch = knob("CK_GRID_CH", 32);  // experiments
   // channel tiles per block: enough blocks for ~8 resident per SM, each
   // walking several tiles
-  static const int tpb_env = getenv("CK_GRID_TPB") ? atoi(getenv("CK_GRID_TPB")) : 0;
+  static const int tpb_env = knob("CK_GRID_TPB", 0);
   auto tiles_per_block = [&](int ctiles, int nb) {
     if (tpb_env > 0) return std::min(tpb_env, ctiles);
     int t = 1;
@@ -1645,7 +1656,7 @@ static CUtensorMap map_im2col(const float* base, int Cp, int H, int W, int N, in
 
 static int pick_bn(int n) {
   // largest MMA N (multiple of 16, <= 256) that tiles n with little waste
-  static const int force = getenv("CK_TC_BN") ? atoi(getenv("CK_TC_BN")) : 0;  // experiments
+  static const int force = knob("CK_TC_BN", 0);  // experiments
   if (force > 0 && force < n) return force;
   if (n <= 256) return rup(n, 16);
   const int cands[] = {256, 192, 128};
@@ -1669,7 +1680,7 @@ static int pick_bn(int n) {
 // then serialises with the next tile) and BM = 128 charged 8 % for its extra
 // B traffic.  FC / wgrad GEMMs: BM = 256 only when TMEM stays double-buffered.
 static int pick_bm(int64_t M, int BN, bool conv = false, int nt = 1) {
-  static const int mode = getenv("CK_TC_BM") ? atoi(getenv("CK_TC_BM")) : 0;  // experiments
+  static const int mode = knob("CK_TC_BM", 0);  // experiments
   if (mode == 256) return M >= 4096 ? 256 : 128;
   if (mode == 128) return 128;
   if (M < 4096) return 128;
@@ -1685,9 +1696,9 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
                    int grid_n, int grid_z, cudaStream_t s) {
   (void)grid_m;
   (void)grid_n;
-  static const int exp = getenv("CK_TC_EXP") ? atoi(getenv("CK_TC_EXP")) : 0;
-  p.exp = exp;
-  static const int snake = getenv("CK_EPI_SNAKE") ? atoi(getenv("CK_EPI_SNAKE")) : 1;
+  static const int exp = knob("CK_TC_EXP", 0);
+  p.exp = exp;  // (read by the kernel only in CK_EXPERIMENTS builds)
+  static const int snake = knob("CK_EPI_SNAKE", 1);
   p.snake = snake;
   if (p.BM != 128 && p.BM != 256) p.BM = 128;
   p.groups = grid_z / p.splits;
@@ -1707,7 +1718,8 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
   const int tiles = ((p.M + p.BM - 1) / p.BM) * ((p.N + p.BN - 1) / p.BN) * grid_z;
   const int grid = std::min(tiles, 148);
   count_launch();
-  static const int mprof = getenv("CK_TC_PROF") ? atoi(getenv("CK_TC_PROF")) : 0;
+  count_tc_launch();
+  static const int mprof = knob("CK_TC_PROF", 0);
   static unsigned long long* mbuf = nullptr;
   if (mprof && !mbuf) cudaMalloc(&mbuf, (148 * 8 + 512) * sizeof(unsigned long long));
   p.prof = mprof ? mbuf : nullptr;
@@ -1764,7 +1776,7 @@ static void prof_conv(const char* pass, const ConvDims& d) {
 
 static int split_for(int tiles, int kblocks) {
   // fill ~1 wave of 148 SMs; keep >= 8 k-blocks per split
-  static const int force = getenv("CK_TC_SPLITS") ? atoi(getenv("CK_TC_SPLITS")) : 0;
+  static const int force = knob("CK_TC_SPLITS", 0);
   if (force > 0) return std::min(force, std::max(1, kblocks));
   int s = 1;
   while (tiles * s * 2 <= 148 && kblocks / (s * 2) >= 8) s *= 2;
@@ -1776,7 +1788,7 @@ static int split_for(int tiles, int kblocks) {
 // makespan, waves * (K blocks per split + a per-tile fill/epilogue cost of
 // ~24 K blocks), over splits that keep >= 16 K blocks per split.
 static int wgrad_splits_for(int tiles, int kblocks) {
-  static const int force = getenv("CK_TC_SPLITS") ? atoi(getenv("CK_TC_SPLITS")) : 0;
+  static const int force = knob("CK_TC_SPLITS", 0);
   if (force > 0) return std::min(force, std::max(1, kblocks));
   const int max_sp = std::max(1, std::min(64, kblocks / 16));
   int best = 1;
@@ -1816,8 +1828,7 @@ static void to_grid_pm(const float* x, float* xg, int H, int W, int C, int N, in
 static bool halo_enabled() {
   // Off by default: measured slower than the im2col kernels on AlexNet
   // (junk grid rows + per-tap filter streaming), kept for experiments.
-  const char* v = getenv("CK_TC_HALO");  // read per call: tests toggle it
-  return v && atoi(v) != 0;
+  return knob("CK_TC_HALO", 0) != 0;  // experiments builds only (read per call)
 }
 
 static CUtensorMap encode_tiled(const float* base, int rank, const cuuint64_t* dims,
@@ -1847,12 +1858,15 @@ static bool halo_ok(int rows, int fh, int fw, int Hg) {
 
 // p carries the epilogue fields (epi, out, ld, img_stride, grp_col, bias, relu,
 // acc, s2d_*); returns false when the shape does not fit the kernel.
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v ? atoi(v) : dflt;
-}
+static int env_int(const char* name, int dflt) { return knob(name, dflt); }
 
 static bool halo_launch(const HaloConv& hc, GemmParams p, cudaStream_t s) {
+#ifndef CK_EXPERIMENTS
+  (void)hc;
+  (void)p;
+  (void)s;
+  return false;
+#else
   if (!halo_enabled()) return false;
   static const int bm_env = env_int("CK_HALO_BM", 256), sb_env = env_int("CK_HALO_SB", 3),
                    tt_env = env_int("CK_HALO_TT", 0), cs_env = env_int("CK_HALO_CS", 2),
@@ -1967,6 +1981,7 @@ static bool halo_launch(const HaloConv& hc, GemmParams p, cudaStream_t s) {
   if (cudaLaunchKernelEx(&cfg, halo_conv_kernel<2>, ta, tb, p) != cudaSuccess)
     throw Err(CK_ERR_CUDA, "halo_conv_kernel cluster launch failed");
   return true;
+#endif
 }
 
 // dy at (0, 0) of an Hg x Wg zero grid, pixel-major [n][Wg][Hg][groups*Kgp]:
@@ -2086,7 +2101,7 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
 // fewer junk rows for the weight-gradient reduction.
 static void grid_dims(const ConvDims& d, int& Hg, int& Wg) {
   const bool shared = std::min(d.pt, d.pb) < d.fh && std::min(d.pl, d.pr) < d.fw &&
-                      !getenv("CK_TC_FULLGRID");
+                      !knob("CK_TC_FULLGRID", 0);
   Hg = d.H + (shared ? std::max(d.pt, d.pb) : d.pt + d.pb);
   Wg = d.W + (shared ? std::max(d.pl, d.pr) : d.pl + d.pr);
 }
@@ -2200,8 +2215,7 @@ static float* x_s2d(ck_handle* h, const float* x, const ConvDims& d, const S2D& 
 // more than the cheaper tiled boxes save -- these GEMMs are bound by shared-
 // memory operand traffic, not TMA issue.  CK_TC_SHIFT=1.
 static bool shift_enabled() {
-  const char* v = getenv("CK_TC_SHIFT");  // read per call: tests toggle it
-  return v && atoi(v) != 0;
+  return knob("CK_TC_SHIFT", 0) != 0;  // experiments builds only (read per call)
 }
 
 // Stride-1 implicit GEMM on a zero-padded pixel-major grid G[N*Hg*Wg][Cp]
@@ -2214,6 +2228,11 @@ static bool shift_enabled() {
 static void shift_conv(const float* G, int Cp, int Hg, int Wg, int N, int base_shift,
                        const float* F, int Cgp, int taps, int fh, int rows, int groups, int ohv,
                        int owv, GemmParams p, cudaStream_t s) {
+#ifndef CK_EXPERIMENTS
+  (void)G; (void)Cp; (void)Hg; (void)Wg; (void)N; (void)base_shift; (void)F; (void)Cgp;
+  (void)taps; (void)fh; (void)rows; (void)groups; (void)ohv; (void)owv; (void)p; (void)s;
+  throw Err(CK_ERR_ARG, "shifted-grid kernels are built only with CK_EXPERIMENTS");
+#else
   const int64_t M = (int64_t)N * Hg * Wg;
   p.M = (int)M;
   p.N = rows;
@@ -2244,6 +2263,7 @@ static void shift_conv(const float* G, int Cp, int Hg, int Wg, int N, int base_s
   cuuint32_t bbox[3] = {32, (cuuint32_t)p.BN, (cuuint32_t)(KS / 32)};
   CUtensorMap tb = encode_tiled(F, 3, bdims, bstr, bbox, CU_TENSOR_MAP_SWIZZLE_128B);
   launch<OP_SHIFT_K, OP_TILED_K3>(ta, tb, p, 0, 0, groups, s);
+#endif
 }
 
 static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float* bias, float* y,
@@ -2403,7 +2423,7 @@ static int grid_wgrad(ck_handle* h, const float* xg, int Cp, int Cgp, const floa
   // 10 x 160), larger on ties
   int BN = Cgp;
   if (Cgp < 128 || Cgp > 256) {
-    static const int force_bn = getenv("CK_TC_WBN") ? atoi(getenv("CK_TC_WBN")) : 0;
+    static const int force_bn = knob("CK_TC_WBN", 0);
     BN = 0;
     int best = INT32_MAX;
     for (int c = 256; c >= 64; c -= 32) {
@@ -2419,7 +2439,7 @@ static int grid_wgrad(ck_handle* h, const float* xg, int Cp, int Cgp, const floa
   const int BM = pick_bm(Kg, BN);
   const int64_t rows = (int64_t)N * Hg * Wg;
   // 64 grid rows per stage: half the TMA boxes per FLOP (both operands MN-major)
-  static const int ks_env = getenv("CK_TC_WKS") ? atoi(getenv("CK_TC_WKS")) : 64;
+  static const int ks_env = knob("CK_TC_WKS", 64);
   const int KS = ks_env == 32 ? 32 : 64;
   const int kblocks = (int)((rows + KS - 1) / KS);
   const int splits = wgrad_splits_for(((Kg + BM - 1) / BM) * ((Ntot + BN - 1) / BN) * groups,

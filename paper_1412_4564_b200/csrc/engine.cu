@@ -116,6 +116,9 @@ struct ck_graph {
   std::vector<void*> allocs;
   float* param_deriv_arena = nullptr;
   size_t param_deriv_elems = 0;
+  float* one_dev = nullptr;  // the objective seed 1.0f, device-resident (graph-capturable)
+  bool has_loss = false;
+  bool lrn_grid = true;  // option "lrn_grid": LRN backward writes the conv's dy grid
   int64_t last_launches = 0;
   bool profiling = false;
   // per layer: fwd begin/end, bwd begin/end
@@ -300,16 +303,44 @@ static void finalize(ck_graph* g) {
     g->allocs.push_back(p);
     return (float*)p;
   };
+  // A parameter's derivative is final once the backward of its FIRST
+  // consumer in firing order has run (every other consumer comes before it
+  // in backward order); the arena follows that completion order, so the
+  // parameters one layer finishes (ck_trainer::done) are adjacent.
+  std::vector<int> pos(g->layers.size());
+  for (size_t k = 0; k < g->order.size(); ++k) pos[g->order[k]] = (int)k;
+  std::vector<std::pair<int, int>> fin;  // (-firing position of first consumer, var)
+  for (size_t i = 0; i < g->vars.size(); ++i) {
+    const Var& v = g->vars[i];
+    if (v.role != 1 || v.consumers.empty()) continue;
+    int first = (int)g->order.size();
+    for (auto [c, sl] : v.consumers) {
+      (void)sl;
+      first = std::min(first, pos[c]);
+    }
+    fin.push_back({-first, (int)i});
+  }
+  std::stable_sort(fin.begin(), fin.end(),
+                   [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+                     return a.first < b.first;
+                   });
   std::vector<int> param_order;
-  for (auto it = g->order.rbegin(); it != g->order.rend(); ++it)
-    for (int i : g->layers[*it].in)
-      if (g->vars[i].role == 1 &&
-          std::find(param_order.begin(), param_order.end(), i) == param_order.end())
-        param_order.push_back(i);
+  for (auto& f : fin) param_order.push_back(f.second);
+  for (size_t i = 0; i < g->vars.size(); ++i)  // params nobody consumes
+    if (g->vars[i].role == 1 && g->vars[i].consumers.empty()) param_order.push_back((int)i);
   size_t total = 0;
   for (int i : param_order) total += (size_t)((elems(g->vars[i].shape) + 31) / 32 * 32);
   g->param_deriv_arena = alloc(total);
   g->param_deriv_elems = total;
+  // zero once: the 32-element pads between parameters are inside allreduce spans
+  check_cuda(cudaMemset(g->param_deriv_arena, 0, sizeof(float) * std::max<size_t>(total, 1)),
+             "memset");
+  g->one_dev = alloc(1);
+  {
+    const float one = 1.0f;
+    check_cuda(cudaMemcpy(g->one_dev, &one, sizeof(float), cudaMemcpyHostToDevice), "seed");
+  }
+  for (auto& l : g->layers) g->has_loss |= l.kind == Kind::loss;
   size_t off = 0;
   for (int i : param_order) {
     g->vars[i].deriv = g->param_deriv_arena + off;
@@ -421,7 +452,7 @@ static void materialize_lrn(ck_graph* g, Var& v, cudaStream_t s) {
   v.lazy_lrn = -1;
 }
 
-static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) {
+static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
   ck_handle* h = g->h;
   auto V = [&](int k) { return tv(g->vars[l.in[k]], false); };
   auto D = [&](int k) { return tv(g->vars[l.in[k]], true); };
@@ -534,7 +565,7 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
       // relu output's derivative is then computed only on request
       Var& xv = g->vars[l.in[0]];
       if (!acc(0) && g->math == CK_MATH_TF32 && xv.producer >= 0 && xv.consumers.size() == 1 &&
-          getenv("CK_NO_LRN_GRID") == nullptr) {
+          g->lrn_grid) {
         Layer& r = g->layers[xv.producer];
         if (r.kind == Kind::relu && r.fused_by >= 0 && r.fused_bwd) {
           Layer& c = g->layers[r.fused_by];
@@ -588,7 +619,12 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
     case Kind::loss: {
       ck_tensor x = V(0), c = V(1), dx = D(0), w;
       if (l.in.size() > 2) w = V(2);
-      st = ck_softmaxlog_backward(h, &x, &c, l.in.size() > 2 ? &w : nullptr, seed_p, &dx, acc(0), s);
+      // the projection (graph.cpp:420-425: proj[0][0], 1 for the objective) is
+      // read on the device from the loss output's derivative: no host sync
+      softmaxlog_backward(x.data, c.data, l.in.size() > 2 ? w.data : nullptr, 1.0f,
+                          g->vars[l.out[0]].deriv, dx.data, h->flag, (int)(x.shape.h * x.shape.w),
+                          (int)x.shape.c, (int)x.shape.n, acc(0), s);
+      after_launch();
       mark(0);  // labels / weights carry no derivative: left for the final zeroing
       break;
     }
@@ -611,6 +647,8 @@ static void layer_backward(ck_graph* g, Layer& l, float seed_p, cudaStream_t s) 
 // graph.cpp:494-545 forward (train mode).
 static void run_forward(ck_graph* g, cudaStream_t s) {
   for (auto& l : g->layers) l.cache.valid = false;
+  // loss layers record label errors (loss.cpp:101-106) in the handle's flag
+  if (g->has_loss) reset_label_flag(g->h, s);
   for (int li : g->order) {
     g->prof(li, 0, s);
     layer_forward(g, g->layers[li], s);
@@ -636,23 +674,16 @@ static void run_backward(ck_graph* g, int objective, cudaStream_t s, LayerDone* 
   for (auto& l : g->layers) l.bwd_deferred = false;
   Var& obj = g->vars[objective];
   if (elems(obj.shape) != 1) throw Err(CK_ERR_ARG, "objective '" + obj.name + "' is not a scalar");
-  const float one = 1.0f;
-  check_cuda(cudaMemcpyAsync(obj.deriv, &one, sizeof(float), cudaMemcpyHostToDevice, s), "seed");
+  check_cuda(cudaMemcpyAsync(obj.deriv, g->one_dev, sizeof(float), cudaMemcpyDeviceToDevice, s),
+             "seed");
   obj.deriv_live = true;
   for (auto it = g->order.rbegin(); it != g->order.rend(); ++it) {
     Layer& l = g->layers[*it];
     bool any = false;
     for (int o : l.out) any |= g->vars[o].deriv_live;
     if (any) {
-      // A loss layer's projection is the objective seed (graph.cpp:420-425).
-      float p = 1.0f;
-      if (l.kind == Kind::loss && l.out[0] != objective) {
-        check_cuda(cudaMemcpyAsync(&p, g->vars[l.out[0]].deriv, sizeof(float),
-                                   cudaMemcpyDeviceToHost, s), "projection");
-        check_cuda(cudaStreamSynchronize(s), "synchronize");
-      }
       g->prof(*it, 2, s);
-      layer_backward(g, l, p, s);
+      layer_backward(g, l, s);
       g->prof(*it, 3, s);
       if (g->profiling) g->prof_bwd_done[*it] = 1;
     }
@@ -682,6 +713,17 @@ struct ck_trainer : ck::LayerDone {
   cudaEvent_t comm_done = nullptr;
   std::vector<std::vector<int>> layer_params;  // params finished by layer li
   float* loss_dev = nullptr;
+  int64_t allreduces = 0;          // NCCL allreduce groups issued (evidence)
+  bool update_stream = true;       // single GPU: SGD on a side stream
+  // label/data flag of each step, copied to pinned host memory at its end
+  // and checked when that copy is known complete (CK_ERR_DATA, loss.cpp:101-106)
+  int* flag_host = nullptr;
+  cudaEvent_t flag_ev = nullptr;
+  bool flag_pending = false;
+  // step timing (profiling steps only): forward / backward on the compute
+  // stream, and the end of the last allreduce+SGD on the comm stream
+  cudaEvent_t t_begin = nullptr, t_fwd = nullptr, t_bwd = nullptr, t_comm = nullptr;
+  bool timed = false;
   // single GPU: each layer's SGD runs on an update stream as soon as that
   // layer's backward is done, overlapping the rest of the backward (the
   // streaming update fits beside a persistent GEMM's CTAs on the same SMs)
@@ -699,30 +741,50 @@ struct ck_trainer : ck::LayerDone {
     std::vector<float*> inputs;
     cudaGraphExec_t exec;
     int64_t launches;
+    uint64_t gen;  // workspace generation the captured pointers belong to
   };
+  uint64_t eager_gen = 0;  // workspace generation after the last eager step
   std::vector<Captured> graphs;
 
   void done(int li, cudaStream_t s) override {
     const auto& ps = layer_params[li];
     if (ps.empty()) return;
+    // a parameter no live derivative reached (its consumers' backward did not
+    // run) has the reference's zero derivative (graph.cpp:551-554) -- before
+    // the allreduce and the update read it
+    for (int p : ps) {
+      ck::Var& v = g->vars[p];
+      if (!v.deriv_live) {
+        ck::check_cuda(cudaMemsetAsync(v.deriv, 0, sizeof(float) * ck::elems(v.shape), s), "zero");
+        v.deriv_live = true;
+      }
+    }
     if (comm) {
-      // Contiguous bucket [first, last] of this layer's parameter derivs.
-      float* lo = nullptr;
-      float* hi = nullptr;
+      // this layer's finished parameters are adjacent in the arena (finalize):
+      // one allreduce per contiguous run (normally exactly one per layer)
+      std::vector<std::pair<float*, float*>> runs;
       for (int p : ps) {
         ck::Var& v = g->vars[p];
-        float* a = v.deriv;
-        float* b = v.deriv + ck::elems(v.shape);
-        if (!lo || a < lo) lo = a;
-        if (!hi || b > hi) hi = b;
+        runs.push_back({v.deriv, v.deriv + (ck::elems(v.shape) + 31) / 32 * 32});
       }
+      std::sort(runs.begin(), runs.end());
+      std::vector<std::pair<float*, float*>> merged;
+      for (auto& r : runs)
+        if (!merged.empty() && r.first <= merged.back().second)
+          merged.back().second = std::max(merged.back().second, r.second);
+        else
+          merged.push_back(r);
       ck::check_cuda(cudaEventRecord(ev[li], s), "event");
       ck::check_cuda(cudaStreamWaitEvent(comm_stream, ev[li], 0), "wait");
-      if (ncclAllReduce(lo, lo, (size_t)(hi - lo), ncclFloat, ncclSum, comm, comm_stream) !=
-          ncclSuccess)
-        throw Err(CK_ERR_CUDA, "ncclAllReduce failed");
+      if (ncclGroupStart() != ncclSuccess) throw Err(CK_ERR_CUDA, "ncclGroupStart failed");
+      for (auto& r : merged)
+        if (ncclAllReduce(r.first, r.first, (size_t)(r.second - r.first), ncclFloat, ncclSum, comm,
+                          comm_stream) != ncclSuccess)
+          throw Err(CK_ERR_CUDA, "ncclAllReduce failed");
+      if (ncclGroupEnd() != ncclSuccess) throw Err(CK_ERR_CUDA, "ncclGroupEnd failed");
+      ++allreduces;
       for (int p : ps) sgd(p, comm_stream);
-    } else if (getenv("CK_NO_UPDATE_STREAM")) {
+    } else if (!update_stream) {
       for (int p : ps) sgd(p, s);
     } else {
       if (!upd_stream) {
@@ -767,6 +829,9 @@ struct ck_trainer : ck::LayerDone {
     if (comm_stream) cudaStreamDestroy(comm_stream);
     if (comm) ncclCommDestroy(comm);
     if (loss_dev) cudaFree(loss_dev);
+    if (flag_host) cudaFreeHost(flag_host);
+    for (auto e : {flag_ev, t_begin, t_fwd, t_bwd, t_comm})
+      if (e) cudaEventDestroy(e);
   }
 };
 
@@ -892,6 +957,14 @@ ck_status ck_graph_forward(ck_graph* g, ck_stream stream) {
   int64_t before = g->h->counter.n;
   run_forward(g, (cudaStream_t)stream);
   g->last_launches = g->h->counter.n - before;
+  // the reference throws DataError from the loss layer: read the flag now
+  if (g->has_loss) {
+    try {
+      read_label_flag(g->h, (cudaStream_t)stream);
+    } catch (const Err& e) {
+      throw Err(e.code, std::string("loss layer: ") + e.what());
+    }
+  }
   CKG_END(g)
 }
 
@@ -915,6 +988,16 @@ ck_status ck_graph_set_profiling(ck_graph* g, int enable) {
   g->prof_fwd_done.assign(g->layers.size(), 0);
   g->prof_bwd_done.assign(g->layers.size(), 0);
   g->profiling = enable != 0;
+  CKG_END(g)
+}
+
+ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value) {
+  CKG_BEGIN(g)
+  const std::string n = name ? name : "";
+  if (n == "lrn_grid")
+    g->lrn_grid = value != 0;
+  else
+    throw Err(CK_ERR_ARG, "unknown graph option '" + n + "'");
   CKG_END(g)
 }
 
@@ -982,6 +1065,11 @@ ck_status ck_trainer_create(ck_graph* g, const char* objective, float lr, float 
   for (auto& e : t->ev) check_cuda(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   check_cuda(cudaEventCreateWithFlags(&t->comm_done, cudaEventDisableTiming), "event");
   check_cuda(cudaMalloc(&t->loss_dev, sizeof(float)), "cudaMalloc");
+  check_cuda(cudaHostAlloc(&t->flag_host, 2 * sizeof(int), cudaHostAllocDefault), "host alloc");
+  t->flag_host[0] = t->flag_host[1] = 0;
+  check_cuda(cudaEventCreateWithFlags(&t->flag_ev, cudaEventDisableTiming), "event");
+  for (cudaEvent_t* e : {&t->t_begin, &t->t_fwd, &t->t_bwd, &t->t_comm})
+    check_cuda(cudaEventCreate(e), "event");
   *out = t.release();
   CKG_END(g)
 }
@@ -998,9 +1086,12 @@ ck_status ck_trainer_init_dp(ck_trainer* t, const char id[128], int rank, int wo
   ck_graph* g = t->g;
   CKG_BEGIN(g)
   if (world < 1 || rank < 0 || rank >= world) throw Err(CK_ERR_ARG, "bad rank/world");
+  if (t->comm) throw Err(CK_ERR_ARG, "data parallelism already initialised");
   t->rank = rank;
   t->world = world;
-  if (world == 1) return CK_OK;
+  // world == 1 still builds a (one-rank) communicator: the step then runs the
+  // real DP path -- per-layer allreduce on the comm stream, event hand-off,
+  // SGD there, loss allreduce -- which is what the one-GPU tests exercise
   ncclUniqueId uid;
   std::memcpy(&uid, id, 128);
   if (ncclCommInitRank(&t->comm, world, uid, rank) != ncclSuccess)
@@ -1012,26 +1103,57 @@ ck_status ck_trainer_init_dp(ck_trainer* t, const char id[128], int rank, int wo
 }
 
 // One training step's device work on stream s: forward, backward with the
-// per-layer gradient allreduce + SGD, objective to loss_dev.
+// per-layer gradient allreduce + SGD, objective to loss_dev, the step's label
+// flag to pinned host memory.
 static void trainer_body(ck_trainer* t, cudaStream_t s) {
   ck_graph* g = t->g;
+  const bool timed = g->profiling;  // profiling steps are always eager
+  if (timed) check_cuda(cudaEventRecord(t->t_begin, s), "event");
   run_forward(g, s);
+  if (timed) check_cuda(cudaEventRecord(t->t_fwd, s), "event");
   run_backward(g, t->objective, s, t);
+  if (timed) check_cuda(cudaEventRecord(t->t_bwd, s), "event");
+  Var& obj = g->vars[t->objective];
   if (t->comm) {
     // Loss: summed over ranks for reporting only.
-    Var& obj = g->vars[t->objective];
     check_cuda(cudaEventRecord(t->ev[0], s), "event");
     check_cuda(cudaStreamWaitEvent(t->comm_stream, t->ev[0], 0), "wait");
     if (ncclAllReduce(obj.value, t->loss_dev, 1, ncclFloat, ncclSum, t->comm, t->comm_stream) !=
         ncclSuccess)
       throw Err(CK_ERR_CUDA, "ncclAllReduce failed");
+    if (timed) check_cuda(cudaEventRecord(t->t_comm, t->comm_stream), "event");
     check_cuda(cudaEventRecord(t->comm_done, t->comm_stream), "event");
     check_cuda(cudaStreamWaitEvent(s, t->comm_done, 0), "wait");
   } else {
-    Var& obj = g->vars[t->objective];
     check_cuda(cudaMemcpyAsync(t->loss_dev, obj.value, sizeof(float), cudaMemcpyDeviceToDevice, s),
                "copy");
     t->join_updates(s);
+    if (timed) check_cuda(cudaEventRecord(t->t_comm, s), "event");
+  }
+  t->timed = timed;
+  if (g->has_loss)
+    check_cuda(cudaMemcpyAsync(t->flag_host, g->h->flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, s),
+               "flag");
+}
+
+// The label flag of the last step, once its copy is known complete (or
+// after a synchronize): CK_ERR_DATA with the reference's message.
+static void check_step_flag(ck_trainer* t, bool synced) {
+  if (!t->flag_pending) return;
+  if (!synced) {
+    const cudaError_t q = cudaEventQuery(t->flag_ev);
+    if (q == cudaErrorNotReady) return;
+    check_cuda(q, "event query");
+  }
+  t->flag_pending = false;
+  const int f = t->flag_host[0], lab = t->flag_host[1];
+  if (f) {
+    t->flag_host[0] = t->flag_host[1] = 0;
+    try {
+      throw_label_flag(f, lab, t->g->h->last_classes);
+    } catch (const Err& e) {
+      throw Err(e.code, std::string("loss layer: ") + e.what());
+    }
   }
 }
 
@@ -1044,24 +1166,42 @@ ck_status ck_trainer_set_graph(ck_trainer* t, int on) {
   CKG_END(g)
 }
 
+ck_status ck_trainer_set_update_stream(ck_trainer* t, int on) {
+  if (!t) return CK_ERR_ARG;
+  ck_graph* g = t->g;
+  CKG_BEGIN(g)
+  t->update_stream = on != 0;
+  t->drop_graph();
+  CKG_END(g)
+}
+
 ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
   if (!t) return CK_ERR_ARG;
   ck_graph* g = t->g;
   CKG_BEGIN(g)
   cudaStream_t s = (cudaStream_t)stream;
+  check_step_flag(t, false);  // a previous step's label error surfaces here at the latest
   int64_t before = g->h->counter.n;
-  // (the legacy default stream cannot be captured: such steps stay eager)
-  if (t->use_graph && s != nullptr && !g->profiling && !g->h->prof.on && t->eager_steps > 0) {
-    // Replay: the step's ~100 launches become one graph launch.  Captured on
-    // the first graph step (after an eager step sized every workspace); the
-    // captured kernel count keeps ck_launch_count honest.
+  // Replay is valid only while every workspace the captured kernels point
+  // into is where it was at capture time (Workspace::get/release bump the
+  // generation): otherwise drop the graphs and run eagerly, which re-sizes
+  // the workspaces; the next step captures again.
+  const uint64_t gen = workspace_generation();
+  bool replay = t->use_graph && s != nullptr && !g->profiling && !g->h->prof.on &&
+                t->eager_steps > 0 && t->eager_gen == gen;
+  ck_trainer::Captured* cap = nullptr;
+  if (replay) {
     std::vector<float*> inputs;
     for (auto& v : g->vars)
       if (v.role == 0) inputs.push_back(v.value);
-    ck_trainer::Captured* cap = nullptr;
     for (auto& c : t->graphs)
       if (c.stream == s && c.inputs == inputs) cap = &c;
+    if (cap && cap->gen != gen) {
+      t->drop_graph();
+      cap = nullptr;
+    }
     if (!cap) {
+      // (the legacy default stream cannot be captured: such steps stay eager)
       if (t->graphs.size() >= 4) t->drop_graph();
       cudaGraph_t graph;
       check_cuda(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
@@ -1069,6 +1209,7 @@ ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
         trainer_body(t, s);
       } catch (...) {
         cudaStreamEndCapture(s, &graph);
+        if (graph) cudaGraphDestroy(graph);
         throw;
       }
       check_cuda(cudaStreamEndCapture(s, &graph), "end capture");
@@ -1076,7 +1217,12 @@ ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
       const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       check_cuda(e, "graph instantiate");
-      t->graphs.push_back({s, inputs, exec, g->h->counter.n - before});
+      if (workspace_generation() != gen) {
+        // something moved during capture: this graph is not replayable
+        cudaGraphExecDestroy(exec);
+        throw Err(CK_ERR_CUDA, "workspace reallocated during step capture");
+      }
+      t->graphs.push_back({s, inputs, exec, g->h->counter.n - before, gen});
       cap = &t->graphs.back();
     } else {
       g->h->counter.n += cap->launches;
@@ -1085,14 +1231,41 @@ ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
   } else {
     trainer_body(t, s);
     ++t->eager_steps;
+    t->eager_gen = workspace_generation();
+  }
+  if (g->has_loss) {
+    check_cuda(cudaEventRecord(t->flag_ev, s), "event");
+    t->flag_pending = true;
   }
   if (loss_host) {
     check_cuda(cudaMemcpyAsync(loss_host, t->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, s),
                "copy");
     check_cuda(cudaStreamSynchronize(s), "synchronize");
+    check_step_flag(t, true);
   }
   g->last_launches = g->h->counter.n - before;
   CKG_END(g)
 }
+
+// Timing of the last profiled (eager) step: forward and backward on the
+// compute stream, and how long after the backward's last kernel the gradient
+// exchange + update finished (the communication NOT hidden behind backward).
+ck_status ck_trainer_last_timing(ck_trainer* t, float* fwd_ms, float* bwd_ms, float* tail_ms) {
+  if (!t) return CK_ERR_ARG;
+  ck_graph* g = t->g;
+  CKG_BEGIN(g)
+  if (!t->timed) throw Err(CK_ERR_ARG, "no profiled step (ck_graph_set_profiling) has run");
+  check_cuda(cudaEventSynchronize(t->t_comm), "synchronize");
+  float a = 0, b = 0, c = 0;
+  check_cuda(cudaEventElapsedTime(&a, t->t_begin, t->t_fwd), "elapsed");
+  check_cuda(cudaEventElapsedTime(&b, t->t_fwd, t->t_bwd), "elapsed");
+  check_cuda(cudaEventElapsedTime(&c, t->t_bwd, t->t_comm), "elapsed");
+  if (fwd_ms) *fwd_ms = a;
+  if (bwd_ms) *bwd_ms = b;
+  if (tail_ms) *tail_ms = c;
+  CKG_END(g)
+}
+
+int64_t ck_trainer_allreduce_count(const ck_trainer* t) { return t ? t->allreduces : 0; }
 
 }  // extern "C"

@@ -1057,6 +1057,7 @@ __device__ __forceinline__ int read_label(const float* labels, int64_t e, int C,
   int c = (int)r;
   if (c != 0 && (c < 1 || c > C)) {
     atomicOr(flag, 2);
+    atomicCAS(flag + 1, 0, c);  // the first offending label, for the message
     return 0;
   }
   return c;
@@ -1120,8 +1121,10 @@ __global__ void sum_sites_k(const float* __restrict__ v, int64_t n, float* out) 
 
 template <bool kAcc>
 __global__ void softmaxlog_bwd_k(const float* __restrict__ x, const float* __restrict__ labels,
-                                 const float* __restrict__ weights, float pscale, float* dx,
-                                 int* flag, int HW, int C, int N) {
+                                 const float* __restrict__ weights, float pscale,
+                                 const float* __restrict__ pdev, float* dx, int* flag, int HW,
+                                 int C, int N) {
+  if (pdev) pscale = *pdev;  // the engine's projection, read on the device (graph.cpp:420-425)
   const int64_t sites = (int64_t)HW * N;
   const int lane = threadIdx.x % 32;
   for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
@@ -1198,8 +1201,10 @@ __global__ void softmaxlog_fwd_reg_k(const float* __restrict__ x, const float* _
 
 template <int R, bool kAcc>
 __global__ void softmaxlog_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ labels,
-                                     const float* __restrict__ weights, float pscale, float* dx,
-                                     int* flag, int HW, int C, int N) {
+                                     const float* __restrict__ weights, float pscale,
+                                     const float* __restrict__ pdev, float* dx, int* flag, int HW,
+                                     int C, int N) {
+  if (pdev) pscale = *pdev;
   const int64_t sites = (int64_t)HW * N;
   const int lane = threadIdx.x % 32;
   for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
@@ -1436,7 +1441,7 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
       const int A = (d.H + d.pt + 1) / 2, B = (d.W + d.pl + 1) / 2;
       const int64_t blocks = (int64_t)A * B * d.C * d.N;
       const FastDiv by_a(A), by_ab(A * B);
-      if (A <= 31 && !getenv("CK_POOL_BWD_FLAT")) {
+      if (A <= 31 && !knob("CK_POOL_BWD_FLAT", 0)) {
         // column strips: one lane segment (SEG >= A + 1 lanes) per plane
         const int planes = d.C * d.N;
         const int seg = A < 8 ? 8 : A < 16 ? 16 : 32;
@@ -1659,24 +1664,25 @@ void softmaxlog_forward(const float* x, const float* labels, const float* weight
 }
 
 void softmaxlog_backward(const float* x, const float* labels, const float* weights, float p,
-                         float* dx, int* flag, int HW, int C, int N, int acc, cudaStream_t s) {
+                         const float* p_dev, float* dx, int* flag, int HW, int C, int N, int acc,
+                         cudaStream_t s) {
   int64_t sites = (int64_t)HW * N;
   count_launch();
   if (C <= 1024) {
     if (acc)
       softmaxlog_bwd_reg_k<32, true><<<blocks_for(sites * 32, 256), 256, 0, s>>>(
-          x, labels, weights, p, dx, flag, HW, C, N);
+          x, labels, weights, p, p_dev, dx, flag, HW, C, N);
     else
       softmaxlog_bwd_reg_k<32, false><<<blocks_for(sites * 32, 256), 256, 0, s>>>(
-          x, labels, weights, p, dx, flag, HW, C, N);
+          x, labels, weights, p, p_dev, dx, flag, HW, C, N);
     return;
   }
   if (acc)
-    softmaxlog_bwd_k<true><<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, p, dx,
-                                                                        flag, HW, C, N);
+    softmaxlog_bwd_k<true><<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, p, p_dev,
+                                                                        dx, flag, HW, C, N);
   else
     softmaxlog_bwd_k<false><<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, p,
-                                                                         dx, flag, HW, C, N);
+                                                                         p_dev, dx, flag, HW, C, N);
 }
 
 void loss_metrics(const float* x, const float* labels, const float* weights, int top_k,

@@ -104,6 +104,10 @@ class Graph:
     def last_launches(self) -> int:
         return lib().ck_graph_last_launches(self.g)
 
+    def set_option(self, name: str, value):
+        """Engine option (ck_graph_set_option), e.g. ``lrn_grid``."""
+        self._check(lib().ck_graph_set_option(self.g, name.encode(), int(value)))
+
     def set_profiling(self, on: bool):
         self._check(lib().ck_graph_set_profiling(self.g, int(on)))
 
@@ -224,6 +228,19 @@ class Trainer:
 
     def init_dp(self, uid: bytes, rank: int, world: int):
         self.graph._check(lib().ck_trainer_init_dp(self.t, uid, rank, world))
+
+    def set_update_stream(self, on: bool):
+        self.graph._check(lib().ck_trainer_set_update_stream(self.t, int(on)))
+
+    def last_timing(self):
+        """(fwd_ms, bwd_ms, exchange_tail_ms) of the last profiled step."""
+        f, b, c = C.c_float(), C.c_float(), C.c_float()
+        self.graph._check(lib().ck_trainer_last_timing(self.t, C.byref(f), C.byref(b), C.byref(c)))
+        return f.value, b.value, c.value
+
+    @property
+    def allreduces(self) -> int:
+        return lib().ck_trainer_allreduce_count(self.t)
 
     def set_graph(self, on: bool):
         """Replay each step as one CUDA graph (ck_trainer_set_graph)."""

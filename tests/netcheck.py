@@ -1,0 +1,128 @@
+"""Layer-by-layer parity of a device DAG evaluation -- TEST INFRASTRUCTURE.
+
+After the device engine (engine.cu) has run forward + backward on a network,
+every layer is re-evaluated on the CPU from the DEVICE's own inputs to that
+layer (its input values and its output derivative), with the reference's
+block functions (oracle/_ref: the convkit sources compiled verbatim,
+OpenBLAS float GEMM), and compared with what the device produced:
+
+  * forward:  layer(device inputs)            vs device output value
+  * backward: layer_backward(device x, dy)     vs device input derivatives
+
+Because each comparison starts from the device's own tensors, errors do not
+compound through the network: every kernel the engine launched for this
+exact configuration -- the batch-dependent tile heights, split-K factors,
+persistent waves, fused epilogues and LRN->grid writers -- is held to the
+block-level tolerance (north star: pooling/ReLU bit-exact, FP32 1e-4
+relative, TF32 1e-2 normwise).  Only chain networks (each variable with one
+consumer) are supported, which is what nets.py builds.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle as O
+
+TOL = {"fp32": 1e-4, "tf32": 1e-2}
+
+
+def rel(a, b):
+    """Per-element relative error, denominator floored at 1% of the tensor's
+    max (test_gpu_blocks.rel), and 10x the normwise error."""
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    floor = 1e-2 * np.max(np.abs(b)) + 1e-30
+    elem = float(np.max(np.abs(a - b) / np.maximum(np.abs(a) + np.abs(b), floor)))
+    norm = float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30))
+    return max(elem, 10 * norm)
+
+
+def normwise(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return max(float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-30)),
+               float(np.max(np.abs(a - b)) / (np.max(np.abs(b)) + 1e-30)))
+
+
+def conv_err(a, b, math):
+    return rel(a, b) if math == "fp32" else normwise(a, b)
+
+
+def check_layers(net, g, math, report=None, strict=True):
+    """Compare every layer of `net` evaluated on device graph `g` (forward and
+    backward already run).  Returns {(layer, what): error}; asserts."""
+    report = {} if report is None else report
+    shapes = {}
+    val, der = {}, {}
+
+    def V(n):
+        if n not in val:
+            val[n] = g.get(n)
+            shapes[n] = g.shape(n)
+        return val[n]
+
+    def D(n):
+        if n not in der:
+            der[n] = g.get(n, deriv=True)
+        return der[n]
+
+    def put(key, e, tol):
+        report[key] = e
+        if strict:
+            assert e <= tol, f"{key}: error {e:.3e} > {tol:.1e}"
+
+    def exact(key, a, b):
+        report[key] = 0.0 if np.array_equal(a, b) else float(np.abs(a - b).max())
+        if strict:
+            assert np.array_equal(a, b), f"{key}: not bit-exact"
+
+    for kind, name, ins, outs, p in net.layers:
+        x = V(ins[0])
+        xs = shapes[ins[0]]
+        y = V(outs[0])
+        dy = D(outs[0])
+        if kind == "conv":
+            f, fs = V(ins[1]), shapes[ins[1]]
+            b = V(ins[2]) if len(ins) > 2 else None
+            yr, _ = O.ref_conv_forward(x, xs, f, fs, b, p)
+            put((name, "y"), conv_err(y, yr, math), TOL[math])
+            dxr, dfr, dbr = O.ref_conv_backward(x, xs, f, fs, p, dy)
+            put((name, "dx"), conv_err(D(ins[0]), dxr, math), TOL[math])
+            put((name, "df"), conv_err(D(ins[1]), dfr, math), TOL[math])
+            if b is not None:
+                # db = sum of dy: a plain (fixed-order, double) reduction on both paths
+                put((name, "db"), rel(D(ins[2]), dbr), 1e-4)
+        elif kind == "relu":
+            exact((name, "y"), y, O.ref_relu(x))
+            exact((name, "dx"), D(ins[0]), O.ref_relu(x, dy))
+        elif kind == "pool":
+            yr, _ = O.ref_pool_forward(x, xs, p)
+            exact((name, "y"), y, yr)
+            exact((name, "dx"), D(ins[0]), O.ref_pool_backward(x, xs, p, dy))
+        elif kind == "lrn":
+            n_, k_, a_, b_ = int(p[0]), p[1], p[2], p[3]
+            put((name, "y"), rel(y, O.ref_lrn_forward(x, xs, n_, k_, a_, b_)), 1e-4)
+            put((name, "dx"), rel(D(ins[0]), O.ref_lrn_backward(x, xs, n_, k_, a_, b_, dy)),
+                1e-4)
+        elif kind == "bnorm":
+            w, b = V(ins[1]), V(ins[2])
+            yr, _, _ = O.ref_bnorm_forward(x, xs, w, b, p[0])
+            put((name, "y"), rel(y, yr), 1e-4)
+            dxr, dwr, dbr = O.ref_bnorm_backward(x, xs, w, b, p[0], dy)
+            put((name, "dx"), rel(D(ins[0]), dxr), 1e-4)
+            put((name, "dw"), rel(D(ins[1]), dwr), 1e-4)
+            put((name, "db"), rel(D(ins[2]), dbr), 1e-4)
+        elif kind == "loss":
+            lab, ls = V(ins[1]), shapes[ins[1]]
+            lr = O.ref_loss_forward(x, xs, lab, ls)
+            put((name, "y"), abs(float(y[0]) - lr) / abs(lr), 1e-5)
+            put((name, "dx"), rel(D(ins[0]), O.ref_loss_backward(x, xs, lab, ls, p=float(dy[0]))),
+                1e-4)
+        else:
+            raise ValueError(kind)
+    return report
+
+
+def format_report(report):
+    worst = {}
+    for (layer, what), e in report.items():
+        worst[f"{layer}.{what}"] = e
+    return ", ".join(f"{k}={v:.1e}" for k, v in worst.items())

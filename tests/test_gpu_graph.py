@@ -151,11 +151,8 @@ def test_lrn_writes_conv_dy_grid(net_name, batch, monkeypatch):
     net = nets.alexnet(batch=batch) if net_name == "alexnet" else nets.cifar(batch=batch)
     out = []
     for fuse in (True, False):
-        if fuse:
-            monkeypatch.delenv("CK_NO_LRN_GRID", raising=False)
-        else:
-            monkeypatch.setenv("CK_NO_LRN_GRID", "1")
         g = device_graph(net, "tf32")
+        g.set_option("lrn_grid", fuse)
         for k, v in {**net.init_params(), **net.init_inputs()}.items():
             g.set(k, v)
         g.forward()
@@ -189,11 +186,8 @@ def test_lrn_grid_envelope(cout, groups, size, monkeypatch):
     n.loss(x)
     out = []
     for fuse in (True, False):
-        if fuse:
-            monkeypatch.delenv("CK_NO_LRN_GRID", raising=False)
-        else:
-            monkeypatch.setenv("CK_NO_LRN_GRID", "1")
         g = device_graph(n, "tf32")
+        g.set_option("lrn_grid", fuse)
         for k, v in {**n.init_params(), **n.init_inputs()}.items():
             g.set(k, v)
         g.forward()
