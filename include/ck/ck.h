@@ -184,6 +184,81 @@ ck_status ck_loss_metrics(ck_handle* h, const ck_tensor* x, const ck_tensor* lab
                           float* topk_err, ck_stream stream);
 ck_status ck_check_labels(ck_handle* h, ck_stream stream);
 
+/* ---- the rest of the reference block set -------------------------------- */
+/* activation.cpp:25-38 sigmoid_forward */
+ck_status ck_sigmoid_forward(ck_handle* h, const ck_tensor* x, ck_tensor* y, ck_stream stream);
+/* activation.cpp:41-48 sigmoid_backward: consumes the forward OUTPUT y */
+ck_status ck_sigmoid_backward(ck_handle* h, const ck_tensor* y, const ck_tensor* dy, ck_tensor* dx,
+                              int accumulate, ck_stream stream);
+/* normalize.cpp:309-328 softmax_forward: channel softmax per site */
+ck_status ck_softmax_forward(ck_handle* h, const ck_tensor* x, ck_tensor* y, ck_stream stream);
+/* normalize.cpp:330-347 softmax_backward: consumes the forward OUTPUT y */
+ck_status ck_softmax_backward(ck_handle* h, const ck_tensor* y, const ck_tensor* dy, ck_tensor* dx,
+                              int accumulate, ck_stream stream);
+
+/* convkit::SpnormParams (normalize.hpp:59-64) */
+typedef struct ck_spnorm_params {
+  int64_t window_h, window_w;
+  double alpha, beta;
+} ck_spnorm_params;
+/* normalize.cpp:268-281 spnorm_forward */
+ck_status ck_spnorm_forward(ck_handle* h, const ck_tensor* x, const ck_spnorm_params* p,
+                            ck_tensor* y, ck_stream stream);
+/* normalize.cpp:284-306 spnorm_backward */
+ck_status ck_spnorm_backward(ck_handle* h, const ck_tensor* x, const ck_spnorm_params* p,
+                             const ck_tensor* dy, ck_tensor* dx, int accumulate, ck_stream stream);
+
+/* bilinear.cpp:48-51 bilinear_output_shape (grid is 2 x outH x outW x N) */
+ck_status ck_bilinear_output_shape(ck_handle* h, ck_shape x, ck_shape grid, ck_shape* out);
+/* bilinear.cpp:58-89 bilinear_forward */
+ck_status ck_bilinear_forward(ck_handle* h, const ck_tensor* x, const ck_tensor* grid,
+                              ck_tensor* y, ck_stream stream);
+/* bilinear.cpp:92-132 bilinear_backward (dx or dgrid may be NULL = skip) */
+ck_status ck_bilinear_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* grid,
+                               const ck_tensor* dy, ck_tensor* dx, ck_tensor* dgrid,
+                               int accumulate, ck_stream stream);
+
+/* loss.cpp:346-371 pdist_forward: y is H x W x 1 x N */
+ck_status ck_pdist_forward(ck_handle* h, const ck_tensor* x, const ck_tensor* target, double p,
+                           int no_root, ck_tensor* y, ck_stream stream);
+/* loss.cpp:374-428 pdist_backward (dx or dtarget may be NULL; dtarget = -dx) */
+ck_status ck_pdist_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* target, double p,
+                            int no_root, const ck_tensor* dy, ck_tensor* dx, ck_tensor* dtarget,
+                            int accumulate, ck_stream stream);
+
+/* convkit::LossKind (loss.hpp:13-24), same order */
+typedef enum ck_loss_kind {
+  CK_LOSS_CLASSERROR = 0,
+  CK_LOSS_TOPK = 1,
+  CK_LOSS_LOG = 2,
+  CK_LOSS_SOFTMAXLOG = 3,
+  CK_LOSS_MHINGE = 4,
+  CK_LOSS_MSHINGE = 5,
+  CK_LOSS_BINARYERROR = 6,
+  CK_LOSS_BINARYLOG = 7,
+  CK_LOSS_LOGISTIC = 8,
+  CK_LOSS_HINGE = 9
+} ck_loss_kind;
+/* convkit::LossOptions (loss.hpp:31-36) */
+typedef struct ck_loss_options {
+  int64_t top_k;       /* topk (default 5) */
+  double threshold;    /* binaryerror (default 0) */
+  int64_t random_ties; /* classerror: break argmax ties randomly */
+  uint64_t tie_seed;
+} ck_loss_options;
+/* loss.cpp:86-228 loss_forward, any kind: the weighted SUM of per-sample
+ * penalties into *loss (a DEVICE float).  check_labels != 0 synchronises and
+ * reports DataError conditions (non-integer / out-of-range labels, log loss
+ * on a non-positive score, binarylog input outside [0,1]).  opts may be NULL
+ * (defaults). */
+ck_status ck_loss_forward(ck_handle* h, const ck_tensor* x, const ck_tensor* labels,
+                          const ck_tensor* weights, ck_loss_kind kind, const ck_loss_options* opts,
+                          float* loss, int check_labels, ck_stream stream);
+/* loss.cpp:231-343 loss_backward, any kind (error kinds give exact zeros) */
+ck_status ck_loss_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* labels,
+                           const ck_tensor* weights, ck_loss_kind kind, const ck_loss_options* opts,
+                           float p, ck_tensor* dx, int accumulate, ck_stream stream);
+
 /* ---- cnn_train SGD step: v = m v - lr (g + wd w); w += v -- */
 ck_status ck_sgd_step(ck_handle* h, float* w, float* v, const float* g, int64_t n, float lr,
                       float momentum, float weight_decay, ck_stream stream);
@@ -199,7 +274,11 @@ void ck_graph_destroy(ck_graph* g);
  *   pool  : win_h win_w stride_h stride_w pad_t pad_b pad_l pad_r mode
  *   lrn   : group_size kappa alpha beta
  *   bnorm : epsilon
- *   loss  : (none; softmaxlog)                                            */
+ *   loss  : [kind top_k threshold random_ties tie_seed] (none: softmaxlog)
+ *   spnorm: win_h win_w alpha beta
+ *   pdist : p no_root
+ *   split : (outputs name the copies)
+ *   sigmoid, softmax, relu, sum, bilinear(x, grid): none                 */
 ck_status ck_graph_add_input(ck_graph* g, const char* name, ck_shape shape);
 ck_status ck_graph_add_param(ck_graph* g, const char* name, ck_shape shape);
 ck_status ck_graph_add_layer(ck_graph* g, const char* kind, const char* name,

@@ -101,7 +101,7 @@ def ref():
         _ref.ref_graph_add_input.argtypes = [C.c_void_p, C.c_char_p]
         _ref.ref_graph_add_param.argtypes = [C.c_void_p, C.c_char_p]
         _ref.ref_graph_add_layer.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_char_p,
-                                             C.c_char_p, D]
+                                             C.c_char_p, D, C.c_int]
         _ref.ref_graph_finalize.argtypes = [C.c_void_p]
         _ref.ref_graph_bind.argtypes = [C.c_void_p, C.c_char_p, F, I64]
         _ref.ref_graph_forward_backward.argtypes = [C.c_void_p, C.c_char_p, C.c_int]
@@ -113,6 +113,17 @@ def ref():
         _ref.ref_bnorm_backward.argtypes = [F, I64, F, F, C.c_double, F, F, F, F]
         _ref.ref_loss_forward.argtypes = [F, I64, F, I64, F, C.c_char_p, C.c_int64, F]
         _ref.ref_loss_backward.argtypes = [F, I64, F, I64, F, C.c_char_p, C.c_float, F]
+        _ref.ref_loss_forward2.argtypes = [F, I64, F, I64, F, C.c_int, C.c_int64, C.c_double,
+                                           C.c_int, C.c_uint64, F]
+        _ref.ref_loss_backward2.argtypes = [F, I64, F, I64, F, C.c_int, C.c_float, F]
+        _ref.ref_spnorm_forward.argtypes = [F, I64, C.c_int64, C.c_int64, C.c_double, C.c_double, F]
+        _ref.ref_spnorm_backward.argtypes = [F, I64, C.c_int64, C.c_int64, C.c_double, C.c_double,
+                                             F, F]
+        _ref.ref_pdist_forward.argtypes = [F, F, I64, C.c_double, C.c_int, F]
+        _ref.ref_pdist_backward.argtypes = [F, F, I64, C.c_double, C.c_int, F, I64, F, F]
+        _ref.ref_write_blob.argtypes = [C.c_char_p, F, I64]
+        _ref.ref_read_blob.argtypes = [C.c_char_p, F, I64]
+        _ref.ref_rng_permutation.argtypes = [C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p]
     return _ref
 
 
@@ -483,6 +494,112 @@ def ref_loss_backward(x, xs, labels, cs, weights=None, kind="softmaxlog", p=1.0)
     return dx
 
 
+def ref_loss(x, xs, labels, cs, weights=None, kind=3, top_k=5, threshold=0.0, random_ties=0,
+             tie_seed=0):
+    """loss.cpp:86 with the full LossOptions (kind: LossKind index)."""
+    x, labels, weights = _f(x), _f(labels), _f(weights)
+    out = C.c_float()
+    _check_ref(ref().ref_loss_forward2(_pf(x), _s(xs), _pf(labels), _s(cs), _pf(weights), kind,
+                                       top_k, threshold, random_ties, tie_seed, C.byref(out)))
+    return out.value
+
+
+def ref_loss_grad(x, xs, labels, cs, weights=None, kind=3, p=1.0):
+    x, labels, weights = _f(x), _f(labels), _f(weights)
+    dx = np.zeros(size(xs), np.float32)
+    _check_ref(ref().ref_loss_backward2(_pf(x), _s(xs), _pf(labels), _s(cs), _pf(weights), kind,
+                                        p, _pf(dx)))
+    return dx
+
+
+def ref_sigmoid(x, dy=None, y=None):
+    """activation.cpp:25 forward (dy None) or :41 backward from the OUTPUT y."""
+    if dy is None:
+        x = _f(x)
+        out = np.zeros_like(x)
+        _check_ref(ref().ref_sigmoid_forward(_pf(x), _s((x.size, 1, 1, 1)), _pf(out)))
+        return out
+    y, dy = _f(y), _f(dy)
+    out = np.zeros_like(y)
+    _check_ref(ref().ref_sigmoid_backward(_pf(y), _s((y.size, 1, 1, 1)), _pf(dy), _pf(out)))
+    return out
+
+
+def ref_softmax(x, xs, dy=None, y=None):
+    """normalize.cpp:309 forward or :330 backward from the OUTPUT y."""
+    if dy is None:
+        x = _f(x)
+        out = np.zeros_like(x)
+        _check_ref(ref().ref_softmax_forward(_pf(x), _s(xs), _pf(out)))
+        return out
+    y, dy = _f(y), _f(dy)
+    out = np.zeros_like(y)
+    _check_ref(ref().ref_softmax_backward(_pf(y), _s(xs), _pf(dy), _pf(out)))
+    return out
+
+
+def ref_spnorm(x, xs, wh, ww, alpha, beta, dy=None):
+    x = _f(x)
+    out = np.zeros_like(x)
+    if dy is None:
+        _check_ref(ref().ref_spnorm_forward(_pf(x), _s(xs), wh, ww, alpha, beta, _pf(out)))
+    else:
+        dy = _f(dy)
+        _check_ref(ref().ref_spnorm_backward(_pf(x), _s(xs), wh, ww, alpha, beta, _pf(dy),
+                                             _pf(out)))
+    return out
+
+
+def ref_bilinear(x, xs, g, gs, dy=None):
+    ys = (gs[1], gs[2], xs[2], xs[3])
+    x, g = _f(x), _f(g)
+    if dy is None:
+        y = np.zeros(size(ys), np.float32)
+        _check_ref(ref().ref_bilinear_forward(_pf(x), _s(xs), _pf(g), _s(gs), _pf(y)))
+        return y
+    dy = _f(dy)
+    dx = np.zeros(size(xs), np.float32)
+    dg = np.zeros(size(gs), np.float32)
+    _check_ref(ref().ref_bilinear_backward(_pf(x), _s(xs), _pf(g), _s(gs), _pf(dy), _s(ys),
+                                           _pf(dx), _pf(dg)))
+    return dx, dg
+
+
+def ref_pdist(x, t, xs, p, no_root, dy=None):
+    ys = (xs[0], xs[1], 1, xs[3])
+    x, t = _f(x), _f(t)
+    if dy is None:
+        y = np.zeros(size(ys), np.float32)
+        _check_ref(ref().ref_pdist_forward(_pf(x), _pf(t), _s(xs), p, int(no_root), _pf(y)))
+        return y
+    dy = _f(dy)
+    dx = np.zeros(size(xs), np.float32)
+    dt = np.zeros(size(xs), np.float32)
+    _check_ref(ref().ref_pdist_backward(_pf(x), _pf(t), _s(xs), p, int(no_root), _pf(dy), _s(ys),
+                                        _pf(dx), _pf(dt)))
+    return dx, dt
+
+
+def ref_write_blob(path, data, shape):
+    _check_ref(ref().ref_write_blob(str(path).encode(), _pf(_f(data)), _s(shape)))
+
+
+def ref_read_blob(path):
+    s = (C.c_int64 * 4)()
+    _check_ref(ref().ref_read_blob(str(path).encode(), None, s))
+    out = np.zeros(size(tuple(s)), np.float32)
+    _check_ref(ref().ref_read_blob(str(path).encode(), _pf(out), s))
+    return out, tuple(s)
+
+
+def ref_permutation(seed, n):
+    """rng.cpp:51-59 Xoshiro256(seed).permutation(n) and the generator state after it."""
+    out = np.zeros(n, np.int64)
+    st = np.zeros(4, np.uint64)
+    _check_ref(ref().ref_rng_permutation(seed, n, out.ctypes.data, st.ctypes.data))
+    return out, st
+
+
 class RefGraph:
     """The reference DAG engine (graph.hpp) driven through oracle/_ref."""
 
@@ -504,7 +621,7 @@ class RefGraph:
         p = (C.c_double * max(1, len(params)))(*[float(v) for v in params])
         _check_ref(ref().ref_graph_add_layer(self.h, kind.encode(), name.encode(),
                                              ",".join(inputs).encode(), ",".join(outputs).encode(),
-                                             p))
+                                             p, len(params)))
 
     def finalize(self):
         _check_ref(ref().ref_graph_finalize(self.h))

@@ -15,6 +15,8 @@
 #include <vector>
 
 #include "convkit/activation.hpp"
+#include "convkit/bilinear.hpp"
+#include "convkit/blob.hpp"
 #include "convkit/conv.hpp"
 #include "convkit/graph.hpp"
 #include "convkit/loss.hpp"
@@ -214,6 +216,117 @@ int ref_loss_backward(const float* x, const int64_t* xs, const float* c, const i
   });
 }
 
+// loss.cpp:86 / :231 with the full LossOptions; kind as LossKind index.
+int ref_loss_forward2(const float* x, const int64_t* xs, const float* c, const int64_t* cs,
+                      const float* w, int kind, int64_t top_k, double threshold, int random_ties,
+                      uint64_t tie_seed, float* out) {
+  return guard([&] {
+    LossOptions o;
+    o.top_k = top_k;
+    o.threshold = threshold;
+    o.random_ties = random_ties != 0;
+    o.tie_seed = tie_seed;
+    TensorF W;
+    if (w) W = tin(w, cs);
+    *out = loss_forward(tin(x, xs), tin(c, cs), static_cast<LossKind>(kind), w ? &W : nullptr, o);
+  });
+}
+int ref_loss_backward2(const float* x, const int64_t* xs, const float* c, const int64_t* cs,
+                       const float* w, int kind, float p, float* dx) {
+  return guard([&] {
+    TensorF W;
+    if (w) W = tin(w, cs);
+    tout(loss_backward(tin(x, xs), tin(c, cs), static_cast<LossKind>(kind), w ? &W : nullptr, p),
+         dx);
+  });
+}
+
+// activation.cpp:25 / :41
+int ref_sigmoid_forward(const float* x, const int64_t* xs, float* y) {
+  return guard([&] { tout(sigmoid_forward(tin(x, xs)), y); });
+}
+int ref_sigmoid_backward(const float* y, const int64_t* ys, const float* dy, float* dx) {
+  return guard([&] { tout(sigmoid_backward(tin(y, ys), tin(dy, ys)), dx); });
+}
+
+// normalize.cpp:309 / :330
+int ref_softmax_forward(const float* x, const int64_t* xs, float* y) {
+  return guard([&] { tout(softmax_forward(tin(x, xs)), y); });
+}
+int ref_softmax_backward(const float* y, const int64_t* ys, const float* dy, float* dx) {
+  return guard([&] { tout(softmax_backward(tin(y, ys), tin(dy, ys)), dx); });
+}
+
+// normalize.cpp:268 / :284
+int ref_spnorm_forward(const float* x, const int64_t* xs, int64_t wh, int64_t ww, double alpha,
+                       double beta, float* y) {
+  return guard([&] {
+    SpnormParams p{wh, ww, alpha, beta};
+    tout(spnorm_forward(tin(x, xs), p), y);
+  });
+}
+int ref_spnorm_backward(const float* x, const int64_t* xs, int64_t wh, int64_t ww, double alpha,
+                        double beta, const float* dy, float* dx) {
+  return guard([&] {
+    SpnormParams p{wh, ww, alpha, beta};
+    tout(spnorm_backward(tin(x, xs), p, tin(dy, xs)), dx);
+  });
+}
+
+// bilinear.cpp:58 / :92
+int ref_bilinear_forward(const float* x, const int64_t* xs, const float* g, const int64_t* gs,
+                         float* y) {
+  return guard([&] { tout(bilinear_forward(tin(x, xs), tin(g, gs)), y); });
+}
+int ref_bilinear_backward(const float* x, const int64_t* xs, const float* g, const int64_t* gs,
+                          const float* dy, const int64_t* ys, float* dx, float* dg) {
+  return guard([&] {
+    TensorF DX, DG;
+    bilinear_backward(tin(x, xs), tin(g, gs), tin(dy, ys), dx ? &DX : nullptr, dg ? &DG : nullptr);
+    if (dx) tout(DX, dx);
+    if (dg) tout(DG, dg);
+  });
+}
+
+// loss.cpp:346 / :374
+int ref_pdist_forward(const float* x, const float* t, const int64_t* xs, double p, int no_root,
+                      float* y) {
+  return guard([&] { tout(pdist_forward(tin(x, xs), tin(t, xs), p, no_root != 0), y); });
+}
+int ref_pdist_backward(const float* x, const float* t, const int64_t* xs, double p, int no_root,
+                       const float* dy, const int64_t* ys, float* dx, float* dt) {
+  return guard([&] {
+    TensorF DX, DT;
+    pdist_backward(tin(x, xs), tin(t, xs), p, no_root != 0, tin(dy, ys), dx ? &DX : nullptr,
+                   dt ? &DT : nullptr);
+    if (dx) tout(DX, dx);
+    if (dt) tout(DT, dt);
+  });
+}
+
+// blob.cpp:29-79 write_blob / read_blob (read: out NULL -> shape only)
+int ref_write_blob(const char* path, const float* data, const int64_t* s) {
+  return guard([&] { write_blob(tin(data, s), std::string(path)); });
+}
+int ref_read_blob(const char* path, float* out, int64_t* s) {
+  return guard([&] {
+    TensorF t = read_blob(std::string(path));
+    s[0] = t.shape().h; s[1] = t.shape().w; s[2] = t.shape().c; s[3] = t.shape().n;
+    if (out) tout(t, out);
+  });
+}
+
+// rng.cpp:51-59 Xoshiro256::permutation, and the state after it (rng.hpp:31-32)
+int ref_rng_permutation(uint64_t seed, int64_t n, int64_t* out, uint64_t* state) {
+  return guard([&] {
+    Xoshiro256 r(seed);
+    std::vector<int64_t> p = r.permutation(n);
+    std::memcpy(out, p.data(), sizeof(int64_t) * (size_t)n);
+    auto st = r.state();
+    for (int k = 0; k < 4; ++k) state[k] = st[k];
+  });
+}
+
 // ---- the reference DAG engine (graph.hpp) ---------------------------------
 
 struct RefNet {
@@ -235,7 +348,7 @@ int ref_graph_add_param(void* h, const char* name) {
 // kind: layer_kind_name (graph.cpp:13-31); p: kind-specific parameters.
 //   conv: geom[7]; pool: pg[9]; lrn: n,kappa,alpha,beta; bnorm: eps; loss: (softmaxlog)
 int ref_graph_add_layer(void* h, const char* kind, const char* name, const char* inputs,
-                        const char* outputs, const double* p) {
+                        const char* outputs, const double* p, int np) {
   return guard([&] {
     LayerDef d;
     d.name = name;
@@ -261,8 +374,31 @@ int ref_graph_add_layer(void* h, const char* kind, const char* name, const char*
       case LayerKind::bnorm:
         d.hyper = BnormHyper{p[0]};
         break;
-      case LayerKind::loss:
-        d.hyper = LossHyper{};
+      case LayerKind::loss: {
+        // p: [kind top_k threshold random_ties tie_seed] or NaN-terminated empty
+        LossHyper lh;
+        if (np > 0) {
+          lh.kind = static_cast<LossKind>(static_cast<int>(p[0]));
+          if (np > 1) lh.opts.top_k = static_cast<int64_t>(p[1]);
+          if (np > 2) lh.opts.threshold = p[2];
+          if (np > 3) lh.opts.random_ties = p[3] != 0;
+          if (np > 4) lh.opts.tie_seed = static_cast<uint64_t>(p[4]);
+        }
+        d.hyper = lh;
+        break;
+      }
+      case LayerKind::spnorm:
+        d.hyper = SpnormParams{static_cast<int64_t>(p[0]), static_cast<int64_t>(p[1]), p[2], p[3]};
+        break;
+      case LayerKind::pdist: {
+        PdistHyper ph;
+        if (np > 0) ph.p = p[0];
+        if (np > 1) ph.no_root = p[1] != 0;
+        d.hyper = ph;
+        break;
+      }
+      case LayerKind::split:
+        d.hyper = SplitHyper{static_cast<int64_t>(d.outputs.size())};
         break;
       default:
         break;

@@ -40,6 +40,16 @@ class ck_pool_geom(C.Structure):
                  "pad_left", "pad_right", "mode")]
 
 
+class ck_spnorm_params(C.Structure):
+    _fields_ = [("window_h", C.c_int64), ("window_w", C.c_int64), ("alpha", C.c_double),
+                ("beta", C.c_double)]
+
+
+class ck_loss_options(C.Structure):
+    _fields_ = [("top_k", C.c_int64), ("threshold", C.c_double), ("random_ties", C.c_int64),
+                ("tie_seed", C.c_uint64)]
+
+
 class ck_lrn_params(C.Structure):
     _fields_ = [("group_size", C.c_int64), ("kappa", C.c_double), ("alpha", C.c_double),
                 ("beta", C.c_double)]
@@ -85,6 +95,20 @@ SIGNATURES = {
     "ck_loss_metrics": (S, [P, T, T, T, C.c_int64, P, P, P]),
     "ck_check_labels": (S, [P, P]),
     "ck_sgd_step": (S, [P, P, P, P, C.c_int64, C.c_float, C.c_float, C.c_float, P]),
+    "ck_sigmoid_forward": (S, [P, T, T, P]),
+    "ck_sigmoid_backward": (S, [P, T, T, T, C.c_int, P]),
+    "ck_softmax_forward": (S, [P, T, T, P]),
+    "ck_softmax_backward": (S, [P, T, T, T, C.c_int, P]),
+    "ck_spnorm_forward": (S, [P, T, C.POINTER(ck_spnorm_params), T, P]),
+    "ck_spnorm_backward": (S, [P, T, C.POINTER(ck_spnorm_params), T, T, C.c_int, P]),
+    "ck_bilinear_output_shape": (S, [P, ck_shape, ck_shape, C.POINTER(ck_shape)]),
+    "ck_bilinear_forward": (S, [P, T, T, T, P]),
+    "ck_bilinear_backward": (S, [P, T, T, T, T, T, C.c_int, P]),
+    "ck_pdist_forward": (S, [P, T, T, C.c_double, C.c_int, T, P]),
+    "ck_pdist_backward": (S, [P, T, T, C.c_double, C.c_int, T, T, T, C.c_int, P]),
+    "ck_loss_forward": (S, [P, T, T, T, C.c_int, C.POINTER(ck_loss_options), P, C.c_int, P]),
+    "ck_loss_backward": (S, [P, T, T, T, C.c_int, C.POINTER(ck_loss_options), C.c_float, T,
+                             C.c_int, P]),
     "ck_graph_create": (S, [P, C.POINTER(P)]),
     "ck_graph_destroy": (None, [P]),
     "ck_graph_add_input": (S, [P, C.c_char_p, ck_shape]),

@@ -19,8 +19,8 @@ import torch
 
 from . import _lib
 from ._lib import (CK_MATH_FP32, CK_MATH_TF32, CkError, DataError, ShapeError,  # noqa: F401
-                   ck_conv_geom, ck_convt_geom, ck_lrn_params, ck_pool_geom, ck_shape,
-                   ck_tensor, lib, raise_for)
+                   ck_conv_geom, ck_convt_geom, ck_loss_options, ck_lrn_params, ck_pool_geom,
+                   ck_shape, ck_spnorm_params, ck_tensor, lib, raise_for)
 
 
 # ---- hyper-parameters (field names as in the reference headers) -------------
@@ -370,3 +370,135 @@ def sgd_step(w, v, g, lr, momentum, weight_decay):
     hd = handle()
     hd.check(lib().ck_sgd_step(hd.h, w.data_ptr(), v.data_ptr(), g.data_ptr(), w.numel(), lr,
                                momentum, weight_decay, _stream()))
+
+
+# ---- the rest of the reference block set (blocks_ext.cu) ---------------------------
+
+LOSS_KINDS = ["classerror", "topk", "log", "softmaxlog", "mhinge", "mshinge", "binaryerror",
+              "binarylog", "logistic", "hinge"]  # loss.hpp:13-24
+
+
+def sigmoid_forward(x):
+    """activation.cpp:25-38."""
+    y = torch.empty_like(x)
+    hd = handle()
+    hd.check(lib().ck_sigmoid_forward(hd.h, _t(x), _t(y), _stream()))
+    return y
+
+
+def sigmoid_backward(y, dy):
+    """activation.cpp:41-48 (from the forward OUTPUT y)."""
+    dx = torch.empty_like(y)
+    hd = handle()
+    hd.check(lib().ck_sigmoid_backward(hd.h, _t(y), _t(dy), _t(dx), 0, _stream()))
+    return dx
+
+
+def softmax_forward(x):
+    """normalize.cpp:309-328 (channel softmax per site)."""
+    y = torch.empty_like(x)
+    hd = handle()
+    hd.check(lib().ck_softmax_forward(hd.h, _t(x), _t(y), _stream()))
+    return y
+
+
+def softmax_backward(y, dy):
+    dx = torch.empty_like(y)
+    hd = handle()
+    hd.check(lib().ck_softmax_backward(hd.h, _t(y), _t(dy), _t(dx), 0, _stream()))
+    return dx
+
+
+@dataclass
+class SpnormParams:
+    """convkit::SpnormParams (normalize.hpp:59-64)."""
+    window_h: int = 1
+    window_w: int = 1
+    alpha: float = 1.0
+    beta: float = 0.5
+
+    def c(self):
+        return ck_spnorm_params(self.window_h, self.window_w, self.alpha, self.beta)
+
+
+def spnorm_forward(x, p: SpnormParams):
+    y = torch.empty_like(x)
+    hd = handle()
+    hd.check(lib().ck_spnorm_forward(hd.h, _t(x), C.byref(p.c()), _t(y), _stream()))
+    return y
+
+
+def spnorm_backward(x, p: SpnormParams, dy):
+    dx = torch.empty_like(x)
+    hd = handle()
+    hd.check(lib().ck_spnorm_backward(hd.h, _t(x), C.byref(p.c()), _t(dy), _t(dx), 0, _stream()))
+    return dx
+
+
+def bilinear_output_shape(xs, gs):
+    out = ck_shape()
+    hd = handle()
+    hd.check(lib().ck_bilinear_output_shape(hd.h, ck_shape(*xs), ck_shape(*gs), C.byref(out)))
+    return (out.h, out.w, out.c, out.n)
+
+
+def bilinear_forward(x, grid):
+    """bilinear.cpp:58-89: grid is 2 x outH x outW x N."""
+    y = from_hwcn(bilinear_output_shape(hwcn_shape(x), hwcn_shape(grid)), x.device)
+    hd = handle()
+    hd.check(lib().ck_bilinear_forward(hd.h, _t(x), _t(grid), _t(y), _stream()))
+    return y
+
+
+def bilinear_backward(x, grid, dy):
+    dx, dg = torch.empty_like(x), torch.empty_like(grid)
+    hd = handle()
+    hd.check(lib().ck_bilinear_backward(hd.h, _t(x), _t(grid), _t(dy), _t(dx), _t(dg), 0,
+                                        _stream()))
+    return dx, dg
+
+
+def pdist_forward(x, target, p=2.0, no_root=False):
+    """loss.cpp:346-371: H x W x 1 x N distances."""
+    h, w, c, n = hwcn_shape(x)
+    y = from_hwcn((h, w, 1, n), x.device)
+    hd = handle()
+    hd.check(lib().ck_pdist_forward(hd.h, _t(x), _t(target), float(p), int(no_root), _t(y),
+                                    _stream()))
+    return y
+
+
+def pdist_backward(x, target, dy, p=2.0, no_root=False):
+    dx, dt = torch.empty_like(x), torch.empty_like(x)
+    hd = handle()
+    hd.check(lib().ck_pdist_backward(hd.h, _t(x), _t(target), float(p), int(no_root), _t(dy),
+                                     _t(dx), _t(dt), 0, _stream()))
+    return dx, dt
+
+
+def _kind(kind):
+    return LOSS_KINDS.index(kind) if isinstance(kind, str) else int(kind)
+
+
+def _opts(top_k=5, threshold=0.0, random_ties=False, tie_seed=0):
+    return ck_loss_options(int(top_k), float(threshold), int(random_ties), int(tie_seed))
+
+
+def loss_kind_forward(x, labels, kind="softmaxlog", weights=None, check_labels=True, **opts):
+    """loss.cpp:86-228, any LossKind: the weighted SUM of per-sample penalties."""
+    out = torch.empty(1, device=x.device)
+    hd = handle()
+    hd.check(lib().ck_loss_forward(hd.h, _t(x), _t(labels), _t(weights), _kind(kind),
+                                   C.byref(_opts(**opts)), out.data_ptr(), int(check_labels),
+                                   _stream()))
+    return out
+
+
+def loss_kind_backward(x, labels, kind="softmaxlog", weights=None, p=1.0):
+    """loss.cpp:231-343, any LossKind (error kinds: exact zeros)."""
+    dx = torch.empty_like(x)
+    hd = handle()
+    hd.check(lib().ck_loss_backward(hd.h, _t(x), _t(labels), _t(weights), _kind(kind), None,
+                                    float(p), _t(dx), 0, _stream()))
+    return dx
+

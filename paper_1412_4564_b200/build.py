@@ -16,7 +16,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libck.so")
-SOURCES = ["kernels.cu", "conv_simt.cu", "conv_tc.cu", "capi.cu", "engine.cu", "host_rng.cu"]
+SOURCES = ["kernels.cu", "conv_simt.cu", "conv_tc.cu", "capi.cu", "engine.cu", "host_rng.cu",
+           "blocks_ext.cu", "capi_ext.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

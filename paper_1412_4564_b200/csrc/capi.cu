@@ -264,22 +264,6 @@ void conv_wgrad_dispatch(ck_handle* h, const float* x, const float* dy, float* d
 
 using namespace ck;
 
-#define CK_API_BEGIN(h)                      \
-  if (!(h)) return CK_ERR_ARG;               \
-  ck::HandleScope _scope(h);                 \
-  try {
-#define CK_API_END(h)                        \
-  return CK_OK;                              \
-  }                                          \
-  catch (const ck::Err& e) {                 \
-    (h)->err = e.what();                     \
-    return e.code;                           \
-  }                                          \
-  catch (const std::exception& e) {          \
-    (h)->err = e.what();                     \
-    return CK_ERR_ARG;                       \
-  }
-
 extern "C" {
 
 const char* ck_version(void) {

@@ -93,6 +93,19 @@ void after_launch();
 void reset_label_flag(ck_handle* h, cudaStream_t s);
 void read_label_flag(ck_handle* h, cudaStream_t s);
 void throw_label_flag(int flag, int label, int64_t classes);
+// capi_ext.cu: shape laws / validation / launch of the extended block set
+ck_shape bilinear_output_shape(const ck_shape& x, const ck_shape& grid);
+ck_shape pdist_output_shape(const ck_shape& x, const ck_shape& target, double p);
+bool loss_is_attribute(int kind);
+void check_loss_kind(const ck_tensor* x, const ck_tensor* labels, const ck_tensor* weights,
+                     int kind);
+ck_loss_options default_loss_options();
+void loss_forward_any(ck_handle* h, const ck_tensor* x, const ck_tensor* labels,
+                      const ck_tensor* weights, int kind, const ck_loss_options& o, float* loss,
+                      cudaStream_t st);
+void loss_backward_any(ck_handle* h, const ck_tensor* x, const ck_tensor* labels,
+                       const ck_tensor* weights, int kind, float p, const float* p_dev,
+                       float* dx, int acc, cudaStream_t st);
 
 void conv_forward_dispatch(ck_handle* h, const float* x, const float* f, const float* bias,
                            float* y, const ConvDims& d, int relu, ck_math math, cudaStream_t s);
@@ -127,3 +140,21 @@ void materialize_pending_dy(ck_handle* h, const float* dy, cudaStream_t s);
 void conv_tc_release(ck_handle* h);
 
 }  // namespace ck
+
+// Entry-point wrapper of every extern "C" function: binds the handle,
+// maps reference exceptions to status codes and keeps the message.
+#define CK_API_BEGIN(h)                      \
+  if (!(h)) return CK_ERR_ARG;               \
+  ck::HandleScope _scope(h);                 \
+  try {
+#define CK_API_END(h)                        \
+  return CK_OK;                              \
+  }                                          \
+  catch (const ck::Err& e) {                 \
+    (h)->err = e.what();                     \
+    return e.code;                           \
+  }                                          \
+  catch (const std::exception& e) {          \
+    (h)->err = e.what();                     \
+    return CK_ERR_ARG;                       \
+  }

@@ -157,6 +157,39 @@ void loss_metrics(const float* x, const float* labels, const float* weights, int
                   float* site_buf, float* top1, float* topk, int* flag, int HW, int C, int N,
                   cudaStream_t s);
 
+// ---- the rest of the block set (blocks_ext.cu) -----------------------------
+void sigmoid_forward(const float* x, float* y, int64_t n, cudaStream_t s);
+void sigmoid_backward(const float* y, const float* dy, float* dx, int64_t n, int acc,
+                      cudaStream_t s);
+void softmax_forward(const float* x, float* y, int HW, int C, int N, cudaStream_t s);
+void softmax_backward(const float* y, const float* dy, float* dx, int HW, int C, int N, int acc,
+                      cudaStream_t s);
+void spnorm_forward(const float* x, float* y, int H, int W, int64_t planes, int wh, int ww,
+                    float alpha, float beta, cudaStream_t s);
+// ws: 2 * H*W*planes floats
+void spnorm_backward(const float* x, const float* dy, float* dx, float* ws, int H, int W,
+                     int64_t planes, int wh, int ww, float alpha, float beta, float c2ab, int acc,
+                     cudaStream_t s);
+void bilinear_forward(const float* x, const float* grid, float* y, int H, int W, int C, int N,
+                      int OH, int OW, cudaStream_t s);
+void bilinear_backward(const float* x, const float* grid, const float* dy, float* dx, float* dgrid,
+                       int H, int W, int C, int N, int OH, int OW, int acc, cudaStream_t s);
+void pdist_forward(const float* x, const float* t, float* y, int HW, int C, int N, double p,
+                   int no_root, cudaStream_t s);
+void pdist_backward(const float* x, const float* t, const float* dy, float* dx, float* dt, int HW,
+                    int C, int N, double p, int no_root, int acc, cudaStream_t s);
+// every loss kind but softmaxlog (ck_loss_kind numbering); site: per-site
+// (classification) or per-element (attribute) scratch
+void loss_forward_kind(const float* x, const float* labels, const float* weights, int kind,
+                       int64_t top_k, double threshold, int random_ties, uint64_t tie_seed,
+                       float* site, float* loss, int* flag, int H, int W, int C, int N,
+                       cudaStream_t s);
+void loss_backward_kind(const float* x, const float* labels, const float* weights, int kind,
+                        float p, const float* p_dev, float* dx, int* flag, int H, int W, int C,
+                        int N, int acc, cudaStream_t s);
+// dx (+)= sum_k srcs[k] (k < m <= 8), in order
+void sum_into(float* dx, const float* const* srcs, int m, int64_t n, int acc, cudaStream_t s);
+
 // ---- convolution -----------------------------------------------------------
 // All conv launchers compute the reference semantics of conv.cpp:193-280 on
 // HWCN tensors; bias may be null; acc != 0 adds into the destination.

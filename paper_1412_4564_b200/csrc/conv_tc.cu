@@ -1483,7 +1483,8 @@ __global__ void s2d_pm_strip_k(const float* __restrict__ x, float* __restrict__ 
 
 // fprop filters of the s2d conv: fT[k][tap = t + Th*t2][c'p]
 __global__ void s2d_repack_fprop_k(const float* __restrict__ f, float* __restrict__ ft, int fh,
-                                   int fw, int Cg, int K, int s, int Th, int Tw, int Csp) {
+                                   int fw, int Cg, int K, int s, int Th, int Tw, int Csp,
+                                   int64_t fsc, int64_t fsk) {
   const int64_t total = (int64_t)K * Th * Tw * Csp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -1495,7 +1496,7 @@ __global__ void s2d_repack_fprop_k(const float* __restrict__ f, float* __restric
     if (cp < s * s * Cg) {
       const int c = cp % Cg, ab = cp / Cg, a = ab % s, b = ab / s;
       const int fi = a + s * (tap % Th), fj = b + s * (tap / Th);
-      if (fi < fh && fj < fw) v = f[fi + (int64_t)fh * (fj + (int64_t)fw * (c + (int64_t)Cg * k))];
+      if (fi < fh && fj < fw) v = f[fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + k * fsk))];
     }
     ft[e] = v;
   }
@@ -1503,7 +1504,8 @@ __global__ void s2d_repack_fprop_k(const float* __restrict__ f, float* __restric
 
 // dgrad filters of the s2d conv (flipped taps): gT[c'][tap'][kp]
 __global__ void s2d_repack_dgrad_k(const float* __restrict__ f, float* __restrict__ gt, int fh,
-                                   int fw, int Cg, int K, int Kp, int s, int Th, int Tw) {
+                                   int fw, int Cg, int K, int Kp, int s, int Th, int Tw,
+                                   int64_t fsc, int64_t fsk) {
   const int Cs = s * s * Cg;
   const int64_t total = (int64_t)Cs * Th * Tw * Kp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -1517,7 +1519,7 @@ __global__ void s2d_repack_dgrad_k(const float* __restrict__ f, float* __restric
       const int c = cp % Cg, ab = cp / Cg, a = ab % s, b = ab / s;
       const int t = Th - 1 - tap % Th, t2 = Tw - 1 - tap / Th;
       const int fi = a + s * t, fj = b + s * t2;
-      if (fi < fh && fj < fw) v = f[fi + (int64_t)fh * (fj + (int64_t)fw * (c + (int64_t)Cg * kp))];
+      if (fi < fh && fj < fw) v = f[fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + kp * fsk))];
     }
     gt[e] = v;
   }
@@ -1526,7 +1528,7 @@ __global__ void s2d_repack_dgrad_k(const float* __restrict__ f, float* __restric
 // wgrad finish of the s2d conv: df[fi,fj,c,k] = sum_s part[s][(tap, c'p)][k]
 __global__ void s2d_wgrad_finish_k(const float* __restrict__ part, float* df, int fh, int fw,
                                    int Cg, int K, int s, int Th, int Csp, int splits,
-                                   int64_t split_stride, int acc) {
+                                   int64_t split_stride, int acc, int64_t fsc, int64_t fsk) {
   const int64_t total = (int64_t)K * fh * fw * Cg;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -1540,7 +1542,7 @@ __global__ void s2d_wgrad_finish_k(const float* __restrict__ part, float* df, in
     const int64_t n = (int64_t)(t + Th * t2) * Csp + c + (int64_t)Cg * (a + s * b);
     float v = 0.f;
     for (int sp = 0; sp < splits; ++sp) v += part[sp * split_stride + n * K + k];
-    float* dst = df + fi + (int64_t)fh * (fj + (int64_t)fw * (c + (int64_t)Cg * k));
+    float* dst = df + fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + k * fsk));
     *dst = acc ? *dst + v : v;
   }
 }
@@ -2162,7 +2164,7 @@ struct S2D {
 };
 
 static bool s2d_plan(const ConvDims& d, S2D& z) {
-  if (d.sh != d.sw || d.sh < 2 || d.groups != 1 || d.fsc != 1) return false;
+  if (d.sh != d.sw || d.sh < 2 || d.groups != 1) return false;
   if (d.pt || d.pb || d.pl || d.pr) return false;
   z.s = d.sh;
   z.U = (d.H + z.s - 1) / z.s;
@@ -2274,7 +2276,7 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   float* ft = (float*)grow(st->ft, sizeof(float) * (size_t)d.K * taps * z.Csp, s);
   count_launch();
   s2d_repack_fprop_k<<<blocks_for((int64_t)d.K * taps * z.Csp), 256, 0, s>>>(
-      f, ft, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Tw, z.Csp);
+      f, ft, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Tw, z.Csp, d.fsc, d.fsk);
   if (halo_ok(d.K, z.Th, z.Tw, z.U)) {
     // the s2d pixel-major tensor is already a (pad-free) grid of pitch U
     GemmParams p{};
@@ -2355,7 +2357,7 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   float* gt = (float*)grow(st->ft, sizeof(float) * (size_t)z.Cs * taps * Kp, s);
   count_launch();
   s2d_repack_dgrad_k<<<blocks_for((int64_t)z.Cs * taps * Kp), 256, 0, s>>>(
-      f, gt, d.fh, d.fw, d.C, d.K, Kp, z.s, z.Th, z.Tw);
+      f, gt, d.fh, d.fw, d.C, d.K, Kp, z.s, z.Th, z.Tw, d.fsc, d.fsk);
   const int Hq = d.OH + 2 * (z.Th - 1), Wq = d.OW + 2 * (z.Tw - 1);
   if (halo_ok(z.Cs, z.Th, z.Tw, Hq)) {
     // dx_s2d = stride-1 conv of dy zero-padded by (Th-1, Tw-1) with the
@@ -2480,7 +2482,7 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
                                 z.Tw, &part, &per, s);
   count_launch();
   s2d_wgrad_finish_k<<<blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s>>>(
-      part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc);
+      part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc, d.fsc, d.fsk);
 }
 
 static bool is_fc(const ConvDims& d) {

@@ -34,7 +34,7 @@ using ck::Err;
 
 namespace ck {
 
-enum class Kind { conv, convt, pool, relu, lrn, bnorm, loss, sum };
+enum class Kind { conv, convt, pool, relu, lrn, bnorm, loss, sum, sigmoid, softmax, spnorm, bilinear, pdist, split };
 
 static Kind kind_from_name(const std::string& s) {
   if (s == "conv") return Kind::conv;
@@ -45,9 +45,13 @@ static Kind kind_from_name(const std::string& s) {
   if (s == "bnorm") return Kind::bnorm;
   if (s == "loss") return Kind::loss;
   if (s == "sum") return Kind::sum;
-  if (s == "bilinear" || s == "sigmoid" || s == "spnorm" || s == "softmax" || s == "pdist" ||
-      s == "split")
-    throw Err(CK_ERR_ARG, "layer kind '" + s + "' is not on the device hot path");
+  if (s == "sigmoid") return Kind::sigmoid;
+  if (s == "softmax") return Kind::softmax;
+  if (s == "spnorm") return Kind::spnorm;
+  if (s == "bilinear") return Kind::bilinear;
+  if (s == "pdist") return Kind::pdist;
+  if (s == "split") return Kind::split;
+  // graph.cpp:33-40 layer_kind_from_name
   throw Err(CK_ERR_ARG, "unknown layer kind '" + s + "'");
 }
 
@@ -186,6 +190,30 @@ static ck_lrn_params lrn_of(const Layer& l) {
   return ck_lrn_params{(int64_t)l.p[0], l.p[1], l.p[2], l.p[3]};
 }
 
+// graph.hpp:53-62 LossHyper: [kind top_k threshold random_ties tie_seed],
+// empty = softmaxlog with the default options
+static int loss_kind_of(const Layer& l) {
+  const int k = l.p.empty() ? (int)CK_LOSS_SOFTMAXLOG : (int)l.p[0];
+  if (k < CK_LOSS_CLASSERROR || k > CK_LOSS_HINGE)
+    throw Err(CK_ERR_DATA, "layer '" + l.name + "': unknown loss kind");
+  return k;
+}
+static ck_loss_options loss_opts_of(const Layer& l) {
+  ck_loss_options o = default_loss_options();
+  if (l.p.size() > 1) o.top_k = (int64_t)l.p[1];
+  if (l.p.size() > 2) o.threshold = l.p[2];
+  if (l.p.size() > 3) o.random_ties = (int64_t)l.p[3];
+  if (l.p.size() > 4) o.tie_seed = (uint64_t)l.p[4];
+  return o;
+}
+static ck_spnorm_params spnorm_of(const Layer& l) {
+  need_params(l, 4);
+  return ck_spnorm_params{(int64_t)l.p[0], (int64_t)l.p[1], l.p[2], l.p[3]};
+}
+// graph.hpp:63-66 PdistHyper {p = 2, no_root = false}
+static double pdist_p(const Layer& l) { return l.p.empty() ? 2.0 : l.p[0]; }
+static int pdist_no_root(const Layer& l) { return l.p.size() > 1 && l.p[1] != 0; }
+
 static ck_tensor tv(Var& v, bool deriv) { return ck_tensor{deriv ? v.deriv : v.value, v.shape}; }
 
 // Graph::finalize: arity, single producer, stable topological order, shapes.
@@ -276,13 +304,46 @@ static void finalize(ck_graph* g) {
         break;
       case Kind::loss: {
         need(l, 2, 3, 1);
-        ck_shape xs = S(0), cs = S(1);
-        if (cs.h != xs.h || cs.w != xs.w || cs.c != 1 || cs.n != xs.n)
-          throw Err(CK_ERR_SHAPE, "layer '" + l.name + "': classification labels must be " +
-                                      shape_str(ck_shape{xs.h, xs.w, 1, xs.n}) + ", got " + shape_str(cs));
+        const int kind = loss_kind_of(l);
+        ck_tensor xt{(float*)1, S(0)}, ct{(float*)1, S(1)}, wt{(float*)1, ck_shape{1, 1, 1, 1}};
+        if (l.in.size() > 2) wt.shape = S(2);
+        try {
+          check_loss_kind(&xt, &ct, l.in.size() > 2 ? &wt : nullptr, kind);
+        } catch (const Err& e) {
+          throw Err(e.code, "layer '" + l.name + "': " + e.what());
+        }
         out = ck_shape{1, 1, 1, 1};
         break;
       }
+      case Kind::sigmoid:
+      case Kind::softmax:
+        need(l, 1, 1, 1);
+        out = S(0);
+        break;
+      case Kind::spnorm: {
+        need(l, 1, 1, 1);
+        const ck_spnorm_params sp = spnorm_of(l);
+        if (sp.window_h < 1 || sp.window_w < 1) throw Err(CK_ERR_SHAPE, "spnorm window must be positive");
+        out = S(0);
+        break;
+      }
+      case Kind::bilinear:
+        need(l, 2, 2, 1);
+        out = bilinear_output_shape(S(0), S(1));
+        break;
+      case Kind::pdist:
+        need(l, 2, 2, 1);
+        out = pdist_output_shape(S(0), S(1), pdist_p(l));
+        break;
+      case Kind::split:
+        if (l.in.size() != 1 || l.out.empty() || l.out.size() > 8)
+          throw Err(CK_ERR_ARG, "layer '" + l.name + "' has wrong arity");
+        out = S(0);
+        for (int o : l.out) {
+          g->vars[o].shape = out;
+          g->vars[o].has_shape = true;
+        }
+        break;
       case Kind::sum:
         need(l, 1, 64, 1);
         for (size_t k = 1; k < l.in.size(); ++k)
@@ -424,9 +485,43 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
     case Kind::loss: {
       ck_tensor x = V(0), c = V(1), w;
       if (l.in.size() > 2) w = V(2);
-      st = ck_softmaxlog_forward(h, &x, &c, l.in.size() > 2 ? &w : nullptr, y.data, 0, s);
+      loss_forward_any(h, &x, &c, l.in.size() > 2 ? &w : nullptr, loss_kind_of(l), loss_opts_of(l),
+                       y.data, s);
+      after_launch();
       break;
     }
+    case Kind::sigmoid:
+      sigmoid_forward(V(0).data, y.data, elems(y.shape), s);
+      after_launch();
+      break;
+    case Kind::softmax: {
+      const ck_shape& xs = V(0).shape;
+      softmax_forward(V(0).data, y.data, (int)(xs.h * xs.w), (int)xs.c, (int)xs.n, s);
+      after_launch();
+      break;
+    }
+    case Kind::spnorm: {
+      ck_tensor x = V(0);
+      const ck_spnorm_params sp = spnorm_of(l);
+      st = ck_spnorm_forward(h, &x, &sp, &y, s);
+      break;
+    }
+    case Kind::bilinear: {
+      ck_tensor x = V(0), gr = V(1);
+      st = ck_bilinear_forward(h, &x, &gr, &y, s);
+      break;
+    }
+    case Kind::pdist: {
+      ck_tensor x = V(0), t = V(1);
+      st = ck_pdist_forward(h, &x, &t, pdist_p(l), pdist_no_root(l), &y, s);
+      break;
+    }
+    case Kind::split:
+      // graph.cpp split: every output is a copy of the input
+      for (int o : l.out)
+        check_cuda(cudaMemcpyAsync(g->vars[o].value, V(0).data, sizeof(float) * elems(y.shape),
+                                   cudaMemcpyDeviceToDevice, s), "copy");
+      break;
     case Kind::sum: {
       ck_tensor x0 = V(0);
       check_cuda(cudaMemcpyAsync(y.data, x0.data, sizeof(float) * elems(y.shape),
@@ -621,11 +716,67 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
       if (l.in.size() > 2) w = V(2);
       // the projection (graph.cpp:420-425: proj[0][0], 1 for the objective) is
       // read on the device from the loss output's derivative: no host sync
-      softmaxlog_backward(x.data, c.data, l.in.size() > 2 ? w.data : nullptr, 1.0f,
-                          g->vars[l.out[0]].deriv, dx.data, h->flag, (int)(x.shape.h * x.shape.w),
-                          (int)x.shape.c, (int)x.shape.n, acc(0), s);
+      loss_backward_any(h, &x, &c, l.in.size() > 2 ? &w : nullptr, loss_kind_of(l), 1.0f,
+                        g->vars[l.out[0]].deriv, dx.data, acc(0), s);
       after_launch();
       mark(0);  // labels / weights carry no derivative: left for the final zeroing
+      break;
+    }
+    case Kind::sigmoid: {
+      // activation.cpp:41-48 consumes the forward output (graph.cpp:388-389)
+      ck_tensor yv = tv(g->vars[l.out[0]], false), dx = D(0);
+      st = ck_sigmoid_backward(h, &yv, &dy, &dx, acc(0), s);
+      mark(0);
+      break;
+    }
+    case Kind::softmax: {
+      ck_tensor yv = tv(g->vars[l.out[0]], false), dx = D(0);
+      st = ck_softmax_backward(h, &yv, &dy, &dx, acc(0), s);
+      mark(0);
+      break;
+    }
+    case Kind::spnorm: {
+      ck_tensor x = V(0), dx = D(0);
+      const ck_spnorm_params sp = spnorm_of(l);
+      st = ck_spnorm_backward(h, &x, &sp, &dy, &dx, acc(0), s);
+      mark(0);
+      break;
+    }
+    case Kind::bilinear: {
+      ck_tensor x = V(0), gr = V(1), dx = D(0), dg = D(1);
+      if (acc(0) == acc(1)) {
+        st = ck_bilinear_backward(h, &x, &gr, &dy, &dx, &dg, acc(0), s);
+      } else {
+        st = ck_bilinear_backward(h, &x, &gr, &dy, &dx, nullptr, acc(0), s);
+        if (st == CK_OK) st = ck_bilinear_backward(h, &x, &gr, &dy, nullptr, &dg, acc(1), s);
+      }
+      mark(0);
+      mark(1);
+      break;
+    }
+    case Kind::pdist: {
+      ck_tensor x = V(0), t = V(1), dx = D(0), dt = D(1);
+      const double p = pdist_p(l);
+      const int nr = pdist_no_root(l);
+      if (acc(0) == acc(1)) {
+        st = ck_pdist_backward(h, &x, &t, p, nr, &dy, &dx, &dt, acc(0), s);
+      } else {
+        st = ck_pdist_backward(h, &x, &t, p, nr, &dy, &dx, nullptr, acc(0), s);
+        if (st == CK_OK) st = ck_pdist_backward(h, &x, &t, p, nr, &dy, nullptr, &dt, acc(1), s);
+      }
+      mark(0);
+      mark(1);
+      break;
+    }
+    case Kind::split: {
+      // graph.cpp split backward: dx = sum of the projections in output order
+      // (outputs no live derivative reached are the reference's zeros: skipped)
+      std::vector<const float*> src;
+      for (int o : l.out)
+        if (g->vars[o].deriv_live) src.push_back(g->vars[o].deriv);
+      sum_into(D(0).data, src.data(), (int)src.size(), elems(D(0).shape), acc(0), s);
+      after_launch();
+      mark(0);
       break;
     }
     case Kind::sum: {

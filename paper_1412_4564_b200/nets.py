@@ -112,9 +112,15 @@ class Net:
                 ys = ((xs[0] + pt + pb - w) // s + 1, (xs[1] + pl + pr - w) // s + 1, xs[2], xs[3])
             elif kind == "loss":
                 ys = (1, 1, 1, 1)
+            elif kind == "bilinear":
+                gs = shapes[ins[1]]
+                ys = (gs[1], gs[2], xs[2], xs[3])
+            elif kind == "pdist":
+                ys = (xs[0], xs[1], 1, xs[3])
             else:
                 ys = xs
-            shapes[outs[0]] = ys
+            for o in outs:  # (split: every output)
+                shapes[o] = ys
         return out
 
     def conv_flops(self):

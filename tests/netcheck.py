@@ -21,9 +21,14 @@ from __future__ import annotations
 
 import numpy as np
 
+import chain
+import fastconv as FC
 import oracle as O
 
 TOL = {"fp32": 1e-4, "tf32": 1e-2}
+# TF32 passes against the double oracle evaluated on the same TF32-rounded
+# operands (chain.tf32_operand): what remains is fp32 accumulation order
+TOL_TF32_EMULATED = 1e-4
 
 
 def rel(a, b):
@@ -46,10 +51,17 @@ def conv_err(a, b, math):
     return rel(a, b) if math == "fp32" else normwise(a, b)
 
 
-def check_layers(net, g, math, report=None, strict=True):
+def check_layers(net, g, math, report=None, strict=True, tc=None):
     """Compare every layer of `net` evaluated on device graph `g` (forward and
-    backward already run).  Returns {(layer, what): error}; asserts."""
+    backward already run).  Returns {(layer, what): error}; asserts.
+
+    Convolutions are checked against the double oracle (oracle/fastconv.py)
+    -- exact operands at TOL[math]; in TF32, the passes that ran on tcgen05
+    (tc: tc_passes(net)) also against TF32-rounded operands at
+    TOL_TF32_EMULATED (keys 'y~', 'dx~', 'df~')."""
     report = {} if report is None else report
+    if math == "tf32" and tc is None:
+        tc = tc_passes(net)
     shapes = {}
     val, der = {}, {}
 
@@ -82,14 +94,26 @@ def check_layers(net, g, math, report=None, strict=True):
         if kind == "conv":
             f, fs = V(ins[1]), shapes[ins[1]]
             b = V(ins[2]) if len(ins) > 2 else None
-            yr, _ = O.ref_conv_forward(x, xs, f, fs, b, p)
+            yr, _ = FC.conv_forward(x, xs, f, fs, b, p)
             put((name, "y"), conv_err(y, yr, math), TOL[math])
-            dxr, dfr, dbr = O.ref_conv_backward(x, xs, f, fs, p, dy)
+            dxr, dfr, dbr = FC.conv_backward(x, xs, f, fs, p, dy)
             put((name, "dx"), conv_err(D(ins[0]), dxr, math), TOL[math])
             put((name, "df"), conv_err(D(ins[1]), dfr, math), TOL[math])
             if b is not None:
                 # db = sum of dy: a plain (fixed-order, double) reduction on both paths
                 put((name, "db"), rel(D(ins[2]), dbr), 1e-4)
+            if math == "tf32":
+                fw, dg, wg = tc[name]
+                q = chain.tf32_operand
+                if fw:
+                    ye, _ = FC.conv_forward(x, xs, f, fs, b, p, q=q)
+                    put((name, "y~"), normwise(y, ye), TOL_TF32_EMULATED)
+                if dg:
+                    dxe, _, _ = FC.conv_backward(x, xs, f, fs, p, dy, (True, False, False), q=q)
+                    put((name, "dx~"), normwise(D(ins[0]), dxe), TOL_TF32_EMULATED)
+                if wg:
+                    _, dfe, _ = FC.conv_backward(x, xs, f, fs, p, dy, (False, True, False), q=q)
+                    put((name, "df~"), normwise(D(ins[1]), dfe), TOL_TF32_EMULATED)
         elif kind == "relu":
             exact((name, "y"), y, O.ref_relu(x))
             exact((name, "dx"), D(ins[0]), O.ref_relu(x, dy))
@@ -126,3 +150,32 @@ def format_report(report):
     for (layer, what), e in report.items():
         worst[f"{layer}.{what}"] = e
     return ", ".join(f"{k}={v:.1e}" for k, v in worst.items())
+
+
+def tc_passes(net):
+    """{conv layer: (fprop, dgrad, wgrad) ran on tcgen05} for a net's conv
+    layers in TF32, measured with the handle's tensor-core launch counter on
+    batch-1 copies of each layer's shapes (the envelope does not depend on
+    the batch)."""
+    import torch
+
+    from paper_1412_4564_b200 import blocks as B
+    out = {}
+    hd = B.handle()
+    for name, xs, fs, p in net.conv_layers():
+        xs1 = (xs[0], xs[1], xs[2], 1)
+        x = B.from_hwcn(xs1, fill=0.5)
+        f = B.from_hwcn(tuple(fs), fill=0.01)
+        g = B.ConvGeom(*p)
+        ys = B.conv_output_shape(xs1, tuple(fs), g)
+        dy = B.from_hwcn(ys, fill=1.0)
+        res = []
+        for want in ((True, False, False), (False, True, False)):
+            t0 = hd.tc_launches
+            B.conv_backward(x, f, g, dy, want_dx=want[0], want_df=want[1], want_db=False)
+            res.append(hd.tc_launches > t0)
+        t0 = hd.tc_launches
+        B.conv_forward(x, f, None, g)
+        torch.cuda.synchronize()
+        out[name] = (hd.tc_launches > t0, res[0], res[1])
+    return out

@@ -85,6 +85,18 @@ CONV_CASES = [
 ]
 
 
+def tc_expected(xs, fs, g):
+    """The shapes the tcgen05 kernels must take (conv_tc.cu envelope): >= 16
+    channels and filters per group, or the stride-s space-to-depth route
+    (groups 1, no padding), or an FC layer (1x1 output, no padding)."""
+    groups = g[6]
+    if xs[2] // groups >= 16 and fs[3] // groups >= 16:
+        return True
+    if g[0] == g[1] >= 2 and groups == 1 and not any(g[2:6]):
+        return True
+    return False
+
+
 @pytest.mark.parametrize("math", ["fp32", "tf32"])
 @pytest.mark.parametrize("xs,fs,g", CONV_CASES)
 def test_conv(xs, fs, g, math):
@@ -93,6 +105,8 @@ def test_conv(xs, fs, g, math):
     f = r.uniform(O.size(fs), -0.1, 0.1)
     b = r.uniform(fs[3])
     geom = B.ConvGeom(*g)
+    hd = B.handle()
+    tc0 = hd.tc_launches
     y_ref, ys = O.conv_forward(x, xs, f, fs, b, g)
     y = B.conv_forward(dev(x, xs), dev(f, fs), torch.from_numpy(b).cuda(), geom, math=math)
     assert B.hwcn_shape(y) == ys
@@ -103,6 +117,36 @@ def test_conv(xs, fs, g, math):
     assert err(host(dx), dx_ref, math) < TOL[math]
     assert err(host(df), df_ref, math) < TOL[math]
     assert rel(host(db), db_ref) < TOL["fp32"]
+    tc = hd.tc_launches - tc0
+    if math == "fp32":
+        assert tc == 0  # the verification path never touches the tensor cores
+    elif tc_expected(xs, fs, g):
+        assert tc >= 3, f"TF32 conv ran {tc} tcgen05 GEMMs (fprop+dgrad+wgrad expected)"
+
+
+@pytest.mark.parametrize("xs,fs,g", [CONV_CASES[9], CONV_CASES[10], CONV_CASES[8],
+                                     CONV_CASES[13]])
+def test_conv_accumulate_tensor_cores(xs, fs, g):
+    """TF32 backward with accumulate=1 (graph.cpp:595 `+=` fused into the
+    tcgen05 epilogues / split-K finishers): dx, df, db land on top of what
+    was there, and the GEMMs really ran on the tensor cores."""
+    r = O.Rng(sum(xs) + 3)
+    x, f = r.uniform(O.size(xs)), r.uniform(O.size(fs), -0.1, 0.1)
+    _, ys = O.conv_forward(x, xs, f, fs, None, g)
+    dy = r.uniform(O.size(ys))
+    dx_ref, df_ref, db_ref = O.conv_backward(x, xs, f, fs, g, dy)
+    base_dx, base_df, base_db = (r.uniform(O.size(xs)), r.uniform(O.size(fs), -0.1, 0.1),
+                                 r.uniform(fs[3]))
+    dx, df = dev(base_dx, xs), dev(base_df, fs)
+    db = torch.from_numpy(base_db.copy()).cuda()
+    hd = B.handle()
+    tc0 = hd.tc_launches
+    B.conv_backward(dev(x, xs), dev(f, fs), B.ConvGeom(*g), dev(dy, ys), math="tf32",
+                    out=(dx, df, db), accumulate=True)
+    assert hd.tc_launches - tc0 >= 2
+    assert err(host(dx), dx_ref + base_dx, "tf32") < TOL["tf32"]
+    assert err(host(df), df_ref + base_df, "tf32") < TOL["tf32"]
+    assert rel(host(db), db_ref + base_db) < 1e-4
 
 
 def test_conv_accumulate_and_skip():
@@ -120,20 +164,40 @@ def test_conv_accumulate_and_skip():
     assert rel(host(df), df_ref + base_df) < 1e-4
 
 
+CONVT_CASES = [
+    # small channel counts: the FP32 SIMT kernels (outside the tcgen05 envelope)
+    ((5, 4, 6, 2), (3, 2, 6, 4), (2, 1, 1, 0, 0, 1), False),
+    # >= 16 channels, up = 1 with crops: the stride-1 tcgen05 path
+    ((9, 8, 32, 2), (3, 3, 32, 48), (1, 1, 1, 1, 0, 1), True),
+    # >= 16 channels, up = 2 (FCN-style 2x upsampling): the space-to-depth tcgen05 path
+    ((7, 6, 64, 3), (4, 4, 64, 32), (2, 2, 0, 0, 0, 0), True),
+    ((8, 8, 48, 2), (3, 3, 48, 16), (2, 2, 0, 0, 0, 0), True),
+]
+
+
 @pytest.mark.parametrize("math", ["fp32", "tf32"])
-def test_convt(math):
-    r = O.Rng(32)
-    xs, fs, cg = (5, 4, 6, 2), (3, 2, 6, 4), (2, 1, 1, 0, 0, 1)
-    x, f = r.uniform(O.size(xs)), r.uniform(O.size(fs))
+@pytest.mark.parametrize("xs,fs,cg,tc", CONVT_CASES)
+def test_convt(xs, fs, cg, tc, math):
+    """conv.cpp:283-365: y = M^T x, dx = conv of dy with the swapped bank, df."""
+    r = O.Rng(32 + sum(xs))
+    x, f = r.uniform(O.size(xs)), r.uniform(O.size(fs), -0.2, 0.2)
     y_ref, ys = O.convt_forward(x, xs, f, fs, cg)
     geom = B.ConvTransposeGeom(*cg)
+    hd = B.handle()
+    tc0 = hd.tc_launches
     y = B.convt_forward(dev(x, xs), dev(f, fs), geom, math=math)
+    assert B.hwcn_shape(y) == ys
     assert err(host(y), y_ref, math) < TOL[math]
     dy = r.uniform(O.size(ys))
     dx_ref, df_ref = O.convt_backward(x, xs, f, fs, cg, dy)
     dx, df = B.convt_backward(dev(x, xs), dev(f, fs), geom, dev(dy, ys), math=math)
     assert err(host(dx), dx_ref, math) < TOL[math]
     assert err(host(df), df_ref, math) < TOL[math]
+    ran = hd.tc_launches - tc0
+    if math == "tf32" and tc:
+        assert ran >= 3, f"convt ran {ran} tcgen05 GEMMs"
+    if math == "fp32":
+        assert ran == 0
 
 
 def test_conv_shape_errors():
