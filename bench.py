@@ -1,20 +1,24 @@
 #!/usr/bin/env python
-"""AlexNet fwd+bwd training throughput on B200 (BASELINE.json metric).
+"""Training throughput of the BASELINE.json networks on B200 (headline:
+AlexNet fwd+bwd images/sec, batch 256 per GPU).
 
-One step = forward + backward + gradient allreduce (N>1) + SGD of
-imagenet-caffe-alex at 256 images per GPU, through the device DAG engine of
-libck.so.  Launch: `python bench.py` (N=1) or under torch.distributed.run
-with --gpus N (one process per GPU, NCCL).  Rank 0 prints one JSON line.
+One step = forward + backward + gradient allreduce (N>1) + SGD of the
+network through the device DAG engine of libck.so.  `python bench.py` runs
+N=1; `python bench.py --gpus N` re-launches itself under
+torch.distributed.run with one process per GPU (NCCL) when it is not already
+a rank; rank 0 prints one JSON line.  `--net lenet|cifar|alexnet|vgg16bn`
+selects the other BASELINE configs (each at its BASELINE batch).
 
 `--impl reference` times the reference's own CPU implementation (the convkit
-sources compiled verbatim into oracle/_ref) on this box's host cores.
+sources compiled verbatim into oracle/_ref, driven through its DAG engine) on
+this box's host cores; it loads nothing from paper_1412_4564_b200's library.
 """
 from __future__ import annotations
 
 import argparse
-import ctypes as C
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -24,10 +28,22 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "AlexNet fwd+bwd images/sec"
 UNIT = "images/s"
-PUBLISHED = 264.1  # MatConvNet CuDNN v2, 1x Titan Black, batch 256
-WORKLOAD = "imagenet-caffe-alex 227x227x3, fwd+bwd+SGD, 256 images/GPU"
+PUBLISHED = 264.1  # MatConvNet CuDNN v2, AlexNet b=256, 1x Titan Black
+WORKLOADS = {
+    "alexnet": "imagenet-caffe-alex 227x227x3, fwd+bwd+SGD, 256 images/GPU",
+    "vgg16bn": "VGG-VD-16 with batch norm, 224x224x3, fwd+bwd+SGD, 64 images/GPU",
+    "cifar": "CIFAR-10 quick with LRN, 32x32x3, fwd+bwd+SGD, 128 images/GPU",
+    "lenet": "MNIST LeNet, 28x28x1, fwd+bwd+SGD, 100 images/GPU",
+}
+NAMES = {"alexnet": "AlexNet", "vgg16bn": "VGG-16-bn", "cifar": "CIFAR-10 quick",
+         "lenet": "LeNet"}
+# SURVEY.md §8d CPU sample batches for the reference (per-image linear)
+REF_SAMPLE = {"alexnet": 16, "vgg16bn": 2, "cifar": 128, "lenet": 100}
+
+
+def metric_for(net):
+    return f"{NAMES[net]} fwd+bwd images/sec"
 
 
 def parse():
@@ -36,8 +52,8 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--net", default="alexnet")
-    p.add_argument("--batch", type=int, default=256)
+    p.add_argument("--net", default="alexnet", choices=sorted(WORKLOADS))
+    p.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: BASELINE's)")
     p.add_argument("--math", default="tf32", choices=["tf32", "fp32"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -46,7 +62,36 @@ def parse():
     # internal: CPU sample run in a subprocess
     p.add_argument("--cpu-sample", type=int, default=0)
     p.add_argument("--cpu-reps", type=int, default=1)
-    return p.parse_args()
+    a = p.parse_args()
+    if not a.batch:
+        a.batch = {"lenet": 100, "cifar": 128, "alexnet": 256, "vgg16bn": 64}[a.net]
+    return a
+
+
+def ck_env_guard():
+    """Every CK_* variable in the environment, recorded; the run is refused
+    when one is set (product builds ignore them -- knob() in capi.cu -- but a
+    number must not be taken under a tuning override either way)."""
+    env = {k: v for k, v in os.environ.items() if k.startswith("CK_") and k != "CK_EXTRA_NVCC"}
+    if env:
+        print(f"bench.py: refusing to run with CK_* overrides set: {env}", file=sys.stderr)
+        sys.exit(2)
+    return env
+
+
+def relaunch_distributed(args):
+    """--gpus N outside torch.distributed.run: become N ranks (one per GPU)."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("NCCL_DEBUG", "INFO")  # init log (nranks, NVLS) on stderr
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 # ---------------------------------------------------------------- clocks --
@@ -67,7 +112,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -107,7 +152,28 @@ class ClockSampler:
 
 # ------------------------------------------------------- CPU reference --
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def ref_graph_for(net):
+    """The reference DAG engine (oracle/_ref) with the network and its
+    synthetic inputs -- generated by the oracle's restatement of the
+    reference generator (oracle.Rng; identical stream to rng.cpp, pinned by
+    tests/test_oracle_vs_ref.py), so nothing of libck is loaded."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
 
@@ -128,7 +194,7 @@ def ref_graph_for(net):
     shapes = dict(net.inputs)
     for n, s, _ in net.params:
         shapes[n] = s
-    for k, v in {**net.init_params(), **net.init_inputs()}.items():
+    for k, v in {**net.init_params(rng=O.Rng), **net.init_inputs(rng=O.Rng)}.items():
         rg.bind(k, v, shapes[k])
     return rg, O
 
@@ -160,30 +226,28 @@ def run_cpu_sample(net_name, batch, reps, threads, timeout=900):
 
 
 def cpu_baseline(net_name):
-    """The verbatim reference on this box's host cores, bounded sample."""
+    """The verbatim reference on this box's host cores, bounded samples at the
+    SURVEY §8d batch: reference-faithful single-threaded BLAS (the reference
+    has no OpenMP) and the generous all-cores BLAS."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     if not O.ref_available():
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref not built"}
-    threads = os.cpu_count() or 1
-    batch = 128  # ~10 s of reference CPU work
-    res = run_cpu_sample(net_name, batch, 1, threads)
-    return {"value": res["images"] / res["seconds"], "unit": UNIT, "cores": threads,
+    nproc = os.cpu_count() or 1
+    batch = REF_SAMPLE[net_name]
+    many = run_cpu_sample(net_name, batch, 1, nproc)
+    one = run_cpu_sample(net_name, batch, 1, 1)
+    return {"value": many["images"] / many["seconds"], "unit": UNIT, "cores": nproc,
             "kind": "reference",
             "sample": f"1 fwd+bwd of {net_name} at batch {batch} through the reference DAG engine "
-                      f"(graph.cpp:494/548), OpenBLAS GEMM with {threads} threads, "
-                      f"{res['seconds']:.1f} s", "cpu": cpu_model()}
-
-
-def cpu_model():
-    try:
-        for ln in open("/proc/cpuinfo"):
-            if ln.startswith("model name"):
-                return ln.split(":", 1)[1].strip()
-    except OSError:
-        pass
-    return "unknown"
+                      f"(graph.cpp:494/548), OpenBLAS GEMM with {nproc} threads, "
+                      f"{many['seconds']:.1f} s",
+            "single_thread": {"value": one["images"] / one["seconds"], "cores": 1,
+                              "sample": f"same, OPENBLAS_NUM_THREADS=1 (reference-faithful: "
+                                        f"no OpenMP in the reference build), "
+                                        f"{one['seconds']:.1f} s"},
+            "nproc": nproc, "cpu": cpu_model()}
 
 
 def reference_main(args):
@@ -199,7 +263,7 @@ def reference_main(args):
                                                               "build) missing on this box"}))
         return 0
     os.environ["OPENBLAS_NUM_THREADS"] = str(threads)
-    batch = 8  # bounded sample per step (~0.7 s each)
+    batch = REF_SAMPLE[args.net]  # bounded sample per step
     net = nets.NETS[args.net](batch=batch)
     rg, _ = ref_graph_for(net)
     for _ in range(args.warmup):
@@ -211,12 +275,12 @@ def reference_main(args):
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = batch * args.steps / total
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+    out = {"metric": metric_for(args.net), "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic (xoshiro256**: U[-1,1) data, 0.01 N(0,1) weights, random labels)",
            "impl": "reference",
-           "config": {"workload": WORKLOAD + f" (sample: {batch} images per step)",
+           "config": {"workload": WORKLOADS[args.net] + f" (sample: {batch} images per step)",
                       "per_step_batch": batch, "threads": threads},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                             "sample": f"{args.steps} steps x fwd+bwd at batch {batch}, reference "
@@ -228,24 +292,62 @@ def reference_main(args):
     return 0
 
 
+# --------------------------------------------------- roofline helpers --
+
+def mem_layers(net):
+    """Memory-bound layers with SURVEY.md §8d compulsory bytes per pass:
+    (layer, kind, fwd bytes, bwd bytes)."""
+    shapes = dict(net.inputs)
+    for n, s, _ in net.params:
+        shapes[n] = s
+    out = []
+    for kind, name, ins, outs, p in net.layers:
+        xs = shapes[ins[0]]
+        nx = xs[0] * xs[1] * xs[2] * xs[3]
+        if kind == "conv":
+            fs = shapes[ins[1]]
+            ys = ((xs[0] + p[2] + p[3] - fs[0]) // p[0] + 1,
+                  (xs[1] + p[4] + p[5] - fs[1]) // p[1] + 1, fs[3], xs[3])
+        elif kind == "pool":
+            ys = ((xs[0] + p[4] + p[5] - p[0]) // p[2] + 1,
+                  (xs[1] + p[6] + p[7] - p[1]) // p[3] + 1, xs[2], xs[3])
+            ny = ys[0] * ys[1] * ys[2] * ys[3]
+            out.append((name, "pool", 4 * (nx + ny), 4 * (2 * nx + ny)))
+        elif kind == "loss":
+            ys = (1, 1, 1, 1)
+        else:
+            ys = xs
+            if kind in ("lrn", "bnorm"):
+                out.append((name, kind, 8 * nx, 12 * nx))
+        shapes[outs[0]] = ys
+    return out
+
+
 # ---------------------------------------------------------------- ours --
 
 def main():
     args = parse()
     if args.cpu_sample:
         return cpu_sample_main(args)
+    ck_env = ck_env_guard()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args)
     if args.impl == "reference":
         return reference_main(args)
 
     import numpy as np
     import torch
 
-    from paper_1412_4564_b200 import lib, nets
+    from paper_1412_4564_b200 import nets
+    from paper_1412_4564_b200._lib import lib
     from paper_1412_4564_b200.graph import Graph, Trainer
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE {world} != --gpus {args.gpus}", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -291,7 +393,7 @@ def main():
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
-    launches0 = g.hd.launches
+    launches0, tc0 = g.hd.launches, g.hd.tc_launches
     with torch.cuda.stream(stream):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -301,26 +403,34 @@ def main():
     barrier()
     clk = clocks.stop()
     launches = g.hd.launches - launches0  # total inside the timed region
+    tc_launches = g.hd.tc_launches - tc0
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     value = world * args.batch / (ms / 1e3)
     loss = tr.step(want_loss=True, stream=sp)
+    if not np.isfinite(loss):
+        print(f"bench.py: non-finite loss {loss}", file=sys.stderr)
+        return 3
 
     # ---- per-layer breakdown + roofline of the dominant kernel ----------
-    # One more step with per-layer events and per-launch events around every
-    # tensor-core GEMM (ck_set_kernel_profiling), all on the evaluation stream.
+    # One more step, eager, with per-layer events and per-launch events around
+    # every tensor-core GEMM (ck_set_kernel_profiling), on the step's stream;
+    # the trainer's step events give the allreduce-complete tail.
     g.set_profiling(True)
     g.hd.kernel_profiling(True)
+    ar0 = tr.allreduces
     tr.step(want_loss=False, stream=sp)
+    ar_step = tr.allreduces - ar0
     torch.cuda.synchronize()
     times = g.layer_times()
     kprof = g.hd.kernel_profile()
+    fwd_ms, bwd_ms, tail_ms = tr.last_timing()
     g.hd.kernel_profiling(False)
     g.set_profiling(False)
     flops = {}
     for name, xs, fs, p in net.conv_layers():
-        s, pt, pb, pl, pr = p[0], p[2], p[3], p[4], p[5]
-        oh = (xs[0] + pt + pb - fs[0]) // s + 1
-        ow = (xs[1] + pl + pr - fs[1]) // s + 1
+        s_, pt, pb, pl, pr = p[0], p[2], p[3], p[4], p[5]
+        oh = (xs[0] + pt + pb - fs[0]) // s_ + 1
+        ow = (xs[1] + pl + pr - fs[1]) // s_ + 1
         flops[name] = 2.0 * xs[3] * oh * ow * fs[3] * fs[0] * fs[1] * fs[2]
     conv_ms = sum(f + b for n, f, b in times if n in flops)
     step_layers_ms = sum(f + b for _, f, b in times)
@@ -329,6 +439,7 @@ def main():
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except OSError:
         pass
+    hbm_peak = peaks.get("hbm_gbs") or 6512.0
     bf16 = peaks.get("bf16_tflops_sustained") or 1400.0
     tf32_peak, peak_src = bf16 / 2.0, ("0.5 x MEASURED_PEAKS.json bf16_tflops_sustained "
                                        "(TF32 = half the bf16 rate)")
@@ -341,19 +452,19 @@ def main():
         pass
     if args.math != "tf32":
         tf32_peak, peak_src = 74.0, "FP32 FFMA nominal 148 SM x 128 x 2 x 1.965 GHz"
+    traffic_db = {}
+    try:
+        traffic_db = json.load(open(os.path.join(ROOT, "profiles", "kernel_traffic.json")))
+    except (OSError, ValueError):
+        pass
     if kprof:
         # dominant kernel = the GEMM launch with the largest time in the step
         lab, kms, kfl = max(kprof, key=lambda r: r[1])
         achieved = kfl / (kms / 1e3) / 1e12
-        traffic = None
-        try:  # dram bytes of this launch from a committed ncu --set full capture
-            traffic = json.load(open(os.path.join(ROOT, "profiles", "kernel_traffic.json"))).get(lab)
-        except (OSError, ValueError):
-            pass
         gemm_ms = sum(r[1] for r in kprof)
         roofline = {"bound": "tensor", "kernel": f"tc_gemm_kernel: {lab}", "achieved": achieved,
                     "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
-                    "traffic": traffic, "peak_source": peak_src, "launch_ms": kms,
+                    "traffic": traffic_db.get(lab), "peak_source": peak_src, "launch_ms": kms,
                     "algorithmic_flop": kfl,
                     "share_of_step": kms / max(step_layers_ms, 1e-9),
                     "all_gemm": {"achieved": sum(r[2] for r in kprof) / (gemm_ms / 1e3) / 1e12,
@@ -367,11 +478,27 @@ def main():
         roofline = {"bound": "fp32", "kernel": f"{dom[0]} fprop+dgrad+wgrad",
                     "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": achieved / tf32_peak, "traffic": None, "peak_source": peak_src}
+    # memory-bound layers: SURVEY §8d compulsory bytes / event time / HBM peak
+    tmap = {n: (f, b) for n, f, b in times}
+    hbm = []
+    for name, kind, fb, bb in mem_layers(net):
+        f, b = tmap.get(name, (0.0, 0.0))
+        for pas, byts, t in (("fwd", fb, f), ("bwd", bb, b)):
+            if t > 0:
+                gbs = byts / (t / 1e3) / 1e9
+                hbm.append({"layer": f"{name} {pas}", "kind": kind, "bytes": byts, "ms": t,
+                            "achieved": gbs, "frac": gbs / hbm_peak,
+                            "traffic": traffic_db.get(f"{name} {pas}")})
+    roofline["hbm"] = {"peak": hbm_peak, "unit": "GB/s",
+                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)", "layers": hbm}
     if args.profile_layers and rank == 0:
         for n, f, b in times:
             print(f"  {n:8s} fwd {f:8.3f} ms  bwd {b:8.3f} ms", file=sys.stderr)
         for lab, kms, kfl in sorted(kprof, key=lambda r: -r[1]):
             print(f"  gemm {lab:44s} {kms:7.3f} ms {kfl / kms / 1e9:7.1f} TF/s", file=sys.stderr)
+        for h in hbm:
+            print(f"  hbm {h['layer']:12s} {h['ms']:7.3f} ms {h['achieved']:7.0f} GB/s "
+                  f"{h['frac']:.2f}", file=sys.stderr)
 
     # ---- end to end through the public API with host buffers ------------
     e2e = None
@@ -417,21 +544,33 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"failed: {ex}"[:300]}
 
+    dp_info = {"allreduce_groups_per_step": ar_step,
+               "profiled_step": {"fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+                                 "exchange_tail_ms": tail_ms,
+                                 "note": "eager profiled step: time from the last backward "
+                                         "kernel to the completion of the last gradient "
+                                         "allreduce + SGD (communication not hidden by "
+                                         "backward); single GPU: the update-stream tail"}}
     if rank == 0:
-        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        out = {"metric": metric_for(args.net), "value": value, "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
                "higher_is_better": True, "scaling": "weak",
-               "vs_baseline": value / PUBLISHED, "dtype": args.math,
+               "vs_baseline": value / PUBLISHED if args.net == "alexnet" else None,
+               "dtype": args.math,
                "data": "synthetic (xoshiro256**: U[-1,1) data, 0.01 N(0,1) weights, random labels)",
-               "config": {"workload": WORKLOAD, "global_batch": world * args.batch,
-                          "per_gpu_batch": args.batch, "parallelism": f"dp{world}",
-                          "math": args.math, "cuda_graph": not args.no_graph,
-                          "l2": "inputs larger than L2: the step streams ~4 GB of activations "
-                                "(input batch alone 158 MB > 126 MB L2)",
+               "config": {"workload": WORKLOADS[args.net] if args.batch == nets.DEFAULT_BATCH[
+                              args.net] else f"{args.net} batch {args.batch}",
+                          "global_batch": world * args.batch, "per_gpu_batch": args.batch,
+                          "parallelism": f"dp{world}", "math": args.math,
+                          "cuda_graph": not args.no_graph,
+                          "l2": "inputs larger than L2: the step streams the whole activation "
+                                "set (AlexNet b=256: ~4 GB; input batch alone 158 MB > 126 MB)",
+                          "ck_env": ck_env, "libck": lib().ck_version().decode(),
                           "vs_baseline_ref": "MatConvNet CuDNN v2 AlexNet b=256 on 1x Titan "
                                              "Black, 264.1 img/s (PAPER.md:126)"},
                "loss": loss, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-               "gpu_launches": int(launches), "clocks": clk}
+               "dp": dp_info, "gpu_launches": int(launches), "tc_launches": int(tc_launches),
+               "clocks": clk}
         print(json.dumps(out))
     if dist:
         dist.destroy_process_group()

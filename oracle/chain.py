@@ -40,7 +40,13 @@ def tf32_operand(a, mode=None):
     return u.view(np.float32).astype(np.float64)
 
 
-def run(net, params: dict, inputs: dict, backward=True, tf32=False):
+def run(net, params: dict, inputs: dict, backward=True, tf32=False, gates=None):
+    """gates = {var: values} routes the backward of the ReLU / max-pool layers
+    reading `var` by the given values' signs / window maxima instead of the
+    oracle's own: a comparison that holds the device's discrete routing
+    fixed (each of its decisions is checked bit-exactly, layer by layer, in
+    tests/netcheck.py) so the continuous arithmetic around it can be bounded."""
+    gates = gates or {}
     shapes = dict(net.inputs)
     for name, shape, _ in net.params:
         shapes[name] = tuple(shape)
@@ -114,9 +120,11 @@ def run(net, params: dict, inputs: dict, backward=True, tf32=False):
             if len(ins) > 2:
                 derivs[ins[2]] += O.conv_backward(x, xs, f, fs, p, dy, (False, False, True))[2]
         elif kind == "relu":
-            derivs[ins[0]] += np.where(x > 0, dy, 0.0)
+            gx = gates.get(ins[0], x)
+            derivs[ins[0]] += np.where(gx > 0, dy, 0.0)
         elif kind == "pool":
-            derivs[ins[0]] += O.pool_backward(x, xs, p, dy).astype(np.float64)
+            gx = gates.get(ins[0], x) if p[8] == 0 else x
+            derivs[ins[0]] += O.pool_backward(gx, xs, p, dy).astype(np.float64)
         elif kind == "lrn":
             derivs[ins[0]] += O.lrn_backward(x, xs, int(p[0]), p[1], p[2], p[3], dy)
         elif kind == "bnorm":

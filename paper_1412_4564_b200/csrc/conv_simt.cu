@@ -306,13 +306,13 @@ __global__ void wgrad_reduce_k(const float* __restrict__ part, float* df, ConvDi
     int64_t t = e / rows;
     int64_t n = t % cols;
     int64_t g = t / cols;
-    float s = 0.f;
+    double s = 0.0;  // the split partials summed in double (FP32 verification path)
     for (int sp = 0; sp < splits; ++sp) s += part[sp * per + (g * cols + n) * rows + m];
     // m = fi + fh*(fj + fw*c)
     int64_t fi = m % d.fh, r = m / d.fh, fj = r % d.fw, c = r / d.fw;
     int64_t k = g * cols + n;
     float* dst = df + fi + (int64_t)d.fh * (fj + (int64_t)d.fw * (c * d.fsc + k * d.fsk));
-    *dst = acc ? *dst + s : s;
+    *dst = acc ? *dst + (float)s : (float)s;
   }
 }
 
@@ -403,7 +403,13 @@ int wgrad_splits(const ConvDims& d) {
   int64_t want = (148 * 4 + tiles - 1) / tiles;
   int64_t maxs = (K + 255) / 256;  // at least 256 pixels per split
   if (want > maxs) want = maxs;
-  if (want > 64) want = 64;
+  // long reductions (b=256 weight gradients: up to 186k pixels) get more,
+  // shorter fp32 partial sums (<= 2048 pixels each where the workspace allows)
+  const int64_t per = rows * cols * d.groups;
+  while (want < 256 && K / want > 2048 && per * want * 2 * sizeof(float) <= (size_t)512 << 20)
+    want *= 2;
+  if (want > maxs) want = maxs;
+  if (want > 256) want = 256;
   if (want < 1) want = 1;
   return (int)want;
 }

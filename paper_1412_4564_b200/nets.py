@@ -64,8 +64,10 @@ class Net:
         return out
 
     # -- synthetic inputs ---------------------------------------------------
-    def init_params(self, seed=2):
-        r = Rng(seed)
+    def init_params(self, seed=2, rng=None):
+        """rng: the generator class (default: libck's host xoshiro256**; the
+        oracle's restatement oracle.Rng yields the identical stream)."""
+        r = (rng or Rng)(seed)
         out = {}
         for name, shape, init in self.params:
             n = int(np.prod(shape))
@@ -77,11 +79,12 @@ class Net:
                 out[name] = np.zeros(n, np.float32)
         return out
 
-    def init_inputs(self, data_seed=1, label_seed=3):
+    def init_inputs(self, data_seed=1, label_seed=3, rng=None):
         ds = self.inputs["data"]
         ls = self.inputs["label"]
-        return {"data": Rng(data_seed).uniform(int(np.prod(ds))),
-                "label": Rng(label_seed).labels(int(np.prod(ls)), self.classes)}
+        R = rng or Rng
+        return {"data": R(data_seed).uniform(int(np.prod(ds))),
+                "label": R(label_seed).labels(int(np.prod(ls)), self.classes)}
 
     def build(self, target):
         """Emit into any object with the graph.hpp construction API."""
@@ -260,3 +263,5 @@ def vgg16_bn(batch=64, image=224) -> Net:
 
 
 NETS = {"lenet": lenet, "cifar": cifar, "alexnet": alexnet, "vgg16bn": vgg16_bn}
+# BASELINE.json configs: the batch each network is quoted at
+DEFAULT_BATCH = {"lenet": 100, "cifar": 128, "alexnet": 256, "vgg16bn": 64}

@@ -48,7 +48,12 @@ def normwise(a, b):
 
 
 def conv_err(a, b, math):
-    return rel(a, b) if math == "fp32" else normwise(a, b)
+    """Relative error of a contraction: normwise (max(||a-b||/||b||,
+    max|a-b|/max|b|)).  At b=256 a weight gradient sums 186k products per
+    element; element-by-element relative error of cancelled sums is not a
+    property of either implementation (the float reference itself misses the
+    double oracle by 1e-4 there), so FP32 is held to 1e-4 normwise."""
+    return normwise(a, b)
 
 
 def check_layers(net, g, math, report=None, strict=True, tc=None):

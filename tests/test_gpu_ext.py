@@ -97,8 +97,10 @@ def test_bilinear(xs, gs):
     rdx, rdg = O.ref_bilinear(x, xs, g, gs, dy=dy)
     assert np.array_equal(host(dg), rdg)      # per-site channel sum, reference order
     assert rel(host(dx), rdx) < 1e-5           # scatter (atomic) order differs
+    # vs the double restatement: the reference's own float rounding of the
+    # channel sums (cancellation) is ~1e-4 of the largest element
     edx, edg = E.bilinear_backward(x, xs, g, gs, dy)
-    assert rel(host(dx), edx) < 1e-4 and rel(host(dg), edg) < 1e-4
+    assert rel(host(dx), edx) < 1e-4 and rel(host(dg), edg) < 1e-3
 
 
 def test_bilinear_grid_errors():
@@ -159,6 +161,12 @@ def test_loss_kinds(kind, fc):
         ref = E.loss_backward(x, xs, lab, cs, wt, kind, p=0.7)
         if np.abs(ref).max() == 0:
             assert np.abs(dx).max() == 0
+        elif kind == 7:
+            # binarylog: q = c (v - 0.5) + 0.5 cancels in float for v near the
+            # label's end (the reference computes it in float too): bit-for-bit
+            # with the verbatim reference, 1e-3 of the double restatement
+            assert rel(dx, O.ref_loss_grad(x, xs, lab, cs, wt, kind, p=0.7)) < 1e-6
+            assert rel(dx, ref) < 1e-3
         else:
             assert rel(dx, ref) < 1e-5
 
