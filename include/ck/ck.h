@@ -323,7 +323,10 @@ void ck_trainer_destroy(ck_trainer* t);
 /* Join an NCCL data-parallel group (one process per GPU). */
 ck_status ck_trainer_init_dp(ck_trainer* t, const char id[128], int rank, int world);
 /* forward + backward + gradient allreduce (overlapped) + SGD on `stream`.
- * If loss_host != NULL the step's objective is copied back (synchronising). */
+ * If loss_host != NULL the step's objective is copied back (synchronising).
+ * A label error (CK_ERR_DATA) or a non-finite objective (CK_ERR_NUMERIC,
+ * SPEC.md:716 "NaN loss aborts") of a step is reported by that call when it
+ * synchronises, else by the next call once the step is complete. */
 ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream);
 /* Replay each step as one CUDA graph: captured on the first graph step after
  * an eager one (same stream; profiling steps stay eager).  A captured step is
@@ -341,6 +344,36 @@ ck_status ck_trainer_last_timing(ck_trainer* t, float* fwd_ms, float* bwd_ms, fl
 /* NCCL allreduce groups issued by eager / captured steps (DP evidence). */
 int64_t ck_trainer_allreduce_count(const ck_trainer* t);
 
+/* ---- files (host only; errors in ck_io_last_error()) -------------------- */
+/* blob.cpp:29-79 / SPEC.md:87: raw tensor blob -- four u64 little-endian dims
+ * (H, W, C, N) then the float32 values, little-endian, H fastest. */
+const char* ck_io_last_error(void);
+ck_status ck_blob_write(const char* path, const float* host_data, ck_shape shape);
+ck_status ck_blob_read_shape(const char* path, ck_shape* shape);
+/* reads into host memory; the stored shape must equal `expect` */
+ck_status ck_blob_read(const char* path, float* host_data, ck_shape expect);
+/* SPEC.md:721-728 load_idx: images -> H x W x 1 x N in [0,1], labels -> 1..C
+ * (raw + 1).  out == NULL returns only dims (H, W, C, N). */
+ck_status ck_idx_read(const char* path, float* out, int64_t dims[4]);
+
+/* Model directory: manifest.txt (line-oriented
+ *   "ck-manifest 1" / "var <name> input|param H W C N" /
+ *   "layer <kind> <name> in=<a,..> out=<b,..> p=<v,..>" / "blob <param> <file>" /
+ *   "meta <key> <value>") plus one blob per parameter.  Lossless: save ->
+ * load -> save is byte-identical.  Load builds and finalizes the graph on h. */
+ck_status ck_graph_save(ck_graph* g, const char* dir);
+ck_status ck_graph_load(ck_handle* h, const char* dir, ck_math math, ck_graph** out);
+/* normalization metadata carried by the manifest */
+ck_status ck_graph_set_meta(ck_graph* g, const char* key, const char* value);
+const char* ck_graph_get_meta(const ck_graph* g, const char* key);
+/* cnn_train checkpoint: the model directory plus the
+ * momentum buffers, the epoch and the shuffling generator's state
+ * (rng.hpp:31-32); resuming reproduces straight-through training bitwise. */
+ck_status ck_trainer_save(ck_trainer* t, const char* dir, const uint64_t rng_state[4],
+                          int64_t epoch);
+ck_status ck_trainer_load(ck_trainer* t, const char* dir, uint64_t rng_state[4],
+                          int64_t* epoch);
+
 /* ---- synthetic data (host): the reference generator, xoshiro256** seeded
  * via splitmix64 (rng.hpp:9-36, rng.cpp:10-59) ---------------------------- */
 void* ck_rng_create(uint64_t seed);
@@ -351,6 +384,11 @@ void ck_rng_uniform(void* rng, float* out, int64_t n, float lo, float hi);
 void ck_rng_normal(void* rng, float* out, int64_t n, float scale);
 /* 1 + below(classes)   (rng.cpp:49) */
 void ck_rng_labels(void* rng, float* out, int64_t n, uint64_t classes);
+/* rng.cpp:51-59 permutation(n): Fisher-Yates with below(k + 1) */
+void ck_rng_permutation(void* rng, int64_t n, int64_t* out);
+/* rng.hpp:31-32 state() / set_state() */
+void ck_rng_get_state(const void* rng, uint64_t state[4]);
+void ck_rng_set_state(void* rng, const uint64_t state[4]);
 
 #ifdef __cplusplus
 }

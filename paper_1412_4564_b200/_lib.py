@@ -140,6 +140,20 @@ SIGNATURES = {
     "ck_rng_uniform": (None, [P, P, C.c_int64, C.c_float, C.c_float]),
     "ck_rng_normal": (None, [P, P, C.c_int64, C.c_float]),
     "ck_rng_labels": (None, [P, P, C.c_int64, C.c_uint64]),
+    "ck_rng_permutation": (None, [P, C.c_int64, P]),
+    "ck_rng_get_state": (None, [P, P]),
+    "ck_rng_set_state": (None, [P, P]),
+    "ck_io_last_error": (C.c_char_p, []),
+    "ck_blob_write": (S, [C.c_char_p, P, ck_shape]),
+    "ck_blob_read_shape": (S, [C.c_char_p, C.POINTER(ck_shape)]),
+    "ck_blob_read": (S, [C.c_char_p, P, ck_shape]),
+    "ck_idx_read": (S, [C.c_char_p, P, P]),
+    "ck_graph_save": (S, [P, C.c_char_p]),
+    "ck_graph_load": (S, [P, C.c_char_p, C.c_int, C.POINTER(P)]),
+    "ck_graph_set_meta": (S, [P, C.c_char_p, C.c_char_p]),
+    "ck_graph_get_meta": (C.c_char_p, [P, C.c_char_p]),
+    "ck_trainer_save": (S, [P, C.c_char_p, P, C.c_int64]),
+    "ck_trainer_load": (S, [P, C.c_char_p, P, P]),
 }
 
 
@@ -186,9 +200,21 @@ def exported_symbols():
     return list(SIGNATURES)
 
 
+class NumericError(CkError):
+    pass
+
+
+def raise_io(code):
+    """Status of a host file function (errors in ck_io_last_error)."""
+    if code == CK_OK:
+        return
+    raise DataError(code, lib().ck_io_last_error().decode(errors="replace"))
+
+
 def raise_for(code, handle):
     if code == CK_OK:
         return
     msg = lib().ck_last_error(handle).decode(errors="replace") if handle else "error"
-    cls = {CK_ERR_SHAPE: ShapeError, CK_ERR_DATA: DataError}.get(code, CkError)
+    cls = {CK_ERR_SHAPE: ShapeError, CK_ERR_DATA: DataError,
+           CK_ERR_NUMERIC: NumericError}.get(code, CkError)
     raise cls(code, msg)

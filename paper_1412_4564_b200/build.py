@@ -17,7 +17,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libck.so")
 SOURCES = ["kernels.cu", "conv_simt.cu", "conv_tc.cu", "capi.cu", "engine.cu", "host_rng.cu",
-           "blocks_ext.cu", "capi_ext.cu"]
+           "blocks_ext.cu", "capi_ext.cu", "io.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -43,7 +43,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     hdr_mtime = max(os.path.getmtime(h) for h in headers)
 
     def compile_one(src):
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
         srcp = os.path.join(CSRC, src)
         if (not force and os.path.exists(obj)
                 and os.path.getmtime(obj) > max(os.path.getmtime(srcp), hdr_mtime)):

@@ -197,6 +197,8 @@ void after_launch() { check_cuda(cudaPeekAtLastError(), "kernel launch"); }
 // the first offending class label.  Messages are loss.cpp's (:14-18, :101-106,
 // :152-154, :201-203, :193-195).
 void throw_label_flag(int flag, int label, int64_t classes) {
+  // SPEC.md:716, :766 exit code 3: a non-finite objective aborts training
+  if (flag & 64) throw Err(CK_ERR_NUMERIC, "non-finite loss (NaN or Inf): training aborted");
   if (flag & 1) throw Err(CK_ERR_DATA, "class label is not an integer");
   if (flag & 2)
     throw Err(CK_ERR_DATA, "class label " + std::to_string(label) + " out of range 1.." +

@@ -109,6 +109,8 @@ inline void count_tc_launch() {
 }
 
 void relu_forward(const float* x, float* y, int64_t n, cudaStream_t s);
+// flag[0] |= bit when any of v[0..n) is not finite (trainer NaN abort)
+void flag_nonfinite(const float* v, int64_t n, int* flag, int bit, cudaStream_t s);
 void relu_backward(const float* x, const float* dy, float* dx, int64_t n, int acc, cudaStream_t s);
 void axpy_inplace(float* y, const float* x, int64_t n, cudaStream_t s);  // y += x
 void sgd_step(float* w, float* v, const float* g, int64_t n, float lr, float mom, float wd,

@@ -26,9 +26,16 @@
 #include <string>
 #include <vector>
 
+#include <sys/stat.h>
+
+#include <cinttypes>
+#include <cmath>
+#include <fstream>
+
 #include "ck/ck.h"
 #include "ck_handle.hpp"
 #include "ck_internal.hpp"
+#include "ck_io.hpp"
 
 using ck::Err;
 
@@ -53,6 +60,26 @@ static Kind kind_from_name(const std::string& s) {
   if (s == "split") return Kind::split;
   // graph.cpp:33-40 layer_kind_from_name
   throw Err(CK_ERR_ARG, "unknown layer kind '" + s + "'");
+}
+
+static const char* kind_name(Kind k) {
+  switch (k) {
+    case Kind::conv: return "conv";
+    case Kind::convt: return "convt";
+    case Kind::pool: return "pool";
+    case Kind::relu: return "relu";
+    case Kind::lrn: return "lrn";
+    case Kind::bnorm: return "bnorm";
+    case Kind::loss: return "loss";
+    case Kind::sum: return "sum";
+    case Kind::sigmoid: return "sigmoid";
+    case Kind::softmax: return "softmax";
+    case Kind::spnorm: return "spnorm";
+    case Kind::bilinear: return "bilinear";
+    case Kind::pdist: return "pdist";
+    case Kind::split: return "split";
+  }
+  return "?";
 }
 
 struct Var {
@@ -123,6 +150,8 @@ struct ck_graph {
   float* one_dev = nullptr;  // the objective seed 1.0f, device-resident (graph-capturable)
   bool has_loss = false;
   bool lrn_grid = true;  // option "lrn_grid": LRN backward writes the conv's dy grid
+  std::vector<std::pair<std::string, std::string>> meta;  // manifest metadata
+  std::vector<int> decl;  // input / param vars in declaration order (manifest order)
   int64_t last_launches = 0;
   bool profiling = false;
   // per layer: fwd begin/end, bwd begin/end
@@ -1027,9 +1056,13 @@ static ck_status add_var(ck_graph* g, const char* name, ck_shape shape, int role
   if (g->by_name.count(name)) throw Err(CK_ERR_ARG, std::string("variable '") + name + "' declared twice");
   if (shape.h < 1 || shape.w < 1 || shape.c < 1 || shape.n < 1)
     throw Err(CK_ERR_SHAPE, "invalid tensor shape " + shape_str(shape));
+  for (const char* c = name; *c; ++c)
+    if (*c == ' ' || *c == '\t' || *c == '\n' || *c == ',' || *c == '=')
+      throw Err(CK_ERR_ARG, std::string("variable name '") + name + "' contains a separator");
   int k = g->intern(name, role);
   g->vars[k].shape = shape;
   g->vars[k].has_shape = true;
+  g->decl.push_back(k);
   CKG_END(g)
 }
 
@@ -1260,7 +1293,10 @@ static void trainer_body(ck_trainer* t, cudaStream_t s) {
   ck_graph* g = t->g;
   const bool timed = g->profiling;  // profiling steps are always eager
   if (timed) check_cuda(cudaEventRecord(t->t_begin, s), "event");
+  if (!g->has_loss) reset_label_flag(g->h, s);  // (run_forward resets it otherwise)
   run_forward(g, s);
+  flag_nonfinite(g->vars[t->objective].value, elems(g->vars[t->objective].shape), g->h->flag, 64,
+                 s);
   if (timed) check_cuda(cudaEventRecord(t->t_fwd, s), "event");
   run_backward(g, t->objective, s, t);
   if (timed) check_cuda(cudaEventRecord(t->t_bwd, s), "event");
@@ -1282,9 +1318,8 @@ static void trainer_body(ck_trainer* t, cudaStream_t s) {
     if (timed) check_cuda(cudaEventRecord(t->t_comm, s), "event");
   }
   t->timed = timed;
-  if (g->has_loss)
-    check_cuda(cudaMemcpyAsync(t->flag_host, g->h->flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, s),
-               "flag");
+  check_cuda(cudaMemcpyAsync(t->flag_host, g->h->flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, s),
+             "flag");
 }
 
 // The label flag of the last step, once its copy is known complete (or
@@ -1384,10 +1419,8 @@ ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
     ++t->eager_steps;
     t->eager_gen = workspace_generation();
   }
-  if (g->has_loss) {
-    check_cuda(cudaEventRecord(t->flag_ev, s), "event");
-    t->flag_pending = true;
-  }
+  check_cuda(cudaEventRecord(t->flag_ev, s), "event");
+  t->flag_pending = true;
   if (loss_host) {
     check_cuda(cudaMemcpyAsync(loss_host, t->loss_dev, sizeof(float), cudaMemcpyDeviceToHost, s),
                "copy");
@@ -1418,5 +1451,277 @@ ck_status ck_trainer_last_timing(ck_trainer* t, float* fwd_ms, float* bwd_ms, fl
 }
 
 int64_t ck_trainer_allreduce_count(const ck_trainer* t) { return t ? t->allreduces : 0; }
+
+}  // extern "C"
+
+namespace ck {
+
+// ---- model files: manifest + blobs, checkpoints ----
+//
+// A model directory holds `manifest.txt` -- line-oriented key/value text:
+//   ck-manifest 1
+//   var <name> input|param <H> <W> <C> <N>       (declaration order)
+//   layer <kind> <name> in=<a,b,..> out=<c,..> p=<v1,v2,..>
+//   blob <param> <file>                           (one per parameter)
+//   meta <key> <value...>                         (e.g. normalization data)
+// -- and one raw tensor blob (blob.cpp:29-79) per parameter.  Hyper-
+// parameters are printed with %.17g so a save -> load -> save round trip
+// is byte-identical.
+
+static std::string join_names(const ck_graph* g, const std::vector<int>& ids) {
+  std::string s;
+  for (size_t k = 0; k < ids.size(); ++k) s += (k ? "," : "") + g->vars[ids[k]].name;
+  return s;
+}
+
+static std::string path_join(const std::string& dir, const std::string& f) {
+  return dir.empty() || dir.back() == '/' ? dir + f : dir + "/" + f;
+}
+
+static void make_dir(const std::string& dir) {
+  if (mkdir(dir.c_str(), 0755) != 0 && errno != EEXIST)
+    throw IoError("cannot create directory " + dir);
+}
+
+static void save_params(ck_graph* g, const std::string& dir, std::string* manifest) {
+  for (int i : g->decl) {
+    const Var& v = g->vars[i];
+    if (v.role != 1) continue;
+    std::vector<float> host((size_t)elems(v.shape));
+    check_cuda(cudaMemcpy(host.data(), v.value, sizeof(float) * host.size(), cudaMemcpyDeviceToHost),
+               "copy");
+    const std::string file = v.name + ".blob";
+    blob_write(path_join(dir, file), host.data(), v.shape);
+    if (manifest) *manifest += "blob " + v.name + " " + file + "\n";
+  }
+}
+
+static std::string manifest_text(const ck_graph* g) {
+  std::string m = "ck-manifest 1\n";
+  char buf[64];
+  for (int i : g->decl) {
+    const Var& v = g->vars[i];
+    snprintf(buf, sizeof(buf), " %" PRId64 " %" PRId64 " %" PRId64 " %" PRId64 "\n", v.shape.h,
+             v.shape.w, v.shape.c, v.shape.n);
+    m += "var " + v.name + (v.role == 0 ? " input" : " param") + buf;
+  }
+  for (const Layer& l : g->layers) {
+    m += std::string("layer ") + kind_name(l.kind) + " " + l.name + " in=" + join_names(g, l.in) +
+         " out=" + join_names(g, l.out) + " p=";
+    for (size_t k = 0; k < l.p.size(); ++k) {
+      snprintf(buf, sizeof(buf), "%s%.17g", k ? "," : "", l.p[k]);
+      m += buf;
+    }
+    m += "\n";
+  }
+  return m;
+}
+
+static std::vector<std::string> split_ws(const std::string& line) {
+  std::vector<std::string> out;
+  std::stringstream ss(line);
+  std::string t;
+  while (ss >> t) out.push_back(t);
+  return out;
+}
+
+}  // namespace ck
+
+extern "C" {
+
+ck_status ck_graph_set_meta(ck_graph* g, const char* key, const char* value) {
+  CKG_BEGIN(g)
+  if (!key || !*key || !value) throw Err(CK_ERR_ARG, "null metadata");
+  for (const char* c = key; *c; ++c)
+    if (*c == ' ' || *c == '\n') throw Err(CK_ERR_ARG, "metadata key contains a separator");
+  if (std::strchr(value, '\n')) throw Err(CK_ERR_ARG, "metadata value contains a newline");
+  for (auto& kv : g->meta)
+    if (kv.first == key) {
+      kv.second = value;
+      return CK_OK;
+    }
+  g->meta.push_back({key, value});
+  CKG_END(g)
+}
+
+const char* ck_graph_get_meta(const ck_graph* g, const char* key) {
+  if (!g || !key) return nullptr;
+  for (auto& kv : g->meta)
+    if (kv.first == key) return kv.second.c_str();
+  return nullptr;
+}
+
+ck_status ck_graph_save(ck_graph* g, const char* dir) {
+  CKG_BEGIN(g)
+  if (!g->finalized) throw Err(CK_ERR_ARG, "save needs a finalized graph");
+  if (!dir) throw Err(CK_ERR_ARG, "null path");
+  try {
+    make_dir(dir);
+    std::string m = manifest_text(g);
+    check_cuda(cudaDeviceSynchronize(), "synchronize");
+    save_params(g, dir, &m);
+    for (auto& kv : g->meta) m += "meta " + kv.first + " " + kv.second + "\n";
+    std::ofstream f(path_join(dir, "manifest.txt"), std::ios::binary);
+    f << m;
+    if (!f) throw IoError(std::string("cannot write ") + path_join(dir, "manifest.txt"));
+  } catch (const IoError& e) {
+    throw Err(CK_ERR_DATA, e.what());
+  }
+  CKG_END(g)
+}
+
+// Builds, finalizes and fills a graph from a model directory.
+ck_status ck_graph_load(ck_handle* h, const char* dir, ck_math math, ck_graph** out) {
+  if (!h || !out) return CK_ERR_ARG;
+  *out = nullptr;
+  ck_graph* g = nullptr;
+  if (ck_graph_create(h, &g) != CK_OK) return CK_ERR_ARG;
+  std::unique_ptr<ck_graph, void (*)(ck_graph*)> guard(g, ck_graph_destroy);
+  const ck_status st = [&]() -> ck_status {
+    CKG_BEGIN(g)
+    if (!dir) throw Err(CK_ERR_ARG, "null path");
+    const std::string mpath = path_join(dir, "manifest.txt");
+    std::ifstream f(mpath);
+    if (!f) throw Err(CK_ERR_DATA, "cannot open " + mpath);
+    std::string line;
+    if (!std::getline(f, line)) throw Err(CK_ERR_DATA, "empty manifest " + mpath);
+    const auto head = split_ws(line);
+    if (head.size() != 2 || head[0] != "ck-manifest")
+      throw Err(CK_ERR_DATA, "not a ck model manifest: " + mpath);
+    if (head[1] != "1") throw Err(CK_ERR_DATA, "manifest version " + head[1] + " not supported");
+    std::vector<std::pair<std::string, std::string>> blobs;
+    int lineno = 1;
+    while (std::getline(f, line)) {
+      ++lineno;
+      if (line.empty() || line[0] == '#') continue;
+      const auto t = split_ws(line);
+      const std::string where = mpath + ":" + std::to_string(lineno);
+      if (t[0] == "var" && t.size() == 7) {
+        ck_shape sh{std::stoll(t[3]), std::stoll(t[4]), std::stoll(t[5]), std::stoll(t[6])};
+        ck_status r = t[2] == "input" ? ck_graph_add_input(g, t[1].c_str(), sh)
+                      : t[2] == "param" ? ck_graph_add_param(g, t[1].c_str(), sh)
+                                        : CK_ERR_DATA;
+        if (r != CK_OK) throw Err(r, where + ": " + (g->h->err.empty() ? "bad role" : g->h->err));
+      } else if (t[0] == "layer" && t.size() == 6 && t[3].rfind("in=", 0) == 0 &&
+                 t[4].rfind("out=", 0) == 0 && t[5].rfind("p=", 0) == 0) {
+        std::vector<double> p;
+        for (auto& v : split_csv(t[5].c_str() + 2)) p.push_back(std::stod(v));
+        ck_status r = ck_graph_add_layer(g, t[1].c_str(), t[2].c_str(), t[3].c_str() + 3,
+                                         t[4].c_str() + 4, p.data(), (int)p.size());
+        if (r != CK_OK) throw Err(r, where + ": " + g->h->err);
+      } else if (t[0] == "blob" && t.size() == 3) {
+        blobs.push_back({t[1], t[2]});
+      } else if (t[0] == "meta" && t.size() >= 2) {
+        const size_t at = line.find(t[1]) + t[1].size();
+        g->meta.push_back({t[1], at < line.size() ? line.substr(at + 1) : std::string()});
+      } else {
+        throw Err(CK_ERR_DATA, where + ": malformed line '" + line + "'");
+      }
+    }
+    if (ck_graph_finalize(g, math) != CK_OK) throw Err(CK_ERR_DATA, g->h->err);
+    for (int i : g->decl) {
+      const Var& v = g->vars[i];
+      if (v.role != 1) continue;
+      bool found = false;
+      for (auto& b : blobs) found |= b.first == v.name;
+      if (!found) throw Err(CK_ERR_DATA, "manifest lists no blob for parameter '" + v.name + "'");
+    }
+    for (auto& b : blobs) {
+      Var& v = g->vars[g->var(b.first)];
+      if (v.role != 1) throw Err(CK_ERR_DATA, "blob for non-parameter '" + b.first + "'");
+      const std::string bp = path_join(dir, b.second);
+      FILE* probe = fopen(bp.c_str(), "rb");
+      if (!probe) throw Err(CK_ERR_DATA, "manifest references missing blob '" + b.second + "'");
+      fclose(probe);
+      std::vector<float> host((size_t)elems(v.shape));
+      try {
+        blob_read(bp, host.data(), &v.shape);
+      } catch (const IoError& e) {
+        throw Err(CK_ERR_DATA, e.what());
+      }
+      check_cuda(cudaMemcpy(v.value, host.data(), sizeof(float) * host.size(),
+                            cudaMemcpyHostToDevice), "copy");
+    }
+    CKG_END(g)
+  }();
+  if (st != CK_OK) {
+    h->err = g->h->err;
+    return st;
+  }
+  *out = guard.release();
+  return CK_OK;
+}
+
+// cnn_train checkpoint: the model directory plus every
+// momentum buffer (<param>.momentum.blob) and trainer.txt with the step
+// hyper-parameters, the epoch and the shuffling generator's state
+// (rng.hpp:31-32), so resuming reproduces straight-through training bitwise.
+ck_status ck_trainer_save(ck_trainer* t, const char* dir, const uint64_t rng_state[4],
+                          int64_t epoch) {
+  if (!t) return CK_ERR_ARG;
+  ck_graph* g = t->g;
+  ck_status st = ck_graph_save(g, dir);
+  if (st != CK_OK) return st;
+  CKG_BEGIN(g)
+  try {
+    for (size_t k = 0; k < t->params.size(); ++k) {
+      const Var& v = g->vars[t->params[k]];
+      std::vector<float> host((size_t)elems(v.shape));
+      check_cuda(cudaMemcpy(host.data(), t->mom[k], sizeof(float) * host.size(),
+                            cudaMemcpyDeviceToHost), "copy");
+      blob_write(path_join(dir, v.name + ".momentum.blob"), host.data(), v.shape);
+    }
+    std::ofstream f(path_join(dir, "trainer.txt"), std::ios::binary);
+    char buf[256];
+    snprintf(buf, sizeof(buf),
+             "ck-trainer 1\nlr %.9g\nmomentum %.9g\nweight_decay %.9g\nepoch %" PRId64
+             "\nrng %016" PRIx64 " %016" PRIx64 " %016" PRIx64 " %016" PRIx64 "\n",
+             (double)t->lr, (double)t->momentum, (double)t->wd, epoch,
+             rng_state ? rng_state[0] : 0, rng_state ? rng_state[1] : 0,
+             rng_state ? rng_state[2] : 0, rng_state ? rng_state[3] : 0);
+    f << buf;
+    if (!f) throw IoError("cannot write " + path_join(dir, "trainer.txt"));
+  } catch (const IoError& e) {
+    throw Err(CK_ERR_DATA, e.what());
+  }
+  CKG_END(g)
+}
+
+// Restores parameters, momentum, epoch and generator state into a trainer
+// over the same graph structure.
+ck_status ck_trainer_load(ck_trainer* t, const char* dir, uint64_t rng_state[4],
+                          int64_t* epoch) {
+  if (!t) return CK_ERR_ARG;
+  ck_graph* g = t->g;
+  CKG_BEGIN(g)
+  if (!dir) throw Err(CK_ERR_ARG, "null path");
+  check_cuda(cudaDeviceSynchronize(), "synchronize");
+  try {
+    for (size_t k = 0; k < t->params.size(); ++k) {
+      Var& v = g->vars[t->params[k]];
+      std::vector<float> host((size_t)elems(v.shape));
+      blob_read(path_join(dir, v.name + ".blob"), host.data(), &v.shape);
+      check_cuda(cudaMemcpy(v.value, host.data(), sizeof(float) * host.size(),
+                            cudaMemcpyHostToDevice), "copy");
+      blob_read(path_join(dir, v.name + ".momentum.blob"), host.data(), &v.shape);
+      check_cuda(cudaMemcpy(t->mom[k], host.data(), sizeof(float) * host.size(),
+                            cudaMemcpyHostToDevice), "copy");
+    }
+    std::ifstream f(path_join(dir, "trainer.txt"));
+    if (!f) throw IoError("cannot open " + path_join(dir, "trainer.txt"));
+    std::string line;
+    std::getline(f, line);
+    if (line != "ck-trainer 1") throw IoError(std::string("not a ck trainer checkpoint: ") + dir);
+    while (std::getline(f, line)) {
+      const auto tk = split_ws(line);
+      if (tk.size() == 2 && tk[0] == "epoch" && epoch) *epoch = std::stoll(tk[1]);
+      if (tk.size() == 5 && tk[0] == "rng" && rng_state)
+        for (int k = 0; k < 4; ++k) rng_state[k] = std::stoull(tk[1 + k], nullptr, 16);
+    }
+  } catch (const IoError& e) {
+    throw Err(CK_ERR_DATA, e.what());
+  }
+  CKG_END(g)
+}
 
 }  // extern "C"

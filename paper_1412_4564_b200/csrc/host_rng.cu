@@ -59,4 +59,22 @@ void ck_rng_labels(void* r, float* out, int64_t n, uint64_t classes) {
   for (int64_t k = 0; k < n; ++k)
     out[k] = (float)(1 + (classes ? next(static_cast<Rng*>(r)) % classes : 0));
 }
+// rng.cpp:51-59 Xoshiro256::permutation: Fisher-Yates with below(k + 1)
+void ck_rng_permutation(void* r, int64_t n, int64_t* out) {
+  Rng* g = static_cast<Rng*>(r);
+  for (int64_t k = 0; k < n; ++k) out[k] = k;
+  for (int64_t k = n - 1; k > 0; --k) {
+    const uint64_t j = next(g) % (uint64_t)(k + 1);  // below(k + 1), rng.cpp:49
+    const int64_t t = out[k];
+    out[k] = out[j];
+    out[j] = t;
+  }
+}
+// rng.hpp:31-32 state() / set_state(): the generator state a checkpoint keeps
+void ck_rng_get_state(const void* r, uint64_t state[4]) {
+  for (int k = 0; k < 4; ++k) state[k] = static_cast<const Rng*>(r)->s[k];
+}
+void ck_rng_set_state(void* r, const uint64_t state[4]) {
+  for (int k = 0; k < 4; ++k) static_cast<Rng*>(r)->s[k] = state[k];
+}
 }

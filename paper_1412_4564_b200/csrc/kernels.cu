@@ -1295,6 +1295,14 @@ __global__ void metrics_k(const float* __restrict__ x, const float* __restrict__
 
 }  // namespace
 
+// SPEC.md:716 "NaN loss aborts with diagnostic": sets `bit` in the handle's
+// flag when any of the n values is NaN or infinite.
+__global__ void flag_nonfinite_k(const float* __restrict__ v, int64_t n, int* flag, int bit) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(v[i])) atomicOr(flag, bit);
+}
+
 // ------------------------------------------------------------ launchers ---
 
 void relu_forward(const float* x, float* y, int64_t n, cudaStream_t s) {
@@ -1694,6 +1702,11 @@ void loss_metrics(const float* x, const float* labels, const float* weights, int
                                                          site_buf + sites, flag, HW, C, N);
   sum_sites_k<<<1, 1024, 0, s>>>(site_buf, sites, top1);
   sum_sites_k<<<1, 1024, 0, s>>>(site_buf + sites, sites, topk);
+}
+
+void flag_nonfinite(const float* v, int64_t n, int* flag, int bit, cudaStream_t s) {
+  count_launch();
+  flag_nonfinite_k<<<blocks_for(n, 256), 256, 0, s>>>(v, n, flag, bit);
 }
 
 }  // namespace ck

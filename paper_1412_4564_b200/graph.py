@@ -18,6 +18,14 @@ from ._lib import ck_shape, ck_tensor, lib, raise_for
 from .blocks import MATH, handle
 
 
+def _u64x4(values=None):
+    arr = (C.c_uint64 * 4)()
+    if values is not None:
+        for k, v in enumerate(values):
+            arr[k] = int(v)
+    return arr
+
+
 class Graph:
     def __init__(self, math: str = "tf32", device: int | None = None):
         self.hd = handle(device)
@@ -28,6 +36,7 @@ class Graph:
         self.shapes = {}
         self.params = []
         self.inputs = []
+        self.layers = []
 
     def __del__(self):
         if getattr(self, "g", None) and _lib._lib is not None:
@@ -49,6 +58,7 @@ class Graph:
         self.params.append(name)
 
     def add_layer(self, kind, name, inputs, outputs, params=()):
+        self.layers.append((kind, name, list(inputs), list(outputs), list(params)))
         p = (C.c_double * max(1, len(params)))(*[float(v) for v in params])
         self._check(lib().ck_graph_add_layer(self.g, kind.encode(), name.encode(),
                                              ",".join(inputs).encode(), ",".join(outputs).encode(),
@@ -103,6 +113,40 @@ class Graph:
     @property
     def last_launches(self) -> int:
         return lib().ck_graph_last_launches(self.g)
+
+    # -- model files (manifest + blobs, ck_graph_save / ck_graph_load) --
+    def save(self, path):
+        """Write the model directory: manifest.txt + one blob per parameter."""
+        self._check(lib().ck_graph_save(self.g, str(path).encode()))
+
+    @classmethod
+    def load(cls, path, math="tf32", device=None):
+        """Build, finalize and fill a graph from a model directory."""
+        self = cls.__new__(cls)
+        self.hd = handle(device)
+        self.math = math
+        g = C.c_void_p()
+        raise_for(lib().ck_graph_load(self.hd.h, str(path).encode(), MATH[math], C.byref(g)),
+                  self.hd.h)
+        self.g = g
+        self.shapes, self.params, self.inputs, self.layers = {}, [], [], []
+        for ln in open(f"{path}/manifest.txt"):
+            t = ln.split()
+            if t and t[0] == "var":
+                shape = tuple(int(v) for v in t[3:7])
+                self.shapes[t[1]] = shape
+                (self.inputs if t[2] == "input" else self.params).append(t[1])
+            elif t and t[0] == "layer":
+                p = [float(v) for v in t[5][2:].split(",") if v]
+                self.layers.append((t[1], t[2], t[3][3:].split(","), t[4][4:].split(","), p))
+        return self
+
+    def set_meta(self, key, value):
+        self._check(lib().ck_graph_set_meta(self.g, key.encode(), str(value).encode()))
+
+    def get_meta(self, key):
+        v = lib().ck_graph_get_meta(self.g, key.encode())
+        return None if v is None else v.decode()
 
     def set_option(self, name: str, value):
         """Engine option (ck_graph_set_option), e.g. ``lrn_grid``."""
@@ -242,6 +286,77 @@ class Trainer:
     def allreduces(self) -> int:
         return lib().ck_trainer_allreduce_count(self.t)
 
+    # -- checkpoints (ck_trainer_save / ck_trainer_load) --
+    def save(self, path, rng_state=None, epoch=0):
+        self.graph._check(lib().ck_trainer_save(self.t, str(path).encode(), _u64x4(rng_state),
+                                                int(epoch)))
+
+    def load(self, path):
+        """Restore parameters + momentum; returns (rng_state, epoch)."""
+        st, ep = _u64x4(), C.c_int64()
+        self.graph._check(lib().ck_trainer_load(self.t, str(path).encode(), st, C.byref(ep)))
+        return [int(v) for v in st], ep.value
+
+    def fit(self, images, labels, epochs, seed=0, data="data", label="label", checkpoint=None,
+            start_epoch=0, rng_state=None, log=None, top_k=5):
+        """cnn_train: epochs x ceil(N / batch) SGD steps over
+        batches drawn by a per-epoch permutation of the reference generator
+        (rng.cpp:51-59, seeded with `seed`); per-epoch records (loss, top-1,
+        top-5, sec, images/sec); a checkpoint (parameters, momentum, epoch,
+        generator state) after every epoch when `checkpoint` is a directory;
+        a non-finite loss aborts with NumericError.  The last
+        batch of an epoch is padded with label-0 (ignored, loss.cpp:100)
+        samples: exact for networks without batch norm.  Resume with
+        (rng_state, epoch) from Trainer.load."""
+        import time
+
+        from .nets import Rng
+        g = self.graph
+        xs, ls = g.shapes[data], g.shapes[label]
+        B = xs[3]
+        per_x, per_l = xs[0] * xs[1] * xs[2], ls[0] * ls[1] * ls[2]
+        images = np.ascontiguousarray(images, np.float32).reshape(-1, per_x)
+        labels = np.ascontiguousarray(labels, np.float32).reshape(-1, per_l)
+        N = images.shape[0]
+        loss_layer = next(l for l in g.layers if l[0] == "loss")
+        pred = loss_layer[2][0]
+        from . import blocks as _B
+        rng = Rng(seed)
+        if rng_state is not None:
+            lib().ck_rng_set_state(rng.h, _u64x4(rng_state))
+        records = []
+        xb = np.empty((B, per_x), np.float32)
+        lb = np.empty((B, per_l), np.float32)
+        for epoch in range(start_epoch, epochs):
+            t0 = time.perf_counter()
+            perm = np.empty(N, np.int64)
+            lib().ck_rng_permutation(rng.h, N, perm.ctypes.data)
+            tot_loss = tot1 = totk = 0.0
+            for b0 in range(0, N, B):
+                idx = perm[b0:b0 + B]
+                xb[: len(idx)] = images[idx]
+                lb[: len(idx)] = labels[idx]
+                xb[len(idx):] = 0.0
+                lb[len(idx):] = 0.0  # ignored samples
+                g.set(data, xb)
+                g.set(label, lb)
+                tot_loss += self.step()
+                m = _B.loss_metrics(_as_torch(g, pred), _as_torch(g, label), None, top_k)
+                m = m.cpu().numpy()
+                tot1 += float(m[0])
+                totk += float(m[1])
+            sec = time.perf_counter() - t0
+            rec = {"epoch": epoch + 1, "split": "train", "loss": tot_loss / N, "top1": tot1 / N,
+                   "top5": totk / N, "sec": sec, "images_per_sec": N / sec}
+            records.append(rec)
+            if log:
+                log(rec)
+            if checkpoint:
+                st = _u64x4()
+                lib().ck_rng_get_state(rng.h, st)
+                self.save(checkpoint, [int(v) for v in st], epoch + 1)
+        return records
+
     def set_graph(self, on: bool):
         """Replay each step as one CUDA graph (ck_trainer_set_graph)."""
         self.graph._check(lib().ck_trainer_set_graph(self.t, int(on)))
@@ -254,3 +369,13 @@ class Trainer:
             return v.value
         self.graph._check(lib().ck_trainer_step(self.t, None, s))
         return None
+
+
+def _as_torch(g: Graph, name):
+    """A device copy (N, C, W, H) of a graph variable's value, in stream order."""
+    t = g.view(name)
+    s = t.shape
+    n = s.h * s.w * s.c * s.n
+    u = torch.empty(n, device="cuda")
+    g._check(lib().ck_memcpy(g.hd.h, u.data_ptr(), t.data, 4 * n, g._stream()))
+    return u.reshape(s.n, s.c, s.w, s.h)
