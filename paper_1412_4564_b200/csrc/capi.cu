@@ -644,8 +644,10 @@ ck_status ck_bnorm_forward(ck_handle* h, const ck_tensor* x, const ck_tensor* w,
   if (!buf) throw Err(CK_ERR_CUDA, "workspace allocation failed");
   double* stats = buf + (size_t)4 * C * splits;
   bnorm_stats(x->data, nullptr, buf, stats, HW, C, N, splits, st);
+  // engine (bnorm -> relu): relu(y) written by the same pass
   bnorm_apply(x->data, w->data, b->data, stats, nullptr, y->data,
-              moments ? moments->data : nullptr, epsilon, HW, C, N, st);
+              moments ? moments->data : nullptr, epsilon, HW, C, N, st, h->fuse_relu);
+  if (h->fuse_relu) h->fuse_relu_done = true;
   after_launch();
   CK_API_END(h)
 }
@@ -685,10 +687,14 @@ ck_status ck_bnorm_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* w
   double* buf = (double*)h->ws.get(sizeof(double) * 4 * (size_t)C * (splits + 1), st);
   if (!buf) throw Err(CK_ERR_CUDA, "workspace allocation failed");
   double* stats = buf + (size_t)4 * C * splits;
-  bnorm_stats(x->data, dy->data, buf, stats, HW, C, N, splits, st);
-  bnorm_backward_apply(x->data, dy->data, w->data, stats, epsilon, dx ? dx->data : nullptr,
+  // engine (bnorm -> relu, relu backward deferred): the derivative reaching
+  // y is fuse_relu_x (= y) > 0 ? fuse_relu_dy : 0, formed inside both passes
+  const float* dyp = h->fuse_relu_x ? h->fuse_relu_dy : dy->data;
+  const float* gate = h->fuse_relu_x;
+  bnorm_stats(x->data, dyp, buf, stats, HW, C, N, splits, st, gate);
+  bnorm_backward_apply(x->data, dyp, w->data, stats, epsilon, dx ? dx->data : nullptr,
                        dw ? dw->data : nullptr, db ? db->data : nullptr, HW, C, N, accumulate,
-                       st);
+                       st, gate);
   after_launch();
   CK_API_END(h)
 }

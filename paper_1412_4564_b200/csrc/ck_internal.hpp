@@ -138,14 +138,17 @@ int lrn_grid_rows(int H, int W, int N);
 // Per-channel sums in double: out[c] = {sum x, sum x^2, sum dy, sum dy*x}
 // (dy may be null).  partial: workspace of splits*C*4 doubles.
 void bnorm_stats(const float* x, const float* dy, double* partial, double* out, int HW, int C,
-                 int N, int splits, cudaStream_t s);
+                 int N, int splits, cudaStream_t s, const float* gate = nullptr);
 int bnorm_splits(int HW, int C, int N);
+// y2 != null: also relu(y) (fused bnorm -> relu)
 void bnorm_apply(const float* x, const float* w, const float* b, const double* stats,
                  const float* fixed_moments, float* y, float* moments_out, double eps, int HW,
-                 int C, int N, cudaStream_t s);
+                 int C, int N, cudaStream_t s, float* y2 = nullptr);
+// gate != null (fused bnorm -> relu backward): the derivative reaching the
+// bnorm output is gate > 0 ? dy : 0 (gate = bnorm output, dy = relu output's)
 void bnorm_backward_apply(const float* x, const float* dy, const float* w, const double* stats,
                           double eps, float* dx, float* dw, float* db, int HW, int C, int N,
-                          int acc, cudaStream_t s);
+                          int acc, cudaStream_t s, const float* gate = nullptr);
 
 // softmaxlog: per-site loss into site_loss, then a fixed-order sum into loss.
 void softmaxlog_forward(const float* x, const float* labels, const float* weights,

@@ -2530,7 +2530,8 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
     s2d_fprop(h, x, f, bias, y, d, z, relu, s);
     return true;
   }
-  if (d.Cg < 16 || Kg < 16) return false;
+  // (any channel count: groups are padded to 32 channels; the MMAs of a tap's
+  // all-zero K steps are skipped (last_k), the epilogue stores n < n_valid)
   const int Cgp = rup(d.Cg, 32), Cp = Cgp * d.groups;
   const int taps = d.fh * d.fw;
   if (d.pt > 127 || d.pl > 127 || d.fh > 128 || d.fw > 128) return false;
@@ -2651,7 +2652,8 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     s2d_dgrad(h, dy, f, dx, d, z, acc, s);
     return true;
   }
-  if (d.Cg < 16 || Kg < 16) return false;
+  // (any channel count: groups are padded to 32 channels; the MMAs of a tap's
+  // all-zero K steps are skipped (last_k), the epilogue stores n < n_valid)
   if (d.pt > d.fh - 1 || d.pb > d.fh - 1 || d.pl > d.fw - 1 || d.pr > d.fw - 1) return false;
   const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
   const int taps = d.fh * d.fw;
@@ -2725,7 +2727,8 @@ bool conv_tc_grid_plan(const ConvDims& d, GridPlan* gp) {
   if (!load_driver() || is_fc(d) || halo_enabled() || shift_enabled()) return false;
   const int Kg = d.Kg();
   if (d.sh == 1 && d.sw == 1) {
-    if (d.Cg < 16 || Kg < 16) return false;
+    // (any channel count: channels are padded to 32 per group, last_k skips the
+    // all-zero K steps of a tap's padded chunk)
     if (d.pt > d.fh - 1 || d.pb > d.fh - 1 || d.pl > d.fw - 1 || d.pr > d.fw - 1) return false;
     if (d.pt > 127 || d.pl > 127 || d.fh > 128 || d.fw > 128) return false;
     grid_dims(d, gp->Hg, gp->Wg);
@@ -2753,7 +2756,8 @@ bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, i
   if (!load_driver() || is_fc(d)) return false;
   const int Kg = d.Kg();
   if (d.sh == 1 && d.sw == 1) {
-    if (d.Cg < 16 || Kg < 16) return false;
+    // (any channel count: channels are padded to 32 per group, last_k skips the
+    // all-zero K steps of a tap's padded chunk)
     int Hg, Wg;
     grid_dims(d, Hg, Wg);
     dy_grid(h, dy, d, Kg, rup(Kg, 32), d.groups, Hg, Wg, s, db, acc, relu_x, relu_dy, skip_gout);
@@ -2798,7 +2802,8 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
     s2d_wgrad(h, x, dy, df, d, z, acc, s);
     return true;
   }
-  if (d.Cg < 16 || Kg < 16) return false;
+  // (any channel count: groups are padded to 32 channels; the MMAs of a tap's
+  // all-zero K steps are skipped (last_k), the epilogue stores n < n_valid)
   if (d.pt > 127 || d.pl > 127 || d.fh > 128 || d.fw > 128) return false;
   const int Cgp = rup(d.Cg, 32), Cp = Cgp * d.groups;
   const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;

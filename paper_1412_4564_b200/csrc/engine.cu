@@ -449,7 +449,9 @@ static void finalize(ck_graph* g) {
     const Var& v = g->vars[r.in[0]];
     if (v.producer < 0 || v.consumers.size() != 1) continue;
     Layer& c = g->layers[v.producer];
-    if (c.kind != Kind::conv || c.relu_out >= 0) continue;
+    // conv -> relu (fused epilogue) and bnorm -> relu (fused apply / gated
+    // backward): the producer writes relu(y) too; the relu layer idles
+    if ((c.kind != Kind::conv && c.kind != Kind::bnorm) || c.relu_out >= 0) continue;
     c.relu_out = r.out[0];
     r.fused_by = v.producer;
     r.fused_bwd = true;
@@ -508,7 +510,14 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
     case Kind::bnorm: {
       ck_tensor x = V(0), w = V(1), b = V(2);
       ck_tensor m{l.aux, ck_shape{x.shape.c, 2, 1, 1}};
+      h->fuse_relu = l.relu_out >= 0 ? g->vars[l.relu_out].value : nullptr;
+      h->fuse_relu_done = false;
       st = ck_bnorm_forward(h, &x, &w, &b, l.p[0], &y, &m, s);
+      h->fuse_relu = nullptr;
+      if (l.relu_out >= 0) {
+        Layer& r = g->layers[g->vars[l.relu_out].producer];
+        r.fused_done = st == CK_OK && h->fuse_relu_done;
+      }
       break;
     }
     case Kind::loss: {
@@ -691,7 +700,8 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
       if (!acc(0) && g->math == CK_MATH_TF32 && xv.producer >= 0 && xv.consumers.size() == 1 &&
           g->lrn_grid) {
         Layer& r = g->layers[xv.producer];
-        if (r.kind == Kind::relu && r.fused_by >= 0 && r.fused_bwd) {
+        if (r.kind == Kind::relu && r.fused_by >= 0 && r.fused_bwd &&
+            g->layers[r.fused_by].kind == Kind::conv) {
           Layer& c = g->layers[r.fused_by];
           const Var& cx = g->vars[c.in[0]];
           const Var& cf = g->vars[c.in[1]];
@@ -728,6 +738,25 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
     case Kind::bnorm: {
       ck_tensor x = V(0), w = V(1), b = V(2), dx = D(0), dw = D(1), db = D(2);
       int a0 = acc(0), a1 = acc(1), a2 = acc(2);
+      // fused bnorm -> relu: the relu backward was deferred; this layer reads
+      // the relu output's derivative gated by its own output (> 0), and its
+      // output's derivative stays unmaterialized (computed on request)
+      const bool fused = l.relu_out >= 0 && g->layers[g->vars[l.relu_out].producer].bwd_deferred;
+      if (fused) {
+        h->fuse_relu_x = g->vars[l.out[0]].value;
+        h->fuse_relu_dy = g->vars[l.relu_out].deriv;
+      }
+      struct ResetB {
+        ck_handle* h;
+        ~ResetB() {
+          h->fuse_relu_x = nullptr;
+          h->fuse_relu_dy = nullptr;
+        }
+      } resetb{h};
+      if (fused) {
+        g->vars[l.out[0]].lazy_gate = l.out[0];
+        g->vars[l.out[0]].lazy_src = l.relu_out;
+      }
       if (a0 == a1 && a1 == a2) {
         st = ck_bnorm_backward(h, &x, &w, &b, l.p[0], &dy, &dx, &dw, &db, a0, s);
       } else {

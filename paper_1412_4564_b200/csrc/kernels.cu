@@ -927,26 +927,71 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-template <bool kGrad>
-__global__ void bnorm_stats_k(const float* __restrict__ x, const float* __restrict__ dy,
-                              double* partial, int HW, int C, int N, int splits) {
+// Element e of a channel's reduction: x, and (backward) the derivative that
+// reaches the bnorm output -- dy itself, or, with a fused bnorm -> relu
+// (engine), dy = gate > 0 ? relu_dy : 0 (activation.cpp:14-22) computed on
+// the fly from the bnorm output `gate` and the relu output's derivative.
+template <bool kGate>
+__device__ __forceinline__ float4 eff_dy4(const float4* dy, const float4* gate, int64_t q) {
+  float4 g = __ldg(dy + q);
+  if (kGate) {
+    const float4 t = __ldg(gate + q);
+    g.x = t.x > 0.f ? g.x : 0.f;
+    g.y = t.y > 0.f ? g.y : 0.f;
+    g.z = t.z > 0.f ? g.z : 0.f;
+    g.w = t.w > 0.f ? g.w : 0.f;
+  }
+  return g;
+}
+
+// Grid (C, splits): block (c, s) reduces images [n0, n1) of channel c.  The
+// planes are contiguous (HWCN), read as float4 with four loads in flight per
+// thread; each float4's terms are summed in float, the running sums in
+// double (fixed order per thread, fixed tree per block, fixed split order in
+// bnorm_finish_k: deterministic).  HW % 4 != 0 (or misaligned): scalar loop.
+template <bool kGrad, bool kGate>
+__global__ void __launch_bounds__(256) bnorm_stats_k(const float* __restrict__ x,
+                                                     const float* __restrict__ dy,
+                                                     const float* __restrict__ gate,
+                                                     double* partial, int HW, int C, int N,
+                                                     int splits, int vec) {
   const int c = blockIdx.x, s = blockIdx.y;
   const int n0 = (int)((int64_t)N * s / splits), n1 = (int)((int64_t)N * (s + 1) / splits);
   double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
   for (int n = n0; n < n1; ++n) {
     const int64_t base = ((int64_t)n * C + c) * HW;
-    for (int p = threadIdx.x; p < HW; p += blockDim.x) {
-      double v = x[base + p];
-      a0 += v;
-      a1 += v * v;
-      if (kGrad) {
-        double g = dy[base + p];
-        a2 += g;
-        a3 += g * v;
+    if (vec) {
+      const float4* xp = (const float4*)(x + base);
+      const float4* gp = (const float4*)(dy + base);
+      const float4* tp = (const float4*)(gate + base);
+      const int Q = HW / 4;
+#pragma unroll 4
+      for (int q = threadIdx.x; q < Q; q += 256) {
+        const float4 v = __ldg(xp + q);
+        a0 += (double)((v.x + v.y) + (v.z + v.w));
+        a1 += (double)((v.x * v.x + v.y * v.y) + (v.z * v.z + v.w * v.w));
+        if (kGrad) {
+          const float4 g = eff_dy4<kGate>(gp, tp, q);
+          a2 += (double)((g.x + g.y) + (g.z + g.w));
+          a3 += (double)((g.x * v.x + g.y * v.y) + (g.z * v.z + g.w * v.w));
+        }
+      }
+    } else {
+      for (int p = threadIdx.x; p < HW; p += 256) {
+        const double v = x[base + p];
+        a0 += v;
+        a1 += v * v;
+        if (kGrad) {
+          float gf = dy[base + p];
+          if (kGate && !(gate[base + p] > 0.f)) gf = 0.f;
+          const double g = gf;
+          a2 += g;
+          a3 += g * v;
+        }
       }
     }
   }
-  __shared__ double red[4][32];
+  __shared__ double red[4][8];
   a0 = warp_sum(a0);
   a1 = warp_sum(a1);
   if (kGrad) {
@@ -963,7 +1008,7 @@ __global__ void bnorm_stats_k(const float* __restrict__ x, const float* __restri
   __syncthreads();
   if (threadIdx.x < 4) {
     double t = 0;
-    for (int k = 0; k < (int)(blockDim.x / 32); ++k) t += red[threadIdx.x][k];
+    for (int k = 0; k < 8; ++k) t += red[threadIdx.x][k];
     partial[((int64_t)s * C + c) * 4 + threadIdx.x] = t;
   }
 }
@@ -979,11 +1024,19 @@ __global__ void bnorm_finish_k(const double* partial, double* out, int C, int sp
 
 // y = w (x - mu) inv + b (normalize.cpp:172-178); moments_out gets the K x 2
 // (mean, var) tensor of graph.cpp:259-266.  fixed_moments (bnorm_infer) takes
-// precedence over stats.
-__global__ void bnorm_apply_k(const float* __restrict__ x, const float* __restrict__ w,
-                              const float* __restrict__ b, const double* __restrict__ stats,
-                              const float* __restrict__ fixed, float* __restrict__ y,
-                              float* __restrict__ mom_out, double eps, int HW, int C, int N) {
+// precedence over stats.  y2 != null (fused bnorm -> relu): also relu(y).
+__device__ __forceinline__ float bn_y(float x, float wk, float mu, float inv, float bk) {
+  return __fadd_rn(__fmul_rn(__fmul_rn(wk, __fadd_rn(x, -mu)), inv), bk);
+}
+
+__global__ void __launch_bounds__(256) bnorm_apply_k(const float* __restrict__ x,
+                                                     const float* __restrict__ w,
+                                                     const float* __restrict__ b,
+                                                     const double* __restrict__ stats,
+                                                     const float* __restrict__ fixed,
+                                                     float* __restrict__ y, float* __restrict__ y2,
+                                                     float* __restrict__ mom_out, double eps,
+                                                     int HW, int C, int N, int vec) {
   const int c = blockIdx.x;
   const double M = (double)HW * N;
   float mu, inv;
@@ -1004,8 +1057,35 @@ __global__ void bnorm_apply_k(const float* __restrict__ x, const float* __restri
   const float wk = w[c], bk = b[c];
   for (int n = blockIdx.y; n < N; n += gridDim.y) {
     const int64_t base = ((int64_t)n * C + c) * HW;
-    for (int p = threadIdx.x; p < HW; p += blockDim.x)
-      y[base + p] = __fadd_rn(__fmul_rn(__fmul_rn(wk, __fadd_rn(x[base + p], -mu)), inv), bk);
+    if (vec) {
+      const float4* xp = (const float4*)(x + base);
+      float4* yp = (float4*)(y + base);
+      float4* rp = (float4*)(y2 + base);
+      const int Q = HW / 4;
+#pragma unroll 4
+      for (int q = threadIdx.x; q < Q; q += 256) {
+        const float4 v = __ldg(xp + q);
+        float4 o;
+        o.x = bn_y(v.x, wk, mu, inv, bk);
+        o.y = bn_y(v.y, wk, mu, inv, bk);
+        o.z = bn_y(v.z, wk, mu, inv, bk);
+        o.w = bn_y(v.w, wk, mu, inv, bk);
+        yp[q] = o;
+        if (y2) {
+          o.x = o.x > 0.f ? o.x : 0.f;
+          o.y = o.y > 0.f ? o.y : 0.f;
+          o.z = o.z > 0.f ? o.z : 0.f;
+          o.w = o.w > 0.f ? o.w : 0.f;
+          rp[q] = o;
+        }
+      }
+    } else {
+      for (int p = threadIdx.x; p < HW; p += 256) {
+        const float o = bn_y(x[base + p], wk, mu, inv, bk);
+        y[base + p] = o;
+        if (y2) y2[base + p] = o > 0.f ? o : 0.f;
+      }
+    }
   }
 }
 
@@ -1013,11 +1093,20 @@ __global__ void bnorm_apply_k(const float* __restrict__ x, const float* __restri
 // stats = {sum x, sum x^2, sum dy, sum dy x}:
 //   sum dy xhat = inv (sum dy x - mu sum dy)
 //   dx = w inv (dy - mean(dy) - xhat mean(dy xhat))
-template <bool kAcc>
-__global__ void bnorm_bwd_k(const float* __restrict__ x, const float* __restrict__ dy,
-                            const float* __restrict__ w, const double* __restrict__ stats,
-                            double eps, float* dx, float* dw, float* db, int HW, int C, int N,
-                            int acc_params) {
+__device__ __forceinline__ float bn_dx(float x, float g, float mu, float inv, float winv, float mdy,
+                                       float mdyx) {
+  const float xhat = __fmul_rn(__fadd_rn(x, -mu), inv);
+  return __fmul_rn(winv, __fadd_rn(__fadd_rn(g, -mdy), -__fmul_rn(xhat, mdyx)));
+}
+
+template <bool kAcc, bool kGate>
+__global__ void __launch_bounds__(256) bnorm_bwd_k(const float* __restrict__ x,
+                                                   const float* __restrict__ dy,
+                                                   const float* __restrict__ gate,
+                                                   const float* __restrict__ w,
+                                                   const double* __restrict__ stats, double eps,
+                                                   float* dx, float* dw, float* db, int HW, int C,
+                                                   int N, int acc_params, int vec) {
   const int c = blockIdx.x;
   const double M = (double)HW * N;
   const double m = stats[c * 4] / M;
@@ -1036,10 +1125,37 @@ __global__ void bnorm_bwd_k(const float* __restrict__ x, const float* __restrict
   const float winv = __fmul_rn(wk, inv);
   for (int n = blockIdx.y; n < N; n += gridDim.y) {
     const int64_t base = ((int64_t)n * C + c) * HW;
-    for (int p = threadIdx.x; p < HW; p += blockDim.x) {
-      float xhat = __fmul_rn(__fadd_rn(x[base + p], -mu), inv);
-      float r = __fmul_rn(winv, __fadd_rn(__fadd_rn(dy[base + p], -mdy), -__fmul_rn(xhat, mdyx)));
-      dx[base + p] = kAcc ? __fadd_rn(dx[base + p], r) : r;
+    if (vec) {
+      const float4* xp = (const float4*)(x + base);
+      const float4* gp = (const float4*)(dy + base);
+      const float4* tp = (const float4*)(gate + base);
+      float4* dp = (float4*)(dx + base);
+      const int Q = HW / 4;
+#pragma unroll 4
+      for (int q = threadIdx.x; q < Q; q += 256) {
+        const float4 v = __ldg(xp + q);
+        const float4 g = eff_dy4<kGate>(gp, tp, q);
+        float4 r;
+        r.x = bn_dx(v.x, g.x, mu, inv, winv, mdy, mdyx);
+        r.y = bn_dx(v.y, g.y, mu, inv, winv, mdy, mdyx);
+        r.z = bn_dx(v.z, g.z, mu, inv, winv, mdy, mdyx);
+        r.w = bn_dx(v.w, g.w, mu, inv, winv, mdy, mdyx);
+        if (kAcc) {
+          const float4 o = dp[q];
+          r.x = __fadd_rn(o.x, r.x);
+          r.y = __fadd_rn(o.y, r.y);
+          r.z = __fadd_rn(o.z, r.z);
+          r.w = __fadd_rn(o.w, r.w);
+        }
+        dp[q] = r;
+      }
+    } else {
+      for (int p = threadIdx.x; p < HW; p += 256) {
+        float g = dy[base + p];
+        if (kGate && !(gate[base + p] > 0.f)) g = 0.f;
+        const float r = bn_dx(x[base + p], g, mu, inv, winv, mdy, mdyx);
+        dx[base + p] = kAcc ? __fadd_rn(dx[base + p], r) : r;
+      }
     }
   }
 }
@@ -1404,6 +1520,84 @@ static void pool_max_bwd_launch(const float* x, const float* dy, float* dx, cons
     pool_max_bwd_t<WH, WW, SH, SW, false, false><<<planes, 256, smem, s>>>(x, dy, dx, d, a, b);
 }
 
+// 2x2 / stride 2 max pooling without padding on even planes (LeNet, VGG):
+// windows tile the input exactly, so each input element belongs to ONE
+// window.  One thread per window reads its 2x2 block as two float2 rows
+// (coalesced along H) and writes the max in the reference's order (j outer,
+// i inner, first strict maximum: pool.cpp:59-64) plus the winner's code
+// a + 2b; the backward writes the window's four dx elements (dy at the
+// argmax, zero elsewhere: pool.cpp:98-110), again as two float2 rows.
+// Planes run along grid.y, so no index ever exceeds a plane.
+__global__ void pool2_fwd_k(const float* __restrict__ x, float* __restrict__ y,
+                            uint8_t* __restrict__ arg, int H, int OH, int OHW, int64_t planes,
+                            FastDiv by_oh) {
+  for (int64_t pl = blockIdx.y; pl < planes; pl += gridDim.y) {
+    const float* xp = x + pl * (int64_t)H * (2 * (OHW / OH));
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < OHW; w += gridDim.x * blockDim.x) {
+      const int oj = (int)by_oh.div((uint32_t)w), oi = w - oj * OH;
+      const float2 r0 = __ldg((const float2*)(xp + 2 * oi + (int64_t)H * (2 * oj)));
+      const float2 r1 = __ldg((const float2*)(xp + 2 * oi + (int64_t)H * (2 * oj + 1)));
+      float best = r0.x;
+      int code = 0;
+      if (r0.y > best) { best = r0.y; code = 1; }
+      if (r1.x > best) { best = r1.x; code = 2; }
+      if (r1.y > best) { best = r1.y; code = 3; }
+      y[pl * OHW + w] = best;
+      if (arg) arg[pl * OHW + w] = (uint8_t)code;
+    }
+  }
+}
+
+template <bool kAcc, bool kArg>
+__global__ void pool2_bwd_k(const float* __restrict__ x, const uint8_t* __restrict__ arg,
+                            const float* __restrict__ dy, float* dx, int H, int OH, int OHW,
+                            int64_t planes, FastDiv by_oh) {
+  for (int64_t pl = blockIdx.y; pl < planes; pl += gridDim.y) {
+    const int64_t xo = pl * (int64_t)H * (2 * (OHW / OH));
+    for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < OHW; w += gridDim.x * blockDim.x) {
+      const int oj = (int)by_oh.div((uint32_t)w), oi = w - oj * OH;
+      const int64_t e0 = xo + 2 * oi + (int64_t)H * (2 * oj), e1 = e0 + H;
+      int code;
+      if (kArg) {
+        code = __ldg(arg + pl * OHW + w);
+      } else {
+        const float2 r0 = __ldg((const float2*)(x + e0)), r1 = __ldg((const float2*)(x + e1));
+        float best = r0.x;
+        code = 0;
+        if (r0.y > best) { best = r0.y; code = 1; }
+        if (r1.x > best) { best = r1.x; code = 2; }
+        if (r1.y > best) { best = r1.y; code = 3; }
+      }
+      const float g = __ldg(dy + pl * OHW + w);
+      float2 o0 = make_float2(code == 0 ? g : 0.f, code == 1 ? g : 0.f);
+      float2 o1 = make_float2(code == 2 ? g : 0.f, code == 3 ? g : 0.f);
+      if (kAcc) {
+        const float2 a0 = *(const float2*)(dx + e0), a1 = *(const float2*)(dx + e1);
+        o0.x = __fadd_rn(a0.x, o0.x);
+        o0.y = __fadd_rn(a0.y, o0.y);
+        o1.x = __fadd_rn(a1.x, o1.x);
+        o1.y = __fadd_rn(a1.y, o1.y);
+      }
+      *(float2*)(dx + e0) = o0;
+      *(float2*)(dx + e1) = o1;
+    }
+  }
+}
+
+static bool pool2_exact(const PoolDims& d) {
+  return d.mode == 0 && d.wh == 2 && d.ww == 2 && d.sh == 2 && d.sw == 2 && d.pt == 0 &&
+         d.pl == 0 && d.H % 2 == 0 && d.W % 2 == 0 && d.OH == d.H / 2 && d.OW == d.W / 2 &&
+         (int64_t)d.OH * d.OW * d.OH < (1ll << 39);
+}
+
+static dim3 pool2_grid(const PoolDims& d) {
+  const int64_t planes = (int64_t)d.C * d.N;
+  const int OHW = d.OH * d.OW;
+  const unsigned gx = (unsigned)std::min<int64_t>((OHW + 255) / 256, 1024);
+  const int64_t want = std::max<int64_t>(1, (int64_t)kSMs * 8 / gx);
+  return dim3(gx, (unsigned)std::min<int64_t>(std::min<int64_t>(planes, want * 4), 65535));
+}
+
 // compile-time window/stride of a max pooling, or 0
 static int pool_fixed(const PoolDims& d) {
   if (d.mode != 0) return 0;
@@ -1429,6 +1623,17 @@ void pool_forward(const float* x, float* y, const PoolDims& d, cudaStream_t s, C
       cache->key = pool_arg_key(x, d);
     }
   }
+  if (pool2_exact(d) && ((uintptr_t)x & 7) == 0) {
+    if (!arg && cache && pool_fixed(d)) arg = (uint8_t*)cache->buf.get((size_t)total, s);
+    if (arg && cache) {
+      cache->valid = true;
+      cache->src = x;
+      cache->key = pool_arg_key(x, d);
+    }
+    pool2_fwd_k<<<pool2_grid(d), 256, 0, s>>>(x, y, arg, d.H, d.OH, d.OH * d.OW,
+                                              (int64_t)d.C * d.N, FastDiv(d.OH));
+    return;
+  }
   switch (fx) {
     case 3: pool_max_fwd_launch<3, 3, 2, 2>(x, y, d, arg, s); return;
     case 2: pool_max_fwd_launch<2, 2, 2, 2>(x, y, d, arg, s); return;
@@ -1442,6 +1647,23 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
   if (total == 0) return;
   count_launch();
   const int fx = pool_fixed(d);
+  if (pool2_exact(d) && (((uintptr_t)x | (uintptr_t)dx) & 7) == 0) {
+    const bool have_arg = cache && cache->valid && cache->src == x &&
+                          cache->key == pool_arg_key(x, d);
+    const uint8_t* arg = have_arg ? (const uint8_t*)cache->buf.ptr : nullptr;
+    const dim3 grid = pool2_grid(d);
+    const int64_t planes = (int64_t)d.C * d.N;
+    const FastDiv by(d.OH);
+    const int OHW = d.OH * d.OW;
+    if (arg) {
+      if (acc) pool2_bwd_k<true, true><<<grid, 256, 0, s>>>(x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
+      else pool2_bwd_k<false, true><<<grid, 256, 0, s>>>(x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
+    } else {
+      if (acc) pool2_bwd_k<true, false><<<grid, 256, 0, s>>>(x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
+      else pool2_bwd_k<false, false><<<grid, 256, 0, s>>>(x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
+    }
+    return;
+  }
   if (fx && cache && cache->valid && cache->src == x && cache->key == pool_arg_key(x, d) &&
       total < (1ll << 31) && total * d.H * d.W < (1ll << 39)) {
     const uint8_t* arg = (const uint8_t*)cache->buf.ptr;
@@ -1614,7 +1836,7 @@ bool lrn_backward_grid(const float* x, const float* dy, float* grid, double* bpa
 int lrn_grid_rows(int H, int W, int N) { return (int)(((int64_t)H * W * N + 31) / 32); }
 
 int bnorm_splits(int HW, int C, int N) {
-  // Aim for ~4 blocks per SM overall.
+  // ~4 blocks of 256 threads per SM overall
   int want = (kSMs * 4 + C - 1) / C;
   if (want > N) want = N;
   if (want < 1) want = 1;
@@ -1622,39 +1844,56 @@ int bnorm_splits(int HW, int C, int N) {
   return want;
 }
 
+static int bnorm_vec(const void* a, const void* b, const void* c, int HW) {
+  return HW % 4 == 0 && ((((uintptr_t)a | (uintptr_t)b | (uintptr_t)c) & 15) == 0);
+}
+
 void bnorm_stats(const float* x, const float* dy, double* partial, double* out, int HW, int C,
-                 int N, int splits, cudaStream_t s) {
+                 int N, int splits, cudaStream_t s, const float* gate) {
   dim3 grid(C, splits);
   count_launch(2);
-  if (dy)
-    bnorm_stats_k<true><<<grid, 256, 0, s>>>(x, dy, partial, HW, C, N, splits);
+  const int vec = bnorm_vec(x, dy, gate, HW);
+  if (dy && gate)
+    bnorm_stats_k<true, true><<<grid, 256, 0, s>>>(x, dy, gate, partial, HW, C, N, splits, vec);
+  else if (dy)
+    bnorm_stats_k<true, false><<<grid, 256, 0, s>>>(x, dy, nullptr, partial, HW, C, N, splits,
+                                                    vec);
   else
-    bnorm_stats_k<false><<<grid, 256, 0, s>>>(x, nullptr, partial, HW, C, N, splits);
+    bnorm_stats_k<false, false><<<grid, 256, 0, s>>>(x, nullptr, nullptr, partial, HW, C, N,
+                                                     splits, vec);
   bnorm_finish_k<<<(C + 127) / 128, 128, 0, s>>>(partial, out, C, splits);
+}
+
+static int bnorm_grid_y(int C, int N) {
+  int gy = (kSMs * 8 + C - 1) / C;
+  if (gy > N) gy = N;
+  if (gy < 1) gy = 1;
+  return gy;
 }
 
 void bnorm_apply(const float* x, const float* w, const float* b, const double* stats,
                  const float* fixed_moments, float* y, float* moments_out, double eps, int HW,
-                 int C, int N, cudaStream_t s) {
-  int gy = (kSMs * 8 + C - 1) / C;
-  if (gy > N) gy = N;
-  if (gy < 1) gy = 1;
+                 int C, int N, cudaStream_t s, float* y2) {
   count_launch();
-  bnorm_apply_k<<<dim3(C, gy), 256, 0, s>>>(x, w, b, stats, fixed_moments, y, moments_out, eps,
-                                            HW, C, N);
+  bnorm_apply_k<<<dim3(C, bnorm_grid_y(C, N)), 256, 0, s>>>(
+      x, w, b, stats, fixed_moments, y, y2, moments_out, eps, HW, C, N,
+      bnorm_vec(x, y, y2, HW));
 }
 
 void bnorm_backward_apply(const float* x, const float* dy, const float* w, const double* stats,
                           double eps, float* dx, float* dw, float* db, int HW, int C, int N,
-                          int acc, cudaStream_t s) {
-  int gy = (kSMs * 8 + C - 1) / C;
-  if (gy > N) gy = N;
-  if (gy < 1) gy = 1;
+                          int acc, cudaStream_t s, const float* gate) {
   count_launch();
-  if (acc)
-    bnorm_bwd_k<true><<<dim3(C, gy), 256, 0, s>>>(x, dy, w, stats, eps, dx, dw, db, HW, C, N, 1);
-  else
-    bnorm_bwd_k<false><<<dim3(C, gy), 256, 0, s>>>(x, dy, w, stats, eps, dx, dw, db, HW, C, N, 0);
+  const dim3 grid(C, bnorm_grid_y(C, N));
+  const int vec = bnorm_vec(x, dy, gate, HW) && bnorm_vec(dx, dx, dx, HW);
+#define CK_BNB(A, G)                                                                        \
+  bnorm_bwd_k<A, G><<<grid, 256, 0, s>>>(x, dy, gate, w, stats, eps, dx, dw, db, HW, C, N,  \
+                                         acc ? 1 : 0, vec)
+  if (acc && gate) CK_BNB(true, true);
+  else if (acc) CK_BNB(true, false);
+  else if (gate) CK_BNB(false, true);
+  else CK_BNB(false, false);
+#undef CK_BNB
 }
 
 void softmaxlog_forward(const float* x, const float* labels, const float* weights,

@@ -86,12 +86,16 @@ CONV_CASES = [
 
 
 def tc_expected(xs, fs, g):
-    """The shapes the tcgen05 kernels must take (conv_tc.cu envelope): >= 16
-    channels and filters per group, or the stride-s space-to-depth route
-    (groups 1, no padding), or an FC layer (1x1 output, no padding)."""
+    """The shapes the tcgen05 kernels must take (conv_tc.cu envelope): stride
+    1 with pads < the filter extent at any channel count, >= 16 channels and
+    filters per group, or the stride-s space-to-depth route (groups 1, no
+    padding)."""
     groups = g[6]
     if xs[2] // groups >= 16 and fs[3] // groups >= 16:
         return True
+    if g[0] == g[1] == 1 and g[2] <= fs[0] - 1 and g[3] <= fs[0] - 1 and g[4] <= fs[1] - 1 \
+            and g[5] <= fs[1] - 1:
+        return True  # stride 1, any channel count (padded to 32 per group)
     if g[0] == g[1] >= 2 and groups == 1 and not any(g[2:6]):
         return True
     return False
@@ -217,7 +221,7 @@ POOLS = [(3, 3, 2, 2, 0, 1, 0, 1, 0), (3, 3, 2, 2, 0, 1, 0, 1, 1), (2, 2, 2, 2, 
 
 
 @pytest.mark.parametrize("pg", POOLS)
-@pytest.mark.parametrize("xs", [(13, 11, 3, 2), (55, 55, 8, 2), (1, 1, 2, 1)])
+@pytest.mark.parametrize("xs", [(13, 11, 3, 2), (55, 55, 8, 2), (1, 1, 2, 1), (28, 24, 5, 3)])
 def test_pool_bitexact(xs, pg):
     try:
         _, ys = O.pool_forward(np.zeros(O.size(xs)), xs, pg)

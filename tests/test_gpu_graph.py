@@ -222,6 +222,51 @@ def test_fused_conv_relu_derivative_materialized_on_request():
             assert np.array_equal(dc, np.where(cv > 0, dr, np.float32(0))), c
 
 
+def test_vgg224_layers_vs_oracle(capsys):
+    """VGG-16-bn at its real 224x224 image (b=2), TF32, layer by layer from
+    the device's own inputs (netcheck): the first conv's 3-channel tcgen05
+    path (channels padded to 32, last_k skipping the zero K steps), the fused
+    bnorm -> relu apply / gated backward, the 2x2 pooling kernels, the fc6
+    7x7x512 layer -- exact pooling/ReLU, TF32 convs 1e-2 (1e-4 against the
+    TF32-operand oracle), bnorm 1e-4."""
+    import netcheck
+    from paper_1412_4564_b200 import nets
+    net = nets.vgg16_bn(batch=2, image=224)
+    params = {k: (v * 20 if k.endswith("f") else v) for k, v in net.init_params().items()}
+    g = device_graph(net, "tf32")
+    for k, v in {**params, **net.init_inputs()}.items():
+        g.set(k, v)
+    g.forward()
+    g.backward("objective")
+    rep = netcheck.check_layers(net, g, "tf32")
+    with capsys.disabled():
+        worst = {}
+        for (layer, what), e in rep.items():
+            worst[what] = max(worst.get(what, 0.0), e)
+        print("\n  [vgg16bn 224 b=2 tf32] worst per quantity: "
+              + ", ".join(f"{k}={v:.1e}" for k, v in sorted(worst.items())))
+
+
+def test_fused_bnorm_relu_derivative_materialized_on_request():
+    """bnorm -> relu (VGG): the bnorm apply writes relu(y) too, the backward
+    gates the relu output's derivative by y > 0 inside both bnorm passes, and
+    the bnorm output's derivative is computed on request -- exactly the relu
+    backward (activation.cpp:14-22)."""
+    from paper_1412_4564_b200 import nets
+    net = nets.vgg16_bn(batch=2, image=32)
+    g = device_graph(net, "tf32")
+    for k, v in {**net.init_params(), **net.init_inputs()}.items():
+        g.set(k, v)
+    for _ in range(2):
+        g.forward()
+        g.backward("objective")
+        for k in (1, 5, 13):
+            b, r = f"b{k}", f"r{k}"
+            bv, dr = g.get(b), g.get(r, deriv=True)
+            assert np.array_equal(g.get(r), np.maximum(bv, 0)), r
+            assert np.array_equal(g.get(b, deriv=True), np.where(bv > 0, dr, np.float32(0))), b
+
+
 @pytest.mark.parametrize("net_name,batch", [("alexnet", 16), ("alexnet", 3), ("cifar", 8)])
 def test_lrn_writes_conv_dy_grid(net_name, batch, monkeypatch):
     """conv -> relu -> lrn chains (TF32): the LRN backward writes the conv's
@@ -285,21 +330,23 @@ def test_lrn_grid_envelope(cout, groups, size, monkeypatch):
             assert np.array_equal(a, b), name
 
 
-@pytest.mark.parametrize("side", [55, 27, 13])
+@pytest.mark.parametrize("side,win", [(55, 3), (27, 3), (13, 3), (28, 2), (112, 2)])
 @pytest.mark.parametrize("pad", [(0, 0, 0, 0), (0, 1, 0, 1)])
-def test_engine_pool_argmax_route_bitexact(pad, side):
+def test_engine_pool_argmax_route_bitexact(pad, side, win):
     """In a graph the max pool records its argmax in the forward and the
     backward routes from it (engine.cu / kernels.cu pool_max3s2_bwd_strip_k:
     SEG 32 / 16 / 8 lane segments at AlexNet's 55 / 27 / 13 planes): dx
     must equal the oracle pool backward (pool.cpp:83-126) of the same dy
     bit for bit, spikes making >= 3 windows share an argmax."""
     from paper_1412_4564_b200.graph import Graph
+    if win == 2 and pad != (0, 0, 0, 0):
+        pad = (0, 1, 0, 1)  # pads must stay below the window: 2x2 with a clipped last window
     xs, n = (side, side, 4, 3), 3
     r = O.Rng(41)
     x = r.uniform(O.size(xs), -0.01, 0.01).reshape(xs[::-1])
     x[:, :, ::2, ::2] += 1.0 + r.uniform(x[:, :, ::2, ::2].size).reshape(x[:, :, ::2, ::2].shape)
     x = x.ravel()
-    pg = (3, 3, 2, 2, *pad, 0)
+    pg = (win, win, 2, 2, *pad, 0)
     _, ps = O.pool_forward(x, xs, pg)
     g = Graph(math="fp32")
     g.add_input("x", xs)
