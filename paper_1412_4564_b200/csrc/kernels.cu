@@ -946,9 +946,9 @@ __device__ __forceinline__ float4 eff_dy4(const float4* dy, const float4* gate, 
 
 // Grid (C, splits): block (c, s) reduces images [n0, n1) of channel c.  The
 // planes are contiguous (HWCN), read as float4 with four loads in flight per
-// thread; each float4's terms are summed in float, the running sums in
-// double (fixed order per thread, fixed tree per block, fixed split order in
-// bnorm_finish_k: deterministic).  HW % 4 != 0 (or misaligned): scalar loop.
+// thread; every term is summed in double (the one-pass moments E[x^2] -
+// E[x]^2 need it), in a fixed order per thread, a fixed tree per block and a
+// fixed split order in bnorm_finish_k: deterministic.  HW % 4 != 0 (or misaligned): scalar loop.
 template <bool kGrad, bool kGate>
 __global__ void __launch_bounds__(256) bnorm_stats_k(const float* __restrict__ x,
                                                      const float* __restrict__ dy,
@@ -968,12 +968,14 @@ __global__ void __launch_bounds__(256) bnorm_stats_k(const float* __restrict__ x
 #pragma unroll 4
       for (int q = threadIdx.x; q < Q; q += 256) {
         const float4 v = __ldg(xp + q);
-        a0 += (double)((v.x + v.y) + (v.z + v.w));
-        a1 += (double)((v.x * v.x + v.y * v.y) + (v.z * v.z + v.w * v.w));
+        const double x0 = v.x, x1 = v.y, x2 = v.z, x3 = v.w;
+        a0 += (x0 + x1) + (x2 + x3);
+        a1 += (x0 * x0 + x1 * x1) + (x2 * x2 + x3 * x3);
         if (kGrad) {
           const float4 g = eff_dy4<kGate>(gp, tp, q);
-          a2 += (double)((g.x + g.y) + (g.z + g.w));
-          a3 += (double)((g.x * v.x + g.y * v.y) + (g.z * v.z + g.w * v.w));
+          const double g0 = g.x, g1 = g.y, g2 = g.z, g3 = g.w;
+          a2 += (g0 + g1) + (g2 + g3);
+          a3 += (g0 * x0 + g1 * x1) + (g2 * x2 + g3 * x3);
         }
       }
     } else {
