@@ -51,6 +51,39 @@ using ConvGeom = ck_conv_geom;            // conv.hpp:9-17 (same field order)
 using ConvTransposeGeom = ck_convt_geom;  // conv.hpp:21-28
 using PoolGeom = ck_pool_geom;            // pool.hpp:13-23
 using LrnParams = ck_lrn_params;          // normalize.hpp:11-16
+using SpnormParams = ck_spnorm_params;    // normalize.hpp:59-64
+
+// loss.hpp:13-24 (same order as convkit::LossKind)
+enum class LossKind : int {
+  classerror = CK_LOSS_CLASSERROR,
+  topk = CK_LOSS_TOPK,
+  log = CK_LOSS_LOG,
+  softmaxlog = CK_LOSS_SOFTMAXLOG,
+  mhinge = CK_LOSS_MHINGE,
+  mshinge = CK_LOSS_MSHINGE,
+  binaryerror = CK_LOSS_BINARYERROR,
+  binarylog = CK_LOSS_BINARYLOG,
+  logistic = CK_LOSS_LOGISTIC,
+  hinge = CK_LOSS_HINGE,
+};
+
+// loss.hpp:31-36
+struct LossOptions {
+  int64_t top_k = 5;
+  double threshold = 0.0;
+  bool random_ties = false;
+  uint64_t tie_seed = 0;
+  ck_loss_options c() const {
+    return ck_loss_options{top_k, threshold, random_ties ? 1 : 0, tie_seed};
+  }
+};
+
+// normalize.hpp:27-31: per-channel batch mean and (biased) variance
+template <class T>
+struct BnormMoments {
+  std::vector<T> mean;
+  std::vector<T> var;
+};
 
 inline ConvGeom conv_geom() { return ConvGeom{1, 1, 0, 0, 0, 0, 1}; }
 
@@ -251,7 +284,7 @@ inline DeviceTensor lrn_backward(const DeviceTensor& x, const LrnParams& p,
 // moments: K x 2 (mean column, variance column), graph.cpp:259-266
 inline DeviceTensor bnorm_forward(const DeviceTensor& x, const DeviceTensor& w,
                                   const DeviceTensor& b, double epsilon,
-                                  DeviceTensor* moments = nullptr) {
+                                  DeviceTensor* moments) {
   Context& c = Context::current();
   DeviceTensor y(x.shape());
   if (moments) *moments = DeviceTensor(Shape(x.shape().c, 2, 1, 1));
@@ -269,6 +302,28 @@ inline DeviceTensor bnorm_infer(const DeviceTensor& x, const DeviceTensor& w,
   ck_tensor xv = x.view(), wv = w.view(), bv = b.view(), mv = moments.view(), yv = y.view();
   c.check(ck_bnorm_infer(c.handle(), &xv, &wv, &bv, epsilon, &mv, &yv, c.stream()));
   return y;
+}
+// normalize.hpp:35-38 with the reference's BnormMoments<T>* (host vectors)
+inline DeviceTensor bnorm_forward(const DeviceTensor& x, const DeviceTensor& w,
+                                  const DeviceTensor& b, double epsilon,
+                                  BnormMoments<float>* moments = nullptr) {
+  if (!moments) return bnorm_forward(x, w, b, epsilon, (DeviceTensor*)nullptr);
+  DeviceTensor m;
+  DeviceTensor y = bnorm_forward(x, w, b, epsilon, &m);
+  std::vector<float> h = m.to_host();
+  const size_t K = (size_t)x.shape().c;
+  moments->mean.assign(h.begin(), h.begin() + K);
+  moments->var.assign(h.begin() + K, h.end());
+  return y;
+}
+// normalize.hpp:41-44 with BnormMoments<T>
+inline DeviceTensor bnorm_infer(const DeviceTensor& x, const DeviceTensor& w,
+                                const DeviceTensor& b, double epsilon,
+                                const BnormMoments<float>& moments) {
+  std::vector<float> h(moments.mean);
+  h.insert(h.end(), moments.var.begin(), moments.var.end());
+  DeviceTensor m(Shape((int64_t)moments.mean.size(), 2, 1, 1), h);
+  return bnorm_infer(x, w, b, epsilon, m);
 }
 inline void bnorm_backward(const DeviceTensor& x, const DeviceTensor& w, const DeviceTensor& b,
                            double epsilon, const DeviceTensor& dy, DeviceTensor* dx,
@@ -305,6 +360,142 @@ inline DeviceTensor softmaxlog_backward(const DeviceTensor& x, const DeviceTenso
   c.check(ck_softmaxlog_backward(c.handle(), &xv, &lv, weights ? &wv : nullptr, p, &dxv, 0,
                                  c.stream()));
   return dx;
+}
+
+
+// ---- loss.hpp:39-49: every LossKind ----------------------------------------
+// loss_forward: the weighted sum of per-sample penalties (a host scalar, as in
+// the reference); label / domain errors raise DataError with its messages.
+inline float loss_forward(const DeviceTensor& x, const DeviceTensor& labels, LossKind kind,
+                          const DeviceTensor* weights = nullptr, const LossOptions& opts = {}) {
+  Context& c = Context::current();
+  DeviceTensor out(Shape(1, 1, 1, 1));
+  ck_tensor xv = x.view(), lv = labels.view(), wv;
+  if (weights) wv = weights->view();
+  const ck_loss_options o = opts.c();
+  c.check(ck_loss_forward(c.handle(), &xv, &lv, weights ? &wv : nullptr, (ck_loss_kind)kind, &o,
+                          out.data(), 1, c.stream()));
+  return out.to_host()[0];
+}
+// loss_backward: projected derivative (p = the scalar projection); error
+// kinds return exact zeros (loss.cpp:239)
+inline DeviceTensor loss_backward(const DeviceTensor& x, const DeviceTensor& labels,
+                                  LossKind kind, const DeviceTensor* weights, float p,
+                                  const LossOptions& opts = {}) {
+  Context& c = Context::current();
+  DeviceTensor dx(x.shape());
+  ck_tensor xv = x.view(), lv = labels.view(), wv, dxv = dx.view();
+  if (weights) wv = weights->view();
+  const ck_loss_options o = opts.c();
+  c.check(ck_loss_backward(c.handle(), &xv, &lv, weights ? &wv : nullptr, (ck_loss_kind)kind, &o,
+                           p, &dxv, 0, c.stream()));
+  return dx;
+}
+// loss.hpp:52-63 pdist
+inline DeviceTensor pdist_forward(const DeviceTensor& x, const DeviceTensor& target, double p,
+                                  bool no_root) {
+  Context& c = Context::current();
+  DeviceTensor y(Shape(x.shape().h, x.shape().w, 1, x.shape().n));
+  ck_tensor xv = x.view(), tv = target.view(), yv = y.view();
+  c.check(ck_pdist_forward(c.handle(), &xv, &tv, p, no_root ? 1 : 0, &yv, c.stream()));
+  return y;
+}
+inline void pdist_backward(const DeviceTensor& x, const DeviceTensor& target, double p,
+                           bool no_root, const DeviceTensor& dy, DeviceTensor* dx,
+                           DeviceTensor* dtarget) {
+  Context& c = Context::current();
+  if (dx) *dx = DeviceTensor(x.shape());
+  if (dtarget) *dtarget = DeviceTensor(x.shape());
+  ck_tensor xv = x.view(), tv = target.view(), dyv = dy.view(), dxv, dtv;
+  if (dx) dxv = dx->view();
+  if (dtarget) dtv = dtarget->view();
+  c.check(ck_pdist_backward(c.handle(), &xv, &tv, p, no_root ? 1 : 0, &dyv, dx ? &dxv : nullptr,
+                            dtarget ? &dtv : nullptr, 0, c.stream()));
+}
+
+// ---- activation.hpp:14-19 sigmoid; normalize.hpp:66-76 softmax, spnorm ------
+inline DeviceTensor sigmoid_forward(const DeviceTensor& x) {
+  Context& c = Context::current();
+  DeviceTensor y(x.shape());
+  ck_tensor xv = x.view(), yv = y.view();
+  c.check(ck_sigmoid_forward(c.handle(), &xv, &yv, c.stream()));
+  return y;
+}
+inline DeviceTensor sigmoid_backward(const DeviceTensor& y, const DeviceTensor& dy) {
+  Context& c = Context::current();
+  DeviceTensor dx(y.shape());
+  ck_tensor yv = y.view(), dyv = dy.view(), dxv = dx.view();
+  c.check(ck_sigmoid_backward(c.handle(), &yv, &dyv, &dxv, 0, c.stream()));
+  return dx;
+}
+inline DeviceTensor softmax_forward(const DeviceTensor& x) {
+  Context& c = Context::current();
+  DeviceTensor y(x.shape());
+  ck_tensor xv = x.view(), yv = y.view();
+  c.check(ck_softmax_forward(c.handle(), &xv, &yv, c.stream()));
+  return y;
+}
+inline DeviceTensor softmax_backward(const DeviceTensor& y, const DeviceTensor& dy) {
+  Context& c = Context::current();
+  DeviceTensor dx(y.shape());
+  ck_tensor yv = y.view(), dyv = dy.view(), dxv = dx.view();
+  c.check(ck_softmax_backward(c.handle(), &yv, &dyv, &dxv, 0, c.stream()));
+  return dx;
+}
+inline DeviceTensor spnorm_forward(const DeviceTensor& x, const SpnormParams& p) {
+  Context& c = Context::current();
+  DeviceTensor y(x.shape());
+  ck_tensor xv = x.view(), yv = y.view();
+  c.check(ck_spnorm_forward(c.handle(), &xv, &p, &yv, c.stream()));
+  return y;
+}
+inline DeviceTensor spnorm_backward(const DeviceTensor& x, const SpnormParams& p,
+                                   const DeviceTensor& dy) {
+  Context& c = Context::current();
+  DeviceTensor dx(x.shape());
+  ck_tensor xv = x.view(), dyv = dy.view(), dxv = dx.view();
+  c.check(ck_spnorm_backward(c.handle(), &xv, &p, &dyv, &dxv, 0, c.stream()));
+  return dx;
+}
+
+// ---- bilinear.hpp:13-22 ---------------------------------------------------
+inline Shape bilinear_output_shape(const Shape& x, const Shape& grid) {
+  Context& c = Context::current();
+  ck_shape o;
+  c.check(ck_bilinear_output_shape(c.handle(), x.c_shape(), grid.c_shape(), &o));
+  return from_c(o);
+}
+inline DeviceTensor bilinear_forward(const DeviceTensor& x, const DeviceTensor& grid) {
+  Context& c = Context::current();
+  DeviceTensor y(bilinear_output_shape(x.shape(), grid.shape()));
+  ck_tensor xv = x.view(), gv = grid.view(), yv = y.view();
+  c.check(ck_bilinear_forward(c.handle(), &xv, &gv, &yv, c.stream()));
+  return y;
+}
+inline void bilinear_backward(const DeviceTensor& x, const DeviceTensor& grid,
+                              const DeviceTensor& dy, DeviceTensor* dx, DeviceTensor* dgrid) {
+  Context& c = Context::current();
+  if (dx) *dx = DeviceTensor(x.shape());
+  if (dgrid) *dgrid = DeviceTensor(grid.shape());
+  ck_tensor xv = x.view(), gv = grid.view(), dyv = dy.view(), dxv, dgv;
+  if (dx) dxv = dx->view();
+  if (dgrid) dgv = dgrid->view();
+  c.check(ck_bilinear_backward(c.handle(), &xv, &gv, &dyv, dx ? &dxv : nullptr,
+                               dgrid ? &dgv : nullptr, 0, c.stream()));
+}
+
+// ---- blob.hpp:11-18: the raw tensor blob <-> a device tensor ----------------
+inline void write_blob(const DeviceTensor& t, const std::string& path) {
+  std::vector<float> h = t.to_host();
+  if (ck_blob_write(path.c_str(), h.data(), t.shape().c_shape()) != CK_OK)
+    throw DataError(ck_io_last_error());
+}
+inline DeviceTensor read_blob(const std::string& path) {
+  ck_shape s;
+  if (ck_blob_read_shape(path.c_str(), &s) != CK_OK) throw DataError(ck_io_last_error());
+  std::vector<float> h((size_t)(s.h * s.w * s.c * s.n));
+  if (ck_blob_read(path.c_str(), h.data(), s) != CK_OK) throw DataError(ck_io_last_error());
+  return DeviceTensor(from_c(s), h);
 }
 
 }  // namespace convkit

@@ -26,6 +26,7 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
 #include <sys/stat.h>
 
 #include <cinttypes>
@@ -854,11 +855,19 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
 }
 
 // graph.cpp:494-545 forward (train mode).
+// NVTX ranges per layer pass and per gradient bucket (host-side markers for
+// nsys / ncu --nvtx; free when no tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const std::string& name) { nvtxRangePushA(name.c_str()); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 static void run_forward(ck_graph* g, cudaStream_t s) {
   for (auto& l : g->layers) l.cache.valid = false;
   // loss layers record label errors (loss.cpp:101-106) in the handle's flag
   if (g->has_loss) reset_label_flag(g->h, s);
   for (int li : g->order) {
+    NvtxRange r(g->layers[li].name + " fwd");
     g->prof(li, 0, s);
     layer_forward(g, g->layers[li], s);
     g->prof(li, 1, s);
@@ -891,6 +900,7 @@ static void run_backward(ck_graph* g, int objective, cudaStream_t s, LayerDone* 
     bool any = false;
     for (int o : l.out) any |= g->vars[o].deriv_live;
     if (any) {
+      NvtxRange r(l.name + " bwd");
       g->prof(*it, 2, s);
       layer_backward(g, l, s);
       g->prof(*it, 3, s);
@@ -983,6 +993,7 @@ struct ck_trainer : ck::LayerDone {
           merged.back().second = std::max(merged.back().second, r.second);
         else
           merged.push_back(r);
+      ck::NvtxRange r("allreduce " + g->layers[li].name);
       ck::check_cuda(cudaEventRecord(ev[li], s), "event");
       ck::check_cuda(cudaStreamWaitEvent(comm_stream, ev[li], 0), "wait");
       if (ncclGroupStart() != ncclSuccess) throw Err(CK_ERR_CUDA, "ncclGroupStart failed");

@@ -1,0 +1,29 @@
+"""compute-sanitizer over the tcgen05 / TMA pipelines and the engine step
+(tools/sanitize_case.py): memcheck (out-of-bounds / misaligned global and
+shared accesses, leaks of the launch errors) and synccheck (illegal barrier
+use -- the mbarrier / elect.sync role loops of the GEMM) must report 0
+errors.  Slow (the sanitizer serialises and instruments every kernel)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not installed")
+    r = subprocess.run([SAN, "--tool", tool, "--error-exitcode", "9", sys.executable,
+                        os.path.join(ROOT, "tools", "sanitize_case.py")],
+                       capture_output=True, text=True, timeout=1800)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert "sanitize case done" in r.stdout, tail
+    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, tail
+    assert r.returncode == 0, tail
