@@ -124,6 +124,11 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
 
 void lrn_forward(const float* x, float* y, int H, int W, int C, int N, int size, float kappa,
                  float alpha, float beta, cudaStream_t s);
+// LRN fused with the 3x3 / stride-2 max pool reading it: y = lrn(x), py =
+// pool(y) and (cache) the pool's argmax for its backward.  False (nothing
+// launched) outside the fused kernel's envelope.
+bool lrn_maxpool_forward(const float* x, float* y, float* py, const PoolDims& pd, int size,
+                         float kappa, float alpha, float beta, cudaStream_t s, ConvCache* cache);
 void lrn_backward(const float* x, const float* dy, float* dx, int H, int W, int C, int N, int size,
                   float kappa, float alpha, float beta, int acc, cudaStream_t s);
 // LRN backward whose output goes (ReLU-gated by x > 0) straight into the dy

@@ -124,6 +124,9 @@ struct Layer {
   Workspace dyg, bpart;
   int pre_rows = 0;
   bool bwd_deferred = false;  // ... and was, in the current backward pass
+  // lrn -> max pool (3x3 / 2): the LRN forward also produces the pool's
+  // output and argmax (lrn_maxpool_forward); lrn_pool = that pool layer
+  int lrn_pool = -1;
 };
 
 static std::vector<std::string> split_csv(const char* s) {
@@ -151,6 +154,7 @@ struct ck_graph {
   float* one_dev = nullptr;  // the objective seed 1.0f, device-resident (graph-capturable)
   bool has_loss = false;
   bool lrn_grid = true;  // option "lrn_grid": LRN backward writes the conv's dy grid
+  bool lrn_pool = true;  // option "lrn_pool": LRN forward also computes the max pool after it
   std::vector<std::pair<std::string, std::string>> meta;  // manifest metadata
   std::vector<int> decl;  // input / param vars in declaration order (manifest order)
   int64_t last_launches = 0;
@@ -457,6 +461,17 @@ static void finalize(ck_graph* g) {
     r.fused_by = v.producer;
     r.fused_bwd = true;
   }
+  // lrn -> max pool pairs whose intermediate has no other reader
+  for (size_t li = 0; li < g->layers.size(); ++li) {
+    Layer& pl = g->layers[li];
+    if (pl.kind != Kind::pool || pl.p.size() < 9 || pl.p[8] != 0) continue;
+    const Var& v = g->vars[pl.in[0]];
+    if (v.producer < 0 || v.consumers.size() != 1) continue;
+    Layer& l = g->layers[v.producer];
+    if (l.kind != Kind::lrn || l.lrn_pool >= 0) continue;
+    l.lrn_pool = (int)li;
+    pl.fused_by = v.producer;
+  }
   g->finalized = true;
 }
 
@@ -489,6 +504,7 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
       break;
     }
     case Kind::pool: {
+      if (l.fused_by >= 0 && l.fused_done) break;  // produced by the LRN before it
       ck_tensor x = V(0);
       ck_pool_geom pg = pool_geom_of(l);
       h->conv_cache = &l.cache;  // records the argmax for this step's backward
@@ -505,6 +521,22 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
     case Kind::lrn: {
       ck_tensor x = V(0);
       ck_lrn_params p = lrn_of(l);
+      if (l.lrn_pool >= 0) {
+        // lrn -> max pool: one kernel writes y, the pool output and its argmax
+        Layer& pl = g->layers[l.lrn_pool];
+        pl.fused_done = false;
+        const Var& pv = g->vars[pl.out[0]];
+        if (g->lrn_pool && p.group_size >= 1 && p.kappa > 0) {
+          const PoolDims pd = pool_dims(y.shape, pv.shape, pool_geom_of(pl));
+          pl.fused_done = lrn_maxpool_forward(x.data, y.data, pv.value, pd, (int)p.group_size,
+                                              (float)p.kappa, (float)p.alpha, (float)p.beta, s,
+                                              &pl.cache);
+          if (pl.fused_done) {
+            after_launch();
+            break;
+          }
+        }
+      }
       st = ck_lrn_forward(h, &x, &p, &y, s);
       break;
     }
@@ -1220,6 +1252,8 @@ ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value) {
   const std::string n = name ? name : "";
   if (n == "lrn_grid")
     g->lrn_grid = value != 0;
+  else if (n == "lrn_pool")
+    g->lrn_pool = value != 0;
   else
     throw Err(CK_ERR_ARG, "unknown graph option '" + n + "'");
   CKG_END(g)

@@ -728,6 +728,96 @@ __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y
   }
 }
 
+// LRN (normalize.cpp:47-71) fused with the 3x3 / stride-2 max pooling that
+// reads it (pool.cpp:49-80; AlexNet norm1 -> pool1, norm2 -> pool2).  A block
+// owns TOI x TOJ pool outputs of one image and computes the LRN of the
+// (2 TOI + 1) x (2 TOJ + 1) input pixels their windows cover (one thread per
+// pixel, the same register channel chain and float operations as
+// lrn_fwd_reg_k, so y is bit-identical); every CH channels the values go
+// through shared memory to the window maxima (first strict maximum, j outer /
+// i inner, the winner's code a + 3b as pool_max_fwd_t records it for the
+// backward).  The pool never re-reads the LRN output from HBM; y is still
+// written (it is a variable of the tape), by the pixel's owning tile only.
+// Requires pad_top = pad_left = 0 and windows covering every input pixel.
+template <int NW>
+__global__ void __launch_bounds__(320) lrn_maxpool3s2_k(
+    const float* __restrict__ x, float* __restrict__ y, float* __restrict__ py,
+    uint8_t* __restrict__ arg, int H, int W, int C, int OH, int OW, float kappa, float alpha,
+    float nbeta) {
+  constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
+  constexpr int TOI = 16, TOJ = 4, TI = 2 * TOI + 1, TJ = 2 * TOJ + 1, CH = 8;
+  __shared__ float tile[CH][TJ][TI + 1];
+  const int n = blockIdx.z;
+  const int oi0 = blockIdx.x * TOI, oj0 = blockIdx.y * TOJ;
+  const int ib = 2 * oi0, jb = 2 * oj0;  // tile origin (pads top/left are 0)
+  const int t = threadIdx.x;
+  const int ti = t % TI, tj = t / TI;
+  const int i = ib + ti, j = jb + tj;
+  const bool active = t < TI * TJ && i < H && j < W;
+  const bool owned = active && (ti < 2 * TOI || oi0 + TOI >= OH) && (tj < 2 * TOJ || oj0 + TOJ >= OW);
+  const int64_t HW = (int64_t)H * W;
+  const float* xp = x + (int64_t)n * C * HW + i + (int64_t)H * j;
+  float* yq = y + (int64_t)n * C * HW + i + (int64_t)H * j;
+  auto ldx = [&](int c) { return (active && c >= 0 && c < C) ? __ldg(xp + (int64_t)c * HW) : 0.f; };
+  float sq[NW], xv[NW];
+#pragma unroll
+  for (int q = 0; q < NW; ++q) {
+    xv[q] = ldx(q - DOWN);
+    sq[q] = __fmul_rn(xv[q], xv[q]);
+  }
+  const int OHW = OH * OW;
+  for (int k0 = 0; k0 < C; k0 += CH) {
+    float nx[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) nx[u] = ldx(k0 + u + UP + 1);
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      float acc = 0.f;
+#pragma unroll
+      for (int q = 0; q < NW; ++q) acc = __fadd_rn(acc, sq[q]);
+      const float scale = __powf(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
+      const float v = __fmul_rn(xv[DOWN], scale);
+      if (owned && k0 + u < C) yq[(int64_t)(k0 + u) * HW] = v;
+      if (t < TI * TJ) tile[u][tj][ti] = v;
+#pragma unroll
+      for (int q = 0; q < NW - 1; ++q) {
+        sq[q] = sq[q + 1];
+        xv[q] = xv[q + 1];
+      }
+      xv[NW - 1] = nx[u];
+      sq[NW - 1] = __fmul_rn(nx[u], nx[u]);
+    }
+    __syncthreads();
+    for (int q = t; q < TOI * TOJ * CH; q += blockDim.x) {
+      const int u = q / (TOI * TOJ), w = q - u * (TOI * TOJ);
+      const int oi = oi0 + w % TOI, oj = oj0 + w / TOI, k = k0 + u;
+      if (oi >= OH || oj >= OW || k >= C) continue;
+      const int si = 2 * oi, sj = 2 * oj;
+      float best = 0.f;
+      int code = 0;
+      bool have = false;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (si + a < H && sj + b < W) {
+            const float v = tile[u][sj + b - jb][si + a - ib];
+            if (!have || v > best) {
+              best = v;
+              code = a + 3 * b;
+            }
+            have = true;
+          }
+        }
+      }
+      const int64_t o = ((int64_t)n * C + k) * OHW + oi + (int64_t)OH * oj;
+      py[o] = best;
+      if (arg) arg[o] = (uint8_t)code;
+    }
+    __syncthreads();
+  }
+}
+
 // GRID: instead of dx, store relu_backward(x, dx) -- x is the output of the
 // ReLU feeding this LRN, so x > 0 is that ReLU's mask (activation.cpp:14-22)
 // -- straight into the pixel-major dy grid of the conv below that ReLU (dy at
@@ -1792,6 +1882,34 @@ void lrn_forward(const float* x, float* y, int H, int W, int C, int N, int size,
   size_t smem = (size_t)C * kLrnPix * sizeof(float);
   lrn_smem_check(C, 1);
   lrn_fwd_k<<<grid, 256, smem, s>>>(x, y, HW, C, size, kappa, alpha, -beta);
+}
+
+bool lrn_maxpool_forward(const float* x, float* y, float* py, const PoolDims& pd, int size,
+                         float kappa, float alpha, float beta, cudaStream_t s, ConvCache* cache) {
+  // 3x3 / stride-2 max pooling, pads top/left 0, windows covering the input
+  if (pd.mode != 0 || pd.wh != 3 || pd.ww != 3 || pd.sh != 2 || pd.sw != 2 || pd.pt != 0 ||
+      pd.pl != 0 || 2 * (pd.OH - 1) + 3 < pd.H || 2 * (pd.OW - 1) + 3 < pd.W)
+    return false;
+  if (size != 5 && size != 3) return false;
+  uint8_t* arg = nullptr;
+  const int64_t total = (int64_t)pd.OH * pd.OW * pd.C * pd.N;
+  if (cache) {
+    arg = (uint8_t*)cache->buf.get((size_t)total, s);
+    if (arg) {
+      cache->valid = true;
+      cache->src = y;
+      cache->key = pool_arg_key(y, pd);
+    }
+  }
+  count_launch();
+  const dim3 grid((pd.OH + 15) / 16, (pd.OW + 3) / 4, pd.N);
+  if (size == 5)
+    lrn_maxpool3s2_k<5><<<grid, 320, 0, s>>>(x, y, py, arg, pd.H, pd.W, pd.C, pd.OH, pd.OW, kappa,
+                                              alpha, -beta);
+  else
+    lrn_maxpool3s2_k<3><<<grid, 320, 0, s>>>(x, y, py, arg, pd.H, pd.W, pd.C, pd.OH, pd.OW, kappa,
+                                              alpha, -beta);
+  return true;
 }
 
 void lrn_backward(const float* x, const float* dy, float* dx, int H, int W, int C, int N, int size,

@@ -297,6 +297,37 @@ def test_lrn_writes_conv_dy_grid(net_name, batch, monkeypatch):
             assert np.array_equal(a, b), name
 
 
+@pytest.mark.parametrize("batch", [3, 32])
+def test_lrn_maxpool_fusion_bitexact(batch):
+    """lrn -> 3x3/2 max pool (AlexNet norm1/pool1, norm2/pool2) as one kernel
+    (kernels.cu lrn_maxpool3s2_k): every value and derivative of the network is
+    bit-identical to the unfused blocks (normalize.cpp:47-71 then
+    pool.cpp:49-80, same float operations, same argmax routing)."""
+    from paper_1412_4564_b200 import nets
+    net = nets.alexnet(batch=batch)
+    out = []
+    for fuse in (True, False):
+        g = device_graph(net, "tf32")
+        g.set_option("lrn_pool", fuse)
+        for k, v in {**net.init_params(), **net.init_inputs()}.items():
+            g.set(k, v)
+        hd = g.hd
+        l0 = hd.launches
+        g.forward()
+        launches = hd.launches - l0
+        g.backward("objective")
+        names = set(net.inputs) | {p[0] for p in net.params} | \
+            {o for layer in net.layers for o in layer[3]}
+        out.append(({n: g.get(n) for n in sorted(names)},
+                    {n: g.get(n, deriv=True) for n in sorted(names) if n != "label"}, launches))
+    (v0, d0, l0), (v1, d1, l1) = out
+    assert l0 == l1 - 2  # the two pool layers launched nothing of their own
+    for n in v1:
+        assert np.array_equal(v0[n], v1[n]), n
+    for n in d1:
+        assert np.array_equal(d0[n], d1[n]), n
+
+
 @pytest.mark.parametrize("cout,groups,size", [(64, 2, 5), (48, 1, 5), (96, 1, 3), (64, 1, 4)])
 def test_lrn_grid_envelope(cout, groups, size, monkeypatch):
     """conv -> relu -> lrn -> pool -> fc on a small image: inside the fused
