@@ -312,8 +312,9 @@ ck_status ck_graph_layer_ms(ck_graph* g, int layer, float* fwd_ms, float* bwd_ms
 /* Engine options (not reference entry points):
  *   "lrn_grid" (default 1): a TF32 conv -> relu -> lrn chain's LRN backward
  *   writes the conv's ReLU-gated dy grid directly (0: the unfused blocks);
- *   "lrn_pool" (default 1): an lrn -> 3x3/2 max pool pair runs as one kernel
- *   (the pool reads the LRN values from shared memory, not HBM). */
+ *   "lrn_pool" (default 0): an lrn -> 3x3/2 max pool pair runs as one kernel
+ *   (the pool reads the LRN values from shared memory, not HBM; bit-identical,
+ *   measured slower than the two tuned kernels on AlexNet). */
 ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value);
 
 /* ---- cnn_train training step with multi-GPU data parallelism ------------ */

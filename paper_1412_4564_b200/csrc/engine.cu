@@ -154,7 +154,11 @@ struct ck_graph {
   float* one_dev = nullptr;  // the objective seed 1.0f, device-resident (graph-capturable)
   bool has_loss = false;
   bool lrn_grid = true;  // option "lrn_grid": LRN backward writes the conv's dy grid
-  bool lrn_pool = true;  // option "lrn_pool": LRN forward also computes the max pool after it
+  // option "lrn_pool": LRN forward also computes the max pool after it.  Off
+  // by default: bit-identical but measured slower on AlexNet (norm1+pool1
+  // 0.247 vs 0.213 ms, norm2+pool2 0.168 vs 0.149: the per-chunk barrier and
+  // the 16% halo recompute cost more than the 297 MB re-read saves)
+  bool lrn_pool = false;
   std::vector<std::pair<std::string, std::string>> meta;  // manifest metadata
   std::vector<int> decl;  // input / param vars in declaration order (manifest order)
   int64_t last_launches = 0;

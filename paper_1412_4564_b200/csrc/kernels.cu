@@ -742,18 +742,20 @@ __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y
 template <int NW>
 __global__ void __launch_bounds__(320) lrn_maxpool3s2_k(
     const float* __restrict__ x, float* __restrict__ y, float* __restrict__ py,
-    uint8_t* __restrict__ arg, int H, int W, int C, int OH, int OW, float kappa, float alpha,
-    float nbeta) {
+    uint8_t* __restrict__ arg, int H, int W, int C, int OH, int OW, int TOI, float kappa,
+    float alpha, float nbeta) {
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
-  constexpr int TOI = 16, TOJ = 4, TI = 2 * TOI + 1, TJ = 2 * TOJ + 1, CH = 8;
-  __shared__ float tile[CH][TJ][TI + 1];
+  constexpr int TOJ = 4, TJ = 2 * TOJ + 1, CH = 8, TIM = 33;
+  __shared__ float tile[2][CH][TJ][TIM + 1];  // double-buffered: one barrier per chunk
+  const int TI = 2 * TOI + 1;
   const int n = blockIdx.z;
   const int oi0 = blockIdx.x * TOI, oj0 = blockIdx.y * TOJ;
   const int ib = 2 * oi0, jb = 2 * oj0;  // tile origin (pads top/left are 0)
   const int t = threadIdx.x;
   const int ti = t % TI, tj = t / TI;
   const int i = ib + ti, j = jb + tj;
-  const bool active = t < TI * TJ && i < H && j < W;
+  const bool in_tile = t < TI * TJ;
+  const bool active = in_tile && i < H && j < W;
   const bool owned = active && (ti < 2 * TOI || oi0 + TOI >= OH) && (tj < 2 * TOJ || oj0 + TOJ >= OW);
   const int64_t HW = (int64_t)H * W;
   const float* xp = x + (int64_t)n * C * HW + i + (int64_t)H * j;
@@ -765,11 +767,24 @@ __global__ void __launch_bounds__(320) lrn_maxpool3s2_k(
     xv[q] = ldx(q - DOWN);
     sq[q] = __fmul_rn(xv[q], xv[q]);
   }
-  const int OHW = OH * OW;
-  for (int k0 = 0; k0 < C; k0 += CH) {
-    float nx[CH];
+  float nx[CH];
 #pragma unroll
-    for (int u = 0; u < CH; ++u) nx[u] = ldx(k0 + u + UP + 1);
+  for (int u = 0; u < CH; ++u) nx[u] = ldx(u + UP + 1);
+  // pool-phase assignment: window w = t % 64 of the tile, channels u = t / 64,
+  // t / 64 + npu, ... of the chunk
+  const int pw = t & 63, pu = t >> 6, npu = max(1, (int)(blockDim.x >> 6));
+  const int poi = oi0 + pw % TOI, poj = oj0 + pw / TOI;
+  const bool pool_thread = pw < TOI * TOJ && poi < OH && poj < OW;
+  const int psi = 2 * (poi - oi0), psj = 2 * (poj - oj0);
+  const bool inside = 2 * poi + 2 < H && 2 * poj + 2 < W;
+  const int OHW = OH * OW;
+  const int64_t po = (int64_t)n * C * OHW + poi + (int64_t)OH * poj;
+  for (int k0 = 0, buf = 0; k0 < C; k0 += CH, buf ^= 1) {
+    float cur[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) cur[u] = nx[u];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) nx[u] = ldx(k0 + CH + u + UP + 1);  // next chunk, in flight
 #pragma unroll
     for (int u = 0; u < CH; ++u) {
       float acc = 0.f;
@@ -778,43 +793,55 @@ __global__ void __launch_bounds__(320) lrn_maxpool3s2_k(
       const float scale = __powf(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
       const float v = __fmul_rn(xv[DOWN], scale);
       if (owned && k0 + u < C) yq[(int64_t)(k0 + u) * HW] = v;
-      if (t < TI * TJ) tile[u][tj][ti] = v;
+      if (in_tile) tile[buf][u][tj][ti] = v;
 #pragma unroll
       for (int q = 0; q < NW - 1; ++q) {
         sq[q] = sq[q + 1];
         xv[q] = xv[q + 1];
       }
-      xv[NW - 1] = nx[u];
-      sq[NW - 1] = __fmul_rn(nx[u], nx[u]);
+      xv[NW - 1] = cur[u];
+      sq[NW - 1] = __fmul_rn(cur[u], cur[u]);
     }
     __syncthreads();
-    for (int q = t; q < TOI * TOJ * CH; q += blockDim.x) {
-      const int u = q / (TOI * TOJ), w = q - u * (TOI * TOJ);
-      const int oi = oi0 + w % TOI, oj = oj0 + w / TOI, k = k0 + u;
-      if (oi >= OH || oj >= OW || k >= C) continue;
-      const int si = 2 * oi, sj = 2 * oj;
-      float best = 0.f;
-      int code = 0;
-      bool have = false;
+    if (pool_thread) {
+      for (int u = pu; u < CH; u += npu) {
+        const int k = k0 + u;
+        if (k >= C) break;
+        float best;
+        int code = 0;
+        if (inside) {
+          best = tile[buf][u][psj][psi];
 #pragma unroll
-      for (int b = 0; b < 3; ++b) {
+          for (int bb = 0; bb < 3; ++bb)
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          if (si + a < H && sj + b < W) {
-            const float v = tile[u][sj + b - jb][si + a - ib];
-            if (!have || v > best) {
-              best = v;
-              code = a + 3 * b;
+            for (int aa = 0; aa < 3; ++aa) {
+              const float v = tile[buf][u][psj + bb][psi + aa];
+              if (v > best) {
+                best = v;
+                code = aa + 3 * bb;
+              }
             }
-            have = true;
-          }
+        } else {  // clipped at the bottom / right edge (pool.cpp:20-33)
+          best = 0.f;
+          bool have = false;
+#pragma unroll
+          for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
+            for (int aa = 0; aa < 3; ++aa) {
+              if (2 * poi + aa < H && 2 * poj + bb < W) {
+                const float v = tile[buf][u][psj + bb][psi + aa];
+                if (!have || v > best) {
+                  best = v;
+                  code = aa + 3 * bb;
+                }
+                have = true;
+              }
+            }
         }
+        py[po + (int64_t)k * OHW] = best;
+        if (arg) arg[po + (int64_t)k * OHW] = (uint8_t)code;
       }
-      const int64_t o = ((int64_t)n * C + k) * OHW + oi + (int64_t)OH * oj;
-      py[o] = best;
-      if (arg) arg[o] = (uint8_t)code;
     }
-    __syncthreads();
   }
 }
 
@@ -1891,6 +1918,7 @@ bool lrn_maxpool_forward(const float* x, float* y, float* py, const PoolDims& pd
       pd.pl != 0 || 2 * (pd.OH - 1) + 3 < pd.H || 2 * (pd.OW - 1) + 3 < pd.W)
     return false;
   if (size != 5 && size != 3) return false;
+  if (((pd.OH <= 16 ? pd.OH : (pd.OH + 1) / 2)) > 16 || pd.N > 65535) return false;
   uint8_t* arg = nullptr;
   const int64_t total = (int64_t)pd.OH * pd.OW * pd.C * pd.N;
   if (cache) {
@@ -1902,13 +1930,17 @@ bool lrn_maxpool_forward(const float* x, float* y, float* py, const PoolDims& pd
     }
   }
   count_launch();
-  const dim3 grid((pd.OH + 15) / 16, (pd.OW + 3) / 4, pd.N);
+  // window rows per tile: the whole column when it fits, else halves
+  const int TOI = pd.OH <= 16 ? pd.OH : (pd.OH + 1) / 2;
+  if (TOI > 16) return false;
+  const int threads = ((2 * TOI + 1) * 9 + 31) / 32 * 32;
+  const dim3 grid((pd.OH + TOI - 1) / TOI, (pd.OW + 3) / 4, pd.N);
   if (size == 5)
-    lrn_maxpool3s2_k<5><<<grid, 320, 0, s>>>(x, y, py, arg, pd.H, pd.W, pd.C, pd.OH, pd.OW, kappa,
-                                              alpha, -beta);
+    lrn_maxpool3s2_k<5><<<grid, threads, 0, s>>>(x, y, py, arg, pd.H, pd.W, pd.C, pd.OH, pd.OW,
+                                                  TOI, kappa, alpha, -beta);
   else
-    lrn_maxpool3s2_k<3><<<grid, 320, 0, s>>>(x, y, py, arg, pd.H, pd.W, pd.C, pd.OH, pd.OW, kappa,
-                                              alpha, -beta);
+    lrn_maxpool3s2_k<3><<<grid, threads, 0, s>>>(x, y, py, arg, pd.H, pd.W, pd.C, pd.OH, pd.OW,
+                                                  TOI, kappa, alpha, -beta);
   return true;
 }
 
