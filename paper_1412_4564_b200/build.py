@@ -31,13 +31,18 @@ def _nvcc():
     return os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, lib: str = LIB, build_dir: str = BUILD,
+          extra=()) -> str:
+    """Product build into paper_1412_4564_b200/libck.so.  (lib, build_dir,
+    extra) build a variant elsewhere, e.g. the CK_EXPERIMENTS library the
+    tools/ A/B scripts load explicitly; the product path never loads it."""
+    BUILD, LIB = build_dir, lib  # noqa: N806
     os.makedirs(BUILD, exist_ok=True)
     inc_nccl, lib_nccl = nccl_paths()
     common = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
               "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-I", inc_nccl,
               "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
-              *os.environ.get("CK_EXTRA_NVCC", "").split()]
+              *os.environ.get("CK_EXTRA_NVCC", "").split(), *extra]
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "ck", "ck.h"))
     hdr_mtime = max(os.path.getmtime(h) for h in headers)
@@ -67,4 +72,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    if "--experiments" in sys.argv:  # tools/: A/B against the measured-slower kernels
+        print(build(verbose="-v" in sys.argv, force=True,
+                    lib=os.path.join(BUILD + "_exp", "libck_exp.so"), build_dir=BUILD + "_exp",
+                    extra=("-DCK_EXPERIMENTS",)))
+    else:
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

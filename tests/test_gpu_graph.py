@@ -595,3 +595,63 @@ def test_graph_extended_kinds(math):
                 ("loss", "l2", ["z", "label"], ["o2"], [5]),          # mshinge
                 ("sum", "obj", ["o1", "o2"], ["objective"], [])])
     _graph_vs_oracle(net, params, inputs, math, 1e-4 if math == "fp32" else 1e-2)
+
+
+def test_replay_survives_workspace_reallocation():
+    """a captured training step holds raw pointers into the
+    handle's workspaces; a larger call on the same handle reallocates them.
+    The trainer must notice (workspace generation) and re-capture: steps stay
+    bit-identical to an eager trainer fed the same batches."""
+    from paper_1412_4564_b200 import blocks as B
+    from paper_1412_4564_b200 import nets
+    from paper_1412_4564_b200.graph import Trainer
+    net = nets.cifar(batch=8)
+    params, inputs = net.init_params(), net.init_inputs()
+    runs = []
+    for graph_mode in (False, True):
+        g = device_graph(net, "tf32")
+        for k, v in {**params, **inputs}.items():
+            g.set(k, v)
+        t = Trainer(g, lr=0.01, momentum=0.9, weight_decay=5e-4)
+        t.set_graph(graph_mode)
+        stream = torch.cuda.Stream()
+        losses = [t.step(stream=stream.cuda_stream) for _ in range(3)]
+        # a much larger conv on the same (thread's) handle grows every workspace
+        x = B.from_hwcn((64, 64, 64, 16)).uniform_(-1, 1)
+        f = B.from_hwcn((5, 5, 64, 64)).uniform_(-0.05, 0.05)
+        y = B.conv_forward(x, f, None, B.ConvGeom(2, 2, 2, 2, 2, 2), math="tf32")
+        B.conv_backward(x, f, B.ConvGeom(2, 2, 2, 2, 2, 2), torch.ones_like(y), math="tf32")
+        torch.cuda.synchronize()
+        losses += [t.step(stream=stream.cuda_stream) for _ in range(3)]
+        runs.append((losses, {p: g.get(p) for p, _, _ in net.params}))
+    (l0, p0), (l1, p1) = runs
+    assert l0 == l1
+    for k in p0:
+        assert np.array_equal(p0[k], p1[k]), k
+
+
+def test_unreached_parameter_gets_zero_derivative():
+    """a parameter whose consumer does not feed the objective has
+    the reference's zero derivative (graph.cpp:551-554) -- also when the
+    trainer updates it (weight decay only) -- not uninitialised memory."""
+    from paper_1412_4564_b200.graph import Graph, Trainer
+    g = Graph(math="fp32")
+    g.add_input("data", (6, 6, 4, 2))
+    g.add_input("label", (1, 1, 1, 2))
+    g.add_param("F", (6, 6, 4, 10))
+    g.add_param("G", (3, 3, 4, 5))                      # feeds a dead branch
+    g.add_layer("conv", "fc", ["data", "F"], ["z"], [1, 1, 0, 0, 0, 0, 1])
+    g.add_layer("conv", "side", ["data", "G"], ["s"], [1, 1, 0, 0, 0, 0, 1])
+    g.add_layer("loss", "loss", ["z", "label"], ["objective"], [])
+    g.finalize()
+    r = O.Rng(5)
+    g.set("data", r.uniform(6 * 6 * 4 * 2))
+    g.set("label", np.array([1, 2], np.float32))
+    G0 = r.uniform(3 * 3 * 4 * 5)
+    g.set("G", G0)
+    g.set("F", r.uniform(6 * 6 * 4 * 10, -0.1, 0.1))
+    t = Trainer(g, lr=0.1, momentum=0.0, weight_decay=0.01)
+    t.step()
+    assert np.all(g.get("G", deriv=True) == 0)
+    w_ref, _ = O.sgd_step(G0, np.zeros_like(G0), np.zeros_like(G0), 0.1, 0.0, 0.01)
+    assert np.array_equal(g.get("G"), w_ref)

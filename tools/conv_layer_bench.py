@@ -2,6 +2,9 @@
 import sys, os, argparse
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+if "--lib" in sys.argv:  # an explicitly built variant (build.py --experiments)
+    from paper_1412_4564_b200 import _lib
+    _lib.LIB_PATH = sys.argv[sys.argv.index("--lib") + 1]
 from paper_1412_4564_b200 import blocks as B
 LAYERS = {
     "conv1": ((227, 227, 3), (11, 11, 3, 96), (4, 4, 0, 0, 0, 0, 1)),
@@ -11,12 +14,17 @@ LAYERS = {
     "conv5": ((13, 13, 384), (3, 3, 192, 256), (1, 1, 1, 1, 1, 1, 2)),
     "fc6": ((6, 6, 256), (6, 6, 256, 4096), (1, 1, 0, 0, 0, 0, 1)),
     "fc7": ((1, 1, 4096), (1, 1, 4096, 4096), (1, 1, 0, 0, 0, 0, 1)),
+    "vgg1": ((224, 224, 3), (3, 3, 3, 64), (1, 1, 1, 1, 1, 1, 1)),
+    "vgg2": ((224, 224, 64), (3, 3, 64, 64), (1, 1, 1, 1, 1, 1, 1)),
+    "vgg4": ((112, 112, 128), (3, 3, 128, 128), (1, 1, 1, 1, 1, 1, 1)),
+    "vgg6": ((56, 56, 256), (3, 3, 256, 256), (1, 1, 1, 1, 1, 1, 1)),
 }
 ap = argparse.ArgumentParser()
 ap.add_argument("--layers", default=",".join(LAYERS))
 ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--passes", default="f,d,w")
+ap.add_argument("--lib", default="")
 a = ap.parse_args()
 for name in a.layers.split(","):
     (H, W, C), fs, g = LAYERS[name]
