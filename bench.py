@@ -301,6 +301,15 @@ def mem_layers(net):
     for n, s, _ in net.params:
         shapes[n] = s
     out = []
+    # a relu whose input has no other reader is fused into its producer (the
+    # bnorm apply writes relu(y), the backward gates inside the bnorm passes):
+    # its compulsory bytes (8n fwd, 12n bwd) are charged to that entry
+    readers = {}
+    for kind, name, ins, outs, p in net.layers:
+        for i in ins:
+            readers[i] = readers.get(i, 0) + 1
+    fused_relu = {ins[0] for kind, name, ins, outs, p in net.layers
+                  if kind == "relu" and readers.get(ins[0]) == 1}
     for kind, name, ins, outs, p in net.layers:
         xs = shapes[ins[0]]
         nx = xs[0] * xs[1] * xs[2] * xs[3]
@@ -317,7 +326,9 @@ def mem_layers(net):
             ys = (1, 1, 1, 1)
         else:
             ys = xs
-            if kind in ("lrn", "bnorm"):
+            if kind == "bnorm" and outs[0] in fused_relu:
+                out.append((name, "bnorm+relu", 16 * nx, 24 * nx))
+            elif kind in ("lrn", "bnorm"):
                 out.append((name, kind, 8 * nx, 12 * nx))
         shapes[outs[0]] = ys
     return out
