@@ -1639,59 +1639,6 @@ static void pool_max_bwd_launch(const float* x, const float* dy, float* dx, cons
     pool_max_bwd_t<WH, WW, SH, SW, false, false><<<planes, 256, smem, s>>>(x, dy, dx, d, a, b);
 }
 
-// 3x3 / stride 2 max pooling (AlexNet pool1/2/5), planes staged in shared
-// memory: a block copies PPB whole contiguous planes with coalesced loads,
-// then one thread per output takes its window from shared memory -- each
-// input element is read from HBM once (the per-output kernel reads every
-// element of the overlapping windows 2.25x through L1/L2).  Same rule and
-// winner code as pool_max_fwd_t (first valid element, then strict >, j
-// outer / i inner; code a + 3 b relative to the window origin).
-__global__ void __launch_bounds__(256) pool3s2_fwd_plane_k(const float* __restrict__ x,
-                                                           float* __restrict__ y,
-                                                           uint8_t* __restrict__ arg, PoolDims d,
-                                                           int ppb, int64_t planes,
-                                                           FastDiv by_ohw, FastDiv by_oh) {
-  extern __shared__ float xs[];
-  const int HW = d.H * d.W, OHW = d.OH * d.OW;
-  const int64_t p0 = (int64_t)blockIdx.x * ppb;
-  const int np = (int)(planes - p0 < ppb ? planes - p0 : ppb);
-  const float* src = x + p0 * HW;
-  const int nin = np * HW;
-#pragma unroll 4
-  for (int e = threadIdx.x; e < nin; e += 256) xs[e] = __ldg(src + e);
-  __syncthreads();
-  const int nout = np * OHW;
-  for (int e = threadIdx.x; e < nout; e += 256) {
-    const int pl = (int)by_ohw.div((uint32_t)e);
-    const int w = e - pl * OHW;
-    const int oj = (int)by_oh.div((uint32_t)w), oi = w - oj * d.OH;
-    const int si = 2 * oi - d.pt, sj = 2 * oj - d.pl;
-    const float* xp = xs + pl * HW;
-    float best = 0.f;
-    int code = 0;
-    bool have = false;
-#pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      const int j = sj + b;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        const int i = si + a;
-        if (i >= 0 && i < d.H && j >= 0 && j < d.W) {
-          const float v = xp[i + d.H * j];
-          if (!have || v > best) {
-            best = v;
-            code = a + 3 * b;
-          }
-          have = true;
-        }
-      }
-    }
-    const int64_t o = (p0 + pl) * OHW + w;
-    y[o] = best;
-    if (arg) arg[o] = (uint8_t)code;
-  }
-}
-
 // 2x2 / stride 2 max pooling without padding on even planes (LeNet, VGG):
 // windows tile the input exactly, so each input element belongs to ONE
 // window.  One thread per window reads its 2x2 block as two float2 rows
@@ -1805,18 +1752,6 @@ void pool_forward(const float* x, float* y, const PoolDims& d, cudaStream_t s, C
     pool2_fwd_k<<<pool2_grid(d), 256, 0, s>>>(x, y, arg, d.H, d.OH, d.OH * d.OW,
                                               (int64_t)d.C * d.N, FastDiv(d.OH));
     return;
-  }
-  if (fx == 3) {
-    // whole planes in shared memory when at least one fits in 48 KB
-    const int HW = d.H * d.W;
-    const int ppb = std::max(1, std::min(64, (24 * 1024 / 4) / HW));
-    if (HW * 4 <= 48 * 1024) {
-      const int64_t planes = (int64_t)d.C * d.N;
-      const unsigned grid = (unsigned)((planes + ppb - 1) / ppb);
-      pool3s2_fwd_plane_k<<<grid, 256, (size_t)ppb * HW * 4, s>>>(
-          x, y, arg, d, ppb, planes, FastDiv(d.OH * d.OW), FastDiv(d.OH));
-      return;
-    }
   }
   switch (fx) {
     case 3: pool_max_fwd_launch<3, 3, 2, 2>(x, y, d, arg, s); return;
