@@ -646,7 +646,8 @@ ck_status ck_bnorm_forward(ck_handle* h, const ck_tensor* x, const ck_tensor* w,
   bnorm_stats(x->data, nullptr, buf, stats, HW, C, N, splits, st);
   // engine (bnorm -> relu): relu(y) written by the same pass
   bnorm_apply(x->data, w->data, b->data, stats, nullptr, y->data,
-              moments ? moments->data : nullptr, epsilon, HW, C, N, st, h->fuse_relu);
+              moments ? moments->data : nullptr, epsilon, HW, C, N, st, h->fuse_relu,
+              h->fuse_relu ? h->bn_muinv : nullptr);
   if (h->fuse_relu) h->fuse_relu_done = true;
   after_launch();
   CK_API_END(h)
@@ -689,12 +690,16 @@ ck_status ck_bnorm_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* w
   double* stats = buf + (size_t)4 * C * splits;
   // engine (bnorm -> relu, relu backward deferred): the derivative reaching
   // y is fuse_relu_x (= y) > 0 ? fuse_relu_dy : 0, formed inside both passes
+  // With the forward's (mu, inv) at hand (h->bn_muinv) the gate y > 0 is
+  // recomputed from x -- bit-identical to the forward's y -- instead of read.
   const float* dyp = h->fuse_relu_x ? h->fuse_relu_dy : dy->data;
-  const float* gate = h->fuse_relu_x;
-  bnorm_stats(x->data, dyp, buf, stats, HW, C, N, splits, st, gate);
+  BnGate rg;
+  if (h->fuse_relu_x && h->bn_muinv) rg = BnGate{w->data, b->data, h->bn_muinv};
+  const float* gate = rg.muinv ? nullptr : h->fuse_relu_x;
+  bnorm_stats(x->data, dyp, buf, stats, HW, C, N, splits, st, gate, rg);
   bnorm_backward_apply(x->data, dyp, w->data, stats, epsilon, dx ? dx->data : nullptr,
                        dw ? dw->data : nullptr, db ? db->data : nullptr, HW, C, N, accumulate,
-                       st, gate);
+                       st, gate, rg);
   after_launch();
   CK_API_END(h)
 }

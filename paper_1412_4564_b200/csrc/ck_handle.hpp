@@ -50,6 +50,9 @@ struct ck_handle {
   const double* pre_bpart = nullptr;
   int pre_rows = 0;
   ck::KernelProfiler prof;
+  // engine, fused bnorm -> relu: per-channel (mu, inv) of the forward, which
+  // the backward uses to recompute the relu gate from x (2 floats / channel)
+  float* bn_muinv = nullptr;
 };
 
 namespace ck {

@@ -142,18 +142,30 @@ int lrn_grid_rows(int H, int W, int N);
 
 // Per-channel sums in double: out[c] = {sum x, sum x^2, sum dy, sum dy*x}
 // (dy may be null).  partial: workspace of splits*C*4 doubles.
+// Gate recomputation of a fused bnorm -> relu backward: the bnorm output's
+// sign from x with the forward's per-channel (mu, inv) floats (muinv, 2 per
+// channel, written by bnorm_apply) and the layer's w, b.
+struct BnGate {
+  const float* w = nullptr;
+  const float* b = nullptr;
+  const float* muinv = nullptr;
+};
 void bnorm_stats(const float* x, const float* dy, double* partial, double* out, int HW, int C,
-                 int N, int splits, cudaStream_t s, const float* gate = nullptr);
+                 int N, int splits, cudaStream_t s, const float* gate = nullptr,
+                 const BnGate& rg = BnGate{});
 int bnorm_splits(int HW, int C, int N);
-// y2 != null: also relu(y) (fused bnorm -> relu)
+// y2 != null: also relu(y) (fused bnorm -> relu); muinv_out: the (mu, inv)
+// floats of every channel, for the backward's gate recomputation
 void bnorm_apply(const float* x, const float* w, const float* b, const double* stats,
                  const float* fixed_moments, float* y, float* moments_out, double eps, int HW,
-                 int C, int N, cudaStream_t s, float* y2 = nullptr);
+                 int C, int N, cudaStream_t s, float* y2 = nullptr, float* muinv_out = nullptr);
 // gate != null (fused bnorm -> relu backward): the derivative reaching the
-// bnorm output is gate > 0 ? dy : 0 (gate = bnorm output, dy = relu output's)
+// bnorm output is gate > 0 ? dy : 0 (gate = bnorm output, dy = relu output's);
+// rg.muinv != null: the gate recomputed from x instead of read
 void bnorm_backward_apply(const float* x, const float* dy, const float* w, const double* stats,
                           double eps, float* dx, float* dw, float* db, int HW, int C, int N,
-                          int acc, cudaStream_t s, const float* gate = nullptr);
+                          int acc, cudaStream_t s, const float* gate = nullptr,
+                          const BnGate& rg = BnGate{});
 
 // softmaxlog: per-site loss into site_loss, then a fixed-order sum into loss.
 void softmaxlog_forward(const float* x, const float* labels, const float* weights,

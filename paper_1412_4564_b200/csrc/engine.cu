@@ -109,6 +109,7 @@ struct Layer {
   std::vector<int> in, out;
   std::vector<double> p;
   float* aux = nullptr;  // bnorm moments (K x 2), graph.cpp:306
+  float* muinv = nullptr;  // bnorm -> relu: the forward's (mu, inv) per channel
   ConvCache cache;       // conv input transform shared by forward and wgrad
   // conv -> relu fusion: the conv's epilogue also writes relu(y) (the relu
   // layer's output) when its output feeds only that relu; the relu forward
@@ -450,7 +451,10 @@ static void finalize(ck_graph* g) {
     if (!v.deriv) v.deriv = alloc((size_t)elems(v.shape));
   }
   for (auto& l : g->layers)
-    if (l.kind == Kind::bnorm) l.aux = alloc(2 * (size_t)g->vars[l.in[0]].shape.c);
+    if (l.kind == Kind::bnorm) {
+      l.aux = alloc(2 * (size_t)g->vars[l.in[0]].shape.c);
+      l.muinv = alloc(2 * (size_t)g->vars[l.in[0]].shape.c);
+    }
   // conv -> relu pairs whose intermediate has no other reader
   for (size_t li = 0; li < g->layers.size(); ++li) {
     Layer& r = g->layers[li];
@@ -549,8 +553,10 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
       ck_tensor m{l.aux, ck_shape{x.shape.c, 2, 1, 1}};
       h->fuse_relu = l.relu_out >= 0 ? g->vars[l.relu_out].value : nullptr;
       h->fuse_relu_done = false;
+      h->bn_muinv = l.muinv;
       st = ck_bnorm_forward(h, &x, &w, &b, l.p[0], &y, &m, s);
       h->fuse_relu = nullptr;
+      h->bn_muinv = nullptr;
       if (l.relu_out >= 0) {
         Layer& r = g->layers[g->vars[l.relu_out].producer];
         r.fused_done = st == CK_OK && h->fuse_relu_done;
@@ -782,12 +788,15 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
       if (fused) {
         h->fuse_relu_x = g->vars[l.out[0]].value;
         h->fuse_relu_dy = g->vars[l.relu_out].deriv;
+        // (mu, inv) written by this step's fused forward, if it ran fused
+        if (g->layers[g->vars[l.relu_out].producer].fused_done) h->bn_muinv = l.muinv;
       }
       struct ResetB {
         ck_handle* h;
         ~ResetB() {
           h->fuse_relu_x = nullptr;
           h->fuse_relu_dy = nullptr;
+          h->bn_muinv = nullptr;
         }
       } resetb{h};
       if (fused) {

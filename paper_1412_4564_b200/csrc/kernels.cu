@@ -1048,17 +1048,46 @@ __device__ __forceinline__ double warp_sum(double v) {
 // reaches the bnorm output -- dy itself, or, with a fused bnorm -> relu
 // (engine), dy = gate > 0 ? relu_dy : 0 (activation.cpp:14-22) computed on
 // the fly from the bnorm output `gate` and the relu output's derivative.
-template <bool kGate>
-__device__ __forceinline__ float4 eff_dy4(const float4* dy, const float4* gate, int64_t q) {
+// G = 0: plain dy.  G = 1: gate read from the stored bnorm output.  G = 2:
+// the bnorm output recomputed from x with the forward's own (mu, inv) floats
+// (muinv, written by the fused apply) -- the same float operations as the
+// forward's bn_y, so the gate is the forward's exactly, without reading y.
+struct BnGateP {
+  float w, b, mu, inv;
+};
+__device__ __forceinline__ float bn_y(float x, float wk, float mu, float inv, float bk) {
+  return __fadd_rn(__fmul_rn(__fmul_rn(wk, __fadd_rn(x, -mu)), inv), bk);
+}
+template <int G>
+__device__ __forceinline__ float eff_dy1(float g, float x, const float* gate, int64_t e,
+                                         const BnGateP& P) {
+  if (G == 1 && !(gate[e] > 0.f)) return 0.f;
+  if (G == 2 && !(bn_y(x, P.w, P.mu, P.inv, P.b) > 0.f)) return 0.f;
+  return g;
+}
+template <int G>
+__device__ __forceinline__ float4 eff_dy4(const float4* dy, const float4* gate, int64_t q,
+                                          const float4& v, const BnGateP& P) {
   float4 g = __ldg(dy + q);
-  if (kGate) {
+  if (G == 1) {
     const float4 t = __ldg(gate + q);
     g.x = t.x > 0.f ? g.x : 0.f;
     g.y = t.y > 0.f ? g.y : 0.f;
     g.z = t.z > 0.f ? g.z : 0.f;
     g.w = t.w > 0.f ? g.w : 0.f;
+  } else if (G == 2) {
+    g.x = bn_y(v.x, P.w, P.mu, P.inv, P.b) > 0.f ? g.x : 0.f;
+    g.y = bn_y(v.y, P.w, P.mu, P.inv, P.b) > 0.f ? g.y : 0.f;
+    g.z = bn_y(v.z, P.w, P.mu, P.inv, P.b) > 0.f ? g.z : 0.f;
+    g.w = bn_y(v.w, P.w, P.mu, P.inv, P.b) > 0.f ? g.w : 0.f;
   }
   return g;
+}
+__device__ __forceinline__ BnGateP bn_gate_params(const float* gw, const float* gb,
+                                                  const float* muinv, int c) {
+  BnGateP P{0.f, 0.f, 0.f, 0.f};
+  if (muinv) P = BnGateP{gw[c], gb[c], muinv[2 * c], muinv[2 * c + 1]};
+  return P;
 }
 
 // Grid (C, splits): block (c, s) reduces images [n0, n1) of channel c.  The
@@ -1066,13 +1095,17 @@ __device__ __forceinline__ float4 eff_dy4(const float4* dy, const float4* gate, 
 // thread; every term is summed in double (the one-pass moments E[x^2] -
 // E[x]^2 need it), in a fixed order per thread, a fixed tree per block and a
 // fixed split order in bnorm_finish_k: deterministic.  HW % 4 != 0 (or misaligned): scalar loop.
-template <bool kGrad, bool kGate>
+template <bool kGrad, int G>
 __global__ void __launch_bounds__(256) bnorm_stats_k(const float* __restrict__ x,
                                                      const float* __restrict__ dy,
                                                      const float* __restrict__ gate,
+                                                     const float* __restrict__ gw,
+                                                     const float* __restrict__ gb,
+                                                     const float* __restrict__ muinv,
                                                      double* partial, int HW, int C, int N,
                                                      int splits, int vec) {
   const int c = blockIdx.x, s = blockIdx.y;
+  const BnGateP P = bn_gate_params(gw, gb, muinv, c);
   const int n0 = (int)((int64_t)N * s / splits), n1 = (int)((int64_t)N * (s + 1) / splits);
   double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
   for (int n = n0; n < n1; ++n) {
@@ -1089,7 +1122,7 @@ __global__ void __launch_bounds__(256) bnorm_stats_k(const float* __restrict__ x
         a0 += (x0 + x1) + (x2 + x3);
         a1 += (x0 * x0 + x1 * x1) + (x2 * x2 + x3 * x3);
         if (kGrad) {
-          const float4 g = eff_dy4<kGate>(gp, tp, q);
+          const float4 g = eff_dy4<G>(gp, tp, q, v, P);
           const double g0 = g.x, g1 = g.y, g2 = g.z, g3 = g.w;
           a2 += (g0 + g1) + (g2 + g3);
           a3 += (g0 * x0 + g1 * x1) + (g2 * x2 + g3 * x3);
@@ -1101,9 +1134,7 @@ __global__ void __launch_bounds__(256) bnorm_stats_k(const float* __restrict__ x
         a0 += v;
         a1 += v * v;
         if (kGrad) {
-          float gf = dy[base + p];
-          if (kGate && !(gate[base + p] > 0.f)) gf = 0.f;
-          const double g = gf;
+          const double g = eff_dy1<G>(dy[base + p], x[base + p], gate, base + p, P);
           a2 += g;
           a3 += g * v;
         }
@@ -1144,17 +1175,14 @@ __global__ void bnorm_finish_k(const double* partial, double* out, int C, int sp
 // y = w (x - mu) inv + b (normalize.cpp:172-178); moments_out gets the K x 2
 // (mean, var) tensor of graph.cpp:259-266.  fixed_moments (bnorm_infer) takes
 // precedence over stats.  y2 != null (fused bnorm -> relu): also relu(y).
-__device__ __forceinline__ float bn_y(float x, float wk, float mu, float inv, float bk) {
-  return __fadd_rn(__fmul_rn(__fmul_rn(wk, __fadd_rn(x, -mu)), inv), bk);
-}
-
 __global__ void __launch_bounds__(256) bnorm_apply_k(const float* __restrict__ x,
                                                      const float* __restrict__ w,
                                                      const float* __restrict__ b,
                                                      const double* __restrict__ stats,
                                                      const float* __restrict__ fixed,
                                                      float* __restrict__ y, float* __restrict__ y2,
-                                                     float* __restrict__ mom_out, double eps,
+                                                     float* __restrict__ mom_out,
+                                                     float* __restrict__ muinv_out, double eps,
                                                      int HW, int C, int N, int vec) {
   const int c = blockIdx.x;
   const double M = (double)HW * N;
@@ -1174,6 +1202,10 @@ __global__ void __launch_bounds__(256) bnorm_apply_k(const float* __restrict__ x
     }
   }
   const float wk = w[c], bk = b[c];
+  if (muinv_out && blockIdx.y == 0 && threadIdx.x == 0) {
+    muinv_out[2 * c] = mu;  // for the backward's gate recomputation
+    muinv_out[2 * c + 1] = inv;
+  }
   for (int n = blockIdx.y; n < N; n += gridDim.y) {
     const int64_t base = ((int64_t)n * C + c) * HW;
     if (vec) {
@@ -1218,10 +1250,12 @@ __device__ __forceinline__ float bn_dx(float x, float g, float mu, float inv, fl
   return __fmul_rn(winv, __fadd_rn(__fadd_rn(g, -mdy), -__fmul_rn(xhat, mdyx)));
 }
 
-template <bool kAcc, bool kGate>
+template <bool kAcc, int G>
 __global__ void __launch_bounds__(256) bnorm_bwd_k(const float* __restrict__ x,
                                                    const float* __restrict__ dy,
                                                    const float* __restrict__ gate,
+                                                   const float* __restrict__ gb,
+                                                   const float* __restrict__ muinv,
                                                    const float* __restrict__ w,
                                                    const double* __restrict__ stats, double eps,
                                                    float* dx, float* dw, float* db, int HW, int C,
@@ -1242,6 +1276,7 @@ __global__ void __launch_bounds__(256) bnorm_bwd_k(const float* __restrict__ x,
   const float mu = (float)m, inv = (float)invd, wk = w[c];
   const float mdy = (float)(sdy / M), mdyx = (float)(sdyx / M);
   const float winv = __fmul_rn(wk, inv);
+  const BnGateP P = bn_gate_params(w, gb, muinv, c);
   for (int n = blockIdx.y; n < N; n += gridDim.y) {
     const int64_t base = ((int64_t)n * C + c) * HW;
     if (vec) {
@@ -1253,7 +1288,7 @@ __global__ void __launch_bounds__(256) bnorm_bwd_k(const float* __restrict__ x,
 #pragma unroll 4
       for (int q = threadIdx.x; q < Q; q += 256) {
         const float4 v = __ldg(xp + q);
-        const float4 g = eff_dy4<kGate>(gp, tp, q);
+        const float4 g = eff_dy4<G>(gp, tp, q, v, P);
         float4 r;
         r.x = bn_dx(v.x, g.x, mu, inv, winv, mdy, mdyx);
         r.y = bn_dx(v.y, g.y, mu, inv, winv, mdy, mdyx);
@@ -1270,8 +1305,7 @@ __global__ void __launch_bounds__(256) bnorm_bwd_k(const float* __restrict__ x,
       }
     } else {
       for (int p = threadIdx.x; p < HW; p += 256) {
-        float g = dy[base + p];
-        if (kGate && !(gate[base + p] > 0.f)) g = 0.f;
+        const float g = eff_dy1<G>(dy[base + p], x[base + p], gate, base + p, P);
         const float r = bn_dx(x[base + p], g, mu, inv, winv, mdy, mdyx);
         dx[base + p] = kAcc ? __fadd_rn(dx[base + p], r) : r;
       }
@@ -2001,18 +2035,22 @@ static int bnorm_vec(const void* a, const void* b, const void* c, int HW) {
 }
 
 void bnorm_stats(const float* x, const float* dy, double* partial, double* out, int HW, int C,
-                 int N, int splits, cudaStream_t s, const float* gate) {
+                 int N, int splits, cudaStream_t s, const float* gate, const BnGate& rg) {
   dim3 grid(C, splits);
   count_launch(2);
   const int vec = bnorm_vec(x, dy, gate, HW);
-  if (dy && gate)
-    bnorm_stats_k<true, true><<<grid, 256, 0, s>>>(x, dy, gate, partial, HW, C, N, splits, vec);
+  if (dy && rg.muinv)
+    bnorm_stats_k<true, 2><<<grid, 256, 0, s>>>(x, dy, nullptr, rg.w, rg.b, rg.muinv, partial, HW,
+                                                C, N, splits, vec);
+  else if (dy && gate)
+    bnorm_stats_k<true, 1><<<grid, 256, 0, s>>>(x, dy, gate, nullptr, nullptr, nullptr, partial,
+                                                HW, C, N, splits, vec);
   else if (dy)
-    bnorm_stats_k<true, false><<<grid, 256, 0, s>>>(x, dy, nullptr, partial, HW, C, N, splits,
-                                                    vec);
+    bnorm_stats_k<true, 0><<<grid, 256, 0, s>>>(x, dy, nullptr, nullptr, nullptr, nullptr, partial,
+                                                HW, C, N, splits, vec);
   else
-    bnorm_stats_k<false, false><<<grid, 256, 0, s>>>(x, nullptr, nullptr, partial, HW, C, N,
-                                                     splits, vec);
+    bnorm_stats_k<false, 0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                 partial, HW, C, N, splits, vec);
   bnorm_finish_k<<<(C + 127) / 128, 128, 0, s>>>(partial, out, C, splits);
 }
 
@@ -2025,26 +2063,32 @@ static int bnorm_grid_y(int C, int N) {
 
 void bnorm_apply(const float* x, const float* w, const float* b, const double* stats,
                  const float* fixed_moments, float* y, float* moments_out, double eps, int HW,
-                 int C, int N, cudaStream_t s, float* y2) {
+                 int C, int N, cudaStream_t s, float* y2, float* muinv_out) {
   count_launch();
   bnorm_apply_k<<<dim3(C, bnorm_grid_y(C, N)), 256, 0, s>>>(
-      x, w, b, stats, fixed_moments, y, y2, moments_out, eps, HW, C, N,
+      x, w, b, stats, fixed_moments, y, y2, moments_out, muinv_out, eps, HW, C, N,
       bnorm_vec(x, y, y2, HW));
 }
 
 void bnorm_backward_apply(const float* x, const float* dy, const float* w, const double* stats,
                           double eps, float* dx, float* dw, float* db, int HW, int C, int N,
-                          int acc, cudaStream_t s, const float* gate) {
+                          int acc, cudaStream_t s, const float* gate, const BnGate& rg) {
   count_launch();
   const dim3 grid(C, bnorm_grid_y(C, N));
   const int vec = bnorm_vec(x, dy, gate, HW) && bnorm_vec(dx, dx, dx, HW);
 #define CK_BNB(A, G)                                                                        \
-  bnorm_bwd_k<A, G><<<grid, 256, 0, s>>>(x, dy, gate, w, stats, eps, dx, dw, db, HW, C, N,  \
-                                         acc ? 1 : 0, vec)
-  if (acc && gate) CK_BNB(true, true);
-  else if (acc) CK_BNB(true, false);
-  else if (gate) CK_BNB(false, true);
-  else CK_BNB(false, false);
+  bnorm_bwd_k<A, G><<<grid, 256, 0, s>>>(x, dy, gate, rg.b, rg.muinv, w, stats, eps, dx, dw,  \
+                                         db, HW, C, N, acc ? 1 : 0, vec)
+  const int G = rg.muinv ? 2 : gate ? 1 : 0;
+  if (acc) {
+    if (G == 2) CK_BNB(true, 2);
+    else if (G == 1) CK_BNB(true, 1);
+    else CK_BNB(true, 0);
+  } else {
+    if (G == 2) CK_BNB(false, 2);
+    else if (G == 1) CK_BNB(false, 1);
+    else CK_BNB(false, 0);
+  }
 #undef CK_BNB
 }
 
