@@ -872,7 +872,7 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
   const float c2ab = __fmul_rn(__fmul_rn(2.f, alpha), beta);
   const int lane = threadIdx.x & 31, warp_in_block = threadIdx.x >> 5;
   __shared__ float gsm[GRID ? 4 : 1][32][33];  // GRID: per-warp [pixel][channel] stage
-  __shared__ int64_t grs[GRID ? 4 : 1][32];     // GRID: per-warp pixel grid row offsets
+  __shared__ int grs[GRID ? 4 : 1][32];  // GRID: per-warp pixel grid row offsets (< 2^31)
   // GRID: whole warps walk the pixels together (the bias partials are warp
   // sums); lanes past the end repeat the last pixel and store nothing
   for (int64_t eb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - (GRID ? lane : 0);
@@ -887,7 +887,7 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
       const int i = p % go.H, jj = p / go.H;
       grow0 = ((int64_t)n * go.Hg * go.Wg + i + (int64_t)go.Hg * jj) * go.Cp;
       __syncwarp();  // the previous pixel group's flushes are done with grs
-      grs[warp_in_block][lane] = live ? grow0 : -1;
+      grs[warp_in_block][lane] = live ? (int)grow0 : -1;
       __syncwarp();
     }
     const int64_t base = n * C * HW + p;
@@ -913,6 +913,13 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
     float* dq = dx + base - (int64_t)DOWN * HW;  // store address of step j (d = j - DOWN)
     float eta[NW];  // eta of indices j-NW+1 .. j (0 outside [0, C))
     float Ls[DOWN + 1], xs[DOWN + 1], gs[DOWN + 1];  // L^-beta, x, dy of j-DOWN .. j
+    // running window sums (sq over the lead window, eta over its window):
+    // one add and one subtract per step instead of NW adds.  They differ from
+    // the reference's fresh sums by rounding only, and only inside kappa +
+    // alpha * sum and the alpha-scaled correction term (alpha ~ 1e-4).
+    float sqsum = 0.f, etasum = 0.f;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) sqsum = __fadd_rn(sqsum, sq[i]);
 #pragma unroll
     for (int i = 0; i < NW; ++i) eta[i] = 0.f;
 #pragma unroll
@@ -921,15 +928,13 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
     auto step = [&](int j, float xlead, float gj_in, bool compute, bool store, int slot) {
       float L = 0.f, xj = 0.f, gj = 0.f, et = 0.f;
       if (compute) {
-        float acc = 0.f;
-#pragma unroll
-        for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
-        const float Lj = __fadd_rn(kappa, __fmul_rn(alpha, acc));
+        const float Lj = __fadd_rn(kappa, __fmul_rn(alpha, sqsum));
         L = __powf(Lj, nb);  // L^-beta; L^(-beta-1) = L^-beta / L
         xj = xw[DOWN];
         gj = gj_in;
         et = __fmul_rn(__fmul_rn(gj, __fdividef(L, Lj)), xj);
       }
+      etasum = __fadd_rn(__fsub_rn(etasum, eta[0]), et);
 #pragma unroll
       for (int i = 0; i < NW - 1; ++i) eta[i] = eta[i + 1];
       eta[NW - 1] = et;
@@ -943,12 +948,9 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
       xs[DOWN] = xj;
       gs[DOWN] = gj;
       if (store) {
-        // k in [d-UP, d+DOWN] = [j-NW+1, j]: the whole eta window, ascending
-        float acc = 0.f;
-#pragma unroll
-        for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, eta[i]);
+        // k in [d-UP, d+DOWN] = [j-NW+1, j]: the whole eta window (etasum)
         const float r = __fadd_rn(__fmul_rn(gs[0], Ls[0]),
-                                  -__fmul_rn(__fmul_rn(c2ab, xs[0]), acc));
+                                  -__fmul_rn(__fmul_rn(c2ab, xs[0]), etasum));
         if (GRID) {
           // staged per warp as [pixel][channel mod 32]; every 32 channels the warp
           // writes each of its pixels' 128-byte channel run with one coalesced store
@@ -967,7 +969,7 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
             float t = 0.f;  // 32-pixel partial in float; partials summed in double
 #pragma unroll 8
             for (int q = 0; q < 32; ++q) {
-              const int64_t rq = grs[warp_in_block][q];  // -1: lane q has no pixel
+              const int rq = grs[warp_in_block][q];  // -1: lane q has no pixel
               const float vq = gsm[warp_in_block][q][lane];
               t += vq;
               if (rq >= 0) gb[rq] = vq;
@@ -981,13 +983,15 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
         }
       }
       // advance the x window to lead index j + 1
+      const float sqin = __fmul_rn(xlead, xlead);
+      sqsum = __fadd_rn(__fsub_rn(sqsum, sq[0]), sqin);
 #pragma unroll
       for (int i = 0; i < NW - 1; ++i) {
         xw[i] = xw[i + 1];
         sq[i] = sq[i + 1];
       }
       xw[NW - 1] = xlead;
-      sq[NW - 1] = __fmul_rn(xlead, xlead);
+      sq[NW - 1] = sqin;
       (void)j;
     };
     const int J = C + DOWN;  // steps
@@ -2001,6 +2005,8 @@ bool lrn_backward_grid(const float* x, const float* dy, float* grid, double* bpa
   const int64_t pixels = (int64_t)HW * N;
   // 32-channel runs never cross a group (and every run completes)
   if (H > Hg || W > Wg || Kg * groups != C || Kg % 32 || C % 32) return false;
+  // grid row offsets are kept as 32-bit ints in the kernel
+  if ((int64_t)N * Hg * Wg * Kgp * groups >= (1ll << 31)) return false;
   LrnGridOut go{grid, bpart, H, Hg, Wg, Kg, Kgp, Kgp * groups};
   const dim3 grid_dim(blocks_for(pixels, 128, 32));
   switch (size) {
