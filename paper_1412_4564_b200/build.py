@@ -72,7 +72,15 @@ def build(verbose: bool = False, force: bool = False, lib: str = LIB, build_dir:
 
 
 if __name__ == "__main__":
-    if "--experiments" in sys.argv:  # tools/: A/B against the measured-slower kernels
+    if "--no-pdl" in sys.argv:  # tools/ab_step.py: A/B of programmatic dependent launch
+        print(build(verbose="-v" in sys.argv, force=True,
+                    lib=os.path.join(BUILD + "_nopdl", "libck_nopdl.so"),
+                    build_dir=BUILD + "_nopdl", extra=("-DCK_NO_PDL",)))
+    elif "--pdl-early" in sys.argv:  # tools/ab_step.py: trigger dependents at kernel entry
+        print(build(verbose="-v" in sys.argv, force=True,
+                    lib=os.path.join(BUILD + "_pdlearly", "libck_pdlearly.so"),
+                    build_dir=BUILD + "_pdlearly", extra=("-DCK_PDL_EARLY_TRIGGER",)))
+    elif "--experiments" in sys.argv:  # tools/: A/B against the measured-slower kernels
         print(build(verbose="-v" in sys.argv, force=True,
                     lib=os.path.join(BUILD + "_exp", "libck_exp.so"), build_dir=BUILD + "_exp",
                     extra=("-DCK_EXPERIMENTS",)))

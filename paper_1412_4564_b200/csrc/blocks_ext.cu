@@ -57,6 +57,7 @@ __device__ __forceinline__ float warp_sum_f(float v) {
 // ------------------------------------------------------------- sigmoid ----
 // activation.cpp:25-38: split on the sign so the exponential never overflows.
 __global__ void sigmoid_fwd_k(const float* __restrict__ x, float* __restrict__ y, int64_t n) {
+  ck::pdl_entry();
   GRID_STRIDE(k, n) {
     const float v = x[k];
     float r;
@@ -74,6 +75,7 @@ __global__ void sigmoid_fwd_k(const float* __restrict__ x, float* __restrict__ y
 template <bool kAcc>
 __global__ void sigmoid_bwd_k(const float* __restrict__ y, const float* __restrict__ dy, float* dx,
                               int64_t n) {
+  ck::pdl_entry();
   GRID_STRIDE(k, n) {
     const float yv = y[k];
     const float r = __fmul_rn(__fmul_rn(dy[k], yv), __fsub_rn(1.f, yv));
@@ -86,6 +88,7 @@ __global__ void sigmoid_bwd_k(const float* __restrict__ y, const float* __restri
 // One thread per site (HW >= 32): the channel loops walk planes HW apart.
 __global__ void softmax_fwd_thread_k(const float* __restrict__ x, float* __restrict__ y, int HW,
                                      int C, int64_t sites) {
+  ck::pdl_entry();
   GRID_STRIDE(s, sites) {
     const int64_t n = s / HW, p = s % HW;
     const float* xs = x + n * (int64_t)C * HW + p;
@@ -105,6 +108,7 @@ __global__ void softmax_fwd_thread_k(const float* __restrict__ x, float* __restr
 // One warp per site (few sites, e.g. H = W = 1): lanes split the channels.
 __global__ void softmax_fwd_warp_k(const float* __restrict__ x, float* __restrict__ y, int HW,
                                    int C, int64_t sites) {
+  ck::pdl_entry();
   const int lane = threadIdx.x % 32;
   for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
        s += (int64_t)gridDim.x * blockDim.x / 32) {
@@ -130,6 +134,7 @@ __global__ void softmax_fwd_warp_k(const float* __restrict__ x, float* __restric
 template <bool kAcc>
 __global__ void softmax_bwd_thread_k(const float* __restrict__ y, const float* __restrict__ dy,
                                      float* dx, int HW, int C, int64_t sites) {
+  ck::pdl_entry();
   GRID_STRIDE(s, sites) {
     const int64_t n = s / HW, p = s % HW;
     const int64_t o = n * (int64_t)C * HW + p;
@@ -147,6 +152,7 @@ __global__ void softmax_bwd_thread_k(const float* __restrict__ y, const float* _
 template <bool kAcc>
 __global__ void softmax_bwd_warp_k(const float* __restrict__ y, const float* __restrict__ dy,
                                    float* dx, int HW, int C, int64_t sites) {
+  ck::pdl_entry();
   const int lane = threadIdx.x % 32;
   for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
        s += (int64_t)gridDim.x * blockDim.x / 32) {
@@ -185,6 +191,7 @@ __device__ __forceinline__ float spnorm_energy(const float* __restrict__ xp, int
 __global__ void spnorm_fwd_k(const float* __restrict__ x, float* __restrict__ y, int H, int W,
                              int64_t planes, int wh, int ww, int pt, int pl, float alpha,
                              float beta) {
+  ck::pdl_entry();
   const int64_t n = (int64_t)H * W * planes;
   GRID_STRIDE(k, n) {
     const int64_t pl_ = k / ((int64_t)H * W);
@@ -201,6 +208,7 @@ __global__ void spnorm_bwd1_k(const float* __restrict__ x, const float* __restri
                               float* __restrict__ share, float* __restrict__ P, int H, int W,
                               int64_t planes, int wh, int ww, int pt, int pl, float alpha,
                               float beta) {
+  ck::pdl_entry();
   const int64_t n = (int64_t)H * W * planes;
   GRID_STRIDE(k, n) {
     const int64_t pl_ = k / ((int64_t)H * W);
@@ -223,6 +231,7 @@ __global__ void spnorm_bwd2_k(const float* __restrict__ x, const float* __restri
                               const float* __restrict__ share, const float* __restrict__ P,
                               float* dx, int H, int W, int64_t planes, int wh, int ww, int pt,
                               int pl, float c2ab) {
+  ck::pdl_entry();
   const int64_t n = (int64_t)H * W * planes;
   GRID_STRIDE(k, n) {
     const int64_t pl_ = k / ((int64_t)H * W);
@@ -272,6 +281,7 @@ __device__ __forceinline__ Tent tent_at(float v, int extent) {
 __global__ void bilinear_fwd_k(const float* __restrict__ x, const float* __restrict__ grid,
                                float* __restrict__ y, int H, int W, int C, int OH, int OW,
                                int64_t n_out, float av, float au) {
+  ck::pdl_entry();
   GRID_STRIDE(e, n_out) {
     const int oi = (int)(e % OH);
     int64_t t = e / OH;
@@ -306,6 +316,7 @@ template <bool kAcc>
 __global__ void bilinear_bwd_k(const float* __restrict__ x, const float* __restrict__ grid,
                                const float* __restrict__ dy, float* dx, float* dgrid, int H,
                                int W, int C, int OH, int OW, int64_t sites, float av, float au) {
+  ck::pdl_entry();
   GRID_STRIDE(s, sites) {
     const int oi = (int)(s % OH);
     const int64_t t = s / OH;
@@ -362,6 +373,7 @@ __device__ __forceinline__ float pdist_site(const float* __restrict__ x,
 __global__ void pdist_fwd_k(const float* __restrict__ x, const float* __restrict__ t,
                             float* __restrict__ y, int HW, int C, int64_t sites, int pk, float tp,
                             float inv_p, int no_root) {
+  ck::pdl_entry();
   GRID_STRIDE(s, sites) {
     const int64_t n = s / HW, p = s % HW;
     const float acc = pdist_site(x, t, n * (int64_t)C * HW + p, HW, C, pk, tp);
@@ -374,6 +386,7 @@ template <bool kAcc>
 __global__ void pdist_bwd_k(const float* __restrict__ x, const float* __restrict__ t,
                             const float* __restrict__ dy, float* dx, float* dt, int HW, int C,
                             int64_t sites, int pk, float tp, float inv_p, int no_root) {
+  ck::pdl_entry();
   GRID_STRIDE(s, sites) {
     const int64_t n = s / HW, p = s % HW;
     const int64_t o = n * (int64_t)C * HW + p;
@@ -469,6 +482,7 @@ struct LossOpts {
 __global__ void cls_loss_fwd_k(const float* __restrict__ x, const float* __restrict__ labels,
                                const float* __restrict__ weights, float* site, int* flag, int H,
                                int W, int C, int64_t sites, int kind, LossOpts o) {
+  ck::pdl_entry();
   const int HW = H * W;
   GRID_STRIDE(s, sites) {
     const int64_t n = s / HW, pix = s % HW;
@@ -546,6 +560,7 @@ __global__ void cls_loss_fwd_k(const float* __restrict__ x, const float* __restr
 __global__ void attr_loss_fwd_k(const float* __restrict__ x, const float* __restrict__ labels,
                                 const float* __restrict__ weights, float* site, int* flag,
                                 int64_t n, int kind, float threshold) {
+  ck::pdl_entry();
   GRID_STRIDE(k, n) {
     const int c = attr_label(labels[k], flag);
     float l = 0.f;
@@ -583,6 +598,7 @@ __global__ void attr_loss_fwd_k(const float* __restrict__ x, const float* __rest
 
 // Deterministic fixed-order sum of per-site values, in double (one block).
 __global__ void sum_values_k(const float* __restrict__ v, int64_t n, float* out) {
+  ck::pdl_entry();
   __shared__ double red[32];
   double a = 0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += v[i];
@@ -604,6 +620,7 @@ __global__ void cls_loss_bwd_k(const float* __restrict__ x, const float* __restr
                                const float* __restrict__ weights, float pscale,
                                const float* __restrict__ pdev, float* dx, int* flag, int HW, int C,
                                int64_t sites, int kind) {
+  ck::pdl_entry();
   if (pdev) pscale = *pdev;
   GRID_STRIDE(s, sites) {
     const int64_t n = s / HW, pix = s % HW;
@@ -655,6 +672,7 @@ __global__ void attr_loss_bwd_k(const float* __restrict__ x, const float* __rest
                                 const float* __restrict__ weights, float pscale,
                                 const float* __restrict__ pdev, float* dx, int* flag, int64_t n,
                                 int kind) {
+  ck::pdl_entry();
   if (pdev) pscale = *pdev;
   GRID_STRIDE(k, n) {
     const int c = attr_label(labels[k], flag);
@@ -701,6 +719,7 @@ struct SumSrcs {
 };
 template <bool kAcc>
 __global__ void sum_into_k(float* dx, SumSrcs srcs, int m, int64_t n) {
+  ck::pdl_entry();
   GRID_STRIDE(i, n) {
     float a = 0.f;
     for (int k = 0; k < m; ++k) a = __fadd_rn(a, srcs.p[k][i]);
@@ -715,7 +734,7 @@ __global__ void sum_into_k(float* dx, SumSrcs srcs, int m, int64_t n) {
 void sigmoid_forward(const float* x, float* y, int64_t n, cudaStream_t s) {
   if (n == 0) return;
   count_launch();
-  sigmoid_fwd_k<<<grid_for(n, 256), 256, 0, s>>>(x, y, n);
+  ck::pdl_launch(sigmoid_fwd_k, grid_for(n, 256), 256, 0, s, x, y, n);
 }
 
 void sigmoid_backward(const float* y, const float* dy, float* dx, int64_t n, int acc,
@@ -723,9 +742,9 @@ void sigmoid_backward(const float* y, const float* dy, float* dx, int64_t n, int
   if (n == 0) return;
   count_launch();
   if (acc)
-    sigmoid_bwd_k<true><<<grid_for(n, 256), 256, 0, s>>>(y, dy, dx, n);
+    ck::pdl_launch(sigmoid_bwd_k<true>, grid_for(n, 256), 256, 0, s, y, dy, dx, n);
   else
-    sigmoid_bwd_k<false><<<grid_for(n, 256), 256, 0, s>>>(y, dy, dx, n);
+    ck::pdl_launch(sigmoid_bwd_k<false>, grid_for(n, 256), 256, 0, s, y, dy, dx, n);
 }
 
 void softmax_forward(const float* x, float* y, int HW, int C, int N, cudaStream_t s) {
@@ -733,9 +752,9 @@ void softmax_forward(const float* x, float* y, int HW, int C, int N, cudaStream_
   if (!sites) return;
   count_launch();
   if (HW >= 32)
-    softmax_fwd_thread_k<<<grid_for(sites, 128), 128, 0, s>>>(x, y, HW, C, sites);
+    ck::pdl_launch(softmax_fwd_thread_k, grid_for(sites, 128), 128, 0, s, x, y, HW, C, sites);
   else
-    softmax_fwd_warp_k<<<grid_for(sites * 32, 256), 256, 0, s>>>(x, y, HW, C, sites);
+    ck::pdl_launch(softmax_fwd_warp_k, grid_for(sites * 32, 256), 256, 0, s, x, y, HW, C, sites);
 }
 
 void softmax_backward(const float* y, const float* dy, float* dx, int HW, int C, int N, int acc,
@@ -745,14 +764,14 @@ void softmax_backward(const float* y, const float* dy, float* dx, int HW, int C,
   count_launch();
   if (HW >= 32) {
     if (acc)
-      softmax_bwd_thread_k<true><<<grid_for(sites, 128), 128, 0, s>>>(y, dy, dx, HW, C, sites);
+      ck::pdl_launch(softmax_bwd_thread_k<true>, grid_for(sites, 128), 128, 0, s, y, dy, dx, HW, C, sites);
     else
-      softmax_bwd_thread_k<false><<<grid_for(sites, 128), 128, 0, s>>>(y, dy, dx, HW, C, sites);
+      ck::pdl_launch(softmax_bwd_thread_k<false>, grid_for(sites, 128), 128, 0, s, y, dy, dx, HW, C, sites);
   } else {
     if (acc)
-      softmax_bwd_warp_k<true><<<grid_for(sites * 32, 256), 256, 0, s>>>(y, dy, dx, HW, C, sites);
+      ck::pdl_launch(softmax_bwd_warp_k<true>, grid_for(sites * 32, 256), 256, 0, s, y, dy, dx, HW, C, sites);
     else
-      softmax_bwd_warp_k<false><<<grid_for(sites * 32, 256), 256, 0, s>>>(y, dy, dx, HW, C, sites);
+      ck::pdl_launch(softmax_bwd_warp_k<false>, grid_for(sites * 32, 256), 256, 0, s, y, dy, dx, HW, C, sites);
   }
 }
 
@@ -761,7 +780,7 @@ void spnorm_forward(const float* x, float* y, int H, int W, int64_t planes, int 
   const int64_t n = (int64_t)H * W * planes;
   if (!n) return;
   count_launch();
-  spnorm_fwd_k<<<grid_for(n, 256), 256, 0, s>>>(x, y, H, W, planes, wh, ww, (wh - 1) / 2,
+  ck::pdl_launch(spnorm_fwd_k, grid_for(n, 256), 256, 0, s, x, y, H, W, planes, wh, ww, (wh - 1) / 2,
                                                 (ww - 1) / 2, alpha, beta);
 }
 
@@ -774,13 +793,13 @@ void spnorm_backward(const float* x, const float* dy, float* dx, float* ws, int 
   float* share = ws;
   float* P = ws + n;
   const int pt = (wh - 1) / 2, pl = (ww - 1) / 2;
-  spnorm_bwd1_k<<<grid_for(n, 256), 256, 0, s>>>(x, dy, share, P, H, W, planes, wh, ww, pt, pl,
+  ck::pdl_launch(spnorm_bwd1_k, grid_for(n, 256), 256, 0, s, x, dy, share, P, H, W, planes, wh, ww, pt, pl,
                                                  alpha, beta);
   if (acc)
-    spnorm_bwd2_k<true><<<grid_for(n, 256), 256, 0, s>>>(x, dy, share, P, dx, H, W, planes, wh,
+    ck::pdl_launch(spnorm_bwd2_k<true>, grid_for(n, 256), 256, 0, s, x, dy, share, P, dx, H, W, planes, wh,
                                                          ww, pt, pl, c2ab);
   else
-    spnorm_bwd2_k<false><<<grid_for(n, 256), 256, 0, s>>>(x, dy, share, P, dx, H, W, planes, wh,
+    ck::pdl_launch(spnorm_bwd2_k<false>, grid_for(n, 256), 256, 0, s, x, dy, share, P, dx, H, W, planes, wh,
                                                           ww, pt, pl, c2ab);
 }
 
@@ -789,7 +808,7 @@ void bilinear_forward(const float* x, const float* grid, float* y, int H, int W,
   const int64_t n = (int64_t)OH * OW * C * N;
   if (!n) return;
   count_launch();
-  bilinear_fwd_k<<<grid_for(n, 256), 256, 0, s>>>(x, grid, y, H, W, C, OH, OW, n,
+  ck::pdl_launch(bilinear_fwd_k, grid_for(n, 256), 256, 0, s, x, grid, y, H, W, C, OH, OW, n,
                                                   (float)(H - 1) / 2.f, (float)(W - 1) / 2.f);
 }
 
@@ -803,10 +822,10 @@ void bilinear_backward(const float* x, const float* grid, const float* dy, float
   count_launch();
   const float av = (float)(H - 1) / 2.f, au = (float)(W - 1) / 2.f;
   if (acc)
-    bilinear_bwd_k<true><<<grid_for(sites, 128), 128, 0, s>>>(x, grid, dy, dx, dgrid, H, W, C, OH,
+    ck::pdl_launch(bilinear_bwd_k<true>, grid_for(sites, 128), 128, 0, s, x, grid, dy, dx, dgrid, H, W, C, OH,
                                                               OW, sites, av, au);
   else
-    bilinear_bwd_k<false><<<grid_for(sites, 128), 128, 0, s>>>(x, grid, dy, dx, dgrid, H, W, C, OH,
+    ck::pdl_launch(bilinear_bwd_k<false>, grid_for(sites, 128), 128, 0, s, x, grid, dy, dx, dgrid, H, W, C, OH,
                                                                OW, sites, av, au);
 }
 
@@ -818,7 +837,7 @@ void pdist_forward(const float* x, const float* t, float* y, int HW, int C, int 
   if (!sites) return;
   count_launch();
   const float tp = (float)p;
-  pdist_fwd_k<<<grid_for(sites, 128), 128, 0, s>>>(x, t, y, HW, C, sites, pdist_kind(p), tp,
+  ck::pdl_launch(pdist_fwd_k, grid_for(sites, 128), 128, 0, s, x, t, y, HW, C, sites, pdist_kind(p), tp,
                                                    1.f / tp, no_root);
 }
 
@@ -829,10 +848,10 @@ void pdist_backward(const float* x, const float* t, const float* dy, float* dx, 
   count_launch();
   const float tp = (float)p;
   if (acc)
-    pdist_bwd_k<true><<<grid_for(sites, 128), 128, 0, s>>>(x, t, dy, dx, dt, HW, C, sites,
+    ck::pdl_launch(pdist_bwd_k<true>, grid_for(sites, 128), 128, 0, s, x, t, dy, dx, dt, HW, C, sites,
                                                            pdist_kind(p), tp, 1.f / tp, no_root);
   else
-    pdist_bwd_k<false><<<grid_for(sites, 128), 128, 0, s>>>(x, t, dy, dx, dt, HW, C, sites,
+    ck::pdl_launch(pdist_bwd_k<false>, grid_for(sites, 128), 128, 0, s, x, t, dy, dx, dt, HW, C, sites,
                                                             pdist_kind(p), tp, 1.f / tp, no_root);
 }
 
@@ -848,14 +867,14 @@ void loss_forward_kind(const float* x, const float* labels, const float* weights
   int64_t n;
   if (attribute_kind(kind)) {
     n = (int64_t)H * W * C * N;
-    attr_loss_fwd_k<<<grid_for(n, 256), 256, 0, s>>>(x, labels, weights, site, flag, n, kind,
+    ck::pdl_launch(attr_loss_fwd_k, grid_for(n, 256), 256, 0, s, x, labels, weights, site, flag, n, kind,
                                                      o.threshold);
   } else {
     n = (int64_t)H * W * N;
-    cls_loss_fwd_k<<<grid_for(n, 128), 128, 0, s>>>(x, labels, weights, site, flag, H, W, C, n,
+    ck::pdl_launch(cls_loss_fwd_k, grid_for(n, 128), 128, 0, s, x, labels, weights, site, flag, H, W, C, n,
                                                     kind, o);
   }
-  sum_values_k<<<1, 1024, 0, s>>>(site, n, loss);
+  ck::pdl_launch(sum_values_k, 1, 1024, 0, s, site, n, loss);
 }
 
 void loss_backward_kind(const float* x, const float* labels, const float* weights, int kind,
@@ -870,18 +889,18 @@ void loss_backward_kind(const float* x, const float* labels, const float* weight
   count_launch();
   if (attribute_kind(kind)) {
     if (acc)
-      attr_loss_bwd_k<true><<<grid_for(total, 256), 256, 0, s>>>(x, labels, weights, p, p_dev, dx,
+      ck::pdl_launch(attr_loss_bwd_k<true>, grid_for(total, 256), 256, 0, s, x, labels, weights, p, p_dev, dx,
                                                                  flag, total, kind);
     else
-      attr_loss_bwd_k<false><<<grid_for(total, 256), 256, 0, s>>>(x, labels, weights, p, p_dev,
+      ck::pdl_launch(attr_loss_bwd_k<false>, grid_for(total, 256), 256, 0, s, x, labels, weights, p, p_dev,
                                                                   dx, flag, total, kind);
   } else {
     const int64_t sites = (int64_t)H * W * N;
     if (acc)
-      cls_loss_bwd_k<true><<<grid_for(sites, 128), 128, 0, s>>>(x, labels, weights, p, p_dev, dx,
+      ck::pdl_launch(cls_loss_bwd_k<true>, grid_for(sites, 128), 128, 0, s, x, labels, weights, p, p_dev, dx,
                                                                  flag, H * W, C, sites, kind);
     else
-      cls_loss_bwd_k<false><<<grid_for(sites, 128), 128, 0, s>>>(x, labels, weights, p, p_dev, dx,
+      ck::pdl_launch(cls_loss_bwd_k<false>, grid_for(sites, 128), 128, 0, s, x, labels, weights, p, p_dev, dx,
                                                                   flag, H * W, C, sites, kind);
   }
 }
@@ -893,9 +912,9 @@ void sum_into(float* dx, const float* const* srcs, int m, int64_t n, int acc, cu
   for (int k = 0; k < m; ++k) a.p[k] = srcs[k];
   count_launch();
   if (acc)
-    sum_into_k<true><<<grid_for(n, 256), 256, 0, s>>>(dx, a, m, n);
+    ck::pdl_launch(sum_into_k<true>, grid_for(n, 256), 256, 0, s, dx, a, m, n);
   else
-    sum_into_k<false><<<grid_for(n, 256), 256, 0, s>>>(dx, a, m, n);
+    ck::pdl_launch(sum_into_k<false>, grid_for(n, 256), 256, 0, s, dx, a, m, n);
 }
 
 }  // namespace ck

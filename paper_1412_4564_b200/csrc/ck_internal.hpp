@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "ck/ck.h"
@@ -40,6 +41,44 @@ struct PoolDims {
 // them), so the trainer re-captures when the generation it captured under
 // is no longer current.
 uint64_t workspace_generation();
+
+#ifdef __CUDACC__
+// Programmatic dependent launch (PDL).  Every kernel of the library starts
+// with pdl_entry(): it lets the next kernel in the stream be scheduled now
+// (griddepcontrol.launch_dependents) and waits until every kernel it depends
+// on has completed and its writes are visible (griddepcontrol.wait) -- so a
+// kernel launched with the programmatic-serialization attribute (pdl_launch)
+// may start, and get its CTAs resident, while its predecessor drains, without
+// ever reading that predecessor's output early.  Inside a captured CUDA graph
+// these become programmatic edges: the ~100 dependent launches of a training
+// step no longer each pay the full launch latency.
+__device__ __forceinline__ void pdl_entry() {
+#ifdef CK_PDL_EARLY_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+#ifndef CK_NO_PDL
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#else
+  (void)attr;
+#endif
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#endif
 
 // Tuning / experiment knobs (CK_* environment variables).  Product builds
 // ignore the environment and return dflt; only a -DCK_EXPERIMENTS build reads

@@ -223,6 +223,7 @@ struct FcDgradProb {
 
 template <class P, bool kSplit>
 __global__ void __launch_bounds__(NT) simt_gemm_k(P p, int splits, int acc) {
+  ck::pdl_entry();
   __shared__ float As[2][BK][BM];
   __shared__ float Bs[2][BK][BN];
   const int tid = threadIdx.x;
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(NT) simt_gemm_k(P p, int splits, int acc) {
 // df[fi, fj, c, k] (+)= sum_s part[s][g][k][(c,fj,fi)], in split order.
 __global__ void wgrad_reduce_k(const float* __restrict__ part, float* df, ConvDims d, int splits,
                                int acc) {
+  ck::pdl_entry();
   const int64_t rows = (int64_t)d.fh * d.fw * d.Cg, cols = d.Kg();
   const int64_t per = rows * cols * d.groups;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per;
@@ -322,6 +324,7 @@ __global__ void wgrad_reduce_k(const float* __restrict__ part, float* df, ConvDi
 // four images in flight; bgrad_finish_k then reduces the S*OHW partials of
 // channel k in a fixed order (deterministic, double accumulation).
 __global__ void bgrad_part_k(const float* __restrict__ dy, double* part, int64_t KP, int N) {
+  ck::pdl_entry();
   const int s = blockIdx.y, S = gridDim.y;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < KP;
        j += (int64_t)gridDim.x * blockDim.x) {
@@ -339,6 +342,7 @@ __global__ void bgrad_part_k(const float* __restrict__ dy, double* part, int64_t
 }
 
 __global__ void bgrad_finish_k(const double* part, float* db, int K, int OHW, int S, int acc) {
+  ck::pdl_entry();
   const int k = blockIdx.x;
   const int64_t KP = (int64_t)K * OHW;
   double t = 0;
@@ -364,6 +368,7 @@ __global__ void bgrad_finish_k(const double* part, float* db, int K, int OHW, in
 template <bool kAcc>
 __global__ void dgrad_strided_k(const float* __restrict__ dy, const float* __restrict__ f,
                                 float* dx, ConvDims d) {
+  ck::pdl_entry();
   const int64_t total = (int64_t)d.H * d.W * d.C * d.N;
   const int Kg = d.Kg();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -422,7 +427,7 @@ void conv_fwd_fp32(const float* x, const float* f, const float* bias, float* y,
   int64_t M = (int64_t)d.N * d.OH * d.OW;
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((d.Kg() + BN - 1) / BN), d.groups);
   count_launch();
-  simt_gemm_k<FpropProb, false><<<grid, NT, 0, s>>>(p, 1, 0);
+  ck::pdl_launch(simt_gemm_k<FpropProb, false>, grid, NT, 0, s, p, 1, 0);
 }
 
 void conv_dgrad_fp32(const float* dy, const float* f, float* dx, const ConvDims& d, int acc,
@@ -434,7 +439,7 @@ void conv_dgrad_fp32(const float* dy, const float* f, float* dx, const ConvDims&
     int64_t Q = (int64_t)d.H * d.W * d.C;
     dim3 grid((unsigned)((Q + BM - 1) / BM), (unsigned)((d.N + BN - 1) / BN), 1);
     count_launch();
-    simt_gemm_k<FcDgradProb, false><<<grid, NT, 0, s>>>(p, 1, acc);
+    ck::pdl_launch(simt_gemm_k<FcDgradProb, false>, grid, NT, 0, s, p, 1, acc);
     return;
   }
   if (d.sh > 1 || d.sw > 1) {
@@ -442,16 +447,16 @@ void conv_dgrad_fp32(const float* dy, const float* f, float* dx, const ConvDims&
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     count_launch();
     if (acc)
-      dgrad_strided_k<true><<<blocks, 256, 0, s>>>(dy, f, dx, d);
+      ck::pdl_launch(dgrad_strided_k<true>, blocks, 256, 0, s, dy, f, dx, d);
     else
-      dgrad_strided_k<false><<<blocks, 256, 0, s>>>(dy, f, dx, d);
+      ck::pdl_launch(dgrad_strided_k<false>, blocks, 256, 0, s, dy, f, dx, d);
     return;
   }
   DgradProb p{dy, f, dx, d};
   int64_t M = (int64_t)d.N * d.H * d.W;
   dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((d.Cg + BN - 1) / BN), d.groups);
   count_launch();
-  simt_gemm_k<DgradProb, false><<<grid, NT, 0, s>>>(p, 1, acc);
+  ck::pdl_launch(simt_gemm_k<DgradProb, false>, grid, NT, 0, s, p, 1, acc);
 }
 
 size_t conv_wgrad_ws_bytes(const ConvDims& d) {
@@ -468,11 +473,11 @@ void conv_wgrad_fp32(const float* x, const float* dy, float* df, const ConvDims&
   dim3 grid((unsigned)((rows + BM - 1) / BM), (unsigned)((d.Kg() + BN - 1) / BN),
             d.groups * splits);
   count_launch(2);
-  simt_gemm_k<WgradProb, true><<<grid, NT, 0, s>>>(p, splits, 0);
+  ck::pdl_launch(simt_gemm_k<WgradProb, true>, grid, NT, 0, s, p, splits, 0);
   int64_t per = rows * d.Kg() * d.groups;
   int blocks = (int)((per + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  wgrad_reduce_k<<<blocks, 256, 0, s>>>((const float*)ws, df, d, splits, acc);
+  ck::pdl_launch(wgrad_reduce_k, blocks, 256, 0, s, (const float*)ws, df, d, splits, acc);
 }
 
 static int bgrad_splits(int64_t KP, int N) {
@@ -492,8 +497,8 @@ void conv_bgrad(const float* dy, float* db, int OHW, int K, int N, int acc, void
   const int S = bgrad_splits(KP, N);
   const int blocks = (int)std::min<int64_t>((KP + 255) / 256, 148 * 8);
   count_launch(2);
-  bgrad_part_k<<<dim3(blocks, S), 256, 0, s>>>(dy, (double*)ws, KP, N);
-  bgrad_finish_k<<<K, 256, 0, s>>>((const double*)ws, db, K, OHW, S, acc);
+  ck::pdl_launch(bgrad_part_k, dim3(blocks, S), 256, 0, s, dy, (double*)ws, KP, N);
+  ck::pdl_launch(bgrad_finish_k, K, 256, 0, s, (const double*)ws, db, K, OHW, S, acc);
 }
 
 }  // namespace ck

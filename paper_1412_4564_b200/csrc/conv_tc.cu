@@ -651,6 +651,7 @@ template <int AK, int BK>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a,
                    const __grid_constant__ CUtensorMap tma_b, const GemmParams p) {
+  ck::pdl_entry();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int S = p.stages;
@@ -972,6 +973,7 @@ template <int CS>
 __global__ void __launch_bounds__(kThreads, 1)
     halo_conv_kernel(const __grid_constant__ CUtensorMap tma_a,
                      const __grid_constant__ CUtensorMap tma_b, const GemmParams p) {
+  ck::pdl_entry();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int halves = p.BM / 128;
@@ -1175,6 +1177,7 @@ __global__ void __launch_bounds__(256, CH == 32 ? (GATE ? 6 : 8) : 4) to_grid_pm
     const float* __restrict__ x, float* __restrict__ xg, int H, int W, int C, int Cg, int Cgp,
     int groups, int Hg, int Wg, int oh, int ow, double* __restrict__ bpart,
     const float* __restrict__ gate, float* __restrict__ gout, int tpb) {
+  ck::pdl_entry();
   // tile: 64 grid pixels x CH padded channels; loads coalesced along pixels
   // (two per channel row per thread, CH/8 rows per warp), stores as float4
   // along channels.  Every load of a tile (and of the relu gate) is issued
@@ -1282,19 +1285,19 @@ static void grid_pm_launch(const float* x, float* xg, int H, int W, int C, int N
     const int ct = Cp / 64, t = tiles_per_block(ct, nb);
     dim3 grid(nb, (ct + t - 1) / t, N);
     if (gate)
-      to_grid_pm_k<64, true><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
+      ck::pdl_launch(to_grid_pm_k<64, true>, grid, 256, 0, s, x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
                                                   bpart, gate, gout, t);
     else
-      to_grid_pm_k<64, false><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
+      ck::pdl_launch(to_grid_pm_k<64, false>, grid, 256, 0, s, x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
                                                    bpart, gate, gout, t);
   } else {
     const int ct = (Cp + 31) / 32, t = tiles_per_block(ct, nb);
     dim3 grid(nb, (ct + t - 1) / t, N);
     if (gate)
-      to_grid_pm_k<32, true><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
+      ck::pdl_launch(to_grid_pm_k<32, true>, grid, 256, 0, s, x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
                                                   bpart, gate, gout, t);
     else
-      to_grid_pm_k<32, false><<<grid, 256, 0, s>>>(x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
+      ck::pdl_launch(to_grid_pm_k<32, false>, grid, 256, 0, s, x, xg, H, W, C, Cg, Cgp, groups, Hg, Wg, oh, ow,
                                                    bpart, gate, gout, t);
   }
 }
@@ -1303,6 +1306,7 @@ static void grid_pm_launch(const float* x, float* xg, int H, int W, int C, int N
 // filter bank f[fi + fh*(fj + fw*(c*fsc + k*fsk))]; zeros for channel pads.
 __global__ void repack_fprop_k(const float* __restrict__ f, float* __restrict__ ft, int fh, int fw,
                                int Cg, int Cgp, int K, int64_t fsc, int64_t fsk) {
+  ck::pdl_entry();
   // 32-bit index math (the bank is far below 2^31 elements); the caller
   // checks the 64-bit total
   const int taps = fh * fw;
@@ -1323,6 +1327,7 @@ __global__ void repack_fprop_k(const float* __restrict__ f, float* __restrict__ 
 // tap' = flipped tap: g[fi', fj', k, c] = f[fh-1-fi', fw-1-fj', c, k].
 __global__ void repack_dgrad_k(const float* __restrict__ f, float* __restrict__ gt, int fh, int fw,
                                int Cg, int Kg, int Kgp, int groups, int64_t fsc, int64_t fsk) {
+  ck::pdl_entry();
   const int taps = fh * fw;
   const int total = Cg * groups * taps * Kgp;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -1344,6 +1349,7 @@ __global__ void repack_dgrad_k(const float* __restrict__ f, float* __restrict__ 
 __global__ void wgrad_finish_k(const float* __restrict__ part, float* df, int fh, int fw, int Cg,
                                int Cgp, int Kg, int groups, int splits, int64_t split_stride,
                                int64_t fsc, int64_t fsk, int acc) {
+  ck::pdl_entry();
   const int taps = fh * fw;
   const int total = groups * Kg * taps * Cg;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -1369,6 +1375,7 @@ __global__ void splitk_finish_k(const float* __restrict__ part, float* out, int 
                                 int64_t ld, int splits, int64_t split_stride,
                                 const float* __restrict__ bias, int relu, int acc,
                                 float* __restrict__ out2) {
+  ck::pdl_entry();
   const int64_t total = (int64_t)rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -1402,6 +1409,7 @@ __device__ __forceinline__ float s2d_read(const float* x, int H, int W, int C, i
 // pixel-major s2d tensor [n][v][u][c'p] for the fprop im2col operand
 __global__ void s2d_pm_k(const float* __restrict__ x, float* __restrict__ out, int H, int W, int C,
                          int N, int s, int U, int V, int Cs, int Csp) {
+  ck::pdl_entry();
   const int64_t total = (int64_t)N * V * U * Csp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -1449,6 +1457,7 @@ __device__ __forceinline__ void s2d_stage_strip(const float* __restrict__ x, flo
 // pixel-major s2d tensor [n][v][u][c'p]; block = (v strip of VB columns, n)
 __global__ void s2d_pm_strip_k(const float* __restrict__ x, float* __restrict__ out, int H, int W,
                                int C, int s, int U, int V, int Cs, int Csp, int VB) {
+  ck::pdl_entry();
   extern __shared__ float strip_pm[];
   __shared__ int offs[256];  // s2d channel c' -> strip offset of (c, a, b), -1 = pad
   const int n = blockIdx.y, v0 = blockIdx.x * VB;
@@ -1485,6 +1494,7 @@ __global__ void s2d_pm_strip_k(const float* __restrict__ x, float* __restrict__ 
 __global__ void s2d_repack_fprop_k(const float* __restrict__ f, float* __restrict__ ft, int fh,
                                    int fw, int Cg, int K, int s, int Th, int Tw, int Csp,
                                    int64_t fsc, int64_t fsk) {
+  ck::pdl_entry();
   const int64_t total = (int64_t)K * Th * Tw * Csp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -1506,6 +1516,7 @@ __global__ void s2d_repack_fprop_k(const float* __restrict__ f, float* __restric
 __global__ void s2d_repack_dgrad_k(const float* __restrict__ f, float* __restrict__ gt, int fh,
                                    int fw, int Cg, int K, int Kp, int s, int Th, int Tw,
                                    int64_t fsc, int64_t fsk) {
+  ck::pdl_entry();
   const int Cs = s * s * Cg;
   const int64_t total = (int64_t)Cs * Th * Tw * Kp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -1529,6 +1540,7 @@ __global__ void s2d_repack_dgrad_k(const float* __restrict__ f, float* __restric
 __global__ void s2d_wgrad_finish_k(const float* __restrict__ part, float* df, int fh, int fw,
                                    int Cg, int K, int s, int Th, int Csp, int splits,
                                    int64_t split_stride, int acc, int64_t fsc, int64_t fsk) {
+  ck::pdl_entry();
   const int64_t total = (int64_t)K * fh * fw * Cg;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -1736,7 +1748,7 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
     cudaEventCreate(&rec.b);
     cudaEventRecord(rec.a, s);
   }
-  tc_gemm_kernel<AK, BK><<<grid, kThreads, smem, s>>>(a, b, p);
+  ck::pdl_launch(tc_gemm_kernel<AK, BK>, grid, kThreads, smem, s, a, b, p);
   if (mprof) {  // debug: where the MMA thread of each CTA spent its time
     unsigned long long hbuf[148 * 8 + 512];
     cudaStreamSynchronize(s);
@@ -1965,7 +1977,7 @@ static bool halo_launch(const HaloConv& hc, GemmParams p, cudaStream_t s) {
   } dump{prof ? prof_buf : nullptr, s, p.M, p.N, BN, TT, SB};
   count_launch();
   if (CS == 1) {
-    halo_conv_kernel<1><<<std::min(items, 148), kThreads, smem, s>>>(ta, tb, p);
+    ck::pdl_launch(halo_conv_kernel<1>, std::min(items, 148), kThreads, smem, s, ta, tb, p);
     return true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -2001,6 +2013,7 @@ static inline int bias_chunks(int rows) {
 }
 __global__ void grid_bias_part_k(const double* __restrict__ bpart, double* __restrict__ part2,
                                  int Cp, int rows, int rpw) {
+  ck::pdl_entry();
   __shared__ double red[8][32];
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   const int cp = blockIdx.x * 32 + lane;
@@ -2021,6 +2034,7 @@ __global__ void grid_bias_part_k(const double* __restrict__ bpart, double* __res
 
 __global__ void grid_bias_finish_k(const double* __restrict__ part2, float* db, int K, int Kg,
                                    int Kgp, int Cp, int chunks, int acc) {
+  ck::pdl_entry();
   // one warp per channel: lanes sum strided chunks, then a fixed shuffle tree
   const int cp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x & 31;
   if (cp >= Cp) return;
@@ -2060,9 +2074,9 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
       const int chunks = bias_chunks(rows);
       double* part2 = (double*)grow(st->bpart, sizeof(double) * (size_t)chunks * Cp, s);
       count_launch(2);
-      grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(h->pre_bpart, part2, Cp, rows,
+      ck::pdl_launch(grid_bias_part_k, dim3((Cp + 31) / 32, chunks), 256, 0, s, h->pre_bpart, part2, Cp, rows,
                                                                      bias_rows_per_warp(rows));
-      grid_bias_finish_k<<<(Cp * 32 + 255) / 256, 256, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp,
+      ck::pdl_launch(grid_bias_finish_k, (Cp * 32 + 255) / 256, 256, 0, s, part2, db, d.K, Kg, Kgp, Cp,
                                                                 chunks, db_acc);
     }
     return h->pre_dyg;
@@ -2079,9 +2093,9 @@ static float* dy_grid(ck_handle* h, const float* dy, const ConvDims& d, int Kg, 
     count_launch(3);
     grid_pm_launch(relu_x ? relu_dy : dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, Hg, Wg, 0,
                    0, bpart, relu_x, relu_x && !skip_gout ? const_cast<float*>(dy) : nullptr, s);
-    grid_bias_part_k<<<dim3((Cp + 31) / 32, chunks), 256, 0, s>>>(bpart, part2, Cp, rows,
+    ck::pdl_launch(grid_bias_part_k, dim3((Cp + 31) / 32, chunks), 256, 0, s, bpart, part2, Cp, rows,
                                                                    bias_rows_per_warp(rows));
-    grid_bias_finish_k<<<(Cp * 32 + 255) / 256, 256, 0, s>>>(part2, db, d.K, Kg, Kgp, Cp, chunks,
+    ck::pdl_launch(grid_bias_finish_k, (Cp * 32 + 255) / 256, 256, 0, s, part2, db, d.K, Kg, Kgp, Cp, chunks,
                                                               db_acc);
   } else {
     to_grid_pm(dy, buf, d.OH, d.OW, d.K, d.N, Kg, Kgp, groups, Hg, Wg, 0, 0, s);
@@ -2188,10 +2202,10 @@ static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, c
   const int col_bytes = (int)sizeof(float) * d.C * z.s * z.U * z.s;  // one s2d column, all c
   const int VB = std::min(z.V, (44 * 1024) / col_bytes);
   if (VB >= 1)
-    s2d_pm_strip_k<<<dim3((z.V + VB - 1) / VB, d.N), 256, (size_t)VB * col_bytes, s>>>(
+    ck::pdl_launch(s2d_pm_strip_k, dim3((z.V + VB - 1) / VB, d.N), 256, (size_t)VB * col_bytes, s, 
         x, xt, d.H, d.W, d.C, z.s, z.U, z.V, z.Cs, z.Csp, VB);
   else
-    s2d_pm_k<<<blocks_for((int64_t)d.N * z.U * z.V * z.Csp), 256, 0, s>>>(
+    ck::pdl_launch(s2d_pm_k, blocks_for((int64_t)d.N * z.U * z.V * z.Csp), 256, 0, s, 
         x, xt, d.H, d.W, d.C, d.N, z.s, z.U, z.V, z.Cs, z.Csp);
 }
 
@@ -2275,7 +2289,7 @@ static void s2d_fprop(ck_handle* h, const float* x, const float* f, const float*
   float* xt = x_s2d(h, x, d, z, s);
   float* ft = (float*)grow(st->ft, sizeof(float) * (size_t)d.K * taps * z.Csp, s);
   count_launch();
-  s2d_repack_fprop_k<<<blocks_for((int64_t)d.K * taps * z.Csp), 256, 0, s>>>(
+  ck::pdl_launch(s2d_repack_fprop_k, blocks_for((int64_t)d.K * taps * z.Csp), 256, 0, s, 
       f, ft, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Tw, z.Csp, d.fsc, d.fsk);
   if (halo_ok(d.K, z.Th, z.Tw, z.U)) {
     // the s2d pixel-major tensor is already a (pad-free) grid of pitch U
@@ -2317,6 +2331,7 @@ __global__ void __launch_bounds__(256) s2d_unpack_k(const float* __restrict__ T,
                                                     float* __restrict__ dx, int H, int W, int C,
                                                     int s, int U, int V, int64_t M, int rows,
                                                     int acc) {
+  ck::pdl_entry();
   constexpr int R = 8;  // image rows (n, c, j) per block, loads of all in flight together
   // per-row source plane base (32-bit index math, once per block row)
   __shared__ int64_t base[R];
@@ -2356,7 +2371,7 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   const int Kp = rup(d.K, 32);
   float* gt = (float*)grow(st->ft, sizeof(float) * (size_t)z.Cs * taps * Kp, s);
   count_launch();
-  s2d_repack_dgrad_k<<<blocks_for((int64_t)z.Cs * taps * Kp), 256, 0, s>>>(
+  ck::pdl_launch(s2d_repack_dgrad_k, blocks_for((int64_t)z.Cs * taps * Kp), 256, 0, s, 
       f, gt, d.fh, d.fw, d.C, d.K, Kp, z.s, z.Th, z.Tw, d.fsc, d.fsk);
   const int Hq = d.OH + 2 * (z.Th - 1), Wq = d.OW + 2 * (z.Tw - 1);
   if (halo_ok(z.Cs, z.Th, z.Tw, Hq)) {
@@ -2402,7 +2417,7 @@ static void s2d_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, 
   launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, (z.Cs + p.BN - 1) / p.BN, 1, s);
   count_launch();
   const int rows = d.N * d.C * d.W;
-  s2d_unpack_k<<<(rows + 7) / 8, d.H <= 128 ? 128 : 256, 0, s>>>(T, dx, d.H, d.W, d.C, z.s, z.U,
+  ck::pdl_launch(s2d_unpack_k, (rows + 7) / 8, d.H <= 128 ? 128 : 256, 0, s, T, dx, d.H, d.W, d.C, z.s, z.U,
                                                                 z.V, (int64_t)p.M, rows, acc);
 }
 
@@ -2481,7 +2496,7 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   const int splits = grid_wgrad(h, xt, z.Csp, z.Csp, dyg, Kp, Kp, d.K, 1, d.N, z.U, z.V, z.Th,
                                 z.Tw, &part, &per, s);
   count_launch();
-  s2d_wgrad_finish_k<<<blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s>>>(
+  ck::pdl_launch(s2d_wgrad_finish_k, blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s, 
       part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc, d.fsc, d.fsk);
 }
 
@@ -2516,7 +2531,7 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
       p.out = part; p.split_stride = per;
       launch<OP_TILED_K, OP_TILED_K>(ta, tb, p, gm, gn, splits, s);
       count_launch();
-      splitk_finish_k<<<std::min<int64_t>((per + 255) / 256, 148 * 8), 256, 0, s>>>(
+      ck::pdl_launch(splitk_finish_k, std::min<int64_t>((per + 255) / 256, 148 * 8), 256, 0, s, 
           part, y, d.K, d.N, d.K, splits, per, bias, relu, 0, h->fuse_relu);
     } else {
       p.out = y;
@@ -2538,7 +2553,7 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
   TcState* st = state(h);
   float* ft = (float*)grow(st->ft, sizeof(float) * (size_t)d.K * taps * Cgp, s);
   count_launch();
-  repack_fprop_k<<<std::min<int64_t>(((int64_t)d.K * taps * Cgp + 255) / 256, 148 * 8), 256, 0, s>>>(
+  ck::pdl_launch(repack_fprop_k, std::min<int64_t>(((int64_t)d.K * taps * Cgp + 255) / 256, 148 * 8), 256, 0, s, 
       f, ft, d.fh, d.fw, d.Cg, Cgp, d.K, d.fsc, d.fsk);
   int Hg, Wg;
   grid_dims(d, Hg, Wg);
@@ -2637,7 +2652,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
       p.out = part; p.split_stride = per;
       launch<OP_TILED_MN, OP_TILED_K>(ta, tb, p, gm, gn, splits, s);
       count_launch();
-      splitk_finish_k<<<std::min<int64_t>((per + 255) / 256, 148 * 8), 256, 0, s>>>(
+      ck::pdl_launch(splitk_finish_k, std::min<int64_t>((per + 255) / 256, 148 * 8), 256, 0, s, 
           part, dx, Q, d.N, Q, splits, per, nullptr, 0, acc, nullptr);
     } else {
       p.out = dx;
@@ -2660,7 +2675,7 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   TcState* st = state(h);
   float* gt = (float*)grow(st->ft, sizeof(float) * (size_t)d.C * taps * Kgp, s);
   count_launch();
-  repack_dgrad_k<<<std::min<int64_t>(((int64_t)d.C * taps * Kgp + 255) / 256, 148 * 8), 256, 0, s>>>(
+  ck::pdl_launch(repack_dgrad_k, std::min<int64_t>(((int64_t)d.C * taps * Kgp + 255) / 256, 148 * 8), 256, 0, s, 
       f, gt, d.fh, d.fw, d.Cg, Kg, Kgp, d.groups, d.fsc, d.fsk);
   const int qt = d.fh - 1 - d.pt, qb = d.fh - 1 - d.pb, ql = d.fw - 1 - d.pl, qr = d.fw - 1 - d.pr;
   const int Hq = d.OH + qt + qb, Wq = d.OW + ql + qr;
@@ -2818,7 +2833,7 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
                                 d.fw, &part, &per, s);
   const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
   count_launch();
-  wgrad_finish_k<<<std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s>>>(
+  ck::pdl_launch(wgrad_finish_k, std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s, 
       part, df, d.fh, d.fw, d.Cg, Cgp, Kg, d.groups, splits, per, d.fsc, d.fsk, acc);
   return true;
 }

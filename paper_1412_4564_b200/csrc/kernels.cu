@@ -36,6 +36,7 @@ inline int blocks_for(int64_t n, int threads, int per_sm = 16) {
 // activation.cpp:8-12 (y = x > 0 ? x : 0) and :15-22 (dx = x > 0 ? dy : 0).
 
 __global__ void relu_fwd_v4(const float4* __restrict__ x, float4* __restrict__ y, int64_t n4) {
+  ck::pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     float4 v = x[i];
@@ -48,6 +49,7 @@ __global__ void relu_fwd_v4(const float4* __restrict__ x, float4* __restrict__ y
 }
 
 __global__ void relu_fwd_s(const float* __restrict__ x, float* __restrict__ y, int64_t n) {
+  ck::pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = x[i] > 0.f ? x[i] : 0.f;
@@ -56,6 +58,7 @@ __global__ void relu_fwd_s(const float* __restrict__ x, float* __restrict__ y, i
 template <bool kAcc>
 __global__ void relu_bwd_v4(const float4* __restrict__ x, const float4* __restrict__ dy,
                             float4* dx, int64_t n4) {
+  ck::pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     float4 a = x[i], g = dy[i], r;
@@ -77,6 +80,7 @@ __global__ void relu_bwd_v4(const float4* __restrict__ x, const float4* __restri
 template <bool kAcc>
 __global__ void relu_bwd_s(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
                            int64_t n) {
+  ck::pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float r = x[i] > 0.f ? dy[i] : 0.f;
@@ -89,6 +93,7 @@ inline bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 // --------------------------------------------------------- axpy / SGD -----
 
 __global__ void axpy_k(float* y, const float* __restrict__ x, int64_t n) {
+  ck::pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     y[i] = __fadd_rn(y[i], x[i]);
@@ -98,6 +103,7 @@ __global__ void axpy_k(float* y, const float* __restrict__ x, int64_t n) {
 // exactly as the scalar C++ expression (no FMA contraction).
 __global__ void sgd_k(float* w, float* v, const float* __restrict__ g, int64_t n, float lr,
                       float mom, float wd) {
+  ck::pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     float wi = w[i];
@@ -111,6 +117,7 @@ __global__ void sgd_k(float* w, float* v, const float* __restrict__ g, int64_t n
 // float4 variant (16-byte aligned arrays, n % 4 == 0): same rounding per lane.
 __global__ void sgd_v4_k(float4* w, float4* v, const float4* __restrict__ g, int64_t n4,
                          float lr, float mom, float wd) {
+  ck::pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
     const float4 wi = w[i], vi0 = v[i], gi = __ldg(g + i);
@@ -147,6 +154,7 @@ __device__ __forceinline__ Win window_at(const PoolDims& d, int oi, int oj) {
 // max: first strict maximum in j-outer / i-inner order (pool.cpp:58-66).
 // avg: sum in the same order, divided by the clipped area (pool.cpp:67-74).
 __global__ void pool_fwd_k(const float* __restrict__ x, float* __restrict__ y, PoolDims d) {
+  ck::pdl_entry();
   const int64_t total = (int64_t)d.OH * d.OW * d.C * d.N;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -182,6 +190,7 @@ __global__ void pool_fwd_k(const float* __restrict__ x, float* __restrict__ y, P
 template <bool kAcc>
 __global__ void pool_bwd_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
                            PoolDims d) {
+  ck::pdl_entry();
   const int64_t total = (int64_t)d.H * d.W * d.C * d.N;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -232,6 +241,7 @@ __global__ void pool_bwd_k(const float* __restrict__ x, const float* __restrict_
 template <bool kAcc>
 __global__ void pool_bwd_plane_k(const float* __restrict__ x, const float* __restrict__ dy,
                                  float* dx, PoolDims d) {
+  ck::pdl_entry();
   extern __shared__ float psm[];
   const int HW = d.H * d.W, OHW = d.OH * d.OW;
   float* xs = psm;                     // [HW]
@@ -306,6 +316,7 @@ struct FastDiv {  // n / d == (n * m) >> 40 for n * d < 2^39
 template <int WH, int WW, int SH, int SW, bool INSIDE>
 __global__ void pool_max_fwd_t(const float* __restrict__ x, float* __restrict__ y, PoolDims d,
                                FastDiv by_ohw, FastDiv by_oh, uint8_t* __restrict__ argout) {
+  ck::pdl_entry();
   const int OHW = d.OH * d.OW, HW = d.H * d.W;
   const uint32_t total = (uint32_t)OHW * d.C * d.N;
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -345,6 +356,7 @@ __global__ void pool_max_fwd_t(const float* __restrict__ x, float* __restrict__ 
 template <int WH, int WW, int SH, int SW, bool kAcc>
 __global__ void pool_max_bwd_arg_t(const uint8_t* __restrict__ arg, const float* __restrict__ dy,
                                    float* dx, PoolDims d, FastDiv by_hw, FastDiv by_h) {
+  ck::pdl_entry();
   constexpr int NI = (WH + SH - 1) / SH, NJ = (WW + SW - 1) / SW;
   const int HW = d.H * d.W, OHW = d.OH * d.OW;
   const uint32_t total = (uint32_t)HW * d.C * d.N;
@@ -388,6 +400,7 @@ template <bool kAcc>
 __global__ void pool_max3s2_bwd_arg_k(const uint8_t* __restrict__ arg,
                                       const float* __restrict__ dy, float* dx, PoolDims d,
                                       int A, int B, FastDiv by_a, FastDiv by_ab) {
+  ck::pdl_entry();
   const int HW = d.H * d.W, OHW = d.OH * d.OW;
   const uint32_t total = (uint32_t)A * B * d.C * d.N;
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total;
@@ -443,6 +456,7 @@ __global__ void __launch_bounds__(256) pool_max3s2_bwd_strip_k(const uint8_t* __
                                                                const float* __restrict__ dy,
                                                                float* __restrict__ dx, PoolDims d,
                                                                int A, int B, int planes) {
+  ck::pdl_entry();
   const int lane = threadIdx.x & 31;
   const int sub = lane % SEG;  // a
   const int64_t plane = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / SEG;
@@ -514,6 +528,7 @@ __global__ void __launch_bounds__(256) pool_max3s2_bwd_strip_k(const uint8_t* __
 template <int WH, int WW, int SH, int SW, bool INSIDE, bool kAcc>
 __global__ void pool_max_bwd_t(const float* __restrict__ x, const float* __restrict__ dy,
                                float* dx, PoolDims d, FastDiv by_oh, FastDiv by_h) {
+  ck::pdl_entry();
   extern __shared__ float psm[];
   const int HW = d.H * d.W, OHW = d.OH * d.OW;
   float* xs = psm;              // [HW]
@@ -583,6 +598,7 @@ constexpr int kLrnPix = 32;
 
 __global__ void lrn_fwd_k(const float* __restrict__ x, float* __restrict__ y, int HW, int C,
                           int size, float kappa, float alpha, float nbeta) {
+  ck::pdl_entry();
   extern __shared__ float sm[];
   float* sq = sm;  // [C][kLrnPix] squares
   const int n = blockIdx.y;
@@ -613,6 +629,7 @@ __global__ void lrn_fwd_k(const float* __restrict__ x, float* __restrict__ y, in
 template <bool kAcc>
 __global__ void lrn_bwd_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
                           int HW, int C, int size, float kappa, float alpha, float beta) {
+  ck::pdl_entry();
   extern __shared__ float sm[];
   float* xs = sm;                  // [C][P]
   float* Ls = sm + C * kLrnPix;    // [C][P]
@@ -669,6 +686,7 @@ __global__ void lrn_bwd_k(const float* __restrict__ x, const float* __restrict__
 template <int NW>
 __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y, int HW, int C,
                               int64_t pixels, float kappa, float alpha, float nbeta) {
+  ck::pdl_entry();
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
   constexpr int P = 8;  // prefetch distance (channels)
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pixels;
@@ -744,6 +762,7 @@ __global__ void __launch_bounds__(320) lrn_maxpool3s2_k(
     const float* __restrict__ x, float* __restrict__ y, float* __restrict__ py,
     uint8_t* __restrict__ arg, int H, int W, int C, int OH, int OW, int TOI, float kappa,
     float alpha, float nbeta) {
+  ck::pdl_entry();
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
   constexpr int TOJ = 4, TJ = 2 * TOJ + 1, CH = 8, TIM = 33;
   __shared__ float tile[2][CH][TJ][TIM + 1];  // double-buffered: one barrier per chunk
@@ -866,6 +885,7 @@ template <int NW, bool kAcc, bool GRID = false>
 __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
                               int HW, int C, int64_t pixels, float kappa, float alpha, float beta,
                               LrnGridOut go = LrnGridOut{}) {
+  ck::pdl_entry();
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
   constexpr int P = CK_LRN_BWD_P;  // prefetch distance (channels): 2P loads in flight per thread
   const float nb = -beta;
@@ -1108,6 +1128,7 @@ __global__ void __launch_bounds__(256) bnorm_stats_k(const float* __restrict__ x
                                                      const float* __restrict__ muinv,
                                                      double* partial, int HW, int C, int N,
                                                      int splits, int vec) {
+  ck::pdl_entry();
   const int c = blockIdx.x, s = blockIdx.y;
   const BnGateP P = bn_gate_params(gw, gb, muinv, c);
   const int n0 = (int)((int64_t)N * s / splits), n1 = (int)((int64_t)N * (s + 1) / splits);
@@ -1168,6 +1189,7 @@ __global__ void __launch_bounds__(256) bnorm_stats_k(const float* __restrict__ x
 }
 
 __global__ void bnorm_finish_k(const double* partial, double* out, int C, int splits) {
+  ck::pdl_entry();
   int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   double t[4] = {0, 0, 0, 0};
@@ -1188,6 +1210,7 @@ __global__ void __launch_bounds__(256) bnorm_apply_k(const float* __restrict__ x
                                                      float* __restrict__ mom_out,
                                                      float* __restrict__ muinv_out, double eps,
                                                      int HW, int C, int N, int vec) {
+  ck::pdl_entry();
   const int c = blockIdx.x;
   const double M = (double)HW * N;
   float mu, inv;
@@ -1264,6 +1287,7 @@ __global__ void __launch_bounds__(256) bnorm_bwd_k(const float* __restrict__ x,
                                                    const double* __restrict__ stats, double eps,
                                                    float* dx, float* dw, float* db, int HW, int C,
                                                    int N, int acc_params, int vec) {
+  ck::pdl_entry();
   const int c = blockIdx.x;
   const double M = (double)HW * N;
   const double m = stats[c * 4] / M;
@@ -1350,6 +1374,7 @@ __device__ __forceinline__ float warp_sumf(float v) {
 __global__ void softmaxlog_fwd_k(const float* __restrict__ x, const float* __restrict__ labels,
                                  const float* __restrict__ weights, float* site_loss, int* flag,
                                  int HW, int C, int N) {
+  ck::pdl_entry();
   const int64_t sites = (int64_t)HW * N;
   const int lane = threadIdx.x % 32;
   for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
@@ -1379,6 +1404,7 @@ __global__ void softmaxlog_fwd_k(const float* __restrict__ x, const float* __res
 
 // Deterministic fixed-order sum of the per-site values (one block).
 __global__ void sum_sites_k(const float* __restrict__ v, int64_t n, float* out) {
+  ck::pdl_entry();
   __shared__ double red[32];
   double a = 0;
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += v[i];
@@ -1397,6 +1423,7 @@ __global__ void softmaxlog_bwd_k(const float* __restrict__ x, const float* __res
                                  const float* __restrict__ weights, float pscale,
                                  const float* __restrict__ pdev, float* dx, int* flag, int HW,
                                  int C, int N) {
+  ck::pdl_entry();
   if (pdev) pscale = *pdev;  // the engine's projection, read on the device (graph.cpp:420-425)
   const int64_t sites = (int64_t)HW * N;
   const int lane = threadIdx.x % 32;
@@ -1438,6 +1465,7 @@ template <int R>
 __global__ void softmaxlog_fwd_reg_k(const float* __restrict__ x, const float* __restrict__ labels,
                                      const float* __restrict__ weights, float* site_loss,
                                      int* flag, int HW, int C, int N) {
+  ck::pdl_entry();
   const int64_t sites = (int64_t)HW * N;
   const int lane = threadIdx.x % 32;
   for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
@@ -1477,6 +1505,7 @@ __global__ void softmaxlog_bwd_reg_k(const float* __restrict__ x, const float* _
                                      const float* __restrict__ weights, float pscale,
                                      const float* __restrict__ pdev, float* dx, int* flag, int HW,
                                      int C, int N) {
+  ck::pdl_entry();
   if (pdev) pscale = *pdev;
   const int64_t sites = (int64_t)HW * N;
   const int lane = threadIdx.x % 32;
@@ -1525,6 +1554,7 @@ __global__ void softmaxlog_bwd_reg_k(const float* __restrict__ x, const float* _
 __global__ void metrics_k(const float* __restrict__ x, const float* __restrict__ labels,
                           const float* __restrict__ weights, int top_k, float* site1,
                           float* sitek, int* flag, int HW, int C, int N) {
+  ck::pdl_entry();
   const int64_t sites = (int64_t)HW * N;
   const int lane = threadIdx.x % 32;
   for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32; s < sites;
@@ -1571,6 +1601,7 @@ __global__ void metrics_k(const float* __restrict__ x, const float* __restrict__
 // SPEC.md:716 "NaN loss aborts with diagnostic": sets `bit` in the handle's
 // flag when any of the n values is NaN or infinite.
 __global__ void flag_nonfinite_k(const float* __restrict__ v, int64_t n, int* flag, int bit) {
+  ck::pdl_entry();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     if (!isfinite(v[i])) atomicOr(flag, bit);
@@ -1582,9 +1613,9 @@ void relu_forward(const float* x, float* y, int64_t n, cudaStream_t s) {
   if (n == 0) return;
   count_launch();
   if (n % 4 == 0 && aligned16(x) && aligned16(y))
-    relu_fwd_v4<<<blocks_for(n / 4, 256), 256, 0, s>>>((const float4*)x, (float4*)y, n / 4);
+    ck::pdl_launch(relu_fwd_v4, blocks_for(n / 4, 256), 256, 0, s, (const float4*)x, (float4*)y, n / 4);
   else
-    relu_fwd_s<<<blocks_for(n, 256), 256, 0, s>>>(x, y, n);
+    ck::pdl_launch(relu_fwd_s, blocks_for(n, 256), 256, 0, s, x, y, n);
 }
 
 void relu_backward(const float* x, const float* dy, float* dx, int64_t n, int acc,
@@ -1593,23 +1624,23 @@ void relu_backward(const float* x, const float* dy, float* dx, int64_t n, int ac
   count_launch();
   if (n % 4 == 0 && aligned16(x) && aligned16(dy) && aligned16(dx)) {
     if (acc)
-      relu_bwd_v4<true><<<blocks_for(n / 4, 256), 256, 0, s>>>((const float4*)x,
+      ck::pdl_launch(relu_bwd_v4<true>, blocks_for(n / 4, 256), 256, 0, s, (const float4*)x,
                                                                (const float4*)dy, (float4*)dx, n / 4);
     else
-      relu_bwd_v4<false><<<blocks_for(n / 4, 256), 256, 0, s>>>((const float4*)x,
+      ck::pdl_launch(relu_bwd_v4<false>, blocks_for(n / 4, 256), 256, 0, s, (const float4*)x,
                                                                 (const float4*)dy, (float4*)dx, n / 4);
   } else {
     if (acc)
-      relu_bwd_s<true><<<blocks_for(n, 256), 256, 0, s>>>(x, dy, dx, n);
+      ck::pdl_launch(relu_bwd_s<true>, blocks_for(n, 256), 256, 0, s, x, dy, dx, n);
     else
-      relu_bwd_s<false><<<blocks_for(n, 256), 256, 0, s>>>(x, dy, dx, n);
+      ck::pdl_launch(relu_bwd_s<false>, blocks_for(n, 256), 256, 0, s, x, dy, dx, n);
   }
 }
 
 void axpy_inplace(float* y, const float* x, int64_t n, cudaStream_t s) {
   if (n == 0) return;
   count_launch();
-  axpy_k<<<blocks_for(n, 256), 256, 0, s>>>(y, x, n);
+  ck::pdl_launch(axpy_k, blocks_for(n, 256), 256, 0, s, y, x, n);
 }
 
 void sgd_step(float* w, float* v, const float* g, int64_t n, float lr, float mom, float wd,
@@ -1617,11 +1648,11 @@ void sgd_step(float* w, float* v, const float* g, int64_t n, float lr, float mom
   if (n == 0) return;
   count_launch();
   if (n % 4 == 0 && (((uintptr_t)w | (uintptr_t)v | (uintptr_t)g) & 15) == 0) {
-    sgd_v4_k<<<blocks_for(n / 4, 256), 256, 0, s>>>((float4*)w, (float4*)v, (const float4*)g,
+    ck::pdl_launch(sgd_v4_k, blocks_for(n / 4, 256), 256, 0, s, (float4*)w, (float4*)v, (const float4*)g,
                                                      n / 4, lr, mom, wd);
     return;
   }
-  sgd_k<<<blocks_for(n, 256), 256, 0, s>>>(w, v, g, n, lr, mom, wd);
+  ck::pdl_launch(sgd_k, blocks_for(n, 256), 256, 0, s, w, v, g, n, lr, mom, wd);
 }
 
 // every window inside the input: no padding and the last window ends in it
@@ -1636,10 +1667,10 @@ static void pool_max_fwd_launch(const float* x, float* y, const PoolDims& d, uin
   const int64_t total = (int64_t)d.OH * d.OW * d.C * d.N;
   const FastDiv a(d.OH * d.OW), b(d.OH);
   if (pool_inside(d))
-    pool_max_fwd_t<WH, WW, SH, SW, true><<<blocks_for(total, 256), 256, 0, s>>>(x, y, d, a, b,
+    ck::pdl_launch(pool_max_fwd_t<WH, WW, SH, SW, true>, blocks_for(total, 256), 256, 0, s, x, y, d, a, b,
                                                                                 arg);
   else
-    pool_max_fwd_t<WH, WW, SH, SW, false><<<blocks_for(total, 256), 256, 0, s>>>(x, y, d, a, b,
+    ck::pdl_launch(pool_max_fwd_t<WH, WW, SH, SW, false>, blocks_for(total, 256), 256, 0, s, x, y, d, a, b,
                                                                                  arg);
 }
 
@@ -1649,10 +1680,10 @@ static void pool_max_bwd_arg_launch(const uint8_t* arg, const float* dy, float* 
   const int64_t total = (int64_t)d.H * d.W * d.C * d.N;
   const FastDiv a(d.H * d.W), b(d.H);
   if (acc)
-    pool_max_bwd_arg_t<WH, WW, SH, SW, true><<<blocks_for(total, 256), 256, 0, s>>>(arg, dy, dx,
+    ck::pdl_launch(pool_max_bwd_arg_t<WH, WW, SH, SW, true>, blocks_for(total, 256), 256, 0, s, arg, dy, dx,
                                                                                      d, a, b);
   else
-    pool_max_bwd_arg_t<WH, WW, SH, SW, false><<<blocks_for(total, 256), 256, 0, s>>>(arg, dy, dx,
+    ck::pdl_launch(pool_max_bwd_arg_t<WH, WW, SH, SW, false>, blocks_for(total, 256), 256, 0, s, arg, dy, dx,
                                                                                       d, a, b);
 }
 
@@ -1668,13 +1699,13 @@ static void pool_max_bwd_launch(const float* x, const float* dy, float* dx, cons
   const FastDiv a(d.OH), b(d.H);
   const bool in = pool_inside(d);
   if (in && acc)
-    pool_max_bwd_t<WH, WW, SH, SW, true, true><<<planes, 256, smem, s>>>(x, dy, dx, d, a, b);
+    ck::pdl_launch(pool_max_bwd_t<WH, WW, SH, SW, true, true>, planes, 256, smem, s, x, dy, dx, d, a, b);
   else if (in)
-    pool_max_bwd_t<WH, WW, SH, SW, true, false><<<planes, 256, smem, s>>>(x, dy, dx, d, a, b);
+    ck::pdl_launch(pool_max_bwd_t<WH, WW, SH, SW, true, false>, planes, 256, smem, s, x, dy, dx, d, a, b);
   else if (acc)
-    pool_max_bwd_t<WH, WW, SH, SW, false, true><<<planes, 256, smem, s>>>(x, dy, dx, d, a, b);
+    ck::pdl_launch(pool_max_bwd_t<WH, WW, SH, SW, false, true>, planes, 256, smem, s, x, dy, dx, d, a, b);
   else
-    pool_max_bwd_t<WH, WW, SH, SW, false, false><<<planes, 256, smem, s>>>(x, dy, dx, d, a, b);
+    ck::pdl_launch(pool_max_bwd_t<WH, WW, SH, SW, false, false>, planes, 256, smem, s, x, dy, dx, d, a, b);
 }
 
 // 2x2 / stride 2 max pooling without padding on even planes (LeNet, VGG):
@@ -1688,6 +1719,7 @@ static void pool_max_bwd_launch(const float* x, const float* dy, float* dx, cons
 __global__ void pool2_fwd_k(const float* __restrict__ x, float* __restrict__ y,
                             uint8_t* __restrict__ arg, int H, int OH, int OHW, int64_t planes,
                             FastDiv by_oh) {
+  ck::pdl_entry();
   for (int64_t pl = blockIdx.y; pl < planes; pl += gridDim.y) {
     const float* xp = x + pl * (int64_t)H * (2 * (OHW / OH));
     for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < OHW; w += gridDim.x * blockDim.x) {
@@ -1709,6 +1741,7 @@ template <bool kAcc, bool kArg>
 __global__ void pool2_bwd_k(const float* __restrict__ x, const uint8_t* __restrict__ arg,
                             const float* __restrict__ dy, float* dx, int H, int OH, int OHW,
                             int64_t planes, FastDiv by_oh) {
+  ck::pdl_entry();
   for (int64_t pl = blockIdx.y; pl < planes; pl += gridDim.y) {
     const int64_t xo = pl * (int64_t)H * (2 * (OHW / OH));
     for (int w = blockIdx.x * blockDim.x + threadIdx.x; w < OHW; w += gridDim.x * blockDim.x) {
@@ -1787,14 +1820,14 @@ void pool_forward(const float* x, float* y, const PoolDims& d, cudaStream_t s, C
       cache->src = x;
       cache->key = pool_arg_key(x, d);
     }
-    pool2_fwd_k<<<pool2_grid(d), 256, 0, s>>>(x, y, arg, d.H, d.OH, d.OH * d.OW,
+    ck::pdl_launch(pool2_fwd_k, pool2_grid(d), 256, 0, s, x, y, arg, d.H, d.OH, d.OH * d.OW,
                                               (int64_t)d.C * d.N, FastDiv(d.OH));
     return;
   }
   switch (fx) {
     case 3: pool_max_fwd_launch<3, 3, 2, 2>(x, y, d, arg, s); return;
     case 2: pool_max_fwd_launch<2, 2, 2, 2>(x, y, d, arg, s); return;
-    default: pool_fwd_k<<<blocks_for(total, 256), 256, 0, s>>>(x, y, d);
+    default: ck::pdl_launch(pool_fwd_k, blocks_for(total, 256), 256, 0, s, x, y, d);
   }
 }
 
@@ -1813,11 +1846,11 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
     const FastDiv by(d.OH);
     const int OHW = d.OH * d.OW;
     if (arg) {
-      if (acc) pool2_bwd_k<true, true><<<grid, 256, 0, s>>>(x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
-      else pool2_bwd_k<false, true><<<grid, 256, 0, s>>>(x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
+      if (acc) ck::pdl_launch(pool2_bwd_k<true, true>, grid, 256, 0, s, x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
+      else ck::pdl_launch(pool2_bwd_k<false, true>, grid, 256, 0, s, x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
     } else {
-      if (acc) pool2_bwd_k<true, false><<<grid, 256, 0, s>>>(x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
-      else pool2_bwd_k<false, false><<<grid, 256, 0, s>>>(x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
+      if (acc) ck::pdl_launch(pool2_bwd_k<true, false>, grid, 256, 0, s, x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
+      else ck::pdl_launch(pool2_bwd_k<false, false>, grid, 256, 0, s, x, arg, dy, dx, d.H, d.OH, OHW, planes, by);
     }
     return;
   }
@@ -1836,8 +1869,8 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
         const unsigned grid = (unsigned)((threads + 255) / 256);
 #define CK_PSB(S)                                                                          \
   do {                                                                                     \
-    if (acc) pool_max3s2_bwd_strip_k<true, S><<<grid, 256, 0, s>>>(arg, dy, dx, d, A, B, planes); \
-    else pool_max3s2_bwd_strip_k<false, S><<<grid, 256, 0, s>>>(arg, dy, dx, d, A, B, planes);   \
+    if (acc) ck::pdl_launch(pool_max3s2_bwd_strip_k<true, S>, grid, 256, 0, s, arg, dy, dx, d, A, B, planes); \
+    else ck::pdl_launch(pool_max3s2_bwd_strip_k<false, S>, grid, 256, 0, s, arg, dy, dx, d, A, B, planes);   \
   } while (0)
         if (seg == 8) CK_PSB(8);
         else if (seg == 16) CK_PSB(16);
@@ -1847,10 +1880,10 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
       }
       if (blocks * A * B < (1ll << 39)) {
         if (acc)
-          pool_max3s2_bwd_arg_k<true><<<blocks_for(blocks, 256), 256, 0, s>>>(arg, dy, dx, d, A,
+          ck::pdl_launch(pool_max3s2_bwd_arg_k<true>, blocks_for(blocks, 256), 256, 0, s, arg, dy, dx, d, A,
                                                                               B, by_a, by_ab);
         else
-          pool_max3s2_bwd_arg_k<false><<<blocks_for(blocks, 256), 256, 0, s>>>(arg, dy, dx, d, A,
+          ck::pdl_launch(pool_max3s2_bwd_arg_k<false>, blocks_for(blocks, 256), 256, 0, s, arg, dy, dx, d, A,
                                                                                B, by_a, by_ab);
         return;
       }
@@ -1879,15 +1912,15 @@ void pool_backward(const float* x, const float* dy, float* dx, const PoolDims& d
       return;
     }
     if (acc)
-      pool_bwd_plane_k<true><<<planes, 256, smem, s>>>(x, dy, dx, d);
+      ck::pdl_launch(pool_bwd_plane_k<true>, planes, 256, smem, s, x, dy, dx, d);
     else
-      pool_bwd_plane_k<false><<<planes, 256, smem, s>>>(x, dy, dx, d);
+      ck::pdl_launch(pool_bwd_plane_k<false>, planes, 256, smem, s, x, dy, dx, d);
     return;
   }
   if (acc)
-    pool_bwd_k<true><<<blocks_for(total, 256), 256, 0, s>>>(x, dy, dx, d);
+    ck::pdl_launch(pool_bwd_k<true>, blocks_for(total, 256), 256, 0, s, x, dy, dx, d);
   else
-    pool_bwd_k<false><<<blocks_for(total, 256), 256, 0, s>>>(x, dy, dx, d);
+    ck::pdl_launch(pool_bwd_k<false>, blocks_for(total, 256), 256, 0, s, x, dy, dx, d);
 }
 
 static void lrn_smem_check(int C, int arrays) {
@@ -1906,7 +1939,7 @@ template <int NW>
 static void lrn_fwd_reg(const float* x, float* y, int HW, int C, int N, float kappa, float alpha,
                         float beta, cudaStream_t s) {
   const int64_t pixels = (int64_t)HW * N;
-  lrn_fwd_reg_k<NW><<<blocks_for(pixels, 128, 32), 128, 0, s>>>(x, y, HW, C, pixels, kappa, alpha,
+  ck::pdl_launch(lrn_fwd_reg_k<NW>, blocks_for(pixels, 128, 32), 128, 0, s, x, y, HW, C, pixels, kappa, alpha,
                                                                  -beta);
 }
 
@@ -1915,11 +1948,11 @@ static void lrn_bwd_reg(const float* x, const float* dy, float* dx, int HW, int 
                         float kappa, float alpha, float beta, int acc, cudaStream_t s) {
   const int64_t pixels = (int64_t)HW * N;
   if (acc)
-    lrn_bwd_reg_k<NW, true><<<blocks_for(pixels, 128, 32), 128, 0, s>>>(x, dy, dx, HW, C, pixels,
-                                                                         kappa, alpha, beta);
+    ck::pdl_launch(lrn_bwd_reg_k<NW, true>, blocks_for(pixels, 128, 32), 128, 0, s, x, dy, dx, HW, C,
+                   pixels, kappa, alpha, beta, LrnGridOut{});
   else
-    lrn_bwd_reg_k<NW, false><<<blocks_for(pixels, 128, 32), 128, 0, s>>>(x, dy, dx, HW, C, pixels,
-                                                                          kappa, alpha, beta);
+    ck::pdl_launch(lrn_bwd_reg_k<NW, false>, blocks_for(pixels, 128, 32), 128, 0, s, x, dy, dx, HW, C,
+                   pixels, kappa, alpha, beta, LrnGridOut{});
 }
 
 #define CK_LRN_SWITCH(size, CALL) \
@@ -1946,7 +1979,7 @@ void lrn_forward(const float* x, float* y, int H, int W, int C, int N, int size,
   dim3 grid((HW + kLrnPix - 1) / kLrnPix, N);
   size_t smem = (size_t)C * kLrnPix * sizeof(float);
   lrn_smem_check(C, 1);
-  lrn_fwd_k<<<grid, 256, smem, s>>>(x, y, HW, C, size, kappa, alpha, -beta);
+  ck::pdl_launch(lrn_fwd_k, grid, 256, smem, s, x, y, HW, C, size, kappa, alpha, -beta);
 }
 
 bool lrn_maxpool_forward(const float* x, float* y, float* py, const PoolDims& pd, int size,
@@ -1974,10 +2007,10 @@ bool lrn_maxpool_forward(const float* x, float* y, float* py, const PoolDims& pd
   const int threads = ((2 * TOI + 1) * 9 + 31) / 32 * 32;
   const dim3 grid((pd.OH + TOI - 1) / TOI, (pd.OW + 3) / 4, pd.N);
   if (size == 5)
-    lrn_maxpool3s2_k<5><<<grid, threads, 0, s>>>(x, y, py, arg, pd.H, pd.W, pd.C, pd.OH, pd.OW,
+    ck::pdl_launch(lrn_maxpool3s2_k<5>, grid, threads, 0, s, x, y, py, arg, pd.H, pd.W, pd.C, pd.OH, pd.OW,
                                                   TOI, kappa, alpha, -beta);
   else
-    lrn_maxpool3s2_k<3><<<grid, threads, 0, s>>>(x, y, py, arg, pd.H, pd.W, pd.C, pd.OH, pd.OW,
+    ck::pdl_launch(lrn_maxpool3s2_k<3>, grid, threads, 0, s, x, y, py, arg, pd.H, pd.W, pd.C, pd.OH, pd.OW,
                                                   TOI, kappa, alpha, -beta);
   return true;
 }
@@ -1993,9 +2026,9 @@ void lrn_backward(const float* x, const float* dy, float* dx, int H, int W, int 
   size_t smem = (size_t)3 * C * kLrnPix * sizeof(float);
   lrn_smem_check(C, 3);
   if (acc)
-    lrn_bwd_k<true><<<grid, 256, smem, s>>>(x, dy, dx, HW, C, size, kappa, alpha, beta);
+    ck::pdl_launch(lrn_bwd_k<true>, grid, 256, smem, s, x, dy, dx, HW, C, size, kappa, alpha, beta);
   else
-    lrn_bwd_k<false><<<grid, 256, smem, s>>>(x, dy, dx, HW, C, size, kappa, alpha, beta);
+    ck::pdl_launch(lrn_bwd_k<false>, grid, 256, smem, s, x, dy, dx, HW, C, size, kappa, alpha, beta);
 }
 
 bool lrn_backward_grid(const float* x, const float* dy, float* grid, double* bpart, int H, int W,
@@ -2012,12 +2045,12 @@ bool lrn_backward_grid(const float* x, const float* dy, float* grid, double* bpa
   switch (size) {
     case 3:
       count_launch();
-      lrn_bwd_reg_k<3, false, true><<<grid_dim, 128, 0, s>>>(x, dy, nullptr, HW, C, pixels, kappa,
+      ck::pdl_launch(lrn_bwd_reg_k<3, false, true>, grid_dim, 128, 0, s, x, dy, nullptr, HW, C, pixels, kappa,
                                                              alpha, beta, go);
       return true;
     case 5:
       count_launch();
-      lrn_bwd_reg_k<5, false, true><<<grid_dim, 128, 0, s>>>(x, dy, nullptr, HW, C, pixels, kappa,
+      ck::pdl_launch(lrn_bwd_reg_k<5, false, true>, grid_dim, 128, 0, s, x, dy, nullptr, HW, C, pixels, kappa,
                                                              alpha, beta, go);
       return true;
     default:
@@ -2046,18 +2079,18 @@ void bnorm_stats(const float* x, const float* dy, double* partial, double* out, 
   count_launch(2);
   const int vec = bnorm_vec(x, dy, gate, HW);
   if (dy && rg.muinv)
-    bnorm_stats_k<true, 2><<<grid, 256, 0, s>>>(x, dy, nullptr, rg.w, rg.b, rg.muinv, partial, HW,
+    ck::pdl_launch(bnorm_stats_k<true, 2>, grid, 256, 0, s, x, dy, nullptr, rg.w, rg.b, rg.muinv, partial, HW,
                                                 C, N, splits, vec);
   else if (dy && gate)
-    bnorm_stats_k<true, 1><<<grid, 256, 0, s>>>(x, dy, gate, nullptr, nullptr, nullptr, partial,
+    ck::pdl_launch(bnorm_stats_k<true, 1>, grid, 256, 0, s, x, dy, gate, nullptr, nullptr, nullptr, partial,
                                                 HW, C, N, splits, vec);
   else if (dy)
-    bnorm_stats_k<true, 0><<<grid, 256, 0, s>>>(x, dy, nullptr, nullptr, nullptr, nullptr, partial,
+    ck::pdl_launch(bnorm_stats_k<true, 0>, grid, 256, 0, s, x, dy, nullptr, nullptr, nullptr, nullptr, partial,
                                                 HW, C, N, splits, vec);
   else
-    bnorm_stats_k<false, 0><<<grid, 256, 0, s>>>(x, nullptr, nullptr, nullptr, nullptr, nullptr,
+    ck::pdl_launch(bnorm_stats_k<false, 0>, grid, 256, 0, s, x, nullptr, nullptr, nullptr, nullptr, nullptr,
                                                  partial, HW, C, N, splits, vec);
-  bnorm_finish_k<<<(C + 127) / 128, 128, 0, s>>>(partial, out, C, splits);
+  ck::pdl_launch(bnorm_finish_k, (C + 127) / 128, 128, 0, s, partial, out, C, splits);
 }
 
 static int bnorm_grid_y(int C, int N) {
@@ -2071,7 +2104,7 @@ void bnorm_apply(const float* x, const float* w, const float* b, const double* s
                  const float* fixed_moments, float* y, float* moments_out, double eps, int HW,
                  int C, int N, cudaStream_t s, float* y2, float* muinv_out) {
   count_launch();
-  bnorm_apply_k<<<dim3(C, bnorm_grid_y(C, N)), 256, 0, s>>>(
+  ck::pdl_launch(bnorm_apply_k, dim3(C, bnorm_grid_y(C, N)), 256, 0, s, 
       x, w, b, stats, fixed_moments, y, y2, moments_out, muinv_out, eps, HW, C, N,
       bnorm_vec(x, y, y2, HW));
 }
@@ -2083,7 +2116,7 @@ void bnorm_backward_apply(const float* x, const float* dy, const float* w, const
   const dim3 grid(C, bnorm_grid_y(C, N));
   const int vec = bnorm_vec(x, dy, gate, HW) && bnorm_vec(dx, dx, dx, HW);
 #define CK_BNB(A, G)                                                                        \
-  bnorm_bwd_k<A, G><<<grid, 256, 0, s>>>(x, dy, gate, rg.b, rg.muinv, w, stats, eps, dx, dw,  \
+  ck::pdl_launch(bnorm_bwd_k<A, G>, grid, 256, 0, s, x, dy, gate, rg.b, rg.muinv, w, stats, eps, dx, dw,  \
                                          db, HW, C, N, acc ? 1 : 0, vec)
   const int G = rg.muinv ? 2 : gate ? 1 : 0;
   if (acc) {
@@ -2104,12 +2137,12 @@ void softmaxlog_forward(const float* x, const float* labels, const float* weight
   int64_t sites = (int64_t)HW * N;
   count_launch(2);
   if (C <= 1024)
-    softmaxlog_fwd_reg_k<32><<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights,
+    ck::pdl_launch(softmaxlog_fwd_reg_k<32>, blocks_for(sites * 32, 256), 256, 0, s, x, labels, weights,
                                                                          site_loss, flag, HW, C, N);
   else
-    softmaxlog_fwd_k<<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, site_loss,
+    ck::pdl_launch(softmaxlog_fwd_k, blocks_for(sites * 32, 256), 256, 0, s, x, labels, weights, site_loss,
                                                                   flag, HW, C, N);
-  sum_sites_k<<<1, 1024, 0, s>>>(site_loss, sites, loss);
+  ck::pdl_launch(sum_sites_k, 1, 1024, 0, s, site_loss, sites, loss);
 }
 
 void softmaxlog_backward(const float* x, const float* labels, const float* weights, float p,
@@ -2119,18 +2152,18 @@ void softmaxlog_backward(const float* x, const float* labels, const float* weigh
   count_launch();
   if (C <= 1024) {
     if (acc)
-      softmaxlog_bwd_reg_k<32, true><<<blocks_for(sites * 32, 256), 256, 0, s>>>(
+      ck::pdl_launch(softmaxlog_bwd_reg_k<32, true>, blocks_for(sites * 32, 256), 256, 0, s, 
           x, labels, weights, p, p_dev, dx, flag, HW, C, N);
     else
-      softmaxlog_bwd_reg_k<32, false><<<blocks_for(sites * 32, 256), 256, 0, s>>>(
+      ck::pdl_launch(softmaxlog_bwd_reg_k<32, false>, blocks_for(sites * 32, 256), 256, 0, s, 
           x, labels, weights, p, p_dev, dx, flag, HW, C, N);
     return;
   }
   if (acc)
-    softmaxlog_bwd_k<true><<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, p, p_dev,
+    ck::pdl_launch(softmaxlog_bwd_k<true>, blocks_for(sites * 32, 256), 256, 0, s, x, labels, weights, p, p_dev,
                                                                         dx, flag, HW, C, N);
   else
-    softmaxlog_bwd_k<false><<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, p,
+    ck::pdl_launch(softmaxlog_bwd_k<false>, blocks_for(sites * 32, 256), 256, 0, s, x, labels, weights, p,
                                                                          p_dev, dx, flag, HW, C, N);
 }
 
@@ -2139,15 +2172,15 @@ void loss_metrics(const float* x, const float* labels, const float* weights, int
                   cudaStream_t s) {
   int64_t sites = (int64_t)HW * N;
   count_launch(3);
-  metrics_k<<<blocks_for(sites * 32, 256), 256, 0, s>>>(x, labels, weights, top_k, site_buf,
+  ck::pdl_launch(metrics_k, blocks_for(sites * 32, 256), 256, 0, s, x, labels, weights, top_k, site_buf,
                                                          site_buf + sites, flag, HW, C, N);
-  sum_sites_k<<<1, 1024, 0, s>>>(site_buf, sites, top1);
-  sum_sites_k<<<1, 1024, 0, s>>>(site_buf + sites, sites, topk);
+  ck::pdl_launch(sum_sites_k, 1, 1024, 0, s, site_buf, sites, top1);
+  ck::pdl_launch(sum_sites_k, 1, 1024, 0, s, site_buf + sites, sites, topk);
 }
 
 void flag_nonfinite(const float* v, int64_t n, int* flag, int bit, cudaStream_t s) {
   count_launch();
-  flag_nonfinite_k<<<blocks_for(n, 256), 256, 0, s>>>(v, n, flag, bit);
+  ck::pdl_launch(flag_nonfinite_k, blocks_for(n, 256), 256, 0, s, v, n, flag, bit);
 }
 
 }  // namespace ck
