@@ -314,7 +314,9 @@ ck_status ck_graph_layer_ms(ck_graph* g, int layer, float* fwd_ms, float* bwd_ms
  *   writes the conv's ReLU-gated dy grid directly (0: the unfused blocks);
  *   "lrn_pool" (default 0): an lrn -> 3x3/2 max pool pair runs as one kernel
  *   (the pool reads the LRN values from shared memory, not HBM; bit-identical,
- *   measured slower than the two tuned kernels on AlexNet). */
+ *   measured slower than the two tuned kernels on AlexNet);
+ *   "producer_grid" (default 1): a TF32 conv -> relu -> conv forward writes the
+ *   second conv's padded x grid from the first conv's epilogue. */
 ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value);
 
 /* ---- cnn_train training step with multi-GPU data parallelism ------------ */

@@ -50,6 +50,11 @@ struct ck_handle {
   const double* pre_bpart = nullptr;
   int pre_rows = 0;
   ck::KernelProfiler prof;
+  // engine, conv -> relu -> conv: the forward of the first conv also writes
+  // relu(y) into the second conv's x grid (next_xg, laid out by next_xg_plan)
+  float* next_xg = nullptr;
+  ck::XGridPlan next_xg_plan{};
+  bool next_xg_done = false;
   // engine, fused bnorm -> relu: per-channel (mu, inv) of the forward, which
   // the backward uses to recompute the relu gate from x (2 floats / channel)
   float* bn_muinv = nullptr;
@@ -128,6 +133,11 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
 bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, int acc,
                   cudaStream_t s, const float* relu_x = nullptr, const float* relu_dy = nullptr,
                   bool skip_gout = false);
+// The x grid a stride-1 TF32 conv forward (and its weight gradient) reads:
+// pixel-major, Cgp channels per group, x at (pt, pl) of an Hg x Wg image grid
+// (key: x_grid's cache key).  conv_tc_xgrid_plan says whether conv d reads x
+// only through it, so the layer producing x may write it instead.
+bool conv_tc_xgrid_plan(const ConvDims& d, XGridPlan* xp);
 // The dy grid a TF32 conv backward consumes (dy at (0, 0) of an Hg x Wg grid,
 // Kgp padded channels per group): conv_tc_grid_plan says whether BOTH the
 // weight and data gradient of d read dy only through that grid, and how it

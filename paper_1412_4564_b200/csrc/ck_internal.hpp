@@ -86,6 +86,13 @@ inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
 int knob(const char* name, int dflt);
 bool experiments_build();
 
+// The x grid a stride-1 TF32 conv reads (conv_tc_xgrid_plan, ck_handle.hpp).
+struct XGridPlan {
+  int Hg, Wg, Cg, Cgp, groups, pt, pl;
+  int64_t key;
+  size_t bytes;
+};
+
 // Per-handle scratch owned by the C ABI / engine.
 struct Workspace {
   void* ptr = nullptr;
@@ -103,6 +110,10 @@ struct ConvCache {
   const float* src = nullptr;
   int64_t key = 0;
   bool valid = false;
+  // the buffer (at zero_ptr) was zero-filled for grid layout zero_key: a
+  // producer writing only the interior keeps the halos and channel pads zero
+  void* zero_ptr = nullptr;
+  int64_t zero_key = 0;
 };
 
 struct LaunchCounter {

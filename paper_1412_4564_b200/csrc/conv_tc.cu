@@ -107,6 +107,12 @@ struct GemmParams {
   int snake;              // epilogue: snake-order (half, chunk) units (CK_EPI_SNAKE=0 disables)
   int last_k;             // OP_IM2COL_K: K=8 MMAs needed in a tap's last 32-channel chunk
                           // (1..4; the rest of the chunk is channel padding = zeros)
+  // EPI_PIX with out2 (fused relu): also store relu(v) into the NEXT conv's
+  // padded pixel-major x grid (the consumer's x_grid, see XGridPlan): row
+  // (n, oi, oj) -> grid pixel (n, oj + gx_pl, oi + gx_pt) of an gx_Hg x gx_Wg
+  // image grid, channel c -> g'*gx_Cgp + (c - g'*gx_Cg), g' = c / gx_Cg
+  float* gx;
+  int gx_Hg, gx_Wg, gx_Cp, gx_Cg, gx_Cgp, gx_pt, gx_pl, gx_OH;
   int BM;                 // 128 or 256 (two M=128 MMAs sharing the B tile)
   int nacc;               // TMEM accumulator buffers (2: epilogue overlaps mainloop)
   int groups;             // tiles = ceil(M/BM) * ceil(N/BN) * groups * splits
@@ -582,7 +588,30 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
               if (p.relu) v = v > 0.f ? v : 0.f;
               if (p.acc) v = __fadd_rn(dst[j * ld], v);
               dst[j * ld] = v;
-              if (dst2) dst2[j * ld] = v > 0.f ? v : 0.f;  // fused relu layer
+              const float rv = v > 0.f ? v : 0.f;
+              if (dst2) dst2[j * ld] = rv;  // fused relu layer
+              r[j] = __float_as_uint(rv);
+            }
+          }
+          if (p.gx) {
+            // the next conv's x grid: this pixel's 32 consecutive channels are
+            // one contiguous 128-byte run of its grid row (host: gx_Cg % 32 == 0)
+            const int oj = pix / p.gx_OH, oi = pix - oj * p.gx_OH;
+            const int col = T.grp * (int)p.grp_col + col0;
+            const int g2 = col / p.gx_Cg;
+            const int64_t grow = (((int64_t)img * p.gx_Wg + oj + p.gx_pl) * p.gx_Hg + oi + p.gx_pt) *
+                                     p.gx_Cp + g2 * p.gx_Cgp + (col - g2 * p.gx_Cg);
+            float* gd = p.gx + grow;
+            if (lim == 32) {
+#pragma unroll
+              for (int q4 = 0; q4 < 8; ++q4)
+                reinterpret_cast<float4*>(gd)[q4] =
+                    make_float4(__uint_as_float(r[4 * q4]), __uint_as_float(r[4 * q4 + 1]),
+                                __uint_as_float(r[4 * q4 + 2]), __uint_as_float(r[4 * q4 + 3]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < lim) gd[j] = __uint_as_float(r[j]);
             }
           }
         }
@@ -2122,11 +2151,15 @@ static void grid_dims(const ConvDims& d, int& Hg, int& Wg) {
   Wg = d.W + (shared ? std::max(d.pl, d.pr) : d.pl + d.pr);
 }
 
+static int64_t x_grid_key(const ConvDims& d, int Cgp, int Hg, int Wg) {
+  return (((((int64_t)Hg * 4099 + Wg) * 65537 + d.C) * 131071 + d.N) * 1031 + Cgp * 17 +
+          d.groups) ^ ((int64_t)(d.pt * 64 + d.pl) << 52) ^ 0x1;
+}
+
 static float* x_grid(ck_handle* h, const float* x, const ConvDims& d, int Cgp, int Hg, int Wg,
                      cudaStream_t s) {
   ConvCache* c = h->conv_cache;
-  const int64_t key = (((((int64_t)Hg * 4099 + Wg) * 65537 + d.C) * 131071 + d.N) * 1031 +
-                       Cgp * 17 + d.groups) ^ ((int64_t)(d.pt * 64 + d.pl) << 52) ^ 0x1;
+  const int64_t key = x_grid_key(d, Cgp, Hg, Wg);
   const size_t bytes = sizeof(float) * (size_t)d.N * Hg * Wg * Cgp * d.groups;
   float* buf = (float*)grow(c ? c->buf : state(h)->xt, bytes, s);
   if (c && c->valid && c->src == x && c->key == key) return buf;
@@ -2602,6 +2635,14 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
   p.bias = bias; p.relu = relu; p.acc = 0; p.n_valid = Kg;
   p.BM = pick_bm(p.M, p.BN, true, (Kg + p.BN - 1) / p.BN * d.groups);
   if (on_grid) p.pt = p.pl = 0;
+  if (h->next_xg && h->fuse_relu && Kg % 32 == 0) {
+    // engine: also write relu(y) into the consumer conv's x grid
+    const XGridPlan& xp = h->next_xg_plan;
+    p.gx = h->next_xg;
+    p.gx_Hg = xp.Hg; p.gx_Wg = xp.Wg; p.gx_Cp = xp.Cgp * xp.groups; p.gx_Cg = xp.Cg;
+    p.gx_Cgp = xp.Cgp; p.gx_pt = xp.pt; p.gx_pl = xp.pl; p.gx_OH = d.OH;
+    h->next_xg_done = true;
+  }
   // on the grid the output extent is (H + pt + pb) - fh + 1 whatever the grid
   // pitch: rows read past a shared-halo grid's column end are TMA zero fill
   CUtensorMap ta = on_grid ? map_im2col(xt, Cp, Hg, Wg, d.N, 0, 0,
@@ -2738,6 +2779,25 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
 // Mirrors the envelopes of conv_tc_bias / conv_tc_wgrad / conv_tc_dgrad: true
 // iff all three read dy only through dy_grid (no fallback, no experimental
 // path that transforms dy itself).
+// Mirrors conv_tc_forward_impl / conv_tc_wgrad: true iff the forward reads x
+// only through x_grid on the padded grid (stride 1, TF32, no experimental
+// path) -- so a producer may write that grid (and mark the consumer's cache).
+bool conv_tc_xgrid_plan(const ConvDims& d, XGridPlan* xp) {
+  if (!load_driver() || is_fc(d) || halo_enabled() || shift_enabled()) return false;
+  if (d.sh != 1 || d.sw != 1) return false;
+  if (d.pt > 127 || d.pl > 127 || d.fh > 128 || d.fw > 128) return false;
+  if (d.pt > d.fh - 1 || d.pb > d.fh - 1 || d.pl > d.fw - 1 || d.pr > d.fw - 1) return false;
+  grid_dims(d, xp->Hg, xp->Wg);
+  xp->Cg = d.Cg;
+  xp->Cgp = rup(d.Cg, 32);
+  xp->groups = d.groups;
+  xp->pt = d.pt;
+  xp->pl = d.pl;
+  xp->key = x_grid_key(d, xp->Cgp, xp->Hg, xp->Wg);
+  xp->bytes = sizeof(float) * (size_t)d.N * xp->Hg * xp->Wg * xp->Cgp * d.groups;
+  return true;
+}
+
 bool conv_tc_grid_plan(const ConvDims& d, GridPlan* gp) {
   if (!load_driver() || is_fc(d) || halo_enabled() || shift_enabled()) return false;
   const int Kg = d.Kg();

@@ -160,6 +160,9 @@ struct ck_graph {
   // 0.247 vs 0.213 ms, norm2+pool2 0.168 vs 0.149: the per-chunk barrier and
   // the 16% halo recompute cost more than the 297 MB re-read saves)
   bool lrn_pool = false;
+  // option "producer_grid": a conv -> relu -> conv forward writes the next
+  // conv's x grid from its epilogue (default on)
+  bool producer_grid = true;
   std::vector<std::pair<std::string, std::string>> meta;  // manifest metadata
   std::vector<int> decl;  // input / param vars in declaration order (manifest order)
   int64_t last_launches = 0;
@@ -496,7 +499,42 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
       h->conv_cache = &l.cache;
       h->fuse_relu = l.relu_out >= 0 ? g->vars[l.relu_out].value : nullptr;
       h->fuse_relu_done = false;
+      // conv -> relu -> conv (AlexNet conv3 -> conv4 -> conv5): this forward's
+      // epilogue also writes relu(y) into the next conv's x grid, whose
+      // forward and weight gradient then skip their input transform
+      Layer* nxt = nullptr;
+      XGridPlan xp{};
+      if (g->producer_grid && g->math == CK_MATH_TF32 && l.relu_out >= 0) {
+        const Var& rv = g->vars[l.relu_out];
+        if (rv.consumers.size() == 1 && rv.consumers[0].second == 0) {
+          Layer& c2 = g->layers[rv.consumers[0].first];
+          if (c2.kind == Kind::conv) {
+            const ConvDims d2 = conv_dims(rv.shape, g->vars[c2.in[1]].shape,
+                                          g->vars[c2.out[0]].shape, conv_geom_of(c2));
+            if (conv_tc_xgrid_plan(d2, &xp) && xp.Cg % 32 == 0) {
+              float* buf = (float*)c2.cache.buf.get(xp.bytes, s);
+              if (!buf) throw Err(CK_ERR_CUDA, "x grid allocation failed");
+              if (c2.cache.zero_ptr != buf || c2.cache.zero_key != xp.key) {
+                check_cuda(cudaMemsetAsync(buf, 0, c2.cache.buf.bytes, s), "zero");
+                c2.cache.zero_ptr = buf;
+                c2.cache.zero_key = xp.key;
+              }
+              h->next_xg = buf;
+              h->next_xg_plan = xp;
+              h->next_xg_done = false;
+              nxt = &c2;
+            }
+          }
+        }
+      }
       st = ck_conv_forward(h, &x, &f, l.in.size() > 2 ? &b : nullptr, &cg, &y, g->math, s);
+      if (nxt && st == CK_OK && h->next_xg_done) {
+        nxt->cache.valid = true;
+        nxt->cache.src = g->vars[l.relu_out].value;
+        nxt->cache.key = xp.key;
+      }
+      h->next_xg = nullptr;
+      h->next_xg_done = false;
       h->conv_cache = nullptr;
       h->fuse_relu = nullptr;
       if (l.relu_out >= 0) {
@@ -1267,6 +1305,8 @@ ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value) {
     g->lrn_grid = value != 0;
   else if (n == "lrn_pool")
     g->lrn_pool = value != 0;
+  else if (n == "producer_grid")
+    g->producer_grid = value != 0;
   else
     throw Err(CK_ERR_ARG, "unknown graph option '" + n + "'");
   CKG_END(g)

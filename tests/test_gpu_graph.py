@@ -328,6 +328,37 @@ def test_lrn_maxpool_fusion_bitexact(batch):
         assert np.array_equal(d0[n], d1[n]), n
 
 
+@pytest.mark.parametrize("batch", [5, 32])
+def test_producer_written_x_grid_bitexact(batch):
+    """conv3 -> relu3 -> conv4 -> relu4 -> conv5 (TF32): each forward epilogue
+    also writes relu(y) into the next conv's padded pixel-major x grid, whose
+    forward and weight gradient then skip their input transform.  Every
+    value and derivative is bit-identical to the transform path, and the
+    engine launches two kernels fewer per forward."""
+    from paper_1412_4564_b200 import nets
+    net = nets.alexnet(batch=batch)
+    out = []
+    for on in (True, False):
+        g = device_graph(net, "tf32")
+        g.set_option("producer_grid", on)
+        for k, v in {**net.init_params(), **net.init_inputs()}.items():
+            g.set(k, v)
+        l0 = g.hd.launches
+        g.forward()
+        launches = g.hd.launches - l0
+        g.backward("objective")
+        names = set(net.inputs) | {p[0] for p in net.params} | \
+            {o for layer in net.layers for o in layer[3]}
+        out.append(({n: g.get(n) for n in sorted(names)},
+                    {n: g.get(n, deriv=True) for n in sorted(names) if n != "label"}, launches))
+    (v0, d0, l0), (v1, d1, l1) = out
+    assert l0 == l1 - 2
+    for n in v1:
+        assert np.array_equal(v0[n], v1[n]), n
+    for n in d1:
+        assert np.array_equal(d0[n], d1[n]), n
+
+
 @pytest.mark.parametrize("cout,groups,size", [(64, 2, 5), (48, 1, 5), (96, 1, 3), (64, 1, 4)])
 def test_lrn_grid_envelope(cout, groups, size, monkeypatch):
     """conv -> relu -> lrn -> pool -> fc on a small image: inside the fused
