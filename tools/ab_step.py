@@ -11,6 +11,7 @@ ap.add_argument("--lib", default="")
 ap.add_argument("--net", default="alexnet")
 ap.add_argument("--steps", type=int, default=30)
 ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--option", action="append", default=[], help="engine option name=value")
 a = ap.parse_args()
 if a.lib:
     from paper_1412_4564_b200 import _lib
@@ -24,6 +25,9 @@ net = nets.NETS[a.net](batch=a.batch or nets.DEFAULT_BATCH[a.net])
 g = Graph(math="tf32")
 net.build(g)
 g.finalize()
+for o in a.option:
+    k, v = o.split("=")
+    g.set_option(k, int(v))
 for k, v in {**net.init_params(), **net.init_inputs()}.items():
     g.set(k, v)
 t = Trainer(g, lr=0.01 / net.batch)  # cnn_train: the step is scaled by the batch (sum loss)
@@ -41,4 +45,5 @@ for rep in range(3):
     e1.record(st)
     torch.cuda.synchronize()
     res.append(e0.elapsed_time(e1) / a.steps)
-print(f"{a.net} {a.lib or 'libck.so'}: ms/step " + " ".join(f"{v:.3f}" for v in res))
+print(f"{a.net} {a.lib or 'libck.so'} {' '.join(a.option)}: ms/step "
+      + " ".join(f"{v:.3f}" for v in res))
