@@ -121,18 +121,29 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self, which):
+        """Host time of the timed region's start ('t0') / end ('t1')."""
+        setattr(self, which, time.perf_counter())
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)  # let a sample land after a short timed region
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        # samples inside the timed region (100 ms period, so a short region
+        # is bracketed by the nearest sample on either side)
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        lines = [ln for t, ln in self.lines if t0 is None or (t0 - 0.1 <= t <= t1 + 0.1)]
+        if not lines and self.lines:
+            lines = [min(self.lines, key=lambda tl: abs(tl[0] - (t0 or 0)))[1]]
         sm, mx, reasons = [], [], set()
-        for ln in self.lines:
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -399,11 +410,12 @@ def main():
     # CUDA-graph replay of the step: warm-up step 1 runs eagerly (sizes every
     # workspace), step 2 is captured, the rest (and the timed steps) replay it.
     tr.set_graph(not args.no_graph)
+    clocks = ClockSampler(local)
+    clocks.start()  # running through the warm-up: samples exist when the region is short
     for _ in range(max(args.warmup, 3)):
         tr.step(want_loss=False, stream=sp)
     barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark("t0")
     launches0, tc0 = g.hd.launches, g.hd.tc_launches
     with torch.cuda.stream(stream):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -412,6 +424,7 @@ def main():
             tr.step(want_loss=False, stream=sp)
         e1.record(stream)
     barrier()
+    clocks.mark("t1")
     clk = clocks.stop()
     launches = g.hd.launches - launches0  # total inside the timed region
     tc_launches = g.hd.tc_launches - tc0
