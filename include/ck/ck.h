@@ -316,7 +316,10 @@ ck_status ck_graph_layer_ms(ck_graph* g, int layer, float* fwd_ms, float* bwd_ms
  *   (the pool reads the LRN values from shared memory, not HBM; bit-identical,
  *   measured slower than the two tuned kernels on AlexNet);
  *   "producer_grid" (default 1): a TF32 conv -> relu -> conv forward writes the
- *   second conv's padded x grid from the first conv's epilogue. */
+ *   second conv's padded x grid from the first conv's epilogue;
+ *   "dgrad_grid" (default 1): a TF32 conv -> relu -> conv backward writes the
+ *   first conv's ReLU-gated dy grid (and bias partials) from the second conv's
+ *   data-gradient epilogue. */
 ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value);
 
 /* ---- cnn_train training step with multi-GPU data parallelism ------------ */

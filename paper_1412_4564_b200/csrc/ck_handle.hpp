@@ -55,6 +55,15 @@ struct ck_handle {
   float* next_xg = nullptr;
   ck::XGridPlan next_xg_plan{};
   bool next_xg_done = false;
+  // engine, conv -> relu -> conv backward: the second conv's data-gradient
+  // epilogue also writes the first conv's relu-gated dy grid (prev_dyg, laid
+  // out by prev_dyg_plan; gate: prev_gate > 0, the second conv's input x)
+  // and that grid's bias partials (prev_bpart, [32-pixel warp][Cp] doubles)
+  float* prev_dyg = nullptr;
+  double* prev_bpart = nullptr;
+  const float* prev_gate = nullptr;
+  ck::GridPlan prev_dyg_plan{};
+  bool prev_dyg_done = false;
   // engine, fused bnorm -> relu: per-channel (mu, inv) of the forward, which
   // the backward uses to recompute the relu gate from x (2 floats / channel)
   float* bn_muinv = nullptr;
@@ -138,15 +147,7 @@ bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, i
 // (key: x_grid's cache key).  conv_tc_xgrid_plan says whether conv d reads x
 // only through it, so the layer producing x may write it instead.
 bool conv_tc_xgrid_plan(const ConvDims& d, XGridPlan* xp);
-// The dy grid a TF32 conv backward consumes (dy at (0, 0) of an Hg x Wg grid,
-// Kgp padded channels per group): conv_tc_grid_plan says whether BOTH the
-// weight and data gradient of d read dy only through that grid, and how it
-// is laid out (key: dy_grid's cache key).
-struct GridPlan {
-  int Hg, Wg, Kg, Kgp, groups, OH, OW;
-  int64_t key;
-  size_t bytes;
-};
+// (GridPlan: ck_internal.hpp)
 bool conv_tc_grid_plan(const ConvDims& d, GridPlan* gp);
 // capi.cu: compute a dy the gated transform left pending (h->pending_dy == dy)
 void materialize_pending_dy(ck_handle* h, const float* dy, cudaStream_t s);

@@ -93,6 +93,16 @@ struct XGridPlan {
   size_t bytes;
 };
 
+// The dy grid a TF32 conv backward consumes (dy at (0, 0) of an Hg x Wg grid,
+// Kgp padded channels per group): conv_tc_grid_plan (ck_handle.hpp) says
+// whether BOTH the weight and data gradient of a conv read dy only through
+// that grid, and how it is laid out (key: dy_grid's cache key).
+struct GridPlan {
+  int Hg, Wg, Kg, Kgp, groups, OH, OW;
+  int64_t key;
+  size_t bytes;
+};
+
 // Per-handle scratch owned by the C ABI / engine.
 struct Workspace {
   void* ptr = nullptr;

@@ -69,8 +69,10 @@ enum EpiKind : int {
 // CK_EXPERIMENTS builds; a product kernel always does all of its work.
 #ifdef CK_EXPERIMENTS
 #define TC_EXP(p) ((p).exp)
+#define DG_SKIP(p) ((p).dg_skip)
 #else
 #define TC_EXP(p) 0
+#define DG_SKIP(p) 0
 #endif
 
 struct GemmParams {
@@ -113,6 +115,15 @@ struct GemmParams {
   // image grid, channel c -> g'*gx_Cgp + (c - g'*gx_Cg), g' = c / gx_Cg
   float* gx;
   int gx_Hg, gx_Wg, gx_Cp, gx_Cg, gx_Cgp, gx_pt, gx_pl, gx_OH;
+  // gx with gx_gate (a data gradient, no relu / bias / accumulate): the grid
+  // gets gx_gate > 0 ? v : 0 (gx_gate laid out like out: the relu output that
+  // fed this conv) instead of relu(v) -- the conv below's relu-gated dy grid --
+  // and gx_bpart[(m / 32) * gx_Cp + grid channel] the per-32-row column sums
+  // of those values (its bias-gradient partials)
+  const float* gx_gate;
+  double* gx_bpart;
+  int dg_skip;  // CK_EXPERIMENTS: 1 no gate loads, 2 no grid store, 4 no bias partials
+  int estage;   // gx: kEpiWarps 32 x 32 float stages after the barriers (coalesced grid rows)
   int BM;                 // 128 or 256 (two M=128 MMAs sharing the B tile)
   int nacc;               // TMEM accumulator buffers (2: epilogue overlaps mainloop)
   int groups;             // tiles = ceil(M/BM) * ceil(N/BN) * groups * splits
@@ -492,7 +503,7 @@ __device__ __forceinline__ float epi_unit_bias(const GemmParams& p, const Tile& 
 
 __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T, uint32_t tacc,
                                               bool empty_split, int halves, int warp, int lane,
-                                              float bias_first) {
+                                              float bias_first, float* estage = nullptr) {
   const int q = warp & 3;
   const int cpart = (warp - 2) / 4, cparts = kEpiWarps / 4;
   float* out = p.out;
@@ -501,7 +512,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
   // plain stores: split-K partials, or no bias / relu / accumulate
   // per-column (EPI_PIX) bias is added to the TMEM values before the stores
   const bool col_bias = p.bias && !partial && p.epi == EPI_PIX;
-  const bool plain = partial || ((!p.bias || col_bias) && !p.relu && !p.acc && !p.out2);
+  const bool plain = partial || ((!p.bias || col_bias) && !p.relu && !p.acc && !p.out2 && !p.gx);
   const int64_t ld = p.ld;
   // (half, 32-column chunk) units dealt to the cparts warps of a lane quarter
   // in snake order (odd halves walk the chunks backwards): balanced when a
@@ -546,6 +557,14 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
       const int col0 = T.n0 + c0;
       // columns of this chunk inside both the tile and the matrix
       const int lim = min(min(32, p.BN - c0), p.n_valid - col0);
+      // gx_gate: this row's 32 gate values, loaded before the accumulator read
+      // (independent loads in flight; the stores below may not alias them)
+      float gv[32];
+      if (p.gx_gate && !(DG_SKIP(p) & 1)) {
+        const float* gsrc = p.gx_gate + row_base + (int64_t)col0 * ld;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) gv[j] = row_ok && j < lim ? __ldg(gsrc + j * ld) : 0.f;
+      }
       // per-column bias (lane j holds column j, loaded one unit ahead): broadcast by shuffle
       CK_LD32(r, taddr);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -580,6 +599,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
             if (j < lim) dst[j * ld] = __uint_as_float(r[j]);
         } else {
           float* dst2 = p.out2 ? p.out2 + row_base + (int64_t)col0 * ld : nullptr;
+          const bool gate = p.gx_gate != nullptr && !(DG_SKIP(p) & 1);
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (j < lim) {
@@ -588,12 +608,12 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
               if (p.relu) v = v > 0.f ? v : 0.f;
               if (p.acc) v = __fadd_rn(dst[j * ld], v);
               dst[j * ld] = v;
-              const float rv = v > 0.f ? v : 0.f;
+              const float rv = gate ? (gv[j] > 0.f ? v : 0.f) : (v > 0.f ? v : 0.f);
               if (dst2) dst2[j * ld] = rv;  // fused relu layer
               r[j] = __float_as_uint(rv);
             }
           }
-          if (p.gx) {
+          if (p.gx && !(DG_SKIP(p) & 2) && !(estage && lim == 32)) {
             // the next conv's x grid: this pixel's 32 consecutive channels are
             // one contiguous 128-byte run of its grid row (host: gx_Cg % 32 == 0)
             const int oj = pix / p.gx_OH, oi = pix - oj * p.gx_OH;
@@ -615,6 +635,86 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
             }
           }
         }
+      }
+      if (estage && p.gx && lim == 32 && !(DG_SKIP(p) & 2)) {  // warp-uniform
+        // grid rows through this warp's shared stage: lane = row writes its 32
+        // values as 8 16-byte chunks (xor-swizzled by row: conflict-free), then
+        // lane (q4, m4) stores chunk m4 of row 4 it + q4 -- each instruction
+        // writes 4 whole 128-byte grid rows instead of 32 half sectors
+        const int colg = T.grp * (int)p.grp_col + col0;
+        const int g2 = colg / p.gx_Cg;
+        const int cbase = g2 * p.gx_Cgp + (colg - g2 * p.gx_Cg);
+        int growi = -1;  // this lane's grid row offset (host: grid < 2^31 floats)
+        if (row_ok && !partial && p.epi == EPI_PIX) {
+          const int oj = pix / p.gx_OH, oi = pix - oj * p.gx_OH;
+          growi = (int)((((int64_t)img * p.gx_Wg + oj + p.gx_pl) * p.gx_Hg + oi + p.gx_pt) *
+                        p.gx_Cp);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          *reinterpret_cast<float4*>(estage + lane * 32 + ((k ^ (lane & 7)) << 2)) =
+              make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                          __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
+        __syncwarp();
+        const int q4 = lane >> 3, m4 = lane & 7;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int row = 4 * it + q4;
+          const int gr = __shfl_sync(0xffffffffu, growi, row);
+          const float4 v =
+              *reinterpret_cast<const float4*>(estage + row * 32 + ((m4 ^ (row & 7)) << 2));
+          if (gr >= 0) {
+            *reinterpret_cast<float4*>(p.gx + gr + cbase + 4 * m4) = v;
+            s0 = __fadd_rn(s0, v.x);
+            s1 = __fadd_rn(s1, v.y);
+            s2 = __fadd_rn(s2, v.z);
+            s3 = __fadd_rn(s3, v.w);
+          }
+        }
+        if (p.gx_bpart && !(DG_SKIP(p) & 4)) {
+          // column sums over the 32 rows: 8 rows per lane in order, then the 4
+          // row lanes of a chunk by a fixed xor tree
+#pragma unroll
+          for (int o = 8; o <= 16; o <<= 1) {
+            s0 = __fadd_rn(s0, __shfl_xor_sync(0xffffffffu, s0, o));
+            s1 = __fadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, o));
+            s2 = __fadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, o));
+            s3 = __fadd_rn(s3, __shfl_xor_sync(0xffffffffu, s3, o));
+          }
+          const int mw = T.m0 + h * 128 + q * 32;  // this warp's first row
+          if (q4 == 0) {
+            double* bp = p.gx_bpart + (int64_t)(mw >> 5) * p.gx_Cp + cbase + 4 * m4;
+            bp[0] = s0;
+            bp[1] = s1;
+            bp[2] = s2;
+            bp[3] = s3;
+          }
+        }
+      } else if (p.gx_bpart && lim > 0 && !(DG_SKIP(p) & 4)) {  // warp-uniform
+        // column sums of the gated grid values over this warp's 32 rows:
+        // transpose-reduce (lane l ends with column l), a fixed tree
+        __syncwarp();
+        const bool okrow = row_ok && !partial;
+        float* v = gv;  // (the gates are consumed)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = okrow && j < lim ? __uint_as_float(r[j]) : 0.f;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const bool upper = lane & o;
+#pragma unroll
+          for (int j = 0; j < o; ++j) {
+            const float send = upper ? v[j] : v[j + o];
+            const float keep = upper ? v[j + o] : v[j];
+            v[j] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
+          }
+        }
+        const int col = T.grp * (int)p.grp_col + col0 + lane;
+        const int g2 = col / p.gx_Cg;
+        const int mw = T.m0 + h * 128 + q * 32;  // this warp's first row
+        if (lane < lim)
+          p.gx_bpart[(int64_t)(mw >> 5) * p.gx_Cp + g2 * p.gx_Cgp + (col - g2 * p.gx_Cg)] = v[0];
       }
       __syncwarp();  // reconverge before the next warp-wide tcgen05.ld
     }
@@ -697,6 +797,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // gx: per epilogue warp a 32 x 32 float stage after the 256 barrier bytes
+  float* estage = p.estage && warp >= 2
+                      ? (float*)(sB + S * stage_b + 256) + (warp - 2) * 32 * 32
+                      : nullptr;
   const int tm = (p.M + p.BM - 1) / p.BM, tn = (p.N + p.BN - 1) / p.BN;
   const int total = tm * tn * p.groups * p.splits;
   const int acc_cols = halves * p.BN;  // TMEM columns per accumulator buffer
@@ -956,7 +1060,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       if (TC_EXP(p) != 5)  // exp 5: no epilogue work
         epilogue_tile(p, T, tmem + (uint32_t)(ab * acc_cols), T.kb0 >= T.kb1, halves, warp, lane,
-                      bias0);
+                      bias0, estage);
       tc_fence_before();
       __syncwarp();
 #ifdef CK_TC_PROFILE
@@ -1749,9 +1853,12 @@ static void launch(const CUtensorMap& a, const CUtensorMap& b, GemmParams p, int
   p.nacc = (2 * halves * p.BN <= 512) ? 2 : 1;
   if (p.kstage != 64) p.kstage = 32;
   const int stage_bytes = (p.BM + p.BN) * p.kstage * 4;
-  const int budget = 227 * 1024 - 1024 - 256;
+  // grid-writing epilogues (gx) stage their rows in shared memory
+  const int estage_bytes = p.gx ? kEpiWarps * 32 * 32 * 4 : 0;
+  const int budget = 227 * 1024 - 1024 - 256 - estage_bytes;
   p.stages = std::min(8, budget / stage_bytes);
-  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + 256;
+  p.estage = estage_bytes > 0;
+  const size_t smem = 1024 + (size_t)p.stages * stage_bytes + 256 + estage_bytes;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(tc_gemm_kernel<AK, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2635,7 +2742,8 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
   p.bias = bias; p.relu = relu; p.acc = 0; p.n_valid = Kg;
   p.BM = pick_bm(p.M, p.BN, true, (Kg + p.BN - 1) / p.BN * d.groups);
   if (on_grid) p.pt = p.pl = 0;
-  if (h->next_xg && h->fuse_relu && Kg % 32 == 0) {
+  if (h->next_xg && h->fuse_relu && Kg % 32 == 0 &&
+      h->next_xg_plan.bytes / sizeof(float) < (size_t(1) << 31)) {
     // engine: also write relu(y) into the consumer conv's x grid
     const XGridPlan& xp = h->next_xg_plan;
     p.gx = h->next_xg;
@@ -2765,6 +2873,21 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   p.img_stride = (int64_t)d.C * d.H * d.W; p.grp_col = d.Cg; p.epi_OHW = d.H * d.W;
   p.bias = nullptr; p.relu = 0; p.acc = acc; p.n_valid = d.Cg;
   p.BM = pick_bm(p.M, p.BN, true, (d.Cg + p.BN - 1) / p.BN * d.groups);
+  if (h->prev_dyg && !acc && d.Cg % 32 == 0) {
+    // engine, conv -> relu -> this conv: also write the conv below's
+    // relu-gated dy grid and its bias partials (ck_handle.hpp prev_dyg)
+    const GridPlan& gp = h->prev_dyg_plan;
+    if (gp.Kg % 32 == 0 && gp.Kgp == gp.Kg && gp.Kg * gp.groups == d.C && gp.OH == d.H &&
+        gp.OW == d.W && (int64_t)d.N * gp.Hg * gp.Wg * gp.Kgp * gp.groups < (1ll << 31)) {
+      p.gx = h->prev_dyg;
+      p.gx_Hg = gp.Hg; p.gx_Wg = gp.Wg; p.gx_Cp = gp.Kgp * gp.groups; p.gx_Cg = gp.Kg;
+      p.gx_Cgp = gp.Kgp; p.gx_pt = 0; p.gx_pl = 0; p.gx_OH = d.H;
+      p.gx_gate = h->prev_gate;
+      p.gx_bpart = h->prev_bpart;
+      p.dg_skip = knob("CK_DG_SKIP", 0);
+      h->prev_dyg_done = true;
+    }
+  }
   CUtensorMap ta = map_im2col(dyt, Kp, Hg, Wg, d.N, -qt, -ql, d.H - Hg - qt, d.W - Wg - ql, 1, 1,
                               p.BM);
   CUtensorMap tb = map_2d(gt, (uint64_t)taps * Kgp, d.C, (uint64_t)taps * Kgp, p.BN);

@@ -163,6 +163,10 @@ struct ck_graph {
   // option "producer_grid": a conv -> relu -> conv forward writes the next
   // conv's x grid from its epilogue (default on)
   bool producer_grid = true;
+  // option "dgrad_grid": a conv -> relu -> conv backward writes the first
+  // conv's relu-gated dy grid from the second conv's data-gradient epilogue
+  // (default on)
+  bool dgrad_grid = true;
   std::vector<std::pair<std::string, std::string>> meta;  // manifest metadata
   std::vector<int> decl;  // input / param vars in declaration order (manifest order)
   int64_t last_launches = 0;
@@ -706,6 +710,42 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
         h->fuse_relu_dy = g->vars[l.relu_out].deriv;
         h->fuse_relu_lazy = true;
       }
+      // conv -> relu -> this conv (AlexNet conv3 -> conv4 -> conv5): this data
+      // gradient's epilogue also writes the conv below's relu-gated dy grid
+      // and bias partials; that conv's backward then skips its dy transform
+      Layer* below = nullptr;
+      GridPlan bgp{};
+      int brows = 0;
+      if (g->dgrad_grid && g->math == CK_MATH_TF32 && !a0 && a0 == a1 && a1 == a2) {
+        const Var& xv = g->vars[l.in[0]];
+        if (xv.producer >= 0 && xv.consumers.size() == 1) {
+          Layer& r = g->layers[xv.producer];
+          if (r.kind == Kind::relu && r.fused_by >= 0 && r.fused_bwd &&
+              g->layers[r.fused_by].kind == Kind::conv) {
+            Layer& c = g->layers[r.fused_by];
+            const ConvDims cd = conv_dims(g->vars[c.in[0]].shape, g->vars[c.in[1]].shape,
+                                          g->vars[c.out[0]].shape, conv_geom_of(c));
+            if (c.in.size() > 2 && !c.pre_grid && conv_tc_grid_plan(cd, &bgp) &&
+                bgp.Kg % 32 == 0) {
+              float* old = (float*)c.dyg.ptr;
+              float* grid = (float*)c.dyg.get(bgp.bytes, s);
+              if (!grid) throw Err(CK_ERR_CUDA, "dy grid allocation failed");
+              if (grid != old)  // the grid's junk rows stay zero from here on
+                check_cuda(cudaMemsetAsync(grid, 0, c.dyg.bytes, s), "zero");
+              brows = (int)(((int64_t)cd.N * cd.OH * cd.OW + 31) / 32);
+              double* bp =
+                  (double*)c.bpart.get(sizeof(double) * (size_t)brows * bgp.Kgp * bgp.groups, s);
+              if (!bp) throw Err(CK_ERR_CUDA, "bias partial allocation failed");
+              h->prev_dyg = grid;
+              h->prev_bpart = bp;
+              h->prev_gate = xv.value;
+              h->prev_dyg_plan = bgp;
+              h->prev_dyg_done = false;
+              below = &c;
+            }
+          }
+        }
+      }
       struct Reset {
         ck_handle* h;
         ~Reset() {
@@ -717,6 +757,10 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
           h->pre_dyg = nullptr;
           h->pre_dyg_src = nullptr;
           h->pre_bpart = nullptr;
+          h->prev_dyg = nullptr;
+          h->prev_bpart = nullptr;
+          h->prev_gate = nullptr;
+          h->prev_dyg_done = false;
         }
       } reset{h};
       if (a0 == a1 && a1 == a2) {
@@ -725,6 +769,11 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
         if (st == CK_OK && fused && h->fuse_relu_pending) {
           g->vars[l.out[0]].lazy_gate = l.out[0];
           g->vars[l.out[0]].lazy_src = l.relu_out;
+        }
+        if (st == CK_OK && below && h->prev_dyg_done) {
+          below->pre_grid = true;
+          below->plan = bgp;
+          below->pre_rows = brows;
         }
       } else {
         st = ck_conv_backward(h, &x, &f, &cg, &dy, &dx, nullptr, nullptr, a0, g->math, s);
@@ -1307,6 +1356,8 @@ ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value) {
     g->lrn_pool = value != 0;
   else if (n == "producer_grid")
     g->producer_grid = value != 0;
+  else if (n == "dgrad_grid")
+    g->dgrad_grid = value != 0;
   else
     throw Err(CK_ERR_ARG, "unknown graph option '" + n + "'");
   CKG_END(g)

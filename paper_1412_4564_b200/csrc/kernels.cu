@@ -32,6 +32,22 @@ inline int blocks_for(int64_t n, int threads, int per_sm = 16) {
   return (int)b;
 }
 
+// x^e as __powf computes it, ex2(e * lg2(x)), minus __powf's subnormal
+// argument / result scaling: the same bits whenever x and x^e are normal
+// floats.  The LRN kernels below use it only when kappa >= FLT_MIN and
+// alpha >= 0 (L = kappa + alpha * sum >= kappa is normal) and beta <= 0.98
+// (L^-beta >= 2^-126 for every finite L) -- lrn_pow_fast_ok() on the host.
+__device__ __forceinline__ float pow_normal(float x, float e) {
+  float l, r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(__fmul_rn(l, e)));
+  return r;
+}
+
+inline bool lrn_pow_fast_ok(float kappa, float alpha, float beta) {
+  return kappa >= 1.17549435e-38f && alpha >= 0.f && beta <= 0.98f;
+}
+
 // ---------------------------------------------------------------- ReLU ----
 // activation.cpp:8-12 (y = x > 0 ? x : 0) and :15-22 (dx = x > 0 ? dy : 0).
 
@@ -711,7 +727,7 @@ __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y
 #pragma unroll
       for (int i = 0; i < NW; ++i) acc = __fadd_rn(acc, sq[i]);
       // fast-math power (MUFU lg2/ex2, a few ulp; normalize.cpp uses std::pow)
-      const float scale = __powf(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
+      const float scale = pow_normal(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
       *yq = __fmul_rn(xv[DOWN], scale);
 #pragma unroll
       for (int i = 0; i < NW - 1; ++i) {
@@ -809,7 +825,7 @@ __global__ void __launch_bounds__(320) lrn_maxpool3s2_k(
       float acc = 0.f;
 #pragma unroll
       for (int q = 0; q < NW; ++q) acc = __fadd_rn(acc, sq[q]);
-      const float scale = __powf(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
+      const float scale = pow_normal(__fadd_rn(kappa, __fmul_rn(alpha, acc)), nbeta);
       const float v = __fmul_rn(xv[DOWN], scale);
       if (owned && k0 + u < C) yq[(int64_t)(k0 + u) * HW] = v;
       if (in_tile) tile[buf][u][tj][ti] = v;
@@ -949,7 +965,7 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
       float L = 0.f, xj = 0.f, gj = 0.f, et = 0.f;
       if (compute) {
         const float Lj = __fadd_rn(kappa, __fmul_rn(alpha, sqsum));
-        L = __powf(Lj, nb);  // L^-beta; L^(-beta-1) = L^-beta / L
+        L = pow_normal(Lj, nb);  // L^-beta; L^(-beta-1) = L^-beta / L
         xj = xw[DOWN];
         gj = gj_in;
         et = __fmul_rn(__fmul_rn(gj, __fdividef(L, Lj)), xj);
@@ -1055,6 +1071,171 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
         if (j < J) step(j, xl, gi, j < C, j >= DOWN, (u + 8 - DOWN) & 7);
         dq += HW;
       }
+    }
+  }
+}
+
+// lrn_bwd_reg_k<NW, false, true> restructured around the 32-channel runs of
+// the grid store (same per-element float operations, so the grid values are
+// bit-identical): the channel loop is unrolled by 32, so the stage slot, the
+// prefetch ring slot and the flush point are compile-time constants (no
+// per-channel index or branch arithmetic; this kernel was issue-bound at
+// ~84 instructions per element), and each flush writes four pixels' 128-byte
+// runs per instruction as float4 (lane = 4 channels of one of 4 pixels).
+// Every chunk's loads are in range except the last chunk's (CHK variant).
+// Bias partials: per warp, per channel, the 32 pixels summed as 8 per lane in
+// pixel order and then across the 4 pixel lanes by a fixed xor tree (float),
+// stored as [pixel warp][Cp] doubles like the generic kernel.
+template <int NW>
+__global__ void __launch_bounds__(128, CK_LRN_GRID_MINB)
+    lrn_bwd_grid_k(const float* __restrict__ x, const float* __restrict__ dy, int HW, int C,
+                   int64_t pixels, float kappa, float alpha, float beta, LrnGridOut go) {
+  ck::pdl_entry();
+  constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
+  constexpr int P = 8;  // prefetch distance (channels); divides 32
+  const float nb = -beta;
+  const float c2ab = __fmul_rn(__fmul_rn(2.f, alpha), beta);
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  __shared__ float gsm[4][32][33];  // per warp [pixel][channel of the run]
+  __shared__ int grs[4][32];        // per warp: pixel grid row offsets (-1: none)
+  const int q4 = lane >> 3, m4 = lane & 7;  // flush role: pixel-in-quad, channel quad
+  for (int64_t eb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; eb < pixels;
+       eb += (int64_t)gridDim.x * blockDim.x) {
+    const bool live = eb + lane < pixels;
+    const int64_t e = live ? eb + lane : pixels - 1;
+    const int64_t n = e / HW;
+    const int p = (int)(e - n * HW);
+    {
+      const int i = p % go.H, jj = p / go.H;
+      const int grow0 = (int)(((int64_t)n * go.Hg * go.Wg + i + (int64_t)go.Hg * jj) * go.Cp);
+      __syncwarp();  // the previous pixel group's flushes are done with grs
+      grs[wib][lane] = live ? grow0 : -1;
+    }
+    const int64_t base = n * C * HW + p;
+    const float* xp = x + base;
+    const float* gp = dy + base;
+    auto ldx = [&](int t) { return (t >= 0 && t < C) ? __ldg(xp + (int64_t)t * HW) : 0.f; };
+    auto ldg = [&](int t) { return t < C ? __ldg(gp + (int64_t)t * HW) : 0.f; };
+    float xw[NW], sq[NW];  // x window of the lead index j: x[j - DOWN + i]
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      xw[i] = ldx(i - DOWN);
+      sq[i] = __fmul_rn(xw[i], xw[i]);
+    }
+    float xpre[P], gpre[P];  // ring slot j % P: x[j + UP + 1], dy[j]
+#pragma unroll
+    for (int u = 0; u < P; ++u) {
+      xpre[u] = ldx(UP + 1 + u);
+      gpre[u] = ldg(u);
+    }
+    const float* lx = xp + (int64_t)(P + UP + 1) * HW;  // next prefetch addresses
+    const float* lg = gp + (int64_t)P * HW;
+    float eta[NW];
+    float Ls[DOWN + 1], xs[DOWN + 1], gs[DOWN + 1];
+    float sqsum = 0.f, etasum = 0.f;
+#pragma unroll
+    for (int i = 0; i < NW; ++i) sqsum = __fadd_rn(sqsum, sq[i]);
+#pragma unroll
+    for (int i = 0; i < NW; ++i) eta[i] = 0.f;
+#pragma unroll
+    for (int i = 0; i <= DOWN; ++i) Ls[i] = xs[i] = gs[i] = 0.f;
+    float* stage = &gsm[wib][lane][0];
+    // step j (ring slot j % P): consume the prefetched lead x / dy, refill the
+    // slot with index j + P, compute index j (if j < C), return the value of
+    // store index j - DOWN (relu-gated)
+    auto step = [&](int j, int slot, bool chk) -> float {
+      const float xlead = xpre[slot], gj_in = gpre[slot];
+      if (!chk) {
+        xpre[slot] = __ldg(lx);
+        gpre[slot] = __ldg(lg);
+      } else {
+        xpre[slot] = j + P + UP + 1 < C ? __ldg(lx) : 0.f;
+        gpre[slot] = j + P < C ? __ldg(lg) : 0.f;
+      }
+      lx += HW;
+      lg += HW;
+      float L = 0.f, xj = 0.f, gj = 0.f, et = 0.f;
+      if (!chk || j < C) {
+        const float Lj = __fadd_rn(kappa, __fmul_rn(alpha, sqsum));
+        L = pow_normal(Lj, nb);
+        xj = xw[DOWN];
+        gj = gj_in;
+        et = __fmul_rn(__fmul_rn(gj, __fdividef(L, Lj)), xj);
+      }
+      etasum = __fadd_rn(__fsub_rn(etasum, eta[0]), et);
+#pragma unroll
+      for (int i = 0; i < NW - 1; ++i) eta[i] = eta[i + 1];
+      eta[NW - 1] = et;
+#pragma unroll
+      for (int i = 0; i < DOWN; ++i) {
+        Ls[i] = Ls[i + 1];
+        xs[i] = xs[i + 1];
+        gs[i] = gs[i + 1];
+      }
+      Ls[DOWN] = L;
+      xs[DOWN] = xj;
+      gs[DOWN] = gj;
+      const float r = __fadd_rn(__fmul_rn(gs[0], Ls[0]), -__fmul_rn(__fmul_rn(c2ab, xs[0]), etasum));
+      const float sqin = __fmul_rn(xlead, xlead);
+      sqsum = __fadd_rn(__fsub_rn(sqsum, sq[0]), sqin);
+#pragma unroll
+      for (int i = 0; i < NW - 1; ++i) {
+        xw[i] = xw[i + 1];
+        sq[i] = sq[i + 1];
+      }
+      xw[NW - 1] = xlead;
+      sq[NW - 1] = sqin;
+      return (live && xs[0] > 0.f) ? r : 0.f;
+    };
+    // steps 0 .. DOWN-1: nothing to store yet (checked: C may be tiny)
+#pragma unroll
+    for (int j = 0; j < DOWN; ++j) (void)step(j, j % P, true);
+    // run b: stores c = 32 b .. 32 b + 31 (steps j = c + DOWN), then the flush
+    auto flush = [&](int c0) {
+      __syncwarp();
+      const int g = c0 / go.Kg;
+      const int cpos = g * go.Kgp + (c0 - g * go.Kg) + 4 * m4;
+      float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int q = 4 * it + q4;
+        const int rq = grs[wib][q];
+        const float* src = &gsm[wib][q][4 * m4];
+        const float4 v = make_float4(src[0], src[1], src[2], src[3]);
+        s0 += v.x;
+        s1 += v.y;
+        s2 += v.z;
+        s3 += v.w;
+        if (rq >= 0) *reinterpret_cast<float4*>(go.grid + rq + cpos) = v;
+      }
+#pragma unroll
+      for (int o = 8; o <= 16; o <<= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+      }
+      if (q4 == 0) {
+        double* bp = go.bpart + (eb >> 5) * go.Cp + cpos;
+        bp[0] = s0;
+        bp[1] = s1;
+        bp[2] = s2;
+        bp[3] = s3;
+      }
+      __syncwarp();
+    };
+    const int runs = C / 32;
+    int b = 0;
+    // unchecked runs: every prefetch index < C (max j + P + UP + 1 in the run)
+    for (; b < runs && 32 * b + 31 + DOWN + P + UP + 1 < C; ++b) {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) stage[u] = step(32 * b + u + DOWN, (u + DOWN) % P, false);
+      flush(32 * b);
+    }
+    for (; b < runs; ++b) {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) stage[u] = step(32 * b + u + DOWN, (u + DOWN) % P, true);
+      flush(32 * b);
     }
   }
 }
@@ -1974,7 +2155,7 @@ void lrn_forward(const float* x, float* y, int H, int W, int C, int N, int size,
   const int HW = H * W;
   count_launch();
 #define CK_FWD(NW) lrn_fwd_reg<NW>(x, y, HW, C, N, kappa, alpha, beta, s)
-  CK_LRN_SWITCH(size, CK_FWD)
+  if (lrn_pow_fast_ok(kappa, alpha, beta)) CK_LRN_SWITCH(size, CK_FWD)
 #undef CK_FWD
   dim3 grid((HW + kLrnPix - 1) / kLrnPix, N);
   size_t smem = (size_t)C * kLrnPix * sizeof(float);
@@ -1985,6 +2166,7 @@ void lrn_forward(const float* x, float* y, int H, int W, int C, int N, int size,
 bool lrn_maxpool_forward(const float* x, float* y, float* py, const PoolDims& pd, int size,
                          float kappa, float alpha, float beta, cudaStream_t s, ConvCache* cache) {
   // 3x3 / stride-2 max pooling, pads top/left 0, windows covering the input
+  if (!lrn_pow_fast_ok(kappa, alpha, beta)) return false;
   if (pd.mode != 0 || pd.wh != 3 || pd.ww != 3 || pd.sh != 2 || pd.sw != 2 || pd.pt != 0 ||
       pd.pl != 0 || 2 * (pd.OH - 1) + 3 < pd.H || 2 * (pd.OW - 1) + 3 < pd.W)
     return false;
@@ -2020,7 +2202,7 @@ void lrn_backward(const float* x, const float* dy, float* dx, int H, int W, int 
   const int HW = H * W;
   count_launch();
 #define CK_BWD(NW) lrn_bwd_reg<NW>(x, dy, dx, HW, C, N, kappa, alpha, beta, acc, s)
-  CK_LRN_SWITCH(size, CK_BWD)
+  if (lrn_pow_fast_ok(kappa, alpha, beta)) CK_LRN_SWITCH(size, CK_BWD)
 #undef CK_BWD
   dim3 grid((HW + kLrnPix - 1) / kLrnPix, N);
   size_t smem = (size_t)3 * C * kLrnPix * sizeof(float);
@@ -2038,6 +2220,7 @@ bool lrn_backward_grid(const float* x, const float* dy, float* grid, double* bpa
   const int64_t pixels = (int64_t)HW * N;
   // 32-channel runs never cross a group (and every run completes)
   if (H > Hg || W > Wg || Kg * groups != C || Kg % 32 || C % 32) return false;
+  if (!lrn_pow_fast_ok(kappa, alpha, beta)) return false;
   // grid row offsets are kept as 32-bit ints in the kernel
   if ((int64_t)N * Hg * Wg * Kgp * groups >= (1ll << 31)) return false;
   LrnGridOut go{grid, bpart, H, Hg, Wg, Kg, Kgp, Kgp * groups};
@@ -2045,13 +2228,13 @@ bool lrn_backward_grid(const float* x, const float* dy, float* grid, double* bpa
   switch (size) {
     case 3:
       count_launch();
-      ck::pdl_launch(lrn_bwd_reg_k<3, false, true>, grid_dim, 128, 0, s, x, dy, nullptr, HW, C, pixels, kappa,
-                                                             alpha, beta, go);
+      ck::pdl_launch(lrn_bwd_grid_k<3>, grid_dim, 128, 0, s, x, dy, HW, C, pixels, kappa, alpha, beta,
+                     go);
       return true;
     case 5:
       count_launch();
-      ck::pdl_launch(lrn_bwd_reg_k<5, false, true>, grid_dim, 128, 0, s, x, dy, nullptr, HW, C, pixels, kappa,
-                                                             alpha, beta, go);
+      ck::pdl_launch(lrn_bwd_grid_k<5>, grid_dim, 128, 0, s, x, dy, HW, C, pixels, kappa, alpha, beta,
+                     go);
       return true;
     default:
       return false;

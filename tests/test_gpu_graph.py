@@ -359,6 +359,41 @@ def test_producer_written_x_grid_bitexact(batch):
         assert np.array_equal(d0[n], d1[n]), n
 
 
+@pytest.mark.parametrize("batch", [3, 16])
+def test_dgrad_writes_conv_dy_grid(batch):
+    """conv -> relu -> conv backward (AlexNet conv3 -> conv4 -> conv5): the
+    second conv's data-gradient epilogue also writes the first conv's
+    ReLU-gated dy grid and bias partials, so the first conv's backward skips
+    its dy transform (2 fewer launches).  Every value and derivative is
+    bit-identical to the unfused engine except the conv3/conv4 bias gradients
+    (32-row float partials in another fixed order): 1e-5 of the largest."""
+    from paper_1412_4564_b200 import nets
+    net = nets.alexnet(batch=batch)
+    out = []
+    for on in (True, False):
+        g = device_graph(net, "tf32")
+        g.set_option("dgrad_grid", on)
+        for k, v in {**net.init_params(), **net.init_inputs()}.items():
+            g.set(k, v)
+        g.forward()
+        l0 = g.hd.launches
+        g.backward("objective")
+        launches = g.hd.launches - l0
+        names = set(net.inputs) | {p[0] for p in net.params} | \
+            {o for layer in net.layers for o in layer[3]}
+        out.append(({n: g.get(n) for n in sorted(names)},
+                    {n: g.get(n, deriv=True) for n in sorted(names) if n != "label"}, launches))
+    (v0, d0, l0), (v1, d1, l1) = out
+    assert l0 == l1 - 2, (l0, l1)
+    for n in v1:
+        assert np.array_equal(v0[n], v1[n]), n
+    for n in d1:
+        if n in ("conv3b", "conv4b"):
+            assert np.abs(d0[n] - d1[n]).max() <= 1e-5 * (np.abs(d1[n]).max() + 1e-30), n
+        else:
+            assert np.array_equal(d0[n], d1[n]), n
+
+
 @pytest.mark.parametrize("cout,groups,size", [(64, 2, 5), (48, 1, 5), (96, 1, 3), (64, 1, 4)])
 def test_lrn_grid_envelope(cout, groups, size, monkeypatch):
     """conv -> relu -> lrn -> pool -> fc on a small image: inside the fused
