@@ -2655,14 +2655,19 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
     // Y[k, n] = sum_q F[q, k] X[q, n]   (A = filters, B = images, both K-major)
     const int Q = d.H * d.W * d.C;
     if (Q % 4 || d.K < 16) return false;
-    const int BN = pick_bn(std::min(d.N, 256));
+    // short reductions with a wave of 128 x 64 tiles (AlexNet fc7): no split-K
+    // partials / finish pass (measured fc7 0.034 -> 0.029 ms; fc6's 9216-long
+    // K keeps split-K, tools/fc_sweep.sh)
+    const bool wave64 = d.N > 64 && Q <= 4096 &&
+                        (int64_t)((d.K + 127) / 128) * ((d.N + 63) / 64) >= 128;
+    const int BN = wave64 ? 64 : pick_bn(std::min(d.N, 256));
     const int gm = (d.K + 127) / 128, gn = (d.N + BN - 1) / BN;
-    const int splits = split_for(gm * gn, rup(Q, 32) / 32);
+    const int splits = wave64 ? 1 : split_for(gm * gn, rup(Q, 32) / 32);
     GemmParams p{};
     p.M = d.K; p.N = d.N; p.K = rup(Q, 32); p.BN = BN; p.splits = splits;
     p.epi = EPI_LINEAR; p.ld = d.K; p.n_valid = d.N; p.relu = relu; p.bias = bias;
     p.out2 = h->fuse_relu;
-    p.BM = pick_bm(p.M, p.BN);
+    p.BM = wave64 ? 128 : pick_bm(p.M, p.BN);
     CUtensorMap ta = map_2d(f, Q, d.K, Q, p.BM);
     CUtensorMap tb = map_2d(x, Q, d.N, Q, BN);
     if (splits > 1) {
@@ -2785,13 +2790,16 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
     // (F[q + Q*k], q contiguous), B = dY K-major ([n][k]).
     const int Q = d.H * d.W * d.C;
     if (Q % 4 || d.K % 4) return false;
-    const int BN = pick_bn(std::min(d.N, 256));
+    // a wave of 128 x 128 tiles without split-K (AlexNet fc6: 72 x 2 tiles;
+    // measured 0.051 -> 0.041 ms, tools/fc_sweep.sh)
+    const bool wave128 = d.N > 128 && (int64_t)((Q + 127) / 128) * ((d.N + 127) / 128) >= 128;
+    const int BN = wave128 ? 128 : pick_bn(std::min(d.N, 256));
     const int gm = (Q + 127) / 128, gn = (d.N + BN - 1) / BN;
-    const int splits = split_for(gm * gn, rup(d.K, 32) / 32);
+    const int splits = wave128 ? 1 : split_for(gm * gn, rup(d.K, 32) / 32);
     GemmParams p{};
     p.M = Q; p.N = d.N; p.K = rup(d.K, 32); p.BN = BN; p.splits = splits;
     p.epi = EPI_LINEAR; p.ld = Q; p.n_valid = d.N; p.acc = acc;
-    p.BM = pick_bm(p.M, p.BN);
+    p.BM = wave128 ? 128 : pick_bm(p.M, p.BN);
     CUtensorMap ta = map_mn(f, d.K, Q, Q, p.BM, &p.a_mn3d);
     materialize_pending_dy(h, dy, s);  // this path reads dy itself
     CUtensorMap tb = map_2d(dy, d.K, d.N, d.K, BN);  // dY as [n][k]

@@ -329,40 +329,61 @@ struct FastDiv {  // n / d == (n * m) >> 40 for n * d < 2^39
   }
 };
 
+// Two outputs per thread per iteration (e and e + stride): both windows'
+// loads are in flight before the first compare.
 template <int WH, int WW, int SH, int SW, bool INSIDE>
 __global__ void pool_max_fwd_t(const float* __restrict__ x, float* __restrict__ y, PoolDims d,
                                FastDiv by_ohw, FastDiv by_oh, uint8_t* __restrict__ argout) {
   ck::pdl_entry();
   const int OHW = d.OH * d.OW, HW = d.H * d.W;
   const uint32_t total = (uint32_t)OHW * d.C * d.N;
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += gridDim.x * blockDim.x) {
-    const uint32_t plane = by_ohw.div(e);
-    const int w = (int)(e - plane * OHW);
-    const int oj = (int)by_oh.div(w), oi = w - oj * d.OH;
-    const int si = oi * SH - d.pt, sj = oj * SW - d.pl;
-    const float* xp = x + (size_t)plane * HW;
-    float best = 0.f;
-    bool have = false;
-    int code = 0;  // window offset a + WH*b of the winner
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += 2 * stride) {
+    float v[2][WW][WH];
+    bool in[2][WW][WH];
 #pragma unroll
-    for (int b = 0; b < WW; ++b) {
-      const int j = sj + b;
+    for (int t = 0; t < 2; ++t) {
+      const uint32_t e = e0 + t * stride;
+      const bool live = e < total;
+      const uint32_t ee = live ? e : e0;
+      const uint32_t plane = by_ohw.div(ee);
+      const int w = (int)(ee - plane * OHW);
+      const int oj = (int)by_oh.div(w), oi = w - oj * d.OH;
+      const int si = oi * SH - d.pt, sj = oj * SW - d.pl;
+      const float* xp = x + (size_t)plane * HW;
 #pragma unroll
-      for (int a = 0; a < WH; ++a) {
-        const int i = si + a;
-        if (INSIDE || (i >= 0 && i < d.H && j >= 0 && j < d.W)) {
-          const float v = __ldg(xp + i + d.H * j);
-          if ((INSIDE && a == 0 && b == 0) || (!INSIDE && !have) || v > best) {
-            best = v;
-            code = a + WH * b;
-          }
-          have = true;
+      for (int b = 0; b < WW; ++b) {
+        const int j = sj + b;
+#pragma unroll
+        for (int a = 0; a < WH; ++a) {
+          const int i = si + a;
+          in[t][b][a] = live && (INSIDE || (i >= 0 && i < d.H && j >= 0 && j < d.W));
+          v[t][b][a] = in[t][b][a] ? __ldg(xp + i + d.H * j) : 0.f;
         }
       }
     }
-    y[e] = best;
-    if (argout) argout[e] = (uint8_t)code;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const uint32_t e = e0 + t * stride;
+      if (e >= total) break;
+      float best = 0.f;
+      bool have = false;
+      int code = 0;  // window offset a + WH*b of the winner
+#pragma unroll
+      for (int b = 0; b < WW; ++b)
+#pragma unroll
+        for (int a = 0; a < WH; ++a)
+          if (in[t][b][a]) {
+            const float u = v[t][b][a];
+            if ((INSIDE && a == 0 && b == 0) || (!INSIDE && !have) || u > best) {
+              best = u;
+              code = a + WH * b;
+            }
+            have = true;
+          }
+      y[e] = best;
+      if (argout) argout[e] = (uint8_t)code;
+    }
   }
 }
 
