@@ -918,6 +918,9 @@ struct LrnGridOut {
 #ifndef CK_LRN_GRID_MINB
 #define CK_LRN_GRID_MINB 5
 #endif
+#ifndef CK_LRN_GRID_P
+#define CK_LRN_GRID_P 8
+#endif
 template <int NW, bool kAcc, bool GRID = false>
 __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
                               int HW, int C, int64_t pixels, float kappa, float alpha, float beta,
@@ -1113,7 +1116,7 @@ __global__ void __launch_bounds__(128, CK_LRN_GRID_MINB)
                    int64_t pixels, float kappa, float alpha, float beta, LrnGridOut go) {
   ck::pdl_entry();
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
-  constexpr int P = 8;  // prefetch distance (channels); divides 32
+  constexpr int P = CK_LRN_GRID_P;  // prefetch distance (channels); divides 32
   const float nb = -beta;
   const float c2ab = __fmul_rn(__fmul_rn(2.f, alpha), beta);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

@@ -12,6 +12,7 @@ ap.add_argument("--net", default="alexnet")
 ap.add_argument("--steps", type=int, default=30)
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--option", action="append", default=[], help="engine option name=value")
+ap.add_argument("--layers", default="", help="also print these layers' eager fwd/bwd ms (5-step mean)")
 a = ap.parse_args()
 if a.lib:
     from paper_1412_4564_b200 import _lib
@@ -47,3 +48,17 @@ for rep in range(3):
     res.append(e0.elapsed_time(e1) / a.steps)
 print(f"{a.net} {a.lib or 'libck.so'} {' '.join(a.option)}: ms/step "
       + " ".join(f"{v:.3f}" for v in res))
+if a.layers:
+    want = a.layers.split(",")
+    acc = {}
+    g.set_profiling(True)
+    t.set_graph(False)
+    for _ in range(5):
+        t.step(want_loss=False, stream=st.cuda_stream)
+        torch.cuda.synchronize()
+        for n, f, b in g.layer_times():
+            if n in want:
+                acc.setdefault(n, []).append((f, b))
+    g.set_profiling(False)
+    print("  " + "  ".join(f"{n} fwd {sum(v[0] for v in acc[n]) / len(acc[n]):.4f} bwd "
+                          f"{sum(v[1] for v in acc[n]) / len(acc[n]):.4f}" for n in want if n in acc))
