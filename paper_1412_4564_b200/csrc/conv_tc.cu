@@ -2654,7 +2654,7 @@ static bool conv_tc_forward_impl(ck_handle* h, const float* x, const float* f, c
   if (is_fc(d)) {
     // Y[k, n] = sum_q F[q, k] X[q, n]   (A = filters, B = images, both K-major)
     const int Q = d.H * d.W * d.C;
-    if (Q % 4 || d.K < 16) return false;
+    if (Q % 4) return false;  // (K < 128 filters: the A box's rows past K are TMA zero fill)
     // short reductions with a wave of 128 x 64 tiles (AlexNet fc7): no split-K
     // partials / finish pass (measured fc7 0.034 -> 0.029 ms; fc6's 9216-long
     // K keeps split-K, tools/fc_sweep.sh)

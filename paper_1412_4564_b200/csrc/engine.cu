@@ -1092,6 +1092,7 @@ struct ck_trainer : ck::LayerDone {
     std::vector<float*> inputs;
     cudaGraphExec_t exec;
     int64_t launches;
+    int64_t tc_launches;  // of which tcgen05 GEMMs
     uint64_t gen;  // workspace generation the captured pointers belong to
   };
   uint64_t eager_gen = 0;  // workspace generation after the last eager step
@@ -1545,7 +1546,7 @@ ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
   CKG_BEGIN(g)
   cudaStream_t s = (cudaStream_t)stream;
   check_step_flag(t, false);  // a previous step's label error surfaces here at the latest
-  int64_t before = g->h->counter.n;
+  int64_t before = g->h->counter.n, before_tc = g->h->counter.tc;
   // Replay is valid only while every workspace the captured kernels point
   // into is where it was at capture time (Workspace::get/release bump the
   // generation): otherwise drop the graphs and run eagerly, which re-sizes
@@ -1586,10 +1587,13 @@ ck_status ck_trainer_step(ck_trainer* t, float* loss_host, ck_stream stream) {
         cudaGraphExecDestroy(exec);
         throw Err(CK_ERR_CUDA, "workspace reallocated during step capture");
       }
-      t->graphs.push_back({s, inputs, exec, g->h->counter.n - before, gen});
+      t->graphs.push_back({s, inputs, exec, g->h->counter.n - before,
+                           g->h->counter.tc - before_tc, gen});
       cap = &t->graphs.back();
     } else {
+      // a replay launches the captured kernels again: count them
       g->h->counter.n += cap->launches;
+      g->h->counter.tc += cap->tc_launches;
     }
     check_cuda(cudaGraphLaunch(cap->exec, s), "graph launch");
   } else {

@@ -60,10 +60,12 @@ def test_tf32_operand_rounding_mode():
 
 # Network-level parity (whole forward + backward through the DAG engine vs the
 # oracle DAG, oracle/chain.py).
-#   FP32: against the exact (double) oracle, every derivative within 1e-4
-#         normwise (max(||a-b||/||b||, max|a-b|/max|b|)).
+#   FP32: against the exact (double) oracle routed by the device's ReLU masks /
+#         max-pool argmaxes (see TF32), every derivative within 1e-4 normwise
+#         (max(||a-b||/||b||, max|a-b|/max|b|)); even FP32 flips a pre-activation
+#         that sits within an ulp of 0 now and then (VGG: 1 site at relu4).
 #   TF32: against the oracle evaluated on the same TF32-rounded conv operands
-#         (the passes that ran on tcgen05, netcheck.tc_passes) AND routed by the
+#         (the passes on TF32 operands, netcheck.tc_passes) AND routed by the
 #         device's own ReLU masks / max-pool argmaxes (chain.run gates): every
 #         derivative within 1e-2 normwise.  Holding the discrete routing fixed is
 #         what makes a network-level TF32 bound meaningful: a 1e-5 difference in
@@ -95,11 +97,14 @@ def test_network_fwd_bwd(name, batch, kw, math, capsys):
     g.forward()
     g.backward("objective")
     vals, derivs = chain.run(net, params, inputs)
-    if math == "tf32":
-        tvals, tderivs = chain.run(net, params, inputs, tf32=netcheck.tc_passes(net),
-                                   gates=_gates(net, g))
-    else:
-        tvals, tderivs = vals, derivs
+    # routed by the device's ReLU masks / max-pool argmaxes in both modes: a
+    # pre-activation within an ulp of 0 may flip between summation orders
+    # (FP32 VGG: 1 site of 2 x 64 x 32 x 32 x 128 at relu4 moves conv1f by
+    # 9e-4 normwise, 7e-6 once routed); the routing itself is checked
+    # bit-exactly in test_headline_layers_vs_oracle
+    tvals, tderivs = chain.run(net, params, inputs,
+                               tf32=netcheck.tc_passes(net) if math == "tf32" else False,
+                               gates=_gates(net, g))
     loss = g.get("objective")[0]
     tol = 1e-4 if math == "fp32" else 1e-2
     assert abs(loss - tvals["objective"][0]) <= tol * abs(tvals["objective"][0])
@@ -118,7 +123,7 @@ def test_network_fwd_bwd(name, batch, kw, math, capsys):
         assert e < tol, (pname, e)
     with capsys.disabled():
         print(f"\n  [{name} b={batch} {math}] worst derivative error {worst:.2e}"
-              + (f" (vs exact free-routing oracle: {drift:.2e})" if math == "tf32" else ""))
+              f" (vs exact free-routing oracle: {drift:.2e})")
     assert g.last_launches > 0
 
 
