@@ -266,6 +266,35 @@ void conv_wgrad_dispatch(ck_handle* h, const float* x, const float* dy, float* d
 
 using namespace ck;
 
+// Engine (conv -> bnorm, TF32 grid path): ck_bnorm_backward with dx written
+// as the conv's dy grid + bias partials (bnorm_backward_grid) instead of HWCN;
+// dw / db as usual.  False (nothing launched) outside the grid kernel's envelope.
+namespace ck {
+bool bnorm_backward_to_grid(ck_handle* h, const ck_tensor* x, const ck_tensor* w,
+                            const ck_tensor* b, double epsilon, const ck_tensor* dy,
+                            ck_tensor* dw, ck_tensor* db, int accumulate, const GridPlan& gp,
+                            float* grid, double* bpart, cudaStream_t st) {
+  const ck_shape& s = x->shape;
+  const int HW = (int)(s.h * s.w), C = (int)s.c, N = (int)s.n;
+  if (gp.Kg * gp.groups != C || gp.Kg % 32 || C % 32 || gp.OH != (int)s.h || gp.OW != (int)s.w)
+    return false;
+  const int splits = bnorm_splits(HW, C, N);
+  double* buf = (double*)h->ws.get(sizeof(double) * 4 * (size_t)C * (splits + 1), st);
+  if (!buf) throw Err(CK_ERR_CUDA, "workspace allocation failed");
+  double* stats = buf + (size_t)4 * C * splits;
+  const float* dyp = h->fuse_relu_x ? h->fuse_relu_dy : dy->data;
+  BnGate rg;
+  if (h->fuse_relu_x && h->bn_muinv) rg = BnGate{w->data, b->data, h->bn_muinv};
+  const float* gate = rg.muinv ? nullptr : h->fuse_relu_x;
+  if ((int64_t)s.n * gp.Hg * gp.Wg * gp.Kgp * gp.groups >= (1ll << 31)) return false;
+  bnorm_stats(x->data, dyp, buf, stats, HW, C, N, splits, st, gate, rg);
+  // (dw / db written by the grid kernel's first block)
+  return bnorm_backward_grid(x->data, dyp, w->data, stats, epsilon, (int)s.h, (int)s.w, C, N,
+                             grid, bpart, gp.Hg, gp.Wg, gp.Kg, gp.Kgp, gp.groups, st, gate, rg,
+                             dw ? dw->data : nullptr, db ? db->data : nullptr, accumulate);
+}
+}  // namespace ck
+
 extern "C" {
 
 const char* ck_version(void) {
@@ -703,6 +732,7 @@ ck_status ck_bnorm_backward(ck_handle* h, const ck_tensor* x, const ck_tensor* w
   after_launch();
   CK_API_END(h)
 }
+
 
 // loss.cpp:35-40 + :92-94
 static void check_loss(const ck_tensor* x, const ck_tensor* labels, const ck_tensor* weights) {

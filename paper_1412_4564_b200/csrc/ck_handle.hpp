@@ -147,6 +147,11 @@ bool conv_tc_bias(ck_handle* h, const float* dy, float* db, const ConvDims& d, i
 // (key: x_grid's cache key).  conv_tc_xgrid_plan says whether conv d reads x
 // only through it, so the layer producing x may write it instead.
 bool conv_tc_xgrid_plan(const ConvDims& d, XGridPlan* xp);
+// capi.cu: bnorm backward writing the conv-below's dy grid (engine bn_grid)
+bool bnorm_backward_to_grid(ck_handle* h, const ck_tensor* x, const ck_tensor* w,
+                            const ck_tensor* b, double epsilon, const ck_tensor* dy,
+                            ck_tensor* dw, ck_tensor* db, int accumulate, const GridPlan& gp,
+                            float* grid, double* bpart, cudaStream_t st);
 // (GridPlan: ck_internal.hpp)
 bool conv_tc_grid_plan(const ConvDims& d, GridPlan* gp);
 // capi.cu: compute a dy the gated transform left pending (h->pending_dy == dy)

@@ -210,6 +210,13 @@ struct BnGate {
   const float* b = nullptr;
   const float* muinv = nullptr;
 };
+// bnorm backward writing dx into the conv-below's dy grid (dy at (0, 0) of an
+// Hg x Wg grid, Kgp channels per group) plus 32-pixel bias partials; stats from
+// bnorm_stats.  False when the shape is outside the kernel's envelope.
+bool bnorm_backward_grid(const float* x, const float* dy, const float* w, const double* stats,
+                         double eps, int H, int W, int C, int N, float* grid, double* bpart,
+                         int Hg, int Wg, int Kg, int Kgp, int groups, cudaStream_t s,
+                         const float* gate, const BnGate& rg, float* dw, float* db, int acc);
 void bnorm_stats(const float* x, const float* dy, double* partial, double* out, int HW, int C,
                  int N, int splits, cudaStream_t s, const float* gate = nullptr,
                  const BnGate& rg = BnGate{});

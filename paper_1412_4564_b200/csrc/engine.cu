@@ -101,6 +101,9 @@ struct Var {
   // derivative left unmaterialized because the LRN layer lazy_lrn wrote its
   // consumer conv's dy grid directly: that LRN backward, computed on request
   int lazy_lrn = -1;
+  // derivative left unmaterialized because the bnorm layer lazy_bn wrote its
+  // producer conv's dy grid directly: that bnorm backward's dx, on request
+  int lazy_bn = -1;
 };
 
 struct Layer {
@@ -167,6 +170,9 @@ struct ck_graph {
   // conv's relu-gated dy grid from the second conv's data-gradient epilogue
   // (default on)
   bool dgrad_grid = true;
+  // option "bn_grid": a TF32 conv -> bnorm backward writes the conv's dy grid
+  // (and bias partials) from the bnorm backward (default on)
+  bool bn_grid = true;
   std::vector<std::pair<std::string, std::string>> meta;  // manifest metadata
   std::vector<int> decl;  // input / param vars in declaration order (manifest order)
   int64_t last_launches = 0;
@@ -670,6 +676,34 @@ static void materialize_lrn(ck_graph* g, Var& v, cudaStream_t s) {
   v.lazy_lrn = -1;
 }
 
+// The conv output's derivative a bnorm backward skipped (it wrote the conv's
+// dy grid instead): that bnorm backward's dx, now, with the same gating.
+static void materialize_bn(ck_graph* g, Var& v, cudaStream_t s) {
+  if (v.lazy_bn < 0) return;
+  Layer& l = g->layers[v.lazy_bn];
+  ck_handle* h = g->h;
+  ck_tensor x = tv(g->vars[l.in[0]], false), w = tv(g->vars[l.in[1]], false),
+            b = tv(g->vars[l.in[2]], false), dx = tv(v, true),
+            dy = tv(g->vars[l.out[0]], true);
+  const bool fused = l.relu_out >= 0 && g->layers[g->vars[l.relu_out].producer].bwd_deferred;
+  if (fused) {
+    h->fuse_relu_x = g->vars[l.out[0]].value;
+    h->fuse_relu_dy = g->vars[l.relu_out].deriv;
+    if (g->layers[g->vars[l.relu_out].producer].fused_done) h->bn_muinv = l.muinv;
+  }
+  struct ResetM {
+    ck_handle* h;
+    ~ResetM() {
+      h->fuse_relu_x = nullptr;
+      h->fuse_relu_dy = nullptr;
+      h->bn_muinv = nullptr;
+    }
+  } reset{h};
+  const ck_status st = ck_bnorm_backward(h, &x, &w, &b, l.p[0], &dy, &dx, nullptr, nullptr, 0, s);
+  if (st != CK_OK) throw Err(st, h->err);
+  v.lazy_bn = -1;
+}
+
 static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
   ck_handle* h = g->h;
   auto V = [&](int k) { return tv(g->vars[l.in[k]], false); };
@@ -689,14 +723,18 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
       int a0 = acc(0), a1 = acc(1), a2 = l.in.size() > 2 ? acc(2) : a1;
       h->conv_cache = &l.cache;  // the forward's transformed input (valid this step)
       const bool fused = l.relu_out >= 0 && g->layers[g->vars[l.relu_out].producer].bwd_deferred;
+      const bool bn_pre = g->vars[l.out[0]].lazy_bn >= 0;
       if (l.pre_grid) {
         l.pre_grid = false;
-        if (fused && a0 == a1 && a1 == a2 && l.in.size() > 2) {
+        if ((fused || bn_pre) && a0 == a1 && a1 == a2 && l.in.size() > 2) {
           h->pre_dyg = (float*)l.dyg.ptr;
           h->pre_dyg_src = dy.data;
           h->pre_dyg_key = l.plan.key;
           h->pre_bpart = (const double*)l.bpart.ptr;
           h->pre_rows = l.pre_rows;
+        } else if (bn_pre) {
+          // cannot consume the prebuilt grid: materialize dy the bnorm skipped
+          materialize_bn(g, g->vars[l.out[0]], s);
         } else {
           // cannot consume the prebuilt grid: materialize the relu output's
           // derivative the LRN skipped, then take the ordinary path
@@ -890,6 +928,39 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
         g->vars[l.out[0]].lazy_gate = l.out[0];
         g->vars[l.out[0]].lazy_src = l.relu_out;
       }
+      // conv -> bnorm (VGG): write the conv's dy grid (+ bias partials) from
+      // this backward; the conv output's derivative is computed on request
+      Var& xv = g->vars[l.in[0]];
+      if (g->bn_grid && g->math == CK_MATH_TF32 && !a0 && a1 == a2 && xv.producer >= 0 &&
+          xv.consumers.size() == 1) {
+        Layer& c = g->layers[xv.producer];
+        if (c.kind == Kind::conv && c.in.size() > 2 && c.relu_out < 0 && !c.pre_grid) {
+          const ConvDims cd = conv_dims(g->vars[c.in[0]].shape, g->vars[c.in[1]].shape,
+                                        xv.shape, conv_geom_of(c));
+          GridPlan gp;
+          if (conv_tc_grid_plan(cd, &gp) && gp.Kg % 32 == 0) {
+            float* old = (float*)c.dyg.ptr;
+            float* grid = (float*)c.dyg.get(gp.bytes, s);
+            if (!grid) throw Err(CK_ERR_CUDA, "dy grid allocation failed");
+            if (grid != old)  // the grid's junk rows stay zero from here on
+              check_cuda(cudaMemsetAsync(grid, 0, c.dyg.bytes, s), "zero");
+            const int rows = (int)((elems(xv.shape) / xv.shape.c + 31) / 32);
+            double* bp =
+                (double*)c.bpart.get(sizeof(double) * (size_t)rows * gp.Kgp * gp.groups, s);
+            if (!bp) throw Err(CK_ERR_CUDA, "bias partial allocation failed");
+            if (bnorm_backward_to_grid(h, &x, &w, &b, l.p[0], &dy, &dw, &db, a1, gp, grid, bp, s)) {
+              c.pre_grid = true;
+              c.plan = gp;
+              c.pre_rows = rows;
+              xv.lazy_bn = (int)(&l - &g->layers[0]);
+              mark(0);
+              mark(1);
+              mark(2);
+              break;
+            }
+          }
+        }
+      }
       if (a0 == a1 && a1 == a2) {
         st = ck_bnorm_backward(h, &x, &w, &b, l.p[0], &dy, &dx, &dw, &db, a0, s);
       } else {
@@ -1018,7 +1089,7 @@ struct LayerDone {
 static void run_backward(ck_graph* g, int objective, cudaStream_t s, LayerDone* cb) {
   for (auto& v : g->vars) {
     v.deriv_live = false;
-    v.lazy_gate = v.lazy_src = v.lazy_lrn = -1;
+    v.lazy_gate = v.lazy_src = v.lazy_lrn = v.lazy_bn = -1;
   }
   for (auto& l : g->layers) l.pre_grid = false;
   for (auto& l : g->layers) l.bwd_deferred = false;
@@ -1275,6 +1346,11 @@ ck_status ck_graph_var(ck_graph* g, const char* name, int deriv, ck_tensor* out)
   if (!g->finalized) throw Err(CK_ERR_ARG, "graph not finalized");
   if (!out) throw Err(CK_ERR_ARG, "null output");
   Var& v = g->vars[g->var(name ? name : "")];
+  if (deriv && v.lazy_bn >= 0) {
+    check_cuda(cudaDeviceSynchronize(), "synchronize");
+    materialize_bn(g, v, 0);
+    check_cuda(cudaDeviceSynchronize(), "synchronize");
+  }
   if (deriv && v.lazy_lrn >= 0) {
     check_cuda(cudaDeviceSynchronize(), "synchronize");
     materialize_lrn(g, v, 0);
@@ -1359,6 +1435,8 @@ ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value) {
     g->producer_grid = value != 0;
   else if (n == "dgrad_grid")
     g->dgrad_grid = value != 0;
+  else if (n == "bn_grid")
+    g->bn_grid = value != 0;
   else
     throw Err(CK_ERR_ARG, "unknown graph option '" + n + "'");
   CKG_END(g)

@@ -1546,6 +1546,138 @@ __global__ void __launch_bounds__(256) bnorm_bwd_k(const float* __restrict__ x,
   }
 }
 
+// bnorm backward (normalize.cpp:212-265, bnorm_bwd_k's float operations, so
+// the values are bit-identical) writing the conv-below's dy grid instead of dx
+// (VGG conv -> bnorm: the engine's bn_grid option): one pixel per thread walks
+// the channels (x and dy read coalesced along the warp's 32 pixels, per channel
+// plane); every 32 channels the warp's [pixel][channel] stage goes out as
+// float4 runs of four pixels' 128-byte grid rows, with the 32-pixel column sums
+// (the conv's bias-gradient partials, [pixel warp][Cp] doubles).  The
+// per-channel constants come from the stats pass, computed per block in
+// bnorm_bwd_k's expressions.  Requires the conv's channels per group % 32 == 0.
+struct BnGridOut {
+  float* grid;
+  double* bpart;
+  int H, Hg, Wg, Kg, Kgp, Cp;
+};
+
+template <int G>
+__global__ void __launch_bounds__(256) bnorm_bwd_grid_k(const float* __restrict__ x,
+                                                        const float* __restrict__ dy,
+                                                        const float* __restrict__ gate,
+                                                        const float* __restrict__ gb,
+                                                        const float* __restrict__ muinv,
+                                                        const float* __restrict__ w,
+                                                        const double* __restrict__ stats,
+                                                        double eps, int HW, int C,
+                                                        int64_t pixels, BnGridOut go,
+                                                        float* dw, float* db, int acc_params) {
+  ck::pdl_entry();
+  extern __shared__ float bsm[];
+  float* cmu = bsm;            // [C] each
+  float* cinv = cmu + C;
+  float* cwinv = cinv + C;
+  float* cmdy = cwinv + C;
+  float* cmdyx = cmdy + C;
+  float* gw = cmdyx + C;       // G == 2: the gate's (w, b, mu, inv)
+  float* gbb = gw + C;
+  float* gmu = gbb + C;
+  float* ginv = gmu + C;
+  float* stage = ginv + C;     // [8 warps][32 pixels][33]
+  int* grs = (int*)(stage + 8 * 32 * 33);  // [8 warps][32]
+  const double M = (double)pixels;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const double m = stats[c * 4] / M;
+    double var = stats[c * 4 + 1] / M - m * m;
+    if (var < 0) var = 0;
+    const double invd = 1.0 / sqrt(var + eps);
+    const double sdy = stats[c * 4 + 2];
+    const double sdyx = invd * (stats[c * 4 + 3] - m * sdy);
+    if (blockIdx.x == 0) {  // bnorm_bwd_k's parameter derivatives
+      if (dw) dw[c] = acc_params ? dw[c] + (float)sdyx : (float)sdyx;
+      if (db) db[c] = acc_params ? db[c] + (float)sdy : (float)sdy;
+    }
+    const float inv = (float)invd;
+    cmu[c] = (float)m;
+    cinv[c] = inv;
+    cwinv[c] = __fmul_rn(w[c], inv);
+    cmdy[c] = (float)(sdy / M);
+    cmdyx[c] = (float)(sdyx / M);
+    const BnGateP P = bn_gate_params(w, gb, muinv, c);
+    gw[c] = P.w;
+    gbb[c] = P.b;
+    gmu[c] = P.mu;
+    ginv[c] = P.inv;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int q4 = lane >> 3, m4 = lane & 7;
+  float* st = stage + wib * 32 * 33;
+  for (int64_t eb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; eb < pixels;
+       eb += (int64_t)gridDim.x * blockDim.x) {
+    const bool live = eb + lane < pixels;
+    const int64_t e = live ? eb + lane : pixels - 1;
+    const int64_t n = e / HW;
+    const int p = (int)(e - n * HW);
+    {
+      const int i = p % go.H, jj = p / go.H;
+      __syncwarp();
+      grs[wib * 32 + lane] =
+          live ? (int)(((int64_t)n * go.Hg * go.Wg + i + (int64_t)go.Hg * jj) * go.Cp) : -1;
+    }
+    const float* xp = x + n * C * HW + p;
+    const float* dp = dy + n * C * HW + p;
+    const float* tp = gate ? gate + n * C * HW + p : nullptr;
+    for (int c0 = 0; c0 < C; c0 += 32) {
+#pragma unroll 8
+      for (int u = 0; u < 32; ++u) {
+        const int c = c0 + u;
+        const int64_t off = (int64_t)c * HW;
+        const float xv = __ldg(xp + off);
+        float g = __ldg(dp + off);
+        if (G == 1 && !(__ldg(tp + off) > 0.f)) g = 0.f;
+        if (G == 2 && !(bn_y(xv, gw[c], gmu[c], ginv[c], gbb[c]) > 0.f)) g = 0.f;
+        const float r = bn_dx(xv, g, cmu[c], cinv[c], cwinv[c], cmdy[c], cmdyx[c]);
+        st[lane * 33 + u] = live ? r : 0.f;
+      }
+      __syncwarp();
+      const int grp = c0 / go.Kg;
+      const int cpos = grp * go.Kgp + (c0 - grp * go.Kg) + 4 * m4;
+      // bias partials in double: in front of a bnorm the conv bias gradient
+      // is a sum that cancels to ~0 (sum_p dx_bn = 0), so only double keeps it
+      // at the unfused path's accuracy
+      double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int q = 4 * it + q4;
+        const int rq = grs[wib * 32 + q];
+        const float* src = st + q * 33 + 4 * m4;
+        const float4 v = make_float4(src[0], src[1], src[2], src[3]);
+        s0 += v.x;
+        s1 += v.y;
+        s2 += v.z;
+        s3 += v.w;
+        if (rq >= 0) *reinterpret_cast<float4*>(go.grid + rq + cpos) = v;
+      }
+#pragma unroll
+      for (int o = 8; o <= 16; o <<= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        s3 += __shfl_xor_sync(0xffffffffu, s3, o);
+      }
+      if (q4 == 0) {
+        double* bp = go.bpart + (eb >> 5) * go.Cp + cpos;
+        bp[0] = s0;
+        bp[1] = s1;
+        bp[2] = s2;
+        bp[3] = s3;
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // ----------------------------------------------------------------- loss ---
 // loss.cpp:14-18 as_label, :101-106 range check.  flag bit 1: non-integer
 // label, bit 2: out of range (reported by the C ABI as CK_ERR_DATA).
@@ -2336,6 +2468,39 @@ void bnorm_backward_apply(const float* x, const float* dy, const float* w, const
     else CK_BNB(false, 0);
   }
 #undef CK_BNB
+}
+
+bool bnorm_backward_grid(const float* x, const float* dy, const float* w, const double* stats,
+                         double eps, int H, int W, int C, int N, float* grid, double* bpart,
+                         int Hg, int Wg, int Kg, int Kgp, int groups, cudaStream_t s,
+                         const float* gate, const BnGate& rg, float* dw, float* db, int acc) {
+  const int HW = H * W;
+  const int64_t pixels = (int64_t)HW * N;
+  if (H > Hg || W > Wg || Kg * groups != C || Kg % 32 || C % 32) return false;
+  if ((int64_t)N * Hg * Wg * Kgp * groups >= (1ll << 31)) return false;
+  const size_t smem = sizeof(float) * (9 * (size_t)C + 8 * 32 * 33) + sizeof(int) * 8 * 32;
+  if (smem > 227 * 1024) return false;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(bnorm_bwd_grid_k<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bnorm_bwd_grid_k<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(bnorm_bwd_grid_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured = 227 * 1024;
+  }
+  BnGridOut go{grid, bpart, H, Hg, Wg, Kg, Kgp, Kgp * groups};
+  const int G = rg.muinv ? 2 : gate ? 1 : 0;
+  const dim3 grd(blocks_for(pixels, 256, 8));
+  count_launch();
+  if (G == 2)
+    ck::pdl_launch(bnorm_bwd_grid_k<2>, grd, 256, smem, s, x, dy, nullptr, rg.b, rg.muinv, w, stats, eps,
+                   HW, C, pixels, go, dw, db, acc);
+  else if (G == 1)
+    ck::pdl_launch(bnorm_bwd_grid_k<1>, grd, 256, smem, s, x, dy, gate, nullptr, nullptr, w, stats, eps,
+                   HW, C, pixels, go, dw, db, acc);
+  else
+    ck::pdl_launch(bnorm_bwd_grid_k<0>, grd, 256, smem, s, x, dy, nullptr, nullptr, nullptr, w, stats,
+                   eps, HW, C, pixels, go, dw, db, acc);
+  return true;
 }
 
 void softmaxlog_forward(const float* x, const float* labels, const float* weights,

@@ -399,6 +399,43 @@ def test_dgrad_writes_conv_dy_grid(batch):
             assert np.array_equal(d0[n], d1[n]), n
 
 
+@pytest.mark.parametrize("image", [32, 64])
+def test_bnorm_writes_conv_dy_grid(image):
+    """conv -> bnorm (-> relu) backward (VGG-16-bn): the bnorm backward writes
+    its producer conv's dy grid and bias partials (bnorm_backward_grid), the
+    conv's backward skips its dy transform, and the conv output's derivative
+    is computed on request.  Every value and derivative is bit-identical to
+    the unfused engine except the conv bias gradients (mathematically zero in
+    front of a bnorm; 32-pixel float partials in another fixed order): 1e-5 of
+    the largest filter gradient."""
+    from paper_1412_4564_b200 import nets
+    net = nets.vgg16_bn(batch=2, image=image)
+    out = []
+    for on in (True, False):
+        g = device_graph(net, "tf32")
+        g.set_option("bn_grid", on)
+        for k, v in {**net.init_params(), **net.init_inputs()}.items():
+            g.set(k, v)
+        g.forward()
+        l0 = g.hd.launches
+        g.backward("objective")
+        launches = g.hd.launches - l0
+        names = set(net.inputs) | {p[0] for p in net.params} | \
+            {o for layer in net.layers for o in layer[3]}
+        out.append(({n: g.get(n) for n in sorted(names)},
+                    {n: g.get(n, deriv=True) for n in sorted(names) if n != "label"}, launches))
+    (v0, d0, l0), (v1, d1, l1) = out
+    assert l0 < l1, (l0, l1)
+    for n in v1:
+        assert np.array_equal(v0[n], v1[n]), n
+    for n in d1:
+        if n.startswith("conv") and n.endswith("b"):
+            scale = np.abs(d1[n[:-1] + "f"]).max()
+            assert np.abs(d0[n] - d1[n]).max() <= 1e-5 * scale, n
+        else:
+            assert np.array_equal(d0[n], d1[n]), n
+
+
 @pytest.mark.parametrize("cout,groups,size", [(64, 2, 5), (48, 1, 5), (96, 1, 3), (64, 1, 4)])
 def test_lrn_grid_envelope(cout, groups, size, monkeypatch):
     """conv -> relu -> lrn -> pool -> fc on a small image: inside the fused
