@@ -319,7 +319,12 @@ ck_status ck_graph_layer_ms(ck_graph* g, int layer, float* fwd_ms, float* bwd_ms
  *   second conv's padded x grid from the first conv's epilogue;
  *   "dgrad_grid" (default 1): a TF32 conv -> relu -> conv backward writes the
  *   first conv's ReLU-gated dy grid (and bias partials) from the second conv's
- *   data-gradient epilogue. */
+ *   data-gradient epilogue;
+ *   "bn_grid" (default 1): a TF32 conv -> bnorm backward writes the conv's dy
+ *   grid (and bias partials) from the bnorm backward;
+ *   "bn_lazy_y" (default 1): a fused bnorm -> relu forward stores only relu(y).
+ * Intermediates these options leave unstored are computed on request
+ * (ck_graph_var). */
 ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value);
 
 /* ---- cnn_train training step with multi-GPU data parallelism ------------ */

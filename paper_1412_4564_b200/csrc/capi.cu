@@ -674,9 +674,11 @@ ck_status ck_bnorm_forward(ck_handle* h, const ck_tensor* x, const ck_tensor* w,
   double* stats = buf + (size_t)4 * C * splits;
   bnorm_stats(x->data, nullptr, buf, stats, HW, C, N, splits, st);
   // engine (bnorm -> relu): relu(y) written by the same pass
-  bnorm_apply(x->data, w->data, b->data, stats, nullptr, y->data,
+  const bool skip_y = h->fuse_relu && h->bn_muinv && h->bn_skip_y;
+  bnorm_apply(x->data, w->data, b->data, stats, nullptr, skip_y ? nullptr : y->data,
               moments ? moments->data : nullptr, epsilon, HW, C, N, st, h->fuse_relu,
               h->fuse_relu ? h->bn_muinv : nullptr);
+  h->bn_y_skipped = skip_y;
   if (h->fuse_relu) h->fuse_relu_done = true;
   after_launch();
   CK_API_END(h)

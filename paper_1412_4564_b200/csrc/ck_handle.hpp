@@ -67,6 +67,10 @@ struct ck_handle {
   // engine, fused bnorm -> relu: per-channel (mu, inv) of the forward, which
   // the backward uses to recompute the relu gate from x (2 floats / channel)
   float* bn_muinv = nullptr;
+  // engine, fused bnorm -> relu with the bnorm output read by nothing else:
+  // the forward stores only relu(y) (y is recomputed from x on request)
+  bool bn_skip_y = false;
+  bool bn_y_skipped = false;
 };
 
 namespace ck {

@@ -210,6 +210,9 @@ struct BnGate {
   const float* b = nullptr;
   const float* muinv = nullptr;
 };
+// y = w (x - mu) inv + b from the forward's float (mu, inv) (muinv, 2 per channel)
+void bnorm_value(const float* x, const float* w, const float* b, const float* muinv, float* y,
+                 int HW, int C, int N, cudaStream_t s);
 // bnorm backward writing dx into the conv-below's dy grid (dy at (0, 0) of an
 // Hg x Wg grid, Kgp channels per group) plus 32-pixel bias partials; stats from
 // bnorm_stats.  False when the shape is outside the kernel's envelope.

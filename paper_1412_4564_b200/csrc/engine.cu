@@ -104,6 +104,9 @@ struct Var {
   // derivative left unmaterialized because the bnorm layer lazy_bn wrote its
   // producer conv's dy grid directly: that bnorm backward's dx, on request
   int lazy_bn = -1;
+  // value left unstored by the fused bnorm -> relu forward of layer
+  // lazy_value (engine option bn_lazy_y): recomputed from x on request
+  int lazy_value = -1;
 };
 
 struct Layer {
@@ -173,6 +176,9 @@ struct ck_graph {
   // option "bn_grid": a TF32 conv -> bnorm backward writes the conv's dy grid
   // (and bias partials) from the bnorm backward (default on)
   bool bn_grid = true;
+  // option "bn_lazy_y": a fused bnorm -> relu forward whose bnorm output has
+  // no other reader stores only relu(y) (default on)
+  bool bn_lazy_y = true;
   std::vector<std::pair<std::string, std::string>> meta;  // manifest metadata
   std::vector<int> decl;  // input / param vars in declaration order (manifest order)
   int64_t last_launches = 0;
@@ -602,9 +608,14 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
       h->fuse_relu = l.relu_out >= 0 ? g->vars[l.relu_out].value : nullptr;
       h->fuse_relu_done = false;
       h->bn_muinv = l.muinv;
+      h->bn_skip_y = g->bn_lazy_y && l.relu_out >= 0 && g->vars[l.out[0]].consumers.size() == 1;
+      h->bn_y_skipped = false;
       st = ck_bnorm_forward(h, &x, &w, &b, l.p[0], &y, &m, s);
+      g->vars[l.out[0]].lazy_value =
+          st == CK_OK && h->bn_y_skipped ? (int)(&l - &g->layers[0]) : -1;
       h->fuse_relu = nullptr;
       h->bn_muinv = nullptr;
+      h->bn_skip_y = false;
       if (l.relu_out >= 0) {
         Layer& r = g->layers[g->vars[l.relu_out].producer];
         r.fused_done = st == CK_OK && h->fuse_relu_done;
@@ -674,6 +685,17 @@ static void materialize_lrn(ck_graph* g, Var& v, cudaStream_t s) {
   const ck_status st = ck_lrn_backward(g->h, &x, &p, &dy, &dx, 0, s);
   if (st != CK_OK) throw Err(st, g->h->err);
   v.lazy_lrn = -1;
+}
+
+// The bnorm output a fused bnorm -> relu forward did not store: from x with
+// the forward's (mu, inv), bit-identical.
+static void materialize_value(ck_graph* g, Var& v, cudaStream_t s) {
+  if (v.lazy_value < 0) return;
+  Layer& l = g->layers[v.lazy_value];
+  const Var& x = g->vars[l.in[0]];
+  bnorm_value(x.value, g->vars[l.in[1]].value, g->vars[l.in[2]].value, l.muinv, v.value,
+              (int)(x.shape.h * x.shape.w), (int)x.shape.c, (int)x.shape.n, s);
+  v.lazy_value = -1;
 }
 
 // The conv output's derivative a bnorm backward skipped (it wrote the conv's
@@ -853,6 +875,7 @@ static void layer_backward(ck_graph* g, Layer& l, cudaStream_t s) {
         mark(0);
         break;
       }
+      materialize_value(g, g->vars[l.in[0]], s);  // (a bnorm output left unstored)
       ck_tensor x = V(0), dx = D(0);
       st = ck_relu_backward(h, &x, &dy, &dx, acc(0), s);
       mark(0);
@@ -1346,6 +1369,11 @@ ck_status ck_graph_var(ck_graph* g, const char* name, int deriv, ck_tensor* out)
   if (!g->finalized) throw Err(CK_ERR_ARG, "graph not finalized");
   if (!out) throw Err(CK_ERR_ARG, "null output");
   Var& v = g->vars[g->var(name ? name : "")];
+  if (!deriv && v.lazy_value >= 0) {
+    check_cuda(cudaDeviceSynchronize(), "synchronize");
+    materialize_value(g, v, 0);
+    check_cuda(cudaDeviceSynchronize(), "synchronize");
+  }
   if (deriv && v.lazy_bn >= 0) {
     check_cuda(cudaDeviceSynchronize(), "synchronize");
     materialize_bn(g, v, 0);
@@ -1365,6 +1393,7 @@ ck_status ck_graph_var(ck_graph* g, const char* name, int deriv, ck_tensor* out)
     // relu backward (activation.cpp:14-22) of the relu output's derivative,
     // gated by this var's own value (x > 0), now, in order with all prior work
     check_cuda(cudaDeviceSynchronize(), "synchronize");
+    materialize_value(g, g->vars[v.lazy_gate], 0);
     relu_backward(g->vars[v.lazy_gate].value, g->vars[v.lazy_src].deriv, v.deriv,
                   elems(v.shape), 0, 0);
     check_cuda(cudaDeviceSynchronize(), "synchronize");
@@ -1437,6 +1466,8 @@ ck_status ck_graph_set_option(ck_graph* g, const char* name, int64_t value) {
     g->dgrad_grid = value != 0;
   else if (n == "bn_grid")
     g->bn_grid = value != 0;
+  else if (n == "bn_lazy_y")
+    g->bn_lazy_y = value != 0;
   else
     throw Err(CK_ERR_ARG, "unknown graph option '" + n + "'");
   CKG_END(g)

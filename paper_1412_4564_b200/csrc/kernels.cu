@@ -1453,7 +1453,7 @@ __global__ void __launch_bounds__(256) bnorm_apply_k(const float* __restrict__ x
         o.y = bn_y(v.y, wk, mu, inv, bk);
         o.z = bn_y(v.z, wk, mu, inv, bk);
         o.w = bn_y(v.w, wk, mu, inv, bk);
-        yp[q] = o;
+        if (y) yp[q] = o;
         if (y2) {
           o.x = o.x > 0.f ? o.x : 0.f;
           o.y = o.y > 0.f ? o.y : 0.f;
@@ -1465,7 +1465,7 @@ __global__ void __launch_bounds__(256) bnorm_apply_k(const float* __restrict__ x
     } else {
       for (int p = threadIdx.x; p < HW; p += 256) {
         const float o = bn_y(x[base + p], wk, mu, inv, bk);
-        y[base + p] = o;
+        if (y) y[base + p] = o;
         if (y2) y2[base + p] = o > 0.f ? o : 0.f;
       }
     }
@@ -2468,6 +2468,30 @@ void bnorm_backward_apply(const float* x, const float* dy, const float* w, const
     else CK_BNB(false, 0);
   }
 #undef CK_BNB
+}
+
+// y = bn_y(x) with the forward's own float (mu, inv) per channel: the bnorm
+// output a fused bnorm -> relu forward did not store (engine bn_lazy_y),
+// bit-identical to what bnorm_apply_k would have written.
+__global__ void __launch_bounds__(256) bnorm_value_k(const float* __restrict__ x,
+                                                     const float* __restrict__ w,
+                                                     const float* __restrict__ b,
+                                                     const float* __restrict__ muinv,
+                                                     float* __restrict__ y, int HW, int C,
+                                                     int64_t n_total) {
+  ck::pdl_entry();
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)((e / HW) % C);
+    y[e] = bn_y(x[e], w[c], muinv[2 * c], muinv[2 * c + 1], b[c]);
+  }
+}
+
+void bnorm_value(const float* x, const float* w, const float* b, const float* muinv, float* y,
+                 int HW, int C, int N, cudaStream_t s) {
+  const int64_t n = (int64_t)HW * C * N;
+  count_launch();
+  ck::pdl_launch(bnorm_value_k, blocks_for(n, 256), 256, 0, s, x, w, b, muinv, y, HW, C, n);
 }
 
 bool bnorm_backward_grid(const float* x, const float* dy, const float* w, const double* stats,

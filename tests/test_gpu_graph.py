@@ -404,7 +404,9 @@ def test_bnorm_writes_conv_dy_grid(image):
     """conv -> bnorm (-> relu) backward (VGG-16-bn): the bnorm backward writes
     its producer conv's dy grid and bias partials (bnorm_backward_grid), the
     conv's backward skips its dy transform, and the conv output's derivative
-    is computed on request.  Every value and derivative is bit-identical to
+    is computed on request; the fused bnorm -> relu forward stores only
+    relu(y), y being recomputed from x on request (bn_lazy_y).  Every value
+    and derivative is bit-identical to
     the unfused engine except the conv bias gradients (mathematically zero in
     front of a bnorm; 32-pixel float partials in another fixed order): 1e-5 of
     the largest filter gradient."""
@@ -414,6 +416,7 @@ def test_bnorm_writes_conv_dy_grid(image):
     for on in (True, False):
         g = device_graph(net, "tf32")
         g.set_option("bn_grid", on)
+        g.set_option("bn_lazy_y", on)
         for k, v in {**net.init_params(), **net.init_inputs()}.items():
             g.set(k, v)
         g.forward()
