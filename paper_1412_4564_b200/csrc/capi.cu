@@ -675,9 +675,21 @@ ck_status ck_bnorm_forward(ck_handle* h, const ck_tensor* x, const ck_tensor* w,
   bnorm_stats(x->data, nullptr, buf, stats, HW, C, N, splits, st);
   // engine (bnorm -> relu): relu(y) written by the same pass
   const bool skip_y = h->fuse_relu && h->bn_muinv && h->bn_skip_y;
-  bnorm_apply(x->data, w->data, b->data, stats, nullptr, skip_y ? nullptr : y->data,
-              moments ? moments->data : nullptr, epsilon, HW, C, N, st, h->fuse_relu,
-              h->fuse_relu ? h->bn_muinv : nullptr);
+  // engine, bnorm -> relu -> conv: relu(y) straight into the conv's x grid
+  // (y and the HWCN relu output left unstored, recomputed on request)
+  bool gridded = false;
+  if (skip_y && h->next_xg) {
+    const XGridPlan& xp = h->next_xg_plan;
+    gridded = bnorm_apply_grid(x->data, w->data, b->data, stats,
+                               moments ? moments->data : nullptr, h->bn_muinv, epsilon, (int)s.h,
+                               (int)s.w, C, N, h->next_xg, xp.Hg, xp.Wg, xp.Cg, xp.Cgp, xp.groups,
+                               xp.pt, xp.pl, st);
+    h->next_xg_done = gridded;
+  }
+  if (!gridded)
+    bnorm_apply(x->data, w->data, b->data, stats, nullptr, skip_y ? nullptr : y->data,
+                moments ? moments->data : nullptr, epsilon, HW, C, N, st, h->fuse_relu,
+                h->fuse_relu ? h->bn_muinv : nullptr);
   h->bn_y_skipped = skip_y;
   if (h->fuse_relu) h->fuse_relu_done = true;
   after_launch();

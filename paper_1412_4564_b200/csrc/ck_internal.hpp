@@ -211,8 +211,16 @@ struct BnGate {
   const float* muinv = nullptr;
 };
 // y = w (x - mu) inv + b from the forward's float (mu, inv) (muinv, 2 per channel)
+// (relu != 0: relu of it, the fused relu output)
 void bnorm_value(const float* x, const float* w, const float* b, const float* muinv, float* y,
-                 int HW, int C, int N, cudaStream_t s);
+                 int HW, int C, int N, int relu, cudaStream_t s);
+// fused bnorm -> relu forward writing relu(y) into the next conv's padded
+// pixel-major x grid (XGridPlan layout) instead of HWCN; moments and (mu, inv)
+// as bnorm_apply.  False outside the kernel's envelope (nothing launched).
+bool bnorm_apply_grid(const float* x, const float* w, const float* b, const double* stats,
+                      float* moments_out, float* muinv_out, double eps, int H, int W, int C, int N,
+                      float* grid, int Hg, int Wg, int Cg, int Cgp, int groups, int pt, int pl,
+                      cudaStream_t s);
 // bnorm backward writing dx into the conv-below's dy grid (dy at (0, 0) of an
 // Hg x Wg grid, Kgp channels per group) plus 32-pixel bias partials; stats from
 // bnorm_stats.  False when the shape is outside the kernel's envelope.

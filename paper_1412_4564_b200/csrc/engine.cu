@@ -107,6 +107,7 @@ struct Var {
   // value left unstored by the fused bnorm -> relu forward of layer
   // lazy_value (engine option bn_lazy_y): recomputed from x on request
   int lazy_value = -1;
+  bool lazy_value_relu = false;  // ... and this var is relu of that bnorm output
 };
 
 struct Layer {
@@ -610,9 +611,46 @@ static void layer_forward(ck_graph* g, Layer& l, cudaStream_t s) {
       h->bn_muinv = l.muinv;
       h->bn_skip_y = g->bn_lazy_y && l.relu_out >= 0 && g->vars[l.out[0]].consumers.size() == 1;
       h->bn_y_skipped = false;
+      // bnorm -> relu -> conv (VGG): relu(y) straight into the conv's x grid
+      Layer* nxt = nullptr;
+      XGridPlan xp{};
+      if (h->bn_skip_y && g->producer_grid && g->math == CK_MATH_TF32) {
+        const Var& rv = g->vars[l.relu_out];
+        if (rv.consumers.size() == 1 && rv.consumers[0].second == 0) {
+          Layer& c2 = g->layers[rv.consumers[0].first];
+          if (c2.kind == Kind::conv) {
+            const ConvDims d2 = conv_dims(rv.shape, g->vars[c2.in[1]].shape,
+                                          g->vars[c2.out[0]].shape, conv_geom_of(c2));
+            if (conv_tc_xgrid_plan(d2, &xp) && xp.Cg % 32 == 0) {
+              float* buf = (float*)c2.cache.buf.get(xp.bytes, s);
+              if (!buf) throw Err(CK_ERR_CUDA, "x grid allocation failed");
+              if (c2.cache.zero_ptr != buf || c2.cache.zero_key != xp.key) {
+                check_cuda(cudaMemsetAsync(buf, 0, c2.cache.buf.bytes, s), "zero");
+                c2.cache.zero_ptr = buf;
+                c2.cache.zero_key = xp.key;
+              }
+              h->next_xg = buf;
+              h->next_xg_plan = xp;
+              h->next_xg_done = false;
+              nxt = &c2;
+            }
+          }
+        }
+      }
       st = ck_bnorm_forward(h, &x, &w, &b, l.p[0], &y, &m, s);
-      g->vars[l.out[0]].lazy_value =
-          st == CK_OK && h->bn_y_skipped ? (int)(&l - &g->layers[0]) : -1;
+      const int self = (int)(&l - &g->layers[0]);
+      g->vars[l.out[0]].lazy_value = st == CK_OK && h->bn_y_skipped ? self : -1;
+      Var& ro = g->vars[l.relu_out >= 0 ? l.relu_out : l.out[0]];
+      if (l.relu_out >= 0) ro.lazy_value = -1;
+      if (nxt && st == CK_OK && h->next_xg_done) {
+        nxt->cache.valid = true;
+        nxt->cache.src = ro.value;
+        nxt->cache.key = xp.key;
+        ro.lazy_value = self;  // the HWCN relu output: relu(bn_y(x)) on request
+        ro.lazy_value_relu = true;
+      }
+      h->next_xg = nullptr;
+      h->next_xg_done = false;
       h->fuse_relu = nullptr;
       h->bn_muinv = nullptr;
       h->bn_skip_y = false;
@@ -694,8 +732,10 @@ static void materialize_value(ck_graph* g, Var& v, cudaStream_t s) {
   Layer& l = g->layers[v.lazy_value];
   const Var& x = g->vars[l.in[0]];
   bnorm_value(x.value, g->vars[l.in[1]].value, g->vars[l.in[2]].value, l.muinv, v.value,
-              (int)(x.shape.h * x.shape.w), (int)x.shape.c, (int)x.shape.n, s);
+              (int)(x.shape.h * x.shape.w), (int)x.shape.c, (int)x.shape.n,
+              v.lazy_value_relu ? 1 : 0, s);
   v.lazy_value = -1;
+  v.lazy_value_relu = false;
 }
 
 // The conv output's derivative a bnorm backward skipped (it wrote the conv's

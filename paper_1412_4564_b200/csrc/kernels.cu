@@ -2470,6 +2470,119 @@ void bnorm_backward_apply(const float* x, const float* dy, const float* w, const
 #undef CK_BNB
 }
 
+// Fused bnorm -> relu forward for a relu output read only by the next conv
+// (VGG bn -> relu -> conv): relu(bn_y(x)) goes straight into that conv's
+// padded pixel-major x grid (x at (pt, pl) of an Hg x Wg grid; channel c of
+// group g' at g' Cgp + c - g' Cg) instead of HWCN -- the conv skips its input
+// transform.  One pixel per thread walks the channels (x read coalesced per
+// channel plane); every 32 channels the warp's stage goes out as float4 runs
+// of four pixels' 128-byte grid rows.  mu / inv / moments exactly as
+// bnorm_apply_k computes them (block 0 writes the moments and (mu, inv)).
+struct BnXGridOut {
+  float* grid;
+  int H, Hg, Wg, Cg, Cgp, Cp, pt, pl;
+};
+
+__global__ void __launch_bounds__(256) bnorm_apply_grid_k(const float* __restrict__ x,
+                                                          const float* __restrict__ w,
+                                                          const float* __restrict__ b,
+                                                          const double* __restrict__ stats,
+                                                          float* __restrict__ mom_out,
+                                                          float* __restrict__ muinv_out,
+                                                          double eps, int HW, int C,
+                                                          int64_t pixels, BnXGridOut go) {
+  ck::pdl_entry();
+  extern __shared__ float asm_[];
+  float* cw = asm_;  // [C] each
+  float* cmu = cw + C;
+  float* cinv = cmu + C;
+  float* cb = cinv + C;
+  float* stage = cb + C;  // [8 warps][32][33]
+  int* grs = (int*)(stage + 8 * 32 * 33);
+  const double M = (double)pixels;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const double m = stats[c * 4] / M;
+    double var = stats[c * 4 + 1] / M - m * m;
+    if (var < 0) var = 0;
+    const float mu = (float)m, inv = (float)(1.0 / sqrt(var + eps));
+    cmu[c] = mu;
+    cinv[c] = inv;
+    cw[c] = w[c];
+    cb[c] = b[c];
+    if (blockIdx.x == 0) {
+      if (mom_out) {
+        mom_out[c] = (float)m;
+        mom_out[C + c] = (float)var;
+      }
+      if (muinv_out) {
+        muinv_out[2 * c] = mu;
+        muinv_out[2 * c + 1] = inv;
+      }
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int q4 = lane >> 3, m4 = lane & 7;
+  float* st = stage + wib * 32 * 33;
+  for (int64_t eb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane; eb < pixels;
+       eb += (int64_t)gridDim.x * blockDim.x) {
+    const bool live = eb + lane < pixels;
+    const int64_t e = live ? eb + lane : pixels - 1;
+    const int64_t n = e / HW;
+    const int p = (int)(e - n * HW);
+    {
+      const int i = p % go.H, jj = p / go.H;
+      __syncwarp();
+      grs[wib * 32 + lane] =
+          live ? (int)(((int64_t)n * go.Wg * go.Hg + (int64_t)(jj + go.pl) * go.Hg + i + go.pt) * go.Cp)
+               : -1;
+    }
+    const float* xp = x + n * C * HW + p;
+    for (int c0 = 0; c0 < C; c0 += 32) {
+#pragma unroll 8
+      for (int u = 0; u < 32; ++u) {
+        const int c = c0 + u;
+        const float o = bn_y(__ldg(xp + (int64_t)c * HW), cw[c], cmu[c], cinv[c], cb[c]);
+        st[lane * 33 + u] = o > 0.f ? o : 0.f;
+      }
+      __syncwarp();
+      const int grp = c0 / go.Cg;
+      const int cpos = grp * go.Cgp + (c0 - grp * go.Cg) + 4 * m4;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int q = 4 * it + q4;
+        const int rq = grs[wib * 32 + q];
+        const float* src = st + q * 33 + 4 * m4;
+        if (rq >= 0)
+          *reinterpret_cast<float4*>(go.grid + rq + cpos) = make_float4(src[0], src[1], src[2], src[3]);
+      }
+      __syncwarp();
+    }
+  }
+}
+
+bool bnorm_apply_grid(const float* x, const float* w, const float* b, const double* stats,
+                      float* moments_out, float* muinv_out, double eps, int H, int W, int C, int N,
+                      float* grid, int Hg, int Wg, int Cg, int Cgp, int groups, int pt, int pl,
+                      cudaStream_t s) {
+  const int HW = H * W;
+  const int64_t pixels = (int64_t)HW * N;
+  if (Cg * groups != C || Cg % 32 || C % 32 || H + pt > Hg || W + pl > Wg) return false;
+  if ((int64_t)N * Hg * Wg * Cgp * groups >= (1ll << 31)) return false;
+  const size_t smem = sizeof(float) * (4 * (size_t)C + 8 * 32 * 33) + sizeof(int) * 8 * 32;
+  if (smem > 227 * 1024) return false;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(bnorm_apply_grid_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    configured = 227 * 1024;
+  }
+  BnXGridOut go{grid, H, Hg, Wg, Cg, Cgp, Cgp * groups, pt, pl};
+  count_launch();
+  ck::pdl_launch(bnorm_apply_grid_k, dim3(blocks_for(pixels, 256, 8)), 256, smem, s, x, w, b, stats,
+                 moments_out, muinv_out, eps, HW, C, pixels, go);
+  return true;
+}
+
 // y = bn_y(x) with the forward's own float (mu, inv) per channel: the bnorm
 // output a fused bnorm -> relu forward did not store (engine bn_lazy_y),
 // bit-identical to what bnorm_apply_k would have written.
@@ -2478,20 +2591,21 @@ __global__ void __launch_bounds__(256) bnorm_value_k(const float* __restrict__ x
                                                      const float* __restrict__ b,
                                                      const float* __restrict__ muinv,
                                                      float* __restrict__ y, int HW, int C,
-                                                     int64_t n_total) {
+                                                     int64_t n_total, int relu) {
   ck::pdl_entry();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)((e / HW) % C);
-    y[e] = bn_y(x[e], w[c], muinv[2 * c], muinv[2 * c + 1], b[c]);
+    const float o = bn_y(x[e], w[c], muinv[2 * c], muinv[2 * c + 1], b[c]);
+    y[e] = relu ? (o > 0.f ? o : 0.f) : o;
   }
 }
 
 void bnorm_value(const float* x, const float* w, const float* b, const float* muinv, float* y,
-                 int HW, int C, int N, cudaStream_t s) {
+                 int HW, int C, int N, int relu, cudaStream_t s) {
   const int64_t n = (int64_t)HW * C * N;
   count_launch();
-  ck::pdl_launch(bnorm_value_k, blocks_for(n, 256), 256, 0, s, x, w, b, muinv, y, HW, C, n);
+  ck::pdl_launch(bnorm_value_k, blocks_for(n, 256), 256, 0, s, x, w, b, muinv, y, HW, C, n, relu);
 }
 
 bool bnorm_backward_grid(const float* x, const float* dy, const float* w, const double* stats,

@@ -405,7 +405,9 @@ def test_bnorm_writes_conv_dy_grid(image):
     its producer conv's dy grid and bias partials (bnorm_backward_grid), the
     conv's backward skips its dy transform, and the conv output's derivative
     is computed on request; the fused bnorm -> relu forward stores only
-    relu(y), y being recomputed from x on request (bn_lazy_y).  Every value
+    relu(y), y being recomputed from x on request (bn_lazy_y), and when the
+    relu output feeds only a conv it goes straight into that conv's x grid
+    (producer_grid), the HWCN relu output recomputed on request.  Every value
     and derivative is bit-identical to
     the unfused engine except the conv bias gradients (mathematically zero in
     front of a bnorm; 32-pixel float partials in another fixed order): 1e-5 of
@@ -417,6 +419,7 @@ def test_bnorm_writes_conv_dy_grid(image):
         g = device_graph(net, "tf32")
         g.set_option("bn_grid", on)
         g.set_option("bn_lazy_y", on)
+        g.set_option("producer_grid", on)
         for k, v in {**net.init_params(), **net.init_inputs()}.items():
             g.set(k, v)
         g.forward()
