@@ -490,6 +490,11 @@ def main():
                     "peak": tf32_peak, "unit": "TFLOP/s", "frac": achieved / tf32_peak,
                     "traffic": traffic_db.get(lab), "peak_source": peak_src, "launch_ms": kms,
                     "algorithmic_flop": kfl,
+                    # the same launch against TF32 = half the pool's measured bf16 rate
+                    # (MEASURED_PEAKS.json), burst and sustained: looser denominators
+                    "frac_vs_half_bf16": {
+                        "burst": achieved / ((peaks.get("bf16_tflops") or 1653.5) / 2.0),
+                        "sustained": achieved / ((peaks.get("bf16_tflops_sustained") or 1397.0) / 2.0)},
                     "share_of_step": kms / max(step_layers_ms, 1e-9),
                     "all_gemm": {"achieved": sum(r[2] for r in kprof) / (gemm_ms / 1e3) / 1e12,
                                  "ms": gemm_ms, "launches": len(kprof)},
