@@ -901,11 +901,12 @@ __global__ void __launch_bounds__(320) lrn_maxpool3s2_k(
   }
 }
 
-// GRID: instead of dx, store relu_backward(x, dx) -- x is the output of the
-// ReLU feeding this LRN, so x > 0 is that ReLU's mask (activation.cpp:14-22)
-// -- straight into the pixel-major dy grid of the conv below that ReLU (dy at
-// (0, 0) of an Hg x Wg grid, channel g*Kgp + c of group g), with per-warp
-// per-channel sums of the stored values (the conv's bias gradient partials).
+// lrn_bwd_grid_k's output: instead of dx, relu_backward(x, dx) -- x is the
+// output of the ReLU feeding this LRN, so x > 0 is that ReLU's mask
+// (activation.cpp:14-22) -- straight into the pixel-major dy grid of the conv
+// below that ReLU (dy at (0, 0) of an Hg x Wg grid, channel g*Kgp + c of group
+// g), with per-warp per-channel sums of the stored values (the conv's bias
+// gradient partials).
 struct LrnGridOut {
   float* grid;
   double* bpart;  // [pixel warp][Kgp * groups]
@@ -921,35 +922,18 @@ struct LrnGridOut {
 #ifndef CK_LRN_GRID_P
 #define CK_LRN_GRID_P 8
 #endif
-template <int NW, bool kAcc, bool GRID = false>
-__global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
-                              int HW, int C, int64_t pixels, float kappa, float alpha, float beta,
-                              LrnGridOut go = LrnGridOut{}) {
+template <int NW, bool kAcc>
+__global__ void __launch_bounds__(128, 6) lrn_bwd_reg_k(const float* __restrict__ x, const float* __restrict__ dy, float* dx,
+                              int HW, int C, int64_t pixels, float kappa, float alpha, float beta) {
   ck::pdl_entry();
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
   constexpr int P = CK_LRN_BWD_P;  // prefetch distance (channels): 2P loads in flight per thread
   const float nb = -beta;
   const float c2ab = __fmul_rn(__fmul_rn(2.f, alpha), beta);
-  const int lane = threadIdx.x & 31, warp_in_block = threadIdx.x >> 5;
-  __shared__ float gsm[GRID ? 4 : 1][32][33];  // GRID: per-warp [pixel][channel] stage
-  __shared__ int grs[GRID ? 4 : 1][32];  // GRID: per-warp pixel grid row offsets (< 2^31)
-  // GRID: whole warps walk the pixels together (the bias partials are warp
-  // sums); lanes past the end repeat the last pixel and store nothing
-  for (int64_t eb = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - (GRID ? lane : 0);
-       eb < pixels; eb += (int64_t)gridDim.x * blockDim.x) {
-    const bool live = !GRID || eb + lane < pixels;
-    const int64_t e = GRID ? (live ? eb + lane : pixels - 1) : eb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pixels;
+       e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = e / HW;
     const int p = (int)(e - n * HW);
-    int64_t grow0 = 0;  // GRID: this pixel's grid row offset (floats)
-    int gch = 0, gcl = 0;  // GRID: (group, channel in group) of the next stored channel
-    if (GRID) {
-      const int i = p % go.H, jj = p / go.H;
-      grow0 = ((int64_t)n * go.Hg * go.Wg + i + (int64_t)go.Hg * jj) * go.Cp;
-      __syncwarp();  // the previous pixel group's flushes are done with grs
-      grs[warp_in_block][lane] = live ? (int)grow0 : -1;
-      __syncwarp();
-    }
     const int64_t base = n * C * HW + p;
     const float* xp = x + base;
     const float* gp = dy + base;
@@ -1011,36 +995,8 @@ __global__ void __launch_bounds__(128, GRID ? CK_LRN_GRID_MINB : 6) lrn_bwd_reg_
         // k in [d-UP, d+DOWN] = [j-NW+1, j]: the whole eta window (etasum)
         const float r = __fadd_rn(__fmul_rn(gs[0], Ls[0]),
                                   -__fmul_rn(__fmul_rn(c2ab, xs[0]), etasum));
-        if (GRID) {
-          // staged per warp as [pixel][channel mod 32]; every 32 channels the warp
-          // writes each of its pixels' 128-byte channel run with one coalesced store
-          const int c = j - DOWN, cpos = gch * go.Kgp + gcl;  // channel c of group gch
-          if (++gcl == go.Kg) {
-            gcl = 0;
-            ++gch;
-          }
-          const float v = (live && xs[0] > 0.f) ? r : 0.f;
-          gsm[warp_in_block][lane][c & 31] = v;
-          if ((c & 31) == 31) {
-            __syncwarp();
-            // lane = channel: store the 32 pixels' values of that channel, and
-            // their sum (the bias partial of this pixel group, pixels in order)
-            float* gb = go.grid + (cpos - 31 + lane);
-            float t = 0.f;  // 32-pixel partial in float; partials summed in double
-#pragma unroll 8
-            for (int q = 0; q < 32; ++q) {
-              const int rq = grs[warp_in_block][q];  // -1: lane q has no pixel
-              const float vq = gsm[warp_in_block][q][lane];
-              t += vq;
-              if (rq >= 0) gb[rq] = vq;
-            }
-            go.bpart[(eb >> 5) * go.Cp + cpos - 31 + lane] = t;
-            __syncwarp();
-          }
-          (void)slot;
-        } else {
-          *dq = kAcc ? __fadd_rn(*dq, r) : r;
-        }
+        *dq = kAcc ? __fadd_rn(*dq, r) : r;
+        (void)slot;
       }
       // advance the x window to lead index j + 1
       const float sqin = __fmul_rn(xlead, xlead);
@@ -2286,10 +2242,10 @@ static void lrn_bwd_reg(const float* x, const float* dy, float* dx, int HW, int 
   const int64_t pixels = (int64_t)HW * N;
   if (acc)
     ck::pdl_launch(lrn_bwd_reg_k<NW, true>, blocks_for(pixels, 128, 32), 128, 0, s, x, dy, dx, HW, C,
-                   pixels, kappa, alpha, beta, LrnGridOut{});
+                   pixels, kappa, alpha, beta);
   else
     ck::pdl_launch(lrn_bwd_reg_k<NW, false>, blocks_for(pixels, 128, 32), 128, 0, s, x, dy, dx, HW, C,
-                   pixels, kappa, alpha, beta, LrnGridOut{});
+                   pixels, kappa, alpha, beta);
 }
 
 #define CK_LRN_SWITCH(size, CALL) \
