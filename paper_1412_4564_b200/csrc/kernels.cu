@@ -1511,6 +1511,16 @@ __global__ void __launch_bounds__(256) bnorm_bwd_k(const float* __restrict__ x,
 // (the conv's bias-gradient partials, [pixel warp][Cp] doubles).  The
 // per-channel constants come from the stats pass, computed per block in
 // bnorm_bwd_k's expressions.  Requires the conv's channels per group % 32 == 0.
+// channels per block of the pixel-major bnorm grid kernels: all of them when
+// the pixels alone fill ~4 blocks per SM, else fewer (a multiple of 32)
+static int bn_grid_cchunk(int64_t pixels, int C) {
+  const int64_t pblocks = std::min<int64_t>((pixels + 255) / 256, 148 * 8);
+  int64_t want = (148 * 4 + pblocks - 1) / pblocks;  // channel chunks wanted
+  int64_t cc = (C + want - 1) / want;
+  cc = (cc + 31) / 32 * 32;
+  return (int)std::max<int64_t>(32, std::min<int64_t>(C, cc));
+}
+
 struct BnGridOut {
   float* grid;
   double* bpart;
@@ -1527,22 +1537,26 @@ __global__ void __launch_bounds__(256) bnorm_bwd_grid_k(const float* __restrict_
                                                         const double* __restrict__ stats,
                                                         double eps, int HW, int C,
                                                         int64_t pixels, BnGridOut go,
-                                                        float* dw, float* db, int acc_params) {
+                                                        float* dw, float* db, int acc_params,
+                                                        int cchunk) {
   ck::pdl_entry();
+  // blockIdx.y: channels [cb, ce) (a multiple of 32 wide) -- small images with
+  // many channels get their parallelism from here
+  const int cb = blockIdx.y * cchunk, ce = min(C, cb + cchunk), CC = ce - cb;
   extern __shared__ float bsm[];
-  float* cmu = bsm;            // [C] each
-  float* cinv = cmu + C;
-  float* cwinv = cinv + C;
-  float* cmdy = cwinv + C;
-  float* cmdyx = cmdy + C;
-  float* gw = cmdyx + C;       // G == 2: the gate's (w, b, mu, inv)
-  float* gbb = gw + C;
-  float* gmu = gbb + C;
-  float* ginv = gmu + C;
-  float* stage = ginv + C;     // [8 warps][32 pixels][33]
+  float* cmu = bsm - cb;       // [cb, ce) each
+  float* cinv = cmu + CC;
+  float* cwinv = cinv + CC;
+  float* cmdy = cwinv + CC;
+  float* cmdyx = cmdy + CC;
+  float* gw = cmdyx + CC;      // G == 2: the gate's (w, b, mu, inv)
+  float* gbb = gw + CC;
+  float* gmu = gbb + CC;
+  float* ginv = gmu + CC;
+  float* stage = ginv + CC + cb;  // [8 warps][32 pixels][33]
   int* grs = (int*)(stage + 8 * 32 * 33);  // [8 warps][32]
   const double M = (double)pixels;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+  for (int c = cb + threadIdx.x; c < ce; c += blockDim.x) {
     const double m = stats[c * 4] / M;
     double var = stats[c * 4 + 1] / M - m * m;
     if (var < 0) var = 0;
@@ -1584,7 +1598,7 @@ __global__ void __launch_bounds__(256) bnorm_bwd_grid_k(const float* __restrict_
     const float* xp = x + n * C * HW + p;
     const float* dp = dy + n * C * HW + p;
     const float* tp = gate ? gate + n * C * HW + p : nullptr;
-    for (int c0 = 0; c0 < C; c0 += 32) {
+    for (int c0 = cb; c0 < ce; c0 += 32) {
 #pragma unroll 8
       for (int u = 0; u < 32; ++u) {
         const int c = c0 + u;
@@ -2446,17 +2460,19 @@ __global__ void __launch_bounds__(256) bnorm_apply_grid_k(const float* __restric
                                                           float* __restrict__ mom_out,
                                                           float* __restrict__ muinv_out,
                                                           double eps, int HW, int C,
-                                                          int64_t pixels, BnXGridOut go) {
+                                                          int64_t pixels, BnXGridOut go,
+                                                          int cchunk) {
   ck::pdl_entry();
+  const int c_b = blockIdx.y * cchunk, c_e = min(C, c_b + cchunk), CC = c_e - c_b;
   extern __shared__ float asm_[];
-  float* cw = asm_;  // [C] each
-  float* cmu = cw + C;
-  float* cinv = cmu + C;
-  float* cb = cinv + C;
-  float* stage = cb + C;  // [8 warps][32][33]
+  float* cw = asm_ - c_b;  // [c_b, c_e) each
+  float* cmu = cw + CC;
+  float* cinv = cmu + CC;
+  float* cb = cinv + CC;
+  float* stage = cb + CC + c_b;  // [8 warps][32][33]
   int* grs = (int*)(stage + 8 * 32 * 33);
   const double M = (double)pixels;
-  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+  for (int c = c_b + threadIdx.x; c < c_e; c += blockDim.x) {
     const double m = stats[c * 4] / M;
     double var = stats[c * 4 + 1] / M - m * m;
     if (var < 0) var = 0;
@@ -2494,7 +2510,7 @@ __global__ void __launch_bounds__(256) bnorm_apply_grid_k(const float* __restric
                : -1;
     }
     const float* xp = x + n * C * HW + p;
-    for (int c0 = 0; c0 < C; c0 += 32) {
+    for (int c0 = c_b; c0 < c_e; c0 += 32) {
 #pragma unroll 8
       for (int u = 0; u < 32; ++u) {
         const int c = c0 + u;
@@ -2525,7 +2541,8 @@ bool bnorm_apply_grid(const float* x, const float* w, const float* b, const doub
   const int64_t pixels = (int64_t)HW * N;
   if (Cg * groups != C || Cg % 32 || C % 32 || H + pt > Hg || W + pl > Wg) return false;
   if ((int64_t)N * Hg * Wg * Cgp * groups >= (1ll << 31)) return false;
-  const size_t smem = sizeof(float) * (4 * (size_t)C + 8 * 32 * 33) + sizeof(int) * 8 * 32;
+  const int cchunk = bn_grid_cchunk(pixels, C);
+  const size_t smem = sizeof(float) * (4 * (size_t)cchunk + 8 * 32 * 33) + sizeof(int) * 8 * 32;
   if (smem > 227 * 1024) return false;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
@@ -2534,8 +2551,8 @@ bool bnorm_apply_grid(const float* x, const float* w, const float* b, const doub
   }
   BnXGridOut go{grid, H, Hg, Wg, Cg, Cgp, Cgp * groups, pt, pl};
   count_launch();
-  ck::pdl_launch(bnorm_apply_grid_k, dim3(blocks_for(pixels, 256, 8)), 256, smem, s, x, w, b, stats,
-                 moments_out, muinv_out, eps, HW, C, pixels, go);
+  ck::pdl_launch(bnorm_apply_grid_k, dim3(blocks_for(pixels, 256, 8), (C + cchunk - 1) / cchunk), 256,
+                 smem, s, x, w, b, stats, moments_out, muinv_out, eps, HW, C, pixels, go, cchunk);
   return true;
 }
 
@@ -2572,7 +2589,8 @@ bool bnorm_backward_grid(const float* x, const float* dy, const float* w, const 
   const int64_t pixels = (int64_t)HW * N;
   if (H > Hg || W > Wg || Kg * groups != C || Kg % 32 || C % 32) return false;
   if ((int64_t)N * Hg * Wg * Kgp * groups >= (1ll << 31)) return false;
-  const size_t smem = sizeof(float) * (9 * (size_t)C + 8 * 32 * 33) + sizeof(int) * 8 * 32;
+  const int cchunk = bn_grid_cchunk(pixels, C);
+  const size_t smem = sizeof(float) * (9 * (size_t)cchunk + 8 * 32 * 33) + sizeof(int) * 8 * 32;
   if (smem > 227 * 1024) return false;
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
@@ -2583,17 +2601,17 @@ bool bnorm_backward_grid(const float* x, const float* dy, const float* w, const 
   }
   BnGridOut go{grid, bpart, H, Hg, Wg, Kg, Kgp, Kgp * groups};
   const int G = rg.muinv ? 2 : gate ? 1 : 0;
-  const dim3 grd(blocks_for(pixels, 256, 8));
+  const dim3 grd(blocks_for(pixels, 256, 8), (C + cchunk - 1) / cchunk);
   count_launch();
   if (G == 2)
     ck::pdl_launch(bnorm_bwd_grid_k<2>, grd, 256, smem, s, x, dy, nullptr, rg.b, rg.muinv, w, stats, eps,
-                   HW, C, pixels, go, dw, db, acc);
+                   HW, C, pixels, go, dw, db, acc, cchunk);
   else if (G == 1)
     ck::pdl_launch(bnorm_bwd_grid_k<1>, grd, 256, smem, s, x, dy, gate, nullptr, nullptr, w, stats, eps,
-                   HW, C, pixels, go, dw, db, acc);
+                   HW, C, pixels, go, dw, db, acc, cchunk);
   else
     ck::pdl_launch(bnorm_bwd_grid_k<0>, grd, 256, smem, s, x, dy, nullptr, nullptr, nullptr, w, stats,
-                   eps, HW, C, pixels, go, dw, db, acc);
+                   eps, HW, C, pixels, go, dw, db, acc, cchunk);
   return true;
 }
 
