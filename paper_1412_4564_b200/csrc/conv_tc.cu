@@ -128,6 +128,7 @@ struct GemmParams {
   int nacc;               // TMEM accumulator buffers (2: epilogue overlaps mainloop)
   int groups;             // tiles = ceil(M/BM) * ceil(N/BN) * groups * splits
   int b_rows;             // OP_SHIFT_MN: channels per TMA box (divides Cgp and BN)
+  int a_rows;             // A = OP_SHIFT_MN (weight gradient, roles swapped): same, dividing BM
   int a_mn3d, b_mn3d;     // OP_TILED_MN: one 3D box per stage (MN % 32 == 0) vs R/32 2D boxes
   int taps;               // OP_SHIFT_MN / halo kernel: fh * fw
   int kstage;             // K per pipeline stage: 32, or 64 (MN-major pair, or SHIFT_K/TILED_K3)
@@ -864,6 +865,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           fj = tap / p.fh;
           fi = tap - fj * p.fh;
         }
+        // OP_SHIFT_MN A boxes (roles swapped: M = (tap, c)), same walk as B's
+        int a_shift[8], a_cb[8];
+        const int nabox = AK == OP_SHIFT_MN ? p.BM / p.a_rows : 0;
+        if (AK == OP_SHIFT_MN) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int mm = T.m0 + j * p.a_rows;
+            int tap = mm / (p.cchunks * 32);
+            const int c = mm - tap * p.cchunks * 32;
+            tap = min(tap, p.taps - 1);  // rows past the last tap are masked
+            const int jj = tap / p.fh, ii = tap - jj * p.fh;
+            a_shift[j] = ii + p.Hp * jj;
+            a_cb[j] = (T.grp * p.a_grp_c + c) / 32;
+          }
+        }
         // OP_SHIFT_MN B boxes: per-tile (row shift, channel block) of each box
         int b_shift[8], b_cb[8];
         const int nbox = BK == OP_SHIFT_MN ? p.BN / p.b_rows : 0;
@@ -898,6 +914,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               else
                 for (int j = 0; j < p.BM / 32; ++j)
                   tma_2d_p(a + j * KS * 128, &tma_a, &full[s], mn0 + 32 * j, k0, lead);
+            } else if (AK == OP_SHIFT_MN) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                if (j < nabox)
+                  tma_3d_p(a + j * p.a_rows * KS * 4, &tma_a, &full[s], 0, k0 + a_shift[j], a_cb[j],
+                           lead);
             } else if (AK == OP_SHIFT_K) {
               // K block = KS channels of one tap (KS divides Cgp): BM consecutive
               // grid rows shifted by the tap, one 3D box of KS/32 channel chunks
@@ -952,7 +974,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // --------------------------------------------------------- MMA issuer --
     // the whole warp walks the loop; one elected lane issues each MMA/commit
     {
-      constexpr bool a_mn = AK == OP_TILED_MN,
+      constexpr bool a_mn = AK == OP_TILED_MN || AK == OP_SHIFT_MN,
                      b_mn = BK == OP_TILED_MN || BK == OP_SHIFT_MN;
       const uint32_t idesc = idesc_tf32(p.BN, a_mn, b_mn);
       int it = 0, tc = 0;
@@ -1479,9 +1501,10 @@ __global__ void repack_dgrad_k(const float* __restrict__ f, float* __restrict__ 
 }
 
 // wgrad: df[fi,fj,c,k] (+)= sum_s part[s][g][n = tap*Cgp + cpos][k]  (fixed order)
+// swapped: the partials of the role-swapped GEMM, part[g][k][(tap, c)]
 __global__ void wgrad_finish_k(const float* __restrict__ part, float* df, int fh, int fw, int Cg,
                                int Cgp, int Kg, int groups, int splits, int64_t split_stride,
-                               int64_t fsc, int64_t fsk, int acc) {
+                               int64_t fsc, int64_t fsk, int acc, int swapped) {
   ck::pdl_entry();
   const int taps = fh * fw;
   const int total = groups * Kg * taps * Cg;
@@ -1492,7 +1515,9 @@ __global__ void wgrad_finish_k(const float* __restrict__ part, float* df, int fh
     int r2 = r / Cg;
     const int c = r - r2 * Cg;
     const int g = r2 / taps, tap = r2 - g * taps;
-    const int64_t src = ((int64_t)g * taps * Cgp + (int64_t)tap * Cgp + c) * Kg + k;
+    const int64_t src = swapped ? (int64_t)g * taps * Cgp * Kg + (int64_t)k * taps * Cgp +
+                                      (int64_t)tap * Cgp + c
+                                : ((int64_t)g * taps * Cgp + (int64_t)tap * Cgp + c) * Kg + k;
     float s = 0.f;
 #pragma unroll 4
     for (int sp = 0; sp < splits; ++sp) s += __ldg(part + sp * split_stride + src);
@@ -2569,6 +2594,55 @@ static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, c
 // A = dYg read MN-major (one 3D box of BM channels x 32 rows); B = Xg rows
 // shifted by the tap, one 3D box per tap of b_rows channels (tiled TMA, no
 // im2col).  Junk grid rows carry dy = 0.  Returns the split count.
+// Roles swapped (M = (tap, c), N = k) when the filter count leaves most of a
+// 128-row tile empty (VGG's 64 filters: half; AlexNet conv4's 192: a third)
+// and the (tap, c) rows fill whole tiles: partials part[g][k][(tap, c)]
+// (wgrad_finish_k swapped).
+static bool wgrad_swap(int Kg, int taps, int Cgp) {
+  static const int on = knob("CK_TC_WSWAP", 1);  // experiments builds: A/B switch
+  if (!on || Kg > 256 || Kg % 16) return false;
+  const double waste_k = (double)rup(Kg, 128) / Kg;
+  const double waste_t = (double)rup(taps * Cgp, 128) / (taps * Cgp);
+  return waste_k >= 1.3 && waste_t <= 1.15;
+}
+
+static int grid_wgrad_swapped(ck_handle* h, const float* xg, int Cp, int Cgp, const float* dyg,
+                              int Kp, int Kgp, int Kg, int groups, int N, int Hg, int Wg, int fh,
+                              int fw, float** part_out, int64_t* per_out, cudaStream_t s) {
+  TcState* st = state(h);
+  const int taps = fh * fw;
+  const int Mtot = taps * Cgp;  // GEMM M = (tap, c) per group
+  const int BN = rup(Kg, 16);
+  const int BM = pick_bm(Mtot, BN);
+  const int a_rows = std::gcd(Cgp, 128);
+  const int64_t rows = (int64_t)N * Hg * Wg;
+  static const int ks_env = knob("CK_TC_WKS", 64);
+  const int KS = ks_env == 32 ? 32 : 64;
+  const int kblocks = (int)((rows + KS - 1) / KS);
+  const int splits = wgrad_splits_for(((Mtot + BM - 1) / BM) * groups, kblocks);
+  const int64_t per_grp = (int64_t)Mtot * Kg;
+  const int64_t per = per_grp * groups;
+  float* part = (float*)grow(st->part, sizeof(float) * per * splits, s);
+  GemmParams p{};
+  p.M = Mtot; p.N = Kg; p.K = kblocks * KS; p.BN = BN; p.BM = BM; p.splits = splits;
+  p.kstage = KS;
+  p.Hp = Hg; p.fh = fh; p.taps = taps; p.cchunks = Cgp / 32; p.a_rows = a_rows;
+  p.a_grp_c = Cgp;
+  p.b_grp_mn = Kgp;
+  // raw partials: part[s*per + g*per_grp + k*Mtot + (tap, c)]
+  p.epi = EPI_LINEAR; p.out = part; p.ld = Mtot; p.grp_out = per_grp; p.n_valid = Kg;
+  p.split_stride = per;
+  cuuint64_t dims[3] = {32, (cuuint64_t)rows, (cuuint64_t)(Cp / 32)};
+  cuuint64_t strides[2] = {(cuuint64_t)Cp * 4, 128};
+  cuuint32_t box[3] = {32, (cuuint32_t)KS, (cuuint32_t)(a_rows / 32)};
+  CUtensorMap ta = encode_tiled(xg, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  CUtensorMap tb = map_mn(dyg, (uint64_t)rows, Kp, Kp, BN, &p.b_mn3d, KS);
+  launch<OP_SHIFT_MN, OP_TILED_MN>(ta, tb, p, 0, 0, groups * splits, s);
+  *part_out = part;
+  *per_out = per;
+  return splits;
+}
+
 static int grid_wgrad(ck_handle* h, const float* xg, int Cp, int Cgp, const float* dyg, int Kp,
                       int Kgp, int Kg, int groups, int N, int Hg, int Wg, int fh, int fw,
                       float** part_out, int64_t* per_out, cudaStream_t s) {
@@ -3020,12 +3094,17 @@ bool conv_tc_wgrad(ck_handle* h, const float* x, const float* dy, float* df, con
   float* dyg = dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s);
   float* part;
   int64_t per;
-  const int splits = grid_wgrad(h, xg, Cp, Cgp, dyg, Kp, Kgp, Kg, d.groups, d.N, Hg, Wg, d.fh,
-                                d.fw, &part, &per, s);
+  const bool swapped = wgrad_swap(Kg, taps, Cgp);
+  const int splits =
+      swapped ? grid_wgrad_swapped(h, xg, Cp, Cgp, dyg, Kp, Kgp, Kg, d.groups, d.N, Hg, Wg, d.fh,
+                                   d.fw, &part, &per, s)
+              : grid_wgrad(h, xg, Cp, Cgp, dyg, Kp, Kgp, Kg, d.groups, d.N, Hg, Wg, d.fh, d.fw,
+                           &part, &per, s);
   const int64_t total = (int64_t)d.groups * Kg * taps * d.Cg;
   count_launch();
   ck::pdl_launch(wgrad_finish_k, std::min<int64_t>((total + 255) / 256, 148 * 8), 256, 0, s, 
-      part, df, d.fh, d.fw, d.Cg, Cgp, Kg, d.groups, splits, per, d.fsc, d.fsk, acc);
+      part, df, d.fh, d.fw, d.Cg, Cgp, Kg, d.groups, splits, per, d.fsc, d.fsk, acc,
+      swapped ? 1 : 0);
   return true;
 }
 
