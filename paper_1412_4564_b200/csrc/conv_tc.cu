@@ -105,6 +105,7 @@ struct GemmParams {
   int base_shift;         // OP_SHIFT_K: row offset added to every tap shift (dgrad: -(qt+Hp*ql))
   int b_grp_row;          // halo kernel: per-group filter row offset
   int s2d, s2d_U, s2d_H, s2d_W, s2d_C;  // EPI_S2D: factor, grid height, target dims
+  int s2d_Ct;             // EPI_S2D with groups: channels per image (s2d_C: per group; 0: = s2d_C)
   int exp;                // debug experiments (CK_TC_EXP)
   int snake;              // epilogue: snake-order (half, chunk) units (CK_EPI_SNAKE=0 disables)
   int last_k;             // OP_IM2COL_K: K=8 MMAs needed in a tap's last 32-channel chunk
@@ -545,7 +546,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmParams& p, const Tile& T
       const int v = pix / p.s2d_U, u = pix - v * p.s2d_U;
       s_i = p.s2d * u;
       s_j = p.s2d * v;
-      row_base = (int64_t)img * p.s2d_C * p.s2d_H * p.s2d_W;
+      row_base = ((int64_t)img * (p.s2d_Ct ? p.s2d_Ct : p.s2d_C) + (int64_t)T.grp * p.grp_col) *
+                 p.s2d_H * p.s2d_W;
     } else if (p.epi == EPI_PIX) {
       row_base = (int64_t)img * p.img_stride + pix + (int64_t)T.grp * p.grp_col * p.ld;
     } else {
@@ -1497,6 +1499,32 @@ __global__ void repack_dgrad_k(const float* __restrict__ f, float* __restrict__ 
       v = __ldg(f + fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + k * fsk)));
     }
     gt[e] = v;
+  }
+}
+
+// B of the 2 x 2-blocked data gradient (conv_tc_dgrad, few channels per
+// group): row n = (da + 2 db) Cg + c of group g, column t' Kgp + k with
+// t' = u' + (fh + 1) v' over the (fh + 1) x (fw + 1) window of a 2 x 2 output
+// block: the flipped tap (u' - da, v' - db) when it lies in the filter, else 0.
+__global__ void repack_dgrad_blk_k(const float* __restrict__ f, float* __restrict__ gt, int fh,
+                                   int fw, int Cg, int Kg, int Kgp, int groups, int64_t fsc,
+                                   int64_t fsk) {
+  ck::pdl_entry();
+  const int th = fh + 1, taps = th * (fw + 1);
+  const int total = groups * 4 * Cg * taps * Kgp;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int kp = e % Kgp, r = e / Kgp;
+    const int tap = r % taps, rr = r / taps;
+    const int g = rr / (4 * Cg), n = rr - g * 4 * Cg;
+    const int blk = n / Cg, c = n - blk * Cg, da = blk & 1, db = blk >> 1;
+    const int u = tap % th, v = tap / th, ti = u - da, tj = v - db;
+    float val = 0.f;
+    if (kp < Kg && ti >= 0 && ti < fh && tj >= 0 && tj < fw) {
+      const int fi = fh - 1 - ti, fj = fw - 1 - tj;
+      const int64_t k = (int64_t)g * Kg + kp;
+      val = __ldg(f + fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + k * fsk)));
+    }
+    gt[e] = val;
   }
 }
 
@@ -2904,6 +2932,48 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   const int Kgp = rup(Kg, 32), Kp = Kgp * d.groups;
   const int taps = d.fh * d.fw;
   TcState* st = state(h);
+  static const int blk_on = knob("CK_TC_DBLK", 1);  // experiments builds: A/B switch
+  if (blk_on && d.Cg % 16 == 0 && d.Cg <= 64 && d.fh >= 3 && d.fw >= 3 && d.fh <= 15 &&
+      d.fw <= 15 && !h->prev_dyg && d.H >= 2 && d.W >= 2) {
+    // few channels per group (AlexNet conv2: 48): the MMA N = Cg is too narrow
+    // for the operand traffic it costs.  Compute 2 x 2 output blocks per GEMM
+    // row instead: N = 4 Cg, K over the (fh+1) x (fw+1) dy window of a block
+    // (im2col with traversal stride 2), 4x fewer A rows -- the window costs
+    // (fh+1)(fw+1) / (fh fw) more MMAs; the EPI_S2D epilogue scatters the
+    // block to dx.
+    const int th = d.fh + 1, tw = d.fw + 1, taps6 = th * tw;
+    const int qt = d.fh - 1 - d.pt, ql = d.fw - 1 - d.pl;
+    float* gb = (float*)grow(st->ft, sizeof(float) * (size_t)d.groups * 4 * d.Cg * taps6 * Kgp, s);
+    count_launch();
+    ck::pdl_launch(repack_dgrad_blk_k,
+                   std::min<int64_t>(((int64_t)d.groups * 4 * d.Cg * taps6 * Kgp + 255) / 256, 148 * 8),
+                   256, 0, s, f, gb, d.fh, d.fw, d.Cg, Kg, Kgp, d.groups, d.fsc, d.fsk);
+    int Hg, Wg;
+    grid_dims(d, Hg, Wg);
+    float* dyt = dy_grid(h, dy, d, Kg, Kgp, d.groups, Hg, Wg, s);
+    const int Ha = (d.H + 1) / 2, Wa = (d.W + 1) / 2;
+    GemmParams p{};
+    p.M = d.N * Ha * Wa;
+    p.N = 4 * d.Cg;
+    p.K = taps6 * Kgp;
+    p.BN = 4 * d.Cg;
+    p.splits = 1;
+    p.OH = Ha; p.OW = Wa; p.sh = 2; p.sw = 2; p.pt = qt; p.pl = ql; p.fh = th;
+    p.cchunks = Kgp / 32;
+    p.last_k = Kg % 32 ? (Kg % 32 + 7) / 8 : 4;
+    p.a_grp_c = Kgp;
+    p.b_grp_mn = 4 * d.Cg;
+    p.epi = EPI_S2D; p.out = dx; p.s2d = 2; p.s2d_U = Ha; p.s2d_H = d.H; p.s2d_W = d.W;
+    p.s2d_C = d.Cg; p.s2d_Ct = d.C; p.grp_col = d.Cg; p.epi_OHW = Ha * Wa;
+    p.acc = acc; p.n_valid = 4 * d.Cg;
+    p.BM = pick_bm(p.M, p.BN, true, d.groups);
+    CUtensorMap ta = map_im2col(dyt, Kp, Hg, Wg, d.N, -qt, -ql, 2 * Ha - 1 - Hg - qt,
+                                2 * Wa - 1 - Wg - ql, 2, 2, p.BM);
+    CUtensorMap tb = map_2d(gb, (uint64_t)taps6 * Kgp, (uint64_t)d.groups * 4 * d.Cg,
+                            (uint64_t)taps6 * Kgp, p.BN);
+    launch<OP_IM2COL_K, OP_TILED_K>(ta, tb, p, (p.M + 127) / 128, 1, d.groups, s);
+    return true;
+  }
   float* gt = (float*)grow(st->ft, sizeof(float) * (size_t)d.C * taps * Kgp, s);
   count_launch();
   ck::pdl_launch(repack_dgrad_k, std::min<int64_t>(((int64_t)d.C * taps * Kgp + 255) / 256, 148 * 8), 256, 0, s, 
