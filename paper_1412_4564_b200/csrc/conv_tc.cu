@@ -2933,8 +2933,11 @@ bool conv_tc_dgrad(ck_handle* h, const float* dy, const float* f, float* dx, con
   const int taps = d.fh * d.fw;
   TcState* st = state(h);
   static const int blk_on = knob("CK_TC_DBLK", 1);  // experiments builds: A/B switch
-  if (blk_on && d.Cg % 16 == 0 && d.Cg <= 64 && d.fh >= 3 && d.fw >= 3 && d.fh <= 15 &&
-      d.fw <= 15 && !h->prev_dyg && d.H >= 2 && d.W >= 2) {
+  // (5 x 5 filters and up: the block window's zero taps cost (f+1)^2 / f^2 more
+  // MMAs, 1.44x at 5 x 5 but 1.78x at 3 x 3; large layers only)
+  if (blk_on && d.Cg % 16 == 0 && d.Cg <= 64 && d.fh >= 5 && d.fw >= 5 && d.fh <= 15 &&
+      d.fw <= 15 && !h->prev_dyg && d.H >= 2 && d.W >= 2 &&
+      (int64_t)d.N * d.H * d.W >= (1 << 17)) {
     // few channels per group (AlexNet conv2: 48): the MMA N = Cg is too narrow
     // for the operand traffic it costs.  Compute 2 x 2 output blocks per GEMM
     // row instead: N = 4 Cg, K over the (fh+1) x (fw+1) dy window of a block
