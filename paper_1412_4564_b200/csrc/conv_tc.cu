@@ -2628,7 +2628,8 @@ static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, c
 // (wgrad_finish_k swapped).
 static bool wgrad_swap(int Kg, int taps, int Cgp) {
   static const int on = knob("CK_TC_WSWAP", 1);  // experiments builds: A/B switch
-  if (!on || Kg > 256 || Kg % 16) return false;
+  // (filter counts that are multiples of 64 -- 64, 192 -- are the measured shapes)
+  if (!on || Kg > 256 || Kg % 64) return false;
   const double waste_k = (double)rup(Kg, 128) / Kg;
   const double waste_t = (double)rup(taps * Cgp, 128) / (taps * Cgp);
   return waste_k >= 1.3 && waste_t <= 1.15;
