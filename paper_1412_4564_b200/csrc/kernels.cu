@@ -1544,7 +1544,7 @@ __global__ void __launch_bounds__(256) bnorm_bwd_grid_k(const float* __restrict_
   // many channels get their parallelism from here
   const int cb = blockIdx.y * cchunk, ce = min(C, cb + cchunk), CC = ce - cb;
   extern __shared__ float bsm[];
-  float* cmu = bsm - cb;       // [cb, ce) each
+  float* cmu = bsm;            // [ce - cb] each, indexed by c - cb
   float* cinv = cmu + CC;
   float* cwinv = cinv + CC;
   float* cmdy = cwinv + CC;
@@ -1553,7 +1553,7 @@ __global__ void __launch_bounds__(256) bnorm_bwd_grid_k(const float* __restrict_
   float* gbb = gw + CC;
   float* gmu = gbb + CC;
   float* ginv = gmu + CC;
-  float* stage = ginv + CC + cb;  // [8 warps][32 pixels][33]
+  float* stage = ginv + CC;    // [8 warps][32 pixels][33]
   int* grs = (int*)(stage + 8 * 32 * 33);  // [8 warps][32]
   const double M = (double)pixels;
   for (int c = cb + threadIdx.x; c < ce; c += blockDim.x) {
@@ -1568,16 +1568,16 @@ __global__ void __launch_bounds__(256) bnorm_bwd_grid_k(const float* __restrict_
       if (db) db[c] = acc_params ? db[c] + (float)sdy : (float)sdy;
     }
     const float inv = (float)invd;
-    cmu[c] = (float)m;
-    cinv[c] = inv;
-    cwinv[c] = __fmul_rn(w[c], inv);
-    cmdy[c] = (float)(sdy / M);
-    cmdyx[c] = (float)(sdyx / M);
+    cmu[c - cb] = (float)m;
+    cinv[c - cb] = inv;
+    cwinv[c - cb] = __fmul_rn(w[c], inv);
+    cmdy[c - cb] = (float)(sdy / M);
+    cmdyx[c - cb] = (float)(sdyx / M);
     const BnGateP P = bn_gate_params(w, gb, muinv, c);
-    gw[c] = P.w;
-    gbb[c] = P.b;
-    gmu[c] = P.mu;
-    ginv[c] = P.inv;
+    gw[c - cb] = P.w;
+    gbb[c - cb] = P.b;
+    gmu[c - cb] = P.mu;
+    ginv[c - cb] = P.inv;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1606,8 +1606,8 @@ __global__ void __launch_bounds__(256) bnorm_bwd_grid_k(const float* __restrict_
         const float xv = __ldg(xp + off);
         float g = __ldg(dp + off);
         if (G == 1 && !(__ldg(tp + off) > 0.f)) g = 0.f;
-        if (G == 2 && !(bn_y(xv, gw[c], gmu[c], ginv[c], gbb[c]) > 0.f)) g = 0.f;
-        const float r = bn_dx(xv, g, cmu[c], cinv[c], cwinv[c], cmdy[c], cmdyx[c]);
+        if (G == 2 && !(bn_y(xv, gw[c - cb], gmu[c - cb], ginv[c - cb], gbb[c - cb]) > 0.f)) g = 0.f;
+        const float r = bn_dx(xv, g, cmu[c - cb], cinv[c - cb], cwinv[c - cb], cmdy[c - cb], cmdyx[c - cb]);
         st[lane * 33 + u] = live ? r : 0.f;
       }
       __syncwarp();
@@ -2465,11 +2465,11 @@ __global__ void __launch_bounds__(256) bnorm_apply_grid_k(const float* __restric
   ck::pdl_entry();
   const int c_b = blockIdx.y * cchunk, c_e = min(C, c_b + cchunk), CC = c_e - c_b;
   extern __shared__ float asm_[];
-  float* cw = asm_ - c_b;  // [c_b, c_e) each
+  float* cw = asm_;  // [c_e - c_b] each, indexed by c - c_b
   float* cmu = cw + CC;
   float* cinv = cmu + CC;
   float* cb = cinv + CC;
-  float* stage = cb + CC + c_b;  // [8 warps][32][33]
+  float* stage = cb + CC;  // [8 warps][32][33]
   int* grs = (int*)(stage + 8 * 32 * 33);
   const double M = (double)pixels;
   for (int c = c_b + threadIdx.x; c < c_e; c += blockDim.x) {
@@ -2477,10 +2477,10 @@ __global__ void __launch_bounds__(256) bnorm_apply_grid_k(const float* __restric
     double var = stats[c * 4 + 1] / M - m * m;
     if (var < 0) var = 0;
     const float mu = (float)m, inv = (float)(1.0 / sqrt(var + eps));
-    cmu[c] = mu;
-    cinv[c] = inv;
-    cw[c] = w[c];
-    cb[c] = b[c];
+    cmu[c - c_b] = mu;
+    cinv[c - c_b] = inv;
+    cw[c - c_b] = w[c];
+    cb[c - c_b] = b[c];
     if (blockIdx.x == 0) {
       if (mom_out) {
         mom_out[c] = (float)m;
@@ -2514,7 +2514,7 @@ __global__ void __launch_bounds__(256) bnorm_apply_grid_k(const float* __restric
 #pragma unroll 8
       for (int u = 0; u < 32; ++u) {
         const int c = c0 + u;
-        const float o = bn_y(__ldg(xp + (int64_t)c * HW), cw[c], cmu[c], cinv[c], cb[c]);
+        const float o = bn_y(__ldg(xp + (int64_t)c * HW), cw[c - c_b], cmu[c - c_b], cinv[c - c_b], cb[c - c_b]);
         st[lane * 33 + u] = o > 0.f ? o : 0.f;
       }
       __syncwarp();
