@@ -329,8 +329,11 @@ struct FastDiv {  // n / d == (n * m) >> 40 for n * d < 2^39
   }
 };
 
-// Two outputs per thread per iteration (e and e + stride): both windows'
-// loads are in flight before the first compare.
+// CK_POOL_FWD_W outputs per thread per iteration (e, e + stride, ...): all
+// the windows' loads are in flight before the first compare.
+#ifndef CK_POOL_FWD_W
+#define CK_POOL_FWD_W 2
+#endif
 template <int WH, int WW, int SH, int SW, bool INSIDE>
 __global__ void pool_max_fwd_t(const float* __restrict__ x, float* __restrict__ y, PoolDims d,
                                FastDiv by_ohw, FastDiv by_oh, uint8_t* __restrict__ argout) {
@@ -338,11 +341,11 @@ __global__ void pool_max_fwd_t(const float* __restrict__ x, float* __restrict__ 
   const int OHW = d.OH * d.OW, HW = d.H * d.W;
   const uint32_t total = (uint32_t)OHW * d.C * d.N;
   const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += 2 * stride) {
-    float v[2][WW][WH];
-    bool in[2][WW][WH];
+  for (uint32_t e0 = blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += CK_POOL_FWD_W * stride) {
+    float v[CK_POOL_FWD_W][WW][WH];
+    bool in[CK_POOL_FWD_W][WW][WH];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < CK_POOL_FWD_W; ++t) {
       const uint32_t e = e0 + t * stride;
       const bool live = e < total;
       const uint32_t ee = live ? e : e0;
@@ -363,7 +366,7 @@ __global__ void pool_max_fwd_t(const float* __restrict__ x, float* __restrict__ 
       }
     }
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < CK_POOL_FWD_W; ++t) {
       const uint32_t e = e0 + t * stride;
       if (e >= total) break;
       float best = 0.f;
