@@ -510,12 +510,17 @@ def test_engine_pool_argmax_route_bitexact(pad, side, win):
     assert np.array_equal(g.get("x", deriv=True), O.pool_backward(x, xs, pg, dp1))
 
 
-def test_trainer_cuda_graph_replay_matches_eager():
+@pytest.mark.parametrize("net_name", ["cifar", "alexnet", "vgg16bn"])
+def test_trainer_cuda_graph_replay_matches_eager(net_name):
     """ck_trainer_set_graph: the captured step replays the same deterministic
-    kernels, so parameters after 4 steps are bit-identical to eager steps."""
+    kernels, so parameters after 4 steps are bit-identical to eager steps --
+    through every fused route of the nets (AlexNet: LRN / dgrad / producer
+    grids; VGG: bnorm grid kernels, unstored bnorm values), and the values a
+    fusion left unstored are recomputed identically after a replayed step."""
     from paper_1412_4564_b200 import nets
     from paper_1412_4564_b200.graph import Trainer
-    net = nets.cifar(batch=8)
+    net = {"cifar": lambda: nets.cifar(batch=8), "alexnet": lambda: nets.alexnet(batch=4),
+           "vgg16bn": lambda: nets.vgg16_bn(batch=2, image=32)}[net_name]()
     params, inputs = net.init_params(), net.init_inputs()
     results = []
     for graph_mode in (False, True):
@@ -528,11 +533,15 @@ def test_trainer_cuda_graph_replay_matches_eager():
         stream = torch.cuda.Stream()  # graph capture needs a non-default stream
         losses = [t.step(stream=stream.cuda_stream) for _ in range(4)]
         assert g.hd.launches - before > 4 * 10  # replayed launches are still counted
-        results.append((losses, {p: g.get(p) for p, _, _ in net.params}))
-    (l0, p0), (l1, p1) = results
+        g.forward()  # (eager) the values of the current parameters, then read them all
+        vals = {o: g.get(o) for layer in net.layers for o in layer[3]}
+        results.append((losses, {p: g.get(p) for p, _, _ in net.params}, vals))
+    (l0, p0, v0), (l1, p1, v1) = results
     assert l0 == l1
     for k in p0:
         assert np.array_equal(p0[k], p1[k]), k
+    for k in v0:
+        assert np.array_equal(v0[k], v1[k]), k
 
 
 def test_feeder_bound_inputs_match_copied_inputs():
