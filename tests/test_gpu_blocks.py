@@ -128,6 +128,34 @@ def test_conv(xs, fs, g, math):
         assert tc >= 3, f"TF32 conv ran {tc} tcgen05 GEMMs (fprop+dgrad+wgrad expected)"
 
 
+@pytest.mark.parametrize("xs,fs,g", [((64, 64, 32, 32), (5, 5, 32, 16), (1, 1, 2, 2, 2, 2, 1)),
+                                     ((48, 48, 96, 64), (5, 5, 48, 64), (1, 1, 2, 2, 2, 2, 2))])
+def test_conv_blocked_dgrad(xs, fs, g):
+    """The 2 x 2-blocked data gradient (conv_tc_dgrad: groups of <= 64
+    channels, 5 x 5 filters, >= 2^17 pixels -- AlexNet conv2's route): dx
+    against the double oracle (oracle/fastconv.py) at the TF32 bound, on
+    tcgen05, and accumulate=1 adding onto dx."""
+    import fastconv as FC
+    r = np.random.default_rng(5)
+    x = r.uniform(-1, 1, O.size(xs)).astype(np.float32)
+    f = r.uniform(-0.1, 0.1, O.size(fs)).astype(np.float32)
+    geom = B.ConvGeom(*g)
+    ys = B.conv_output_shape(xs, fs, geom)
+    dy = r.uniform(-1, 1, O.size(ys)).astype(np.float32)
+    dx_ref, _, _ = FC.conv_backward(x, xs, f, fs, g, dy, want=(True, False, False))
+    hd = B.handle()
+    tc0 = hd.tc_launches
+    dx, _, _ = B.conv_backward(dev(x, xs), dev(f, fs), geom, dev(dy, ys), want_df=False,
+                               want_db=False, math="tf32")
+    assert hd.tc_launches > tc0
+    assert err(host(dx), dx_ref, "tf32") < TOL["tf32"]
+    base = r.uniform(-1, 1, O.size(xs)).astype(np.float32)
+    acc = dev(base, xs)
+    B.conv_backward(dev(x, xs), dev(f, fs), geom, dev(dy, ys), out=(acc, None, None),
+                    math="tf32", accumulate=True)
+    assert err(host(acc), dx_ref + base, "tf32") < TOL["tf32"]
+
+
 @pytest.mark.parametrize("xs,fs,g", [CONV_CASES[9], CONV_CASES[10], CONV_CASES[8],
                                      CONV_CASES[13]])
 def test_conv_accumulate_tensor_cores(xs, fs, g):
