@@ -2628,7 +2628,8 @@ static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, c
 // (wgrad_finish_k swapped).
 static bool wgrad_swap(int Kg, int taps, int Cgp) {
   static const int on = knob("CK_TC_WSWAP", 1);  // experiments builds: A/B switch
-  // (filter counts that are multiples of 64 -- 64, 192 -- are the measured shapes)
+  // (filter counts that are multiples of 64 -- 64, 192 -- are the measured shapes;
+  // the MN-major dy operand needs BN % 32 == 0: its boxes are 32 columns wide)
   if (!on || Kg > 256 || Kg % 64) return false;
   const double waste_k = (double)rup(Kg, 128) / Kg;
   const double waste_t = (double)rup(taps * Cgp, 128) / (taps * Cgp);
