@@ -1723,9 +1723,11 @@ __global__ void s2d_repack_dgrad_k(const float* __restrict__ f, float* __restric
 }
 
 // wgrad finish of the s2d conv: df[fi,fj,c,k] = sum_s part[s][(tap, c'p)][k]
+// swapped: partials of the role-swapped GEMM, part[k][n] (n = the s2d (tap, c'))
 __global__ void s2d_wgrad_finish_k(const float* __restrict__ part, float* df, int fh, int fw,
                                    int Cg, int K, int s, int Th, int Csp, int splits,
-                                   int64_t split_stride, int acc, int64_t fsc, int64_t fsk) {
+                                   int64_t split_stride, int acc, int64_t fsc, int64_t fsk,
+                                   int swapped, int64_t ntot) {
   ck::pdl_entry();
   const int64_t total = (int64_t)K * fh * fw * Cg;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -1739,7 +1741,8 @@ __global__ void s2d_wgrad_finish_k(const float* __restrict__ part, float* df, in
     const int t = fi / s, a = fi % s, t2 = fj / s, b = fj % s;
     const int64_t n = (int64_t)(t + Th * t2) * Csp + c + (int64_t)Cg * (a + s * b);
     float v = 0.f;
-    for (int sp = 0; sp < splits; ++sp) v += part[sp * split_stride + n * K + k];
+    const int64_t src = swapped ? (int64_t)k * ntot + n : n * K + k;
+    for (int sp = 0; sp < splits; ++sp) v += part[sp * split_stride + src];
     float* dst = df + fi + (int64_t)fh * (fj + (int64_t)fw * (c * fsc + k * fsk));
     *dst = acc ? *dst + v : v;
   }
@@ -2628,9 +2631,9 @@ static void s2d_pm(const float* x, float* xt, const ConvDims& d, const S2D& z, c
 // (wgrad_finish_k swapped).
 static bool wgrad_swap(int Kg, int taps, int Cgp) {
   static const int on = knob("CK_TC_WSWAP", 1);  // experiments builds: A/B switch
-  // (filter counts that are multiples of 64 -- 64, 192 -- are the measured shapes;
-  // the MN-major dy operand needs BN % 32 == 0: its boxes are 32 columns wide)
-  if (!on || Kg > 256 || Kg % 64) return false;
+  // (the MN-major dy operand needs BN = Kg % 32 == 0: its TMA boxes are 32
+  // columns wide, a narrower tail would leave the stage's expected bytes short)
+  if (!on || Kg > 256 || Kg < 64 || Kg % 32) return false;
   const double waste_k = (double)rup(Kg, 128) / Kg;
   const double waste_t = (double)rup(taps * Cgp, 128) / (taps * Cgp);
   return waste_k >= 1.3 && waste_t <= 1.15;
@@ -2737,11 +2740,16 @@ static void s2d_wgrad(ck_handle* h, const float* x, const float* dy, float* df, 
   float* dyg = dy_grid(h, dy, d, d.K, Kp, 1, z.U, z.V, s);
   float* part;
   int64_t per;
-  const int splits = grid_wgrad(h, xt, z.Csp, z.Csp, dyg, Kp, Kp, d.K, 1, d.N, z.U, z.V, z.Th,
-                                z.Tw, &part, &per, s);
+  const bool swapped = wgrad_swap(d.K, z.Th * z.Tw, z.Csp);
+  const int splits =
+      swapped ? grid_wgrad_swapped(h, xt, z.Csp, z.Csp, dyg, Kp, Kp, d.K, 1, d.N, z.U, z.V, z.Th,
+                                   z.Tw, &part, &per, s)
+              : grid_wgrad(h, xt, z.Csp, z.Csp, dyg, Kp, Kp, d.K, 1, d.N, z.U, z.V, z.Th, z.Tw,
+                           &part, &per, s);
   count_launch();
   ck::pdl_launch(s2d_wgrad_finish_k, blocks_for((int64_t)d.K * d.fh * d.fw * d.C), 256, 0, s, 
-      part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc, d.fsc, d.fsk);
+      part, df, d.fh, d.fw, d.C, d.K, z.s, z.Th, z.Csp, splits, per, acc, d.fsc, d.fsk,
+      swapped ? 1 : 0, (int64_t)z.Th * z.Tw * z.Csp);
 }
 
 static bool is_fc(const ConvDims& d) {
