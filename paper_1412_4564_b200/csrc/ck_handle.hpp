@@ -65,7 +65,8 @@ struct ck_handle {
   ck::GridPlan prev_dyg_plan{};
   bool prev_dyg_done = false;
   // engine, fused bnorm -> relu: per-channel (mu, inv) of the forward, which
-  // the backward uses to recompute the relu gate from x (2 floats / channel)
+  // the backward uses to recompute the relu gate from x, followed by the
+  // forward's w and b (4 floats / channel: [2C] (mu, inv), [C] w, [C] b)
   float* bn_muinv = nullptr;
   // engine, fused bnorm -> relu with the bnorm output read by nothing else:
   // the forward stores only relu(y) (y is recomputed from x on request)

@@ -116,7 +116,11 @@ struct Layer {
   std::vector<int> in, out;
   std::vector<double> p;
   float* aux = nullptr;  // bnorm moments (K x 2), graph.cpp:306
-  float* muinv = nullptr;  // bnorm -> relu: the forward's (mu, inv) per channel
+  // bnorm -> relu: the forward's (mu, inv) per channel, then its (w, b)
+  // snapshot -- [2C] interleaved (mu, inv), [C] w, [C] b -- so values and
+  // derivatives left unstored are recomputed with the parameters of that
+  // forward even after the trainer's SGD moved them
+  float* muinv = nullptr;
   ConvCache cache;       // conv input transform shared by forward and wgrad
   // conv -> relu fusion: the conv's epilogue also writes relu(y) (the relu
   // layer's output) when its output feeds only that relu; the relu forward
@@ -473,7 +477,7 @@ static void finalize(ck_graph* g) {
   for (auto& l : g->layers)
     if (l.kind == Kind::bnorm) {
       l.aux = alloc(2 * (size_t)g->vars[l.in[0]].shape.c);
-      l.muinv = alloc(2 * (size_t)g->vars[l.in[0]].shape.c);
+      l.muinv = alloc(4 * (size_t)g->vars[l.in[0]].shape.c);
     }
   // conv -> relu pairs whose intermediate has no other reader
   for (size_t li = 0; li < g->layers.size(); ++li) {
@@ -731,7 +735,8 @@ static void materialize_value(ck_graph* g, Var& v, cudaStream_t s) {
   if (v.lazy_value < 0) return;
   Layer& l = g->layers[v.lazy_value];
   const Var& x = g->vars[l.in[0]];
-  bnorm_value(x.value, g->vars[l.in[1]].value, g->vars[l.in[2]].value, l.muinv, v.value,
+  const int64_t C = x.shape.c;  // the forward's (w, b), not the current parameters
+  bnorm_value(x.value, l.muinv + 2 * C, l.muinv + 3 * C, l.muinv, v.value,
               (int)(x.shape.h * x.shape.w), (int)x.shape.c, (int)x.shape.n,
               v.lazy_value_relu ? 1 : 0, s);
   v.lazy_value = -1;
@@ -747,6 +752,13 @@ static void materialize_bn(ck_graph* g, Var& v, cudaStream_t s) {
   ck_tensor x = tv(g->vars[l.in[0]], false), w = tv(g->vars[l.in[1]], false),
             b = tv(g->vars[l.in[2]], false), dx = tv(v, true),
             dy = tv(g->vars[l.out[0]], true);
+  if (g->layers[g->vars[l.relu_out].producer].fused_done) {
+    // the parameters of the forward this derivative belongs to (the trainer's
+    // SGD may have moved w, b since): the snapshot after (mu, inv)
+    const int64_t C = x.shape.c;
+    w.data = l.muinv + 2 * C;
+    b.data = l.muinv + 3 * C;
+  }
   const bool fused = l.relu_out >= 0 && g->layers[g->vars[l.relu_out].producer].bwd_deferred;
   if (fused) {
     h->fuse_relu_x = g->vars[l.out[0]].value;

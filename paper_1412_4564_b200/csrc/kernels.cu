@@ -1396,6 +1396,8 @@ __global__ void __launch_bounds__(256) bnorm_apply_k(const float* __restrict__ x
   if (muinv_out && blockIdx.y == 0 && threadIdx.x == 0) {
     muinv_out[2 * c] = mu;  // for the backward's gate recomputation
     muinv_out[2 * c + 1] = inv;
+    muinv_out[2 * C + c] = wk;  // the parameter snapshot (engine recomputation)
+    muinv_out[3 * C + c] = bk;
   }
   for (int n = blockIdx.y; n < N; n += gridDim.y) {
     const int64_t base = ((int64_t)n * C + c) * HW;
@@ -2492,6 +2494,8 @@ __global__ void __launch_bounds__(256) bnorm_apply_grid_k(const float* __restric
       if (muinv_out) {
         muinv_out[2 * c] = mu;
         muinv_out[2 * c + 1] = inv;
+        muinv_out[2 * C + c] = w[c];  // the parameter snapshot (engine recomputation)
+        muinv_out[3 * C + c] = b[c];
       }
     }
   }

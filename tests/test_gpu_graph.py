@@ -442,6 +442,34 @@ def test_bnorm_writes_conv_dy_grid(image):
             assert np.array_equal(d0[n], d1[n]), n
 
 
+def test_unstored_values_after_trainer_step():
+    """Values and derivatives a fusion left unstored (bn_lazy_y, bn_grid,
+    producer_grid) are recomputed on request with the parameters of the
+    forward they belong to -- also after the trainer's SGD has moved them:
+    one training step with every fusion on equals the unfused engine's
+    stored tape (every layer output's value and derivative) bit for bit."""
+    from paper_1412_4564_b200 import nets
+    from paper_1412_4564_b200.graph import Trainer
+    net = nets.vgg16_bn(batch=2, image=32)
+    out = []
+    for on in (True, False):
+        g = device_graph(net, "tf32")
+        for opt in ("bn_grid", "bn_lazy_y", "producer_grid", "dgrad_grid", "lrn_grid"):
+            g.set_option(opt, on)
+        for k, v in {**net.init_params(), **net.init_inputs()}.items():
+            g.set(k, v)
+        t = Trainer(g, lr=0.05, momentum=0.9, weight_decay=5e-4)
+        t.step()
+        names = {o for layer in net.layers for o in layer[3]}
+        out.append(({n: g.get(n) for n in sorted(names)},
+                    {n: g.get(n, deriv=True) for n in sorted(names)}))
+    (v0, d0), (v1, d1) = out
+    for n in v1:
+        assert np.array_equal(v0[n], v1[n]), n
+    for n in d1:
+        assert np.array_equal(d0[n], d1[n]), n
+
+
 @pytest.mark.parametrize("cout,groups,size", [(64, 2, 5), (48, 1, 5), (96, 1, 3), (64, 1, 4)])
 def test_lrn_grid_envelope(cout, groups, size, monkeypatch):
     """conv -> relu -> lrn -> pool -> fc on a small image: inside the fused
