@@ -1516,11 +1516,15 @@ __global__ void __launch_bounds__(256) bnorm_bwd_k(const float* __restrict__ x,
 // (the conv's bias-gradient partials, [pixel warp][Cp] doubles).  The
 // per-channel constants come from the stats pass, computed per block in
 // bnorm_bwd_k's expressions.  Requires the conv's channels per group % 32 == 0.
+#ifndef CK_BN_GRID_BPS
+#define CK_BN_GRID_BPS 16
+#endif
 // channels per block of the pixel-major bnorm grid kernels: all of them when
-// the pixels alone fill ~4 blocks per SM, else fewer (a multiple of 32)
+// the pixels alone fill ~CK_BN_GRID_BPS blocks per SM, else fewer (a multiple
+// of 32; sweep on VGG: 16 beats 4 and 8 by ~1% of the step)
 static int bn_grid_cchunk(int64_t pixels, int C) {
   const int64_t pblocks = std::min<int64_t>((pixels + 255) / 256, 148 * 8);
-  int64_t want = (148 * 4 + pblocks - 1) / pblocks;  // channel chunks wanted
+  int64_t want = (148 * CK_BN_GRID_BPS + pblocks - 1) / pblocks;  // channel chunks wanted
   int64_t cc = (C + want - 1) / want;
   cc = (cc + 31) / 32 * 32;
   return (int)std::max<int64_t>(32, std::min<int64_t>(C, cc));
