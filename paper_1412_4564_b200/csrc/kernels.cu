@@ -723,12 +723,15 @@ __global__ void lrn_bwd_k(const float* __restrict__ x, const float* __restrict__
 // the steady state (all prefetches in range) runs without bounds tests and
 // walks the channel planes with pointer increments -- these kernels are
 // instruction-bound otherwise.
+#ifndef CK_LRN_FWD_P
+#define CK_LRN_FWD_P 8
+#endif
 template <int NW>
 __global__ void lrn_fwd_reg_k(const float* __restrict__ x, float* __restrict__ y, int HW, int C,
                               int64_t pixels, float kappa, float alpha, float nbeta) {
   ck::pdl_entry();
   constexpr int DOWN = (NW - 1) / 2, UP = NW - 1 - DOWN;
-  constexpr int P = 8;  // prefetch distance (channels)
+  constexpr int P = CK_LRN_FWD_P;  // prefetch distance (channels)
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < pixels;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t n = e / HW;
