@@ -156,6 +156,66 @@ def test_conv_blocked_dgrad(xs, fs, g):
     assert err(host(acc), dx_ref + base, "tf32") < TOL["tf32"]
 
 
+def _route_cases():
+    """Random geometries on the round-2 GEMM routes: 2 x 2-blocked data
+    gradients (groups of 16..64 channels, 5x5 / 7x7 filters, >= 2^17 output
+    pixels), role-swapped weight gradients (64 / 96 / 192 / 256 filters per
+    group), space-to-depth strides with the swap."""
+    r = np.random.default_rng(2026)
+    cases = []
+    for k in range(10):  # blocked dgrad
+        cg = int(r.choice([16, 32, 48, 64]))
+        groups = int(r.choice([1, 2]))
+        f = int(r.choice([5, 7]))
+        side = int(r.integers(20, 40))
+        n = int(np.ceil(131072 / (side * side)))
+        p = int(r.integers(0, f))
+        cases.append(((side, side + int(r.integers(0, 3)), cg * groups, n),
+                      (f, f, cg, 16 * int(r.integers(1, 5)) * groups),
+                      (1, 1, p, f - 1 - p, p, int(r.integers(0, f)), groups)))
+    for k in range(8):  # swapped wgrad (stride 1)
+        kg = int(r.choice([64, 96, 192]))
+        groups = int(r.choice([1, 2]))
+        cg = int(r.choice([32, 64, 96]))
+        cases.append(((int(r.integers(7, 20)), int(r.integers(7, 20)), cg * groups,
+                       int(r.integers(2, 9))), (3, 3, cg, kg * groups), (1, 1, 1, 1, 1, 1, groups)))
+    for k in range(4):  # space-to-depth with 64..96 filters (sizes 3 mod 4: the s2d envelope)
+        cases.append(((4 * int(r.integers(8, 15)) + 3, 4 * int(r.integers(8, 15)) + 3, 3,
+                       int(r.integers(1, 4))),
+                      (int(r.choice([7, 11])), int(r.choice([7, 11])), 3, int(r.choice([64, 96]))),
+                      (4, 4, 0, 0, 0, 0, 1)))
+    return cases
+
+
+@pytest.mark.parametrize("xs,fs,g", _route_cases())
+def test_conv_round2_routes(xs, fs, g):
+    """Forward and backward of random geometries on the blocked-dgrad /
+    swapped-wgrad / space-to-depth routes against the double oracle
+    (oracle/fastconv.py) at the TF32 bound, on tcgen05."""
+    import fastconv as FC
+    r = np.random.default_rng(sum(xs) + sum(fs))
+    geom = B.ConvGeom(*g)
+    try:
+        ys = B.conv_output_shape(xs, fs, geom)
+    except Exception:
+        pytest.skip("invalid geometry")
+    x = r.uniform(-1, 1, O.size(xs)).astype(np.float32)
+    f = r.uniform(-0.1, 0.1, O.size(fs)).astype(np.float32)
+    b = r.uniform(-1, 1, fs[3]).astype(np.float32)
+    dy = r.uniform(-1, 1, O.size(ys)).astype(np.float32)
+    y_ref, _ = FC.conv_forward(x, xs, f, fs, b, g)
+    dx_ref, df_ref, db_ref = FC.conv_backward(x, xs, f, fs, g, dy)
+    hd = B.handle()
+    tc0 = hd.tc_launches
+    y = B.conv_forward(dev(x, xs), dev(f, fs), torch.from_numpy(b).cuda(), geom, math="tf32")
+    dx, df, db = B.conv_backward(dev(x, xs), dev(f, fs), geom, dev(dy, ys), math="tf32")
+    assert hd.tc_launches - tc0 >= 3
+    assert err(host(y), y_ref, "tf32") < TOL["tf32"]
+    assert err(host(dx), dx_ref, "tf32") < TOL["tf32"]
+    assert err(host(df), df_ref, "tf32") < TOL["tf32"]
+    assert rel(host(db), db_ref) < 1e-4
+
+
 @pytest.mark.parametrize("xs,fs,g", [CONV_CASES[9], CONV_CASES[10], CONV_CASES[8],
                                      CONV_CASES[13]])
 def test_conv_accumulate_tensor_cores(xs, fs, g):
