@@ -536,6 +536,9 @@ def main():
         roofline = {"bound": "fp32", "kernel": f"{dom[0]} fprop+dgrad+wgrad",
                     "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": achieved / tf32_peak, "traffic": None, "peak_source": peak_src}
+    if ms < 1.0:
+        roofline["note"] = (f"latency-bound step: {launches / max(args.steps, 1):.0f} kernels in "
+                            f"{ms:.3f} ms; the dominant launch's fraction is not the bound")
     # memory-bound layers: SURVEY §8d compulsory bytes / event time / HBM peak
     tmap = {n: (f, b) for n, f, b in times}
     hbm = []
