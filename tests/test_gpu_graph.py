@@ -538,6 +538,47 @@ def test_engine_pool_argmax_route_bitexact(pad, side, win):
     assert np.array_equal(g.get("x", deriv=True), O.pool_backward(x, xs, pg, dp1))
 
 
+@pytest.mark.parametrize("side", [55, 27, 29, 61, 63])
+def test_pool_forward_special_values(side):
+    """The compile-time 3x3/2 max-pool forward (kernels.cu pool_max_fwd_t)
+    picks the reference's winner (pool.cpp:49-80: the first strict maximum in
+    (column, row) order) under heavy ties, -inf and NaN: the pooled values
+    equal the oracle's (NaN where it has NaN), and in a graph the argmax codes
+    it records route the backward exactly as the oracle's dx (heavy ties)."""
+    from paper_1412_4564_b200 import blocks as B
+    from paper_1412_4564_b200.graph import Graph
+    xs, n = (side, side, 5, 3), 3
+    r = O.Rng(43)
+    x = np.floor(r.uniform(O.size(xs), 0.0, 4.0)).astype(np.float32)  # many ties
+    m = r.uniform(O.size(xs))
+    x[m < 0.05] = -np.inf
+    pg = (3, 3, 2, 2, 0, 0, 0, 0, 0)
+    geom = B.PoolGeom(3, 3, 2, 2, 0, 0, 0, 0, mode="max")
+    xn = x.copy()
+    xn[m > 0.97] = np.nan
+    yn_ref, ps = O.pool_forward(xn, xs, pg)
+    yn = B.pool_forward(B.as_hwcn(torch.from_numpy(xn).cuda(), xs), geom)
+    assert np.array_equal(yn.cpu().numpy().ravel(), yn_ref, equal_nan=True)
+    assert np.isnan(yn_ref).any()
+    g = Graph(math="fp32")
+    g.add_input("x", xs)
+    g.add_input("label", (1, 1, 1, n))
+    g.add_layer("pool", "pool1", ["x"], ["p1"], list(pg))
+    g.add_layer("pool", "pool2", ["p1"], ["p2"], [ps[0], ps[1], 1, 1, 0, 0, 0, 0, 1])
+    g.add_layer("loss", "loss", ["p2", "label"], ["objective"], [])
+    g.finalize()
+    xf = np.where(np.isinf(x), np.float32(-1.0), x)  # heavy ties, finite
+    g.set("x", xf)
+    g.set("label", np.array([1, 3, 2], np.float32))
+    g.forward()
+    y_ref, _ = O.pool_forward(xf, xs, pg)
+    assert np.array_equal(g.get("p1"), y_ref)
+    g.backward("objective")
+    dp1 = g.get("p1", deriv=True)
+    assert np.isfinite(dp1).all()
+    assert np.array_equal(g.get("x", deriv=True), O.pool_backward(xf, xs, pg, dp1))
+
+
 @pytest.mark.parametrize("net_name", ["cifar", "alexnet", "vgg16bn"])
 def test_trainer_cuda_graph_replay_matches_eager(net_name):
     """ck_trainer_set_graph: the captured step replays the same deterministic
