@@ -1,6 +1,7 @@
-"""A/B of the 3x3/2 max-pool forward routes (CUDA events): AlexNet pool1 / pool2 / pool5
-shapes at b=256 through the block API; run with the experiments library and
-CK_POOL_FWD_STRIP=0/1."""
+"""Time the 3x3/2 max-pool forward (CUDA events) at AlexNet's pool1 / pool2 / pool5
+shapes, b=256, through the block API, with the achieved HBM rate (x read + y write).
+Used for the round-2 A/B of a column-strip forward (rejected list);
+pass --lib to time a variant library."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 if "--lib" in sys.argv:
